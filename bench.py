@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""bench.py -- one "step" = one pass of the whole hot path over
+BASELINE.json config 2: the 2D Poisson 5-point matrix on a 2048 x 2048 grid (4,194,304 rows,
+20,963,328 nonzeros, fp64), dense width k = 32:
+
+    a7  csr_transpose (plan: pattern + perm)          a1  spmv_fwd        a2+a3 spmv_bwd
+    a4  spmm_fwd                                      a5+a6 spmm_bwd
+    a8+a9 spgemm_symbolic (C = A A, one host sync)    a10 spgemm_numeric  a11+a12 spgemm_bwd
+    a13 (N > 1) row-block partition + halo reduction of the dx / dX / dB partials over NCCL
+
+Metric (BASELINE.json): algorithmic GB/s of the step (SURVEY.md 8(d) d.4 bytes; one read of
+every operand, one write of every result) -- plus GFLOP/s and the roofline fraction of the
+dominant kernel against the measured HBM copy bandwidth (MEASURED_PEAKS.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun): weak scaling -- rank r owns rows [r m, (r+1) m) of the 2D Poisson matrix on a
+(2048 N) x 2048 grid; x / X / dC are replicated over each rank's column interval and the
+partial gradients are combined by the halo reduction in paper_2212_05159_b200.dist.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+GRID = 2048
+K = 32
+S = 8  # bytes per fp64 value
+
+
+# ---------------------------------------------------------------- algorithmic bytes / flops
+def pat_bytes(m, nnz):
+    return 8 * (m + 1) + 4 * nnz
+
+
+def op_costs(m, n, nnz, nnzC, prod, k=K, s=S):
+    A = pat_bytes(m, nnz) + s * nnz
+    return {
+        "csr_transpose": (pat_bytes(m, nnz) + pat_bytes(n, nnz) + 8 * nnz, 0),
+        "spmv_fwd": (A + s * n + s * m, 2 * nnz),
+        "spmv_bwd": (A + s * m + s * n + s * n + s * nnz, 3 * nnz),
+        "spmm_fwd": (A + s * k * n + s * k * m, 2 * nnz * k),
+        "spmm_bwd": (A + s * k * (m + 2 * n) + s * nnz, 4 * nnz * k),
+        # B aliases A (C = A A): the aliased operand is counted once
+        "spgemm_symbolic": (pat_bytes(m, nnz) + pat_bytes(m, nnzC), 0),
+        "spgemm_numeric": (A + 8 * (m + 1) + s * nnzC, 2 * prod),
+        "spgemm_bwd": (A + pat_bytes(m, nnzC) + s * nnzC + 2 * s * nnz, 4 * prod),
+    }
+
+
+OPS = ["csr_transpose", "spmv_fwd", "spmv_bwd", "spmm_fwd", "spmm_bwd", "spgemm_symbolic", "spgemm_numeric",
+       "spgemm_bwd"]
+
+
+# ---------------------------------------------------------------- clocks sampler
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=5)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        if not self.lines:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[1]))
+                smax = max(smax, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- workload
+class Workload:
+    """Config-2 inputs resident on the device plus preallocated outputs."""
+
+    def __init__(self, torch, ck, rank=0, world=1, dist=None):
+        self.torch, self.ck, self.dist = torch, ck, dist
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.dev = dev
+        # rank's row block of the (GRID*world) x GRID grid: rows [r*m, (r+1)*m)
+        if world == 1:
+            A = synth.poisson2d(GRID)
+            self.col_lo = 0
+        else:
+            A, self.col_lo = dist.poisson2d_row_block(GRID * world, GRID, rank, world)
+        self.A_host = A
+        self.m, self.n, self.nnz = A.nrows, A.ncols, A.nnz
+        ck_ = ck
+        self.A = ck_.CSR.from_host(A)
+        cfg = 2
+        self.x = torch.from_numpy(synth.dense(self.n, synth.seed_of(cfg, 3) + 100 * rank)).to(dev)
+        self.dy = torch.from_numpy(synth.dense(self.m, synth.seed_of(cfg, 4) + 100 * rank)).to(dev)
+        self.X = torch.from_numpy(synth.dense((self.n, K), synth.seed_of(cfg, 3) + 100 * rank + 1)).to(dev)
+        self.dY = torch.from_numpy(synth.dense((self.m, K), synth.seed_of(cfg, 4) + 100 * rank + 1)).to(dev)
+        # C = A B with B = the rows of A over this rank's column interval (B = A at N = 1)
+        self.B = self.A if world == 1 else ck_.CSR.from_host(dist.halo_rows_block(GRID * world, GRID, rank, world))
+        # outputs / plans (allocated once, reused)
+        self.plan = ck_.csr_transpose(self.A, with_values=False)
+        self.C = ck_.spgemm_symbolic(self.A, self.B)
+        self.nnzC = self.C.nnz
+        self.prod = int(np.diff(self.B.indptr.cpu().numpy())[A.indices].sum())
+        self.dC = torch.from_numpy(synth.dense(self.nnzC, synth.seed_of(cfg, 5) + 100 * rank)).to(dev)
+        e = torch.empty
+        f64 = torch.float64
+        self.y = e(self.m, dtype=f64, device=dev)
+        self.dA_v = e(self.nnz, dtype=f64, device=dev)
+        self.dx = e(self.n, dtype=f64, device=dev)
+        self.Y = e((self.m, K), dtype=f64, device=dev)
+        self.dA_m = e(self.nnz, dtype=f64, device=dev)
+        self.dX = e((self.n, K), dtype=f64, device=dev)
+        self.Cv = e(self.nnzC, dtype=f64, device=dev)
+        self.dA_g = e(self.nnz, dtype=f64, device=dev)
+        self.dB_g = e(self.B.nnz, dtype=f64, device=dev)
+        self.costs = op_costs(self.m, self.n, self.nnz, self.nnzC, self.prod)
+
+    def step(self, ev=None):
+        """One pass of the hot path; `ev` (dict op -> (start, end) events) brackets each op."""
+        ck, torch = self.ck, self.torch
+        st = torch.cuda.current_stream()
+
+        def rec(name, i):
+            if ev is not None:
+                ev[name][i].record(st)
+
+        rec("csr_transpose", 0)
+        ck.csr_transpose(self.A, with_values=False, out=self.plan)
+        rec("csr_transpose", 1)
+        rec("spmv_fwd", 0)
+        ck.spmv_fwd(self.A, self.x, out=self.y)
+        rec("spmv_fwd", 1)
+        rec("spmv_bwd", 0)
+        ck.spmv_bwd(self.A, self.x, self.dy, plan=self.plan, dA=self.dA_v, dx=self.dx)
+        rec("spmv_bwd", 1)
+        rec("spmm_fwd", 0)
+        ck.spmm_fwd(self.A, self.X, out=self.Y)
+        rec("spmm_fwd", 1)
+        rec("spmm_bwd", 0)
+        ck.spmm_bwd(self.A, self.X, self.dY, plan=self.plan, dA=self.dA_m, dX=self.dX)
+        rec("spmm_bwd", 1)
+        rec("spgemm_symbolic", 0)
+        C = ck.spgemm_symbolic(self.A, self.B)
+        rec("spgemm_symbolic", 1)
+        assert C.nnz == self.nnzC
+        self.C = C
+        rec("spgemm_numeric", 0)
+        ck.spgemm_numeric(self.A, self.B, C, out=self.Cv)
+        rec("spgemm_numeric", 1)
+        rec("spgemm_bwd", 0)
+        ck.spgemm_bwd(self.A, self.B, C, self.dC, dA=self.dA_g, dB=self.dB_g)
+        rec("spgemm_bwd", 1)
+        if self.dist is not None:
+            rec("halo_reduce", 0)
+            self.dist.reduce_partials(self)
+            rec("halo_reduce", 1)
+
+
+def flush_l2(torch, buf):
+    buf.zero_()
+
+
+def run_cpu_baseline(threads=None, rows_sample=1 << 22):
+    """The oracle, as it stands, on a bounded sample of the same workload: the 2D Poisson
+    5-point stencil on a (rows_sample/2048) x 2048 grid, the same step (all ops), fp64."""
+    import oracle
+    nthreads = threads or len(os.sched_getaffinity(0))
+    oracle.set_threads(nthreads)
+    A = synth.poisson2d(rows_sample // GRID, GRID)
+    m = A.nrows
+    x, dy = synth.dense(m, 1), synth.dense(m, 2)
+    X, dY = synth.dense((m, K), 3), synth.dense((m, K), 4)
+    t0 = time.perf_counter()
+    oracle.csr_transpose(A)
+    oracle.spmv_fwd(A, x)
+    oracle.spmv_bwd(A, x, dy)
+    oracle.spmm_fwd(A, X)
+    oracle.spmm_bwd(A, X, dY)
+    Cp, Ci = oracle.spgemm_symbolic(A, A)
+    oracle.spgemm_numeric(A, A, Cp, Ci)
+    dC = synth.dense(len(Ci), 5)
+    t1 = time.perf_counter()
+    oracle.spgemm_bwd(A, A, Cp, Ci, dC)
+    t2 = time.perf_counter()
+    prod = int(np.diff(A.indptr)[A.indices].sum())
+    costs = op_costs(m, m, A.nnz, len(Ci), prod)
+    tot_bytes = sum(b for b, _ in costs.values())
+    secs = t2 - t0 - 0.0 * (t2 - t1)
+    return {"value": tot_bytes / secs / 1e9, "unit": "GB/s", "cores": nthreads, "kind": "oracle",
+            "sample": f"2D Poisson {m // GRID}x{GRID} ({m} rows, nnz {A.nnz}), whole step, fp64, "
+                      f"{secs:.2f} s wall", "seconds": secs}
+
+
+def run_reference(args):
+    """--impl reference: the oracle (the only reference this paper-only tier has) on bounded
+    samples of the config-2 workload, timed on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    for _ in range(args.warmup):
+        run_cpu_baseline(rows_sample=1 << 15)
+    vals, secs = [], []
+    for _ in range(args.steps):
+        r = run_cpu_baseline(rows_sample=1 << 16)
+        vals.append(r["value"])
+        secs.append(r["seconds"])
+    v = float(np.median(vals))
+    out = {"impl": "reference", "metric": "SpMV/SpMM/SpGEMM fwd+bwd step algorithmic GB/s (config 2 workload)",
+           "value": v, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": float(np.median(secs)) * 1e3, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": "config2-sample: 2D Poisson 32x2048 grid, whole hot-path step (oracle)"},
+           "cpu_baseline": {"value": v, "unit": "GB/s", "cores": r["cores"], "kind": "oracle", "sample": r["sample"]},
+           "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as tdist
+    from paper_2212_05159_b200 import csrk as ck
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_2212_05159_b200 import dist as dist_mod
+        dist = dist_mod.HaloBench(world, rank)
+    W = Workload(torch, ck, rank, world, dist)
+    if dist is not None:
+        dist.setup(W)
+    l2_flush = torch.empty(512 << 20, dtype=torch.uint8, device=W.dev)  # > 126 MB L2
+
+    for _ in range(args.warmup):
+        W.step()
+    torch.cuda.synchronize()
+
+    names = OPS + (["halo_reduce"] if dist is not None else [])
+    evs = [{nm: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for nm in names}
+           for _ in range(args.steps)]
+    step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ck.launch_count()
+    st = torch.cuda.current_stream()
+    with Clocks(local) as clk:
+        for i in range(args.steps):
+            flush_l2(torch, l2_flush)
+            step_ev[i][0].record(st)
+            W.step(evs[i])
+            step_ev[i][1].record(st)
+        torch.cuda.synchronize()
+    launches = ck.launch_count() - launches0
+    if world > 1:
+        tdist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in step_ev]
+    tot_ms = float(sum(step_ms))
+    op_ms = {nm: float(np.mean([e[nm][0].elapsed_time(e[nm][1]) for e in evs])) for nm in names}
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=W.dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms_per_step = tot_ms / args.steps
+    step_bytes = sum(b for b, _ in W.costs.values())
+    step_flops = sum(f for _, f in W.costs.values())
+    value = step_bytes * world / (ms_per_step * 1e-3) / 1e9
+
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = peaks.get("hbm_gbs", 6650.0)
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    # dominant kernel: the op with the largest share of the step
+    dom = max(OPS, key=lambda nm: op_ms[nm])
+    dom_bytes = W.costs[dom][0]
+    achieved = dom_bytes / (op_ms[dom] * 1e-3) / 1e9
+    ops_report = {nm: {"ms": round(op_ms[nm], 4),
+                       "GB/s": round(W.costs[nm][0] / (op_ms[nm] * 1e-3) / 1e9, 1) if nm in W.costs else None,
+                       "GFLOP/s": round(W.costs[nm][1] / (op_ms[nm] * 1e-3) / 1e9, 1) if nm in W.costs else None,
+                       "frac": round(W.costs[nm][0] / (op_ms[nm] * 1e-3) / 1e9 / peak, 3) if nm in W.costs else None}
+                  for nm in names}
+
+    out = None
+    if rank == 0:
+        out = {"metric": "SpMV/SpMM/SpGEMM fwd+bwd step algorithmic GB/s (config 2 workload)",
+               "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "config": {"workload": "config2: 2D Poisson 5-point 2048x2048 per GPU (4,194,304 rows, "
+                                      "20,963,328 nnz), fp64, SpMM k=32, C=A*A; all 8(a) rows per step",
+                          "rows_per_gpu": W.m, "nnz_per_gpu": W.nnz, "nnzC_per_gpu": W.nnzC, "k": K,
+                          "l2": "flushed (512 MiB write) between timed steps",
+                          "parallelism": f"rowblock{world}"},
+               "gflops": round(step_flops * world / (ms_per_step * 1e-3) / 1e9, 2),
+               "step_bytes_per_gpu": step_bytes,
+               "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+                            "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                            "traffic": None, "algorithmic_bytes": dom_bytes},
+               "ops": ops_report, "gpu_launches": int(launches),
+               "clocks": clk.summary()}
+    # ---------------- e2e: same metric through the public API with pinned host buffers
+    if not args.no_e2e:
+        e2e = run_e2e(torch, ck, W, args, world)
+        if out is not None:
+            out["e2e"] = e2e
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = run_cpu_baseline()
+        cb.pop("seconds", None)
+        out["cpu_baseline"] = cb
+    if out is not None:
+        print(json.dumps(out))
+    if world > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
+    return 0
+
+
+def run_e2e(torch, ck, W, args, world):
+    """Per step: H2D of every input (A, x, dy, X, dY, dC) from pinned memory, the step, and D2H
+    of every result (y, dA, dx, Y, dA, dX, C, dA, dB) -- inside the timed region."""
+    pin = lambda t: t.cpu().pin_memory()
+    hA = [pin(W.A.indptr), pin(W.A.indices), pin(W.A.values)]
+    hin = [pin(W.x), pin(W.dy), pin(W.X), pin(W.dY), pin(W.dC)]
+    outs = [W.y, W.dA_v, W.dx, W.Y, W.dA_m, W.dX, W.Cv, W.dA_g, W.dB_g]
+    hout = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in outs]
+    hCp = torch.empty(W.C.indptr.shape, dtype=torch.int64).pin_memory()
+    hCi = torch.empty(W.C.indices.shape, dtype=torch.int32).pin_memory()
+    dA_in = [W.A.indptr, W.A.indices, W.A.values]
+    din = [W.x, W.dy, W.X, W.dY, W.dC]
+    h2d = sum(t.numel() * t.element_size() for t in hA + hin)
+    d2h = sum(t.numel() * t.element_size() for t in hout) + hCp.numel() * 8 + hCi.numel() * 4
+    st = torch.cuda.current_stream()
+    steps = max(1, min(args.steps, 3))
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(st)
+    for _ in range(steps):
+        for d, h in zip(dA_in + din, hA + hin):
+            d.copy_(h, non_blocking=True)
+        W.step()
+        for h, d in zip(hout, outs):
+            h.copy_(d, non_blocking=True)
+        hCp.copy_(W.C.indptr, non_blocking=True)
+        hCi.copy_(W.C.indices, non_blocking=True)
+    ev1.record(st)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / steps
+    if world > 1:
+        import torch.distributed as tdist
+        t = torch.tensor([ms], dtype=torch.float64, device=W.dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        ms = float(t.item())
+    step_bytes = sum(b for b, _ in W.costs.values())
+    return {"value": round(step_bytes * world / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+            "ms_per_step": round(ms, 3), "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "steps": steps}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

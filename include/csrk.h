@@ -1,0 +1,197 @@
+/*
+ * csrk.h -- C-ABI of the B200 (sm_100a) CSR kernel library for the hot path of
+ * Nytko et al., "Optimized Sparse Matrix Operations for Reverse Mode Automatic
+ * Differentiation" (arXiv 2212.05159).  "P:n" = PAPER.md line n (with section /
+ * table), "S:n" = SPEC.md line n.
+ *
+ * CONVENTIONS (apply to every entry point)
+ *   Memory     Every array argument is a DEVICE pointer on the current CUDA device,
+ *              owned by the caller.  The library never allocates device memory;
+ *              scratch is the caller's `ws` (size from csrk_workspace_size()).
+ *              The only host pointer is csrk_spgemm_symbolic's `nnzC_host`.
+ *   Streams    Every call enqueues on `stream` (0 = legacy default) and returns
+ *              without synchronising, except csrk_spgemm_symbolic's count phase.
+ *   Outputs    Overwritten (beta = 0); gradients are NOT accumulated into
+ *              (reading A16).  A NULL optional output skips its work
+ *              (mirrors requires_grad = False).
+ *   CSR        indptr int64[nrows+1], indices int32[nnz]; canonical: indptr[0] = 0,
+ *              nondecreasing, indptr[nrows] = nnz, indices strictly increasing
+ *              within a row and in [0, ncols).  Stored zeros are structural
+ *              entries (reading A1).  Canonical form is the caller's contract; it
+ *              is checked (CSRK_ERR_PATTERN) only when env CSRK_VALIDATE=1.
+ *   Values     dtype CSRK_F32 or CSRK_F64; values and dense operands share dtype.
+ *              Reductions accumulate in fp64 for both dtypes (reading A5/A18).
+ *   Dense      row-major, leading dimension ld >= k (elements).
+ *   Transpose  Ops that need A^T accept an optional cached transpose plan
+ *              (AT = pattern of A^T, AT_perm[q] = position in A of A^T's q-th
+ *              entry), as produced by csrk_csr_transpose.  With a plan, A^T work is
+ *              a deterministic gather ("take the sparse transpose of A and re-execute
+ *              the forward routine"); without one it is an atomic scatter
+ *              ("atomically reduced into correct entries"; reading A7/A8).
+ *   Errors     Every call returns a csrk_status (0 = OK, negative = error) and
+ *              launches nothing on error.  Asynchronous device faults surface at the
+ *              caller's next synchronisation.
+ *   Threads    Stateless and reentrant; safe on concurrent streams.
+ */
+#ifndef CSRK_H
+#define CSRK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *csrk_stream_t; /* == cudaStream_t */
+
+typedef enum {
+    CSRK_OK = 0,
+    CSRK_ERR_INVALID_ARG = -1,   /* NULL where required, negative size, unknown dtype/op */
+    CSRK_ERR_DIM_MISMATCH = -2,  /* e.g. A.ncols != B.nrows ("dimension mismatch") */
+    CSRK_ERR_PATTERN = -3,       /* non-canonical CSR, or patterns that do not match (CSRK_VALIDATE=1) */
+    CSRK_ERR_WORKSPACE = -4,     /* ws_bytes smaller than csrk_workspace_size() */
+    CSRK_ERR_INDEX_OVERFLOW = -5,/* a size exceeds the index types (ncols > INT32_MAX, ...) */
+    CSRK_ERR_CUDA = -6           /* a CUDA launch or runtime call failed */
+} csrk_status;
+
+typedef enum { CSRK_F32 = 0, CSRK_F64 = 1 } csrk_dtype;
+typedef enum { CSRK_OP_N = 0, CSRK_OP_T = 1 } csrk_op;
+
+/* Pattern (structure) of an nrows x ncols CSR matrix; indptr/indices are device pointers. */
+typedef struct {
+    int64_t nrows;
+    int64_t ncols;
+    int64_t nnz;
+    const int64_t *indptr;
+    const int32_t *indices;
+} csrk_pattern;
+
+/* Operation ids for csrk_workspace_size. */
+typedef enum {
+    CSRK_WS_SPMV_FWD = 0,
+    CSRK_WS_SPMV_BWD = 1,
+    CSRK_WS_SPMM_FWD = 2,
+    CSRK_WS_SPMM_BWD = 3,
+    CSRK_WS_CSR_TRANSPOSE = 4,
+    CSRK_WS_SPGEMM_SYMBOLIC = 5,
+    CSRK_WS_SPGEMM_NUMERIC = 6,
+    CSRK_WS_SPGEMM_BWD = 7
+} csrk_ws_op;
+
+/*
+ * SpMV forward (PAPER 3.1.1; Table 1).
+ *   op = N:  y[m] = A x,    y_i = sum_{p in row i} A[p] x[idx p]   ("inner products of each
+ *            row of A and x ... executed in parallel")
+ *   op = T:  y[n] = A^T x,  y_j = sum_{(i,j) in A} A_ij x_i
+ * A_val[nnz]; x[n] (op N) or x[m] (op T); y overwritten.  AT/AT_perm: optional plan,
+ * used only for op T (both NULL or both set).
+ */
+int csrk_spmv_fwd(csrk_dtype dtype, csrk_op op, csrk_pattern A, const void *A_val,
+                  const csrk_pattern *AT, const int64_t *AT_perm,
+                  const void *x, void *y, void *ws, size_t ws_bytes, csrk_stream_t stream);
+
+/*
+ * SpMV backward = VJP of y = op(A) x (Table 1).
+ *   op = N:  dA[p] = dy_i x_{idx p}  at stored p ONLY ("masked to a sparse matrix, only
+ *            requiring computation of nonzero entries of A") -- one multiply,
+ *            bit-exact;  dx[n] = A^T dy.
+ *   op = T:  dA[p] = x_i dy_{idx p};  dx[m] = A dy.
+ * dA_val (nullable) is aligned with A's indices; dx (nullable).  x, dy as in forward.
+ * AT/AT_perm optional (op N only): deterministic transposed traversal computing dx and
+ * dA together; without a plan dx uses atomic adds.
+ */
+int csrk_spmv_bwd(csrk_dtype dtype, csrk_op op, csrk_pattern A, const void *A_val,
+                  const csrk_pattern *AT, const int64_t *AT_perm,
+                  const void *x, const void *dy, void *dA_val, void *dx,
+                  void *ws, size_t ws_bytes, csrk_stream_t stream);
+
+/*
+ * SpMM (SpDMM) forward (PAPER 3.1.3; Table 1; reading A10/A21).
+ *   Y[m x k] = A X,  X[n x k] row-major with leading dimension ldx >= k, Y with ldy >= k.
+ */
+int csrk_spmm_fwd(csrk_dtype dtype, csrk_pattern A, const void *A_val, int64_t k,
+                  const void *X, int64_t ldx, void *Y, int64_t ldy,
+                  void *ws, size_t ws_bytes, csrk_stream_t stream);
+
+/*
+ * SpMM backward = VJP of Y = A X (Table 1).
+ *   dA[p]   = sum_c dY[i,c] X[idx p, c]     ((dY X^T) (.) mask(A), an SDDMM)
+ *   dX[n x k] = A^T dY                      ("take the sparse transpose of A and re-execute
+ *                                             the forward routine")
+ * dA_val, dX nullable.  AT/AT_perm: optional plan.  With a plan, one fused transposed
+ * traversal produces dA and dX; without one, dA is a row traversal and dX builds the
+ * transpose in `ws` first (workspace size accounts for it).
+ */
+int csrk_spmm_bwd(csrk_dtype dtype, csrk_pattern A, const void *A_val,
+                  const csrk_pattern *AT, const int64_t *AT_perm, int64_t k,
+                  const void *X, int64_t ldx, const void *dY, int64_t lddy,
+                  void *dA_val, void *dX, int64_t lddx,
+                  void *ws, size_t ws_bytes, csrk_stream_t stream);
+
+/*
+ * CSR transpose.  Writes A^T (n x m) in canonical CSR:
+ *   AT_indptr[n+1], AT_indices[nnz] (rows of A, ascending within each A^T row),
+ *   AT_perm[nnz] (nullable): position in A of A^T's q-th entry,
+ *   AT_val[nnz]  (nullable; A_val may then be NULL): A_val[AT_perm[q]].
+ * Pattern outputs are bit-exact against the stable counting sort of the oracle.
+ */
+int csrk_csr_transpose(csrk_dtype dtype, csrk_pattern A, const void *A_val,
+                       int64_t *AT_indptr, int32_t *AT_indices, void *AT_val, int64_t *AT_perm,
+                       void *ws, size_t ws_bytes, csrk_stream_t stream);
+
+/*
+ * SpGEMM symbolic phase (PAPER 3.1.2):
+ *   pattern(C) = {(i,j) : exists k, (i,k) in A and (k,j) in B}, STRUCTURAL (values never
+ *   consulted; entries that would cancel are kept -- reading A2), columns ascending.
+ * Two calls with the same arguments:
+ *   (1) C_indices == NULL: writes C_indptr[m+1] (int64, reading A4), synchronises `stream`,
+ *       and stores nnz(C) in *nnzC_host (host pointer, required).
+ *   (2) C_indices != NULL (caller allocated nnz(C) int32): fills the sorted indices
+ *       (C_indptr must hold the result of call 1).  Does not synchronise.
+ * A is m x n, B is n x p.
+ */
+int csrk_spgemm_symbolic(csrk_pattern A, csrk_pattern B, int64_t *C_indptr, int32_t *C_indices,
+                         int64_t *nnzC_host, void *ws, size_t ws_bytes, csrk_stream_t stream);
+
+/*
+ * SpGEMM numeric phase: C_ij = sum_k A_ik B_kj over the symbolic pattern C
+ * (C.indptr / C.indices from csrk_spgemm_symbolic).  C_val[nnz(C)] overwritten.
+ */
+int csrk_spgemm_numeric(csrk_dtype dtype, csrk_pattern A, const void *A_val,
+                        csrk_pattern B, const void *B_val, csrk_pattern C, void *C_val,
+                        void *ws, size_t ws_bytes, csrk_stream_t stream);
+
+/*
+ * SpGEMM backward = VJP of C = A B (Table 1; Fig. 3):
+ *   dA_ik = sum_{j in row k of B} dC_ij B_kj        ((dC B^T) (.) mask(A))
+ *   dB_kj = sum_{i : (i,k) in A}   A_ik dC_ij        ((A^T dC) (.) mask(B))
+ * dC_val[nnz(C)] aligned with C's pattern (reading A15); dA_val[nnz(A)], dB_val[nnz(B)]
+ * nullable.  When B aliases A the caller sums dA + dB (reading A13).
+ */
+int csrk_spgemm_bwd(csrk_dtype dtype, csrk_pattern A, const void *A_val,
+                    csrk_pattern B, const void *B_val, csrk_pattern C, const void *dC_val,
+                    void *dA_val, void *dB_val, void *ws, size_t ws_bytes, csrk_stream_t stream);
+
+/*
+ * Scratch bytes needed by operation `op` for operands A (and B for SpGEMM, or the
+ * output pattern C for numeric/bwd passed as B), width k (SpMM) and dtype.
+ * have_plan = 1 if a transpose plan will be passed.  Writes *bytes; host-only, no launch.
+ */
+int csrk_workspace_size(csrk_ws_op op, csrk_dtype dtype, const csrk_pattern *A,
+                        const csrk_pattern *B, int64_t k, int have_plan, size_t *bytes);
+
+/* Static text for a status code. */
+const char *csrk_status_string(int status);
+
+/* Number of kernels this library has launched in this process (all devices). */
+uint64_t csrk_launch_count(void);
+
+/* Library version, e.g. "csrk 0.1 sm_100a". */
+const char *csrk_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CSRK_H */

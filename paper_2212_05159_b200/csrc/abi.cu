@@ -1,0 +1,226 @@
+// abi.cu -- extern "C" entry points of include/csrk.h: argument checks, workspace sizing
+// and dispatch.  Nothing is launched when a check fails.
+#include <climits>
+
+#include "ops.cuh"
+
+using namespace csrk;
+
+namespace {
+
+int check_pat(const csrk_pattern &A)
+{
+    if (A.nrows < 0 || A.ncols < 0 || A.nnz < 0) return CSRK_ERR_INVALID_ARG;
+    if (A.nrows > INT32_MAX || A.ncols > INT32_MAX) return CSRK_ERR_INDEX_OVERFLOW;
+    if (!A.indptr) return CSRK_ERR_INVALID_ARG;
+    if (A.nnz > 0 && !A.indices) return CSRK_ERR_INVALID_ARG;
+    return CSRK_OK;
+}
+
+int check_dtype(csrk_dtype dt) { return (dt == CSRK_F32 || dt == CSRK_F64) ? CSRK_OK : CSRK_ERR_INVALID_ARG; }
+int check_op(csrk_op op) { return (op == CSRK_OP_N || op == CSRK_OP_T) ? CSRK_OK : CSRK_ERR_INVALID_ARG; }
+
+int check_plan(const csrk_pattern &A, const csrk_pattern *AT, const int64_t *perm)
+{
+    if (!AT && !perm) return CSRK_OK;
+    if (!AT || (!perm && AT->nnz > 0)) return CSRK_ERR_INVALID_ARG;
+    CSRK_TRY(check_pat(*AT));
+    if (AT->nrows != A.ncols || AT->ncols != A.nrows || AT->nnz != A.nnz) return CSRK_ERR_DIM_MISMATCH;
+    return CSRK_OK;
+}
+
+// Run `f(Bump&)` once in sizing mode to learn the bytes, then for real.
+template <typename F>
+int with_ws(void *ws, size_t ws_bytes, F &&f)
+{
+    Bump sz(nullptr, 0);
+    CSRK_TRY(f(sz));
+    if (sz.used > 0 && (!ws || ws_bytes < sz.used)) return CSRK_ERR_WORKSPACE;
+    static char dummy[16];
+    Bump real(ws ? ws : static_cast<void *>(dummy), ws ? ws_bytes : 0);
+    return f(real);
+}
+
+}  // namespace
+
+extern "C" {
+
+int csrk_spmv_fwd(csrk_dtype dtype, csrk_op op, csrk_pattern A, const void *A_val, const csrk_pattern *AT,
+                  const int64_t *AT_perm, const void *x, void *y, void *ws, size_t ws_bytes, csrk_stream_t stream)
+{
+    CSRK_TRY(check_dtype(dtype));
+    CSRK_TRY(check_op(op));
+    CSRK_TRY(check_pat(A));
+    CSRK_TRY(check_plan(A, AT, AT_perm));
+    const int64_t out_len = op == CSRK_OP_N ? A.nrows : A.ncols;
+    const int64_t in_len = op == CSRK_OP_N ? A.ncols : A.nrows;
+    if ((A.nnz > 0 && (!A_val || !x)) || (out_len > 0 && !y) || (in_len > 0 && !x && A.nnz > 0))
+        return CSRK_ERR_INVALID_ARG;
+    CSRK_TRY(validate_pattern(A, (cudaStream_t)stream));
+    return with_ws(ws, ws_bytes, [&](Bump &b) {
+        return spmv_fwd(dtype, op, A, A_val, AT, AT_perm, x, y, b, (cudaStream_t)stream);
+    });
+}
+
+int csrk_spmv_bwd(csrk_dtype dtype, csrk_op op, csrk_pattern A, const void *A_val, const csrk_pattern *AT,
+                  const int64_t *AT_perm, const void *x, const void *dy, void *dA_val, void *dx, void *ws,
+                  size_t ws_bytes, csrk_stream_t stream)
+{
+    CSRK_TRY(check_dtype(dtype));
+    CSRK_TRY(check_op(op));
+    CSRK_TRY(check_pat(A));
+    CSRK_TRY(check_plan(A, AT, AT_perm));
+    if (A.nnz > 0 && (!dy || (dA_val && !x) || (dx && !A_val))) return CSRK_ERR_INVALID_ARG;
+    if (!dA_val && !dx) return CSRK_OK;
+    CSRK_TRY(validate_pattern(A, (cudaStream_t)stream));
+    return with_ws(ws, ws_bytes, [&](Bump &b) {
+        return spmv_bwd(dtype, op, A, A_val, AT, AT_perm, x, dy, dA_val, dx, b, (cudaStream_t)stream);
+    });
+}
+
+int csrk_spmm_fwd(csrk_dtype dtype, csrk_pattern A, const void *A_val, int64_t k, const void *X, int64_t ldx, void *Y,
+                  int64_t ldy, void *ws, size_t ws_bytes, csrk_stream_t stream)
+{
+    CSRK_TRY(check_dtype(dtype));
+    CSRK_TRY(check_pat(A));
+    if (k < 0 || ldx < k || ldy < k) return CSRK_ERR_INVALID_ARG;
+    if (k > 0 && ((A.nrows > 0 && !Y) || (A.nnz > 0 && (!A_val || !X)))) return CSRK_ERR_INVALID_ARG;
+    CSRK_TRY(validate_pattern(A, (cudaStream_t)stream));
+    return with_ws(ws, ws_bytes, [&](Bump &b) {
+        return spmm_fwd(dtype, A, A_val, k, X, ldx, Y, ldy, b, (cudaStream_t)stream);
+    });
+}
+
+int csrk_spmm_bwd(csrk_dtype dtype, csrk_pattern A, const void *A_val, const csrk_pattern *AT, const int64_t *AT_perm,
+                  int64_t k, const void *X, int64_t ldx, const void *dY, int64_t lddy, void *dA_val, void *dX,
+                  int64_t lddx, void *ws, size_t ws_bytes, csrk_stream_t stream)
+{
+    CSRK_TRY(check_dtype(dtype));
+    CSRK_TRY(check_pat(A));
+    CSRK_TRY(check_plan(A, AT, AT_perm));
+    if (k < 0 || ldx < k || lddy < k || (dX && lddx < k)) return CSRK_ERR_INVALID_ARG;
+    if (!dA_val && !dX) return CSRK_OK;
+    if (k > 0 && A.nnz > 0 && (!dY || (dA_val && !X) || (dX && !A_val))) return CSRK_ERR_INVALID_ARG;
+    CSRK_TRY(validate_pattern(A, (cudaStream_t)stream));
+    return with_ws(ws, ws_bytes, [&](Bump &b) {
+        return spmm_bwd(dtype, A, A_val, AT, AT_perm, k, X, ldx, dY, lddy, dA_val, dX, lddx, b, (cudaStream_t)stream);
+    });
+}
+
+int csrk_csr_transpose(csrk_dtype dtype, csrk_pattern A, const void *A_val, int64_t *AT_indptr, int32_t *AT_indices,
+                       void *AT_val, int64_t *AT_perm, void *ws, size_t ws_bytes, csrk_stream_t stream)
+{
+    CSRK_TRY(check_dtype(dtype));
+    CSRK_TRY(check_pat(A));
+    if (!AT_indptr || (A.nnz > 0 && !AT_indices) || (AT_val && A.nnz > 0 && !A_val)) return CSRK_ERR_INVALID_ARG;
+    CSRK_TRY(validate_pattern(A, (cudaStream_t)stream));
+    return with_ws(ws, ws_bytes, [&](Bump &b) {
+        return csr_transpose(dtype, A, A_val, AT_indptr, AT_indices, AT_val, AT_perm, b, (cudaStream_t)stream);
+    });
+}
+
+int csrk_spgemm_symbolic(csrk_pattern A, csrk_pattern B, int64_t *C_indptr, int32_t *C_indices, int64_t *nnzC_host,
+                         void *ws, size_t ws_bytes, csrk_stream_t stream)
+{
+    CSRK_TRY(check_pat(A));
+    CSRK_TRY(check_pat(B));
+    if (A.ncols != B.nrows) return CSRK_ERR_DIM_MISMATCH;
+    if (!C_indptr || (!C_indices && !nnzC_host)) return CSRK_ERR_INVALID_ARG;
+    CSRK_TRY(validate_pattern(A, (cudaStream_t)stream));
+    CSRK_TRY(validate_pattern(B, (cudaStream_t)stream));
+    return with_ws(ws, ws_bytes, [&](Bump &b) {
+        return spgemm_symbolic(A, B, C_indptr, C_indices, nnzC_host, b, (cudaStream_t)stream);
+    });
+}
+
+int csrk_spgemm_numeric(csrk_dtype dtype, csrk_pattern A, const void *A_val, csrk_pattern B, const void *B_val,
+                        csrk_pattern C, void *C_val, void *ws, size_t ws_bytes, csrk_stream_t stream)
+{
+    CSRK_TRY(check_dtype(dtype));
+    CSRK_TRY(check_pat(A));
+    CSRK_TRY(check_pat(B));
+    CSRK_TRY(check_pat(C));
+    if (A.ncols != B.nrows || C.nrows != A.nrows || C.ncols != B.ncols) return CSRK_ERR_DIM_MISMATCH;
+    if ((A.nnz > 0 && !A_val) || (B.nnz > 0 && !B_val) || (C.nnz > 0 && !C_val)) return CSRK_ERR_INVALID_ARG;
+    return with_ws(ws, ws_bytes, [&](Bump &b) {
+        return spgemm_numeric(dtype, A, A_val, B, B_val, C, C_val, b, (cudaStream_t)stream);
+    });
+}
+
+int csrk_spgemm_bwd(csrk_dtype dtype, csrk_pattern A, const void *A_val, csrk_pattern B, const void *B_val,
+                    csrk_pattern C, const void *dC_val, void *dA_val, void *dB_val, void *ws, size_t ws_bytes,
+                    csrk_stream_t stream)
+{
+    CSRK_TRY(check_dtype(dtype));
+    CSRK_TRY(check_pat(A));
+    CSRK_TRY(check_pat(B));
+    CSRK_TRY(check_pat(C));
+    if (A.ncols != B.nrows || C.nrows != A.nrows || C.ncols != B.ncols) return CSRK_ERR_DIM_MISMATCH;
+    if (!dA_val && !dB_val) return CSRK_OK;
+    if ((C.nnz > 0 && !dC_val) || (A.nnz > 0 && !A_val && dB_val) || (B.nnz > 0 && !B_val && dA_val))
+        return CSRK_ERR_INVALID_ARG;
+    return with_ws(ws, ws_bytes, [&](Bump &b) {
+        return spgemm_bwd(dtype, A, A_val, B, B_val, C, dC_val, dA_val, dB_val, b, (cudaStream_t)stream);
+    });
+}
+
+int csrk_workspace_size(csrk_ws_op op, csrk_dtype dtype, const csrk_pattern *A, const csrk_pattern *B, int64_t k,
+                        int have_plan, size_t *bytes)
+{
+    if (!A || !bytes) return CSRK_ERR_INVALID_ARG;
+    CSRK_TRY(check_dtype(dtype));
+    Bump b(nullptr, 0);
+    const csrk_pattern &Ar = *A;
+    csrk_pattern dummyT{Ar.ncols, Ar.nrows, Ar.nnz, Ar.indptr, Ar.indices};
+    const csrk_pattern *plan = have_plan ? &dummyT : nullptr;
+    const int64_t *pperm = have_plan ? Ar.indptr : nullptr;
+    const void *d = Ar.indptr;  // non-null placeholder; nothing is dereferenced while sizing
+    int st = CSRK_OK;
+    switch (op) {
+    case CSRK_WS_SPMV_FWD: st = spmv_fwd(dtype, CSRK_OP_N, Ar, d, plan, pperm, d, (void *)d, b, 0); break;
+    case CSRK_WS_SPMV_BWD: st = spmv_bwd(dtype, CSRK_OP_N, Ar, d, plan, pperm, d, d, (void *)d, (void *)d, b, 0); break;
+    case CSRK_WS_SPMM_FWD: st = spmm_fwd(dtype, Ar, d, k, d, k, (void *)d, k, b, 0); break;
+    case CSRK_WS_SPMM_BWD:
+        st = spmm_bwd(dtype, Ar, d, plan, pperm, k, d, k, d, k, (void *)d, (void *)d, k, b, 0);
+        break;
+    case CSRK_WS_CSR_TRANSPOSE:
+        st = csr_transpose(dtype, Ar, d, (int64_t *)d, (int32_t *)d, (void *)d, (int64_t *)d, b, 0);
+        break;
+    case CSRK_WS_SPGEMM_SYMBOLIC:
+        if (!B) return CSRK_ERR_INVALID_ARG;
+        st = spgemm_symbolic(Ar, *B, (int64_t *)d, nullptr, (int64_t *)d, b, 0);
+        break;
+    case CSRK_WS_SPGEMM_NUMERIC:
+        if (!B) return CSRK_ERR_INVALID_ARG;
+        st = spgemm_numeric(dtype, Ar, d, *B, d, Ar, (void *)d, b, 0);
+        break;
+    case CSRK_WS_SPGEMM_BWD:
+        if (!B) return CSRK_ERR_INVALID_ARG;
+        st = spgemm_bwd(dtype, Ar, d, *B, d, Ar, d, (void *)d, (void *)d, b, 0);
+        break;
+    default: return CSRK_ERR_INVALID_ARG;
+    }
+    if (st != CSRK_OK) return st;
+    *bytes = b.used;
+    return CSRK_OK;
+}
+
+const char *csrk_status_string(int status)
+{
+    switch (status) {
+    case CSRK_OK: return "CSRK_OK";
+    case CSRK_ERR_INVALID_ARG: return "CSRK_ERR_INVALID_ARG: null/negative/unknown argument";
+    case CSRK_ERR_DIM_MISMATCH: return "CSRK_ERR_DIM_MISMATCH: dimension mismatch";
+    case CSRK_ERR_PATTERN: return "CSRK_ERR_PATTERN: non-canonical or mismatched CSR pattern";
+    case CSRK_ERR_WORKSPACE: return "CSRK_ERR_WORKSPACE: workspace too small";
+    case CSRK_ERR_INDEX_OVERFLOW: return "CSRK_ERR_INDEX_OVERFLOW: size exceeds index types";
+    case CSRK_ERR_CUDA: return "CSRK_ERR_CUDA: CUDA launch/runtime failure";
+    default: return "unknown csrk status";
+    }
+}
+
+uint64_t csrk_launch_count(void) { return g_launches.load(); }
+
+const char *csrk_version(void) { return "csrk 0.1 sm_100a"; }
+
+}  // extern "C"

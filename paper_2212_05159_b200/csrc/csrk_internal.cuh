@@ -1,0 +1,98 @@
+// csrk_internal.cuh -- shared device/host utilities of the sm_100a CSR kernel library.
+// Nothing here is visible through the C-ABI (include/csrk.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+#include <atomic>
+
+#include "csrk.h"
+
+namespace csrk {
+
+// ---------------------------------------------------------------- launches / status
+extern std::atomic<uint64_t> g_launches;
+
+#define CSRK_TRY(expr)                          \
+    do {                                        \
+        int _st = (expr);                       \
+        if (_st != CSRK_OK) return _st;         \
+    } while (0)
+
+#define CSRK_CUDA(expr)                                         \
+    do {                                                        \
+        if ((expr) != cudaSuccess) return CSRK_ERR_CUDA;        \
+    } while (0)
+
+// Launch a kernel, count it, and surface launch-configuration errors.
+#define CSRK_LAUNCH(kernel, grid, block, smem, stream, ...)                      \
+    do {                                                                         \
+        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);              \
+        ::csrk::g_launches.fetch_add(1, std::memory_order_relaxed);              \
+        if (cudaPeekAtLastError() != cudaSuccess) {                              \
+            (void)cudaGetLastError();                                            \
+            return CSRK_ERR_CUDA;                                                \
+        }                                                                        \
+    } while (0)
+
+constexpr int kNumSMs = 148;
+
+// ---------------------------------------------------------------- workspace carving
+// One planning routine per op carves its scratch from `ws` through a Bump.  In size
+// mode (base == nullptr) it only counts, so csrk_workspace_size and the op agree.
+struct Bump {
+    char *base;
+    size_t cap;
+    size_t used = 0;
+    bool overflow = false;
+    Bump(void *b, size_t c) : base(static_cast<char *>(b)), cap(c) {}
+    template <typename U>
+    U *take(size_t count) {
+        size_t off = (used + 255) & ~size_t(255);
+        size_t bytes = count * sizeof(U);
+        used = off + bytes;
+        if (base && used > cap) overflow = true;
+        return base ? reinterpret_cast<U *>(base + off) : nullptr;
+    }
+    bool sizing() const { return base == nullptr; }
+};
+
+// ---------------------------------------------------------------- dtype helpers
+template <typename T> struct Acc { using type = double; };   // fp32 and fp64 data accumulate in fp64
+
+__device__ __forceinline__ void red_add(double *a, double v) { atomicAdd(a, v); }
+__device__ __forceinline__ void red_add(float *a, float v) { atomicAdd(a, v); }
+
+// ---------------------------------------------------------------- merge-path search
+// Merge of (row-end offsets a[0..nr), nnz indices 0..Z-1): at state (i, j) the next item
+// is the end of row i if a[i] <= j, else nnz j.  Returns i (rows consumed) for diagonal d.
+__device__ __forceinline__ int merge_path_rows(int d, int nr, int Z, const int64_t *s_ptr, int64_t base)
+{
+    int lo = d - Z > 0 ? d - Z : 0;
+    int hi = d < nr ? d : nr;
+    while (lo < hi) {
+        int piv = (lo + hi) >> 1;
+        if (s_ptr[piv + 1] - base <= (int64_t)(d - piv - 1)) lo = piv + 1;
+        else hi = piv;
+    }
+    return lo;
+}
+
+// ---------------------------------------------------------------- host utilities (utils.cu)
+// In-place int64 prefix sum: data[0] := 0 is NOT written; data[1..n] := inclusive scan of
+// data[1..n].  Used to turn counts stored at indptr[1..] into a CSR indptr.
+int scan_counts_i64(int64_t *indptr, int64_t n, Bump &ws, cudaStream_t s);
+size_t scan_ws_bytes(int64_t n);
+
+// Row-length classification etc.
+int validate_pattern(const csrk_pattern &A, cudaStream_t s);  // honours CSRK_VALIDATE
+
+// Internal transpose (pattern + perm, optional values) used by ops that need A^T when
+// the caller passes no plan.  ws sized by transpose_ws(A).
+int transpose_impl(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int64_t *AT_indptr,
+                   int32_t *AT_indices, void *AT_val, int64_t *perm, Bump &ws, cudaStream_t s);
+
+__host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace csrk

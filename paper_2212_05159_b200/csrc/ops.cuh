@@ -1,0 +1,26 @@
+// ops.cuh -- internal entry points behind the C-ABI (abi.cu does validation + dispatch).
+#pragma once
+
+#include "csrk_internal.cuh"
+
+namespace csrk {
+
+int spmv_fwd(csrk_dtype dt, csrk_op op, const csrk_pattern &A, const void *A_val, const csrk_pattern *AT,
+             const int64_t *perm, const void *x, void *y, Bump &ws, cudaStream_t s);
+int spmv_bwd(csrk_dtype dt, csrk_op op, const csrk_pattern &A, const void *A_val, const csrk_pattern *AT,
+             const int64_t *perm, const void *x, const void *dy, void *dA, void *dx, Bump &ws, cudaStream_t s);
+int spmm_fwd(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int64_t k, const void *X, int64_t ldx,
+             void *Y, int64_t ldy, Bump &ws, cudaStream_t s);
+int spmm_bwd(csrk_dtype dt, const csrk_pattern &A, const void *A_val, const csrk_pattern *AT, const int64_t *perm,
+             int64_t k, const void *X, int64_t ldx, const void *dY, int64_t lddy, void *dA, void *dX, int64_t lddx,
+             Bump &ws, cudaStream_t s);
+int csr_transpose(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int64_t *AT_indptr, int32_t *AT_indices,
+                  void *AT_val, int64_t *perm, Bump &ws, cudaStream_t s);
+int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *C_indptr, int32_t *C_indices,
+                    int64_t *nnzC_host, Bump &ws, cudaStream_t s);
+int spgemm_numeric(csrk_dtype dt, const csrk_pattern &A, const void *A_val, const csrk_pattern &B,
+                   const void *B_val, const csrk_pattern &C, void *C_val, Bump &ws, cudaStream_t s);
+int spgemm_bwd(csrk_dtype dt, const csrk_pattern &A, const void *A_val, const csrk_pattern &B, const void *B_val,
+               const csrk_pattern &C, const void *dC, void *dA, void *dB, Bump &ws, cudaStream_t s);
+
+}  // namespace csrk

@@ -1,0 +1,96 @@
+// spmv.cu -- SpMV forward and backward (PAPER 3.1.1; Table 1).
+#include "ops.cuh"
+#include "tile.cuh"
+
+namespace csrk {
+
+template <typename T>
+static int spmv_fwd_t(csrk_op op, const csrk_pattern &A, const T *A_val, const csrk_pattern *AT,
+                      const int64_t *perm, const T *x, T *y, Bump &ws, cudaStream_t s)
+{
+    if (ws.sizing()) return CSRK_OK;
+    TileArgs<T> a{};
+    if (op == CSRK_OP_N) {
+        // y_i = sum_{p in row i} A[p] x[idx p]
+        a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices;
+        a.vals = A_val; a.v = x; a.y = y;
+        a.R = tile_rows(A.nrows, A.nnz);
+        return launch_tile<T, MODE_REDUCE, false, false>(a, s);
+    }
+    if (AT) {
+        // y = A^T x as row inner products of the cached transpose, values gathered via perm
+        a.nrows = AT->nrows; a.indptr = AT->indptr; a.indices = AT->indices;
+        a.vals = A_val; a.perm = perm; a.v = x; a.y = y;
+        a.R = tile_rows(AT->nrows, AT->nnz);
+        return launch_tile<T, MODE_REDUCE, true, false>(a, s);
+    }
+    // y = A^T x by atomic scatter of A_ij x_i into y_j
+    CSRK_CUDA(cudaMemsetAsync(y, 0, sizeof(T) * (size_t)A.ncols, s));
+    a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices;
+    a.vals = A_val; a.u = x; a.y = y;
+    a.R = tile_rows(A.nrows, A.nnz);
+    return launch_tile<T, MODE_SCATTER, false, false>(a, s);
+}
+
+template <typename T>
+static int spmv_bwd_t(csrk_op op, const csrk_pattern &A, const T *A_val, const csrk_pattern *AT,
+                      const int64_t *perm, const T *x, const T *dy, T *dA, T *dx, Bump &ws, cudaStream_t s)
+{
+    if (ws.sizing()) return CSRK_OK;
+    TileArgs<T> a{};
+    if (op == CSRK_OP_T) {
+        // y = A^T x:  dx = A dy (row inner products),  dA[p] = x_i dy_{idx p}
+        a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices;
+        a.vals = A_val; a.v = dy; a.u = x;
+        a.R = tile_rows(A.nrows, A.nnz);
+        if (dx) {
+            a.y = dx;
+            if (dA) {
+                a.D = dA;
+                return launch_tile<T, MODE_REDUCE, false, true>(a, s);
+            }
+            return launch_tile<T, MODE_REDUCE, false, false>(a, s);
+        }
+        a.D = dA;  // dA only: scatter mode without the atomic output
+        return launch_tile<T, MODE_SCATTER, false, true>(a, s);
+    }
+    // op N (y = A x)
+    if (AT && dx) {
+        // transposed traversal: dx_j = sum_q A[perm q] dy[AT idx q];  dA[perm q] = dy[AT idx q] x_j
+        a.nrows = AT->nrows; a.indptr = AT->indptr; a.indices = AT->indices;
+        a.vals = A_val; a.perm = perm; a.v = dy; a.u = x; a.y = dx;
+        a.R = tile_rows(AT->nrows, AT->nnz);
+        if (dA) {
+            a.D = dA;
+            return launch_tile<T, MODE_REDUCE, true, true>(a, s);
+        }
+        return launch_tile<T, MODE_REDUCE, true, false>(a, s);
+    }
+    // row traversal: dA[p] = dy_i x[idx p] (coalesced), dx[idx p] += A[p] dy_i (atomic)
+    if (dx) CSRK_CUDA(cudaMemsetAsync(dx, 0, sizeof(T) * (size_t)A.ncols, s));
+    a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices;
+    a.vals = A_val; a.u = dy; a.v = x; a.y = dx; a.D = dA;
+    a.R = tile_rows(A.nrows, A.nnz);
+    if (dA) return launch_tile<T, MODE_SCATTER, false, true>(a, s);
+    return launch_tile<T, MODE_SCATTER, false, false>(a, s);
+}
+
+int spmv_fwd(csrk_dtype dt, csrk_op op, const csrk_pattern &A, const void *A_val, const csrk_pattern *AT,
+             const int64_t *perm, const void *x, void *y, Bump &ws, cudaStream_t s)
+{
+    if (dt == CSRK_F64)
+        return spmv_fwd_t<double>(op, A, (const double *)A_val, AT, perm, (const double *)x, (double *)y, ws, s);
+    return spmv_fwd_t<float>(op, A, (const float *)A_val, AT, perm, (const float *)x, (float *)y, ws, s);
+}
+
+int spmv_bwd(csrk_dtype dt, csrk_op op, const csrk_pattern &A, const void *A_val, const csrk_pattern *AT,
+             const int64_t *perm, const void *x, const void *dy, void *dA, void *dx, Bump &ws, cudaStream_t s)
+{
+    if (dt == CSRK_F64)
+        return spmv_bwd_t<double>(op, A, (const double *)A_val, AT, perm, (const double *)x, (const double *)dy,
+                                  (double *)dA, (double *)dx, ws, s);
+    return spmv_bwd_t<float>(op, A, (const float *)A_val, AT, perm, (const float *)x, (const float *)dy,
+                             (float *)dA, (float *)dx, ws, s);
+}
+
+}  // namespace csrk

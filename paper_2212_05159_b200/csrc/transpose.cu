@@ -1,0 +1,296 @@
+// transpose.cu -- CSR transpose with position map ("take the sparse transpose of A";
+// S:53-61).  Counting sort by column:
+//   1. column histogram (int64 atomics into AT_indptr[1..n])
+//   2. int64 prefix scan -> AT_indptr
+//   3. row-tile scatter: each nonzero claims a slot of its column (atomic cursor) and
+//      writes its row and source position (tile.cuh, MODE_TRANSPOSE)
+//   4. per-column sort by row (thread / warp / CTA / merge-sort bins by length) -- makes
+//      the result canonical and bit-identical to the stable counting sort of the oracle
+//   5. AT_val[q] = A_val[perm[q]]
+#include "ops.cuh"
+#include "tile.cuh"
+
+namespace csrk {
+
+constexpr int kShortMax = 16;
+constexpr int kWarpMax = 1024;
+constexpr int kBlockMax = 8192;
+constexpr int kSortTPB = 256;
+
+__global__ void k_col_count(int64_t nnz, const int32_t *__restrict__ indices, unsigned long long *__restrict__ cnt)
+{
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&cnt[indices[p]], 1ULL);
+}
+
+struct SortLists {
+    int32_t *mid, *big, *huge;
+    int *count;  // [3]
+    int64_t cap_mid, cap_big, cap_huge;
+};
+
+// Short columns are sorted in place by one thread (insertion sort); longer ones are queued.
+__global__ void k_sort_short(int64_t n, const int64_t *__restrict__ ATp, int32_t *__restrict__ ATi,
+                             int64_t *__restrict__ perm, SortLists L)
+{
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = ATp[j], len = ATp[j + 1] - s;
+        if (len <= 1) continue;
+        if (len <= kShortMax) {
+            int32_t key[kShortMax];
+            int64_t pay[kShortMax];
+            for (int i = 0; i < len; ++i) { key[i] = ATi[s + i]; pay[i] = perm[s + i]; }
+            for (int i = 1; i < len; ++i) {
+                int32_t k = key[i];
+                int64_t p = pay[i];
+                int t = i - 1;
+                while (t >= 0 && key[t] > k) { key[t + 1] = key[t]; pay[t + 1] = pay[t]; --t; }
+                key[t + 1] = k;
+                pay[t + 1] = p;
+            }
+            for (int i = 0; i < len; ++i) { ATi[s + i] = key[i]; perm[s + i] = pay[i]; }
+        } else if (len <= kWarpMax) {
+            L.mid[atomicAdd(&L.count[0], 1)] = (int32_t)j;
+        } else if (len <= kBlockMax) {
+            L.big[atomicAdd(&L.count[1], 1)] = (int32_t)j;
+        } else {
+            L.huge[atomicAdd(&L.count[2], 1)] = (int32_t)j;
+        }
+    }
+}
+
+// Bitonic sort of (key, payload) pairs held in shared memory; `nt` threads cooperate.
+template <bool WARP>
+__device__ __forceinline__ void smem_bitonic(int32_t *key, int64_t *pay, int P, int t, int nt)
+{
+    for (int k = 2; k <= P; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = t; i < P; i += nt) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const bool asc = (i & k) == 0;
+                    if ((key[i] > key[ixj]) == asc) {
+                        int32_t tk = key[i]; key[i] = key[ixj]; key[ixj] = tk;
+                        int64_t tp = pay[i]; pay[i] = pay[ixj]; pay[ixj] = tp;
+                    }
+                }
+            }
+            if (WARP) __syncwarp(); else __syncthreads();
+        }
+}
+
+__device__ __forceinline__ int pow2ceil(int x)
+{
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+constexpr int kWarpsPerSortCTA = 4;
+
+__global__ __launch_bounds__(32 * kWarpsPerSortCTA) void k_sort_warp(const int64_t *__restrict__ ATp,
+                                                                     int32_t *__restrict__ ATi,
+                                                                     int64_t *__restrict__ perm, SortLists L)
+{
+    __shared__ int32_t s_key[kWarpsPerSortCTA][kWarpMax];
+    __shared__ int64_t s_pay[kWarpsPerSortCTA][kWarpMax];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cnt = *(volatile int *)&L.count[0];
+    for (int it = blockIdx.x * kWarpsPerSortCTA + w; it < cnt; it += gridDim.x * kWarpsPerSortCTA) {
+        const int64_t j = L.mid[it];
+        const int64_t s = ATp[j];
+        const int len = (int)(ATp[j + 1] - s);
+        const int P = pow2ceil(len);
+        for (int i = lane; i < P; i += 32) {
+            s_key[w][i] = i < len ? ATi[s + i] : INT32_MAX;
+            s_pay[w][i] = i < len ? perm[s + i] : 0;
+        }
+        __syncwarp();
+        smem_bitonic<true>(s_key[w], s_pay[w], P, lane, 32);
+        for (int i = lane; i < len; i += 32) {
+            ATi[s + i] = s_key[w][i];
+            perm[s + i] = s_pay[w][i];
+        }
+        __syncwarp();
+    }
+}
+
+__global__ __launch_bounds__(kSortTPB) void k_sort_block(const int64_t *__restrict__ ATp, int32_t *__restrict__ ATi,
+                                                         int64_t *__restrict__ perm, SortLists L)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    int64_t *s_pay = reinterpret_cast<int64_t *>(smem);
+    int32_t *s_key = reinterpret_cast<int32_t *>(smem + sizeof(int64_t) * kBlockMax);
+    const int cnt = *(volatile int *)&L.count[1];
+    for (int it = blockIdx.x; it < cnt; it += gridDim.x) {
+        const int64_t j = L.big[it];
+        const int64_t s = ATp[j];
+        const int len = (int)(ATp[j + 1] - s);
+        const int P = pow2ceil(len);
+        for (int i = threadIdx.x; i < P; i += kSortTPB) {
+            s_key[i] = i < len ? ATi[s + i] : INT32_MAX;
+            s_pay[i] = i < len ? perm[s + i] : 0;
+        }
+        __syncthreads();
+        smem_bitonic<false>(s_key, s_pay, P, threadIdx.x, kSortTPB);
+        for (int i = threadIdx.x; i < len; i += kSortTPB) {
+            ATi[s + i] = s_key[i];
+            perm[s + i] = s_pay[i];
+        }
+        __syncthreads();
+    }
+}
+
+// Huge columns: sort the source positions only (p ascending <=> row ascending within a
+// column), by CTA-wide bitonic runs of kBlockMax followed by merge passes through `buf`;
+// then recover the row of each position by binary search in A.indptr.
+__global__ __launch_bounds__(kSortTPB) void k_sort_huge(int64_t m, const int64_t *__restrict__ Ap,
+                                                        const int64_t *__restrict__ ATp, int32_t *__restrict__ ATi,
+                                                        int64_t *__restrict__ perm, int64_t *__restrict__ buf,
+                                                        SortLists L)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    int64_t *s_pay = reinterpret_cast<int64_t *>(smem);
+    int32_t *s_key = reinterpret_cast<int32_t *>(smem + sizeof(int64_t) * kBlockMax);
+    const int cnt = *(volatile int *)&L.count[2];
+    for (int it = blockIdx.x; it < cnt; it += gridDim.x) {
+        const int64_t j = L.huge[it];
+        const int64_t s = ATp[j];
+        const int64_t len = ATp[j + 1] - s;
+        // runs of kBlockMax sorted in shared memory (keys = low bits unused; sort by payload)
+        for (int64_t r = 0; r < len; r += kBlockMax) {
+            const int rl = (int)(len - r < kBlockMax ? len - r : kBlockMax);
+            const int P = pow2ceil(rl);
+            for (int i = threadIdx.x; i < P; i += kSortTPB) {
+                // order by position: use the row as key (rows are distinct and increasing with p)
+                s_key[i] = i < rl ? ATi[s + r + i] : INT32_MAX;
+                s_pay[i] = i < rl ? perm[s + r + i] : 0;
+            }
+            __syncthreads();
+            smem_bitonic<false>(s_key, s_pay, P, threadIdx.x, kSortTPB);
+            for (int i = threadIdx.x; i < rl; i += kSortTPB) perm[s + r + i] = s_pay[i];
+            __syncthreads();
+        }
+        // merge passes (payload only), ping-pong between perm and buf
+        int64_t *src = perm + s, *dst = buf + s;
+        for (int64_t width = kBlockMax; width < len; width <<= 1) {
+            for (int64_t lo = 0; lo < len; lo += 2 * width) {
+                const int64_t mid = lo + width < len ? lo + width : len;
+                const int64_t hi = lo + 2 * width < len ? lo + 2 * width : len;
+                const int64_t na = mid - lo, nb = hi - mid, tot = na + nb;
+                const int64_t per = cdiv(tot, kSortTPB);
+                const int64_t d0 = (int64_t)threadIdx.x * per < tot ? (int64_t)threadIdx.x * per : tot;
+                const int64_t d1 = d0 + per < tot ? d0 + per : tot;
+                // merge-path search for d0
+                int64_t a_lo = d0 - nb > 0 ? d0 - nb : 0, a_hi = d0 < na ? d0 : na;
+                while (a_lo < a_hi) {
+                    int64_t piv = (a_lo + a_hi) >> 1;
+                    if (src[lo + piv] < src[mid + d0 - piv - 1]) a_lo = piv + 1;
+                    else a_hi = piv;
+                }
+                int64_t ia = a_lo, ib = d0 - a_lo;
+                for (int64_t d = d0; d < d1; ++d) {
+                    if (ib >= nb || (ia < na && src[lo + ia] < src[mid + ib])) dst[lo + d] = src[lo + ia++];
+                    else dst[lo + d] = src[mid + ib++];
+                }
+            }
+            __syncthreads();
+            int64_t *t = src; src = dst; dst = t;
+        }
+        if (src != perm + s)
+            for (int64_t i = threadIdx.x; i < len; i += kSortTPB) perm[s + i] = src[i];
+        __syncthreads();
+        // rows from positions
+        for (int64_t i = threadIdx.x; i < len; i += kSortTPB) {
+            const int64_t p = perm[s + i];
+            int64_t lo = 0, hi = m;  // largest row with Ap[row] <= p
+            while (hi - lo > 1) {
+                int64_t piv = (lo + hi) >> 1;
+                if (Ap[piv] <= p) lo = piv; else hi = piv;
+            }
+            ATi[s + i] = (int32_t)lo;
+        }
+        __syncthreads();
+    }
+}
+
+template <typename T>
+__global__ void k_gather_vals(int64_t nnz, const int64_t *__restrict__ perm, const T *__restrict__ A_val,
+                              T *__restrict__ AT_val)
+{
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz; q += (int64_t)gridDim.x * blockDim.x)
+        AT_val[q] = A_val[perm[q]];
+}
+
+static unsigned grid_for(int64_t work, int tpb)
+{
+    int64_t g = cdiv(work, tpb);
+    const int64_t cap = (int64_t)kNumSMs * 16;
+    return (unsigned)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+int transpose_impl(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int64_t *ATp, int32_t *ATi,
+                   void *AT_val, int64_t *perm, Bump &ws, cudaStream_t s)
+{
+    const int64_t n = A.ncols, nnz = A.nnz;
+    int64_t *cursor = ws.take<int64_t>(n > 0 ? n : 1);
+    int64_t *pm = perm ? perm : ws.take<int64_t>(nnz > 0 ? nnz : 1);
+    SortLists L{};
+    L.cap_mid = nnz / (kShortMax + 1) + 1;
+    L.cap_big = nnz / (kWarpMax + 1) + 1;
+    L.cap_huge = nnz / (kBlockMax + 1) + 1;
+    L.mid = ws.take<int32_t>(L.cap_mid);
+    L.big = ws.take<int32_t>(L.cap_big);
+    L.huge = ws.take<int32_t>(L.cap_huge);
+    L.count = ws.take<int>(4);
+    int64_t *buf = ws.take<int64_t>(nnz > kBlockMax ? nnz : 1);
+    if (ws.sizing()) return scan_counts_i64(nullptr, n, ws, s);  // carve the scan scratch
+
+    CSRK_CUDA(cudaMemsetAsync(ATp, 0, sizeof(int64_t) * (size_t)(n + 1), s));
+    if (nnz > 0)
+        CSRK_LAUNCH(k_col_count, grid_for(nnz, 256), 256, 0, s, nnz, A.indices,
+                    reinterpret_cast<unsigned long long *>(ATp + 1));
+    CSRK_TRY(scan_counts_i64(ATp, n, ws, s));
+    if (nnz == 0) return CSRK_OK;
+    CSRK_CUDA(cudaMemcpyAsync(cursor, ATp, sizeof(int64_t) * (size_t)n, cudaMemcpyDeviceToDevice, s));
+    CSRK_CUDA(cudaMemsetAsync(L.count, 0, sizeof(int) * 4, s));
+    {
+        TileArgs<double> a{};
+        a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices;
+        a.cursor = cursor; a.out_idx = ATi; a.out_perm = pm;
+        a.R = tile_rows(A.nrows, nnz);
+        CSRK_TRY((launch_tile<double, MODE_TRANSPOSE, false, false>(a, s)));
+    }
+    CSRK_LAUNCH(k_sort_short, grid_for(n, 256), 256, 0, s, n, (const int64_t *)ATp, ATi, pm, L);
+    if (nnz > kShortMax)
+        CSRK_LAUNCH(k_sort_warp, (unsigned)(kNumSMs * 4), 32 * kWarpsPerSortCTA, 0, s, (const int64_t *)ATp, ATi, pm, L);
+    const size_t big_smem = (sizeof(int64_t) + sizeof(int32_t)) * kBlockMax;
+    static bool attr = false;
+    if (!attr) {
+        CSRK_CUDA(cudaFuncSetAttribute(k_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big_smem));
+        CSRK_CUDA(cudaFuncSetAttribute(k_sort_huge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big_smem));
+        attr = true;
+    }
+    if (nnz > kWarpMax)
+        CSRK_LAUNCH(k_sort_block, (unsigned)kNumSMs, kSortTPB, big_smem, s, (const int64_t *)ATp, ATi, pm, L);
+    if (nnz > kBlockMax)
+        CSRK_LAUNCH(k_sort_huge, (unsigned)kNumSMs, kSortTPB, big_smem, s, A.nrows, A.indptr, (const int64_t *)ATp,
+                    ATi, pm, buf, L);
+    if (AT_val) {
+        if (dt == CSRK_F64)
+            CSRK_LAUNCH(k_gather_vals<double>, grid_for(nnz, 256), 256, 0, s, nnz, (const int64_t *)pm,
+                        (const double *)A_val, (double *)AT_val);
+        else
+            CSRK_LAUNCH(k_gather_vals<float>, grid_for(nnz, 256), 256, 0, s, nnz, (const int64_t *)pm,
+                        (const float *)A_val, (float *)AT_val);
+    }
+    return CSRK_OK;
+}
+
+int csr_transpose(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int64_t *AT_indptr, int32_t *AT_indices,
+                  void *AT_val, int64_t *perm, Bump &ws, cudaStream_t s)
+{
+    return transpose_impl(dt, A, A_val, AT_indptr, AT_indices, AT_val, perm, ws, s);
+}
+
+}  // namespace csrk

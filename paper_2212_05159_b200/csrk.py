@@ -1,0 +1,269 @@
+"""Thin Python binding of the C-ABI in include/csrk.h (argument marshalling only).
+
+Every function here forwards device pointers of torch CUDA tensors to libcsrk.so on the
+current torch stream; all arithmetic runs in the sm_100a kernels.  There is no CPU or
+PyTorch fallback: if libcsrk.so is missing or a call fails, an exception is raised.
+
+Names follow the ABI (and the paper's operations, Table 1):
+spmv_fwd / spmv_bwd (SpMV), spmm_fwd / spmm_bwd (SpDMM), csr_transpose,
+spgemm_symbolic / spgemm_numeric / spgemm_bwd (SpSpMM).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libcsrk.so")
+
+F32, F64 = 0, 1
+OP_N, OP_T = 0, 1
+WS = dict(spmv_fwd=0, spmv_bwd=1, spmm_fwd=2, spmm_bwd=3, csr_transpose=4, spgemm_symbolic=5,
+          spgemm_numeric=6, spgemm_bwd=7)
+
+# Every symbol declared in include/csrk.h (checked by tests/test_abi_cpu.py).
+ABI_SYMBOLS = ("csrk_spmv_fwd", "csrk_spmv_bwd", "csrk_spmm_fwd", "csrk_spmm_bwd", "csrk_csr_transpose",
+               "csrk_spgemm_symbolic", "csrk_spgemm_numeric", "csrk_spgemm_bwd", "csrk_workspace_size",
+               "csrk_status_string", "csrk_launch_count", "csrk_version")
+
+
+class Pattern(ctypes.Structure):
+    _fields_ = [("nrows", ctypes.c_int64), ("ncols", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("indptr", ctypes.c_void_p), ("indices", ctypes.c_void_p)]
+
+
+class CsrkError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libcsrk.so; raises if the CUDA extension has not been built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libcsrk.so not found at {LIB_PATH}: run `python -m paper_2212_05159_b200.build` "
+                          "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    P, I64, SZ, Pat = ctypes.c_void_p, ctypes.c_int64, ctypes.c_size_t, Pattern
+    PatP = ctypes.POINTER(Pattern)
+    I = ctypes.c_int
+    L.csrk_spmv_fwd.argtypes = [I, I, Pat, P, PatP, P, P, P, P, SZ, P]
+    L.csrk_spmv_bwd.argtypes = [I, I, Pat, P, PatP, P, P, P, P, P, P, SZ, P]
+    L.csrk_spmm_fwd.argtypes = [I, Pat, P, I64, P, I64, P, I64, P, SZ, P]
+    L.csrk_spmm_bwd.argtypes = [I, Pat, P, PatP, P, I64, P, I64, P, I64, P, P, I64, P, SZ, P]
+    L.csrk_csr_transpose.argtypes = [I, Pat, P, P, P, P, P, P, SZ, P]
+    L.csrk_spgemm_symbolic.argtypes = [Pat, Pat, P, P, ctypes.POINTER(I64), P, SZ, P]
+    L.csrk_spgemm_numeric.argtypes = [I, Pat, P, Pat, P, Pat, P, P, SZ, P]
+    L.csrk_spgemm_bwd.argtypes = [I, Pat, P, Pat, P, Pat, P, P, P, P, SZ, P]
+    L.csrk_workspace_size.argtypes = [I, I, PatP, PatP, I64, I, ctypes.POINTER(SZ)]
+    L.csrk_status_string.restype = ctypes.c_char_p
+    L.csrk_status_string.argtypes = [I]
+    L.csrk_launch_count.restype = ctypes.c_uint64
+    L.csrk_version.restype = ctypes.c_char_p
+    for name in ABI_SYMBOLS:
+        if name not in ("csrk_status_string", "csrk_launch_count", "csrk_version"):
+            getattr(L, name).restype = I
+    _lib = L
+    return L
+
+
+def launch_count() -> int:
+    return int(lib().csrk_launch_count())
+
+
+def _check(st: int, what: str):
+    if st != 0:
+        raise CsrkError(f"{what}: {lib().csrk_status_string(st).decode()} ({st})")
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.float64:
+        return F64
+    if t.dtype == torch.float32:
+        return F32
+    raise TypeError(f"unsupported dtype {t.dtype}")
+
+
+@dataclass
+class CSR:
+    """Device CSR: indptr int64[nrows+1], indices int32[nnz], values float32/64[nnz] or None."""
+    nrows: int
+    ncols: int
+    indptr: torch.Tensor
+    indices: torch.Tensor
+    values: torch.Tensor | None = None
+
+    @property
+    def nnz(self) -> int:
+        return int(self.indices.numel())
+
+    def pattern(self) -> Pattern:
+        return Pattern(self.nrows, self.ncols, self.nnz, self.indptr.data_ptr(), self.indices.data_ptr())
+
+    @staticmethod
+    def from_host(A, device="cuda", dtype=None) -> "CSR":
+        """Upload a synth.CSR (numpy) to the device."""
+        vals = None if A.values is None else torch.from_numpy(A.values).to(device)
+        if vals is not None and dtype is not None:
+            vals = vals.to(dtype)
+        return CSR(A.nrows, A.ncols, torch.from_numpy(A.indptr).to(device), torch.from_numpy(A.indices).to(device), vals)
+
+
+@dataclass
+class TransposePlan:
+    """Cached A^T: pattern (n x m) plus perm[q] = position in A of A^T's q-th entry."""
+    AT: CSR
+    perm: torch.Tensor
+
+    def args(self):
+        p = self.AT.pattern()
+        return ctypes.byref(p), _ptr(self.perm), p  # keep p alive
+
+
+_ws_cache: dict = {}
+
+
+def _workspace(op: str, dtype: int, A: CSR, B: CSR | None = None, k: int = 0, have_plan: bool = False):
+    pa = A.pattern()
+    pb = B.pattern() if B is not None else None
+    n = ctypes.c_size_t(0)
+    _check(lib().csrk_workspace_size(WS[op], dtype, ctypes.byref(pa), ctypes.byref(pb) if pb else None, k,
+                                     int(have_plan), ctypes.byref(n)), f"workspace_size({op})")
+    nbytes = int(n.value)
+    if nbytes == 0:
+        return None, 0
+    dev = A.indptr.device
+    buf = _ws_cache.get(dev)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
+        _ws_cache[dev] = buf
+    return _ptr(buf), buf.numel()
+
+
+def spmv_fwd(A: CSR, x: torch.Tensor, op: int = OP_N, plan: TransposePlan | None = None,
+             out: torch.Tensor | None = None) -> torch.Tensor:
+    """y = A x (op N) or y = A^T x (op T).  PAPER 3.1.1."""
+    dt = _dt(A.values)
+    y = out if out is not None else torch.empty(A.nrows if op == OP_N else A.ncols, dtype=A.values.dtype,
+                                                device=A.values.device)
+    pp = plan.args() if plan else (None, None, None)
+    ws, wsb = _workspace("spmv_fwd", dt, A, have_plan=plan is not None)
+    _check(lib().csrk_spmv_fwd(dt, op, A.pattern(), _ptr(A.values), pp[0], pp[1], _ptr(x), _ptr(y), ws, wsb,
+                               _stream()), "spmv_fwd")
+    return y
+
+
+def spmv_bwd(A: CSR, x: torch.Tensor, dy: torch.Tensor, op: int = OP_N, plan: TransposePlan | None = None,
+             need_dA: bool = True, need_dx: bool = True, dA: torch.Tensor | None = None,
+             dx: torch.Tensor | None = None):
+    """VJP of SpMV (Table 1): dA = (dy x^T) (.) mask(A) on A's pattern, dx = A^T dy."""
+    dt = _dt(A.values)
+    if need_dA and dA is None:
+        dA = torch.empty_like(A.values)
+    if need_dx and dx is None:
+        dx = torch.empty(A.ncols if op == OP_N else A.nrows, dtype=A.values.dtype, device=A.values.device)
+    pp = plan.args() if plan else (None, None, None)
+    ws, wsb = _workspace("spmv_bwd", dt, A, have_plan=plan is not None)
+    _check(lib().csrk_spmv_bwd(dt, op, A.pattern(), _ptr(A.values), pp[0], pp[1], _ptr(x), _ptr(dy),
+                               _ptr(dA if need_dA else None), _ptr(dx if need_dx else None), ws, wsb, _stream()),
+           "spmv_bwd")
+    return (dA if need_dA else None), (dx if need_dx else None)
+
+
+def spmm_fwd(A: CSR, X: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Y = A X, X row-major n x k."""
+    dt = _dt(A.values)
+    k = X.shape[1]
+    Y = out if out is not None else torch.empty((A.nrows, k), dtype=X.dtype, device=X.device)
+    ws, wsb = _workspace("spmm_fwd", dt, A, k=k)
+    _check(lib().csrk_spmm_fwd(dt, A.pattern(), _ptr(A.values), k, _ptr(X), X.stride(0), _ptr(Y), Y.stride(0), ws,
+                               wsb, _stream()), "spmm_fwd")
+    return Y
+
+
+def spmm_bwd(A: CSR, X: torch.Tensor, dY: torch.Tensor, plan: TransposePlan | None = None, need_dA: bool = True,
+             need_dX: bool = True, dA: torch.Tensor | None = None, dX: torch.Tensor | None = None):
+    """VJP of SpDMM (Table 1): dA = (dY X^T) (.) mask(A), dX = A^T dY."""
+    dt = _dt(A.values)
+    k = X.shape[1]
+    if need_dA and dA is None:
+        dA = torch.empty_like(A.values)
+    if need_dX and dX is None:
+        dX = torch.empty((A.ncols, k), dtype=X.dtype, device=X.device)
+    pp = plan.args() if plan else (None, None, None)
+    ws, wsb = _workspace("spmm_bwd", dt, A, k=k, have_plan=plan is not None)
+    _check(lib().csrk_spmm_bwd(dt, A.pattern(), _ptr(A.values), pp[0], pp[1], k, _ptr(X), X.stride(0), _ptr(dY),
+                               dY.stride(0), _ptr(dA if need_dA else None), _ptr(dX if need_dX else None),
+                               dX.stride(0) if need_dX else k, ws, wsb, _stream()), "spmm_bwd")
+    return (dA if need_dA else None), (dX if need_dX else None)
+
+
+def csr_transpose(A: CSR, with_values: bool = True, out: TransposePlan | None = None) -> TransposePlan:
+    """A^T in canonical CSR + perm.  Values optional (gathered through perm)."""
+    dev = A.indptr.device
+    dt = _dt(A.values) if A.values is not None else F64
+    if out is None:
+        ATv = torch.empty_like(A.values) if (with_values and A.values is not None) else None
+        out = TransposePlan(CSR(A.ncols, A.nrows, torch.empty(A.ncols + 1, dtype=torch.int64, device=dev),
+                                torch.empty(A.nnz, dtype=torch.int32, device=dev), ATv),
+                            torch.empty(A.nnz, dtype=torch.int64, device=dev))
+    ws, wsb = _workspace("csr_transpose", dt, A)
+    _check(lib().csrk_csr_transpose(dt, A.pattern(), _ptr(A.values), _ptr(out.AT.indptr), _ptr(out.AT.indices),
+                                    _ptr(out.AT.values), _ptr(out.perm), ws, wsb, _stream()), "csr_transpose")
+    return out
+
+
+def spgemm_symbolic(A: CSR, B: CSR) -> CSR:
+    """Structural pattern of C = A B, columns sorted.  One host sync for nnz(C)."""
+    dev = A.indptr.device
+    Cp = torch.empty(A.nrows + 1, dtype=torch.int64, device=dev)
+    nnz = ctypes.c_int64(0)
+    ws, wsb = _workspace("spgemm_symbolic", F64, A, B)
+    _check(lib().csrk_spgemm_symbolic(A.pattern(), B.pattern(), _ptr(Cp), None, ctypes.byref(nnz), ws, wsb,
+                                      _stream()), "spgemm_symbolic(count)")
+    Ci = torch.empty(int(nnz.value), dtype=torch.int32, device=dev)
+    if Ci.numel() == 0:
+        return CSR(A.nrows, B.ncols, Cp, Ci, None)
+    _check(lib().csrk_spgemm_symbolic(A.pattern(), B.pattern(), _ptr(Cp), _ptr(Ci), None, ws, wsb, _stream()),
+           "spgemm_symbolic(fill)")
+    return CSR(A.nrows, B.ncols, Cp, Ci, None)
+
+
+def spgemm_numeric(A: CSR, B: CSR, C: CSR, out: torch.Tensor | None = None) -> torch.Tensor:
+    """C_ij = sum_k A_ik B_kj over the symbolic pattern."""
+    dt = _dt(A.values)
+    Cv = out if out is not None else torch.empty(C.nnz, dtype=A.values.dtype, device=A.values.device)
+    ws, wsb = _workspace("spgemm_numeric", dt, A, B)
+    _check(lib().csrk_spgemm_numeric(dt, A.pattern(), _ptr(A.values), B.pattern(), _ptr(B.values), C.pattern(),
+                                     _ptr(Cv), ws, wsb, _stream()), "spgemm_numeric")
+    return Cv
+
+
+def spgemm_bwd(A: CSR, B: CSR, C: CSR, dC: torch.Tensor, need_dA: bool = True, need_dB: bool = True,
+               dA: torch.Tensor | None = None, dB: torch.Tensor | None = None):
+    """VJP of SpGEMM (Table 1): dA = (dC B^T) (.) mask(A), dB = (A^T dC) (.) mask(B)."""
+    dt = _dt(A.values)
+    if need_dA and dA is None:
+        dA = torch.empty_like(A.values)
+    if need_dB and dB is None:
+        dB = torch.empty_like(B.values)
+    ws, wsb = _workspace("spgemm_bwd", dt, A, B)
+    _check(lib().csrk_spgemm_bwd(dt, A.pattern(), _ptr(A.values), B.pattern(), _ptr(B.values), C.pattern(),
+                                 _ptr(dC), _ptr(dA if need_dA else None), _ptr(dB if need_dB else None), ws, wsb,
+                                 _stream()), "spgemm_bwd")
+    return (dA if need_dA else None), (dB if need_dB else None)

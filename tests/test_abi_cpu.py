@@ -1,0 +1,72 @@
+"""CPU-only checks of the C-ABI boundary: libcsrk.so builds for sm_100a, loads, exports every
+function include/csrk.h declares, and rejects bad arguments on the host (no GPU needed)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2212_05159_b200 import build
+    build.build()
+    from paper_2212_05159_b200 import csrk
+    return csrk.lib()
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "csrk.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(csrk_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared_functions()
+    for op in ["spmv_fwd", "spmv_bwd", "spmm_fwd", "spmm_bwd", "spgemm_symbolic", "spgemm_numeric",
+               "spgemm_bwd", "csr_transpose"]:
+        assert f"csrk_{op}" in names
+
+
+def test_every_declared_symbol_is_exported(lib):
+    from paper_2212_05159_b200 import csrk
+    names = declared_functions()
+    assert set(names) == set(csrk.ABI_SYMBOLS)
+    for n in names:
+        assert hasattr(lib, n), n
+
+
+def test_sass_is_sm100a(lib):
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf",
+                          os.path.join(ROOT, "paper_2212_05159_b200", "libcsrk.so")],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_host_side_argument_checks(lib):
+    from paper_2212_05159_b200 import csrk
+    P = csrk.Pattern
+    assert lib.csrk_version().decode().startswith("csrk")
+    assert b"WORKSPACE" in lib.csrk_status_string(-4)
+    bad = P(-1, 3, 0, 8, 0)
+    assert lib.csrk_spmv_fwd(1, 0, bad, None, None, None, None, None, None, 0, None) == -1
+    assert lib.csrk_spmv_fwd(7, 0, P(2, 2, 0, 8, 0), None, None, None, None, None, None, 0, None) == -1
+    assert lib.csrk_spmv_fwd(1, 5, P(2, 2, 0, 8, 0), None, None, None, None, None, None, 0, None) == -1
+    huge = P(1 << 32, 4, 0, 8, 0)
+    assert lib.csrk_spmv_fwd(1, 0, huge, None, None, None, None, None, None, 0, None) == -5
+    A, B = P(3, 4, 0, 8, 0), P(5, 2, 0, 8, 0)
+    nnz = ctypes.c_int64(0)
+    assert lib.csrk_spgemm_symbolic(A, B, 8, None, ctypes.byref(nnz), None, 0, None) == -2
+    # transpose plan with the wrong shape
+    T = P(3, 3, 0, 8, 0)
+    assert lib.csrk_spmv_fwd(1, 1, P(3, 4, 0, 8, 0), None, ctypes.byref(T), 8, None, 8, None, 0, None) == -2
+    # workspace sizing is host-only
+    n = ctypes.c_size_t(0)
+    A = P(1000, 1000, 5000, 8, 8)
+    assert lib.csrk_workspace_size(4, 1, ctypes.byref(A), None, 0, 0, ctypes.byref(n)) == 0 and n.value > 0
+    assert lib.csrk_workspace_size(0, 1, ctypes.byref(A), None, 0, 0, ctypes.byref(n)) == 0 and n.value == 0
+    assert lib.csrk_workspace_size(5, 1, ctypes.byref(A), ctypes.byref(A), 0, 0, ctypes.byref(n)) == 0 and n.value > 0
+    assert lib.csrk_launch_count() == 0

@@ -1,0 +1,267 @@
+"""GPU parity: every hot-path op through the C-ABI (paper_2212_05159_b200.csrk -> libcsrk.so)
+against the CPU oracle, element by element, on seeded synthetic inputs.
+
+Bar (BASELINE.json north_star): patterns (indptr / indices / perm)
+bit-exact; values |gpu - oracle| <= rtol * S with S = sum |terms| (rtol 1e-12 fp64, 1e-5
+fp32); integer-valued inputs and the single-product masked gradient bit-exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from util import assert_S_close
+
+pytestmark = pytest.mark.gpu
+
+RTOL = {np.float64: 1e-12, np.float32: 1e-5}
+
+
+@pytest.fixture(scope="module")
+def ck():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2212_05159_b200 import build
+    build.build()
+    from paper_2212_05159_b200 import csrk
+    return csrk
+
+
+def skew(n, long_row, seed, dtype=np.float64, values="real"):
+    """Row 0 holds `long_row` entries and column 0 is full (a dense column): exercises
+    multi-chunk tiles, the huge-column transpose sort and the large-row SpGEMM bins."""
+    rng = np.random.default_rng(seed)
+    rows = []
+    for i in range(n):
+        if i == 0:
+            cols = np.sort(rng.choice(n, long_row, replace=False))
+            cols = np.union1d([0], cols)
+        else:
+            cols = np.union1d([0, i], rng.choice(n, 2))
+        rows.append(cols)
+    indptr = np.zeros(n + 1, np.int64)
+    np.cumsum([len(c) for c in rows], out=indptr[1:])
+    indices = np.concatenate(rows).astype(np.int32)
+    vr = np.random.default_rng(seed + 1)
+    vals = synth.real_values(vr, len(indices), dtype) if values == "real" else synth.int_values(vr, len(indices), dtype)
+    return synth.CSR(n, n, indptr, indices, vals)
+
+
+def empty_matrix(m, n, dtype=np.float64):
+    return synth.CSR(m, n, np.zeros(m + 1, np.int64), np.zeros(0, np.int32), np.zeros(0, dtype))
+
+
+CASES = {
+    "config1_poisson16": lambda dt, v: synth.poisson2d(16, dtype=dt),
+    "poisson2d_70": lambda dt, v: synth.poisson2d(70, dtype=dt),
+    "poisson3d_17": lambda dt, v: synth.poisson3d(17, dtype=dt),
+    "rand_rect_empty_rows": lambda dt, v: synth.random_csr(3001, 2003, 0.004, 11, dt, v, empty_rows=True),
+    "powerlaw_16k": lambda dt, v: synth.powerlaw(1 << 14, seed=41, dtype=dt, values=v),
+    "skew_mid": lambda dt, v: skew(3000, 700, 5, dt, v),
+    "tiny_3x3": lambda dt, v: synth.poisson1d(3, dtype=dt),
+    "one_row": lambda dt, v: synth.random_csr(1, 50, 0.5, 3, dt, v),
+    "nnz0": lambda dt, v: empty_matrix(40, 30, dt),
+}
+
+
+def make(case, dt, values="real"):
+    A = CASES[case](dt, values)
+    if values == "int" and case.startswith(("config1", "poisson", "tiny")):
+        A = A.with_values(synth.int_values(np.random.default_rng(9), A.nnz, dt))
+    return A
+
+
+def dev(ck, A):
+    return ck.CSR.from_host(A)
+
+
+def t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def close(got, ref, S, dt, what, exact=False):
+    got = got.cpu().numpy() if isinstance(got, torch.Tensor) else got
+    if exact:
+        np.testing.assert_array_equal(got, ref, err_msg=what)
+    else:
+        assert_S_close(got, ref, S, RTOL[dt], what)
+
+
+DTS = [np.float64, np.float32]
+
+
+# ---------------------------------------------------------------- SpMV
+@pytest.mark.parametrize("case", list(CASES))
+@pytest.mark.parametrize("dt", DTS)
+@pytest.mark.parametrize("values", ["real", "int"])
+def test_spmv_fwd_bwd(ck, orc, case, dt, values):
+    A = make(case, dt, values)
+    m, n = A.nrows, A.ncols
+    x = synth.dense(n, 3, dt, values)
+    xt = synth.dense(m, 4, dt, values)
+    dy = synth.dense(m, 5, dt, values)
+    dyt = synth.dense(n, 6, dt, values)
+    exact = values == "int"
+    Ad = dev(ck, A)
+    plan = ck.csr_transpose(Ad)
+    # forward, op N and op T (with and without the transpose plan)
+    r = orc.spmv_fwd(A, x)
+    close(ck.spmv_fwd(Ad, t(x)), r.value, r.S, dt, "y=Ax", exact)
+    r = orc.spmv_fwd(A, xt, op=1)
+    close(ck.spmv_fwd(Ad, t(xt), op=ck.OP_T), r.value, r.S, dt, "y=A^T x atomic", exact)
+    close(ck.spmv_fwd(Ad, t(xt), op=ck.OP_T, plan=plan), r.value, r.S, dt, "y=A^T x plan", exact)
+    # backward op N: dA bit-exact (one product), dx = A^T dy
+    dA_ref, dx_ref = orc.spmv_bwd(A, x, dy)
+    for p in (None, plan):
+        dA, dx = ck.spmv_bwd(Ad, t(x), t(dy), plan=p)
+        np.testing.assert_array_equal(dA.cpu().numpy(), dA_ref, err_msg=f"dA plan={p is not None}")
+        close(dx, dx_ref.value, dx_ref.S, dt, f"dx plan={p is not None}", exact)
+    dA, _ = ck.spmv_bwd(Ad, t(x), t(dy), need_dx=False)
+    np.testing.assert_array_equal(dA.cpu().numpy(), dA_ref)
+    _, dx = ck.spmv_bwd(Ad, t(x), t(dy), plan=plan, need_dA=False)
+    close(dx, dx_ref.value, dx_ref.S, dt, "dx only", exact)
+    # backward op T
+    dA_ref, dx_ref = orc.spmv_bwd(A, xt, dyt, op=1)
+    dA, dx = ck.spmv_bwd(Ad, t(xt), t(dyt), op=ck.OP_T)
+    np.testing.assert_array_equal(dA.cpu().numpy(), dA_ref)
+    close(dx, dx_ref.value, dx_ref.S, dt, "dx op T", exact)
+    dA, _ = ck.spmv_bwd(Ad, t(xt), t(dyt), op=ck.OP_T, need_dx=False)
+    np.testing.assert_array_equal(dA.cpu().numpy(), dA_ref)
+
+
+def test_spmv_deterministic(ck):
+    A = synth.powerlaw(1 << 14, seed=3, dtype=np.float64)
+    Ad = dev(ck, A)
+    x = t(synth.dense(A.ncols, 1))
+    dy = t(synth.dense(A.nrows, 2))
+    plan = ck.csr_transpose(Ad)
+    y0 = ck.spmv_fwd(Ad, x)
+    dA0, dx0 = ck.spmv_bwd(Ad, x, dy, plan=plan)
+    for _ in range(3):
+        assert torch.equal(ck.spmv_fwd(Ad, x), y0)
+        dA, dx = ck.spmv_bwd(Ad, x, dy, plan=plan)
+        assert torch.equal(dA, dA0) and torch.equal(dx, dx0)
+
+
+# ---------------------------------------------------------------- transpose
+@pytest.mark.parametrize("case", list(CASES) + ["skew_huge"])
+def test_csr_transpose(ck, orc, case):
+    A = skew(9000, 8500, 8) if case == "skew_huge" else make(case, np.float64)
+    ATp, ATi, ATv, perm = orc.csr_transpose(A)
+    plan = ck.csr_transpose(dev(ck, A))
+    np.testing.assert_array_equal(plan.AT.indptr.cpu().numpy(), ATp)
+    np.testing.assert_array_equal(plan.AT.indices.cpu().numpy(), ATi)
+    np.testing.assert_array_equal(plan.perm.cpu().numpy(), perm)
+    np.testing.assert_array_equal(plan.AT.values.cpu().numpy(), ATv)
+    # involution
+    back = ck.csr_transpose(plan.AT)
+    np.testing.assert_array_equal(back.AT.indptr.cpu().numpy(), A.indptr)
+    np.testing.assert_array_equal(back.AT.indices.cpu().numpy(), A.indices)
+    np.testing.assert_array_equal(back.AT.values.cpu().numpy(), A.values)
+
+
+# ---------------------------------------------------------------- SpMM
+@pytest.mark.parametrize("case", ["config1_poisson16", "poisson2d_70", "rand_rect_empty_rows", "skew_mid",
+                                  "tiny_3x3", "nnz0", "powerlaw_16k"])
+@pytest.mark.parametrize("dt,k", [(np.float64, 32), (np.float32, 32), (np.float64, 5), (np.float32, 7),
+                                  (np.float64, 200), (np.float64, 300), (np.float32, 16)])
+def test_spmm_fwd_bwd(ck, orc, case, dt, k):
+    values = "int" if k in (5, 16) else "real"
+    A = make(case, dt, values)
+    if case == "powerlaw_16k" and k > 32:
+        pytest.skip("large k on the power-law case is covered by smaller cases")
+    m, n = A.nrows, A.ncols
+    X = synth.dense((n, k), 3, dt, values)
+    dY = synth.dense((m, k), 4, dt, values)
+    exact = values == "int"
+    Ad = dev(ck, A)
+    r = orc.spmm_fwd(A, X)
+    close(ck.spmm_fwd(Ad, t(X)), r.value, r.S, dt, "Y", exact)
+    dA_ref, dX_ref = orc.spmm_bwd(A, X, dY)
+    plan = ck.csr_transpose(Ad)
+    for p in (plan, None):
+        dA, dX = ck.spmm_bwd(Ad, t(X), t(dY), plan=p)
+        close(dA, dA_ref.value, dA_ref.S, dt, f"dA plan={p is not None}", exact)
+        close(dX, dX_ref.value, dX_ref.S, dt, f"dX plan={p is not None}", exact)
+    dA, _ = ck.spmm_bwd(Ad, t(X), t(dY), need_dX=False)
+    close(dA, dA_ref.value, dA_ref.S, dt, "dA only (SDDMM)", exact)
+    _, dX = ck.spmm_bwd(Ad, t(X), t(dY), plan=plan, need_dA=False)
+    close(dX, dX_ref.value, dX_ref.S, dt, "dX only", exact)
+
+
+def test_spmm_strided_operands(ck, orc):
+    """Leading dimensions > k (row-major with padding, reading A10)."""
+    A = synth.poisson2d(20)
+    k, ld = 6, 9
+    Xf = synth.dense((A.ncols, ld), 1)
+    dYf = synth.dense((A.nrows, ld), 2)
+    Ad = dev(ck, A)
+    Xt, dYt = t(Xf)[:, :k], t(dYf)[:, :k]
+    r = orc.spmm_fwd(A, Xf[:, :k])
+    close(ck.spmm_fwd(Ad, Xt), r.value, r.S, np.float64, "Y strided")
+    dA_ref, dX_ref = orc.spmm_bwd(A, Xf[:, :k], dYf[:, :k])
+    dA, dX = ck.spmm_bwd(Ad, Xt, dYt, plan=ck.csr_transpose(Ad))
+    close(dA, dA_ref.value, dA_ref.S, np.float64, "dA strided")
+    close(dX, dX_ref.value, dX_ref.S, np.float64, "dX strided")
+
+
+# ---------------------------------------------------------------- SpGEMM
+GEMM_CASES = ["config1_poisson16", "poisson2d_70", "poisson3d_17", "rand_rect_empty_rows", "powerlaw_16k",
+              "skew_mid", "tiny_3x3", "one_row", "nnz0", "skew_big"]
+
+
+def gemm_operands(case, dt, values):
+    if case == "skew_big":
+        A = skew(9000, 8500, 21, dt, values)
+        return A, A
+    A = make(case, dt, values)
+    if case in ("rand_rect_empty_rows", "one_row"):
+        B = synth.random_csr(A.ncols, 777, 0.01 if case != "one_row" else 0.2, 12, dt, values)
+        return A, B
+    if case == "nnz0":
+        return A, synth.random_csr(A.ncols, 20, 0.3, 2, dt, values)
+    return A, A
+
+
+@pytest.mark.parametrize("case", GEMM_CASES)
+@pytest.mark.parametrize("dt", DTS)
+@pytest.mark.parametrize("values", ["real", "int"])
+def test_spgemm(ck, orc, case, dt, values):
+    if case == "skew_big" and (dt == np.float32 or values == "int"):
+        pytest.skip("one dtype suffices for the big skewed case")
+    A, B = gemm_operands(case, dt, values)
+    exact = values == "int"
+    Ad, Bd = dev(ck, A), dev(ck, B)
+    Cp, Ci = orc.spgemm_symbolic(A, B)
+    C = ck.spgemm_symbolic(Ad, Bd)
+    np.testing.assert_array_equal(C.indptr.cpu().numpy(), Cp)
+    np.testing.assert_array_equal(C.indices.cpu().numpy(), Ci)
+    r = orc.spgemm_numeric(A, B, Cp, Ci)
+    close(ck.spgemm_numeric(Ad, Bd, C), r.value, r.S, dt, "C values", exact)
+    dC = synth.dense(len(Ci), 7, dt, values)
+    dA_ref, dB_ref = orc.spgemm_bwd(A, B, Cp, Ci, dC)
+    dA, dB = ck.spgemm_bwd(Ad, Bd, C, t(dC))
+    close(dA, dA_ref.value, dA_ref.S, dt, "dA", exact)
+    close(dB, dB_ref.value, dB_ref.S, dt, "dB", exact)
+    dA2, _ = ck.spgemm_bwd(Ad, Bd, C, t(dC), need_dB=False)
+    close(dA2, dA_ref.value, dA_ref.S, dt, "dA only", exact)
+    _, dB2 = ck.spgemm_bwd(Ad, Bd, C, t(dC), need_dA=False)
+    close(dB2, dB_ref.value, dB_ref.S, dt, "dB only", exact)
+
+
+def test_spgemm_fig3(ck, orc):
+    """PAPER Fig. 3: the printed 9x3 product pattern, on the GPU."""
+    from util import csr_from_pattern, load_fig3, pattern_dense
+    mats, _ = load_fig3()
+    A, B = csr_from_pattern(mats["A"]), csr_from_pattern(mats["B"])
+    C = ck.spgemm_symbolic(dev(ck, A), dev(ck, B))
+    got = synth.CSR(9, 3, C.indptr.cpu().numpy(), C.indices.cpu().numpy(), np.ones(C.nnz))
+    np.testing.assert_array_equal(pattern_dense(got), mats["C"])
+
+
+def test_launch_counter_advances(ck):
+    before = ck.launch_count()
+    A = dev(ck, synth.poisson2d(8))
+    ck.spmv_fwd(A, torch.ones(64, dtype=torch.float64, device="cuda"))
+    torch.cuda.synchronize()
+    assert ck.launch_count() > before
