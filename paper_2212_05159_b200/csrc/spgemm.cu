@@ -1,19 +1,24 @@
 // spgemm.cu -- SpGEMM C = A B: symbolic, numeric and backward
 // (PAPER 3.1.2; Table 1; Fig. 3).
 //
-// Rows of A are binned by l_i = row length and w_i = sum_{k in row i} len_B(k) (the
-// product count, "estimated work"):
-//   S  (l_i <= 8, w_i <= 512): one THREAD per row runs an l_i-way merge of the sorted
-//      B rows.  The merge emits C's columns in ascending order, so symbolic needs no
-//      sort, numeric sums each C_ij over k ascending (deterministic, the oracle's order)
-//      and the backward pass meets dC_ij in C's storage order without any search.
-//   M  (w_i <= 8192): one CTA per row; products gathered to shared memory.  Symbolic:
-//      bitonic sort + unique.  Numeric/backward: binary search of each product's column
-//      in the C row (shared memory) -- numeric accumulates with shared-memory atomics.
-//   L  (w_i > 8192): one CTA per row; symbolic uses shared-memory bitmap windows over the
-//      column range (sorted output for free); numeric/backward search the C row in global
-//      memory and accumulate with global atomics.
-// Rows with w_i = 0 ("E") produce empty C rows and zero dA.
+// Every phase (COUNT, FILL of the symbolic pattern; NUM; BWD) runs two kernels:
+//
+//   k_gemm_S   one THREAD per row of A.  A row with l_i <= 8 entries whose product count
+//              w_i = sum_k len_B(k) is <= 512 ("short") runs an l_i-way merge of its sorted B
+//              rows.  The merge emits C's columns in ascending order, so the symbolic phase
+//              needs no sort, the numeric phase sums each C_ij over k ascending (the
+//              oracle's order, deterministic) and the backward pass meets dC_ij in C's
+//              storage order with no search.  The merge is specialised on the warp's
+//              largest l_i, and when all 32 rows of a warp are short their C (and dA)
+//              ranges are contiguous, so outputs are staged in shared memory and written
+//              (and dC read) coalesced.  Every other row is queued (warp-aggregated atomic).
+//   k_gemm_big one CTA per queued row.  w_i <= 8192: products gathered to shared memory;
+//              symbolic = bitonic sort + unique; numeric/backward binary-search each
+//              product's column in the C row (shared memory) -- numeric accumulates with
+//              shared-memory atomics.  w_i > 8192: symbolic uses shared-memory bitmap
+//              windows over the column range (sorted output for free); numeric/backward
+//              search the C row in global memory and accumulate with global atomics.
+//
 // The backward pass computes dA_ik = sum_j dC_ij B_kj per A entry (deterministic) and
 // scatters dB_kj += A_ik dC_ij with global atomic adds (reading A9).
 #include "ops.cuh"
@@ -23,92 +28,64 @@ namespace csrk {
 constexpr int kSMaxL = 8;
 constexpr int64_t kSMaxW = 512;
 constexpr int kMMaxW = 8192;
-constexpr int kGemmTPB = 256;
+constexpr int kSTPB = 128;           // k_gemm_S: 4 warps
+constexpr int kSWarps = kSTPB / 32;
+constexpr int kSBuf = 832;           // staged C entries per warp (3D 7-point A^2: 32 x 25 = 800)
+constexpr int kSBufA = 32 * kSMaxL;  // staged dA entries per warp
+constexpr int kGemmTPB = 256;        // k_gemm_big
 constexpr int kBitmapWords = 24576;  // 96 KB -> windows of 786,432 columns
 
-enum : uint8_t { BIN_E = 0, BIN_S = 1, BIN_M = 2, BIN_L = 3 };
 enum { PH_COUNT = 0, PH_FILL = 1, PH_NUM = 2, PH_BWD = 3 };
 
-struct Bins {
-    uint8_t *bin;
-    int32_t *listM, *listL;
-    int *cnt;  // [2]
+struct BigList {
+    int32_t *rows;
+    int *count;
 };
 
-// ---------------------------------------------------------------- binning (8 lanes per row)
-__global__ __launch_bounds__(256) void k_gemm_bin(int64_t m, const int64_t *__restrict__ Ap,
-                                                  const int32_t *__restrict__ Ai, const int64_t *__restrict__ Bp,
-                                                  Bins b)
+// ---------------------------------------------------------------- short rows: thread-per-row merge
+template <typename T, int PH, int L>
+__device__ __forceinline__ int64_t s_merge(int64_t as, int l, const int32_t *__restrict__ Ai,
+                                           const T *__restrict__ Av, const int64_t *__restrict__ Bp,
+                                           const int32_t *__restrict__ Bi, const T *__restrict__ Bv,
+                                           int32_t *outI, T *outV, const T *dCrow, T *dArow, T *__restrict__ dB)
 {
-    constexpr int G = 8;
-    const int lane = threadIdx.x & (G - 1);
-    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
-    if (i >= m) return;
-    const unsigned gmask = 0xffu << ((threadIdx.x & 31) & ~(G - 1));
-    const int64_t s = Ap[i], e = Ap[i + 1];
-    int64_t w = 0;
-    for (int64_t p = s + lane; p < e; p += G) {
-        const int32_t k = Ai[p];
-        w += Bp[k + 1] - Bp[k];
-    }
-    for (int o = G >> 1; o > 0; o >>= 1) w += __shfl_xor_sync(gmask, w, o, G);
-    if (lane == 0) {
-        const int64_t l = e - s;
-        uint8_t bin = w == 0 ? BIN_E : ((l <= kSMaxL && w <= kSMaxW) ? BIN_S : (w <= kMMaxW ? BIN_M : BIN_L));
-        b.bin[i] = bin;
-        if (bin == BIN_M) b.listM[atomicAdd(&b.cnt[0], 1)] = (int32_t)i;
-        if (bin == BIN_L) b.listL[atomicAdd(&b.cnt[1], 1)] = (int32_t)i;
-    }
-}
-
-// ---------------------------------------------------------------- S rows: thread-per-row merge
-template <typename T, int PH>
-__global__ __launch_bounds__(kGemmTPB) void k_gemm_S(int64_t m, const uint8_t *__restrict__ bin,
-                                                     const int64_t *__restrict__ Ap, const int32_t *__restrict__ Ai,
-                                                     const T *__restrict__ Av, const int64_t *__restrict__ Bp,
-                                                     const int32_t *__restrict__ Bi, const T *__restrict__ Bv,
-                                                     int64_t *__restrict__ Cp, int32_t *__restrict__ Ci,
-                                                     T *__restrict__ Cv, const T *__restrict__ dC, T *__restrict__ dA,
-                                                     T *__restrict__ dB)
-{
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= m) return;
-    const uint8_t bn = bin[i];
-    const int64_t as = Ap[i];
-    if (bn == BIN_E) {
-        if (PH == PH_COUNT) Cp[i + 1] = 0;
-        if (PH == PH_BWD && dA)
-            for (int64_t p = as; p < Ap[i + 1]; ++p) dA[p] = (T)0;
-        return;
-    }
-    if (bn != BIN_S) return;
-    const int l = (int)(Ap[i + 1] - as);
-    int64_t cur[kSMaxL], end[kSMaxL];
-    int32_t head[kSMaxL];
-    double av[kSMaxL], dacc[kSMaxL];
+    int64_t cur[L];   // position in B of list t's head
+    int rem[L];
+    int32_t head[L];
+    double av[L], dacc[L];
 #pragma unroll
-    for (int t = 0; t < kSMaxL; ++t) {
+    for (int t = 0; t < L; ++t) {
+        rem[t] = 0;
         head[t] = INT32_MAX;
-        cur[t] = end[t] = 0;
+        cur[t] = 0;
         av[t] = dacc[t] = 0.0;
         if (t < l) {
             const int32_t k = Ai[as + t];
             cur[t] = Bp[k];
-            end[t] = Bp[k + 1];
-            if (cur[t] < end[t]) head[t] = Bi[cur[t]];
+            rem[t] = (int)(Bp[k + 1] - cur[t]);
             if (PH == PH_NUM || PH == PH_BWD) av[t] = (double)Av[as + t];
+            if (rem[t] > 0) {
+                // pull the list's index (and value) lines into L1: the merge then walks them
+                // with L1 latency instead of a dependent L2 round trip per step
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(Bi + cur[t] + rem[t] - 1));
+                if (PH == PH_NUM || PH == PH_BWD) {
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(Bv + cur[t]));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(Bv + cur[t] + rem[t] - 1));
+                }
+                head[t] = Bi[cur[t]];
+            }
         }
     }
-    int64_t c = PH == PH_COUNT ? 0 : Cp[i];
+    int64_t c = 0;
     while (true) {
-        int32_t v = INT32_MAX;
+        int32_t v = head[0];
 #pragma unroll
-        for (int t = 0; t < kSMaxL; ++t) v = head[t] < v ? head[t] : v;
+        for (int t = 1; t < L; ++t) v = head[t] < v ? head[t] : v;
         if (v == INT32_MAX) break;
         double acc = 0.0;
-        const double g = PH == PH_BWD ? (double)dC[c] : 0.0;
+        const double g = PH == PH_BWD ? (double)dCrow[c] : 0.0;
 #pragma unroll
-        for (int t = 0; t < kSMaxL; ++t) {
+        for (int t = 0; t < L; ++t) {
             if (head[t] == v) {
                 if (PH == PH_NUM) acc = fma(av[t], (double)Bv[cur[t]], acc);
                 if (PH == PH_BWD) {
@@ -116,18 +93,109 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_S(int64_t m, const uint8_t *_
                     if (dB) red_add(&dB[cur[t]], (T)(av[t] * g));
                 }
                 ++cur[t];
-                head[t] = cur[t] < end[t] ? Bi[cur[t]] : INT32_MAX;
+                head[t] = --rem[t] > 0 ? Bi[cur[t]] : INT32_MAX;
             }
         }
-        if (PH == PH_FILL) Ci[c] = v;
-        if (PH == PH_NUM) Cv[c] = (T)acc;
+        if (PH == PH_FILL) outI[c] = v;
+        if (PH == PH_NUM) outV[c] = (T)acc;
         ++c;
     }
-    if (PH == PH_COUNT) Cp[i + 1] = c;
-    if (PH == PH_BWD && dA) {
+    if (PH == PH_BWD && dArow) {
 #pragma unroll
-        for (int t = 0; t < kSMaxL; ++t)
-            if (t < l) dA[as + t] = (T)dacc[t];
+        for (int t = 0; t < L; ++t)
+            if (t < l) dArow[t] = (T)dacc[t];
+    }
+    return c;
+}
+
+template <typename T, int PH>
+__global__ __launch_bounds__(kSTPB) void k_gemm_S(int64_t m, const int64_t *__restrict__ Ap,
+                                                  const int32_t *__restrict__ Ai, const T *__restrict__ Av,
+                                                  const int64_t *__restrict__ Bp, const int32_t *__restrict__ Bi,
+                                                  const T *__restrict__ Bv, int64_t *__restrict__ Cp,
+                                                  int32_t *__restrict__ Ci, T *__restrict__ Cv,
+                                                  const T *__restrict__ dC, T *__restrict__ dA, T *__restrict__ dB,
+                                                  BigList big)
+{
+    constexpr int BUFB = (PH == PH_FILL) ? (int)sizeof(int32_t) * kSBuf : (int)sizeof(T) * kSBuf;
+    __shared__ __align__(16) unsigned char s_buf[kSWarps][PH == PH_COUNT ? 16 : BUFB];
+    __shared__ T s_dA[kSWarps][PH == PH_BWD ? kSBufA : 1];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t i0 = (int64_t)blockIdx.x * kSTPB + warp * 32;   // first row of this warp
+    const int64_t i = i0 + lane;
+    const bool valid = i < m;
+    int64_t as = 0;
+    int l = 0;
+    int64_t w = 0;
+    if (valid) {
+        as = Ap[i];
+        const int64_t ll = Ap[i + 1] - as;
+        l = ll > kSMaxL ? kSMaxL + 1 : (int)ll;
+        if (l <= kSMaxL)
+            for (int t = 0; t < l; ++t) {
+                const int32_t k = Ai[as + t];
+                w += Bp[k + 1] - Bp[k];
+            }
+    }
+    const bool isS = valid && l <= kSMaxL && w <= kSMaxW;
+    // queue the other rows (warp-aggregated)
+    const unsigned bigmask = __ballot_sync(0xffffffffu, valid && !isS);
+    if (bigmask) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(big.count, __popc(bigmask));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (valid && !isS) big.rows[base + __popc(bigmask & ((1u << lane) - 1))] = (int32_t)i;
+    }
+    const int Lw = (int)__reduce_max_sync(0xffffffffu, isS ? (unsigned)l : 0u);
+    // staging: all rows of the warp short, C range of the warp small enough
+    const int64_t iend = i0 + 32 < m ? i0 + 32 : m;
+    bool stage = false;
+    int64_t c_lo = 0, a_lo = 0;
+    if (PH != PH_COUNT) {
+        stage = __all_sync(0xffffffffu, !valid || isS) && i0 < m;
+        if (stage) {
+            c_lo = Cp[i0];
+            stage = Cp[iend] - c_lo <= kSBuf;
+            a_lo = Ap[i0];
+        }
+    }
+    const int64_t c_hi = stage ? Cp[iend] : 0;
+    T *sv = reinterpret_cast<T *>(s_buf[warp]);
+    int32_t *si = reinterpret_cast<int32_t *>(s_buf[warp]);
+    if (PH == PH_BWD && stage) {
+        for (int64_t e = c_lo + lane; e < c_hi; e += 32) sv[e - c_lo] = dC[e];
+        __syncwarp();
+    }
+    if (isS) {
+        const int64_t cs = PH == PH_COUNT ? 0 : Cp[i];
+        int32_t *outI = PH == PH_FILL ? (stage ? si + (cs - c_lo) : Ci + cs) : nullptr;
+        T *outV = PH == PH_NUM ? (stage ? sv + (cs - c_lo) : Cv + cs) : nullptr;
+        const T *dCrow = PH == PH_BWD ? (stage ? sv + (cs - c_lo) : dC + cs) : nullptr;
+        T *dArow = (PH == PH_BWD && dA) ? (stage ? &s_dA[warp][as - a_lo] : dA + as) : nullptr;
+        int64_t cnt = 0;
+        switch (Lw) {
+        case 1: cnt = s_merge<T, PH, 1>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
+        case 2: cnt = s_merge<T, PH, 2>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
+        case 3: cnt = s_merge<T, PH, 3>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
+        case 4: cnt = s_merge<T, PH, 4>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
+        case 5: cnt = s_merge<T, PH, 5>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
+        case 6: cnt = s_merge<T, PH, 6>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
+        case 7: cnt = s_merge<T, PH, 7>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
+        case 8: cnt = s_merge<T, PH, 8>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
+        default: break;  // l == 0: empty row
+        }
+        if (PH == PH_COUNT) Cp[i + 1] = cnt;
+    }
+    if (stage) {
+        __syncwarp();
+        if (PH == PH_FILL)
+            for (int64_t e = c_lo + lane; e < c_hi; e += 32) Ci[e] = si[e - c_lo];
+        if (PH == PH_NUM)
+            for (int64_t e = c_lo + lane; e < c_hi; e += 32) Cv[e] = sv[e - c_lo];
+        if (PH == PH_BWD && dA) {
+            const int64_t a_hi = Ap[iend];
+            for (int64_t e = a_lo + lane; e < a_hi; e += 32) dA[e] = s_dA[warp][e - a_lo];
+        }
     }
 }
 
@@ -201,73 +269,74 @@ __device__ __forceinline__ int64_t lbound(const int32_t *c, int64_t n, int32_t v
     return lo;
 }
 
-// ---------------------------------------------------------------- M rows: symbolic
-template <int PH>
-__global__ __launch_bounds__(kGemmTPB) void k_gemm_M_sym(const int32_t *__restrict__ list, const int *__restrict__ cnt,
-                                                         const int64_t *__restrict__ Ap, const int32_t *__restrict__ Ai,
-                                                         const int64_t *__restrict__ Bp, const int32_t *__restrict__ Bi,
-                                                         int64_t *__restrict__ Cp, int32_t *__restrict__ Ci)
+// w_i = sum_k len_B(k) over row i (block reduction)
+__device__ __forceinline__ int64_t row_work(int64_t as, int64_t ae, const int32_t *__restrict__ Ai,
+                                            const int64_t *__restrict__ Bp, int64_t *s_red)
 {
-    __shared__ int32_t s_key[kMMaxW];
-    __shared__ int s_cnt;
-    __shared__ int64_t s_red[kGemmTPB / 32];
-    const int nrows = *cnt;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int it = blockIdx.x; it < nrows; it += gridDim.x) {
-        const int64_t i = list[it];
-        const int64_t as = Ap[i], ae = Ap[i + 1];
-        if (threadIdx.x == 0) s_cnt = 0;
-        __syncthreads();
-        for (int64_t a = as + warp; a < ae; a += kGemmTPB / 32) {
-            const int32_t k = Ai[a];
-            const int64_t bs = Bp[k];
-            const int bl = (int)(Bp[k + 1] - bs);
-            int base = 0;
-            if (lane == 0 && bl > 0) base = atomicAdd(&s_cnt, bl);
-            base = __shfl_sync(0xffffffffu, base, 0);
-            for (int j = lane; j < bl; j += 32) s_key[base + j] = Bi[bs + j];
-        }
-        __syncthreads();
-        const int w = s_cnt;
-        const int P = pow2ceil_i(w);
-        for (int e = w + threadIdx.x; e < P; e += kGemmTPB) s_key[e] = INT32_MAX;
-        __syncthreads();
-        bitonic_keys(s_key, P);
-        // thread-contiguous chunks of the sorted keys
-        const int per = (P + kGemmTPB - 1) / kGemmTPB;
-        const int e0 = threadIdx.x * per;
-        int64_t mine = 0;
-        for (int e = e0; e < e0 + per && e < w; ++e) mine += (e == 0 || s_key[e] != s_key[e - 1]);
-        if (PH == PH_COUNT) {
-            const int64_t tot = block_sum_i64(mine, s_red);
-            if (threadIdx.x == 0) Cp[i + 1] = tot;
-        } else {
-            int64_t tot;
-            int64_t r = Cp[i] + block_excl_scan_i64(mine, s_red, tot);
-            for (int e = e0; e < e0 + per && e < w; ++e)
-                if (e == 0 || s_key[e] != s_key[e - 1]) Ci[r++] = s_key[e];
-        }
-        __syncthreads();
+    int64_t w = 0;
+    for (int64_t a = as + threadIdx.x; a < ae; a += kGemmTPB) {
+        const int32_t k = Ai[a];
+        w += Bp[k + 1] - Bp[k];
     }
+    return block_sum_i64(w, s_red);
 }
 
-// ---------------------------------------------------------------- L rows: symbolic (bitmap windows)
+// ---------------------------------------------------------------- big rows: symbolic
 template <int PH>
-__global__ __launch_bounds__(kGemmTPB) void k_gemm_L_sym(const int32_t *__restrict__ list, const int *__restrict__ cnt,
-                                                         int64_t ncolsB, const int64_t *__restrict__ Ap,
-                                                         const int32_t *__restrict__ Ai, const int64_t *__restrict__ Bp,
-                                                         const int32_t *__restrict__ Bi, int64_t *__restrict__ Cp,
-                                                         int32_t *__restrict__ Ci)
+__global__ __launch_bounds__(kGemmTPB) void k_gemm_big_sym(BigList big, int64_t ncolsB,
+                                                           const int64_t *__restrict__ Ap,
+                                                           const int32_t *__restrict__ Ai,
+                                                           const int64_t *__restrict__ Bp,
+                                                           const int32_t *__restrict__ Bi, int64_t *__restrict__ Cp,
+                                                           int32_t *__restrict__ Ci)
 {
     extern __shared__ __align__(16) unsigned char smem[];
-    uint32_t *bm = reinterpret_cast<uint32_t *>(smem);
+    int32_t *s_key = reinterpret_cast<int32_t *>(smem);   // kMMaxW keys (M path)
+    uint32_t *bm = reinterpret_cast<uint32_t *>(smem);    // kBitmapWords (L path)
+    __shared__ int s_cnt;
     __shared__ int64_t s_red[kGemmTPB / 32];
-    const int nrows = *cnt;
+    const int nrows = *(volatile int *)big.count;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t W = (int64_t)kBitmapWords * 32;
     for (int it = blockIdx.x; it < nrows; it += gridDim.x) {
-        const int64_t i = list[it];
+        const int64_t i = big.rows[it];
         const int64_t as = Ap[i], ae = Ap[i + 1];
+        const int64_t w = row_work(as, ae, Ai, Bp, s_red);
+        if (w <= kMMaxW) {
+            if (threadIdx.x == 0) s_cnt = 0;
+            __syncthreads();
+            for (int64_t a = as + warp; a < ae; a += kGemmTPB / 32) {
+                const int32_t k = Ai[a];
+                const int64_t bs = Bp[k];
+                const int bl = (int)(Bp[k + 1] - bs);
+                int base = 0;
+                if (lane == 0 && bl > 0) base = atomicAdd(&s_cnt, bl);
+                base = __shfl_sync(0xffffffffu, base, 0);
+                for (int j = lane; j < bl; j += 32) s_key[base + j] = Bi[bs + j];
+            }
+            __syncthreads();
+            const int wn = s_cnt;
+            const int P = pow2ceil_i(wn > 0 ? wn : 1);
+            for (int e = wn + threadIdx.x; e < P; e += kGemmTPB) s_key[e] = INT32_MAX;
+            __syncthreads();
+            bitonic_keys(s_key, P);
+            const int per = (P + kGemmTPB - 1) / kGemmTPB;
+            const int e0 = threadIdx.x * per;
+            int64_t mine = 0;
+            for (int e = e0; e < e0 + per && e < wn; ++e) mine += (e == 0 || s_key[e] != s_key[e - 1]);
+            if (PH == PH_COUNT) {
+                const int64_t tot = block_sum_i64(mine, s_red);
+                if (threadIdx.x == 0) Cp[i + 1] = tot;
+            } else {
+                int64_t tot;
+                int64_t r = Cp[i] + block_excl_scan_i64(mine, s_red, tot);
+                for (int e = e0; e < e0 + per && e < wn; ++e)
+                    if (e == 0 || s_key[e] != s_key[e - 1]) Ci[r++] = s_key[e];
+            }
+            __syncthreads();
+            continue;
+        }
+        // bitmap windows over [0, ncolsB)
+        const int64_t W = (int64_t)kBitmapWords * 32;
         int64_t done = 0;
         for (int64_t w0 = 0; w0 < ncolsB; w0 += W) {
             for (int e = threadIdx.x; e < kBitmapWords; e += kGemmTPB) bm[e] = 0u;
@@ -306,24 +375,25 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_L_sym(const int32_t *__restri
     }
 }
 
-// ---------------------------------------------------------------- M/L rows: numeric + backward
+// ---------------------------------------------------------------- big rows: numeric + backward
 // C row in shared memory when it fits (nnz(C_i) <= kMMaxW), else searched in global memory.
 template <typename T, int PH>
-__global__ __launch_bounds__(kGemmTPB) void k_gemm_ML_val(const int32_t *__restrict__ list, const int *__restrict__ cnt,
-                                                          const int64_t *__restrict__ Ap, const int32_t *__restrict__ Ai,
-                                                          const T *__restrict__ Av, const int64_t *__restrict__ Bp,
-                                                          const int32_t *__restrict__ Bi, const T *__restrict__ Bv,
-                                                          const int64_t *__restrict__ Cp, const int32_t *__restrict__ Ci,
-                                                          T *__restrict__ Cv, const T *__restrict__ dC,
-                                                          T *__restrict__ dA, T *__restrict__ dB)
+__global__ __launch_bounds__(kGemmTPB) void k_gemm_big_val(BigList big, const int64_t *__restrict__ Ap,
+                                                           const int32_t *__restrict__ Ai, const T *__restrict__ Av,
+                                                           const int64_t *__restrict__ Bp,
+                                                           const int32_t *__restrict__ Bi, const T *__restrict__ Bv,
+                                                           const int64_t *__restrict__ Cp,
+                                                           const int32_t *__restrict__ Ci, T *__restrict__ Cv,
+                                                           const T *__restrict__ dC, T *__restrict__ dA,
+                                                           T *__restrict__ dB)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     double *s_val = reinterpret_cast<double *>(smem);                             // acc (NUM) or dC (BWD)
     int32_t *s_col = reinterpret_cast<int32_t *>(smem + sizeof(double) * kMMaxW);
-    const int nrows = *cnt;
+    const int nrows = *(volatile int *)big.count;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int it = blockIdx.x; it < nrows; it += gridDim.x) {
-        const int64_t i = list[it];
+        const int64_t i = big.rows[it];
         const int64_t as = Ap[i], ae = Ap[i + 1];
         const int64_t cs = Cp[i], nc = Cp[i + 1] - cs;
         const bool in_smem = nc <= kMMaxW;
@@ -367,62 +437,50 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_ML_val(const int32_t *__restr
 }
 
 // ---------------------------------------------------------------- host side
-static int carve_bins(const csrk_pattern &A, Bins &b, Bump &ws)
-{
-    const int64_t m = A.nrows > 0 ? A.nrows : 1;
-    b.bin = ws.take<uint8_t>(m);
-    b.listM = ws.take<int32_t>(m);
-    b.listL = ws.take<int32_t>(m);
-    b.cnt = ws.take<int>(2);
-    return CSRK_OK;
-}
+static unsigned big_grid() { return (unsigned)(kNumSMs * 2); }
 
-static int run_bins(const csrk_pattern &A, const csrk_pattern &B, Bins &b, cudaStream_t s)
-{
-    CSRK_CUDA(cudaMemsetAsync(b.cnt, 0, sizeof(int) * 2, s));
-    CSRK_LAUNCH(k_gemm_bin, (unsigned)cdiv(A.nrows * 8, 256), 256, 0, s, A.nrows, A.indptr, A.indices, B.indptr, b);
-    return CSRK_OK;
-}
-
-static unsigned ml_grid() { return (unsigned)(kNumSMs * 4); }
+static size_t big_sym_smem() { return sizeof(uint32_t) * kBitmapWords; }
+static size_t big_val_smem() { return (sizeof(double) + sizeof(int32_t)) * kMMaxW; }
 
 static int set_smem_attrs()
 {
     static bool done = false;
     if (done) return CSRK_OK;
-    const int bm = (int)(sizeof(uint32_t) * kBitmapWords);
-    const int mv = (int)((sizeof(double) + sizeof(int32_t)) * kMMaxW);
-    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_L_sym<PH_COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bm));
-    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_L_sym<PH_FILL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bm));
-    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_ML_val<double, PH_NUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, mv));
-    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_ML_val<double, PH_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, mv));
-    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_ML_val<float, PH_NUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, mv));
-    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_ML_val<float, PH_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, mv));
+    const int bs = (int)big_sym_smem(), bv = (int)big_val_smem();
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_sym<PH_COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bs));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_sym<PH_FILL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bs));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_val<double, PH_NUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, bv));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_val<double, PH_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, bv));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_val<float, PH_NUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, bv));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_val<float, PH_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, bv));
     done = true;
     return CSRK_OK;
+}
+
+static void carve_big(const csrk_pattern &A, BigList &b, Bump &ws)
+{
+    b.rows = ws.take<int32_t>(A.nrows > 0 ? A.nrows : 1);
+    b.count = ws.take<int>(1);
 }
 
 int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, int32_t *Ci, int64_t *nnzC_host,
                     Bump &ws, cudaStream_t s)
 {
-    Bins b{};
-    carve_bins(A, b, ws);
+    BigList b{};
+    carve_big(A, b, ws);
     if (ws.sizing()) return scan_counts_i64(nullptr, A.nrows, ws, s);
     const int64_t m = A.nrows;
     CSRK_TRY(set_smem_attrs());
+    const unsigned gS = (unsigned)cdiv(m, kSTPB);
     if (!Ci) {
         CSRK_CUDA(cudaMemsetAsync(Cp, 0, sizeof(int64_t), s));
         if (m > 0) {
-            CSRK_TRY(run_bins(A, B, b, s));
-            CSRK_LAUNCH((k_gemm_S<double, PH_COUNT>), (unsigned)cdiv(m, kGemmTPB), kGemmTPB, 0, s, m,
-                        (const uint8_t *)b.bin, A.indptr, A.indices, (const double *)nullptr, B.indptr, B.indices,
-                        (const double *)nullptr, Cp, (int32_t *)nullptr, (double *)nullptr, (const double *)nullptr,
-                        (double *)nullptr, (double *)nullptr);
-            CSRK_LAUNCH(k_gemm_M_sym<PH_COUNT>, ml_grid(), kGemmTPB, 0, s, (const int32_t *)b.listM,
-                        (const int *)b.cnt, A.indptr, A.indices, B.indptr, B.indices, Cp, (int32_t *)nullptr);
-            CSRK_LAUNCH(k_gemm_L_sym<PH_COUNT>, (unsigned)kNumSMs, kGemmTPB, sizeof(uint32_t) * kBitmapWords, s,
-                        (const int32_t *)b.listL, (const int *)(b.cnt + 1), B.ncols, A.indptr, A.indices, B.indptr,
-                        B.indices, Cp, (int32_t *)nullptr);
+            CSRK_CUDA(cudaMemsetAsync(b.count, 0, sizeof(int), s));
+            CSRK_LAUNCH((k_gemm_S<double, PH_COUNT>), gS, kSTPB, 0, s, m, A.indptr, A.indices,
+                        (const double *)nullptr, B.indptr, B.indices, (const double *)nullptr, Cp, (int32_t *)nullptr,
+                        (double *)nullptr, (const double *)nullptr, (double *)nullptr, (double *)nullptr, b);
+            CSRK_LAUNCH(k_gemm_big_sym<PH_COUNT>, big_grid(), kGemmTPB, big_sym_smem(), s, b, B.ncols, A.indptr,
+                        A.indices, B.indptr, B.indices, Cp, (int32_t *)nullptr);
             CSRK_TRY(scan_counts_i64(Cp, m, ws, s));
         }
         CSRK_CUDA(cudaMemcpyAsync(nnzC_host, Cp + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -430,15 +488,12 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, i
         return CSRK_OK;
     }
     if (m == 0) return CSRK_OK;
-    CSRK_TRY(run_bins(A, B, b, s));
-    CSRK_LAUNCH((k_gemm_S<double, PH_FILL>), (unsigned)cdiv(m, kGemmTPB), kGemmTPB, 0, s, m, (const uint8_t *)b.bin,
-                A.indptr, A.indices, (const double *)nullptr, B.indptr, B.indices, (const double *)nullptr, Cp, Ci,
-                (double *)nullptr, (const double *)nullptr, (double *)nullptr, (double *)nullptr);
-    CSRK_LAUNCH(k_gemm_M_sym<PH_FILL>, ml_grid(), kGemmTPB, 0, s, (const int32_t *)b.listM, (const int *)b.cnt,
-                A.indptr, A.indices, B.indptr, B.indices, Cp, Ci);
-    CSRK_LAUNCH(k_gemm_L_sym<PH_FILL>, (unsigned)kNumSMs, kGemmTPB, sizeof(uint32_t) * kBitmapWords, s,
-                (const int32_t *)b.listL, (const int *)(b.cnt + 1), B.ncols, A.indptr, A.indices, B.indptr, B.indices,
-                Cp, Ci);
+    CSRK_CUDA(cudaMemsetAsync(b.count, 0, sizeof(int), s));
+    CSRK_LAUNCH((k_gemm_S<double, PH_FILL>), gS, kSTPB, 0, s, m, A.indptr, A.indices, (const double *)nullptr,
+                B.indptr, B.indices, (const double *)nullptr, Cp, Ci, (double *)nullptr, (const double *)nullptr,
+                (double *)nullptr, (double *)nullptr, b);
+    CSRK_LAUNCH(k_gemm_big_sym<PH_FILL>, big_grid(), kGemmTPB, big_sym_smem(), s, b, B.ncols, A.indptr, A.indices,
+                B.indptr, B.indices, Cp, Ci);
     return CSRK_OK;
 }
 
@@ -446,35 +501,26 @@ template <typename T>
 static int spgemm_values_t(int PH, const csrk_pattern &A, const T *Av, const csrk_pattern &B, const T *Bv,
                            const csrk_pattern &C, T *Cv, const T *dC, T *dA, T *dB, Bump &ws, cudaStream_t s)
 {
-    Bins b{};
-    carve_bins(A, b, ws);
+    BigList b{};
+    carve_big(A, b, ws);
     if (ws.sizing()) return CSRK_OK;
     CSRK_TRY(set_smem_attrs());
     if (PH == PH_BWD && dB) CSRK_CUDA(cudaMemsetAsync(dB, 0, sizeof(T) * (size_t)B.nnz, s));
     const int64_t m = A.nrows;
     if (m == 0) return CSRK_OK;
-    CSRK_TRY(run_bins(A, B, b, s));
-    const size_t mv = (sizeof(double) + sizeof(int32_t)) * kMMaxW;
+    CSRK_CUDA(cudaMemsetAsync(b.count, 0, sizeof(int), s));
+    const unsigned gS = (unsigned)cdiv(m, kSTPB);
+    int64_t *Cp = const_cast<int64_t *>(C.indptr);
     if (PH == PH_NUM) {
-        CSRK_LAUNCH((k_gemm_S<T, PH_NUM>), (unsigned)cdiv(m, kGemmTPB), kGemmTPB, 0, s, m, (const uint8_t *)b.bin,
-                    A.indptr, A.indices, Av, B.indptr, B.indices, Bv, (int64_t *)C.indptr, (int32_t *)nullptr, Cv,
-                    (const T *)nullptr, (T *)nullptr, (T *)nullptr);
-        CSRK_LAUNCH((k_gemm_ML_val<T, PH_NUM>), ml_grid(), kGemmTPB, mv, s, (const int32_t *)b.listM,
-                    (const int *)b.cnt, A.indptr, A.indices, Av, B.indptr, B.indices, Bv, C.indptr, C.indices, Cv,
-                    (const T *)nullptr, (T *)nullptr, (T *)nullptr);
-        CSRK_LAUNCH((k_gemm_ML_val<T, PH_NUM>), ml_grid(), kGemmTPB, mv, s, (const int32_t *)b.listL,
-                    (const int *)(b.cnt + 1), A.indptr, A.indices, Av, B.indptr, B.indices, Bv, C.indptr, C.indices,
-                    Cv, (const T *)nullptr, (T *)nullptr, (T *)nullptr);
+        CSRK_LAUNCH((k_gemm_S<T, PH_NUM>), gS, kSTPB, 0, s, m, A.indptr, A.indices, Av, B.indptr, B.indices, Bv, Cp,
+                    (int32_t *)nullptr, Cv, (const T *)nullptr, (T *)nullptr, (T *)nullptr, b);
+        CSRK_LAUNCH((k_gemm_big_val<T, PH_NUM>), big_grid(), kGemmTPB, big_val_smem(), s, b, A.indptr, A.indices, Av,
+                    B.indptr, B.indices, Bv, C.indptr, C.indices, Cv, (const T *)nullptr, (T *)nullptr, (T *)nullptr);
     } else {
-        CSRK_LAUNCH((k_gemm_S<T, PH_BWD>), (unsigned)cdiv(m, kGemmTPB), kGemmTPB, 0, s, m, (const uint8_t *)b.bin,
-                    A.indptr, A.indices, Av, B.indptr, B.indices, Bv, (int64_t *)C.indptr, (int32_t *)nullptr,
-                    (T *)nullptr, dC, dA, dB);
-        CSRK_LAUNCH((k_gemm_ML_val<T, PH_BWD>), ml_grid(), kGemmTPB, mv, s, (const int32_t *)b.listM,
-                    (const int *)b.cnt, A.indptr, A.indices, Av, B.indptr, B.indices, Bv, C.indptr, C.indices,
-                    (T *)nullptr, dC, dA, dB);
-        CSRK_LAUNCH((k_gemm_ML_val<T, PH_BWD>), ml_grid(), kGemmTPB, mv, s, (const int32_t *)b.listL,
-                    (const int *)(b.cnt + 1), A.indptr, A.indices, Av, B.indptr, B.indices, Bv, C.indptr, C.indices,
-                    (T *)nullptr, dC, dA, dB);
+        CSRK_LAUNCH((k_gemm_S<T, PH_BWD>), gS, kSTPB, 0, s, m, A.indptr, A.indices, Av, B.indptr, B.indices, Bv, Cp,
+                    (int32_t *)nullptr, (T *)nullptr, dC, dA, dB, b);
+        CSRK_LAUNCH((k_gemm_big_val<T, PH_BWD>), big_grid(), kGemmTPB, big_val_smem(), s, b, A.indptr, A.indices, Av,
+                    B.indptr, B.indices, Bv, C.indptr, C.indices, (T *)nullptr, dC, dA, dB);
     }
     return CSRK_OK;
 }

@@ -1,15 +1,19 @@
 // spmm.cu -- SpDMM forward and backward (PAPER 3.1.3; Table 1).
 //
-// A group of G lanes owns one row (of A, or of A^T for the backward); each lane owns V
-// consecutive columns of the k-wide dense rows (16-byte vectors when aligned), so every
-// gathered X/dY row is one coalesced G*V*sizeof(T)-byte transaction.  Row nonzeros are
-// fetched G at a time (coalesced) and broadcast with shuffles.  Accumulation is fp64.
+// A CTA owns a tile of RT consecutive rows (of A, or of A^T for the transposed backward).
+// The tile's row pointers, column indices and values (for the transposed traversal: the
+// values gathered through perm, A[perm q], and perm itself) are staged in shared memory
+// with coalesced loads.  A group of G lanes then walks one row at a time; each lane owns W
+// consecutive columns of the k-wide dense rows (two 16-byte vectors when the rows are
+// aligned), so every gathered X / dY row is one coalesced G*W*sizeof(T)-byte transaction,
+// and the loop over a row's nonzeros is unrolled so its gathers are in flight together.
+// Accumulation is fp64 for both dtypes.
 //
 //   FWD      Y[i,:]  = sum_p A[p] X[idx p,:]
-//   FWD_PERM same over the cached transpose with values A[perm q]  (dX = A^T dY)
+//   FWD_PERM same over the cached transpose, values A[perm q]      (dX = A^T dY)
 //   SDDMM    dA[p]   = <dY[i,:], X[idx p,:]>                        ((dY X^T)(.)mask(A))
-//   FUSED_T  over row j of A^T: dX[j,:] = sum_q A[perm q] dY[i_q,:] and, from the same
-//            dY row, dA[perm q] = <dY[i_q,:], X[j,:]>  -- one pass for both gradients.
+//   FUSED_T  row j of A^T: dX[j,:] = sum_q A[perm q] dY[i_q,:] and, from the same dY row,
+//            dA[perm q] = <dY[i_q,:], X[j,:]>  -- both gradients in one pass.
 #include "ops.cuh"
 
 namespace csrk {
@@ -26,188 +30,231 @@ struct SpmmArgs {
     int64_t k;
     const T *X;  int64_t ldx;   // gathered operand (FWD: X, FUSED_T/FWD_PERM: dY, SDDMM: X)
     const T *W;  int64_t ldw;   // row operand (SDDMM: dY[i,:], FUSED_T: X[j,:])
-    T *Y;        int64_t ldy;   // dense output (FWD: Y, FUSED_T: dX)
+    T *Y;        int64_t ldy;   // dense output (FWD: Y, FUSED_T / FWD_PERM: dX)
     T *D;                       // dA (SDDMM, FUSED_T)
-    int G;                      // lanes per row (power of two, <= 32)
 };
 
-template <typename T, int V> struct VecT;
-template <> struct VecT<double, 1> { using type = double; };
-template <> struct VecT<double, 2> { using type = double2; };
-template <> struct VecT<float, 1> { using type = float; };
-template <> struct VecT<float, 4> { using type = float4; };
-
-template <typename T, int V>
-__device__ __forceinline__ void vload(const T *p, double (&r)[V])
-{
-    using VT = typename VecT<T, V>::type;
-    VT v = __ldg(reinterpret_cast<const VT *>(p));
-    const T *e = reinterpret_cast<const T *>(&v);
-#pragma unroll
-    for (int i = 0; i < V; ++i) r[i] = (double)e[i];
-}
-
-template <typename T, int V>
-__device__ __forceinline__ void vstore(T *p, const double (&r)[V])
-{
-    using VT = typename VecT<T, V>::type;
-    VT v;
-    T *e = reinterpret_cast<T *>(&v);
-#pragma unroll
-    for (int i = 0; i < V; ++i) e[i] = (T)r[i];
-    *reinterpret_cast<VT *>(p) = v;
-}
-
 constexpr int kSpmmTPB = 256;
+constexpr int kSpmmRPG = 4;        // rows per group per tile
+constexpr int kSpmmCAP = 1536;     // staged nonzeros per tile
+constexpr int kFusedMaxPasses = 2;
 
-template <typename T, int V, int MODE, int NP>
+// W consecutive elements of T, as fp64.
+template <typename T, int W>
+__device__ __forceinline__ void ldw(const T *p, double (&r)[W])
+{
+    if constexpr (W * sizeof(T) == 32) {
+        using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+        constexpr int E = 16 / sizeof(T);
+        V a = __ldg(reinterpret_cast<const V *>(p));
+        V b = __ldg(reinterpret_cast<const V *>(p) + 1);
+        const T *ea = reinterpret_cast<const T *>(&a), *eb = reinterpret_cast<const T *>(&b);
+#pragma unroll
+        for (int i = 0; i < E; ++i) { r[i] = (double)ea[i]; r[E + i] = (double)eb[i]; }
+    } else if constexpr (W * sizeof(T) == 16) {
+        using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+        V a = __ldg(reinterpret_cast<const V *>(p));
+        const T *ea = reinterpret_cast<const T *>(&a);
+#pragma unroll
+        for (int i = 0; i < W; ++i) r[i] = (double)ea[i];
+    } else {
+#pragma unroll
+        for (int i = 0; i < W; ++i) r[i] = (double)__ldg(p + i);
+    }
+}
+
+template <typename T, int W>
+__device__ __forceinline__ void stw(T *p, const double (&r)[W])
+{
+    if constexpr (W * sizeof(T) == 32) {
+        using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+        constexpr int E = 16 / sizeof(T);
+        V a, b;
+        T *ea = reinterpret_cast<T *>(&a), *eb = reinterpret_cast<T *>(&b);
+#pragma unroll
+        for (int i = 0; i < E; ++i) { ea[i] = (T)r[i]; eb[i] = (T)r[E + i]; }
+        reinterpret_cast<V *>(p)[0] = a;
+        reinterpret_cast<V *>(p)[1] = b;
+    } else if constexpr (W * sizeof(T) == 16) {
+        using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+        V a;
+        T *ea = reinterpret_cast<T *>(&a);
+#pragma unroll
+        for (int i = 0; i < W; ++i) ea[i] = (T)r[i];
+        *reinterpret_cast<V *>(p) = a;
+    } else {
+#pragma unroll
+        for (int i = 0; i < W; ++i) p[i] = (T)r[i];
+    }
+}
+
+template <int G>
+__device__ __forceinline__ double group_sum(double v)
+{
+#pragma unroll
+    for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, G);
+    return v;
+}
+
+template <typename T, int G, int W, int MODE>
 __global__ __launch_bounds__(kSpmmTPB) void k_spmm(SpmmArgs<T> a)
 {
-    const int G = a.G;
-    const int lane = threadIdx.x & (G - 1);
-    const int64_t row = ((int64_t)blockIdx.x * kSpmmTPB + threadIdx.x) / G;
-    if (row >= a.nrows) return;  // whole group leaves together
-    const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
-    const int64_t s = a.indptr[row], e = a.indptr[row + 1];
-    const int64_t stride = (int64_t)G * V;
+    constexpr int NG = kSpmmTPB / G;           // groups per CTA
+    constexpr int RT = NG * kSpmmRPG;          // rows per tile
+    constexpr bool PERM = MODE == SP_FWD_PERM || MODE == SP_FUSED_T;
+    __shared__ int64_t s_ptr[RT + 1];
+    __shared__ int32_t s_idx[kSpmmCAP];
+    __shared__ double s_val[kSpmmCAP];
+    __shared__ int64_t s_perm[MODE == SP_FUSED_T ? kSpmmCAP : 1];
 
-    if (MODE == SP_FWD || MODE == SP_FWD_PERM) {
-        for (int64_t col0 = 0; col0 < a.k; col0 += stride) {
-            const int64_t col = col0 + (int64_t)lane * V;
-            const bool act = col < a.k;
-            double acc[V];
-#pragma unroll
-            for (int i = 0; i < V; ++i) acc[i] = 0.0;
-            for (int64_t p0 = s; p0 < e; p0 += G) {
-                const int nb = (int)(e - p0 < G ? e - p0 : G);
-                int c_l = 0;
-                double a_l = 0.0;
-                if (lane < nb) {
-                    c_l = a.indices[p0 + lane];
-                    a_l = (double)a.vals[MODE == SP_FWD_PERM ? a.perm[p0 + lane] : p0 + lane];
-                }
-#pragma unroll 4
-                for (int b = 0; b < nb; ++b) {
-                    const int cb = __shfl_sync(gmask, c_l, b, G);
-                    const double ab = __shfl_sync(gmask, a_l, b, G);
-                    if (act) {
-                        double xv[V];
-                        vload<T, V>(a.X + (int64_t)cb * a.ldx + col, xv);
-#pragma unroll
-                        for (int i = 0; i < V; ++i) acc[i] = fma(ab, xv[i], acc[i]);
-                    }
-                }
-            }
-            if (act) vstore<T, V>(a.Y + row * a.ldy + col, acc);
+    const int tid = threadIdx.x, g = tid / G, lane = tid % G;
+    const int64_t r0 = (int64_t)blockIdx.x * RT;
+    const int nr = (int)(a.nrows - r0 < RT ? a.nrows - r0 : RT);
+    for (int i = tid; i <= nr; i += kSpmmTPB) s_ptr[i] = a.indptr[r0 + i];
+    __syncthreads();
+    const int64_t base = s_ptr[0];
+    const int64_t tnz = s_ptr[nr] - base;
+    const int staged = (int)(tnz < kSpmmCAP ? tnz : kSpmmCAP);
+    for (int e = tid; e < staged; e += kSpmmTPB) {
+        const int64_t p = base + e;
+        s_idx[e] = a.indices[p];
+        if (MODE != SP_SDDMM) {
+            const int64_t pv = PERM ? a.perm[p] : p;
+            s_val[e] = (double)a.vals[pv];
+            if (MODE == SP_FUSED_T) s_perm[e] = pv;
         }
-    } else if (MODE == SP_SDDMM) {
-        for (int64_t p0 = s; p0 < e; p0 += G) {
-            const int nb = (int)(e - p0 < G ? e - p0 : G);
-            const int c_l = lane < nb ? a.indices[p0 + lane] : 0;
-            double mine = 0.0;
-            for (int b = 0; b < nb; ++b) {
-                const int cb = __shfl_sync(gmask, c_l, b, G);
-                double dot = 0.0;
-                for (int64_t col0 = 0; col0 < a.k; col0 += stride) {
-                    const int64_t col = col0 + (int64_t)lane * V;
-                    if (col < a.k) {
-                        double xv[V], wv[V];
-                        vload<T, V>(a.X + (int64_t)cb * a.ldx + col, xv);
-                        vload<T, V>(a.W + row * a.ldw + col, wv);
+    }
+    __syncthreads();
+
+    // nonzero e of the tile (relative to base): staged in shared memory or read from global
+    auto idx_of = [&](int64_t e) -> int32_t { return e < staged ? s_idx[e] : a.indices[base + e]; };
+    auto val_of = [&](int64_t e) -> double {
+        return e < staged ? s_val[e] : (double)a.vals[PERM ? a.perm[base + e] : base + e];
+    };
+    auto perm_of = [&](int64_t e) -> int64_t { return e < staged ? s_perm[e] : a.perm[base + e]; };
+
+    const int64_t stride = (int64_t)G * W;
+    const int npass = (int)((a.k + stride - 1) / stride);
+
+    for (int j = 0; j < kSpmmRPG; ++j) {
+        const int rl = g + j * NG;   // adjacent groups take adjacent rows
+        const bool valid = rl < nr;
+        const int64_t row = r0 + rl;
+        const int64_t s = valid ? s_ptr[rl] - base : 0, e = valid ? s_ptr[rl + 1] - base : 0;
+        if (MODE == SP_SDDMM || MODE == SP_FUSED_T) {
+            // warp-uniform trip count: the group reductions below shuffle across the warp
+            const int len = (int)(e - s);
+            const int maxlen = (int)__reduce_max_sync(0xffffffffu, (unsigned)len);
+            if (!__any_sync(0xffffffffu, valid)) break;
+            if (MODE == SP_SDDMM) {
+                for (int t = 0; t < maxlen; ++t) {
+                    const bool on = t < len;
+                    const int32_t c = on ? idx_of(s + t) : 0;
+                    double dot = 0.0;
+                    for (int ps = 0; ps < npass; ++ps) {
+                        const int64_t col = ps * stride + (int64_t)lane * W;
+                        if (on && col < a.k) {
+                            double xv[W], wv[W];
+                            ldw<T, W>(a.X + (int64_t)c * a.ldx + col, xv);
+                            ldw<T, W>(a.W + row * a.ldw + col, wv);
 #pragma unroll
-                        for (int i = 0; i < V; ++i) dot = fma(wv[i], xv[i], dot);
-                    }
-                }
-                for (int o = G >> 1; o > 0; o >>= 1) dot += __shfl_xor_sync(gmask, dot, o, G);
-                if (lane == b) mine = dot;
-            }
-            if (lane < nb) a.D[p0 + lane] = (T)mine;
-        }
-    } else {  // SP_FUSED_T: row `row` of A^T (= column j of A)
-        double xj[NP][V], acc[NP][V];
-#pragma unroll
-        for (int q = 0; q < NP; ++q) {
-            const int64_t col = q * stride + (int64_t)lane * V;
-#pragma unroll
-            for (int i = 0; i < V; ++i) { xj[q][i] = 0.0; acc[q][i] = 0.0; }
-            if (col < a.k) vload<T, V>(a.W + row * a.ldw + col, xj[q]);
-        }
-        for (int64_t p0 = s; p0 < e; p0 += G) {
-            const int nb = (int)(e - p0 < G ? e - p0 : G);
-            int i_l = 0;
-            int64_t pv_l = 0;
-            double a_l = 0.0;
-            if (lane < nb) {
-                i_l = a.indices[p0 + lane];
-                pv_l = a.perm[p0 + lane];
-                a_l = (double)a.vals[pv_l];
-            }
-            double mine = 0.0;
-#pragma unroll 2
-            for (int b = 0; b < nb; ++b) {
-                const int ib = __shfl_sync(gmask, i_l, b, G);
-                const double ab = __shfl_sync(gmask, a_l, b, G);
-                double dot = 0.0;
-#pragma unroll
-                for (int q = 0; q < NP; ++q) {
-                    const int64_t col = q * stride + (int64_t)lane * V;
-                    if (col < a.k) {
-                        double g[V];
-                        vload<T, V>(a.X + (int64_t)ib * a.ldx + col, g);
-#pragma unroll
-                        for (int i = 0; i < V; ++i) {
-                            acc[q][i] = fma(ab, g[i], acc[q][i]);
-                            dot = fma(g[i], xj[q][i], dot);
+                            for (int i = 0; i < W; ++i) dot = fma(wv[i], xv[i], dot);
                         }
                     }
+                    dot = group_sum<G>(dot);
+                    if (on && lane == 0) a.D[base + s + t] = (T)dot;
                 }
-                for (int o = G >> 1; o > 0; o >>= 1) dot += __shfl_xor_sync(gmask, dot, o, G);
-                if (lane == b) mine = dot;
-            }
-            if (a.D && lane < nb) a.D[pv_l] = (T)mine;
-        }
+            } else {
+                double xj[kFusedMaxPasses][W], acc[kFusedMaxPasses][W];
 #pragma unroll
-        for (int q = 0; q < NP; ++q) {
-            const int64_t col = q * stride + (int64_t)lane * V;
-            if (col < a.k) vstore<T, V>(a.Y + row * a.ldy + col, acc[q]);
+                for (int ps = 0; ps < kFusedMaxPasses; ++ps) {
+                    const int64_t col = ps * stride + (int64_t)lane * W;
+#pragma unroll
+                    for (int i = 0; i < W; ++i) { xj[ps][i] = 0.0; acc[ps][i] = 0.0; }
+                    if (valid && ps < npass && col < a.k) ldw<T, W>(a.W + row * a.ldw + col, xj[ps]);
+                }
+#pragma unroll 2
+                for (int t = 0; t < maxlen; ++t) {
+                    const bool on = t < len;
+                    const int32_t i_row = on ? idx_of(s + t) : 0;
+                    const double av = on ? val_of(s + t) : 0.0;
+                    double dot = 0.0;
+#pragma unroll
+                    for (int ps = 0; ps < kFusedMaxPasses; ++ps) {
+                        const int64_t col = ps * stride + (int64_t)lane * W;
+                        if (on && ps < npass && col < a.k) {
+                            double gv[W];
+                            ldw<T, W>(a.X + (int64_t)i_row * a.ldx + col, gv);
+#pragma unroll
+                            for (int i = 0; i < W; ++i) {
+                                acc[ps][i] = fma(av, gv[i], acc[ps][i]);
+                                dot = fma(gv[i], xj[ps][i], dot);
+                            }
+                        }
+                    }
+                    dot = group_sum<G>(dot);
+                    if (on && a.D && lane == 0) a.D[perm_of(s + t)] = (T)dot;
+                }
+#pragma unroll
+                for (int ps = 0; ps < kFusedMaxPasses; ++ps) {
+                    const int64_t col = ps * stride + (int64_t)lane * W;
+                    if (valid && ps < npass && col < a.k) stw<T, W>(a.Y + row * a.ldy + col, acc[ps]);
+                }
+            }
+            continue;
+        }
+        if (!valid) break;
+
+        if (MODE == SP_FWD || MODE == SP_FWD_PERM) {
+            for (int ps = 0; ps < npass; ++ps) {
+                const int64_t col = ps * stride + (int64_t)lane * W;
+                const bool act = col < a.k;
+                double acc[W];
+#pragma unroll
+                for (int i = 0; i < W; ++i) acc[i] = 0.0;
+                if (act) {
+                    const T *Xc = a.X + col;
+#pragma unroll 4
+                    for (int64_t q = s; q < e; ++q) {
+                        const double av = val_of(q);
+                        double xv[W];
+                        ldw<T, W>(Xc + (int64_t)idx_of(q) * a.ldx, xv);
+#pragma unroll
+                        for (int i = 0; i < W; ++i) acc[i] = fma(av, xv[i], acc[i]);
+                    }
+                    stw<T, W>(a.Y + row * a.ldy + col, acc);
+                }
+            }
         }
     }
 }
 
-template <typename T, int V, int MODE, int NP>
+template <typename T, int G, int W, int MODE>
 static int launch_spmm(const SpmmArgs<T> &a, cudaStream_t s)
 {
     if (a.nrows <= 0) return CSRK_OK;
-    const int64_t per_cta = kSpmmTPB / a.G;
-    CSRK_LAUNCH((k_spmm<T, V, MODE, NP>), (unsigned)cdiv(a.nrows, per_cta), kSpmmTPB, 0, s, a);
+    constexpr int RT = (kSpmmTPB / G) * kSpmmRPG;
+    CSRK_LAUNCH((k_spmm<T, G, W, MODE>), (unsigned)cdiv(a.nrows, RT), kSpmmTPB, 0, s, a);
     return CSRK_OK;
 }
 
-// Vector width: 16-byte lanes when every dense row start is 16-byte aligned.
+// Vector path: each lane owns 4 consecutive columns (16 or 32 bytes; 8 lanes cover 32 columns);
+// needs 16-byte aligned row starts and k a multiple of 4.  Otherwise the scalar path (32 x 1).
 template <typename T>
-static int pick_v(int64_t k, std::initializer_list<std::pair<const void *, int64_t>> ops)
+static bool vec_ok(int64_t k, std::initializer_list<std::pair<const void *, int64_t>> ops)
 {
-    const int vmax = 16 / (int)sizeof(T);
-    if (k % vmax) return 1;
-    for (auto &o : ops) {
-        if (o.first && ((reinterpret_cast<uintptr_t>(o.first) & 15) || (o.second % vmax))) return 1;
-    }
-    return vmax;
+    if (k % 4) return false;
+    for (auto &o : ops)
+        if (o.first && ((reinterpret_cast<uintptr_t>(o.first) & 15) || ((o.second * (int64_t)sizeof(T)) % 16)))
+            return false;
+    return true;
 }
 
-static int pick_g(int64_t k, int V)
+template <typename T, int MODE>
+static int dispatch(bool vec, const SpmmArgs<T> &a, cudaStream_t s)
 {
-    int64_t need = cdiv(k, V);
-    int G = 4;
-    while (G < 32 && G < need) G <<= 1;
-    return G;
-}
-
-template <typename T, int MODE, int NP>
-static int dispatch_v(int V, const SpmmArgs<T> &a, cudaStream_t s)
-{
-    if (V == 1) return launch_spmm<T, 1, MODE, NP>(a, s);
-    return launch_spmm<T, 16 / sizeof(T), MODE, NP>(a, s);
+    if (vec) return launch_spmm<T, 8, 4, MODE>(a, s);
+    return launch_spmm<T, 32, 1, MODE>(a, s);
 }
 
 template <typename T>
@@ -218,9 +265,7 @@ static int spmm_fwd_t(const csrk_pattern &A, const T *A_val, int64_t k, const T 
     SpmmArgs<T> a{};
     a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices; a.vals = A_val;
     a.k = k; a.X = X; a.ldx = ldx; a.Y = Y; a.ldy = ldy;
-    const int V = pick_v<T>(k, {{X, ldx}, {Y, ldy}});
-    a.G = pick_g(k, V);
-    return dispatch_v<T, SP_FWD, 1>(V, a, s);
+    return dispatch<T, SP_FWD>(vec_ok<T>(k, {{X, ldx}, {Y, ldy}}), a, s);
 }
 
 template <typename T>
@@ -228,43 +273,40 @@ static int spmm_bwd_t(const csrk_pattern &A, const T *A_val, const csrk_pattern 
                       int64_t k, const T *X, int64_t ldx, const T *dY, int64_t lddy, T *dA, T *dX, int64_t lddx,
                       Bump &ws, cudaStream_t s)
 {
-    const int V = pick_v<T>(k, {{X, ldx}, {dY, lddy}, {dX, lddx}});
-    const int G = pick_g(k, V);
-    const int64_t np = cdiv(k, (int64_t)G * V);
+    const bool vec = vec_ok<T>(k, {{X, ldx}, {dY, lddy}, {dX, lddx}});
+    const int64_t stride = 32;  // columns per pass: 8 lanes x 4 (vector) or 32 lanes x 1
+    const int64_t np = cdiv(k, stride);
     // Transpose plan: the caller's, or built in the workspace.
     csrk_pattern ATl{};
     const int64_t *permu = perm;
     if (dX && !AT) {
         int64_t *ATp = ws.take<int64_t>(A.ncols + 1);
-        int32_t *ATi = ws.take<int32_t>(A.nnz);
-        int64_t *pm = ws.take<int64_t>(A.nnz);
+        int32_t *ATi = ws.take<int32_t>(A.nnz > 0 ? A.nnz : 1);
+        int64_t *pm = ws.take<int64_t>(A.nnz > 0 ? A.nnz : 1);
         CSRK_TRY(transpose_impl(CSRK_F64, A, nullptr, ATp, ATi, nullptr, pm, ws, s));
         ATl = csrk_pattern{A.ncols, A.nrows, A.nnz, ATp, ATi};
         AT = &ATl;
         permu = pm;
     }
-    if (ws.overflow) return CSRK_ERR_WORKSPACE;
     if (ws.sizing() || k == 0) return CSRK_OK;
     SpmmArgs<T> a{};
-    a.k = k; a.G = G; a.vals = A_val;
-    if (dX && np <= 4) {
+    a.k = k; a.vals = A_val;
+    if (dX && np <= kFusedMaxPasses) {
         // fused transposed traversal: dX and (optionally) dA in one pass
         a.nrows = AT->nrows; a.indptr = AT->indptr; a.indices = AT->indices; a.perm = permu;
         a.X = dY; a.ldx = lddy; a.W = X; a.ldw = ldx; a.Y = dX; a.ldy = lddx; a.D = dA;
-        if (np == 1) return dispatch_v<T, SP_FUSED_T, 1>(V, a, s);
-        if (np == 2) return dispatch_v<T, SP_FUSED_T, 2>(V, a, s);
-        return dispatch_v<T, SP_FUSED_T, 4>(V, a, s);
+        return dispatch<T, SP_FUSED_T>(vec, a, s);
     }
     if (dX) {
         SpmmArgs<T> b = a;
         b.nrows = AT->nrows; b.indptr = AT->indptr; b.indices = AT->indices; b.perm = permu;
         b.X = dY; b.ldx = lddy; b.Y = dX; b.ldy = lddx;
-        CSRK_TRY((dispatch_v<T, SP_FWD_PERM, 1>(V, b, s)));
+        CSRK_TRY((dispatch<T, SP_FWD_PERM>(vec, b, s)));
     }
     if (dA && A.nrows > 0) {
         a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices;
         a.X = X; a.ldx = ldx; a.W = dY; a.ldw = lddy; a.D = dA;
-        CSRK_TRY((dispatch_v<T, SP_SDDMM, 1>(V, a, s)));
+        CSRK_TRY((dispatch<T, SP_SDDMM>(vec, a, s)));
     }
     return CSRK_OK;
 }

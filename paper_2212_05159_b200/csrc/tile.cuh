@@ -26,6 +26,8 @@ enum { MODE_REDUCE = 0, MODE_SCATTER = 1, MODE_TRANSPOSE = 2 };
 constexpr int kTileTPB = 256;
 constexpr int kTileIPT = 6;
 constexpr int kTileCAP = kTileTPB * kTileIPT;
+constexpr int kTileShortRow = 256;   // fast path: all rows of the tile at most this long
+constexpr int kTileMaxRPT = 4;        // rows per thread in the fast path (R <= 1024)
 
 template <typename T>
 struct TileArgs {
@@ -39,8 +41,7 @@ struct TileArgs {
     const T *u;             // row vector (SIDE / SCATTER)
     T *D;                   // SIDE output aligned with the values
     int64_t *cursor;        // TRANSPOSE
-    int32_t *out_idx;       // TRANSPOSE: AT indices
-    int64_t *out_perm;      // TRANSPOSE: perm
+    uint64_t *out_keys;     // TRANSPOSE: packed (p << 31) | row per claimed slot
     int R;                  // rows per tile
 };
 
@@ -109,6 +110,78 @@ __global__ __launch_bounds__(kTileTPB) void k_csr_tile(TileArgs<T> a)
     const int64_t total = nr + Z;
     int cc_row = -1;
     double cc_val = 0.0;
+
+    // ---- fast path: every row of the tile is short -> a thread owns its rows (tid + i*TPB)
+    bool mine_short = true;
+    for (int i = tid; i < nr; i += kTileTPB) mine_short &= (s_ptr[i + 1] - s_ptr[i]) <= kTileShortRow;
+    if (__syncthreads_and(mine_short)) {
+        double acc[kTileMaxRPT];
+#pragma unroll
+        for (int j = 0; j < kTileMaxRPT; ++j) acc[j] = 0.0;
+        for (int64_t c0 = 0; c0 < Z; c0 += kTileCAP) {
+            const int64_t c1 = c0 + kTileCAP < Z ? c0 + kTileCAP : Z;
+            if (MODE == MODE_REDUCE) {
+#pragma unroll 2
+                for (int64_t e = c0 + tid; e < c1; e += kTileTPB) {
+                    const int64_t p = nzb + e;
+                    const int64_t pv = PERM ? a.perm[p] : p;
+                    s_prod[e - c0] = (double)a.vals[pv] * (double)a.v[a.indices[p]];
+                }
+            }
+            if (NEED_ROW) {
+#pragma unroll
+                for (int j = 0; j < kTileMaxRPT; ++j) {
+                    const int r = tid + j * kTileTPB;
+                    if (r < nr) {
+                        const int64_t s = s_ptr[r] - nzb, e = s_ptr[r + 1] - nzb;
+                        for (int64_t q = (s > c0 ? s : c0); q < (e < c1 ? e : c1); ++q) s_row[q - c0] = r;
+                    }
+                }
+            }
+            __syncthreads();
+            if (MODE == MODE_REDUCE) {
+#pragma unroll
+                for (int j = 0; j < kTileMaxRPT; ++j) {
+                    const int r = tid + j * kTileTPB;
+                    if (r < nr) {
+                        const int64_t s = s_ptr[r] - nzb, e = s_ptr[r + 1] - nzb;
+                        double t = acc[j];
+                        for (int64_t q = (s > c0 ? s : c0); q < (e < c1 ? e : c1); ++q) t += s_prod[q - c0];
+                        acc[j] = t;
+                    }
+                }
+            }
+            if (NEED_ROW) {
+#pragma unroll 4
+                for (int64_t e = c0 + tid; e < c1; e += kTileTPB) {
+                    const int64_t p = nzb + e;
+                    const int r = s_row[e - c0];
+                    const int32_t c = a.indices[p];
+                    if (MODE == MODE_SCATTER) {
+                        const T w = s_u[r];
+                        if (SIDE) a.D[p] = w * a.v[c];
+                        if (a.y) red_add(&a.y[c], (T)((double)a.vals[p] * (double)w));
+                    } else if (MODE == MODE_REDUCE) {
+                        const int64_t pv = PERM ? a.perm[p] : p;
+                        a.D[pv] = a.v[c] * s_u[r];
+                    } else {
+                        const int64_t slot =
+                            (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(&a.cursor[c]), 1ULL);
+                        a.out_keys[slot] = ((uint64_t)p << 31) | (uint64_t)(r0 + r);
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        if (MODE == MODE_REDUCE) {
+#pragma unroll
+            for (int j = 0; j < kTileMaxRPT; ++j) {
+                const int r = tid + j * kTileTPB;
+                if (r < nr) a.y[r0 + r] = (T)acc[j];
+            }
+        }
+        return;
+    }
 
     for (int64_t D0 = 0; D0 < total; D0 += kTileCAP) {
         const int64_t D1 = D0 + kTileCAP < total ? D0 + kTileCAP : total;
@@ -196,8 +269,7 @@ __global__ __launch_bounds__(kTileTPB) void k_csr_tile(TileArgs<T> a)
                     a.D[pv] = a.v[c] * s_u[r];
                 } else {  // TRANSPOSE
                     const int64_t slot = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(&a.cursor[c]), 1ULL);
-                    a.out_idx[slot] = (int32_t)(r0 + r);
-                    a.out_perm[slot] = p;
+                    a.out_keys[slot] = ((uint64_t)p << 31) | (uint64_t)(r0 + r);
                 }
             }
         }

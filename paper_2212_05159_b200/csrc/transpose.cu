@@ -1,21 +1,30 @@
 // transpose.cu -- CSR transpose with position map ("take the sparse transpose of A";
-// S:53-61).  Counting sort by column:
+// S:53-61).  A counting sort by column:
 //   1. column histogram (int64 atomics into AT_indptr[1..n])
 //   2. int64 prefix scan -> AT_indptr
-//   3. row-tile scatter: each nonzero claims a slot of its column (atomic cursor) and
-//      writes its row and source position (tile.cuh, MODE_TRANSPOSE)
-//   4. per-column sort by row (thread / warp / CTA / merge-sort bins by length) -- makes
-//      the result canonical and bit-identical to the stable counting sort of the oracle
-//   5. AT_val[q] = A_val[perm[q]]
+//   3. row-tile scatter (tile.cuh, MODE_TRANSPOSE): every nonzero claims a slot of its column
+//      with an atomic cursor and stores ONE packed key  (p << 31) | row  (p = its position in
+//      A).  Within a column rows are distinct and p grows with the row, so ordering keys
+//      orders rows.
+//   4. per-column sort of the keys (register network for <= 16, warp / CTA bitonic in shared
+//      memory, merge sort through a workspace buffer beyond 8192), then unpack into
+//      AT_indices (row) and AT_perm (p) -- canonical CSR, bit-identical to the stable
+//      counting sort of the oracle regardless of the atomic order.
+//   5. AT_val[q] = A_val[perm[q]] (optional)
+// Packing needs nnz < 2^33 (checked).
 #include "ops.cuh"
 #include "tile.cuh"
 
 namespace csrk {
 
-constexpr int kShortMax = 16;
+constexpr int kRegMax = 16;
 constexpr int kWarpMax = 1024;
 constexpr int kBlockMax = 8192;
 constexpr int kSortTPB = 256;
+constexpr uint64_t kKeyPad = ~0ull;
+
+__device__ __forceinline__ int32_t key_row(uint64_t k) { return (int32_t)(k & 0x7fffffffull); }
+__device__ __forceinline__ int64_t key_pos(uint64_t k) { return (int64_t)(k >> 31); }
 
 __global__ void k_col_count(int64_t nnz, const int32_t *__restrict__ indices, unsigned long long *__restrict__ cnt)
 {
@@ -26,29 +35,54 @@ __global__ void k_col_count(int64_t nnz, const int32_t *__restrict__ indices, un
 struct SortLists {
     int32_t *mid, *big, *huge;
     int *count;  // [3]
-    int64_t cap_mid, cap_big, cap_huge;
 };
 
-// Short columns are sorted in place by one thread (insertion sort); longer ones are queued.
-__global__ void k_sort_short(int64_t n, const int64_t *__restrict__ ATp, int32_t *__restrict__ ATi,
-                             int64_t *__restrict__ perm, SortLists L)
+template <int N>
+__device__ __forceinline__ void reg_sort(uint64_t (&k)[N])
+{
+#pragma unroll
+    for (int size = 2; size <= N; size <<= 1)
+#pragma unroll
+        for (int stride = size / 2; stride > 0; stride >>= 1)
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const bool asc = (i & size) == 0;
+                    const uint64_t a = k[i], b = k[j];
+                    if ((a > b) == asc) { k[i] = b; k[j] = a; }
+                }
+            }
+}
+
+template <int N>
+__device__ __forceinline__ void sort_unpack_regs(const uint64_t *__restrict__ keys, int64_t s, int len,
+                                                 int32_t *__restrict__ ATi, int64_t *__restrict__ perm)
+{
+    uint64_t k[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) k[i] = i < len ? keys[s + i] : kKeyPad;
+    reg_sort<N>(k);
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+        if (i < len) {
+            ATi[s + i] = key_row(k[i]);
+            perm[s + i] = key_pos(k[i]);
+        }
+}
+
+// Columns of length <= 16 are sorted in registers by their own thread; longer ones queued.
+__global__ __launch_bounds__(256) void k_sort_short(int64_t n, const int64_t *__restrict__ ATp,
+                                                    const uint64_t *__restrict__ keys, int32_t *__restrict__ ATi,
+                                                    int64_t *__restrict__ perm, SortLists L)
 {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
         const int64_t s = ATp[j], len = ATp[j + 1] - s;
-        if (len <= 1) continue;
-        if (len <= kShortMax) {
-            int32_t key[kShortMax];
-            int64_t pay[kShortMax];
-            for (int i = 0; i < len; ++i) { key[i] = ATi[s + i]; pay[i] = perm[s + i]; }
-            for (int i = 1; i < len; ++i) {
-                int32_t k = key[i];
-                int64_t p = pay[i];
-                int t = i - 1;
-                while (t >= 0 && key[t] > k) { key[t + 1] = key[t]; pay[t + 1] = pay[t]; --t; }
-                key[t + 1] = k;
-                pay[t + 1] = p;
-            }
-            for (int i = 0; i < len; ++i) { ATi[s + i] = key[i]; perm[s + i] = pay[i]; }
+        if (len == 0) continue;
+        if (len <= 8) {
+            sort_unpack_regs<8>(keys, s, (int)len, ATi, perm);
+        } else if (len <= kRegMax) {
+            sort_unpack_regs<16>(keys, s, (int)len, ATi, perm);
         } else if (len <= kWarpMax) {
             L.mid[atomicAdd(&L.count[0], 1)] = (int32_t)j;
         } else if (len <= kBlockMax) {
@@ -59,9 +93,9 @@ __global__ void k_sort_short(int64_t n, const int64_t *__restrict__ ATp, int32_t
     }
 }
 
-// Bitonic sort of (key, payload) pairs held in shared memory; `nt` threads cooperate.
+// Bitonic sort of u64 keys in shared memory; `nt` threads cooperate.
 template <bool WARP>
-__device__ __forceinline__ void smem_bitonic(int32_t *key, int64_t *pay, int P, int t, int nt)
+__device__ __forceinline__ void smem_bitonic(uint64_t *key, int P, int t, int nt)
 {
     for (int k = 2; k <= P; k <<= 1)
         for (int j = k >> 1; j > 0; j >>= 1) {
@@ -69,10 +103,8 @@ __device__ __forceinline__ void smem_bitonic(int32_t *key, int64_t *pay, int P, 
                 const int ixj = i ^ j;
                 if (ixj > i) {
                     const bool asc = (i & k) == 0;
-                    if ((key[i] > key[ixj]) == asc) {
-                        int32_t tk = key[i]; key[i] = key[ixj]; key[ixj] = tk;
-                        int64_t tp = pay[i]; pay[i] = pay[ixj]; pay[ixj] = tp;
-                    }
+                    const uint64_t a = key[i], b = key[ixj];
+                    if ((a > b) == asc) { key[i] = b; key[ixj] = a; }
                 }
             }
             if (WARP) __syncwarp(); else __syncthreads();
@@ -89,11 +121,11 @@ __device__ __forceinline__ int pow2ceil(int x)
 constexpr int kWarpsPerSortCTA = 4;
 
 __global__ __launch_bounds__(32 * kWarpsPerSortCTA) void k_sort_warp(const int64_t *__restrict__ ATp,
+                                                                     const uint64_t *__restrict__ keys,
                                                                      int32_t *__restrict__ ATi,
                                                                      int64_t *__restrict__ perm, SortLists L)
 {
-    __shared__ int32_t s_key[kWarpsPerSortCTA][kWarpMax];
-    __shared__ int64_t s_pay[kWarpsPerSortCTA][kWarpMax];
+    __shared__ uint64_t s_key[kWarpsPerSortCTA][kWarpMax];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int cnt = *(volatile int *)&L.count[0];
     for (int it = blockIdx.x * kWarpsPerSortCTA + w; it < cnt; it += gridDim.x * kWarpsPerSortCTA) {
@@ -101,78 +133,63 @@ __global__ __launch_bounds__(32 * kWarpsPerSortCTA) void k_sort_warp(const int64
         const int64_t s = ATp[j];
         const int len = (int)(ATp[j + 1] - s);
         const int P = pow2ceil(len);
-        for (int i = lane; i < P; i += 32) {
-            s_key[w][i] = i < len ? ATi[s + i] : INT32_MAX;
-            s_pay[w][i] = i < len ? perm[s + i] : 0;
-        }
+        for (int i = lane; i < P; i += 32) s_key[w][i] = i < len ? keys[s + i] : kKeyPad;
         __syncwarp();
-        smem_bitonic<true>(s_key[w], s_pay[w], P, lane, 32);
+        smem_bitonic<true>(s_key[w], P, lane, 32);
         for (int i = lane; i < len; i += 32) {
-            ATi[s + i] = s_key[w][i];
-            perm[s + i] = s_pay[w][i];
+            ATi[s + i] = key_row(s_key[w][i]);
+            perm[s + i] = key_pos(s_key[w][i]);
         }
         __syncwarp();
     }
 }
 
-__global__ __launch_bounds__(kSortTPB) void k_sort_block(const int64_t *__restrict__ ATp, int32_t *__restrict__ ATi,
+__global__ __launch_bounds__(kSortTPB) void k_sort_block(const int64_t *__restrict__ ATp,
+                                                         const uint64_t *__restrict__ keys, int32_t *__restrict__ ATi,
                                                          int64_t *__restrict__ perm, SortLists L)
 {
     extern __shared__ __align__(16) unsigned char smem[];
-    int64_t *s_pay = reinterpret_cast<int64_t *>(smem);
-    int32_t *s_key = reinterpret_cast<int32_t *>(smem + sizeof(int64_t) * kBlockMax);
+    uint64_t *s_key = reinterpret_cast<uint64_t *>(smem);
     const int cnt = *(volatile int *)&L.count[1];
     for (int it = blockIdx.x; it < cnt; it += gridDim.x) {
         const int64_t j = L.big[it];
         const int64_t s = ATp[j];
         const int len = (int)(ATp[j + 1] - s);
         const int P = pow2ceil(len);
-        for (int i = threadIdx.x; i < P; i += kSortTPB) {
-            s_key[i] = i < len ? ATi[s + i] : INT32_MAX;
-            s_pay[i] = i < len ? perm[s + i] : 0;
-        }
+        for (int i = threadIdx.x; i < P; i += kSortTPB) s_key[i] = i < len ? keys[s + i] : kKeyPad;
         __syncthreads();
-        smem_bitonic<false>(s_key, s_pay, P, threadIdx.x, kSortTPB);
+        smem_bitonic<false>(s_key, P, threadIdx.x, kSortTPB);
         for (int i = threadIdx.x; i < len; i += kSortTPB) {
-            ATi[s + i] = s_key[i];
-            perm[s + i] = s_pay[i];
+            ATi[s + i] = key_row(s_key[i]);
+            perm[s + i] = key_pos(s_key[i]);
         }
         __syncthreads();
     }
 }
 
-// Huge columns: sort the source positions only (p ascending <=> row ascending within a
-// column), by CTA-wide bitonic runs of kBlockMax followed by merge passes through `buf`;
-// then recover the row of each position by binary search in A.indptr.
-__global__ __launch_bounds__(kSortTPB) void k_sort_huge(int64_t m, const int64_t *__restrict__ Ap,
-                                                        const int64_t *__restrict__ ATp, int32_t *__restrict__ ATi,
-                                                        int64_t *__restrict__ perm, int64_t *__restrict__ buf,
-                                                        SortLists L)
+// Huge columns: runs of kBlockMax sorted in shared memory, then pairwise merge passes
+// (merge-path split across the CTA) ping-ponging between `keys` and `buf`.
+__global__ __launch_bounds__(kSortTPB) void k_sort_huge(const int64_t *__restrict__ ATp, uint64_t *__restrict__ keys,
+                                                        uint64_t *__restrict__ buf, int32_t *__restrict__ ATi,
+                                                        int64_t *__restrict__ perm, SortLists L)
 {
     extern __shared__ __align__(16) unsigned char smem[];
-    int64_t *s_pay = reinterpret_cast<int64_t *>(smem);
-    int32_t *s_key = reinterpret_cast<int32_t *>(smem + sizeof(int64_t) * kBlockMax);
+    uint64_t *s_key = reinterpret_cast<uint64_t *>(smem);
     const int cnt = *(volatile int *)&L.count[2];
     for (int it = blockIdx.x; it < cnt; it += gridDim.x) {
         const int64_t j = L.huge[it];
         const int64_t s = ATp[j];
         const int64_t len = ATp[j + 1] - s;
-        // runs of kBlockMax sorted in shared memory (keys = low bits unused; sort by payload)
         for (int64_t r = 0; r < len; r += kBlockMax) {
             const int rl = (int)(len - r < kBlockMax ? len - r : kBlockMax);
             const int P = pow2ceil(rl);
-            for (int i = threadIdx.x; i < P; i += kSortTPB) {
-                // order by position: use the row as key (rows are distinct and increasing with p)
-                s_key[i] = i < rl ? ATi[s + r + i] : INT32_MAX;
-                s_pay[i] = i < rl ? perm[s + r + i] : 0;
-            }
+            for (int i = threadIdx.x; i < P; i += kSortTPB) s_key[i] = i < rl ? keys[s + r + i] : kKeyPad;
             __syncthreads();
-            smem_bitonic<false>(s_key, s_pay, P, threadIdx.x, kSortTPB);
-            for (int i = threadIdx.x; i < rl; i += kSortTPB) perm[s + r + i] = s_pay[i];
+            smem_bitonic<false>(s_key, P, threadIdx.x, kSortTPB);
+            for (int i = threadIdx.x; i < rl; i += kSortTPB) keys[s + r + i] = s_key[i];
             __syncthreads();
         }
-        // merge passes (payload only), ping-pong between perm and buf
-        int64_t *src = perm + s, *dst = buf + s;
+        uint64_t *src = keys + s, *dst = buf + s;
         for (int64_t width = kBlockMax; width < len; width <<= 1) {
             for (int64_t lo = 0; lo < len; lo += 2 * width) {
                 const int64_t mid = lo + width < len ? lo + width : len;
@@ -181,10 +198,9 @@ __global__ __launch_bounds__(kSortTPB) void k_sort_huge(int64_t m, const int64_t
                 const int64_t per = cdiv(tot, kSortTPB);
                 const int64_t d0 = (int64_t)threadIdx.x * per < tot ? (int64_t)threadIdx.x * per : tot;
                 const int64_t d1 = d0 + per < tot ? d0 + per : tot;
-                // merge-path search for d0
                 int64_t a_lo = d0 - nb > 0 ? d0 - nb : 0, a_hi = d0 < na ? d0 : na;
                 while (a_lo < a_hi) {
-                    int64_t piv = (a_lo + a_hi) >> 1;
+                    const int64_t piv = (a_lo + a_hi) >> 1;
                     if (src[lo + piv] < src[mid + d0 - piv - 1]) a_lo = piv + 1;
                     else a_hi = piv;
                 }
@@ -195,20 +211,12 @@ __global__ __launch_bounds__(kSortTPB) void k_sort_huge(int64_t m, const int64_t
                 }
             }
             __syncthreads();
-            int64_t *t = src; src = dst; dst = t;
+            uint64_t *t = src; src = dst; dst = t;
         }
-        if (src != perm + s)
-            for (int64_t i = threadIdx.x; i < len; i += kSortTPB) perm[s + i] = src[i];
-        __syncthreads();
-        // rows from positions
         for (int64_t i = threadIdx.x; i < len; i += kSortTPB) {
-            const int64_t p = perm[s + i];
-            int64_t lo = 0, hi = m;  // largest row with Ap[row] <= p
-            while (hi - lo > 1) {
-                int64_t piv = (lo + hi) >> 1;
-                if (Ap[piv] <= p) lo = piv; else hi = piv;
-            }
-            ATi[s + i] = (int32_t)lo;
+            const uint64_t k = src[i];
+            ATi[s + i] = key_row(k);
+            perm[s + i] = key_pos(k);
         }
         __syncthreads();
     }
@@ -233,17 +241,16 @@ int transpose_impl(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int6
                    void *AT_val, int64_t *perm, Bump &ws, cudaStream_t s)
 {
     const int64_t n = A.ncols, nnz = A.nnz;
+    if (nnz >= (int64_t(1) << 33)) return CSRK_ERR_INDEX_OVERFLOW;
     int64_t *cursor = ws.take<int64_t>(n > 0 ? n : 1);
+    uint64_t *keys = ws.take<uint64_t>(nnz > 0 ? nnz : 1);
     int64_t *pm = perm ? perm : ws.take<int64_t>(nnz > 0 ? nnz : 1);
     SortLists L{};
-    L.cap_mid = nnz / (kShortMax + 1) + 1;
-    L.cap_big = nnz / (kWarpMax + 1) + 1;
-    L.cap_huge = nnz / (kBlockMax + 1) + 1;
-    L.mid = ws.take<int32_t>(L.cap_mid);
-    L.big = ws.take<int32_t>(L.cap_big);
-    L.huge = ws.take<int32_t>(L.cap_huge);
+    L.mid = ws.take<int32_t>(nnz / (kRegMax + 1) + 1);
+    L.big = ws.take<int32_t>(nnz / (kWarpMax + 1) + 1);
+    L.huge = ws.take<int32_t>(nnz / (kBlockMax + 1) + 1);
     L.count = ws.take<int>(4);
-    int64_t *buf = ws.take<int64_t>(nnz > kBlockMax ? nnz : 1);
+    uint64_t *buf = ws.take<uint64_t>(nnz > kBlockMax ? nnz : 1);
     if (ws.sizing()) return scan_counts_i64(nullptr, n, ws, s);  // carve the scan scratch
 
     CSRK_CUDA(cudaMemsetAsync(ATp, 0, sizeof(int64_t) * (size_t)(n + 1), s));
@@ -257,14 +264,15 @@ int transpose_impl(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int6
     {
         TileArgs<double> a{};
         a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices;
-        a.cursor = cursor; a.out_idx = ATi; a.out_perm = pm;
+        a.cursor = cursor; a.out_keys = keys;
         a.R = tile_rows(A.nrows, nnz);
         CSRK_TRY((launch_tile<double, MODE_TRANSPOSE, false, false>(a, s)));
     }
-    CSRK_LAUNCH(k_sort_short, grid_for(n, 256), 256, 0, s, n, (const int64_t *)ATp, ATi, pm, L);
-    if (nnz > kShortMax)
-        CSRK_LAUNCH(k_sort_warp, (unsigned)(kNumSMs * 4), 32 * kWarpsPerSortCTA, 0, s, (const int64_t *)ATp, ATi, pm, L);
-    const size_t big_smem = (sizeof(int64_t) + sizeof(int32_t)) * kBlockMax;
+    CSRK_LAUNCH(k_sort_short, grid_for(n, 256), 256, 0, s, n, (const int64_t *)ATp, (const uint64_t *)keys, ATi, pm, L);
+    if (nnz > kRegMax)
+        CSRK_LAUNCH(k_sort_warp, (unsigned)(kNumSMs * 4), 32 * kWarpsPerSortCTA, 0, s, (const int64_t *)ATp,
+                    (const uint64_t *)keys, ATi, pm, L);
+    const size_t big_smem = sizeof(uint64_t) * kBlockMax;
     static bool attr = false;
     if (!attr) {
         CSRK_CUDA(cudaFuncSetAttribute(k_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big_smem));
@@ -272,10 +280,11 @@ int transpose_impl(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int6
         attr = true;
     }
     if (nnz > kWarpMax)
-        CSRK_LAUNCH(k_sort_block, (unsigned)kNumSMs, kSortTPB, big_smem, s, (const int64_t *)ATp, ATi, pm, L);
+        CSRK_LAUNCH(k_sort_block, (unsigned)kNumSMs, kSortTPB, big_smem, s, (const int64_t *)ATp,
+                    (const uint64_t *)keys, ATi, pm, L);
     if (nnz > kBlockMax)
-        CSRK_LAUNCH(k_sort_huge, (unsigned)kNumSMs, kSortTPB, big_smem, s, A.nrows, A.indptr, (const int64_t *)ATp,
-                    ATi, pm, buf, L);
+        CSRK_LAUNCH(k_sort_huge, (unsigned)kNumSMs, kSortTPB, big_smem, s, (const int64_t *)ATp, keys, buf, ATi, pm,
+                    L);
     if (AT_val) {
         if (dt == CSRK_F64)
             CSRK_LAUNCH(k_gather_vals<double>, grid_for(nnz, 256), 256, 0, s, nnz, (const int64_t *)pm,
