@@ -335,6 +335,14 @@ def main():
     dom = max(OPS, key=lambda nm: op_ms[nm])
     dom_bytes = W.costs[dom][0]
     achieved = dom_bytes / (op_ms[dom] * 1e-3) / 1e9
+    # DRAM traffic of that op per launch, from the committed ncu capture (tools/profile_summary.py)
+    traffic, traffic_src = None, None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "latest_ops.json")))
+        traffic = prof["ops"][dom]["dram_bytes"]
+        traffic_src = prof.get("source")
+    except Exception:
+        pass
     ops_report = {nm: {"ms": round(op_ms[nm], 4),
                        "GB/s": round(W.costs[nm][0] / (op_ms[nm] * 1e-3) / 1e9, 1) if nm in W.costs else None,
                        "GFLOP/s": round(W.costs[nm][1] / (op_ms[nm] * 1e-3) / 1e9, 1) if nm in W.costs else None,
@@ -356,7 +364,7 @@ def main():
                "step_bytes_per_gpu": step_bytes,
                "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                             "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                            "traffic": None, "algorithmic_bytes": dom_bytes},
+                            "traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes": dom_bytes},
                "ops": ops_report, "gpu_launches": int(launches),
                "clocks": clk.summary()}
     # ---------------- e2e: same metric through the public API with pinned host buffers

@@ -96,43 +96,48 @@ __device__ __forceinline__ double group_sum(double v)
     return v;
 }
 
-template <typename T, int G, int W, int MODE>
-__global__ __launch_bounds__(kSpmmTPB) void k_spmm(SpmmArgs<T> a)
+// Reduce four per-lane values d[0..3] across a group of G (>= 4) lanes at once ("transpose
+// reduce"): the first two butterfly steps exchange halves of the vector, the rest reduce one
+// value.  Lane l ends with the group sum of d[v], v = l / (G/4).  8 shuffles for G = 8
+// instead of 4 x 6 for four separate reductions.
+template <int G>
+__device__ __forceinline__ double group_sum4(const double (&d)[4], int lane)
 {
-    constexpr int NG = kSpmmTPB / G;           // groups per CTA
-    constexpr int RT = NG * kSpmmRPG;          // rows per tile
+    constexpr int o1 = G >> 1, o2 = G >> 2;
+    const bool lo1 = (lane & o1) == 0;
+    const double s0 = lo1 ? d[2] : d[0], s1 = lo1 ? d[3] : d[1];
+    const double k0 = (lo1 ? d[0] : d[2]) + __shfl_xor_sync(0xffffffffu, s0, o1, G);
+    const double k1 = (lo1 ? d[1] : d[3]) + __shfl_xor_sync(0xffffffffu, s1, o1, G);
+    const bool lo2 = (lane & o2) == 0;
+    double v = (lo2 ? k0 : k1) + __shfl_xor_sync(0xffffffffu, lo2 ? k1 : k0, o2, G);
+#pragma unroll
+    for (int o = o2 >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, G);
+    return v;
+}
+
+// Rows [r0, r0 + nr) of a tile.  STAGED: the tile's nonzeros are in shared memory as
+// (byte offset of the gathered row, value[, perm]); otherwise they are read from global.
+template <typename T, int G, int W, int MODE, bool STAGED>
+__device__ __forceinline__ void spmm_rows(const SpmmArgs<T> &a, const int64_t *s_ptr, const int64_t *s_off,
+                                          const double *s_val, const int64_t *s_perm, int64_t r0, int nr,
+                                          int64_t base)
+{
+    constexpr int NG = kSpmmTPB / G;
     constexpr bool PERM = MODE == SP_FWD_PERM || MODE == SP_FUSED_T;
-    __shared__ int64_t s_ptr[RT + 1];
-    __shared__ int32_t s_idx[kSpmmCAP];
-    __shared__ double s_val[kSpmmCAP];
-    __shared__ int64_t s_perm[MODE == SP_FUSED_T ? kSpmmCAP : 1];
-
     const int tid = threadIdx.x, g = tid / G, lane = tid % G;
-    const int64_t r0 = (int64_t)blockIdx.x * RT;
-    const int nr = (int)(a.nrows - r0 < RT ? a.nrows - r0 : RT);
-    for (int i = tid; i <= nr; i += kSpmmTPB) s_ptr[i] = a.indptr[r0 + i];
-    __syncthreads();
-    const int64_t base = s_ptr[0];
-    const int64_t tnz = s_ptr[nr] - base;
-    const int staged = (int)(tnz < kSpmmCAP ? tnz : kSpmmCAP);
-    for (int e = tid; e < staged; e += kSpmmTPB) {
-        const int64_t p = base + e;
-        s_idx[e] = a.indices[p];
-        if (MODE != SP_SDDMM) {
-            const int64_t pv = PERM ? a.perm[p] : p;
-            s_val[e] = (double)a.vals[pv];
-            if (MODE == SP_FUSED_T) s_perm[e] = pv;
-        }
-    }
-    __syncthreads();
-
-    // nonzero e of the tile (relative to base): staged in shared memory or read from global
-    auto idx_of = [&](int64_t e) -> int32_t { return e < staged ? s_idx[e] : a.indices[base + e]; };
-    auto val_of = [&](int64_t e) -> double {
-        return e < staged ? s_val[e] : (double)a.vals[PERM ? a.perm[base + e] : base + e];
+    const int64_t rowbytes = a.ldx * (int64_t)sizeof(T);
+    auto off_of = [&](int64_t e) -> int64_t {
+        if constexpr (STAGED) return s_off[e];
+        else return (int64_t)(uint32_t)a.indices[base + e] * rowbytes;
     };
-    auto perm_of = [&](int64_t e) -> int64_t { return e < staged ? s_perm[e] : a.perm[base + e]; };
-
+    auto val_of = [&](int64_t e) -> double {
+        if constexpr (STAGED) return s_val[e];
+        else return (double)a.vals[PERM ? a.perm[base + e] : base + e];
+    };
+    auto perm_of = [&](int64_t e) -> int64_t {
+        if constexpr (STAGED) return s_perm[e];
+        else return a.perm[base + e];
+    };
     const int64_t stride = (int64_t)G * W;
     const int npass = (int)((a.k + stride - 1) / stride);
 
@@ -140,22 +145,22 @@ __global__ __launch_bounds__(kSpmmTPB) void k_spmm(SpmmArgs<T> a)
         const int rl = g + j * NG;   // adjacent groups take adjacent rows
         const bool valid = rl < nr;
         const int64_t row = r0 + rl;
-        const int64_t s = valid ? s_ptr[rl] - base : 0, e = valid ? s_ptr[rl + 1] - base : 0;
+        const int s = valid ? (int)(s_ptr[rl] - base) : 0, e = valid ? (int)(s_ptr[rl + 1] - base) : 0;
         if (MODE == SP_SDDMM || MODE == SP_FUSED_T) {
             // warp-uniform trip count: the group reductions below shuffle across the warp
-            const int len = (int)(e - s);
+            const int len = e - s;
             const int maxlen = (int)__reduce_max_sync(0xffffffffu, (unsigned)len);
             if (!__any_sync(0xffffffffu, valid)) break;
             if (MODE == SP_SDDMM) {
                 for (int t = 0; t < maxlen; ++t) {
                     const bool on = t < len;
-                    const int32_t c = on ? idx_of(s + t) : 0;
+                    const int64_t off = on ? off_of(s + t) : 0;
                     double dot = 0.0;
                     for (int ps = 0; ps < npass; ++ps) {
                         const int64_t col = ps * stride + (int64_t)lane * W;
                         if (on && col < a.k) {
                             double xv[W], wv[W];
-                            ldw<T, W>(a.X + (int64_t)c * a.ldx + col, xv);
+                            ldw<T, W>(reinterpret_cast<const T *>(reinterpret_cast<const char *>(a.X + col) + off), xv);
                             ldw<T, W>(a.W + row * a.ldw + col, wv);
 #pragma unroll
                             for (int i = 0; i < W; ++i) dot = fma(wv[i], xv[i], dot);
@@ -173,10 +178,11 @@ __global__ __launch_bounds__(kSpmmTPB) void k_spmm(SpmmArgs<T> a)
                     for (int i = 0; i < W; ++i) { xj[ps][i] = 0.0; acc[ps][i] = 0.0; }
                     if (valid && ps < npass && col < a.k) ldw<T, W>(a.W + row * a.ldw + col, xj[ps]);
                 }
+                const char *Xl = reinterpret_cast<const char *>(a.X + (int64_t)lane * W);
 #pragma unroll 2
                 for (int t = 0; t < maxlen; ++t) {
                     const bool on = t < len;
-                    const int32_t i_row = on ? idx_of(s + t) : 0;
+                    const int64_t off = on ? off_of(s + t) : 0;
                     const double av = on ? val_of(s + t) : 0.0;
                     double dot = 0.0;
 #pragma unroll
@@ -184,7 +190,7 @@ __global__ __launch_bounds__(kSpmmTPB) void k_spmm(SpmmArgs<T> a)
                         const int64_t col = ps * stride + (int64_t)lane * W;
                         if (on && ps < npass && col < a.k) {
                             double gv[W];
-                            ldw<T, W>(a.X + (int64_t)i_row * a.ldx + col, gv);
+                            ldw<T, W>(reinterpret_cast<const T *>(Xl + off) + ps * stride, gv);
 #pragma unroll
                             for (int i = 0; i < W; ++i) {
                                 acc[ps][i] = fma(av, gv[i], acc[ps][i]);
@@ -204,29 +210,61 @@ __global__ __launch_bounds__(kSpmmTPB) void k_spmm(SpmmArgs<T> a)
             continue;
         }
         if (!valid) break;
-
-        if (MODE == SP_FWD || MODE == SP_FWD_PERM) {
-            for (int ps = 0; ps < npass; ++ps) {
-                const int64_t col = ps * stride + (int64_t)lane * W;
-                const bool act = col < a.k;
-                double acc[W];
+        // FWD / FWD_PERM
+        for (int ps = 0; ps < npass; ++ps) {
+            const int64_t col = ps * stride + (int64_t)lane * W;
+            if (col >= a.k) break;
+            double acc[W];
 #pragma unroll
-                for (int i = 0; i < W; ++i) acc[i] = 0.0;
-                if (act) {
-                    const T *Xc = a.X + col;
+            for (int i = 0; i < W; ++i) acc[i] = 0.0;
+            const char *Xc = reinterpret_cast<const char *>(a.X + col);
 #pragma unroll 4
-                    for (int64_t q = s; q < e; ++q) {
-                        const double av = val_of(q);
-                        double xv[W];
-                        ldw<T, W>(Xc + (int64_t)idx_of(q) * a.ldx, xv);
+            for (int q = s; q < e; ++q) {
+                const double av = val_of(q);
+                double xv[W];
+                ldw<T, W>(reinterpret_cast<const T *>(Xc + off_of(q)), xv);
 #pragma unroll
-                        for (int i = 0; i < W; ++i) acc[i] = fma(av, xv[i], acc[i]);
-                    }
-                    stw<T, W>(a.Y + row * a.ldy + col, acc);
-                }
+                for (int i = 0; i < W; ++i) acc[i] = fma(av, xv[i], acc[i]);
             }
+            stw<T, W>(a.Y + row * a.ldy + col, acc);
         }
     }
+}
+
+template <typename T, int G, int W, int MODE>
+__global__ __launch_bounds__(kSpmmTPB, MODE == SP_FUSED_T ? 4 : 5) void k_spmm(SpmmArgs<T> a)
+{
+    constexpr int NG = kSpmmTPB / G;           // groups per CTA
+    constexpr int RT = NG * kSpmmRPG;          // rows per tile
+    constexpr bool PERM = MODE == SP_FWD_PERM || MODE == SP_FUSED_T;
+    __shared__ int64_t s_ptr[RT + 1];
+    __shared__ int64_t s_off[kSpmmCAP];
+    __shared__ double s_val[MODE == SP_SDDMM ? 1 : kSpmmCAP];
+    __shared__ int64_t s_perm[MODE == SP_FUSED_T ? kSpmmCAP : 1];
+
+    const int tid = threadIdx.x;
+    const int64_t r0 = (int64_t)blockIdx.x * RT;
+    const int nr = (int)(a.nrows - r0 < RT ? a.nrows - r0 : RT);
+    for (int i = tid; i <= nr; i += kSpmmTPB) s_ptr[i] = a.indptr[r0 + i];
+    __syncthreads();
+    const int64_t base = s_ptr[0];
+    const int64_t tnz = s_ptr[nr] - base;
+    if (tnz > kSpmmCAP) {   // tile-uniform: nonzeros read from global memory
+        spmm_rows<T, G, W, MODE, false>(a, s_ptr, s_off, s_val, s_perm, r0, nr, base);
+        return;
+    }
+    const int64_t rowbytes = a.ldx * (int64_t)sizeof(T);
+    for (int e = tid; e < (int)tnz; e += kSpmmTPB) {
+        const int64_t p = base + e;
+        s_off[e] = (int64_t)(uint32_t)a.indices[p] * rowbytes;
+        if (MODE != SP_SDDMM) {
+            const int64_t pv = PERM ? a.perm[p] : p;
+            s_val[e] = (double)a.vals[pv];
+            if (MODE == SP_FUSED_T) s_perm[e] = pv;
+        }
+    }
+    __syncthreads();
+    spmm_rows<T, G, W, MODE, true>(a, s_ptr, s_off, s_val, s_perm, r0, nr, base);
 }
 
 template <typename T, int G, int W, int MODE>
