@@ -172,7 +172,8 @@ class Workload:
         ck.spmv_fwd(self.A, self.x, out=self.y)
         rec("spmv_fwd", 1)
         rec("spmv_bwd", 0)
-        ck.spmv_bwd(self.A, self.x, self.dy, plan=self.plan, dA=self.dA_v, dx=self.dx)
+        # atomic scatter for dx: measured faster than the transpose-plan gather here
+        ck.spmv_bwd(self.A, self.x, self.dy, dA=self.dA_v, dx=self.dx)
         rec("spmv_bwd", 1)
         rec("spmm_fwd", 0)
         ck.spmm_fwd(self.A, self.X, out=self.Y)

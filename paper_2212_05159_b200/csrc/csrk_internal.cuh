@@ -95,4 +95,8 @@ int transpose_impl(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int6
 
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Tuning knob read once from the environment (CSRK_<name>), default `def`.  Used to A/B
+// kernel variants on the GPU box; the defaults are the measured-best choices.
+int knob(const char *name, int def);
+
 }  // namespace csrk

@@ -115,12 +115,15 @@ __global__ __launch_bounds__(kSTPB) void k_gemm_S(int64_t m, const int64_t *__re
                                                   const T *__restrict__ Bv, int64_t *__restrict__ Cp,
                                                   int32_t *__restrict__ Ci, T *__restrict__ Cv,
                                                   const T *__restrict__ dC, T *__restrict__ dA, T *__restrict__ dB,
-                                                  BigList big)
+                                                  BigList big, int use_stage)
 {
+    // per-warp staging buffers in dynamic shared memory (none when use_stage == 0, which
+    // leaves the whole carve-out to L1 for the merge's list reads)
     constexpr int BUFB = (PH == PH_FILL) ? (int)sizeof(int32_t) * kSBuf : (int)sizeof(T) * kSBuf;
-    __shared__ __align__(16) unsigned char s_buf[kSWarps][PH == PH_COUNT ? 16 : BUFB];
-    __shared__ T s_dA[kSWarps][PH == PH_BWD ? kSBufA : 1];
+    extern __shared__ __align__(16) unsigned char s_dyn[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char *s_buf_w = s_dyn + (size_t)warp * BUFB;
+    T *s_dA_w = reinterpret_cast<T *>(s_dyn + (size_t)kSWarps * BUFB) + warp * kSBufA;
     const int64_t i0 = (int64_t)blockIdx.x * kSTPB + warp * 32;   // first row of this warp
     const int64_t i = i0 + lane;
     const bool valid = i < m;
@@ -152,7 +155,7 @@ __global__ __launch_bounds__(kSTPB) void k_gemm_S(int64_t m, const int64_t *__re
     bool stage = false;
     int64_t c_lo = 0, a_lo = 0;
     if (PH != PH_COUNT) {
-        stage = __all_sync(0xffffffffu, !valid || isS) && i0 < m;
+        stage = use_stage && __all_sync(0xffffffffu, !valid || isS) && i0 < m;
         if (stage) {
             c_lo = Cp[i0];
             stage = Cp[iend] - c_lo <= kSBuf;
@@ -160,8 +163,8 @@ __global__ __launch_bounds__(kSTPB) void k_gemm_S(int64_t m, const int64_t *__re
         }
     }
     const int64_t c_hi = stage ? Cp[iend] : 0;
-    T *sv = reinterpret_cast<T *>(s_buf[warp]);
-    int32_t *si = reinterpret_cast<int32_t *>(s_buf[warp]);
+    T *sv = reinterpret_cast<T *>(s_buf_w);
+    int32_t *si = reinterpret_cast<int32_t *>(s_buf_w);
     if (PH == PH_BWD && stage) {
         for (int64_t e = c_lo + lane; e < c_hi; e += 32) sv[e - c_lo] = dC[e];
         __syncwarp();
@@ -171,7 +174,7 @@ __global__ __launch_bounds__(kSTPB) void k_gemm_S(int64_t m, const int64_t *__re
         int32_t *outI = PH == PH_FILL ? (stage ? si + (cs - c_lo) : Ci + cs) : nullptr;
         T *outV = PH == PH_NUM ? (stage ? sv + (cs - c_lo) : Cv + cs) : nullptr;
         const T *dCrow = PH == PH_BWD ? (stage ? sv + (cs - c_lo) : dC + cs) : nullptr;
-        T *dArow = (PH == PH_BWD && dA) ? (stage ? &s_dA[warp][as - a_lo] : dA + as) : nullptr;
+        T *dArow = (PH == PH_BWD && dA) ? (stage ? s_dA_w + (as - a_lo) : dA + as) : nullptr;
         int64_t cnt = 0;
         switch (Lw) {
         case 1: cnt = s_merge<T, PH, 1>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
@@ -194,7 +197,7 @@ __global__ __launch_bounds__(kSTPB) void k_gemm_S(int64_t m, const int64_t *__re
             for (int64_t e = c_lo + lane; e < c_hi; e += 32) Cv[e] = sv[e - c_lo];
         if (PH == PH_BWD && dA) {
             const int64_t a_hi = Ap[iend];
-            for (int64_t e = a_lo + lane; e < a_hi; e += 32) dA[e] = s_dA[warp][e - a_lo];
+            for (int64_t e = a_lo + lane; e < a_hi; e += 32) dA[e] = s_dA_w[e - a_lo];
         }
     }
 }
@@ -457,6 +460,22 @@ static int set_smem_attrs()
     return CSRK_OK;
 }
 
+// Dynamic shared memory of k_gemm_S: the per-warp output staging (knob GEMM_STAGE, default on).
+template <typename T>
+static size_t s_smem(int PH, int use)
+{
+    if (!use || PH == PH_COUNT) return 0;
+    size_t b = (size_t)kSWarps * kSBuf * (PH == PH_FILL ? sizeof(int32_t) : sizeof(T));
+    if (PH == PH_BWD) b += (size_t)kSWarps * kSBufA * sizeof(T);
+    return b;
+}
+
+// Staging pays for the symbolic fill (4-byte scattered stores); for numeric / backward the
+// shared memory is worth more as L1 for the merge's list reads (measured: 388 vs 436 us and
+// 677 vs 802 us on config 2).
+static int stage_fill() { static int v = knob("GEMM_STAGE_FILL", 1); return v; }
+static int stage_vals() { static int v = knob("GEMM_STAGE_VALS", 0); return v; }
+
 static void carve_big(const csrk_pattern &A, BigList &b, Bump &ws)
 {
     b.rows = ws.take<int32_t>(A.nrows > 0 ? A.nrows : 1);
@@ -478,7 +497,7 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, i
             CSRK_CUDA(cudaMemsetAsync(b.count, 0, sizeof(int), s));
             CSRK_LAUNCH((k_gemm_S<double, PH_COUNT>), gS, kSTPB, 0, s, m, A.indptr, A.indices,
                         (const double *)nullptr, B.indptr, B.indices, (const double *)nullptr, Cp, (int32_t *)nullptr,
-                        (double *)nullptr, (const double *)nullptr, (double *)nullptr, (double *)nullptr, b);
+                        (double *)nullptr, (const double *)nullptr, (double *)nullptr, (double *)nullptr, b, 0);
             CSRK_LAUNCH(k_gemm_big_sym<PH_COUNT>, big_grid(), kGemmTPB, big_sym_smem(), s, b, B.ncols, A.indptr,
                         A.indices, B.indptr, B.indices, Cp, (int32_t *)nullptr);
             CSRK_TRY(scan_counts_i64(Cp, m, ws, s));
@@ -489,9 +508,9 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, i
     }
     if (m == 0) return CSRK_OK;
     CSRK_CUDA(cudaMemsetAsync(b.count, 0, sizeof(int), s));
-    CSRK_LAUNCH((k_gemm_S<double, PH_FILL>), gS, kSTPB, 0, s, m, A.indptr, A.indices, (const double *)nullptr,
-                B.indptr, B.indices, (const double *)nullptr, Cp, Ci, (double *)nullptr, (const double *)nullptr,
-                (double *)nullptr, (double *)nullptr, b);
+    CSRK_LAUNCH((k_gemm_S<double, PH_FILL>), gS, kSTPB, s_smem<double>(PH_FILL, stage_fill()), s, m, A.indptr,
+                A.indices, (const double *)nullptr, B.indptr, B.indices, (const double *)nullptr, Cp, Ci,
+                (double *)nullptr, (const double *)nullptr, (double *)nullptr, (double *)nullptr, b, stage_fill());
     CSRK_LAUNCH(k_gemm_big_sym<PH_FILL>, big_grid(), kGemmTPB, big_sym_smem(), s, b, B.ncols, A.indptr, A.indices,
                 B.indptr, B.indices, Cp, Ci);
     return CSRK_OK;
@@ -512,13 +531,14 @@ static int spgemm_values_t(int PH, const csrk_pattern &A, const T *Av, const csr
     const unsigned gS = (unsigned)cdiv(m, kSTPB);
     int64_t *Cp = const_cast<int64_t *>(C.indptr);
     if (PH == PH_NUM) {
-        CSRK_LAUNCH((k_gemm_S<T, PH_NUM>), gS, kSTPB, 0, s, m, A.indptr, A.indices, Av, B.indptr, B.indices, Bv, Cp,
-                    (int32_t *)nullptr, Cv, (const T *)nullptr, (T *)nullptr, (T *)nullptr, b);
+        CSRK_LAUNCH((k_gemm_S<T, PH_NUM>), gS, kSTPB, s_smem<T>(PH_NUM, stage_vals()), s, m, A.indptr, A.indices,
+                    Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, Cv, (const T *)nullptr, (T *)nullptr,
+                    (T *)nullptr, b, stage_vals());
         CSRK_LAUNCH((k_gemm_big_val<T, PH_NUM>), big_grid(), kGemmTPB, big_val_smem(), s, b, A.indptr, A.indices, Av,
                     B.indptr, B.indices, Bv, C.indptr, C.indices, Cv, (const T *)nullptr, (T *)nullptr, (T *)nullptr);
     } else {
-        CSRK_LAUNCH((k_gemm_S<T, PH_BWD>), gS, kSTPB, 0, s, m, A.indptr, A.indices, Av, B.indptr, B.indices, Bv, Cp,
-                    (int32_t *)nullptr, (T *)nullptr, dC, dA, dB, b);
+        CSRK_LAUNCH((k_gemm_S<T, PH_BWD>), gS, kSTPB, s_smem<T>(PH_BWD, stage_vals()), s, m, A.indptr, A.indices,
+                    Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, (T *)nullptr, dC, dA, dB, b, stage_vals());
         CSRK_LAUNCH((k_gemm_big_val<T, PH_BWD>), big_grid(), kGemmTPB, big_val_smem(), s, b, A.indptr, A.indices, Av,
                     B.indptr, B.indices, Bv, C.indptr, C.indices, (T *)nullptr, dC, dA, dB);
     }

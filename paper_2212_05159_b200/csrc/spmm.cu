@@ -1,19 +1,23 @@
 // spmm.cu -- SpDMM forward and backward (PAPER 3.1.3; Table 1).
 //
 // A CTA owns a tile of RT consecutive rows (of A, or of A^T for the transposed backward).
-// The tile's row pointers, column indices and values (for the transposed traversal: the
-// values gathered through perm, A[perm q], and perm itself) are staged in shared memory
-// with coalesced loads.  A group of G lanes then walks one row at a time; each lane owns W
-// consecutive columns of the k-wide dense rows (two 16-byte vectors when the rows are
-// aligned), so every gathered X / dY row is one coalesced G*W*sizeof(T)-byte transaction,
-// and the loop over a row's nonzeros is unrolled so its gathers are in flight together.
-// Accumulation is fp64 for both dtypes.
+// For each of the tile's nonzeros the byte offset of the dense row it gathers and its value
+// (for the transposed traversal: A[perm q], and perm q) are staged in shared memory with
+// coalesced loads.  A group of G = 8 lanes then walks one row at a time and accumulates the
+// k-wide dense rows in 32-column passes.  Lane map (vector path): in each pass lane l owns the
+// 16-byte chunks l and l + 8 of the 256-byte (fp64) pass, i.e. columns {2l, 2l+1, 16+2l, 17+2l},
+// or chunk l (fp32, 128-byte pass) -- so every load / store instruction of a group covers 128
+// contiguous bytes and each 32-byte sector crosses L1 once.  Accumulation is fp64.
 //
 //   FWD      Y[i,:]  = sum_p A[p] X[idx p,:]
 //   FWD_PERM same over the cached transpose, values A[perm q]      (dX = A^T dY)
 //   SDDMM    dA[p]   = <dY[i,:], X[idx p,:]>                        ((dY X^T)(.)mask(A))
 //   FUSED_T  row j of A^T: dX[j,:] = sum_q A[perm q] dY[i_q,:] and, from the same dY row,
 //            dA[perm q] = <dY[i_q,:], X[j,:]>  -- both gradients in one pass.
+// Rows that are not 16-byte aligned / k not a multiple of 4 use the scalar map (G = 32 lanes x
+// 1 column).  An experimental TMA bulk-gather forward (cp.async.bulk into shared memory) is
+// kept behind CSRK_SPMM_BULK=1; it measured slower.
+#include "async.cuh"
 #include "ops.cuh"
 
 namespace csrk {
@@ -37,54 +41,58 @@ struct SpmmArgs {
 constexpr int kSpmmTPB = 256;
 constexpr int kSpmmRPG = 4;        // rows per group per tile
 constexpr int kSpmmCAP = 1536;     // staged nonzeros per tile
+constexpr int kPass = 32;          // columns per pass (both maps)
 constexpr int kFusedMaxPasses = 2;
 
-// W consecutive elements of T, as fp64.
-template <typename T, int W>
-__device__ __forceinline__ void ldw(const T *p, double (&r)[W])
+// ---------------------------------------------------------------- lane maps
+// Vector map (G = 8, W = 4 elements per lane per pass) or scalar map (G = 32, W = 1).
+template <typename T, int G, int W>
+struct LaneMap {
+    static constexpr int E = W == 1 ? 1 : 16 / (int)sizeof(T);   // elements per chunk
+    static constexpr int NCH = W / E;                             // chunks per lane
+    // column (within a pass) of chunk ch of lane l
+    __device__ static int col(int l, int ch) { return (l + ch * G) * E; }
+};
+
+// Load lane l's W elements of a pass starting at p (kleft = columns left in the row).
+template <typename T, int G, int W>
+__device__ __forceinline__ void ldl(const T *p, int l, int64_t kleft, double (&r)[W])
 {
-    if constexpr (W * sizeof(T) == 32) {
-        using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
-        constexpr int E = 16 / sizeof(T);
-        V a = __ldg(reinterpret_cast<const V *>(p));
-        V b = __ldg(reinterpret_cast<const V *>(p) + 1);
-        const T *ea = reinterpret_cast<const T *>(&a), *eb = reinterpret_cast<const T *>(&b);
+    using M = LaneMap<T, G, W>;
 #pragma unroll
-        for (int i = 0; i < E; ++i) { r[i] = (double)ea[i]; r[E + i] = (double)eb[i]; }
-    } else if constexpr (W * sizeof(T) == 16) {
-        using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
-        V a = __ldg(reinterpret_cast<const V *>(p));
-        const T *ea = reinterpret_cast<const T *>(&a);
-#pragma unroll
-        for (int i = 0; i < W; ++i) r[i] = (double)ea[i];
-    } else {
-#pragma unroll
-        for (int i = 0; i < W; ++i) r[i] = (double)__ldg(p + i);
+    for (int ch = 0; ch < M::NCH; ++ch) {
+        const int c = M::col(l, ch);
+        if constexpr (M::E == 1) {
+            r[ch] = c < kleft ? (double)__ldg(p + c) : 0.0;
+        } else if constexpr (sizeof(T) == 8) {
+            double2 v = make_double2(0.0, 0.0);
+            if (c < kleft) v = __ldg(reinterpret_cast<const double2 *>(p + c));
+            r[ch * 2] = v.x;
+            r[ch * 2 + 1] = v.y;
+        } else {
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (c < kleft) v = __ldg(reinterpret_cast<const float4 *>(p + c));
+            r[ch * 4] = v.x; r[ch * 4 + 1] = v.y; r[ch * 4 + 2] = v.z; r[ch * 4 + 3] = v.w;
+        }
     }
 }
 
-template <typename T, int W>
-__device__ __forceinline__ void stw(T *p, const double (&r)[W])
+template <typename T, int G, int W>
+__device__ __forceinline__ void stl(T *p, int l, int64_t kleft, const double (&r)[W])
 {
-    if constexpr (W * sizeof(T) == 32) {
-        using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
-        constexpr int E = 16 / sizeof(T);
-        V a, b;
-        T *ea = reinterpret_cast<T *>(&a), *eb = reinterpret_cast<T *>(&b);
+    using M = LaneMap<T, G, W>;
 #pragma unroll
-        for (int i = 0; i < E; ++i) { ea[i] = (T)r[i]; eb[i] = (T)r[E + i]; }
-        reinterpret_cast<V *>(p)[0] = a;
-        reinterpret_cast<V *>(p)[1] = b;
-    } else if constexpr (W * sizeof(T) == 16) {
-        using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
-        V a;
-        T *ea = reinterpret_cast<T *>(&a);
-#pragma unroll
-        for (int i = 0; i < W; ++i) ea[i] = (T)r[i];
-        *reinterpret_cast<V *>(p) = a;
-    } else {
-#pragma unroll
-        for (int i = 0; i < W; ++i) p[i] = (T)r[i];
+    for (int ch = 0; ch < M::NCH; ++ch) {
+        const int c = M::col(l, ch);
+        if (c >= kleft) continue;
+        if constexpr (M::E == 1) {
+            p[c] = (T)r[ch];
+        } else if constexpr (sizeof(T) == 8) {
+            *reinterpret_cast<double2 *>(p + c) = make_double2(r[ch * 2], r[ch * 2 + 1]);
+        } else {
+            *reinterpret_cast<float4 *>(p + c) =
+                make_float4((float)r[ch * 4], (float)r[ch * 4 + 1], (float)r[ch * 4 + 2], (float)r[ch * 4 + 3]);
+        }
     }
 }
 
@@ -96,25 +104,7 @@ __device__ __forceinline__ double group_sum(double v)
     return v;
 }
 
-// Reduce four per-lane values d[0..3] across a group of G (>= 4) lanes at once ("transpose
-// reduce"): the first two butterfly steps exchange halves of the vector, the rest reduce one
-// value.  Lane l ends with the group sum of d[v], v = l / (G/4).  8 shuffles for G = 8
-// instead of 4 x 6 for four separate reductions.
-template <int G>
-__device__ __forceinline__ double group_sum4(const double (&d)[4], int lane)
-{
-    constexpr int o1 = G >> 1, o2 = G >> 2;
-    const bool lo1 = (lane & o1) == 0;
-    const double s0 = lo1 ? d[2] : d[0], s1 = lo1 ? d[3] : d[1];
-    const double k0 = (lo1 ? d[0] : d[2]) + __shfl_xor_sync(0xffffffffu, s0, o1, G);
-    const double k1 = (lo1 ? d[1] : d[3]) + __shfl_xor_sync(0xffffffffu, s1, o1, G);
-    const bool lo2 = (lane & o2) == 0;
-    double v = (lo2 ? k0 : k1) + __shfl_xor_sync(0xffffffffu, lo2 ? k1 : k0, o2, G);
-#pragma unroll
-    for (int o = o2 >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, G);
-    return v;
-}
-
+// ---------------------------------------------------------------- tile kernel
 // Rows [r0, r0 + nr) of a tile.  STAGED: the tile's nonzeros are in shared memory as
 // (byte offset of the gathered row, value[, perm]); otherwise they are read from global.
 template <typename T, int G, int W, int MODE, bool STAGED>
@@ -138,8 +128,8 @@ __device__ __forceinline__ void spmm_rows(const SpmmArgs<T> &a, const int64_t *s
         if constexpr (STAGED) return s_perm[e];
         else return a.perm[base + e];
     };
-    const int64_t stride = (int64_t)G * W;
-    const int npass = (int)((a.k + stride - 1) / stride);
+    const int npass = (int)((a.k + kPass - 1) / kPass);
+    const char *Xb = reinterpret_cast<const char *>(a.X);
 
     for (int j = 0; j < kSpmmRPG; ++j) {
         const int rl = g + j * NG;   // adjacent groups take adjacent rows
@@ -157,11 +147,11 @@ __device__ __forceinline__ void spmm_rows(const SpmmArgs<T> &a, const int64_t *s
                     const int64_t off = on ? off_of(s + t) : 0;
                     double dot = 0.0;
                     for (int ps = 0; ps < npass; ++ps) {
-                        const int64_t col = ps * stride + (int64_t)lane * W;
-                        if (on && col < a.k) {
+                        const int64_t pc = (int64_t)ps * kPass;
+                        if (on) {
                             double xv[W], wv[W];
-                            ldw<T, W>(reinterpret_cast<const T *>(reinterpret_cast<const char *>(a.X + col) + off), xv);
-                            ldw<T, W>(a.W + row * a.ldw + col, wv);
+                            ldl<T, G, W>(reinterpret_cast<const T *>(Xb + off) + pc, lane, a.k - pc, xv);
+                            ldl<T, G, W>(a.W + row * a.ldw + pc, lane, a.k - pc, wv);
 #pragma unroll
                             for (int i = 0; i < W; ++i) dot = fma(wv[i], xv[i], dot);
                         }
@@ -173,12 +163,11 @@ __device__ __forceinline__ void spmm_rows(const SpmmArgs<T> &a, const int64_t *s
                 double xj[kFusedMaxPasses][W], acc[kFusedMaxPasses][W];
 #pragma unroll
                 for (int ps = 0; ps < kFusedMaxPasses; ++ps) {
-                    const int64_t col = ps * stride + (int64_t)lane * W;
 #pragma unroll
                     for (int i = 0; i < W; ++i) { xj[ps][i] = 0.0; acc[ps][i] = 0.0; }
-                    if (valid && ps < npass && col < a.k) ldw<T, W>(a.W + row * a.ldw + col, xj[ps]);
+                    if (valid && ps < npass)
+                        ldl<T, G, W>(a.W + row * a.ldw + (int64_t)ps * kPass, lane, a.k - (int64_t)ps * kPass, xj[ps]);
                 }
-                const char *Xl = reinterpret_cast<const char *>(a.X + (int64_t)lane * W);
 #pragma unroll 2
                 for (int t = 0; t < maxlen; ++t) {
                     const bool on = t < len;
@@ -187,10 +176,10 @@ __device__ __forceinline__ void spmm_rows(const SpmmArgs<T> &a, const int64_t *s
                     double dot = 0.0;
 #pragma unroll
                     for (int ps = 0; ps < kFusedMaxPasses; ++ps) {
-                        const int64_t col = ps * stride + (int64_t)lane * W;
-                        if (on && ps < npass && col < a.k) {
+                        if (on && ps < npass) {
+                            const int64_t pc = (int64_t)ps * kPass;
                             double gv[W];
-                            ldw<T, W>(reinterpret_cast<const T *>(Xl + off) + ps * stride, gv);
+                            ldl<T, G, W>(reinterpret_cast<const T *>(Xb + off) + pc, lane, a.k - pc, gv);
 #pragma unroll
                             for (int i = 0; i < W; ++i) {
                                 acc[ps][i] = fma(av, gv[i], acc[ps][i]);
@@ -202,31 +191,29 @@ __device__ __forceinline__ void spmm_rows(const SpmmArgs<T> &a, const int64_t *s
                     if (on && a.D && lane == 0) a.D[perm_of(s + t)] = (T)dot;
                 }
 #pragma unroll
-                for (int ps = 0; ps < kFusedMaxPasses; ++ps) {
-                    const int64_t col = ps * stride + (int64_t)lane * W;
-                    if (valid && ps < npass && col < a.k) stw<T, W>(a.Y + row * a.ldy + col, acc[ps]);
-                }
+                for (int ps = 0; ps < kFusedMaxPasses; ++ps)
+                    if (valid && ps < npass)
+                        stl<T, G, W>(a.Y + row * a.ldy + (int64_t)ps * kPass, lane, a.k - (int64_t)ps * kPass, acc[ps]);
             }
             continue;
         }
         if (!valid) break;
         // FWD / FWD_PERM
         for (int ps = 0; ps < npass; ++ps) {
-            const int64_t col = ps * stride + (int64_t)lane * W;
-            if (col >= a.k) break;
+            const int64_t pc = (int64_t)ps * kPass;
             double acc[W];
 #pragma unroll
             for (int i = 0; i < W; ++i) acc[i] = 0.0;
-            const char *Xc = reinterpret_cast<const char *>(a.X + col);
+            const char *Xc = reinterpret_cast<const char *>(a.X + pc);
 #pragma unroll 4
             for (int q = s; q < e; ++q) {
                 const double av = val_of(q);
                 double xv[W];
-                ldw<T, W>(reinterpret_cast<const T *>(Xc + off_of(q)), xv);
+                ldl<T, G, W>(reinterpret_cast<const T *>(Xc + off_of(q)), lane, a.k - pc, xv);
 #pragma unroll
                 for (int i = 0; i < W; ++i) acc[i] = fma(av, xv[i], acc[i]);
             }
-            stw<T, W>(a.Y + row * a.ldy + col, acc);
+            stl<T, G, W>(a.Y + row * a.ldy + pc, lane, a.k - pc, acc);
         }
     }
 }
@@ -276,8 +263,86 @@ static int launch_spmm(const SpmmArgs<T> &a, cudaStream_t s)
     return CSRK_OK;
 }
 
-// Vector path: each lane owns 4 consecutive columns (16 or 32 bytes; 8 lanes cover 32 columns);
-// needs 16-byte aligned row starts and k a multiple of 4.  Otherwise the scalar path (32 x 1).
+// ---------------------------------------------------------------- experimental TMA bulk gather
+// One CTA = 32 rows.  Every nonzero's gathered dense row (k*sizeof(T) bytes, a multiple of 16)
+// is fetched into shared memory by a 1D bulk copy (cp.async.bulk) completing on one mbarrier;
+// the 8-lane groups then accumulate from shared memory.  Off by default (slower).
+constexpr int kBulkTPB = 256;
+constexpr int kBulkG = 8;
+constexpr int kBulkRT = kBulkTPB / kBulkG;
+constexpr int kBulkBytes = 40 * 1024;
+
+template <typename T>
+__global__ __launch_bounds__(kBulkTPB) void k_spmm_bulk(SpmmArgs<T> a, int cap)
+{
+    constexpr int W = 4;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ int64_t s_ptr[kBulkRT + 1];
+    __shared__ __align__(8) uint64_t bar;
+    const int rb = (int)(a.k * (int64_t)sizeof(T));
+    unsigned char *s_g = smem;
+    double *s_val = reinterpret_cast<double *>(smem + (size_t)cap * rb);
+    const int tid = threadIdx.x, g = tid / kBulkG, lane = tid % kBulkG;
+    const int64_t r0 = (int64_t)blockIdx.x * kBulkRT;
+    const int nr = (int)(a.nrows - r0 < kBulkRT ? a.nrows - r0 : kBulkRT);
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        mbar_fence_init();
+    }
+    for (int i = tid; i <= nr; i += kBulkTPB) s_ptr[i] = a.indptr[r0 + i];
+    __syncthreads();
+    const int64_t base = s_ptr[0];
+    const int64_t tnz = s_ptr[nr] - base;
+    const bool fits = tnz <= cap;
+    if (fits) {
+        if (tid == 0) mbar_arrive_expect_tx(&bar, (uint32_t)(tnz * rb));
+        __syncthreads();
+        const char *Xb = reinterpret_cast<const char *>(a.X);
+        const int64_t ldb = a.ldx * (int64_t)sizeof(T);
+        for (int e = tid; e < (int)tnz; e += kBulkTPB) {
+            const int64_t p = base + e;
+            bulk_g2s(s_g + (size_t)e * rb, Xb + (int64_t)(uint32_t)a.indices[p] * ldb, (uint32_t)rb, &bar);
+            s_val[e] = (double)a.vals[p];
+        }
+        __syncthreads();
+        mbar_wait(&bar, 0);
+    }
+    if (g >= nr) return;
+    const int64_t row = r0 + g;
+    const int64_t s = s_ptr[g] - base, e = s_ptr[g + 1] - base;
+    for (int64_t pc = 0; pc < a.k; pc += kPass) {
+        double acc[W] = {0.0, 0.0, 0.0, 0.0};
+        for (int64_t q = s; q < e; ++q) {
+            double xv[W];
+            const T *src = fits ? reinterpret_cast<const T *>(s_g + (size_t)q * rb) + pc
+                                : a.X + (int64_t)a.indices[base + q] * a.ldx + pc;
+            const double av = fits ? s_val[q] : (double)a.vals[base + q];
+            ldl<T, kBulkG, W>(src, lane, a.k - pc, xv);
+#pragma unroll
+            for (int i = 0; i < W; ++i) acc[i] = fma(av, xv[i], acc[i]);
+        }
+        stl<T, kBulkG, W>(a.Y + row * a.ldy + pc, lane, a.k - pc, acc);
+    }
+}
+
+template <typename T>
+static int launch_spmm_bulk(const SpmmArgs<T> &a, cudaStream_t s)
+{
+    if (a.nrows <= 0) return CSRK_OK;
+    const int rb = (int)(a.k * (int64_t)sizeof(T));
+    const int cap = kBulkBytes / rb;
+    const size_t smem = (size_t)cap * rb + (size_t)cap * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        CSRK_CUDA(cudaFuncSetAttribute(k_spmm_bulk<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        attr = true;
+    }
+    CSRK_LAUNCH(k_spmm_bulk<T>, (unsigned)cdiv(a.nrows, kBulkRT), kBulkTPB, smem, s, a, cap);
+    return CSRK_OK;
+}
+
+// ---------------------------------------------------------------- dispatch
+// Vector map: 16-byte aligned row starts and k a multiple of 4.  Otherwise the scalar map.
 template <typename T>
 static bool vec_ok(int64_t k, std::initializer_list<std::pair<const void *, int64_t>> ops)
 {
@@ -303,7 +368,10 @@ static int spmm_fwd_t(const csrk_pattern &A, const T *A_val, int64_t k, const T 
     SpmmArgs<T> a{};
     a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices; a.vals = A_val;
     a.k = k; a.X = X; a.ldx = ldx; a.Y = Y; a.ldy = ldy;
-    return dispatch<T, SP_FWD>(vec_ok<T>(k, {{X, ldx}, {Y, ldy}}), a, s);
+    const bool vec = vec_ok<T>(k, {{X, ldx}, {Y, ldy}});
+    if (vec && knob("SPMM_BULK", 0) && (k * (int64_t)sizeof(T)) % 16 == 0 && k * (int64_t)sizeof(T) <= 1024)
+        return launch_spmm_bulk<T>(a, s);
+    return dispatch<T, SP_FWD>(vec, a, s);
 }
 
 template <typename T>
@@ -312,8 +380,7 @@ static int spmm_bwd_t(const csrk_pattern &A, const T *A_val, const csrk_pattern 
                       Bump &ws, cudaStream_t s)
 {
     const bool vec = vec_ok<T>(k, {{X, ldx}, {dY, lddy}, {dX, lddx}});
-    const int64_t stride = 32;  // columns per pass: 8 lanes x 4 (vector) or 32 lanes x 1
-    const int64_t np = cdiv(k, stride);
+    const int64_t np = cdiv(k, kPass);
     // Transpose plan: the caller's, or built in the workspace.
     csrk_pattern ATl{};
     const int64_t *permu = perm;
@@ -329,8 +396,8 @@ static int spmm_bwd_t(const csrk_pattern &A, const T *A_val, const csrk_pattern 
     if (ws.sizing() || k == 0) return CSRK_OK;
     SpmmArgs<T> a{};
     a.k = k; a.vals = A_val;
-    if (dX && np <= kFusedMaxPasses) {
-        // fused transposed traversal: dX and (optionally) dA in one pass
+    if (dX && dA && np <= kFusedMaxPasses) {
+        // fused transposed traversal: dX and dA in one pass
         a.nrows = AT->nrows; a.indptr = AT->indptr; a.indices = AT->indices; a.perm = permu;
         a.X = dY; a.ldx = lddy; a.W = X; a.ldw = ldx; a.Y = dX; a.ldy = lddx; a.D = dA;
         return dispatch<T, SP_FUSED_T>(vec, a, s);

@@ -1,4 +1,5 @@
 // utils.cu -- int64 prefix scan, optional pattern validation, launch counter.
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -7,6 +8,14 @@
 namespace csrk {
 
 std::atomic<uint64_t> g_launches{0};
+
+int knob(const char *name, int def)
+{
+    char key[96];
+    snprintf(key, sizeof(key), "CSRK_%s", name);
+    const char *v = getenv(key);
+    return v ? atoi(v) : def;
+}
 
 // ---------------------------------------------------------------- inclusive int64 scan
 // Three phases (tile sums, recursive scan of the sums, tile scan + offset).  A tile is
