@@ -43,13 +43,36 @@ struct BigList {
 };
 
 // ---------------------------------------------------------------- short rows: thread-per-row merge
-template <typename T, int PH, int L>
-__device__ __forceinline__ int64_t s_merge(int64_t as, int l, const int32_t *__restrict__ Ai,
-                                           const T *__restrict__ Av, const int64_t *__restrict__ Bp,
-                                           const int32_t *__restrict__ Bi, const T *__restrict__ Bv,
-                                           int32_t *outI, T *outV, const T *dCrow, T *dArow, T *__restrict__ dB)
+// Predicated loads (no branch): the merge step updates every list with selects so the warp
+// never diverges per list.
+__device__ __forceinline__ void ld_pred(int32_t &v, const int32_t *p, bool pred)
 {
-    int64_t cur[L];   // position in B of list t's head
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q ld.global.nc.b32 %0, [%1]; }"
+                 : "+r"(v) : "l"(p), "r"((int)pred));
+}
+__device__ __forceinline__ void ld_pred(double &v, const double *p, bool pred)
+{
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q ld.global.nc.f64 %0, [%1]; }"
+                 : "+d"(v) : "l"(p), "r"((int)pred));
+}
+__device__ __forceinline__ void ld_pred(double &v, const float *p, bool pred)
+{
+    float f = 0.f;
+    asm volatile("{ .reg .pred q; setp.ne.b32 q, %2, 0; @q ld.global.nc.f32 %0, [%1]; }"
+                 : "+f"(f) : "l"(p), "r"((int)pred));
+    if (pred) v = (double)f;
+}
+
+// Branchy merge: only the lists whose head matched advance (a divergent branch per list).
+// Measured best for the symbolic phases and the backward pass (fewer registers).
+template <typename T, int PH, int L>
+__device__ __forceinline__ int64_t s_merge_br(int64_t as, int l, const int32_t *__restrict__ Ai,
+                                              const T *__restrict__ Av, const int64_t *__restrict__ Bp,
+                                              const int32_t *__restrict__ Bi, const T *__restrict__ Bv,
+                                              int32_t *outI, T *outV, const T *dCrow, T *dArow,
+                                              T *__restrict__ dB)
+{
+    int64_t cur[L];
     int rem[L];
     int32_t head[L];
     double av[L], dacc[L];
@@ -64,16 +87,7 @@ __device__ __forceinline__ int64_t s_merge(int64_t as, int l, const int32_t *__r
             cur[t] = Bp[k];
             rem[t] = (int)(Bp[k + 1] - cur[t]);
             if (PH == PH_NUM || PH == PH_BWD) av[t] = (double)Av[as + t];
-            if (rem[t] > 0) {
-                // pull the list's index (and value) lines into L1: the merge then walks them
-                // with L1 latency instead of a dependent L2 round trip per step
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(Bi + cur[t] + rem[t] - 1));
-                if (PH == PH_NUM || PH == PH_BWD) {
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(Bv + cur[t]));
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(Bv + cur[t] + rem[t] - 1));
-                }
-                head[t] = Bi[cur[t]];
-            }
+            if (rem[t] > 0) head[t] = Bi[cur[t]];
         }
     }
     int64_t c = 0;
@@ -106,6 +120,85 @@ __device__ __forceinline__ int64_t s_merge(int64_t as, int l, const int32_t *__r
             if (t < l) dArow[t] = (T)dacc[t];
     }
     return c;
+}
+
+// Branch-free merge: every list is updated with selects and predicated loads each step, the
+// head's value cached in a register.  Measured best for the numeric phase.
+template <typename T, int PH, int L>
+__device__ __forceinline__ int64_t s_merge_bl(int64_t as, int l, const int32_t *__restrict__ Ai,
+                                              const T *__restrict__ Av, const int64_t *__restrict__ Bp,
+                                              const int32_t *__restrict__ Bi, const T *__restrict__ Bv,
+                                              int32_t *outI, T *outV, const T *dCrow, T *dArow,
+                                              T *__restrict__ dB)
+{
+    constexpr bool VAL = PH == PH_NUM || PH == PH_BWD;
+    int64_t cur[L];   // position in B of list t's head
+    int rem[L];       // entries left in list t including the head
+    int32_t head[L];  // column at the head (INT32_MAX when exhausted)
+    double hv[L];     // value at the head (VAL)
+    double av[L], dacc[L];
+#pragma unroll
+    for (int t = 0; t < L; ++t) {
+        rem[t] = 0;
+        head[t] = INT32_MAX;
+        cur[t] = 0;
+        hv[t] = av[t] = dacc[t] = 0.0;
+        if (t < l) {
+            const int32_t k = Ai[as + t];
+            cur[t] = Bp[k];
+            rem[t] = (int)(Bp[k + 1] - cur[t]);
+            if (VAL) av[t] = (double)Av[as + t];
+            if (rem[t] > 0) {
+                head[t] = Bi[cur[t]];
+                if (VAL) hv[t] = (double)Bv[cur[t]];
+            }
+        }
+    }
+    int64_t c = 0;
+    while (true) {
+        int32_t v = head[0];
+#pragma unroll
+        for (int t = 1; t < L; ++t) v = min(v, head[t]);
+        if (v == INT32_MAX) break;
+        double acc = 0.0;
+        const double g = PH == PH_BWD ? (double)dCrow[c] : 0.0;
+#pragma unroll
+        for (int t = 0; t < L; ++t) {
+            const bool mt = head[t] == v;
+            if (PH == PH_NUM) acc = fma(av[t], mt ? hv[t] : 0.0, acc);
+            if (PH == PH_BWD) {
+                dacc[t] = fma(g, mt ? hv[t] : 0.0, dacc[t]);
+                if (dB && mt) red_add(&dB[cur[t]], (T)(av[t] * g));
+            }
+            cur[t] += mt;
+            rem[t] -= mt;
+            const bool more = mt && rem[t] > 0;
+            ld_pred(head[t], Bi + cur[t], more);
+            if (VAL) ld_pred(hv[t], Bv + cur[t], more);
+            head[t] = (mt && !more) ? INT32_MAX : head[t];
+        }
+        if (PH == PH_FILL) outI[c] = v;
+        if (PH == PH_NUM) outV[c] = (T)acc;
+        ++c;
+    }
+    if (PH == PH_BWD && dArow) {
+#pragma unroll
+        for (int t = 0; t < L; ++t)
+            if (t < l) dArow[t] = (T)dacc[t];
+    }
+    return c;
+}
+
+template <typename T, int PH, int L>
+__device__ __forceinline__ int64_t s_merge(int64_t as, int l, const int32_t *__restrict__ Ai,
+                                           const T *__restrict__ Av, const int64_t *__restrict__ Bp,
+                                           const int32_t *__restrict__ Bi, const T *__restrict__ Bv,
+                                           int32_t *outI, T *outV, const T *dCrow, T *dArow, T *__restrict__ dB)
+{
+    if constexpr (PH == PH_NUM)
+        return s_merge_bl<T, PH, L>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB);
+    else
+        return s_merge_br<T, PH, L>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB);
 }
 
 template <typename T, int PH>
