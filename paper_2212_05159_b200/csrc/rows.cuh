@@ -1,0 +1,111 @@
+// rows.cuh -- thread-per-row CSR traversal with a warp-per-row pass for long rows.
+//
+// k_rows: one thread per row.  Rows of at most kShortRow nonzeros are processed by their
+// thread; the thread's index/value loads are contiguous, and across a warp the L1 serves the
+// neighbouring rows' lines, so short-row matrices (stencils) stream at near copy bandwidth
+// without staging or block synchronisation.  Longer rows are appended (warp-aggregated) to a
+// list that k_rows_long processes with one warp per row (coalesced over the row).
+// Modes (same semantics as tile.cuh):
+//   REDUCE    y[row] = sum_p val(pv) v[idx p]  (in p order -- the oracle's order -- for short
+//             rows; lane-strided + fixed shuffle tree for long rows; both deterministic)
+//             SIDE: D[pv] = v[idx p] * u[row]
+//   SCATTER   w = u[row]; SIDE: D[p] = w v[idx p]; y (nullable): y[idx p] += val[p] w (atomic)
+//   TRANSPOSE slot = cursor[idx p]++ (atomic); keys[slot] = (p << 31) | row
+#pragma once
+
+#include "csrk_internal.cuh"
+#include "tile.cuh"
+
+namespace csrk {
+
+constexpr int kShortRow = 32;
+constexpr int kRowsTPB = 256;
+
+struct RowList {
+    int32_t *rows;
+    int *count;
+};
+
+template <typename T, int MODE, bool PERM, bool SIDE>
+__device__ __forceinline__ void row_elem(const TileArgs<T> &a, int64_t row, int64_t p, double &acc)
+{
+    const int32_t c = a.indices[p];
+    if (MODE == MODE_REDUCE) {
+        const int64_t pv = PERM ? a.perm[p] : p;
+        const T vc = a.v[c];
+        acc = fma((double)a.vals[pv], (double)vc, acc);
+        if (SIDE) a.D[pv] = vc * a.u[row];
+    } else if (MODE == MODE_SCATTER) {
+        const T w = a.u[row];
+        if (SIDE) a.D[p] = w * a.v[c];
+        if (a.y) red_add(&a.y[c], (T)((double)a.vals[p] * (double)w));
+    } else {
+        const int64_t slot = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(&a.cursor[c]), 1ULL);
+        a.out_keys[slot] = ((uint64_t)p << 31) | (uint64_t)row;
+    }
+}
+
+template <typename T, int MODE, bool PERM, bool SIDE>
+__global__ __launch_bounds__(kRowsTPB) void k_rows(TileArgs<T> a, RowList L)
+{
+    const int64_t row = (int64_t)blockIdx.x * kRowsTPB + threadIdx.x;
+    const bool valid = row < a.nrows;
+    int64_t s = 0, e = 0;
+    if (valid) {
+        s = a.indptr[row];
+        e = a.indptr[row + 1];
+    }
+    const bool lng = valid && e - s > kShortRow;
+    const unsigned lm = __ballot_sync(0xffffffffu, lng);
+    if (lm) {
+        const int lane = threadIdx.x & 31;
+        int base = 0;
+        if (lane == 0) base = atomicAdd(L.count, __popc(lm));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (lng) L.rows[base + __popc(lm & ((1u << lane) - 1))] = (int32_t)row;
+    }
+    if (!valid || lng) return;
+    double acc = 0.0;
+#pragma unroll 4
+    for (int64_t p = s; p < e; ++p) row_elem<T, MODE, PERM, SIDE>(a, row, p, acc);
+    if (MODE == MODE_REDUCE) a.y[row] = (T)acc;
+}
+
+constexpr int kLongWarps = 8;
+
+template <typename T, int MODE, bool PERM, bool SIDE>
+__global__ __launch_bounds__(32 * kLongWarps) void k_rows_long(TileArgs<T> a, RowList L)
+{
+    const int n = *(volatile int *)L.count;
+    const int lane = threadIdx.x & 31;
+    for (int it = blockIdx.x * kLongWarps + (threadIdx.x >> 5); it < n; it += gridDim.x * kLongWarps) {
+        const int64_t row = L.rows[it];
+        const int64_t s = a.indptr[row], e = a.indptr[row + 1];
+        double acc = 0.0;
+        for (int64_t p = s + lane; p < e; p += 32) row_elem<T, MODE, PERM, SIDE>(a, row, p, acc);
+        if (MODE == MODE_REDUCE) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) a.y[row] = (T)acc;
+        }
+    }
+}
+
+// Workspace: the long-row list (int32 per row + a counter).
+inline void carve_rowlist(int64_t nrows, RowList &L, Bump &ws)
+{
+    L.rows = ws.take<int32_t>(nrows > 0 ? nrows : 1);
+    L.count = ws.take<int>(1);
+}
+
+template <typename T, int MODE, bool PERM, bool SIDE>
+int launch_rows(const TileArgs<T> &a, const RowList &L, cudaStream_t s)
+{
+    if (a.nrows <= 0) return CSRK_OK;
+    CSRK_CUDA(cudaMemsetAsync(L.count, 0, sizeof(int), s));
+    CSRK_LAUNCH((k_rows<T, MODE, PERM, SIDE>), (unsigned)cdiv(a.nrows, kRowsTPB), kRowsTPB, 0, s, a, L);
+    CSRK_LAUNCH((k_rows_long<T, MODE, PERM, SIDE>), (unsigned)(kNumSMs * 2), 32 * kLongWarps, 0, s, a, L);
+    return CSRK_OK;
+}
+
+}  // namespace csrk

@@ -1,13 +1,27 @@
 // spmv.cu -- SpMV forward and backward (PAPER 3.1.1; Table 1).
+//
+// Traversal: rows.cuh (thread per row, warp per long row) by default; the row-tile /
+// merge-path kernel of tile.cuh is kept behind CSRK_SPMV_TILE=1 (measured 135 vs 70 us for
+// the config-2 forward).
 #include "ops.cuh"
+#include "rows.cuh"
 #include "tile.cuh"
 
 namespace csrk {
+
+template <typename T, int MODE, bool PERM, bool SIDE>
+static int run(TileArgs<T> a, const RowList &L, cudaStream_t s)
+{
+    if (knob("SPMV_TILE", 0)) return launch_tile<T, MODE, PERM, SIDE>(a, s);
+    return launch_rows<T, MODE, PERM, SIDE>(a, L, s);
+}
 
 template <typename T>
 static int spmv_fwd_t(csrk_op op, const csrk_pattern &A, const T *A_val, const csrk_pattern *AT,
                       const int64_t *perm, const T *x, T *y, Bump &ws, cudaStream_t s)
 {
+    RowList L{};
+    carve_rowlist(A.nrows > A.ncols ? A.nrows : A.ncols, L, ws);
     if (ws.sizing()) return CSRK_OK;
     TileArgs<T> a{};
     if (op == CSRK_OP_N) {
@@ -15,27 +29,29 @@ static int spmv_fwd_t(csrk_op op, const csrk_pattern &A, const T *A_val, const c
         a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices;
         a.vals = A_val; a.v = x; a.y = y;
         a.R = tile_rows(A.nrows, A.nnz);
-        return launch_tile<T, MODE_REDUCE, false, false>(a, s);
+        return run<T, MODE_REDUCE, false, false>(a, L, s);
     }
     if (AT) {
         // y = A^T x as row inner products of the cached transpose, values gathered via perm
         a.nrows = AT->nrows; a.indptr = AT->indptr; a.indices = AT->indices;
         a.vals = A_val; a.perm = perm; a.v = x; a.y = y;
         a.R = tile_rows(AT->nrows, AT->nnz);
-        return launch_tile<T, MODE_REDUCE, true, false>(a, s);
+        return run<T, MODE_REDUCE, true, false>(a, L, s);
     }
     // y = A^T x by atomic scatter of A_ij x_i into y_j
     CSRK_CUDA(cudaMemsetAsync(y, 0, sizeof(T) * (size_t)A.ncols, s));
     a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices;
     a.vals = A_val; a.u = x; a.y = y;
     a.R = tile_rows(A.nrows, A.nnz);
-    return launch_tile<T, MODE_SCATTER, false, false>(a, s);
+    return run<T, MODE_SCATTER, false, false>(a, L, s);
 }
 
 template <typename T>
 static int spmv_bwd_t(csrk_op op, const csrk_pattern &A, const T *A_val, const csrk_pattern *AT,
                       const int64_t *perm, const T *x, const T *dy, T *dA, T *dx, Bump &ws, cudaStream_t s)
 {
+    RowList L{};
+    carve_rowlist(A.nrows > A.ncols ? A.nrows : A.ncols, L, ws);
     if (ws.sizing()) return CSRK_OK;
     TileArgs<T> a{};
     if (op == CSRK_OP_T) {
@@ -47,12 +63,12 @@ static int spmv_bwd_t(csrk_op op, const csrk_pattern &A, const T *A_val, const c
             a.y = dx;
             if (dA) {
                 a.D = dA;
-                return launch_tile<T, MODE_REDUCE, false, true>(a, s);
+                return run<T, MODE_REDUCE, false, true>(a, L, s);
             }
-            return launch_tile<T, MODE_REDUCE, false, false>(a, s);
+            return run<T, MODE_REDUCE, false, false>(a, L, s);
         }
         a.D = dA;  // dA only: scatter mode without the atomic output
-        return launch_tile<T, MODE_SCATTER, false, true>(a, s);
+        return run<T, MODE_SCATTER, false, true>(a, L, s);
     }
     // op N (y = A x)
     if (AT && dx) {
@@ -62,17 +78,17 @@ static int spmv_bwd_t(csrk_op op, const csrk_pattern &A, const T *A_val, const c
         a.R = tile_rows(AT->nrows, AT->nnz);
         if (dA) {
             a.D = dA;
-            return launch_tile<T, MODE_REDUCE, true, true>(a, s);
+            return run<T, MODE_REDUCE, true, true>(a, L, s);
         }
-        return launch_tile<T, MODE_REDUCE, true, false>(a, s);
+        return run<T, MODE_REDUCE, true, false>(a, L, s);
     }
     // row traversal: dA[p] = dy_i x[idx p] (coalesced), dx[idx p] += A[p] dy_i (atomic)
     if (dx) CSRK_CUDA(cudaMemsetAsync(dx, 0, sizeof(T) * (size_t)A.ncols, s));
     a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices;
     a.vals = A_val; a.u = dy; a.v = x; a.y = dx; a.D = dA;
     a.R = tile_rows(A.nrows, A.nnz);
-    if (dA) return launch_tile<T, MODE_SCATTER, false, true>(a, s);
-    return launch_tile<T, MODE_SCATTER, false, false>(a, s);
+    if (dA) return run<T, MODE_SCATTER, false, true>(a, L, s);
+    return run<T, MODE_SCATTER, false, false>(a, L, s);
 }
 
 int spmv_fwd(csrk_dtype dt, csrk_op op, const csrk_pattern &A, const void *A_val, const csrk_pattern *AT,

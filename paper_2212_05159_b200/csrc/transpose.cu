@@ -13,6 +13,7 @@
 //   5. AT_val[q] = A_val[perm[q]] (optional)
 // Packing needs nnz < 2^33 (checked).
 #include "ops.cuh"
+#include "rows.cuh"
 #include "tile.cuh"
 
 namespace csrk {
@@ -26,6 +27,7 @@ constexpr uint64_t kKeyPad = ~0ull;
 __device__ __forceinline__ int32_t key_row(uint64_t k) { return (int32_t)(k & 0x7fffffffull); }
 __device__ __forceinline__ int64_t key_pos(uint64_t k) { return (int64_t)(k >> 31); }
 
+// Column histogram (plain atomics: warp aggregation with __match_any_sync measured 2x slower).
 __global__ void k_col_count(int64_t nnz, const int32_t *__restrict__ indices, unsigned long long *__restrict__ cnt)
 {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x)
@@ -71,18 +73,65 @@ __device__ __forceinline__ void sort_unpack_regs(const uint64_t *__restrict__ ke
         }
 }
 
-// Columns of length <= 16 are sorted in registers by their own thread; longer ones queued.
-__global__ __launch_bounds__(256) void k_sort_short(int64_t n, const int64_t *__restrict__ ATp,
-                                                    const uint64_t *__restrict__ keys, int32_t *__restrict__ ATi,
-                                                    int64_t *__restrict__ perm, SortLists L)
+// Sort one short column held in shared memory (keys s[0..len)) in registers, in place.
+template <int N>
+__device__ __forceinline__ void sort_smem_regs(uint64_t *s, int len)
 {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t s = ATp[j], len = ATp[j + 1] - s;
+    uint64_t k[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) k[i] = i < len ? s[i] : kKeyPad;
+    reg_sort<N>(k);
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+        if (i < len) s[i] = k[i];
+}
+
+constexpr int kShortWarps = 8;
+constexpr int kShortBuf = 512;   // keys staged per warp
+
+// A warp owns 32 consecutive columns.  When they are all short (<= 16) and their keys fit the
+// warp's buffer, the keys are loaded coalesced into shared memory, each lane sorts its column
+// there with a register network, and the unpacked rows / positions are stored coalesced.
+// Otherwise each lane sorts its short column straight from global memory; longer columns are
+// queued for the warp / CTA / merge-sort kernels.
+__global__ __launch_bounds__(32 * kShortWarps) void k_sort_short(int64_t n, const int64_t *__restrict__ ATp,
+                                                                 const uint64_t *__restrict__ keys,
+                                                                 int32_t *__restrict__ ATi,
+                                                                 int64_t *__restrict__ perm, SortLists L)
+{
+    __shared__ uint64_t s_key[kShortWarps][kShortBuf];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t j0 = ((int64_t)blockIdx.x * kShortWarps + w) * 32; j0 < n;
+         j0 += (int64_t)gridDim.x * kShortWarps * 32) {
+        const int64_t j = j0 + lane;
+        const bool valid = j < n;
+        const int64_t s = valid ? ATp[j] : 0, e = valid ? ATp[j + 1] : 0;
+        const int len = (int)(e - s);
+        const int64_t lastj = (n - j0 < 32 ? n - j0 : 32) - 1;
+        const int64_t R0 = __shfl_sync(0xffffffffu, s, 0), R1 = __shfl_sync(0xffffffffu, e, (int)lastj);
+        const bool fast = __all_sync(0xffffffffu, len <= kRegMax) && R1 - R0 <= kShortBuf;
+        if (fast) {
+            const int span = (int)(R1 - R0);
+            for (int i = lane; i < span; i += 32) s_key[w][i] = keys[R0 + i];
+            __syncwarp();
+            if (len > 1) {
+                if (len <= 8) sort_smem_regs<8>(&s_key[w][s - R0], len);
+                else sort_smem_regs<16>(&s_key[w][s - R0], len);
+            }
+            __syncwarp();
+            for (int i = lane; i < span; i += 32) {
+                const uint64_t k = s_key[w][i];
+                ATi[R0 + i] = key_row(k);
+                perm[R0 + i] = key_pos(k);
+            }
+            __syncwarp();
+            continue;
+        }
         if (len == 0) continue;
         if (len <= 8) {
-            sort_unpack_regs<8>(keys, s, (int)len, ATi, perm);
+            sort_unpack_regs<8>(keys, s, len, ATi, perm);
         } else if (len <= kRegMax) {
-            sort_unpack_regs<16>(keys, s, (int)len, ATi, perm);
+            sort_unpack_regs<16>(keys, s, len, ATi, perm);
         } else if (len <= kWarpMax) {
             L.mid[atomicAdd(&L.count[0], 1)] = (int32_t)j;
         } else if (len <= kBlockMax) {
@@ -251,6 +300,8 @@ int transpose_impl(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int6
     L.huge = ws.take<int32_t>(nnz / (kBlockMax + 1) + 1);
     L.count = ws.take<int>(4);
     uint64_t *buf = ws.take<uint64_t>(nnz > kBlockMax ? nnz : 1);
+    RowList RL{};
+    carve_rowlist(A.nrows, RL, ws);
     if (ws.sizing()) return scan_counts_i64(nullptr, n, ws, s);  // carve the scan scratch
 
     CSRK_CUDA(cudaMemsetAsync(ATp, 0, sizeof(int64_t) * (size_t)(n + 1), s));
@@ -266,9 +317,11 @@ int transpose_impl(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int6
         a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices;
         a.cursor = cursor; a.out_keys = keys;
         a.R = tile_rows(A.nrows, nnz);
-        CSRK_TRY((launch_tile<double, MODE_TRANSPOSE, false, false>(a, s)));
+        if (knob("SPMV_TILE", 0)) CSRK_TRY((launch_tile<double, MODE_TRANSPOSE, false, false>(a, s)));
+        else CSRK_TRY((launch_rows<double, MODE_TRANSPOSE, false, false>(a, RL, s)));
     }
-    CSRK_LAUNCH(k_sort_short, grid_for(n, 256), 256, 0, s, n, (const int64_t *)ATp, (const uint64_t *)keys, ATi, pm, L);
+    CSRK_LAUNCH(k_sort_short, grid_for(cdiv(n, 32) * 32, 32 * kShortWarps), 32 * kShortWarps, 0, s, n,
+                (const int64_t *)ATp, (const uint64_t *)keys, ATi, pm, L);
     if (nnz > kRegMax)
         CSRK_LAUNCH(k_sort_warp, (unsigned)(kNumSMs * 4), 32 * kWarpsPerSortCTA, 0, s, (const int64_t *)ATp,
                     (const uint64_t *)keys, ATi, pm, L);

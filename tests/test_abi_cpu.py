@@ -67,6 +67,8 @@ def test_host_side_argument_checks(lib):
     n = ctypes.c_size_t(0)
     A = P(1000, 1000, 5000, 8, 8)
     assert lib.csrk_workspace_size(4, 1, ctypes.byref(A), None, 0, 0, ctypes.byref(n)) == 0 and n.value > 0
-    assert lib.csrk_workspace_size(0, 1, ctypes.byref(A), None, 0, 0, ctypes.byref(n)) == 0 and n.value == 0
+    assert lib.csrk_workspace_size(0, 1, ctypes.byref(A), None, 0, 0, ctypes.byref(n)) == 0 and n.value > 0
+    # a too-small workspace is rejected on the host before any launch
+    assert lib.csrk_spmv_fwd(1, 0, A, 8, None, None, 8, 8, None, 0, None) == -4
     assert lib.csrk_workspace_size(5, 1, ctypes.byref(A), ctypes.byref(A), 0, 0, ctypes.byref(n)) == 0 and n.value > 0
     assert lib.csrk_launch_count() == 0
