@@ -263,6 +263,36 @@ static int launch_spmm(const SpmmArgs<T> &a, cudaStream_t s)
     return CSRK_OK;
 }
 
+// ---------------------------------------------------------------- lean row kernel (no staging)
+// One G-lane group per row, RPW rows per group strided by the grid; index and value read with
+// group-broadcast loads (one L1 request per group), no shared memory, no block barrier.
+template <typename T, int G, int W, bool PERM>
+__global__ __launch_bounds__(256) void k_spmm_lean(SpmmArgs<T> a)
+{
+    const int lane = threadIdx.x % G;
+    const int64_t ngroups = (int64_t)gridDim.x * (256 / G);
+    const int npass = (int)((a.k + kPass - 1) / kPass);
+    for (int64_t row = (int64_t)blockIdx.x * (256 / G) + threadIdx.x / G; row < a.nrows; row += ngroups) {
+        const int64_t s = a.indptr[row], e = a.indptr[row + 1];
+        for (int ps = 0; ps < npass; ++ps) {
+            const int64_t pc = (int64_t)ps * kPass;
+            double acc[W];
+#pragma unroll
+            for (int i = 0; i < W; ++i) acc[i] = 0.0;
+            const T *Xc = a.X + pc;
+#pragma unroll 4
+            for (int64_t q = s; q < e; ++q) {
+                const double av = (double)a.vals[PERM ? a.perm[q] : q];
+                double xv[W];
+                ldl<T, G, W>(Xc + (int64_t)(uint32_t)a.indices[q] * a.ldx, lane, a.k - pc, xv);
+#pragma unroll
+                for (int i = 0; i < W; ++i) acc[i] = fma(av, xv[i], acc[i]);
+            }
+            stl<T, G, W>(a.Y + row * a.ldy + pc, lane, a.k - pc, acc);
+        }
+    }
+}
+
 // ---------------------------------------------------------------- experimental TMA bulk gather
 // One CTA = 32 rows.  Every nonzero's gathered dense row (k*sizeof(T) bytes, a multiple of 16)
 // is fetched into shared memory by a 1D bulk copy (cp.async.bulk) completing on one mbarrier;
@@ -356,6 +386,13 @@ static bool vec_ok(int64_t k, std::initializer_list<std::pair<const void *, int6
 template <typename T, int MODE>
 static int dispatch(bool vec, const SpmmArgs<T> &a, cudaStream_t s)
 {
+    const int lean = knob("SPMM_LEAN", 0);
+    if (vec && lean && (MODE == SP_FWD || MODE == SP_FWD_PERM) && a.nrows > 0) {
+        const int64_t groups = 256 / 8;
+        int64_t grid = cdiv(a.nrows, groups * lean);
+        CSRK_LAUNCH((k_spmm_lean<T, 8, 4, MODE == SP_FWD_PERM>), (unsigned)grid, 256, 0, s, a);
+        return CSRK_OK;
+    }
     if (vec) return launch_spmm<T, 8, 4, MODE>(a, s);
     return launch_spmm<T, 32, 1, MODE>(a, s);
 }
