@@ -76,7 +76,8 @@ typedef enum {
     CSRK_WS_CSR_TRANSPOSE = 4,
     CSRK_WS_SPGEMM_SYMBOLIC = 5,
     CSRK_WS_SPGEMM_NUMERIC = 6,
-    CSRK_WS_SPGEMM_BWD = 7
+    CSRK_WS_SPGEMM_BWD = 7,
+    CSRK_WS_PCG = 8          /* B = L, k = n_it */
 } csrk_ws_op;
 
 /*
@@ -172,6 +173,24 @@ int csrk_spgemm_numeric(csrk_dtype dtype, csrk_pattern A, const void *A_val,
 int csrk_spgemm_bwd(csrk_dtype dtype, csrk_pattern A, const void *A_val,
                     csrk_pattern B, const void *B_val, csrk_pattern C, const void *dC_val,
                     void *dA_val, void *dB_val, void *ws, size_t ws_bytes, csrk_stream_t stream);
+
+/*
+ * Learned-preconditioner PCG training step -- the config-5 composition of SURVEY 8(a) row a14
+ * (PAPER 4.3).  Runs n_it iterations of preconditioned CG on A x = b with x0 = 0 and
+ * M = L L^T (L lower triangular, e.g. the lower-bidiagonal L of P:857), records the
+ * residuals r^(1..n_it), evaluates the weighted loss
+ *     loss = sum_i w_i ||r^(i)||_2 / ||b||_2,   w_i = gamma^(n_it - i) / sum_j gamma^(n_it - j),
+ * and back-propagates to dL_val[nnz(L)] = d loss / d L.values (on L's pattern).
+ * The reverse pass is the adjoint of every CG step (SpMV VJPs for L, L^T and A; dot / axpy
+ * adjoints), run with the same kernels as the forward.  fp64 only.  All vectors are device
+ * arrays of length n = A.nrows; loss_host (required) and resid_host (nullable, n_it entries,
+ * ||r^(i)||) are host pointers: the call synchronises `stream` once at the end.
+ * Workspace: csrk_workspace_size(CSRK_WS_PCG, CSRK_F64, &A, &L, n_it, 0, &bytes) -- the saved
+ * p, q, r vectors of every iteration, (3 n_it + 12) n doubles.
+ */
+int csrk_pcg_loss_grad(csrk_pattern A, const double *A_val, csrk_pattern L, const double *L_val,
+                       const double *b, int n_it, double gamma, double *loss_host, double *resid_host,
+                       double *dL_val, void *ws, size_t ws_bytes, csrk_stream_t stream);
 
 /*
  * Scratch bytes needed by operation `op` for operands A (and B for SpGEMM, or the

@@ -22,12 +22,12 @@ LIB_PATH = os.path.join(_PKG, "libcsrk.so")
 F32, F64 = 0, 1
 OP_N, OP_T = 0, 1
 WS = dict(spmv_fwd=0, spmv_bwd=1, spmm_fwd=2, spmm_bwd=3, csr_transpose=4, spgemm_symbolic=5,
-          spgemm_numeric=6, spgemm_bwd=7)
+          spgemm_numeric=6, spgemm_bwd=7, pcg=8)
 
 # Every symbol declared in include/csrk.h (checked by tests/test_abi_cpu.py).
 ABI_SYMBOLS = ("csrk_spmv_fwd", "csrk_spmv_bwd", "csrk_spmm_fwd", "csrk_spmm_bwd", "csrk_csr_transpose",
                "csrk_spgemm_symbolic", "csrk_spgemm_numeric", "csrk_spgemm_bwd", "csrk_workspace_size",
-               "csrk_status_string", "csrk_launch_count", "csrk_version")
+               "csrk_status_string", "csrk_launch_count", "csrk_version", "csrk_pcg_loss_grad")
 
 
 class Pattern(ctypes.Structure):
@@ -63,6 +63,8 @@ def lib() -> ctypes.CDLL:
     L.csrk_spgemm_numeric.argtypes = [I, Pat, P, Pat, P, Pat, P, P, SZ, P]
     L.csrk_spgemm_bwd.argtypes = [I, Pat, P, Pat, P, Pat, P, P, P, P, SZ, P]
     L.csrk_workspace_size.argtypes = [I, I, PatP, PatP, I64, I, ctypes.POINTER(SZ)]
+    D = ctypes.c_double
+    L.csrk_pcg_loss_grad.argtypes = [Pat, P, Pat, P, P, I, D, ctypes.POINTER(D), ctypes.POINTER(D), P, P, SZ, P]
     L.csrk_status_string.restype = ctypes.c_char_p
     L.csrk_status_string.argtypes = [I]
     L.csrk_launch_count.restype = ctypes.c_uint64
@@ -267,3 +269,23 @@ def spgemm_bwd(A: CSR, B: CSR, C: CSR, dC: torch.Tensor, need_dA: bool = True, n
                                  _ptr(dC), _ptr(dA if need_dA else None), _ptr(dB if need_dB else None), ws, wsb,
                                  _stream()), "spgemm_bwd")
     return (dA if need_dA else None), (dB if need_dB else None)
+
+
+def pcg_loss_grad(A: CSR, L: CSR, b: torch.Tensor, n_it: int = 50, gamma: float = 0.6,
+                  dL: torch.Tensor | None = None):
+    """Config-5 composition (PAPER 4.3): n_it PCG iterations with M = L L^T, the
+    weighted residual loss and its gradient w.r.t. L.values.  fp64.
+    Returns (loss, residual norms ||r^(1..n_it)||, dL on L's pattern)."""
+    if dL is None:
+        dL = torch.empty_like(L.values)
+    pa, pl = A.pattern(), L.pattern()
+    nbytes = ctypes.c_size_t(0)
+    _check(lib().csrk_workspace_size(WS["pcg"], F64, ctypes.byref(pa), ctypes.byref(pl), n_it, 0,
+                                     ctypes.byref(nbytes)), "workspace_size(pcg)")
+    ws = torch.empty(max(int(nbytes.value), 1), dtype=torch.uint8, device=b.device)
+    loss = ctypes.c_double(0.0)
+    resid = (ctypes.c_double * n_it)()
+    _check(lib().csrk_pcg_loss_grad(pa, _ptr(A.values), pl, _ptr(L.values), _ptr(b), int(n_it), float(gamma),
+                                    ctypes.byref(loss), resid, _ptr(dL), _ptr(ws), ws.numel(), _stream()),
+           "pcg_loss_grad")
+    return float(loss.value), list(resid), dL

@@ -151,6 +151,21 @@ def powerlaw(n: int = 1 << 23, seed: int = seed_of(4, 1), mean: int = 16, dtype=
     return CSR(n, n, indptr, indices, vals)
 
 
+def bidiag_lower(n: int, init: str = "identity", seed: int = seed_of(5, 6)) -> CSR:
+    """Lower-bidiagonal L of PAPER 4.3 ("a lower bidiagonal L"), 2n - 1 stored entries.
+    init 'identity': L = I with the subdiagonal stored as explicit zeros (SURVEY A17);
+    init 'seeded': diagonal U[0.9, 1.1], subdiagonal U[-0.1, 0.1]."""
+    i = np.arange(n, dtype=np.int64)
+    cols = np.stack([i - 1, i], axis=1)
+    valid = cols >= 0
+    if init == "identity":
+        vals = np.broadcast_to(np.array([0.0, 1.0]), cols.shape)
+    else:
+        rng = np.random.default_rng(seed)
+        vals = np.stack([rng.uniform(-0.1, 0.1, n), rng.uniform(0.9, 1.1, n)], axis=1)
+    return _from_candidates(n, n, cols, vals, valid, np.float64)
+
+
 def random_csr(m: int, n: int, density: float, seed: int, dtype=np.float64, values: str = "real",
                empty_rows: bool = False) -> CSR:
     """Bernoulli(density) pattern on an m x n grid (density 1.0 = full pattern).  With
