@@ -64,6 +64,66 @@ OPS = ["csr_transpose", "spmv_fwd", "spmv_bwd", "spmm_fwd", "spmm_bwd", "spgemm_
        "spgemm_bwd"]
 
 
+def pcg_costs(n, nnzA, nnzL, N, s=S):
+    """Algorithmic bytes / flops of one config-5 training step (csrk_pcg_loss_grad), op by op:
+    SpMV = pattern + values + in + out; VJP of SpMV adds dy, dx, dA; dot 2n reads; a linear
+    combination of k vectors k reads + 1 write."""
+    spa = 8 * (n + 1) + (4 + s) * nnzA + 2 * s * n
+    spl = 8 * (n + 1) + (4 + s) * nnzL + 2 * s * n
+    splb = 8 * (n + 1) + (4 + s) * nnzL + 3 * s * n + s * nnzL
+    spl_dA = 8 * (n + 1) + 4 * nnzL + 2 * s * n + s * nnzL
+    dot, lin = 2 * s * n, lambda k, m=n: (k + 1) * s * m
+    fwd = dot + lin(1) + 2 * spl + dot
+    fwd += N * (spa + dot + lin(2)) + (N - 1) * (2 * spl + dot + lin(2))
+    bwd = lin(2)
+    bwd += (N - 1) * (dot + 2 * spl + lin(2) + lin(3) + 2 * splb + 2 * lin(2, nnzL) + lin(2))
+    bwd += N * (dot + lin(2) + spa + lin(3))
+    bwd += lin(2) + spl + splb + lin(2, nnzL) + spl_dA + lin(2, nnzL)
+    flops = N * 2 * (2 * nnzA + 4 * nnzL) * 2 + N * 20 * n
+    return fwd + bwd, flops
+
+
+def run_cfg5(args, torch, ck):
+    """BASELINE config 5: one training step = 50 PCG iterations on the 2D
+    Poisson 4096^2 matrix with M = L L^T (lower-bidiagonal L), loss and d loss / d L.values."""
+    A = synth.poisson2d(4096)
+    L = synth.bidiag_lower(A.nrows, "seeded")
+    b = np.full(A.nrows, 1.0 / np.sqrt(A.nrows))
+    Ad, Ld = ck.CSR.from_host(A), ck.CSR.from_host(L)
+    bt = torch.from_numpy(b).cuda()
+    dL = torch.empty_like(Ld.values)
+    N = 50
+    for _ in range(args.warmup):
+        ck.pcg_loss_grad(Ad, Ld, bt, N, 0.6, dL=dL)
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    l0 = ck.launch_count()
+    ts = []
+    with Clocks(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        for _ in range(args.steps):
+            a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            loss, res, _ = ck.pcg_loss_grad(Ad, Ld, bt, N, 0.6, dL=dL)
+            e.record(st)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(e))
+    byts, flops = pcg_costs(A.nrows, A.nnz, L.nnz, N)
+    ms = float(np.mean(ts))
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    out = {"metric": "PCG training-step algorithmic GB/s (config 5)", "value": round(byts / (ms * 1e-3) / 1e9, 2),
+           "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": "config5: 2D Poisson 4096^2 (16,777,216 rows, 83,869,696 nnz), lower-bidiagonal "
+                                  "L (33,554,431 nnz), 50 PCG iterations fwd + reverse, gamma 0.6, 1 GPU"},
+           "step_bytes": byts, "gflops": round(flops / (ms * 1e-3) / 1e9, 2), "loss": loss,
+           "roofline": {"bound": "hbm", "kernel": "whole step", "achieved": round(byts / (ms * 1e-3) / 1e9, 1),
+                        "peak": peak, "unit": "GB/s", "frac": round(byts / (ms * 1e-3) / 1e9 / peak, 4)},
+           "gpu_launches": int((ck.launch_count() - l0) / max(args.steps, 1)), "clocks": clk.summary()}
+    print(json.dumps(out))
+    return 0
+
+
 # ---------------------------------------------------------------- clocks sampler
 class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
@@ -266,6 +326,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -274,6 +335,9 @@ def main():
     import torch
     import torch.distributed as tdist
     from paper_2212_05159_b200 import csrk as ck
+
+    if args.workload == "cfg5":
+        return run_cfg5(args, torch, ck)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
