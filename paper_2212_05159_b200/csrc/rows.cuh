@@ -64,6 +64,22 @@ __global__ __launch_bounds__(kRowsTPB) void k_rows(TileArgs<T> a, RowList L)
         base = __shfl_sync(0xffffffffu, base, 0);
         if (lng) L.rows[base + __popc(lm & ((1u << lane) - 1))] = (int32_t)row;
     }
+    if (MODE != MODE_REDUCE && !lm) {
+        // per-element outputs (scatter / transpose): the warp's 32 rows span one contiguous
+        // element range; map element -> row in shared memory, then stream the range coalesced
+        __shared__ uint8_t s_rw[kRowsTPB / 32][32 * kShortRow];
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        const int64_t e0 = __shfl_sync(0xffffffffu, s, 0);
+        const int64_t elast = valid ? e : 0;
+        const int64_t e1 = __reduce_max_sync(0xffffffffu, (unsigned)(elast - e0 < 0 ? 0 : elast - e0)) + e0;
+        for (int64_t p = s; p < e; ++p) s_rw[w][p - e0] = (uint8_t)lane;
+        __syncwarp();
+        const int64_t r0 = row - lane;
+        double dummy = 0.0;
+#pragma unroll 4
+        for (int64_t p = e0 + lane; p < e1; p += 32) row_elem<T, MODE, PERM, SIDE>(a, r0 + s_rw[w][p - e0], p, dummy);
+        return;
+    }
     if (!valid || lng) return;
     double acc = 0.0;
 #pragma unroll 4

@@ -55,7 +55,8 @@ struct LaneMap {
 };
 
 // Load lane l's W elements of a pass starting at p (kleft = columns left in the row).
-template <typename T, int G, int W>
+// GLOBAL: read-only global path (__ldg); otherwise a generic load (shared-memory staging).
+template <typename T, int G, int W, bool GLOBAL = true>
 __device__ __forceinline__ void ldl(const T *p, int l, int64_t kleft, double (&r)[W])
 {
     using M = LaneMap<T, G, W>;
@@ -63,15 +64,21 @@ __device__ __forceinline__ void ldl(const T *p, int l, int64_t kleft, double (&r
     for (int ch = 0; ch < M::NCH; ++ch) {
         const int c = M::col(l, ch);
         if constexpr (M::E == 1) {
-            r[ch] = c < kleft ? (double)__ldg(p + c) : 0.0;
+            r[ch] = c < kleft ? (double)(GLOBAL ? __ldg(p + c) : p[c]) : 0.0;
         } else if constexpr (sizeof(T) == 8) {
             double2 v = make_double2(0.0, 0.0);
-            if (c < kleft) v = __ldg(reinterpret_cast<const double2 *>(p + c));
+            if (c < kleft) {
+                const double2 *q = reinterpret_cast<const double2 *>(p + c);
+                v = GLOBAL ? __ldg(q) : *q;
+            }
             r[ch * 2] = v.x;
             r[ch * 2 + 1] = v.y;
         } else {
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (c < kleft) v = __ldg(reinterpret_cast<const float4 *>(p + c));
+            if (c < kleft) {
+                const float4 *q = reinterpret_cast<const float4 *>(p + c);
+                v = GLOBAL ? __ldg(q) : *q;
+            }
             r[ch * 4] = v.x; r[ch * 4 + 1] = v.y; r[ch * 4 + 2] = v.z; r[ch * 4 + 3] = v.w;
         }
     }
@@ -168,7 +175,7 @@ __device__ __forceinline__ void spmm_rows(const SpmmArgs<T> &a, const int64_t *s
                     if (valid && ps < npass)
                         ldl<T, G, W>(a.W + row * a.ldw + (int64_t)ps * kPass, lane, a.k - (int64_t)ps * kPass, xj[ps]);
                 }
-#pragma unroll 2
+#pragma unroll 4
                 for (int t = 0; t < maxlen; ++t) {
                     const bool on = t < len;
                     const int64_t off = on ? off_of(s + t) : 0;
@@ -302,56 +309,88 @@ constexpr int kBulkG = 8;
 constexpr int kBulkRT = kBulkTPB / kBulkG;
 constexpr int kBulkBytes = 40 * 1024;
 
+// Persistent CTAs, two buffers: the bulk copies of tile t+grid are issued before tile t is
+// computed from shared memory, so the TMA gathers of one tile overlap the math of the other.
 template <typename T>
-__global__ __launch_bounds__(kBulkTPB) void k_spmm_bulk(SpmmArgs<T> a, int cap)
+__global__ __launch_bounds__(kBulkTPB) void k_spmm_bulk(SpmmArgs<T> a, int cap, int64_t ntiles)
 {
     constexpr int W = 4;
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ int64_t s_ptr[kBulkRT + 1];
-    __shared__ __align__(8) uint64_t bar;
+    __shared__ int64_t s_ptr[2][kBulkRT + 1];
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ int s_fits[2];
     const int rb = (int)(a.k * (int64_t)sizeof(T));
-    unsigned char *s_g = smem;
-    double *s_val = reinterpret_cast<double *>(smem + (size_t)cap * rb);
+    const size_t bufb = (size_t)cap * rb + (size_t)cap * sizeof(double);
     const int tid = threadIdx.x, g = tid / kBulkG, lane = tid % kBulkG;
-    const int64_t r0 = (int64_t)blockIdx.x * kBulkRT;
-    const int nr = (int)(a.nrows - r0 < kBulkRT ? a.nrows - r0 : kBulkRT);
     if (tid == 0) {
-        mbar_init(&bar, 1);
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
         mbar_fence_init();
     }
-    for (int i = tid; i <= nr; i += kBulkTPB) s_ptr[i] = a.indptr[r0 + i];
     __syncthreads();
-    const int64_t base = s_ptr[0];
-    const int64_t tnz = s_ptr[nr] - base;
-    const bool fits = tnz <= cap;
-    if (fits) {
-        if (tid == 0) mbar_arrive_expect_tx(&bar, (uint32_t)(tnz * rb));
+    const char *Xb = reinterpret_cast<const char *>(a.X);
+    const int64_t ldb = a.ldx * (int64_t)sizeof(T);
+    auto issue = [&](int64_t t, int b) {
+        const int64_t r0 = t * kBulkRT;
+        const int nr = (int)(a.nrows - r0 < kBulkRT ? a.nrows - r0 : kBulkRT);
+        for (int i = tid; i <= nr; i += kBulkTPB) s_ptr[b][i] = a.indptr[r0 + i];
         __syncthreads();
-        const char *Xb = reinterpret_cast<const char *>(a.X);
-        const int64_t ldb = a.ldx * (int64_t)sizeof(T);
+        const int64_t base = s_ptr[b][0];
+        const int64_t tnz = s_ptr[b][nr] - base;
+        const bool fits = tnz <= cap;
+        if (tid == 0) s_fits[b] = fits;
+        if (!fits) return;
+        if (tid == 0) mbar_arrive_expect_tx(&bar[b], (uint32_t)(tnz * rb));
+        __syncthreads();
+        unsigned char *s_g = smem + b * bufb;
+        double *s_val = reinterpret_cast<double *>(s_g + (size_t)cap * rb);
         for (int e = tid; e < (int)tnz; e += kBulkTPB) {
             const int64_t p = base + e;
-            bulk_g2s(s_g + (size_t)e * rb, Xb + (int64_t)(uint32_t)a.indices[p] * ldb, (uint32_t)rb, &bar);
+            bulk_g2s(s_g + (size_t)e * rb, Xb + (int64_t)(uint32_t)a.indices[p] * ldb, (uint32_t)rb, &bar[b]);
             s_val[e] = (double)a.vals[p];
         }
-        __syncthreads();
-        mbar_wait(&bar, 0);
-    }
-    if (g >= nr) return;
-    const int64_t row = r0 + g;
-    const int64_t s = s_ptr[g] - base, e = s_ptr[g + 1] - base;
-    for (int64_t pc = 0; pc < a.k; pc += kPass) {
-        double acc[W] = {0.0, 0.0, 0.0, 0.0};
-        for (int64_t q = s; q < e; ++q) {
-            double xv[W];
-            const T *src = fits ? reinterpret_cast<const T *>(s_g + (size_t)q * rb) + pc
-                                : a.X + (int64_t)a.indices[base + q] * a.ldx + pc;
-            const double av = fits ? s_val[q] : (double)a.vals[base + q];
-            ldl<T, kBulkG, W>(src, lane, a.k - pc, xv);
-#pragma unroll
-            for (int i = 0; i < W; ++i) acc[i] = fma(av, xv[i], acc[i]);
+    };
+    uint32_t phase[2] = {0u, 0u};
+    int64_t t = blockIdx.x;
+    if (t < ntiles) issue(t, 0);
+    for (int it = 0; t < ntiles; t += gridDim.x, ++it) {
+        const int b = it & 1;
+        if (t + gridDim.x < ntiles) issue(t + gridDim.x, b ^ 1);
+        __syncthreads();                        // s_val / s_fits of buffer b visible
+        const bool fits = s_fits[b];
+        if (fits) {
+            mbar_wait(&bar[b], phase[b]);
+            phase[b] ^= 1u;
         }
-        stl<T, kBulkG, W>(a.Y + row * a.ldy + pc, lane, a.k - pc, acc);
+        const unsigned char *s_g = smem + b * bufb;
+        const double *s_val = reinterpret_cast<const double *>(s_g + (size_t)cap * rb);
+        const int64_t r0 = t * kBulkRT;
+        const int nr = (int)(a.nrows - r0 < kBulkRT ? a.nrows - r0 : kBulkRT);
+        if (g < nr) {
+            const int64_t base = s_ptr[b][0];
+            const int64_t row = r0 + g;
+            const int64_t s = s_ptr[b][g] - base, e = s_ptr[b][g + 1] - base;
+            for (int64_t pc = 0; pc < a.k; pc += kPass) {
+                double acc[W] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
+                for (int64_t q = s; q < e; ++q) {
+                    double xv[W];
+                    double av;
+                    if (fits) {
+                        ldl<T, kBulkG, W, false>(reinterpret_cast<const T *>(s_g + (size_t)q * rb) + pc, lane,
+                                                 a.k - pc, xv);
+                        av = s_val[q];
+                    } else {
+                        ldl<T, kBulkG, W>(a.X + (int64_t)a.indices[base + q] * a.ldx + pc, lane, a.k - pc, xv);
+                        av = (double)a.vals[base + q];
+                    }
+#pragma unroll
+                    for (int i = 0; i < W; ++i) acc[i] = fma(av, xv[i], acc[i]);
+                }
+                stl<T, kBulkG, W>(a.Y + row * a.ldy + pc, lane, a.k - pc, acc);
+            }
+        }
+        __syncthreads();                        // buffer b free for tile t + 2 grid
     }
 }
 
@@ -361,13 +400,15 @@ static int launch_spmm_bulk(const SpmmArgs<T> &a, cudaStream_t s)
     if (a.nrows <= 0) return CSRK_OK;
     const int rb = (int)(a.k * (int64_t)sizeof(T));
     const int cap = kBulkBytes / rb;
-    const size_t smem = (size_t)cap * rb + (size_t)cap * sizeof(double);
+    const size_t smem = 2 * ((size_t)cap * rb + (size_t)cap * sizeof(double));
     static bool attr = false;
     if (!attr) {
-        CSRK_CUDA(cudaFuncSetAttribute(k_spmm_bulk<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        CSRK_CUDA(cudaFuncSetAttribute(k_spmm_bulk<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    CSRK_LAUNCH(k_spmm_bulk<T>, (unsigned)cdiv(a.nrows, kBulkRT), kBulkTPB, smem, s, a, cap);
+    const int64_t ntiles = cdiv(a.nrows, kBulkRT);
+    const int64_t grid = ntiles < (int64_t)kNumSMs * 2 ? ntiles : (int64_t)kNumSMs * 2;
+    CSRK_LAUNCH(k_spmm_bulk<T>, (unsigned)grid, kBulkTPB, smem, s, a, cap, ntiles);
     return CSRK_OK;
 }
 
