@@ -17,7 +17,10 @@ import sys
 
 OP_OF = [  # (substring of the kernel name, op) -- order of the step in bench.py
     ("k_col_count", "csr_transpose"), ("k_sort_", "csr_transpose"), ("k_csr_tile<double, 2", "csr_transpose"),
+    ("k_rows<double, 2", "csr_transpose"), ("k_rows_long<double, 2", "csr_transpose"),
     ("k_csr_tile<double, 0, 0, 0>", "spmv_fwd"), ("k_csr_tile<double, 0, 1, 1>", "spmv_bwd"),
+    ("k_rows<double, 0, 0, 0>", "spmv_fwd"), ("k_rows_long<double, 0, 0, 0>", "spmv_fwd"),
+    ("k_rows<double, 1, 0, 1>", "spmv_bwd"), ("k_rows_long<double, 1, 0, 1>", "spmv_bwd"),
     ("k_spmm<double, 8, 4, 0>", "spmm_fwd"), ("k_spmm<double, 8, 4, 3>", "spmm_bwd"),
     ("k_gemm_S<double, 0>", "spgemm_symbolic"), ("k_gemm_big_sym<0>", "spgemm_symbolic"),
     ("k_gemm_S<double, 1>", "spgemm_symbolic"), ("k_gemm_big_sym<1>", "spgemm_symbolic"),
