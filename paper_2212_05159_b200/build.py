@@ -33,7 +33,8 @@ def _deps_mtime() -> float:
 
 def _compile(src: str, ptxas_v: bool) -> str:
     obj = os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    # CSRK_NVCC_EXTRA: developer-only extra flags (e.g. -D tuning constants for A/B runs)
+    cmd = [NVCC, *ARCH, *FLAGS, *os.environ.get("CSRK_NVCC_EXTRA", "").split(), "-c", src, "-o", obj]
     if ptxas_v:
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)

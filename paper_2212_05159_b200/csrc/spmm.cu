@@ -19,6 +19,7 @@
 // kept behind CSRK_SPMM_BULK=1; it measured slower.
 #include "async.cuh"
 #include "ops.cuh"
+#include "vec.cuh"
 
 namespace csrk {
 
@@ -36,6 +37,7 @@ struct SpmmArgs {
     const T *W;  int64_t ldw;   // row operand (SDDMM: dY[i,:], FUSED_T: X[j,:])
     T *Y;        int64_t ldy;   // dense output (FWD: Y, FUSED_T / FWD_PERM: dX)
     T *D;                       // dA (SDDMM, FUSED_T)
+    int64_t xrows;              // rows of the gathered operand (= ncols of the traversed matrix)
 };
 
 constexpr int kSpmmTPB = 256;
@@ -412,6 +414,227 @@ static int launch_spmm_bulk(const SpmmArgs<T> &a, cudaStream_t s)
     return CSRK_OK;
 }
 
+// ---------------------------------------------------------------- wide path (256-bit vectors)
+// For dense rows of exactly 128 or 256 bytes (fp64 k = 16 / 32, fp32 k = 32): a group of 4
+// lanes owns a row, each lane holding NV 32-byte vectors, so one load / store instruction of a
+// group covers a whole 128-byte line.  A group walks the CONTIGUOUS nonzero stream of its
+// kWRPG consecutive rows in batches of 4: the 4 gathers of a batch are issued before any is
+// consumed (memory-level parallelism), row transitions flush the accumulator, and the 4 dot
+// products of a batch (SDDMM / fused backward) are finished by one transpose-reduction, after
+// which lane l stores dA of the batch's l-th nonzero.
+constexpr int kWG = 4;
+constexpr int kWRPG = 4;
+constexpr int kWCAP = 1536;
+// CTA size per mode (measured, config 2): 256 threads with the band for the forward modes,
+// 128 threads (more, smaller CTAs per SM) for the dot-product modes.
+template <int MODE> constexpr int wide_tpb() { return MODE == SP_FWD || MODE == SP_FWD_PERM ? 256 : 128; }
+
+struct __align__(16) WideNz {
+    double val;
+    int64_t off;   // element offset of the gathered dense row
+};
+
+// Near-diagonal band (BAND): the gathered operand's rows [b0, b1) around the tile's own row
+// range (scaled to the column space, +-kBandH) are brought into shared memory by ONE TMA bulk
+// copy per tile; gathers inside the band read shared memory.  On a stencil 3 of 5 gathers per
+// row fall in the band, so the L2 traffic of the gathers drops from 5 to ~3 dense rows per row.
+constexpr int kBandH = 8;
+template <int MODE> constexpr int band_cap() { return wide_tpb<MODE>() / kWG * kWRPG + 2 * kBandH + 1; }
+
+template <typename T, int NV, int MODE, bool BAND>
+__global__ __launch_bounds__(wide_tpb<MODE>(), 512 / wide_tpb<MODE>()) void k_spmm_wide(SpmmArgs<T> a)
+{
+    constexpr int kWTPB = wide_tpb<MODE>();
+    constexpr int kWRT = kWTPB / kWG * kWRPG;
+    constexpr int kBandCap = band_cap<MODE>();
+    constexpr int E = V32<T>::E;
+    constexpr int NE = NV * E;
+    constexpr bool PERM = MODE == SP_FWD_PERM || MODE == SP_FUSED_T;
+    constexpr bool ACC = MODE != SP_SDDMM;
+    constexpr bool DOT = MODE == SP_SDDMM || MODE == SP_FUSED_T;
+    __shared__ int64_t s_ptr[kWRT + 1];
+    __shared__ WideNz s_nz[kWCAP];
+    __shared__ int64_t s_perm[MODE == SP_FUSED_T ? kWCAP : 1];
+
+    constexpr int RB = NV * 128;   // bytes per dense row
+    extern __shared__ __align__(128) unsigned char s_band[];
+    __shared__ __align__(8) uint64_t s_bar;
+
+    const int tid = threadIdx.x;
+    const int64_t r0 = (int64_t)blockIdx.x * kWRT;
+    const int nr = (int)(a.nrows - r0 < kWRT ? a.nrows - r0 : kWRT);
+    int64_t b0 = 0, b1 = 0;
+    if (BAND) {
+        const double sc = (double)a.xrows / (double)a.nrows;
+        b0 = (int64_t)((double)r0 * sc) - kBandH;
+        b0 = b0 < 0 ? 0 : b0;
+        b1 = (int64_t)((double)(r0 + nr) * sc) + kBandH + 1;
+        b1 = b1 > a.xrows ? a.xrows : b1;
+        b1 = b1 > b0 + kBandCap ? b0 + kBandCap : b1;
+        b1 = b1 < b0 ? b0 : b1;
+        if (tid == 0) {
+            mbar_init(&s_bar, 1);
+            mbar_fence_init();
+        }
+    }
+    for (int i = tid; i <= nr; i += kWTPB) s_ptr[i] = a.indptr[r0 + i];
+    __syncthreads();
+    if (BAND && tid == 0 && b1 > b0) {
+        const uint32_t bytes = (uint32_t)((b1 - b0) * RB);
+        mbar_arrive_expect_tx(&s_bar, bytes);
+        bulk_g2s(s_band, a.X + b0 * a.ldx, bytes, &s_bar);
+    }
+    // element offset of a gathered row in global memory, or (band) -1 - its shared byte offset
+    auto where = [&](int64_t c) -> int64_t {
+        if (BAND && c >= b0 && c < b1) return -1 - (c - b0) * RB;
+        return c * a.ldx;
+    };
+    const int64_t base = s_ptr[0];
+    const bool staged = s_ptr[nr] - base <= kWCAP;   // tile-uniform
+    if (staged) {
+        const int tnz = (int)(s_ptr[nr] - base);
+        for (int e = tid; e < tnz; e += kWTPB) {
+            const int64_t p = base + e;
+            const int64_t pv = PERM ? a.perm[p] : p;
+            WideNz z;
+            z.off = where((int64_t)(uint32_t)a.indices[p]);
+            z.val = ACC ? (double)a.vals[pv] : 0.0;
+            s_nz[e] = z;
+            if (MODE == SP_FUSED_T) s_perm[e] = pv;
+        }
+        __syncthreads();
+    }
+    auto meta = [&](int64_t e) -> WideNz {
+        if (staged) return s_nz[e];
+        WideNz z;
+        z.off = where((int64_t)(uint32_t)a.indices[base + e]);
+        z.val = ACC ? (double)a.vals[PERM ? a.perm[base + e] : base + e] : 0.0;
+        return z;
+    };
+
+    const int g = tid / kWG, l = tid % kWG;
+    const int rb = g * kWRPG < nr ? g * kWRPG : nr;
+    const int re = rb + kWRPG < nr ? rb + kWRPG : nr;
+    const int64_t sb = s_ptr[rb] - base, se = s_ptr[re] - base;   // the group's nonzero stream
+    const int nbw = (int)__reduce_max_sync(0xffffffffu, (unsigned)((se - sb + 3) >> 2));
+    const int lo = l * E;   // this lane's first element; vector v at lo + v * kWG * E
+
+    double acc[NE], xr[NE];
+    int cur = rb;
+    int64_t cend = rb < re ? s_ptr[rb + 1] - base : 0;
+    auto begin = [&]() {
+        if (ACC) {
+#pragma unroll
+            for (int i = 0; i < NE; ++i) acc[i] = 0.0;
+        }
+        if (DOT) {
+            const T *w = a.W + (r0 + cur) * a.ldw + lo;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) ldv32(w + v * kWG * E, xr + v * E);
+        }
+    };
+    auto finish = [&]() {
+        if (ACC) {
+            T *y = a.Y + (r0 + cur) * a.ldy + lo;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) stv32(y + v * kWG * E, acc + v * E);
+        }
+    };
+    if (BAND && b1 > b0) mbar_wait(&s_bar, 0);
+    const int h = g & 1;   // shared-memory half order (bank spread between the 2 groups of a phase)
+    if (rb < re) begin();
+    for (int t = 0; t < nbw; ++t) {
+        const int64_t e0 = sb + 4 * t;
+        WideNz z[4];
+        double gv[4][NE];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            if (e0 + b < se) {
+                z[b] = meta(e0 + b);
+                if (!BAND || z[b].off >= 0) {
+                    const T *xp = a.X + z[b].off + lo;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) ldv32(xp + v * kWG * E, gv[b] + v * E);
+                } else {
+                    const T *xp = reinterpret_cast<const T *>(s_band + (-1 - z[b].off)) + lo;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) lds32(xp + v * kWG * E, gv[b] + v * E, h);
+                }
+            } else {
+                z[b].val = 0.0;
+#pragma unroll
+                for (int i = 0; i < NE; ++i) gv[b][i] = 0.0;
+            }
+        }
+        double d[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            if (e0 + b < se) {
+                while (e0 + b >= cend) {   // row transition (skips empty rows)
+                    finish();
+                    ++cur;
+                    cend = s_ptr[cur + 1] - base;
+                    begin();
+                }
+            }
+            if (ACC) {
+#pragma unroll
+                for (int i = 0; i < NE; ++i) acc[i] = fma(z[b].val, gv[b][i], acc[i]);
+            }
+            if (DOT) {
+                double s = 0.0;
+#pragma unroll
+                for (int i = 0; i < NE; ++i) s = fma(gv[b][i], xr[i], s);
+                d[b] = s;
+            }
+        }
+        if (DOT) {
+            const double dd = transpose_reduce4(d, l);
+            const int64_t e = e0 + l;
+            if (e < se) a.D[MODE == SP_FUSED_T ? (staged ? s_perm[e] : a.perm[base + e]) : base + e] = (T)dd;
+        }
+    }
+    if (rb < re) {   // the current row and any trailing empty rows
+        finish();
+        while (++cur < re) {
+            if (ACC) {
+#pragma unroll
+                for (int i = 0; i < NE; ++i) acc[i] = 0.0;
+            }
+            finish();
+        }
+    }
+}
+
+template <typename T, int MODE>
+static bool launch_wide(const SpmmArgs<T> &a, cudaStream_t s, int &st)
+{
+    if (!knob("SPMM_WIDE", 1)) return false;
+    const int64_t rb = a.k * (int64_t)sizeof(T);
+    const int nv = rb == 128 ? 1 : rb == 256 && sizeof(T) == 8 ? 2 : 0;
+    if (!nv) return false;
+    auto al = [](const void *p, int64_t ld) {
+        return !p || (!(reinterpret_cast<uintptr_t>(p) & 31) && !((ld * (int64_t)sizeof(T)) & 31));
+    };
+    if (!al(a.X, a.ldx) || !al(a.W, a.ldw) || !al(a.Y, a.ldy)) return false;
+    st = CSRK_OK;
+    if (a.nrows <= 0) return true;
+    constexpr int kWTPB = wide_tpb<MODE>();
+    const unsigned grid = (unsigned)cdiv(a.nrows, kWTPB / kWG * kWRPG);
+    // band staging needs contiguous dense rows (one bulk copy)
+    const bool band = knob("SPMM_BAND", 1) && (MODE == SP_FWD || MODE == SP_FWD_PERM) && a.ldx == a.k && a.xrows > 0;
+    auto go = [&](auto kern, bool bnd) -> int {
+        const size_t smem = bnd ? (size_t)band_cap<MODE>() * rb : 0;
+        if (bnd) CSRK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CSRK_LAUNCH(kern, grid, kWTPB, smem, s, a);
+        return CSRK_OK;
+    };
+    constexpr int NV2 = sizeof(T) == 8 ? 2 : 1;
+    if (nv == 1) st = band ? go(k_spmm_wide<T, 1, MODE, true>, true) : go(k_spmm_wide<T, 1, MODE, false>, false);
+    else st = band ? go(k_spmm_wide<T, NV2, MODE, true>, true) : go(k_spmm_wide<T, NV2, MODE, false>, false);
+    return true;
+}
+
 // ---------------------------------------------------------------- dispatch
 // Vector map: 16-byte aligned row starts and k a multiple of 4.  Otherwise the scalar map.
 template <typename T>
@@ -427,6 +650,8 @@ static bool vec_ok(int64_t k, std::initializer_list<std::pair<const void *, int6
 template <typename T, int MODE>
 static int dispatch(bool vec, const SpmmArgs<T> &a, cudaStream_t s)
 {
+    int st = CSRK_OK;
+    if (vec && launch_wide<T, MODE>(a, s, st)) return st;
     const int lean = knob("SPMM_LEAN", 0);
     if (vec && lean && (MODE == SP_FWD || MODE == SP_FWD_PERM) && a.nrows > 0) {
         const int64_t groups = 256 / 8;
@@ -445,7 +670,7 @@ static int spmm_fwd_t(const csrk_pattern &A, const T *A_val, int64_t k, const T 
     if (ws.sizing() || A.nrows == 0 || k == 0) return CSRK_OK;
     SpmmArgs<T> a{};
     a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices; a.vals = A_val;
-    a.k = k; a.X = X; a.ldx = ldx; a.Y = Y; a.ldy = ldy;
+    a.k = k; a.X = X; a.ldx = ldx; a.Y = Y; a.ldy = ldy; a.xrows = A.ncols;
     const bool vec = vec_ok<T>(k, {{X, ldx}, {Y, ldy}});
     if (vec && knob("SPMM_BULK", 0) && (k * (int64_t)sizeof(T)) % 16 == 0 && k * (int64_t)sizeof(T) <= 1024)
         return launch_spmm_bulk<T>(a, s);
@@ -477,17 +702,19 @@ static int spmm_bwd_t(const csrk_pattern &A, const T *A_val, const csrk_pattern 
     if (dX && dA && np <= kFusedMaxPasses) {
         // fused transposed traversal: dX and dA in one pass
         a.nrows = AT->nrows; a.indptr = AT->indptr; a.indices = AT->indices; a.perm = permu;
+        a.xrows = AT->ncols;
         a.X = dY; a.ldx = lddy; a.W = X; a.ldw = ldx; a.Y = dX; a.ldy = lddx; a.D = dA;
         return dispatch<T, SP_FUSED_T>(vec, a, s);
     }
     if (dX) {
         SpmmArgs<T> b = a;
         b.nrows = AT->nrows; b.indptr = AT->indptr; b.indices = AT->indices; b.perm = permu;
+        b.xrows = AT->ncols;
         b.X = dY; b.ldx = lddy; b.Y = dX; b.ldy = lddx;
         CSRK_TRY((dispatch<T, SP_FWD_PERM>(vec, b, s)));
     }
     if (dA && A.nrows > 0) {
-        a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices;
+        a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices; a.xrows = A.ncols;
         a.X = X; a.ldx = ldx; a.W = dY; a.ldw = lddy; a.D = dA;
         CSRK_TRY((dispatch<T, SP_SDDMM>(vec, a, s)));
     }

@@ -164,7 +164,8 @@ def test_csr_transpose(ck, orc, case):
 @pytest.mark.parametrize("case", ["config1_poisson16", "poisson2d_70", "rand_rect_empty_rows", "skew_mid",
                                   "tiny_3x3", "nnz0", "powerlaw_16k"])
 @pytest.mark.parametrize("dt,k", [(np.float64, 32), (np.float32, 32), (np.float64, 5), (np.float32, 7),
-                                  (np.float64, 200), (np.float64, 300), (np.float32, 16)])
+                                  (np.float64, 200), (np.float64, 300), (np.float32, 16),
+                                  (np.float64, 16)])
 def test_spmm_fwd_bwd(ck, orc, case, dt, k):
     values = "int" if k in (5, 16) else "real"
     A = make(case, dt, values)
