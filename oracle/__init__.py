@@ -59,6 +59,12 @@ def lib():
         L.orc_spgemm_numeric.restype = ctypes.c_int
         L.orc_spgemm_bwd.argtypes = [_I64, _I64, _I64] + [_P] * 13
         L.orc_spgemm_bwd.restype = ctypes.c_int
+        L.orc_spadd_symbolic.argtypes = [_I64, _P, _P, _P, _P, _P, _P]
+        L.orc_spadd_symbolic.restype = _I64
+        L.orc_spadd_numeric.argtypes = [_I64, ctypes.c_double, ctypes.c_double] + [_P] * 10
+        L.orc_spadd_numeric.restype = ctypes.c_int
+        L.orc_spadd_bwd.argtypes = [_I64, ctypes.c_double, ctypes.c_double] + [_P] * 9
+        L.orc_spadd_bwd.restype = ctypes.c_int
         L.orc_set_threads.argtypes = [ctypes.c_int]
         L.orc_get_threads.restype = ctypes.c_int
     return _lib
@@ -206,3 +212,44 @@ def spgemm_bwd(A, B, Cp, Ci, dC, want_dA: bool = True, want_dB: bool = True):
     if rc != 0:
         raise ValueError("spgemm_bwd: dC's pattern does not cover the products")
     return (None if dA is None else Result(_out(dA, dt), SA)), (None if dB is None else Result(_out(dB, dt), SB))
+
+
+def spadd_symbolic(A, B):
+    """pattern(alpha A + beta B) = pattern(A) U pattern(B), row by row."""
+    assert (A.nrows, A.ncols) == (B.nrows, B.ncols), "Sp+Sp: shape mismatch"
+    ap, ai = _pat(A)
+    bp, bi = _pat(B)
+    Cp = np.empty(A.nrows + 1, np.int64)
+    nnz = lib().orc_spadd_symbolic(A.nrows, _p(ap), _p(ai), _p(bp), _p(bi), _p(Cp), None)
+    Ci = np.empty(nnz, np.int32)
+    lib().orc_spadd_symbolic(A.nrows, _p(ap), _p(ai), _p(bp), _p(bi), _p(Cp), _p(Ci))
+    return Cp, Ci
+
+
+def spadd_numeric(alpha, A, beta, B, Cp, Ci) -> Result:
+    """C = alpha A + beta B on the union pattern."""
+    ap, ai = _pat(A)
+    bp, bi = _pat(B)
+    dt = A.values.dtype
+    Cv = np.empty(Ci.shape[0], np.float64)
+    S = np.empty(Ci.shape[0], np.float64)
+    rc = lib().orc_spadd_numeric(A.nrows, float(alpha), float(beta), _p(ap), _p(ai), _p(_f64(A.values)),
+                                 _p(bp), _p(bi), _p(_f64(B.values)), _p(Cp), _p(Ci), _p(Cv), _p(S))
+    if rc != 0:
+        raise ValueError("spadd_numeric: an entry of A or B is missing from C's pattern")
+    return Result(_out(Cv, dt), S)
+
+
+def spadd_bwd(alpha, A, beta, B, Cp, Ci, dC, want_dA: bool = True, want_dB: bool = True):
+    """VJP of Sp+Sp (Table 1): (alpha V (.) mask(A), beta V (.) mask(B))."""
+    ap, ai = _pat(A)
+    bp, bi = _pat(B)
+    dt = dC.dtype
+    g = _f64(dC)
+    dA = np.empty(A.nnz, np.float64) if want_dA else None
+    dB = np.empty(B.nnz, np.float64) if want_dB else None
+    rc = lib().orc_spadd_bwd(A.nrows, float(alpha), float(beta), _p(ap), _p(ai), _p(bp), _p(bi), _p(Cp), _p(Ci),
+                             _p(g), _p(dA), _p(dB))
+    if rc != 0:
+        raise ValueError("spadd_bwd: V's pattern misses an entry of A or B")
+    return (None if dA is None else _out(dA, dt)), (None if dB is None else _out(dB, dt))

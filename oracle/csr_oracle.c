@@ -359,3 +359,103 @@ int orc_spgemm_bwd(int64_t m, int64_t n, int64_t p,
     free(in);
     return bad ? -1 : 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* Sp + Sp  C = alpha A + beta B  (PAPER 3.1.4; Table 1) */
+/* ------------------------------------------------------------------------ */
+
+/* Symbolic: mask(C) = mask(A) U mask(B) ("the computation of C is viewed as a union over
+ * the rows of A and B").  Per row, the sorted union of the two column lists
+ * (structural: a sum that is 0 keeps its entry).  C_indices == NULL: counts only.
+ * Returns nnz(C). */
+int64_t orc_spadd_symbolic(int64_t m, const int64_t *A_indptr, const int32_t *A_indices,
+                           const int64_t *B_indptr, const int32_t *B_indices,
+                           int64_t *C_indptr, int32_t *C_indices)
+{
+    C_indptr[0] = 0;
+    for (int64_t i = 0; i < m; ++i) {
+        int64_t a = A_indptr[i], ae = A_indptr[i + 1], b = B_indptr[i], be = B_indptr[i + 1];
+        int64_t c = C_indptr[i];
+        while (a < ae || b < be) {
+            int32_t j;
+            if (b >= be || (a < ae && A_indices[a] < B_indices[b])) j = A_indices[a++];
+            else if (a >= ae || B_indices[b] < A_indices[a]) j = B_indices[b++];
+            else { j = A_indices[a]; ++a; ++b; }
+            if (C_indices) C_indices[c] = j;
+            ++c;
+        }
+        C_indptr[i + 1] = c;
+    }
+    return C_indptr[m];
+}
+
+/* value of row i of M at column j, or 0 with *found = 0 (linear scan: plain and slow) */
+static double orc_row_value(const int64_t *Mp, const int32_t *Mi, const double *Mv, int64_t i, int32_t j,
+                            int64_t *pos)
+{
+    for (int64_t q = Mp[i]; q < Mp[i + 1]; ++q)
+        if (Mi[q] == j) { *pos = q; return Mv ? Mv[q] : 0.0; }
+    *pos = -1;
+    return 0.0;
+}
+
+/* Numeric: C_ij = alpha A_ij + beta B_ij over C's pattern (absent entries are 0).  The two
+ * products and their sum are formed in long double and rounded once; S = |alpha A_ij| +
+ * |beta B_ij|.  Returns -1 if an entry of A or B is missing from C's pattern. */
+int orc_spadd_numeric(int64_t m, double alpha, double beta,
+                      const int64_t *A_indptr, const int32_t *A_indices, const double *A_val,
+                      const int64_t *B_indptr, const int32_t *B_indices, const double *B_val,
+                      const int64_t *C_indptr, const int32_t *C_indices, double *C_val, double *S)
+{
+    for (int64_t i = 0; i < m; ++i) {
+        for (int64_t c = C_indptr[i]; c < C_indptr[i + 1]; ++c) {
+            int64_t pa, pb;
+            const double a = orc_row_value(A_indptr, A_indices, A_val, i, C_indices[c], &pa);
+            const double b = orc_row_value(B_indptr, B_indices, B_val, i, C_indices[c], &pb);
+            const acc_t ta = (acc_t)alpha * (acc_t)a, tb = (acc_t)beta * (acc_t)b;
+            C_val[c] = (double)(ta + tb);
+            if (S) S[c] = (double)(fabsl(ta) + fabsl(tb));
+        }
+        /* every stored entry of A and B must appear in C */
+        for (int64_t q = A_indptr[i]; q < A_indptr[i + 1]; ++q) {
+            int64_t pc;
+            orc_row_value(C_indptr, C_indices, NULL, i, A_indices[q], &pc);
+            if (pc < 0) return -1;
+        }
+        for (int64_t q = B_indptr[i]; q < B_indptr[i + 1]; ++q) {
+            int64_t pc;
+            orc_row_value(C_indptr, C_indices, NULL, i, B_indices[q], &pc);
+            if (pc < 0) return -1;
+        }
+    }
+    return 0;
+}
+
+/* VJP (Table 1): dA = alpha V (.) mask(A), dB = beta V (.) mask(B) --
+ * "the row-wise reduction from V to the sparsity mask of A or B": each stored entry picks
+ * V at the same (i,j) (one IEEE double multiply, no accumulation).  dA / dB nullable.
+ * Returns -1 if V's pattern (= C's) misses an entry of A or B. */
+int orc_spadd_bwd(int64_t m, double alpha, double beta,
+                  const int64_t *A_indptr, const int32_t *A_indices,
+                  const int64_t *B_indptr, const int32_t *B_indices,
+                  const int64_t *C_indptr, const int32_t *C_indices, const double *dC,
+                  double *dA, double *dB)
+{
+    for (int64_t i = 0; i < m; ++i) {
+        if (dA)
+            for (int64_t q = A_indptr[i]; q < A_indptr[i + 1]; ++q) {
+                int64_t pc;
+                orc_row_value(C_indptr, C_indices, NULL, i, A_indices[q], &pc);
+                if (pc < 0) return -1;
+                dA[q] = alpha * dC[pc];
+            }
+        if (dB)
+            for (int64_t q = B_indptr[i]; q < B_indptr[i + 1]; ++q) {
+                int64_t pc;
+                orc_row_value(C_indptr, C_indices, NULL, i, B_indices[q], &pc);
+                if (pc < 0) return -1;
+                dB[q] = beta * dC[pc];
+            }
+    }
+    return 0;
+}
