@@ -77,7 +77,8 @@ typedef enum {
     CSRK_WS_SPGEMM_SYMBOLIC = 5,
     CSRK_WS_SPGEMM_NUMERIC = 6,
     CSRK_WS_SPGEMM_BWD = 7,
-    CSRK_WS_PCG = 8          /* B = L, k = n_it */
+    CSRK_WS_PCG = 8,         /* B = L, k = n_it */
+    CSRK_WS_SPADD_SYMBOLIC = 9 /* numeric / bwd need no workspace */
 } csrk_ws_op;
 
 /*
@@ -173,6 +174,39 @@ int csrk_spgemm_numeric(csrk_dtype dtype, csrk_pattern A, const void *A_val,
 int csrk_spgemm_bwd(csrk_dtype dtype, csrk_pattern A, const void *A_val,
                     csrk_pattern B, const void *B_val, csrk_pattern C, const void *dC_val,
                     void *dA_val, void *dB_val, void *ws, size_t ws_bytes, csrk_stream_t stream);
+
+/*
+ * Sp + Sp symbolic phase (PAPER 3.1.4):
+ *   pattern(C) = pattern(A) U pattern(B) ("mask(C) = mask(A) U mask(B) ... a union over the
+ *   rows"), columns ascending, structural (an entry whose values would sum to 0 is
+ *   kept).  A and B are m x n.  Same two-call protocol as csrk_spgemm_symbolic:
+ *   (1) C_indices == NULL: writes C_indptr[m+1], synchronises `stream`, stores nnz(C) in
+ *       *nnzC_host;  (2) C_indices != NULL: fills the sorted indices (no synchronisation).
+ */
+int csrk_spadd_symbolic(csrk_pattern A, csrk_pattern B, int64_t *C_indptr, int32_t *C_indices,
+                        int64_t *nnzC_host, void *ws, size_t ws_bytes, csrk_stream_t stream);
+
+/*
+ * Sp + Sp numeric phase:  C_ij = alpha A_ij + beta B_ij on C's pattern (absent
+ * entries count as 0), formed in fp64 and rounded once to dtype.  C MUST be the pattern
+ * returned by csrk_spadd_symbolic for (A, B) (CSRK_ERR_PATTERN if nnz(C) < nnz(A) or nnz(B));
+ * C_val[nnz(C)] overwritten.
+ */
+int csrk_spadd_numeric(csrk_dtype dtype, double alpha, csrk_pattern A, const void *A_val, double beta,
+                       csrk_pattern B, const void *B_val, csrk_pattern C, void *C_val,
+                       void *ws, size_t ws_bytes, csrk_stream_t stream);
+
+/*
+ * Sp + Sp backward = VJP of C = alpha A + beta B (Table 1):
+ *   dA = alpha dC (.) mask(A),  dB = beta dC (.) mask(B)
+ * ("the row-wise reduction from V to the sparsity mask of A or B"): each stored entry of A (B)
+ * takes dC at the same (i, j) times alpha (beta) -- one fp64 multiply, rounded once (bit-exact
+ * against the oracle).  dC_val aligned with C = csrk_spadd_symbolic(A, B); dA_val[nnz(A)],
+ * dB_val[nnz(B)] nullable.
+ */
+int csrk_spadd_bwd(csrk_dtype dtype, double alpha, csrk_pattern A, double beta, csrk_pattern B,
+                   csrk_pattern C, const void *dC_val, void *dA_val, void *dB_val,
+                   void *ws, size_t ws_bytes, csrk_stream_t stream);
 
 /*
  * Learned-preconditioner PCG training step -- the config-5 composition of SURVEY 8(a) row a14

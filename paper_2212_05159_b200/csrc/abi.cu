@@ -164,6 +164,53 @@ int csrk_spgemm_bwd(csrk_dtype dtype, csrk_pattern A, const void *A_val, csrk_pa
     });
 }
 
+int csrk_spadd_symbolic(csrk_pattern A, csrk_pattern B, int64_t *C_indptr, int32_t *C_indices, int64_t *nnzC_host,
+                        void *ws, size_t ws_bytes, csrk_stream_t stream)
+{
+    CSRK_TRY(check_pat(A));
+    CSRK_TRY(check_pat(B));
+    if (A.nrows != B.nrows || A.ncols != B.ncols) return CSRK_ERR_DIM_MISMATCH;
+    if (!C_indptr || (!C_indices && !nnzC_host)) return CSRK_ERR_INVALID_ARG;
+    CSRK_TRY(validate_pattern(A, (cudaStream_t)stream));
+    CSRK_TRY(validate_pattern(B, (cudaStream_t)stream));
+    return with_ws(ws, ws_bytes, [&](Bump &b) {
+        return spadd_symbolic(A, B, C_indptr, C_indices, nnzC_host, b, (cudaStream_t)stream);
+    });
+}
+
+int csrk_spadd_numeric(csrk_dtype dtype, double alpha, csrk_pattern A, const void *A_val, double beta, csrk_pattern B,
+                       const void *B_val, csrk_pattern C, void *C_val, void *ws, size_t ws_bytes, csrk_stream_t stream)
+{
+    CSRK_TRY(check_dtype(dtype));
+    CSRK_TRY(check_pat(A));
+    CSRK_TRY(check_pat(B));
+    CSRK_TRY(check_pat(C));
+    if (A.nrows != B.nrows || A.ncols != B.ncols || C.nrows != A.nrows || C.ncols != A.ncols)
+        return CSRK_ERR_DIM_MISMATCH;
+    if (C.nnz < A.nnz || C.nnz < B.nnz) return CSRK_ERR_PATTERN;
+    if ((A.nnz > 0 && !A_val) || (B.nnz > 0 && !B_val) || (C.nnz > 0 && !C_val)) return CSRK_ERR_INVALID_ARG;
+    return with_ws(ws, ws_bytes, [&](Bump &b) {
+        return spadd_numeric(dtype, alpha, beta, A, A_val, B, B_val, C, C_val, b, (cudaStream_t)stream);
+    });
+}
+
+int csrk_spadd_bwd(csrk_dtype dtype, double alpha, csrk_pattern A, double beta, csrk_pattern B, csrk_pattern C,
+                   const void *dC_val, void *dA_val, void *dB_val, void *ws, size_t ws_bytes, csrk_stream_t stream)
+{
+    CSRK_TRY(check_dtype(dtype));
+    CSRK_TRY(check_pat(A));
+    CSRK_TRY(check_pat(B));
+    CSRK_TRY(check_pat(C));
+    if (A.nrows != B.nrows || A.ncols != B.ncols || C.nrows != A.nrows || C.ncols != A.ncols)
+        return CSRK_ERR_DIM_MISMATCH;
+    if (C.nnz < A.nnz || C.nnz < B.nnz) return CSRK_ERR_PATTERN;
+    if (!dA_val && !dB_val) return CSRK_OK;
+    if (C.nnz > 0 && !dC_val) return CSRK_ERR_INVALID_ARG;
+    return with_ws(ws, ws_bytes, [&](Bump &b) {
+        return spadd_bwd(dtype, alpha, beta, A, B, C, dC_val, dA_val, dB_val, b, (cudaStream_t)stream);
+    });
+}
+
 int csrk_pcg_loss_grad(csrk_pattern A, const double *A_val, csrk_pattern L, const double *L_val, const double *b,
                        int n_it, double gamma, double *loss_host, double *resid_host, double *dL_val, void *ws,
                        size_t ws_bytes, csrk_stream_t stream)
@@ -215,6 +262,10 @@ int csrk_workspace_size(csrk_ws_op op, csrk_dtype dtype, const csrk_pattern *A, 
     case CSRK_WS_SPGEMM_BWD:
         if (!B) return CSRK_ERR_INVALID_ARG;
         st = spgemm_bwd(dtype, Ar, d, *B, d, Ar, d, (void *)d, (void *)d, b, 0);
+        break;
+    case CSRK_WS_SPADD_SYMBOLIC:
+        if (!B) return CSRK_ERR_INVALID_ARG;
+        st = spadd_symbolic(Ar, *B, (int64_t *)d, nullptr, (int64_t *)d, b, 0);
         break;
     case CSRK_WS_PCG: {
         if (!B || k < 1) return CSRK_ERR_INVALID_ARG;

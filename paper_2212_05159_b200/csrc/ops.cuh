@@ -23,6 +23,14 @@ int spgemm_numeric(csrk_dtype dt, const csrk_pattern &A, const void *A_val, cons
 int spgemm_bwd(csrk_dtype dt, const csrk_pattern &A, const void *A_val, const csrk_pattern &B, const void *B_val,
                const csrk_pattern &C, const void *dC, void *dA, void *dB, Bump &ws, cudaStream_t s);
 
+int spadd_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *C_indptr, int32_t *C_indices,
+                   int64_t *nnzC_host, Bump &ws, cudaStream_t s);
+int spadd_numeric(csrk_dtype dt, double alpha, double beta, const csrk_pattern &A, const void *A_val,
+                  const csrk_pattern &B, const void *B_val, const csrk_pattern &C, void *C_val, Bump &ws,
+                  cudaStream_t s);
+int spadd_bwd(csrk_dtype dt, double alpha, double beta, const csrk_pattern &A, const csrk_pattern &B,
+              const csrk_pattern &C, const void *dC, void *dA, void *dB, Bump &ws, cudaStream_t s);
+
 int pcg_loss_grad(const csrk_pattern &A, const double *Av, const csrk_pattern &L, const double *Lv, const double *b,
                   int N, double gamma, double *loss_host, double *resid_host, double *dL, Bump &ws, cudaStream_t s);
 

@@ -6,7 +6,8 @@ PyTorch fallback: if libcsrk.so is missing or a call fails, an exception is rais
 
 Names follow the ABI (and the paper's operations, Table 1):
 spmv_fwd / spmv_bwd (SpMV), spmm_fwd / spmm_bwd (SpDMM), csr_transpose,
-spgemm_symbolic / spgemm_numeric / spgemm_bwd (SpSpMM).
+spgemm_symbolic / spgemm_numeric / spgemm_bwd (SpSpMM), spadd_symbolic / spadd_numeric /
+spadd_bwd (Sp + Sp).
 """
 from __future__ import annotations
 
@@ -22,12 +23,13 @@ LIB_PATH = os.path.join(_PKG, "libcsrk.so")
 F32, F64 = 0, 1
 OP_N, OP_T = 0, 1
 WS = dict(spmv_fwd=0, spmv_bwd=1, spmm_fwd=2, spmm_bwd=3, csr_transpose=4, spgemm_symbolic=5,
-          spgemm_numeric=6, spgemm_bwd=7, pcg=8)
+          spgemm_numeric=6, spgemm_bwd=7, pcg=8, spadd_symbolic=9)
 
 # Every symbol declared in include/csrk.h (checked by tests/test_abi_cpu.py).
 ABI_SYMBOLS = ("csrk_spmv_fwd", "csrk_spmv_bwd", "csrk_spmm_fwd", "csrk_spmm_bwd", "csrk_csr_transpose",
                "csrk_spgemm_symbolic", "csrk_spgemm_numeric", "csrk_spgemm_bwd", "csrk_workspace_size",
-               "csrk_status_string", "csrk_launch_count", "csrk_version", "csrk_pcg_loss_grad")
+               "csrk_status_string", "csrk_launch_count", "csrk_version", "csrk_pcg_loss_grad",
+               "csrk_spadd_symbolic", "csrk_spadd_numeric", "csrk_spadd_bwd")
 
 
 class Pattern(ctypes.Structure):
@@ -65,6 +67,9 @@ def lib() -> ctypes.CDLL:
     L.csrk_workspace_size.argtypes = [I, I, PatP, PatP, I64, I, ctypes.POINTER(SZ)]
     D = ctypes.c_double
     L.csrk_pcg_loss_grad.argtypes = [Pat, P, Pat, P, P, I, D, ctypes.POINTER(D), ctypes.POINTER(D), P, P, SZ, P]
+    L.csrk_spadd_symbolic.argtypes = [Pat, Pat, P, P, ctypes.POINTER(I64), P, SZ, P]
+    L.csrk_spadd_numeric.argtypes = [I, D, Pat, P, D, Pat, P, Pat, P, P, SZ, P]
+    L.csrk_spadd_bwd.argtypes = [I, D, Pat, D, Pat, Pat, P, P, P, P, SZ, P]
     L.csrk_status_string.restype = ctypes.c_char_p
     L.csrk_status_string.argtypes = [I]
     L.csrk_launch_count.restype = ctypes.c_uint64
@@ -268,6 +273,45 @@ def spgemm_bwd(A: CSR, B: CSR, C: CSR, dC: torch.Tensor, need_dA: bool = True, n
     _check(lib().csrk_spgemm_bwd(dt, A.pattern(), _ptr(A.values), B.pattern(), _ptr(B.values), C.pattern(),
                                  _ptr(dC), _ptr(dA if need_dA else None), _ptr(dB if need_dB else None), ws, wsb,
                                  _stream()), "spgemm_bwd")
+    return (dA if need_dA else None), (dB if need_dB else None)
+
+
+def spadd_symbolic(A: CSR, B: CSR) -> CSR:
+    """pattern(alpha A + beta B) = pattern(A) U pattern(B), columns sorted.  One
+    host sync for nnz(C)."""
+    dev = A.indptr.device
+    Cp = torch.empty(A.nrows + 1, dtype=torch.int64, device=dev)
+    nnz = ctypes.c_int64(0)
+    ws, wsb = _workspace("spadd_symbolic", F64, A, B)
+    _check(lib().csrk_spadd_symbolic(A.pattern(), B.pattern(), _ptr(Cp), None, ctypes.byref(nnz), ws, wsb,
+                                     _stream()), "spadd_symbolic(count)")
+    Ci = torch.empty(int(nnz.value), dtype=torch.int32, device=dev)
+    if Ci.numel() > 0:
+        _check(lib().csrk_spadd_symbolic(A.pattern(), B.pattern(), _ptr(Cp), _ptr(Ci), None, ws, wsb, _stream()),
+               "spadd_symbolic(fill)")
+    return CSR(A.nrows, A.ncols, Cp, Ci, None)
+
+
+def spadd_numeric(alpha: float, A: CSR, beta: float, B: CSR, C: CSR, out: torch.Tensor | None = None):
+    """C = alpha A + beta B on C = spadd_symbolic(A, B)."""
+    dt = _dt(A.values)
+    Cv = out if out is not None else torch.empty(C.nnz, dtype=A.values.dtype, device=A.values.device)
+    _check(lib().csrk_spadd_numeric(dt, float(alpha), A.pattern(), _ptr(A.values), float(beta), B.pattern(),
+                                    _ptr(B.values), C.pattern(), _ptr(Cv), None, 0, _stream()), "spadd_numeric")
+    return Cv
+
+
+def spadd_bwd(alpha: float, A: CSR, beta: float, B: CSR, C: CSR, dC: torch.Tensor, need_dA: bool = True,
+              need_dB: bool = True, dA: torch.Tensor | None = None, dB: torch.Tensor | None = None):
+    """VJP of Sp+Sp (Table 1): dA = alpha dC (.) mask(A), dB = beta dC (.) mask(B)."""
+    dt = _dt(dC)
+    if need_dA and dA is None:
+        dA = torch.empty(A.nnz, dtype=dC.dtype, device=dC.device)
+    if need_dB and dB is None:
+        dB = torch.empty(B.nnz, dtype=dC.dtype, device=dC.device)
+    _check(lib().csrk_spadd_bwd(dt, float(alpha), A.pattern(), float(beta), B.pattern(), C.pattern(), _ptr(dC),
+                                _ptr(dA if need_dA else None), _ptr(dB if need_dB else None), None, 0, _stream()),
+           "spadd_bwd")
     return (dA if need_dA else None), (dB if need_dB else None)
 
 
