@@ -78,7 +78,8 @@ typedef enum {
     CSRK_WS_SPGEMM_NUMERIC = 6,
     CSRK_WS_SPGEMM_BWD = 7,
     CSRK_WS_PCG = 8,         /* B = L, k = n_it */
-    CSRK_WS_SPADD_SYMBOLIC = 9 /* numeric / bwd need no workspace */
+    CSRK_WS_SPADD_SYMBOLIC = 9,/* numeric / bwd need no workspace */
+    CSRK_WS_SPAI = 10        /* A = C = pattern(M A), B = R = pattern(I) U C, k = n */
 } csrk_ws_op;
 
 /*
@@ -207,6 +208,22 @@ int csrk_spadd_numeric(csrk_dtype dtype, double alpha, csrk_pattern A, const voi
 int csrk_spadd_bwd(csrk_dtype dtype, double alpha, csrk_pattern A, double beta, csrk_pattern B,
                    csrk_pattern C, const void *dC_val, void *dA_val, void *dB_val,
                    void *ws, size_t ws_bytes, csrk_stream_t stream);
+
+/*
+ * SPAI loss and gradient -- the SURVEY 8(f) row-f2 workload (PAPER 4.6):
+ *     loss = || I - M A ||_F^2   (Eq. spai_loss),
+ *     dM_val[nnz(M)] = d loss / d M.values on M's fixed pattern.
+ * Composed from this library's kernels (C = M A by csrk_spgemm_numeric, R = I - C by
+ * csrk_spadd_numeric, loss = sum R^2 and dR = 2R, dC by csrk_spadd_bwd, dM by the left VJP of
+ * csrk_spgemm_bwd); deterministic.  fp64.  A, M: n x n.  Cached patterns, built once by the
+ * caller: C = csrk_spgemm_symbolic(M, A); I = the n x n identity pattern (indptr[i] = i,
+ * indices[i] = i); R = csrk_spadd_symbolic(I, C).  loss_host: host pointer (required); the
+ * call synchronises `stream` once at the end.
+ * Workspace: csrk_workspace_size(CSRK_WS_SPAI, CSRK_F64, &C, &R, n, 0, &bytes).
+ */
+int csrk_spai_loss_grad(csrk_pattern A, const double *A_val, csrk_pattern M, const double *M_val,
+                        csrk_pattern C, csrk_pattern R, csrk_pattern I, double *loss_host, double *dM_val,
+                        void *ws, size_t ws_bytes, csrk_stream_t stream);
 
 /*
  * Learned-preconditioner PCG training step -- the config-5 composition of SURVEY 8(a) row a14

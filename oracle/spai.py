@@ -29,7 +29,7 @@ def spai_loss_grad(A_dense: np.ndarray, M_pattern: np.ndarray, M_dense: np.ndarr
     R = torch.eye(N, dtype=torch.float64) - M @ A
     loss = (R * R).sum()
     loss.backward()
-    return float(loss), torch.where(mask, Mv.grad, torch.zeros_like(Mv.grad)).numpy()
+    return float(loss.detach()), torch.where(mask, Mv.grad, torch.zeros_like(Mv.grad)).numpy()
 
 
 def spai_loss_by_columns(A_dense: np.ndarray, M_dense: np.ndarray) -> float:

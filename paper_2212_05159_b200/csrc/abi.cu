@@ -211,6 +211,28 @@ int csrk_spadd_bwd(csrk_dtype dtype, double alpha, csrk_pattern A, double beta, 
     });
 }
 
+int csrk_spai_loss_grad(csrk_pattern A, const double *A_val, csrk_pattern M, const double *M_val, csrk_pattern C,
+                        csrk_pattern R, csrk_pattern I, double *loss_host, double *dM_val, void *ws, size_t ws_bytes,
+                        csrk_stream_t stream)
+{
+    CSRK_TRY(check_pat(A));
+    CSRK_TRY(check_pat(M));
+    CSRK_TRY(check_pat(C));
+    CSRK_TRY(check_pat(R));
+    CSRK_TRY(check_pat(I));
+    const int64_t n = A.nrows;
+    if (A.ncols != n || M.nrows != n || M.ncols != n || C.nrows != n || C.ncols != n || R.nrows != n ||
+        R.ncols != n || I.nrows != n || I.ncols != n || I.nnz != n)
+        return CSRK_ERR_DIM_MISMATCH;
+    if (R.nnz < C.nnz || R.nnz < I.nnz) return CSRK_ERR_PATTERN;
+    if (!loss_host || !dM_val || (A.nnz > 0 && !A_val) || (M.nnz > 0 && !M_val)) return CSRK_ERR_INVALID_ARG;
+    CSRK_TRY(validate_pattern(A, (cudaStream_t)stream));
+    CSRK_TRY(validate_pattern(M, (cudaStream_t)stream));
+    return with_ws(ws, ws_bytes, [&](Bump &b) {
+        return spai_loss_grad(A, A_val, M, M_val, C, R, I, loss_host, dM_val, b, (cudaStream_t)stream);
+    });
+}
+
 int csrk_pcg_loss_grad(csrk_pattern A, const double *A_val, csrk_pattern L, const double *L_val, const double *b,
                        int n_it, double gamma, double *loss_host, double *resid_host, double *dL_val, void *ws,
                        size_t ws_bytes, csrk_stream_t stream)
@@ -267,6 +289,15 @@ int csrk_workspace_size(csrk_ws_op op, csrk_dtype dtype, const csrk_pattern *A, 
         if (!B) return CSRK_ERR_INVALID_ARG;
         st = spadd_symbolic(Ar, *B, (int64_t *)d, nullptr, (int64_t *)d, b, 0);
         break;
+    case CSRK_WS_SPAI: {
+        // A := C = pattern(M A), B := R = pattern(I) U C; k = n (rows of A and M)
+        if (!B || k < 0) return CSRK_ERR_INVALID_ARG;
+        csrk_pattern sq{k, k, Ar.nnz, Ar.indptr, Ar.indices};   // stand-in for A and M: sizes only
+        csrk_pattern In{k, k, k, Ar.indptr, Ar.indices};
+        double dummy = 0.0;
+        st = spai_loss_grad(sq, (const double *)d, sq, (const double *)d, Ar, *B, In, &dummy, (double *)d, b, 0);
+        break;
+    }
     case CSRK_WS_PCG: {
         if (!B || k < 1) return CSRK_ERR_INVALID_ARG;
         double dummy = 0.0;

@@ -31,6 +31,10 @@ int spadd_numeric(csrk_dtype dt, double alpha, double beta, const csrk_pattern &
 int spadd_bwd(csrk_dtype dt, double alpha, double beta, const csrk_pattern &A, const csrk_pattern &B,
               const csrk_pattern &C, const void *dC, void *dA, void *dB, Bump &ws, cudaStream_t s);
 
+int spai_loss_grad(const csrk_pattern &A, const double *Av, const csrk_pattern &M, const double *Mv,
+                   const csrk_pattern &C, const csrk_pattern &R, const csrk_pattern &I, double *loss_host,
+                   double *dM, Bump &ws, cudaStream_t s);
+
 int pcg_loss_grad(const csrk_pattern &A, const double *Av, const csrk_pattern &L, const double *Lv, const double *b,
                   int N, double gamma, double *loss_host, double *resid_host, double *dL, Bump &ws, cudaStream_t s);
 

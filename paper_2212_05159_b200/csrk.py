@@ -23,13 +23,13 @@ LIB_PATH = os.path.join(_PKG, "libcsrk.so")
 F32, F64 = 0, 1
 OP_N, OP_T = 0, 1
 WS = dict(spmv_fwd=0, spmv_bwd=1, spmm_fwd=2, spmm_bwd=3, csr_transpose=4, spgemm_symbolic=5,
-          spgemm_numeric=6, spgemm_bwd=7, pcg=8, spadd_symbolic=9)
+          spgemm_numeric=6, spgemm_bwd=7, pcg=8, spadd_symbolic=9, spai=10)
 
 # Every symbol declared in include/csrk.h (checked by tests/test_abi_cpu.py).
 ABI_SYMBOLS = ("csrk_spmv_fwd", "csrk_spmv_bwd", "csrk_spmm_fwd", "csrk_spmm_bwd", "csrk_csr_transpose",
                "csrk_spgemm_symbolic", "csrk_spgemm_numeric", "csrk_spgemm_bwd", "csrk_workspace_size",
                "csrk_status_string", "csrk_launch_count", "csrk_version", "csrk_pcg_loss_grad",
-               "csrk_spadd_symbolic", "csrk_spadd_numeric", "csrk_spadd_bwd")
+               "csrk_spadd_symbolic", "csrk_spadd_numeric", "csrk_spadd_bwd", "csrk_spai_loss_grad")
 
 
 class Pattern(ctypes.Structure):
@@ -70,6 +70,7 @@ def lib() -> ctypes.CDLL:
     L.csrk_spadd_symbolic.argtypes = [Pat, Pat, P, P, ctypes.POINTER(I64), P, SZ, P]
     L.csrk_spadd_numeric.argtypes = [I, D, Pat, P, D, Pat, P, Pat, P, P, SZ, P]
     L.csrk_spadd_bwd.argtypes = [I, D, Pat, D, Pat, Pat, P, P, P, P, SZ, P]
+    L.csrk_spai_loss_grad.argtypes = [Pat, P, Pat, P, Pat, Pat, Pat, ctypes.POINTER(D), P, P, SZ, P]
     L.csrk_status_string.restype = ctypes.c_char_p
     L.csrk_status_string.argtypes = [I]
     L.csrk_launch_count.restype = ctypes.c_uint64
@@ -313,6 +314,43 @@ def spadd_bwd(alpha: float, A: CSR, beta: float, B: CSR, C: CSR, dC: torch.Tenso
                                 _ptr(dA if need_dA else None), _ptr(dB if need_dB else None), None, 0, _stream()),
            "spadd_bwd")
     return (dA if need_dA else None), (dB if need_dB else None)
+
+
+@dataclass
+class SpaiPlan:
+    """Cached patterns of the SPAI workload: C = pattern(M A), the identity
+    pattern I and R = pattern(I) U C.  Value-independent: built once per pattern(M), pattern(A)."""
+    C: CSR
+    I: CSR
+    R: CSR
+
+
+def spai_plan(M: CSR, A: CSR) -> SpaiPlan:
+    n = A.nrows
+    dev = A.indptr.device
+    I = CSR(n, n, torch.arange(n + 1, dtype=torch.int64, device=dev), torch.arange(n, dtype=torch.int32, device=dev))
+    C = spgemm_symbolic(M, A)
+    return SpaiPlan(C, I, spadd_symbolic(I, C))
+
+
+def spai_loss_grad(plan: SpaiPlan, M: CSR, A: CSR, dM: torch.Tensor | None = None):
+    """loss = ||I - M A||_F^2 and d loss / d M.values (PAPER 4.6).  fp64."""
+    if dM is None:
+        dM = torch.empty_like(M.values)
+    pc, pr = plan.C.pattern(), plan.R.pattern()
+    nbytes = ctypes.c_size_t(0)
+    _check(lib().csrk_workspace_size(WS["spai"], F64, ctypes.byref(pc), ctypes.byref(pr), A.nrows, 0,
+                                     ctypes.byref(nbytes)), "workspace_size(spai)")
+    dev = A.indptr.device
+    buf = _ws_cache.get(dev)
+    if buf is None or buf.numel() < int(nbytes.value):
+        buf = torch.empty(max(int(nbytes.value), 1 << 20), dtype=torch.uint8, device=dev)
+        _ws_cache[dev] = buf
+    loss = ctypes.c_double(0.0)
+    _check(lib().csrk_spai_loss_grad(A.pattern(), _ptr(A.values), M.pattern(), _ptr(M.values), pc, pr,
+                                     plan.I.pattern(), ctypes.byref(loss), _ptr(dM), _ptr(buf), buf.numel(),
+                                     _stream()), "spai_loss_grad")
+    return float(loss.value), dM
 
 
 def pcg_loss_grad(A: CSR, L: CSR, b: torch.Tensor, n_it: int = 50, gamma: float = 0.6,
