@@ -22,6 +22,7 @@ OP_OF = [  # (substring of the kernel name, op) -- order of the step in bench.py
     ("k_rows<double, 0, 0, 0>", "spmv_fwd"), ("k_rows_long<double, 0, 0, 0>", "spmv_fwd"),
     ("k_rows<double, 1, 0, 1>", "spmv_bwd"), ("k_rows_long<double, 1, 0, 1>", "spmv_bwd"),
     ("k_spmm<double, 8, 4, 0>", "spmm_fwd"), ("k_spmm<double, 8, 4, 3>", "spmm_bwd"),
+    ("k_spmm_wide<double, 2, 0", "spmm_fwd"), ("k_spmm_wide<double, 2, 3", "spmm_bwd"),
     ("k_gemm_S<double, 0>", "spgemm_symbolic"), ("k_gemm_big_sym<0>", "spgemm_symbolic"),
     ("k_gemm_S<double, 1>", "spgemm_symbolic"), ("k_gemm_big_sym<1>", "spgemm_symbolic"),
     ("k_gemm_S<double, 2>", "spgemm_numeric"), ("k_gemm_big_val<double, 2>", "spgemm_numeric"),
