@@ -124,6 +124,101 @@ def run_cfg5(args, torch, ck):
     return 0
 
 
+def run_ops_workload(args, torch, ck, cfg):
+    """BASELINE configs 3 and 4 at N = 1, op by op: each op timed with CUDA
+    events on the launching stream, L2 flushed (512 MiB write) before every timed op.
+      cfg3: 3D 7-point Poisson 160^3, fp64, C = A A: symbolic (count + host sync + fill), numeric
+            on the reused pattern, backward (dA and dB, summed by the caller per reading A13).
+      cfg4: power-law n = 2^23, 16 nnz/row, fp32: spmv fwd, spmv bwd (atomic dx), transpose,
+            spmv bwd with the plan, then C = A A symbolic / numeric / backward (nnz(C) ~ 2.1e9)."""
+    dev = torch.device("cuda", 0)
+    if cfg == 3:
+        A = synth.poisson3d(160)
+        s, dt_np, dt = 8, np.float64, torch.float64
+    else:
+        A = synth.powerlaw()
+        s, dt_np, dt = 4, np.float32, torch.float32
+    m, n, nnz = A.nrows, A.ncols, A.nnz
+    Ad = ck.CSR.from_host(A)
+    lens = np.diff(A.indptr)
+    prod = int(lens[A.indices].sum())
+    del A
+    x = torch.from_numpy(synth.dense(n, synth.seed_of(cfg, 3), dt_np)).to(dev)
+    dy = torch.from_numpy(synth.dense(m, synth.seed_of(cfg, 4), dt_np)).to(dev)
+    y, dA_v, dx = torch.empty(m, dtype=dt, device=dev), torch.empty(nnz, dtype=dt, device=dev), \
+        torch.empty(n, dtype=dt, device=dev)
+    plan = ck.csr_transpose(Ad, with_values=False)
+    C = ck.spgemm_symbolic(Ad, Ad)
+    nnzC = C.nnz
+    q = torch.arange(nnzC, device=dev, dtype=torch.int64)  # counter-based dC (too large for the host at cfg4)
+    dC = (((q * 2654435761 + 12345) % 1000003).to(torch.float64) / 500001.5 - 1.0).to(dt)
+    del q
+    Cv = torch.empty(nnzC, dtype=dt, device=dev)
+    dA_g, dB_g = torch.empty(nnz, dtype=dt, device=dev), torch.empty(nnz, dtype=dt, device=dev)
+    c = op_costs(m, n, nnz, nnzC, prod, k=1, s=s)
+    ops = {}
+    if cfg == 4:
+        ops["spmv_fwd"] = (lambda: ck.spmv_fwd(Ad, x, out=y), c["spmv_fwd"])
+        ops["spmv_bwd"] = (lambda: ck.spmv_bwd(Ad, x, dy, dA=dA_v, dx=dx), c["spmv_bwd"])
+        ops["csr_transpose"] = (lambda: ck.csr_transpose(Ad, with_values=False, out=plan), c["csr_transpose"])
+        ops["spmv_bwd_plan"] = (lambda: ck.spmv_bwd(Ad, x, dy, plan=plan, dA=dA_v, dx=dx), c["spmv_bwd"])
+    ops["spgemm_symbolic"] = (lambda: ck.spgemm_symbolic(Ad, Ad), c["spgemm_symbolic"])
+    ops["spgemm_numeric"] = (lambda: ck.spgemm_numeric(Ad, Ad, C, out=Cv), c["spgemm_numeric"])
+    ops["spgemm_bwd"] = (lambda: ck.spgemm_bwd(Ad, Ad, C, dC, dA=dA_g, dB=dB_g), c["spgemm_bwd"])
+    l2 = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        for f, _c in ops.values():
+            f()
+    torch.cuda.synchronize()
+    times = {k: [] for k in ops}
+    l0 = ck.launch_count()
+    with Clocks(0) as clk:
+        for _ in range(args.steps):
+            for k, (f, _c) in ops.items():
+                l2.zero_()
+                a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                f()
+                e.record(st)
+                times[k].append((a, e))
+        torch.cuda.synchronize()
+    launches = ck.launch_count() - l0
+    peak = _peak()
+    rep = {}
+    tot_b, tot_f, tot_ms = 0, 0, 0.0
+    for k, ev in times.items():
+        ms = float(np.median([a.elapsed_time(e) for a, e in ev]))
+        b, fl = ops[k][1]
+        rep[k] = {"ms": round(ms, 4), "GB/s": round(b / ms / 1e6, 1), "GFLOP/s": round(fl / ms / 1e6, 1),
+                  "frac": round(b / ms / 1e6 / peak, 3), "bytes": b}
+        if k != "spmv_bwd_plan":
+            tot_b, tot_f, tot_ms = tot_b + b, tot_f + fl, tot_ms + ms
+    dom = max((k for k in rep if k != "spmv_bwd_plan"), key=lambda k: rep[k]["ms"])
+    wl = ("config3: 3D Poisson 7-point 160^3 (4,096,000 rows, 28,518,400 nnz), fp64, C = A A "
+          f"(nnz(C) {nnzC:,}, prod {prod:,}): symbolic + numeric + bwd" if cfg == 3 else
+          "config4: power-law n = 2^23, 2^27 nnz, rows 8..32,769, fp32: spmv fwd/bwd, transpose, C = A A "
+          f"(nnz(C) {nnzC:,}, prod {prod:,}) symbolic + numeric + bwd")
+    out = {"metric": f"SpMV/SpGEMM fwd+bwd algorithmic GB/s (config {cfg})",
+           "value": round(tot_b / tot_ms / 1e6, 2), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(tot_ms, 4), "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64" if cfg == 3 else "f32", "data": "synthetic",
+           "config": {"workload": wl, "l2": "flushed (512 MiB write) before every timed op"},
+           "gflops": round(tot_f / tot_ms / 1e6, 2),
+           "roofline": {"bound": "hbm", "kernel": dom, "achieved": rep[dom]["GB/s"], "peak": peak,
+                        "unit": "GB/s", "frac": rep[dom]["frac"], "traffic": None},
+           "ops": rep, "gpu_launches": int(launches / max(args.steps, 1)), "clocks": clk.summary()}
+    print(json.dumps(out))
+    return 0
+
+
+def _peak():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except Exception:
+        return 6650.0
+
+
 # ---------------------------------------------------------------- clocks sampler
 class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
@@ -326,7 +421,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -338,6 +433,8 @@ def main():
 
     if args.workload == "cfg5":
         return run_cfg5(args, torch, ck)
+    if args.workload in ("cfg3", "cfg4"):
+        return run_ops_workload(args, torch, ck, int(args.workload[-1]))
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -65,6 +65,10 @@ def lib():
         L.orc_spadd_numeric.restype = ctypes.c_int
         L.orc_spadd_bwd.argtypes = [_I64, ctypes.c_double, ctypes.c_double] + [_P] * 9
         L.orc_spadd_bwd.restype = ctypes.c_int
+        L.orc_sptrsv.argtypes = [ctypes.c_int, ctypes.c_int, _I64] + [_P] * 6
+        L.orc_sptrsv.restype = ctypes.c_int
+        L.orc_sptrsv_bwd.argtypes = [ctypes.c_int, ctypes.c_int, _I64] + [_P] * 8
+        L.orc_sptrsv_bwd.restype = ctypes.c_int
         L.orc_set_threads.argtypes = [ctypes.c_int]
         L.orc_get_threads.restype = ctypes.c_int
     return _lib
@@ -253,3 +257,41 @@ def spadd_bwd(alpha, A, beta, B, Cp, Ci, dC, want_dA: bool = True, want_dB: bool
     if rc != 0:
         raise ValueError("spadd_bwd: V's pattern misses an entry of A or B")
     return (None if dA is None else _out(dA, dt)), (None if dB is None else _out(dB, dt))
+
+
+class TriangularError(ValueError):
+    pass
+
+
+def _trsv_rc(rc, what):
+    if rc == -2:
+        raise TriangularError(f"{what}: stored entry on the wrong side of the diagonal (S:203 shape error)")
+    if rc == -3:
+        raise TriangularError(f"{what}: missing diagonal with unit_diag = False (S:203 singular)")
+
+
+def sptrsv(T, b, upper: bool = False, unit: bool = False) -> Result:
+    """x = T^{-1} b by forward (lower) or backward (upper) substitution.
+    S = M(T)^{-1} |T| |x| (the componentwise error magnitude, DESIGN reading R-TRSV)."""
+    assert T.nrows == T.ncols and b.shape == (T.nrows,)
+    ip, ix = _pat(T)
+    dt = T.values.dtype
+    x = np.empty(T.nrows, np.float64)
+    S = np.empty(T.nrows, np.float64)
+    _trsv_rc(lib().orc_sptrsv(int(upper), int(unit), T.nrows, _p(ip), _p(ix), _p(_f64(T.values)), _p(_f64(b)),
+                          _p(x), _p(S)), "sptrsv")
+    return Result(_out(x, dt), S)
+
+
+def sptrsv_bwd(T, x, v, upper: bool = False, unit: bool = False, want_dT: bool = True, want_db: bool = True):
+    """VJP of x = T^{-1} b (Table 1): db = T^{-T} v, dT = -db x^T (.) mask(T).
+    Returns (dT on T's pattern, Result(db, S))."""
+    ip, ix = _pat(T)
+    dt = T.values.dtype
+    dT = np.empty(T.nnz, np.float64) if want_dT else None
+    db = np.empty(T.nrows, np.float64)
+    S = np.empty(T.nrows, np.float64)
+    _trsv_rc(lib().orc_sptrsv_bwd(int(upper), int(unit), T.nrows, _p(ip), _p(ix), _p(_f64(T.values)), _p(_f64(x)),
+                                  _p(_f64(v)), _p(dT), _p(db), _p(S)), "sptrsv_bwd")
+    return (None if dT is None else _out(dT, dt)), (Result(_out(db, dt), S) if want_db else None)
+

@@ -459,3 +459,88 @@ int orc_spadd_bwd(int64_t m, double alpha, double beta,
     }
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* SpTRSV  x = T^{-1} b, T triangular  (PAPER 3.1.5; Table 2) */
+/* ------------------------------------------------------------------------ */
+
+/* Forward: "each row depends on the intermediate values of previous rows only".
+ *   lower (upper == 0): for i = 0, 1, ..., n-1   x_i = (b_i - sum_{p in row i, j < i} T[p] x_j) / d_i
+ *   upper (upper == 1): for i = n-1, ..., 0      x_i = (b_i - sum_{p in row i, j > i} T[p] x_j) / d_i
+ *     (P:482 converts U x = b by "matrix flip operations" into a lower system; the flip
+ *      reverses the row and column order, i.e. this backward substitution -- SPEC S:202)
+ *   d_i = the stored diagonal T_ii, or 1 when unit != 0 (a stored diagonal is then unused).
+ * The numerator is accumulated in long double (p ascending) and divided there; x_i is rounded
+ * once to double.  S (nullable) receives the componentwise forward-error magnitude
+ *   S = M(T)^{-1} (|T| |x|),   M(T) = comparison matrix (|d_i| on the diagonal, -|T_ij| off it),
+ * the textbook bound |x - x_computed| <= gamma * M(T)^{-1}|T||x| for substitution (reading
+ * R-TRSV in DESIGN.md).  Returns 0, -2 if an entry lies on the wrong side of the diagonal
+ * ("L_ij != 0 if i >= j"; SPEC S:203 shape error), -3 if a diagonal is missing and
+ * unit == 0 (singular).  A zero stored diagonal divides by zero (IEEE). */
+int orc_sptrsv(int upper, int unit, int64_t n, const int64_t *indptr, const int32_t *indices,
+               const double *val, const double *b, double *x, double *S)
+{
+    for (int64_t i = 0; i < n; ++i) {
+        int has_d = 0;
+        for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) {
+            if (indices[p] == i) has_d = 1;
+            if (upper ? indices[p] < i : indices[p] > i) return -2;
+        }
+        if (!has_d && !unit) return -3;
+    }
+    for (int64_t t = 0; t < n; ++t) {
+        const int64_t i = upper ? n - 1 - t : t;
+        acc_t s = (acc_t)b[i];
+        acc_t d = 1;
+        for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) {
+            if (indices[p] == i) { if (!unit) d = (acc_t)val[p]; continue; }
+            s -= (acc_t)val[p] * (acc_t)x[indices[p]];
+        }
+        x[i] = (double)(s / d);
+    }
+    if (S) {
+        for (int64_t t = 0; t < n; ++t) {
+            const int64_t i = upper ? n - 1 - t : t;
+            acc_t tx = 0, off = 0, d = 1;
+            for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) {
+                const int32_t j = indices[p];
+                if (j == i) { if (!unit) d = fabsl((acc_t)val[p]); continue; }
+                tx += fabsl((acc_t)val[p] * (acc_t)x[j]);
+                off += fabsl((acc_t)val[p]) * (acc_t)S[j];
+            }
+            tx += d * fabsl((acc_t)x[i]);
+            S[i] = (double)((tx + off) / d);
+        }
+    }
+    return 0;
+}
+
+/* VJP (Table 1 SpSolve row P:290-293 applied to a triangular T):
+ *   db = T^{-T} v   "we first find L^{-T} v with our existing forward triangular solve routine":
+ *                   T^T (the oracle's own counting-sort transpose, stored values kept) is
+ *                   triangular on the other side, solved by orc_sptrsv with !upper;
+ *   dT = -(db) x^T (.) mask(T)   "the masked outer-product ... in parallel over the nonzero
+ *                   entries": dT[p] = -(db_i x_j), one IEEE double multiply; with unit != 0 a
+ *                   stored diagonal is unused, so its gradient is 0.
+ * dT, db nullable; S_db as in orc_sptrsv (for T^T).  Returns orc_sptrsv's codes. */
+int orc_sptrsv_bwd(int upper, int unit, int64_t n, const int64_t *indptr, const int32_t *indices,
+                   const double *val, const double *x, const double *v,
+                   double *dT, double *db, double *S_db)
+{
+    const int64_t nnz = indptr[n];
+    int64_t *Tp = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
+    int32_t *Ti = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nnz > 0 ? nnz : 1));
+    double *Tv = (double *)malloc(sizeof(double) * (size_t)(nnz > 0 ? nnz : 1));
+    double *w = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    orc_csr_transpose(n, n, indptr, indices, val, Tp, Ti, Tv, NULL);
+    int rc = orc_sptrsv(!upper, unit, n, Tp, Ti, Tv, v, w, S_db);
+    if (rc == 0) {
+        if (db) memcpy(db, w, sizeof(double) * (size_t)n);
+        if (dT)
+            for (int64_t i = 0; i < n; ++i)
+                for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p)
+                    dT[p] = (unit && indices[p] == i) ? 0.0 : -(w[i] * x[indices[p]]);
+    }
+    free(Tp); free(Ti); free(Tv); free(w);
+    return rc;
+}

@@ -195,3 +195,40 @@ def int_values(rng: np.random.Generator, size, dtype=np.float64) -> np.ndarray:
 def dense(shape, seed: int, dtype=np.float64, values: str = "real") -> np.ndarray:
     rng = np.random.default_rng(seed)
     return real_values(rng, shape, dtype) if values == "real" else int_values(rng, shape, dtype)
+
+
+def tri_random(n: int, density: float, seed: int, upper: bool = False, values: str = "real",
+               unit: bool = False) -> CSR:
+    """Random triangular matrix for the SpTRSV tests (PAPER 3.1.5): a Bernoulli(density)
+    pattern strictly below (or above) the diagonal plus the diagonal (omitted when unit).
+    'real': off-diagonal U[-1, 1) / (1 + row length), diagonal +-U[1, 2) -- diagonally
+    dominant, so substitution is well conditioned.  'int': off-diagonal U{-3..3}, diagonal
+    from {+-1, +-2, +-4} (so b = T x_int keeps every step exact in binary floating point)."""
+    rng = np.random.default_rng(seed)
+    mask = rng.random((n, n)) < density
+    mask = np.triu(mask, 1) if upper else np.tril(mask, -1)
+    if not unit:
+        mask |= np.eye(n, dtype=bool)
+    counts = mask.sum(axis=1, dtype=np.int64)
+    indptr = np.zeros(n + 1, np.int64)
+    np.cumsum(counts, out=indptr[1:])
+    rows, cols = np.nonzero(mask)
+    diag = rows == cols
+    if values == "real":
+        vals = rng.uniform(-1.0, 1.0, rows.size) / (1.0 + counts[rows])
+        vals[diag] = rng.choice([-1.0, 1.0], diag.sum()) * rng.uniform(1.0, 2.0, diag.sum())
+    else:
+        vals = rng.integers(-3, 4, rows.size).astype(np.float64)
+        vals[diag] = rng.choice([-4.0, -2.0, -1.0, 1.0, 2.0, 4.0], diag.sum())
+    return CSR(n, n, indptr, cols.astype(np.int32), vals)
+
+
+def lower_part(A: CSR) -> CSR:
+    """The lower triangle (j <= i) of A, entries kept in place -- e.g. the IC(0) pattern of a
+    Poisson matrix (SURVEY 8(f) f3 workload)."""
+    rows = np.repeat(np.arange(A.nrows, dtype=np.int64), np.diff(A.indptr))
+    keep = A.indices <= rows
+    indptr = np.zeros(A.nrows + 1, np.int64)
+    np.cumsum(np.bincount(rows[keep], minlength=A.nrows), out=indptr[1:])
+    return CSR(A.nrows, A.ncols, indptr, A.indices[keep].copy(),
+               None if A.values is None else A.values[keep].copy())
