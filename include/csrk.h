@@ -79,7 +79,9 @@ typedef enum {
     CSRK_WS_SPGEMM_BWD = 7,
     CSRK_WS_PCG = 8,         /* B = L, k = n_it */
     CSRK_WS_SPADD_SYMBOLIC = 9,/* numeric / bwd need no workspace */
-    CSRK_WS_SPAI = 10        /* A = C = pattern(M A), B = R = pattern(I) U C, k = n */
+    CSRK_WS_SPAI = 10,       /* A = C = pattern(M A), B = R = pattern(I) U C, k = n */
+    CSRK_WS_SPTRSV_FWD = 11, /* A = T */
+    CSRK_WS_SPTRSV_BWD = 12  /* A = T; have_plan = 1 if T^T (pattern + perm) is passed */
 } csrk_ws_op;
 
 /*
@@ -224,6 +226,40 @@ int csrk_spadd_bwd(csrk_dtype dtype, double alpha, csrk_pattern A, double beta, 
 int csrk_spai_loss_grad(csrk_pattern A, const double *A_val, csrk_pattern M, const double *M_val,
                         csrk_pattern C, csrk_pattern R, csrk_pattern I, double *loss_host, double *dM_val,
                         void *ws, size_t ws_bytes, csrk_stream_t stream);
+
+/*
+ * Sparse triangular solve (PAPER 3.1.5):  x = T^{-1} b.
+ *   upper = 0: T lower triangular ("L_ij != 0 if i >= j"); forward substitution
+ *              x_i = (b_i - sum_{j<i} T_ij x_j) / T_ii ("each row depends on the intermediate
+ *              values of previous rows only").
+ *   upper = 1: T upper triangular, solved in reverse row order (the "matrix flip" of P:482).
+ *   unit_diag: the diagonal is taken as 1 (a stored diagonal entry is then unused).
+ * T is n x n, canonical CSR; b[n], x[n] (overwritten; must not alias b).  Method: a one-pass
+ * decoupled look-back scan when every row depends only on its neighbour (bidiagonal chains),
+ * otherwise the synchronisation-free solve of P:487 (see sptrsv.cu).  Stored entries on the
+ * wrong side of the diagonal are ignored, a missing / zero diagonal (unit_diag = 0) divides
+ * by zero; with CSRK_VALIDATE=1 both are rejected (CSRK_ERR_PATTERN).
+ * Workspace: csrk_workspace_size(CSRK_WS_SPTRSV_FWD, dtype, &T, NULL, 0, 0, &bytes).
+ */
+int csrk_sptrsv_fwd(csrk_dtype dtype, csrk_pattern T, const void *T_val, int upper, int unit_diag, const void *b,
+                    void *x, void *ws, size_t ws_bytes, csrk_stream_t stream);
+
+/*
+ * SpTRSV backward = VJP of x = T^{-1} b (Table 1 SpSolve row P:290-293):
+ *   db = T^{-T} v                 ("we first find L^{-T} v with our existing forward triangular
+ *                                   solve routine": the same solve on T^T, triangular on the
+ *                                   other side)
+ *   dT = -(db) x^T (.) mask(T)    (dT[p] = -(db_i x_j) at stored (i, j); "the masked
+ *                                   outer-product can be executed in parallel over the nonzero
+ *                                   entries"); with unit_diag a stored diagonal gets 0.
+ * x = the forward solution (saved operand), v = dL/dx.  dT_val[nnz] and db[n] nullable (both
+ * NULL: no-op); db must not alias v.  TT / TT_perm: optional cached transpose plan of T from
+ * csrk_csr_transpose (both NULL: T^T is built in the workspace).
+ * Workspace: csrk_workspace_size(CSRK_WS_SPTRSV_BWD, dtype, &T, NULL, 0, have_plan, &bytes).
+ */
+int csrk_sptrsv_bwd(csrk_dtype dtype, csrk_pattern T, const void *T_val, const csrk_pattern *TT,
+                    const int64_t *TT_perm, int upper, int unit_diag, const void *x, const void *v, void *dT_val,
+                    void *db, void *ws, size_t ws_bytes, csrk_stream_t stream);
 
 /*
  * Learned-preconditioner PCG training step -- the config-5 composition of SURVEY 8(a) row a14

@@ -233,6 +233,38 @@ int csrk_spai_loss_grad(csrk_pattern A, const double *A_val, csrk_pattern M, con
     });
 }
 
+int csrk_sptrsv_fwd(csrk_dtype dtype, csrk_pattern T, const void *T_val, int upper, int unit_diag, const void *b,
+                    void *x, void *ws, size_t ws_bytes, csrk_stream_t stream)
+{
+    CSRK_TRY(check_dtype(dtype));
+    CSRK_TRY(check_pat(T));
+    if (T.nrows != T.ncols) return CSRK_ERR_DIM_MISMATCH;
+    if ((T.nrows > 0 && (!b || !x)) || (T.nnz > 0 && !T_val)) return CSRK_ERR_INVALID_ARG;
+    CSRK_TRY(validate_pattern(T, (cudaStream_t)stream));
+    CSRK_TRY(validate_triangular(T, upper, unit_diag, (cudaStream_t)stream));
+    return with_ws(ws, ws_bytes, [&](Bump &bw) {
+        return sptrsv_fwd(dtype, T, T_val, upper ? 1 : 0, unit_diag ? 1 : 0, b, x, bw, (cudaStream_t)stream);
+    });
+}
+
+int csrk_sptrsv_bwd(csrk_dtype dtype, csrk_pattern T, const void *T_val, const csrk_pattern *TT,
+                    const int64_t *TT_perm, int upper, int unit_diag, const void *x, const void *v, void *dT_val,
+                    void *db, void *ws, size_t ws_bytes, csrk_stream_t stream)
+{
+    CSRK_TRY(check_dtype(dtype));
+    CSRK_TRY(check_pat(T));
+    CSRK_TRY(check_plan(T, TT, TT_perm));
+    if (T.nrows != T.ncols) return CSRK_ERR_DIM_MISMATCH;
+    if (!dT_val && !db) return CSRK_OK;
+    if ((T.nrows > 0 && (!x || !v)) || (T.nnz > 0 && !T_val)) return CSRK_ERR_INVALID_ARG;
+    CSRK_TRY(validate_pattern(T, (cudaStream_t)stream));
+    CSRK_TRY(validate_triangular(T, upper, unit_diag, (cudaStream_t)stream));
+    return with_ws(ws, ws_bytes, [&](Bump &bw) {
+        return sptrsv_bwd(dtype, T, T_val, TT, TT_perm, upper ? 1 : 0, unit_diag ? 1 : 0, x, v, dT_val, db, bw,
+                          (cudaStream_t)stream);
+    });
+}
+
 int csrk_pcg_loss_grad(csrk_pattern A, const double *A_val, csrk_pattern L, const double *L_val, const double *b,
                        int n_it, double gamma, double *loss_host, double *resid_host, double *dL_val, void *ws,
                        size_t ws_bytes, csrk_stream_t stream)
@@ -298,6 +330,10 @@ int csrk_workspace_size(csrk_ws_op op, csrk_dtype dtype, const csrk_pattern *A, 
         st = spai_loss_grad(sq, (const double *)d, sq, (const double *)d, Ar, *B, In, &dummy, (double *)d, b, 0);
         break;
     }
+    case CSRK_WS_SPTRSV_FWD: st = sptrsv_fwd(dtype, Ar, d, 0, 0, d, (void *)d, b, 0); break;
+    case CSRK_WS_SPTRSV_BWD:
+        st = sptrsv_bwd(dtype, Ar, d, plan, pperm, 0, 0, d, d, (void *)d, (void *)d, b, 0);
+        break;
     case CSRK_WS_PCG: {
         if (!B || k < 1) return CSRK_ERR_INVALID_ARG;
         double dummy = 0.0;

@@ -87,6 +87,7 @@ size_t scan_ws_bytes(int64_t n);
 
 // Row-length classification etc.
 int validate_pattern(const csrk_pattern &A, cudaStream_t s);  // honours CSRK_VALIDATE
+int validate_triangular(const csrk_pattern &A, int upper, int unit, cudaStream_t s);  // honours CSRK_VALIDATE
 
 // Internal transpose (pattern + perm, optional values) used by ops that need A^T when
 // the caller passes no plan.  ws sized by transpose_ws(A).

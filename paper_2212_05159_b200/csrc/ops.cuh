@@ -35,6 +35,11 @@ int spai_loss_grad(const csrk_pattern &A, const double *Av, const csrk_pattern &
                    const csrk_pattern &C, const csrk_pattern &R, const csrk_pattern &I, double *loss_host,
                    double *dM, Bump &ws, cudaStream_t s);
 
+int sptrsv_fwd(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int upper, int unit, const void *b, void *x,
+               Bump &ws, cudaStream_t s);
+int sptrsv_bwd(csrk_dtype dt, const csrk_pattern &A, const void *A_val, const csrk_pattern *AT, const int64_t *perm,
+               int upper, int unit, const void *x, const void *v, void *dA, void *db, Bump &ws, cudaStream_t s);
+
 int pcg_loss_grad(const csrk_pattern &A, const double *Av, const csrk_pattern &L, const double *Lv, const double *b,
                   int N, double gamma, double *loss_host, double *resid_host, double *dL, Bump &ws, cudaStream_t s);
 

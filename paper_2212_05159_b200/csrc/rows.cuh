@@ -3,8 +3,11 @@
 // k_rows: one thread per row.  Rows of at most kShortRow nonzeros are processed by their
 // thread; the thread's index/value loads are contiguous, and across a warp the L1 serves the
 // neighbouring rows' lines, so short-row matrices (stencils) stream at near copy bandwidth
-// without staging or block synchronisation.  Longer rows are appended (warp-aggregated) to a
-// list that k_rows_long processes with one warp per row (coalesced over the row).
+// without staging or block synchronisation.  Rows of kShortRow < l <= kHugeRow are then taken
+// by the whole warp one at a time (coalesced over the row); longer rows are appended
+// (warp-aggregated) to a list that k_rows_long processes with one CTA per row.  Per-element
+// modes (scatter, transpose) stream the warp's element range instead, unless it holds a
+// huge row.
 // Modes (same semantics as tile.cuh):
 //   REDUCE    y[row] = sum_p val(pv) v[idx p]  (in p order -- the oracle's order -- for short
 //             rows; lane-strided + fixed shuffle tree for long rows; both deterministic)
@@ -19,6 +22,7 @@
 namespace csrk {
 
 constexpr int kShortRow = 32;
+constexpr int kHugeRow = 4096;
 constexpr int kRowsTPB = 256;
 
 struct RowList {
@@ -48,6 +52,8 @@ __device__ __forceinline__ void row_elem(const TileArgs<T> &a, int64_t row, int6
 template <typename T, int MODE, bool PERM, bool SIDE>
 __global__ __launch_bounds__(kRowsTPB) void k_rows(TileArgs<T> a, RowList L)
 {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
     const int64_t row = (int64_t)blockIdx.x * kRowsTPB + threadIdx.x;
     const bool valid = row < a.nrows;
     int64_t s = 0, e = 0;
@@ -55,54 +61,102 @@ __global__ __launch_bounds__(kRowsTPB) void k_rows(TileArgs<T> a, RowList L)
         s = a.indptr[row];
         e = a.indptr[row + 1];
     }
-    const bool lng = valid && e - s > kShortRow;
-    const unsigned lm = __ballot_sync(0xffffffffu, lng);
-    if (lm) {
-        const int lane = threadIdx.x & 31;
+    const bool huge = valid && e - s > kHugeRow;
+    const unsigned hm = __ballot_sync(FULL, huge);
+    if (hm) {  // rows longer than kHugeRow: one CTA each in k_rows_long
         int base = 0;
-        if (lane == 0) base = atomicAdd(L.count, __popc(lm));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (lng) L.rows[base + __popc(lm & ((1u << lane) - 1))] = (int32_t)row;
+        if (lane == 0) base = atomicAdd(L.count, __popc(hm));
+        base = __shfl_sync(FULL, base, 0);
+        if (huge) L.rows[base + __popc(hm & ((1u << lane) - 1))] = (int32_t)row;
     }
-    if (MODE != MODE_REDUCE && !lm) {
-        // per-element outputs (scatter / transpose): the warp's 32 rows span one contiguous
-        // element range; map element -> row in shared memory, then stream the range coalesced
-        __shared__ uint8_t s_rw[kRowsTPB / 32][32 * kShortRow];
-        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-        const int64_t e0 = __shfl_sync(0xffffffffu, s, 0);
-        const int64_t elast = valid ? e : 0;
-        const int64_t e1 = __reduce_max_sync(0xffffffffu, (unsigned)(elast - e0 < 0 ? 0 : elast - e0)) + e0;
-        for (int64_t p = s; p < e; ++p) s_rw[w][p - e0] = (uint8_t)lane;
-        __syncwarp();
+    const bool lng = valid && e - s > kShortRow && !huge;
+    if (MODE != MODE_REDUCE && !hm) {
+        // per-element outputs (scatter / transpose): stream the warp's contiguous element range
+        // coalesced; element -> row by a shuffle binary search over the 32 row starts
+        const int64_t s_eff = valid ? s : INT64_MAX;
+        const int64_t e0 = __shfl_sync(FULL, s, 0);
+        int64_t e1 = valid ? e : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const int64_t y = __shfl_xor_sync(FULL, e1, o);
+            e1 = y > e1 ? y : e1;
+        }
         const int64_t r0 = row - lane;
         double dummy = 0.0;
+        if (!__any_sync(FULL, lng)) {
+            // all rows short: element -> lane map in shared memory (<= 32 x kShortRow elements)
+            __shared__ uint8_t s_rw[kRowsTPB / 32][32 * kShortRow];
+            const int w = threadIdx.x >> 5;
+            for (int64_t p = s; p < e; ++p) s_rw[w][p - e0] = (uint8_t)lane;
+            __syncwarp();
 #pragma unroll 4
-        for (int64_t p = e0 + lane; p < e1; p += 32) row_elem<T, MODE, PERM, SIDE>(a, r0 + s_rw[w][p - e0], p, dummy);
+            for (int64_t p = e0 + lane; p < e1; p += 32) row_elem<T, MODE, PERM, SIDE>(a, r0 + s_rw[w][p - e0], p, dummy);
+            return;
+        }
+        for (int64_t pb = e0; pb < e1; pb += 32) {
+            const int64_t p = pb + lane;
+            int lo = 0;
+#pragma unroll
+            for (int st = 16; st > 0; st >>= 1) {
+                const int64_t sc = __shfl_sync(FULL, s_eff, lo + st);
+                if (sc <= p) lo += st;
+            }
+            if (p < e1) row_elem<T, MODE, PERM, SIDE>(a, r0 + lo, p, dummy);
+        }
         return;
     }
-    if (!valid || lng) return;
-    double acc = 0.0;
+    if (valid && !lng && !huge) {
+        double acc = 0.0;
 #pragma unroll 4
-    for (int64_t p = s; p < e; ++p) row_elem<T, MODE, PERM, SIDE>(a, row, p, acc);
-    if (MODE == MODE_REDUCE) a.y[row] = (T)acc;
+        for (int64_t p = s; p < e; ++p) row_elem<T, MODE, PERM, SIDE>(a, row, p, acc);
+        if (MODE == MODE_REDUCE) a.y[row] = (T)acc;
+    }
+    // rows of kShortRow < l <= kHugeRow: the warp takes them one by one (coalesced over the row,
+    // fixed shuffle tree -- deterministic)
+    unsigned lm = __ballot_sync(FULL, lng);
+    while (lm) {
+        const int src = __ffs(lm) - 1;
+        lm &= lm - 1;
+        const int64_t rs = __shfl_sync(FULL, s, src), re = __shfl_sync(FULL, e, src);
+        const int64_t r = row - lane + src;
+        double acc = 0.0;
+#pragma unroll 4
+        for (int64_t p = rs + lane; p < re; p += 32) row_elem<T, MODE, PERM, SIDE>(a, r, p, acc);
+        if (MODE == MODE_REDUCE) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+            if (lane == 0) a.y[r] = (T)acc;
+        }
+    }
 }
 
-constexpr int kLongWarps = 8;
+constexpr int kLongTPB = 256;
 
+// One CTA per row longer than kHugeRow (power-law heads).
 template <typename T, int MODE, bool PERM, bool SIDE>
-__global__ __launch_bounds__(32 * kLongWarps) void k_rows_long(TileArgs<T> a, RowList L)
+__global__ __launch_bounds__(kLongTPB) void k_rows_long(TileArgs<T> a, RowList L)
 {
+    __shared__ double s_red[kLongTPB / 32];
     const int n = *(volatile int *)L.count;
-    const int lane = threadIdx.x & 31;
-    for (int it = blockIdx.x * kLongWarps + (threadIdx.x >> 5); it < n; it += gridDim.x * kLongWarps) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int it = blockIdx.x; it < n; it += gridDim.x) {
         const int64_t row = L.rows[it];
         const int64_t s = a.indptr[row], e = a.indptr[row + 1];
         double acc = 0.0;
-        for (int64_t p = s + lane; p < e; p += 32) row_elem<T, MODE, PERM, SIDE>(a, row, p, acc);
+#pragma unroll 4
+        for (int64_t p = s + threadIdx.x; p < e; p += kLongTPB) row_elem<T, MODE, PERM, SIDE>(a, row, p, acc);
         if (MODE == MODE_REDUCE) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0) a.y[row] = (T)acc;
+            if (lane == 0) s_red[w] = acc;
+            __syncthreads();
+            if (w == 0) {
+                acc = lane < kLongTPB / 32 ? s_red[lane] : 0.0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (lane == 0) a.y[row] = (T)acc;
+            }
+            __syncthreads();
         }
     }
 }
@@ -120,7 +174,7 @@ int launch_rows(const TileArgs<T> &a, const RowList &L, cudaStream_t s)
     if (a.nrows <= 0) return CSRK_OK;
     CSRK_CUDA(cudaMemsetAsync(L.count, 0, sizeof(int), s));
     CSRK_LAUNCH((k_rows<T, MODE, PERM, SIDE>), (unsigned)cdiv(a.nrows, kRowsTPB), kRowsTPB, 0, s, a, L);
-    CSRK_LAUNCH((k_rows_long<T, MODE, PERM, SIDE>), (unsigned)(kNumSMs * 2), 32 * kLongWarps, 0, s, a, L);
+    CSRK_LAUNCH((k_rows_long<T, MODE, PERM, SIDE>), (unsigned)(kNumSMs * 2), kLongTPB, 0, s, a, L);
     return CSRK_OK;
 }
 

@@ -1,0 +1,436 @@
+// sptrsv.cu -- sparse triangular solve x = T^{-1} b and its VJP (PAPER 3.1.5, P:477-488;
+// SURVEY 8(f) row f3).
+//
+// Forward.  "each row depends on the intermediate values of previous rows only": row i
+// of a lower T needs x_j for its stored j < i (upper: j > i, solved in reverse order -- the
+// paper's "matrix flip").  Two kernels, launched back to back:
+//
+//   k_trsv_chain  single-pass decoupled look-back scan for CHAIN matrices (every row's
+//                 off-diagonal entries lie on the first sub-diagonal: bidiagonal L of the
+//                 PCG preconditioner, or the triangle of A_N, Table 2).  Row i is
+//                 the affine map x_i = c_i + a_i x_{i-1} (a_i = -l_i / d_i, c_i = b_i / d_i);
+//                 maps compose associatively, so a tile of 2048 rows scans its maps in the
+//                 CTA, publishes the tile aggregate, looks back over its predecessors for the
+//                 carry-in x and then evaluates x_i = (b_i - l_i x_{i-1}) / d_i row by row from
+//                 it.  One HBM pass (pattern, values, b, x): a 16.7M-row chain that the
+//                 sync-free method would walk one dependency at a time streams like an SpMV.
+//                 A row with any other dependency aborts the pass (every tile then publishes
+//                 ABORT so no successor waits).
+//   k_trsv_sf     the synchronisation-free solve the paper uses (Capellini et al.):
+//                 warps take 32-row blocks in solve order from an atomic ticket; each lane
+//                 owns a row, waits (acquire) on the ready flag of every dependency outside
+//                 the block, then the warp resolves the dependencies inside the block in lane
+//                 order through shuffles; x_i is stored and its flag released.  Tickets are
+//                 claimed by running warps in order, so every awaited row belongs to a warp
+//                 that is resident or done: no deadlock.  Runs only if the chain pass aborted.
+//
+// Backward: db = T^{-T} v "with our existing forward triangular solve routine" -- the
+// same two kernels on T^T (cached transpose plan, or one built in the workspace), values
+// gathered through perm; dT = -(db) x^T (.) mask(T) "executed in parallel over the nonzero
+// entries of L" (k_trsv_dT).
+//
+// Stored entries on the wrong side of the diagonal are ignored (CSRK_VALIDATE=1 rejects
+// them); a missing diagonal (unit == 0) divides by zero.
+#include "ops.cuh"
+
+namespace csrk {
+
+enum { CH_NONE = 0, CH_AGG = 1, CH_INCL = 2, CH_ABORT = 3 };
+constexpr int kChTPB = 256;
+constexpr int kChPer = 8;
+constexpr int kChTile = kChTPB * kChPer;
+constexpr int kSfTPB = 256;
+
+__device__ __forceinline__ int ld_acquire(const int *p)
+{
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int *p, int v)
+{
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ double ld_relaxed(const double *p)
+{
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ double ld_relaxed(const float *p)
+{
+    float v;
+    asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+    return (double)v;
+}
+
+template <typename T>
+struct TrsvArgs {
+    int64_t n;
+    const int64_t *indptr;
+    const int32_t *indices;
+    const T *vals;
+    const int64_t *perm;  // nullable: value of entry p is vals[perm[p]]
+    const T *b;
+    T *x;
+    int upper, unit;
+    // chain pass
+    int *status;
+    double *aggA, *aggC, *inclX;
+    int *ticket_chain;
+    int *abort;
+    // sync-free pass
+    int *ready;
+    int *ticket_sf;
+};
+
+template <typename T>
+__device__ __forceinline__ double tval(const TrsvArgs<T> &a, int64_t p)
+{
+    return (double)a.vals[a.perm ? a.perm[p] : p];
+}
+
+// ---------------------------------------------------------------- chain pass
+template <typename T>
+__global__ __launch_bounds__(kChTPB) void k_trsv_chain(TrsvArgs<T> a)
+{
+    __shared__ int s_tile, s_abort;
+    __shared__ double s_wA[kChTPB / 32], s_wC[kChTPB / 32];
+    __shared__ double s_xin;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned FULL = 0xffffffffu;
+    if (tid == 0) {
+        s_tile = atomicAdd(a.ticket_chain, 1);
+        s_abort = *(volatile int *)a.abort;
+    }
+    __syncthreads();
+    const int tile = s_tile;
+    const int64_t n = a.n;
+    if (s_abort) {
+        if (tid == 0) st_release(&a.status[tile], CH_ABORT);
+        return;
+    }
+    // this thread's rows: solve orders o0 .. o0 + kChPer - 1
+    const int64_t o0 = (int64_t)tile * kChTile + (int64_t)tid * kChPer;
+    double lv[kChPer], dv[kChPer], bv[kChPer];
+    double mA = 1.0, mC = 0.0;  // composition of this thread's row maps
+    bool bad = false;
+#pragma unroll
+    for (int r = 0; r < kChPer; ++r) {
+        const int64_t o = o0 + r;
+        lv[r] = 0.0;
+        dv[r] = 1.0;
+        bv[r] = 0.0;
+        if (o < n) {
+            const int64_t i = a.upper ? n - 1 - o : o;
+            const int64_t prev = a.upper ? i + 1 : i - 1;
+            double d = a.unit ? 1.0 : 0.0, l = 0.0;
+            for (int64_t p = a.indptr[i]; p < a.indptr[i + 1]; ++p) {
+                const int64_t j = a.indices[p];
+                if (j == i) {
+                    if (!a.unit) d = tval(a, p);
+                } else if (j == prev) {
+                    l = tval(a, p);
+                } else if (a.upper ? j > i : j < i) {
+                    bad = true;
+                }
+            }
+            lv[r] = l;
+            dv[r] = d;
+            bv[r] = (double)a.b[i];
+            const double ar = -l / d, cr = bv[r] / d;
+            mC = ar * mC + cr;
+            mA = ar * mA;
+        }
+    }
+    if (__syncthreads_or(bad)) {
+        if (tid == 0) {
+            atomicExch(a.abort, 1);
+            st_release(&a.status[tile], CH_ABORT);
+        }
+        return;
+    }
+    // inclusive warp scan of the maps (later map applied after earlier: (A, C) o (Ap, Cp))
+    double iA = mA, iC = mC;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double pA = __shfl_up_sync(FULL, iA, o), pC = __shfl_up_sync(FULL, iC, o);
+        if (lane >= o) {
+            iC = iA * pC + iC;
+            iA = iA * pA;
+        }
+    }
+    if (lane == 31) {
+        s_wA[warp] = iA;
+        s_wC[warp] = iC;
+    }
+    // exclusive in-warp prefix
+    double eA = __shfl_up_sync(FULL, iA, 1), eC = __shfl_up_sync(FULL, iC, 1);
+    if (lane == 0) {
+        eA = 1.0;
+        eC = 0.0;
+    }
+    __syncthreads();
+    // prefix over earlier warps, composed in order
+    double wA = 1.0, wC = 0.0;
+    for (int w = 0; w < warp; ++w) {
+        wC = s_wA[w] * wC + s_wC[w];
+        wA = s_wA[w] * wA;
+    }
+    // thread prefix = in-warp exclusive after warp prefix
+    const double tA = eA * wA, tC = eA * wC + eC;
+    if (tid == 0) {
+        // tile aggregate
+        double gA = 1.0, gC = 0.0;
+        for (int w = 0; w < kChTPB / 32; ++w) {
+            gC = s_wA[w] * gC + s_wC[w];
+            gA = s_wA[w] * gA;
+        }
+        double xin = 0.0;  // x before the first row: no carry
+        bool abort = false;
+        if (tile > 0) {
+            a.aggA[tile] = gA;
+            a.aggC[tile] = gC;
+            st_release(&a.status[tile], CH_AGG);
+            double MA = 1.0, MC = 0.0;  // maps x_in(pred) -> x_in(tile)
+            for (int p = tile - 1;; ) {
+                const int st = ld_acquire(&a.status[p]);
+                if (st == CH_NONE) continue;
+                if (st == CH_ABORT) {
+                    abort = true;
+                    break;
+                }
+                if (st == CH_INCL) {
+                    xin = MA * ld_relaxed(&a.inclX[p]) + MC;
+                    break;
+                }
+                const double pA = ld_relaxed(&a.aggA[p]), pC = ld_relaxed(&a.aggC[p]);
+                MC = MA * pC + MC;
+                MA = MA * pA;
+                --p;
+            }
+        }
+        s_xin = xin;
+        s_abort = abort;
+        if (abort) st_release(&a.status[tile], CH_ABORT);
+    }
+    __syncthreads();
+    if (s_abort) return;
+    // rows from the carried-in value, by the substitution formula
+    double xp = tid == 0 ? s_xin : tA * s_xin + tC;
+#pragma unroll
+    for (int r = 0; r < kChPer; ++r) {
+        const int64_t o = o0 + r;
+        if (o < n) {
+            const int64_t i = a.upper ? n - 1 - o : o;
+            const T xi = (T)((bv[r] - lv[r] * xp) / dv[r]);
+            a.x[i] = xi;
+            xp = (double)xi;
+        }
+    }
+    // the tile's last row publishes the inclusive prefix (its x)
+    const int64_t last = (int64_t)tile * kChTile + kChTile - 1;
+    if (o0 <= last && last < o0 + kChPer) {
+        a.inclX[tile] = xp;
+        st_release(&a.status[tile], CH_INCL);
+    }
+}
+
+// zero the ready flags only when the chain pass aborted
+template <typename T>
+__global__ void k_trsv_prep(TrsvArgs<T> a)
+{
+    if (*(volatile int *)a.abort == 0) return;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x)
+        a.ready[i] = 0;
+}
+
+// ---------------------------------------------------------------- sync-free pass
+template <typename T>
+__global__ __launch_bounds__(kSfTPB) void k_trsv_sf(TrsvArgs<T> a)
+{
+    if (*(volatile int *)a.abort == 0) return;  // the chain pass solved it
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int64_t n = a.n;
+    const int64_t nblk = cdiv(n, 32);
+    while (true) {
+        int blk = 0;
+        if (lane == 0) blk = atomicAdd(a.ticket_sf, 1);
+        blk = __shfl_sync(FULL, blk, 0);
+        if (blk >= nblk) return;
+        const int64_t blo = (int64_t)blk * 32;
+        const int64_t o = blo + lane;
+        const bool valid = o < n;
+        const int64_t i = valid ? (a.upper ? n - 1 - o : o) : 0;
+        int64_t s = 0, e = 0;
+        if (valid) {
+            s = a.indptr[i];
+            e = a.indptr[i + 1];
+        }
+        double acc = valid ? (double)a.b[i] : 0.0;
+        double d = a.unit ? 1.0 : 0.0;
+        int64_t qs = e, qe = e;  // intra-block dependencies: contiguous positions [qs, qe)
+        for (int64_t p = s; p < e; ++p) {
+            const int64_t j = a.indices[p];
+            if (j == i) {
+                if (!a.unit) d = tval(a, p);
+                continue;
+            }
+            const int64_t oj = a.upper ? n - 1 - j : j;
+            if (oj >= o) continue;  // wrong side of the diagonal: ignored
+            if (oj >= blo) {
+                if (qs == e) qs = p;
+                qe = p + 1;
+                continue;
+            }
+            while (ld_acquire(&a.ready[j]) == 0) {
+            }
+            acc = fma(-tval(a, p), ld_relaxed(&a.x[j]), acc);
+        }
+        const unsigned im = __ballot_sync(FULL, valid && qs < qe);
+        double xi = 0.0;
+        if (im) {
+            // lanes depended upon are below the highest dependent lane; resolve in lane order
+            const int last = 31 - __clz(im);
+            int64_t q = a.upper ? qe - 1 : qs;
+            for (int src = 0; src < last; ++src) {
+                if (lane == src) xi = (double)(T)(acc / d);
+                const double xs = __shfl_sync(FULL, xi, src);
+                const int64_t rs = a.upper ? n - 1 - (blo + src) : blo + src;
+                if (valid && lane > src && (a.upper ? q >= qs : q < qe) && a.indices[q] == rs) {
+                    acc = fma(-tval(a, q), xs, acc);
+                    q += a.upper ? -1 : 1;
+                }
+            }
+            if (lane >= last) xi = acc / d;
+        } else {
+            xi = acc / d;
+        }
+        if (valid) {
+            a.x[i] = (T)xi;
+            st_release(&a.ready[i], 1);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- VJP: masked outer product
+template <typename T>
+__global__ void k_trsv_dT(int64_t n, const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
+                          const T *__restrict__ w, const T *__restrict__ x, int unit, T *__restrict__ dT)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double wi = (double)w[i];
+    for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) {
+        const int32_t j = indices[p];
+        dT[p] = (unit && j == i) ? (T)0 : (T)(-(wi * (double)x[j]));
+    }
+}
+
+// ---------------------------------------------------------------- host side
+template <typename T>
+static int carve_solve(TrsvArgs<T> &a, int64_t n, Bump &ws)
+{
+    const int64_t ntiles = cdiv(n, kChTile);
+    a.status = ws.take<int>(ntiles > 0 ? ntiles : 1);
+    a.aggA = ws.take<double>(ntiles > 0 ? ntiles : 1);
+    a.aggC = ws.take<double>(ntiles > 0 ? ntiles : 1);
+    a.inclX = ws.take<double>(ntiles > 0 ? ntiles : 1);
+    a.ready = ws.take<int>(n > 0 ? n : 1);
+    int *cnt = ws.take<int>(4);
+    a.ticket_chain = cnt;
+    a.ticket_sf = cnt ? cnt + 1 : nullptr;
+    a.abort = cnt ? cnt + 2 : nullptr;
+    return CSRK_OK;
+}
+
+template <typename T>
+static int launch_solve(TrsvArgs<T> &a, cudaStream_t s)
+{
+    const int64_t n = a.n;
+    if (n == 0) return CSRK_OK;
+    const int64_t ntiles = cdiv(n, kChTile);
+    CSRK_CUDA(cudaMemsetAsync(a.status, 0, sizeof(int) * (size_t)ntiles, s));
+    CSRK_CUDA(cudaMemsetAsync(a.ticket_chain, 0, 4 * sizeof(int), s));
+    if (ntiles > INT32_MAX) return CSRK_ERR_INDEX_OVERFLOW;
+    CSRK_LAUNCH(k_trsv_chain<T>, (unsigned)ntiles, kChTPB, 0, s, a);
+    CSRK_LAUNCH(k_trsv_prep<T>, (unsigned)(kNumSMs * 4), 256, 0, s, a);
+    const int64_t nwarps = cdiv(n, 32);
+    const int64_t grid = cdiv(nwarps, kSfTPB / 32) < kNumSMs * 8 ? cdiv(nwarps, kSfTPB / 32) : kNumSMs * 8;
+    CSRK_LAUNCH(k_trsv_sf<T>, (unsigned)grid, kSfTPB, 0, s, a);
+    return CSRK_OK;
+}
+
+template <typename T>
+static int sptrsv_fwd_t(const csrk_pattern &A, const T *Av, int upper, int unit, const T *b, T *x, Bump &ws,
+                        cudaStream_t s)
+{
+    TrsvArgs<T> a{};
+    carve_solve(a, A.nrows, ws);
+    if (ws.sizing()) return CSRK_OK;
+    a.n = A.nrows;
+    a.indptr = A.indptr;
+    a.indices = A.indices;
+    a.vals = Av;
+    a.b = b;
+    a.x = x;
+    a.upper = upper;
+    a.unit = unit;
+    return launch_solve(a, s);
+}
+
+template <typename T>
+static int sptrsv_bwd_t(const csrk_pattern &A, const T *Av, const csrk_pattern *AT, const int64_t *perm, int upper,
+                        int unit, const T *x, const T *v, T *dA, T *db, Bump &ws, cudaStream_t s)
+{
+    const int64_t n = A.nrows;
+    csrk_pattern Tt{};
+    int64_t *tp = nullptr;
+    if (AT) {
+        Tt = *AT;
+    } else {
+        int64_t *ATp = ws.take<int64_t>(n + 1);
+        int32_t *ATi = ws.take<int32_t>(A.nnz > 0 ? A.nnz : 1);
+        tp = ws.take<int64_t>(A.nnz > 0 ? A.nnz : 1);
+        Tt = csrk_pattern{n, n, A.nnz, ATp, ATi};
+    }
+    T *w = db ? db : ws.take<T>(n > 0 ? n : 1);
+    TrsvArgs<T> a{};
+    carve_solve(a, n, ws);
+    if (!AT) CSRK_TRY(transpose_impl(sizeof(T) == 8 ? CSRK_F64 : CSRK_F32, A, nullptr, const_cast<int64_t *>(Tt.indptr),
+                                     const_cast<int32_t *>(Tt.indices), nullptr, tp, ws, s));
+    if (ws.sizing()) return CSRK_OK;
+    a.n = n;
+    a.indptr = Tt.indptr;
+    a.indices = Tt.indices;
+    a.vals = Av;
+    a.perm = AT ? perm : tp;
+    a.b = v;
+    a.x = w;
+    a.upper = !upper;
+    a.unit = unit;
+    CSRK_TRY(launch_solve(a, s));
+    if (dA && n > 0) CSRK_LAUNCH(k_trsv_dT<T>, (unsigned)cdiv(n, 256), 256, 0, s, n, A.indptr, A.indices, w, x, unit, dA);
+    return CSRK_OK;
+}
+
+int sptrsv_fwd(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int upper, int unit, const void *b, void *x,
+               Bump &ws, cudaStream_t s)
+{
+    if (dt == CSRK_F64)
+        return sptrsv_fwd_t<double>(A, (const double *)A_val, upper, unit, (const double *)b, (double *)x, ws, s);
+    return sptrsv_fwd_t<float>(A, (const float *)A_val, upper, unit, (const float *)b, (float *)x, ws, s);
+}
+
+int sptrsv_bwd(csrk_dtype dt, const csrk_pattern &A, const void *A_val, const csrk_pattern *AT, const int64_t *perm,
+               int upper, int unit, const void *x, const void *v, void *dA, void *db, Bump &ws, cudaStream_t s)
+{
+    if (dt == CSRK_F64)
+        return sptrsv_bwd_t<double>(A, (const double *)A_val, AT, perm, upper, unit, (const double *)x,
+                                    (const double *)v, (double *)dA, (double *)db, ws, s);
+    return sptrsv_bwd_t<float>(A, (const float *)A_val, AT, perm, upper, unit, (const float *)x, (const float *)v,
+                               (float *)dA, (float *)db, ws, s);
+}
+
+}  // namespace csrk

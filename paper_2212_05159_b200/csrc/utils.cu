@@ -145,14 +145,46 @@ __global__ void k_validate(int64_t m, int64_t n, int64_t nnz, const int64_t *__r
     }
 }
 
-int validate_pattern(const csrk_pattern &A, cudaStream_t s)
+static bool validate_on()
 {
     static int mode = -1;
     if (mode < 0) {
         const char *e = getenv("CSRK_VALIDATE");
         mode = (e && strcmp(e, "1") == 0) ? 1 : 0;
     }
-    if (!mode || A.nrows == 0) return CSRK_OK;
+    return mode == 1;
+}
+
+// triangular structure (PAPER 3.1.5 P:482 "L_ij != 0 if i >= j"): no entry on the
+// wrong side of the diagonal, and a stored diagonal in every row unless unit
+__global__ void k_validate_tri(int64_t m, const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
+                               int upper, int unit)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        bool diag = false, bad = false;
+        for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) {
+            const int64_t c = indices[p];
+            diag |= c == i;
+            bad |= upper ? c < i : c > i;
+        }
+        if (bad || (!unit && !diag)) g_bad_pattern = 1;
+    }
+}
+
+int validate_triangular(const csrk_pattern &A, int upper, int unit, cudaStream_t s)
+{
+    if (!validate_on() || A.nrows == 0) return CSRK_OK;
+    int zero = 0, bad = 0;
+    CSRK_CUDA(cudaMemcpyToSymbolAsync(g_bad_pattern, &zero, sizeof(int), 0, cudaMemcpyHostToDevice, s));
+    CSRK_LAUNCH(k_validate_tri, 1024, 256, 0, s, A.nrows, A.indptr, A.indices, upper, unit);
+    CSRK_CUDA(cudaMemcpyFromSymbolAsync(&bad, g_bad_pattern, sizeof(int), 0, cudaMemcpyDeviceToHost, s));
+    CSRK_CUDA(cudaStreamSynchronize(s));
+    return bad ? CSRK_ERR_PATTERN : CSRK_OK;
+}
+
+int validate_pattern(const csrk_pattern &A, cudaStream_t s)
+{
+    if (!validate_on() || A.nrows == 0) return CSRK_OK;
     int zero = 0, bad = 0;
     CSRK_CUDA(cudaMemcpyToSymbolAsync(g_bad_pattern, &zero, sizeof(int), 0, cudaMemcpyHostToDevice, s));
     CSRK_LAUNCH(k_validate, 1024, 256, 0, s, A.nrows, A.ncols, A.nnz, A.indptr, A.indices);

@@ -7,7 +7,7 @@ PyTorch fallback: if libcsrk.so is missing or a call fails, an exception is rais
 Names follow the ABI (and the paper's operations, Table 1):
 spmv_fwd / spmv_bwd (SpMV), spmm_fwd / spmm_bwd (SpDMM), csr_transpose,
 spgemm_symbolic / spgemm_numeric / spgemm_bwd (SpSpMM), spadd_symbolic / spadd_numeric /
-spadd_bwd (Sp + Sp).
+spadd_bwd (Sp + Sp), sptrsv_fwd / sptrsv_bwd (SpTRSV).
 """
 from __future__ import annotations
 
@@ -23,13 +23,15 @@ LIB_PATH = os.path.join(_PKG, "libcsrk.so")
 F32, F64 = 0, 1
 OP_N, OP_T = 0, 1
 WS = dict(spmv_fwd=0, spmv_bwd=1, spmm_fwd=2, spmm_bwd=3, csr_transpose=4, spgemm_symbolic=5,
-          spgemm_numeric=6, spgemm_bwd=7, pcg=8, spadd_symbolic=9, spai=10)
+          spgemm_numeric=6, spgemm_bwd=7, pcg=8, spadd_symbolic=9, spai=10, sptrsv_fwd=11,
+          sptrsv_bwd=12)
 
 # Every symbol declared in include/csrk.h (checked by tests/test_abi_cpu.py).
 ABI_SYMBOLS = ("csrk_spmv_fwd", "csrk_spmv_bwd", "csrk_spmm_fwd", "csrk_spmm_bwd", "csrk_csr_transpose",
                "csrk_spgemm_symbolic", "csrk_spgemm_numeric", "csrk_spgemm_bwd", "csrk_workspace_size",
                "csrk_status_string", "csrk_launch_count", "csrk_version", "csrk_pcg_loss_grad",
-               "csrk_spadd_symbolic", "csrk_spadd_numeric", "csrk_spadd_bwd", "csrk_spai_loss_grad")
+               "csrk_spadd_symbolic", "csrk_spadd_numeric", "csrk_spadd_bwd", "csrk_spai_loss_grad",
+               "csrk_sptrsv_fwd", "csrk_sptrsv_bwd")
 
 
 class Pattern(ctypes.Structure):
@@ -71,6 +73,8 @@ def lib() -> ctypes.CDLL:
     L.csrk_spadd_numeric.argtypes = [I, D, Pat, P, D, Pat, P, Pat, P, P, SZ, P]
     L.csrk_spadd_bwd.argtypes = [I, D, Pat, D, Pat, Pat, P, P, P, P, SZ, P]
     L.csrk_spai_loss_grad.argtypes = [Pat, P, Pat, P, Pat, Pat, Pat, ctypes.POINTER(D), P, P, SZ, P]
+    L.csrk_sptrsv_fwd.argtypes = [I, Pat, P, I, I, P, P, P, SZ, P]
+    L.csrk_sptrsv_bwd.argtypes = [I, Pat, P, PatP, P, I, I, P, P, P, P, P, SZ, P]
     L.csrk_status_string.restype = ctypes.c_char_p
     L.csrk_status_string.argtypes = [I]
     L.csrk_launch_count.restype = ctypes.c_uint64
@@ -351,6 +355,34 @@ def spai_loss_grad(plan: SpaiPlan, M: CSR, A: CSR, dM: torch.Tensor | None = Non
                                      plan.I.pattern(), ctypes.byref(loss), _ptr(dM), _ptr(buf), buf.numel(),
                                      _stream()), "spai_loss_grad")
     return float(loss.value), dM
+
+
+def sptrsv_fwd(T: CSR, b: torch.Tensor, upper: bool = False, unit: bool = False,
+               out: torch.Tensor | None = None) -> torch.Tensor:
+    """x = T^{-1} b, T triangular (PAPER 3.1.5)."""
+    dt = _dt(T.values)
+    x = out if out is not None else torch.empty(T.nrows, dtype=T.values.dtype, device=T.values.device)
+    ws, wsb = _workspace("sptrsv_fwd", dt, T)
+    _check(lib().csrk_sptrsv_fwd(dt, T.pattern(), _ptr(T.values), int(upper), int(unit), _ptr(b), _ptr(x), ws, wsb,
+                                 _stream()), "sptrsv_fwd")
+    return x
+
+
+def sptrsv_bwd(T: CSR, x: torch.Tensor, v: torch.Tensor, upper: bool = False, unit: bool = False,
+               plan: TransposePlan | None = None, need_dT: bool = True, need_db: bool = True,
+               dT: torch.Tensor | None = None, db: torch.Tensor | None = None):
+    """VJP of x = T^{-1} b: db = T^{-T} v, dT = -db x^T (.) mask(T)."""
+    dt = _dt(T.values)
+    if need_dT and dT is None:
+        dT = torch.empty_like(T.values)
+    if need_db and db is None:
+        db = torch.empty(T.nrows, dtype=T.values.dtype, device=T.values.device)
+    pp = plan.args() if plan else (None, None, None)
+    ws, wsb = _workspace("sptrsv_bwd", dt, T, have_plan=plan is not None)
+    _check(lib().csrk_sptrsv_bwd(dt, T.pattern(), _ptr(T.values), pp[0], pp[1], int(upper), int(unit), _ptr(x),
+                                 _ptr(v), _ptr(dT if need_dT else None), _ptr(db if need_db else None), ws, wsb,
+                                 _stream()), "sptrsv_bwd")
+    return (dT if need_dT else None), (db if need_db else None)
 
 
 def pcg_loss_grad(A: CSR, L: CSR, b: torch.Tensor, n_it: int = 50, gamma: float = 0.6,

@@ -232,3 +232,39 @@ def lower_part(A: CSR) -> CSR:
     np.cumsum(np.bincount(rows[keep], minlength=A.nrows), out=indptr[1:])
     return CSR(A.nrows, A.ncols, indptr, A.indices[keep].copy(),
                None if A.values is None else A.values[keep].copy())
+
+
+def tri_banded(n: int, per_row: int, band: int, seed: int, upper: bool = False, values: str = "real",
+               unit: bool = False) -> CSR:
+    """Large random triangular matrix without a dense mask: row i draws per_row candidate
+    columns uniformly from the band [i - band, i) (upper: (i, i + band]), duplicates and
+    out-of-range candidates dropped, plus the diagonal (omitted when unit).  Values as in
+    tri_random (diagonally dominant 'real', or integer with diagonal in {+-1, +-2, +-4})."""
+    rng = np.random.default_rng(seed)
+    i = np.arange(n, dtype=np.int64)[:, None]
+    off = rng.integers(1, band + 1, size=(n, per_row))
+    cand = i + off if upper else i - off
+    cand = np.where((cand >= 0) & (cand < n), cand, -1)
+    cand = np.sort(cand, axis=1)
+    dup = np.zeros_like(cand, dtype=bool)
+    dup[:, 1:] = cand[:, 1:] == cand[:, :-1]
+    keep = (cand >= 0) & ~dup
+    if not unit:
+        cand = np.concatenate([cand, np.broadcast_to(i, (n, 1))], axis=1)
+        keep = np.concatenate([keep, np.ones((n, 1), bool)], axis=1)
+    order = np.argsort(np.where(keep, cand, np.iinfo(np.int64).max), axis=1, kind="stable")
+    cand = np.take_along_axis(cand, order, axis=1)
+    keep = np.take_along_axis(keep, order, axis=1)
+    counts = keep.sum(axis=1)
+    indptr = np.zeros(n + 1, np.int64)
+    np.cumsum(counts, out=indptr[1:])
+    rows = np.repeat(np.arange(n), counts)
+    cols = cand[keep]
+    diag = rows == cols
+    if values == "real":
+        vals = rng.uniform(-1.0, 1.0, cols.size) / (1.0 + counts[rows])
+        vals[diag] = rng.choice([-1.0, 1.0], diag.sum()) * rng.uniform(1.0, 2.0, diag.sum())
+    else:
+        vals = rng.integers(-3, 4, cols.size).astype(np.float64)
+        vals[diag] = rng.choice([-4.0, -2.0, -1.0, 1.0, 2.0, 4.0], diag.sum())
+    return CSR(n, n, indptr, cols.astype(np.int32), vals)
