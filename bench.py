@@ -212,6 +212,76 @@ def run_ops_workload(args, torch, ck, cfg):
     return 0
 
 
+def run_trsv_workload(args, torch, ck):
+    """SpTRSV (PAPER 3.1.5) at N = 1, op by op (CUDA events, L2 flushed before
+    every op): the config-5 lower-bidiagonal L (4096^2 = 16,777,216 rows; the chain pass) and
+    the IC(0) pattern of the 2D Poisson 2048^2 matrix (its lower triangle; wavefront, the
+    sync-free pass), forward x = T^{-1} b and backward (db = T^{-T} v, dT) with a cached plan.
+    Algorithmic bytes: fwd = pattern + values + b + x; bwd = pattern + values + v + x + db + dT."""
+    dev = torch.device("cuda", 0)
+    s = 8
+    mats = {"chain": synth.bidiag_lower(4096 * 4096, "seeded"),
+            "ic0": synth.lower_part(synth.poisson2d(2048))}
+    ops = {}
+    keep = []
+    for nm, T in mats.items():
+        n, nnz = T.nrows, T.nnz
+        Td = ck.CSR.from_host(T)
+        b = torch.from_numpy(synth.dense(n, synth.seed_of(5, 3))).to(dev)
+        v = torch.from_numpy(synth.dense(n, synth.seed_of(5, 4))).to(dev)
+        x = ck.sptrsv_fwd(Td, b)
+        plan = ck.csr_transpose(Td, with_values=False)
+        dT, db = torch.empty_like(Td.values), torch.empty_like(b)
+        keep += [Td, b, v, x, plan, dT, db]
+        pat = 8 * (n + 1) + 4 * nnz
+        ops[f"sptrsv_fwd_{nm}"] = ((lambda Td=Td, b=b, x=x: ck.sptrsv_fwd(Td, b, out=x)),
+                                   (pat + s * nnz + 2 * s * n, 2 * nnz))
+        ops[f"sptrsv_bwd_{nm}"] = ((lambda Td=Td, x=x, v=v, plan=plan, dT=dT, db=db:
+                                    ck.sptrsv_bwd(Td, x, v, plan=plan, dT=dT, db=db)),
+                                   (pat + s * nnz + 4 * s * n + s * nnz, 3 * nnz))
+    l2 = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        for f, _c in ops.values():
+            f()
+    torch.cuda.synchronize()
+    times = {k: [] for k in ops}
+    l0 = ck.launch_count()
+    with Clocks(0) as clk:
+        for _ in range(args.steps):
+            for k, (f, _c) in ops.items():
+                l2.zero_()
+                a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                f()
+                e.record(st)
+                times[k].append((a, e))
+        torch.cuda.synchronize()
+    launches = ck.launch_count() - l0
+    peak = _peak()
+    rep, tot_b, tot_f, tot_ms = {}, 0, 0, 0.0
+    for k, ev in times.items():
+        ms = float(np.median([a.elapsed_time(e) for a, e in ev]))
+        b, fl = ops[k][1]
+        rep[k] = {"ms": round(ms, 4), "GB/s": round(b / ms / 1e6, 1), "GFLOP/s": round(fl / ms / 1e6, 1),
+                  "frac": round(b / ms / 1e6 / peak, 3), "bytes": b}
+        tot_b, tot_f, tot_ms = tot_b + b, tot_f + fl, tot_ms + ms
+    dom = max(rep, key=lambda k: rep[k]["ms"])
+    out = {"metric": "SpTRSV fwd+bwd algorithmic GB/s", "value": round(tot_b / tot_ms / 1e6, 2), "unit": "GB/s",
+           "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot_ms, 4),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": "SpTRSV: config-5 bidiagonal L (16,777,216 rows, chain pass) and the lower "
+                                  "triangle of 2D Poisson 2048^2 (4,194,304 rows, wavefront, sync-free pass), fwd + "
+                                  "bwd with a cached transpose plan",
+                      "l2": "flushed (512 MiB write) before every timed op"},
+           "gflops": round(tot_f / tot_ms / 1e6, 2),
+           "roofline": {"bound": "hbm", "kernel": dom, "achieved": rep[dom]["GB/s"], "peak": peak, "unit": "GB/s",
+                        "frac": rep[dom]["frac"], "traffic": None},
+           "ops": rep, "gpu_launches": int(launches / max(args.steps, 1)), "clocks": clk.summary()}
+    print(json.dumps(out))
+    return 0
+
+
 def _peak():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
@@ -421,7 +491,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5", "trsv"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -433,6 +503,8 @@ def main():
 
     if args.workload == "cfg5":
         return run_cfg5(args, torch, ck)
+    if args.workload == "trsv":
+        return run_trsv_workload(args, torch, ck)
     if args.workload in ("cfg3", "cfg4"):
         return run_ops_workload(args, torch, ck, int(args.workload[-1]))
 

@@ -12,7 +12,14 @@
 //              largest l_i, and when all 32 rows of a warp are short their C (and dA)
 //              ranges are contiguous, so outputs are staged in shared memory and written
 //              (and dC read) coalesced.  Every other row is queued (warp-aggregated atomic).
-//   k_gemm_big one CTA per queued row.  w_i <= 8192: products gathered to shared memory;
+//   k_gemm_W   one WARP per queued row with l_i <= kWL and w_i <= kWW (power-law "medium" rows,
+//              SURVEY 8(d) config 4): the row's products are enumerated flat (list offsets in
+//              shared memory); COUNT inserts the columns into a shared-memory hash table, FILL
+//              sorts them (warp bitonic network) and compacts the unique ones, NUM / BWD
+//              binary-search each product's column in the C row staged in shared memory
+//              (NUM: shared atomics into the row accumulator; BWD: dA by a segmented warp
+//              reduction per A entry, dB by global atomics).  Rows with w_i > kWW are passed on.
+//   k_gemm_big one CTA per remaining row.  w_i <= 8192: products gathered to shared memory;
 //              symbolic = bitonic sort + unique; numeric/backward binary-search each
 //              product's column in the C row (shared memory) -- numeric accumulates with
 //              shared-memory atomics.  w_i > 8192: symbolic uses shared-memory bitmap
@@ -32,8 +39,12 @@ constexpr int kSTPB = 128;           // k_gemm_S: 4 warps
 constexpr int kSWarps = kSTPB / 32;
 constexpr int kSBuf = 832;           // staged C entries per warp (3D 7-point A^2: 32 x 25 = 800)
 constexpr int kSBufA = 32 * kSMaxL;  // staged dA entries per warp
-constexpr int kGemmTPB = 256;        // k_gemm_big
+constexpr int kGemmTPB = 512;        // k_gemm_big*
 constexpr int kBitmapWords = 24576;  // 96 KB -> windows of 786,432 columns
+constexpr int kWL = 64;              // k_gemm_W: max entries of the A row
+constexpr int kWW = 512;             // k_gemm_W: max products w_i
+constexpr int kWTPB = 128;           // k_gemm_W: 4 warps
+constexpr int kWWarps = kWTPB / 32;
 
 enum { PH_COUNT = 0, PH_FILL = 1, PH_NUM = 2, PH_BWD = 3 };
 
@@ -208,7 +219,7 @@ __global__ __launch_bounds__(kSTPB) void k_gemm_S(int64_t m, const int64_t *__re
                                                   const T *__restrict__ Bv, int64_t *__restrict__ Cp,
                                                   int32_t *__restrict__ Ci, T *__restrict__ Cv,
                                                   const T *__restrict__ dC, T *__restrict__ dA, T *__restrict__ dB,
-                                                  BigList big, int use_stage)
+                                                  BigList wl, BigList big, int use_stage)
 {
     // per-warp staging buffers in dynamic shared memory (none when use_stage == 0, which
     // leaves the whole carve-out to L1 for the merge's list reads)
@@ -223,9 +234,10 @@ __global__ __launch_bounds__(kSTPB) void k_gemm_S(int64_t m, const int64_t *__re
     int64_t as = 0;
     int l = 0;
     int64_t w = 0;
+    int64_t ll = 0;
     if (valid) {
         as = Ap[i];
-        const int64_t ll = Ap[i + 1] - as;
+        ll = Ap[i + 1] - as;
         l = ll > kSMaxL ? kSMaxL + 1 : (int)ll;
         if (l <= kSMaxL)
             for (int t = 0; t < l; ++t) {
@@ -234,13 +246,21 @@ __global__ __launch_bounds__(kSTPB) void k_gemm_S(int64_t m, const int64_t *__re
             }
     }
     const bool isS = valid && l <= kSMaxL && w <= kSMaxW;
-    // queue the other rows (warp-aggregated)
-    const unsigned bigmask = __ballot_sync(0xffffffffu, valid && !isS);
+    // queue the other rows (warp-aggregated): l_i <= kWL to the warp path, longer to the CTA path
+    const bool toW = valid && !isS && ll <= kWL;
+    const unsigned wmask = __ballot_sync(0xffffffffu, toW);
+    if (wmask) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(wl.count, __popc(wmask));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (toW) wl.rows[base + __popc(wmask & ((1u << lane) - 1))] = (int32_t)i;
+    }
+    const unsigned bigmask = __ballot_sync(0xffffffffu, valid && !isS && !toW);
     if (bigmask) {
         int base = 0;
         if (lane == 0) base = atomicAdd(big.count, __popc(bigmask));
         base = __shfl_sync(0xffffffffu, base, 0);
-        if (valid && !isS) big.rows[base + __popc(bigmask & ((1u << lane) - 1))] = (int32_t)i;
+        if (valid && !isS && !toW) big.rows[base + __popc(bigmask & ((1u << lane) - 1))] = (int32_t)i;
     }
     const int Lw = (int)__reduce_max_sync(0xffffffffu, isS ? (unsigned)l : 0u);
     // staging: all rows of the warp short, C range of the warp small enough
@@ -292,6 +312,248 @@ __global__ __launch_bounds__(kSTPB) void k_gemm_S(int64_t m, const int64_t *__re
             const int64_t a_hi = Ap[iend];
             for (int64_t e = a_lo + lane; e < a_hi; e += 32) dA[e] = s_dA_w[e - a_lo];
         }
+    }
+}
+
+
+// lower_bound of v in sorted c[0..n)
+__device__ __forceinline__ int64_t lbound(const int32_t *c, int64_t n, int32_t v)
+{
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (c[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// ---------------------------------------------------------------- medium rows: warp per row
+struct WSmem {
+    double val[kWW];     // NUM: row accumulator; BWD: dC row; COUNT: hash table (2 kWW int32)
+    double dA[kWL];      // BWD: dA of the row's A entries
+    double av[kWL];      // NUM / BWD: A values of the row
+    int64_t bs[kWL];     // start in B of list t
+    int32_t key[kWW];    // FILL: product columns (sorted); NUM / BWD: C row columns
+    int32_t off[kWL + 1];// flat offset of list t (off[l] = w)
+};
+
+// last t in [0, l) with off[t] <= e (the list holding flat product e; empty lists skipped)
+__device__ __forceinline__ int w_list_of(const int32_t *off, int l, int e)
+{
+    int lo = 0, hi = l - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (off[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ uint32_t w_hash(int32_t j) { return (uint32_t)j * 0x9E3779B1u; }
+
+
+// Bitonic sort of P = 32 R keys held in registers, element r * 32 + lane in v[r] (ascending):
+// partners within a lane are register compare-exchanges, partners across lanes shuffles.
+template <int R>
+__device__ __forceinline__ void warp_bitonic(int32_t (&v)[R], int lane)
+{
+    constexpr int P = 32 * R;
+#pragma unroll
+    for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+                const int jr = j >> 5;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int pr = r ^ jr;
+                    if (pr > r) {
+                        const bool asc = (((r << 5) + lane) & k) == 0;
+                        const int32_t a = v[r], b = v[pr];
+                        const bool sw = (a > b) == asc;
+                        v[r] = sw ? b : a;
+                        v[pr] = sw ? a : b;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int32_t o = __shfl_xor_sync(0xffffffffu, v[r], j);
+                    const bool asc = (((r << 5) + lane) & k) == 0;
+                    const bool lower = (lane & j) == 0;
+                    v[r] = (lower == asc) ? min(v[r], o) : max(v[r], o);
+                }
+            }
+        }
+    }
+}
+
+// FILL of a warp-path row: sort the w gathered columns, write the distinct ones in order
+template <int R>
+__device__ __forceinline__ void w_sort_fill(const int32_t *key, int w, int32_t *out, int lane)
+{
+    int32_t v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = (r << 5) + lane < w ? key[(r << 5) + lane] : INT32_MAX;
+    warp_bitonic<R>(v, lane);
+    int base = 0;
+    int32_t carry = 0;  // last key of the previous register row (lane 31)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int e = (r << 5) + lane;
+        int32_t prev = __shfl_up_sync(0xffffffffu, v[r], 1);
+        if (lane == 0) prev = carry;
+        const bool f = e < w && (e == 0 || v[r] != prev);
+        const unsigned m = __ballot_sync(0xffffffffu, f);
+        if (f) out[base + __popc(m & ((1u << lane) - 1))] = v[r];
+        base += __popc(m);
+        carry = __shfl_sync(0xffffffffu, v[r], 31);
+    }
+}
+
+template <typename T, int PH>
+__global__ __launch_bounds__(kWTPB) void k_gemm_W(BigList wl, BigList big, const int64_t *__restrict__ Ap,
+                                                  const int32_t *__restrict__ Ai, const T *__restrict__ Av,
+                                                  const int64_t *__restrict__ Bp, const int32_t *__restrict__ Bi,
+                                                  const T *__restrict__ Bv, int64_t *__restrict__ Cp,
+                                                  int32_t *__restrict__ Ci, T *__restrict__ Cv,
+                                                  const T *__restrict__ dC, T *__restrict__ dA, T *__restrict__ dB)
+{
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WSmem &S = reinterpret_cast<WSmem *>(s_dyn)[warp];
+    const unsigned FULL = 0xffffffffu;
+    const int nrows = *(volatile int *)wl.count;
+    for (int it = blockIdx.x * kWWarps + warp; it < nrows; it += gridDim.x * kWWarps) {
+        const int64_t i = wl.rows[it];
+        const int64_t as = Ap[i];
+        const int l = (int)(Ap[i + 1] - as);
+        // flat offsets of the l lists (warp scan of the B row lengths)
+        int64_t run = 0;
+        for (int t0 = 0; t0 < l; t0 += 32) {
+            const int t = t0 + lane;
+            int64_t len = 0, bs = 0;
+            if (t < l) {
+                const int32_t k = Ai[as + t];
+                bs = Bp[k];
+                len = Bp[k + 1] - bs;
+            }
+            int64_t x = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int64_t y = __shfl_up_sync(FULL, x, o);
+                if (lane >= o) x += y;
+            }
+            const int64_t excl = run + x - len;
+            if (t < l) {
+                S.off[t] = excl > kWW ? kWW + 1 : (int32_t)excl;
+                S.bs[t] = bs;
+                if (PH == PH_NUM || PH == PH_BWD) S.av[t] = (double)Av[as + t];
+            }
+            run += __shfl_sync(FULL, x, 31);
+        }
+        if (run > kWW) {  // too many products for the warp: the CTA path takes the row
+            if (lane == 0) big.rows[atomicAdd(big.count, 1)] = (int32_t)i;
+            continue;
+        }
+        const int w = (int)run;
+        if (lane == 0) S.off[l] = w;
+        __syncwarp();
+        const int64_t cs = PH == PH_COUNT ? 0 : Cp[i];
+        const int nc = PH == PH_COUNT ? 0 : (int)(Cp[i + 1] - cs);
+        int32_t *tab = reinterpret_cast<int32_t *>(S.val);
+        int H = 64;
+        if (PH == PH_COUNT) {
+            while (H < 2 * w) H <<= 1;
+            for (int e = lane; e < H; e += 32) tab[e] = -1;
+        } else if (PH == PH_NUM || PH == PH_BWD) {
+            for (int c = lane; c < nc; c += 32) {
+                S.key[c] = Ci[cs + c];
+                S.val[c] = PH == PH_NUM ? 0.0 : (double)dC[cs + c];
+            }
+            if (PH == PH_BWD)
+                for (int t = lane; t < l; t += 32) S.dA[t] = 0.0;
+        }
+        __syncwarp();
+        int cnt = 0;
+        int t = w > 0 ? w_list_of(S.off, l, lane < w ? lane : 0) : 0;
+        constexpr int U = 8;  // products gathered per lane before use: U loads in flight
+        for (int e00 = 0; e00 < w; e00 += 32 * U) {
+            int32_t jv[U];
+            double bv[U];
+            int64_t bb[U];
+            int tv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int e = e00 + u * 32 + lane;
+                const bool ok = e < w;
+                while (ok && t + 1 < l && S.off[t + 1] <= e) ++t;
+                tv[u] = ok ? t : -1;
+                bb[u] = ok ? S.bs[t] + (e - S.off[t]) : 0;
+                jv[u] = ok ? Bi[bb[u]] : 0;
+                bv[u] = (PH == PH_NUM || PH == PH_BWD) && ok ? (double)Bv[bb[u]] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int e = e00 + u * 32 + lane;
+                const bool ok = e < w;
+                const int32_t j = jv[u];
+                if (PH == PH_COUNT && ok) {
+                    uint32_t h = w_hash(j) & (uint32_t)(H - 1);
+                    while (true) {
+                        const int32_t old = atomicCAS(&tab[h], -1, j);
+                        if (old == -1) { ++cnt; break; }
+                        if (old == j) break;
+                        h = (h + 1) & (uint32_t)(H - 1);
+                    }
+                }
+                if (PH == PH_FILL && ok) S.key[e] = j;
+                if (PH == PH_NUM && ok) {
+                    const int64_t pos = lbound(S.key, nc, j);
+                    atomicAdd(&S.val[pos], S.av[tv[u]] * bv[u]);
+                }
+                if (PH == PH_BWD && e00 + u * 32 < w) {
+                    double g = 0.0, v = 0.0;
+                    if (ok) {
+                        const int64_t pos = lbound(S.key, nc, j);
+                        g = S.val[pos];
+                        v = g * bv[u];
+                        if (dB) red_add(&dB[bb[u]], (T)(S.av[tv[u]] * g));
+                    }
+                    // segmented sum of v over lanes with equal list (nondecreasing in the lane)
+                    const int tt = tv[u];
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const double y = __shfl_up_sync(FULL, v, o);
+                        const int ty = __shfl_up_sync(FULL, tt, o);
+                        if (lane >= o && ty == tt) v += y;
+                    }
+                    const int tn = __shfl_down_sync(FULL, tt, 1);
+                    if (ok && (lane == 31 || tn != tt)) atomicAdd(&S.dA[tt], v);
+                }
+            }
+        }
+        if (PH == PH_COUNT) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+            if (lane == 0) Cp[i + 1] = cnt;
+        }
+        if (PH == PH_FILL) {
+            __syncwarp();
+            const int P = w <= 32 ? 32 : w <= 64 ? 64 : w <= 128 ? 128 : w <= 256 ? 256 : 512;
+            switch (P) {
+            case 32: w_sort_fill<1>(S.key, w, Ci + cs, lane); break;
+            case 64: w_sort_fill<2>(S.key, w, Ci + cs, lane); break;
+            case 128: w_sort_fill<4>(S.key, w, Ci + cs, lane); break;
+            case 256: w_sort_fill<8>(S.key, w, Ci + cs, lane); break;
+            default: w_sort_fill<16>(S.key, w, Ci + cs, lane); break;
+            }
+        }
+        __syncwarp();
+        if (PH == PH_NUM)
+            for (int c = lane; c < nc; c += 32) Cv[cs + c] = (T)S.val[c];
+        if (PH == PH_BWD && dA)
+            for (int tq = lane; tq < l; tq += 32) dA[as + tq] = (T)S.dA[tq];
+        __syncwarp();
     }
 }
 
@@ -354,32 +616,123 @@ __device__ __forceinline__ void bitonic_keys(int32_t *key, int P)
         }
 }
 
-// lower_bound of v in sorted c[0..n)
-__device__ __forceinline__ int64_t lbound(const int32_t *c, int64_t n, int32_t v)
+
+// ---------------------------------------------------------------- big rows
+// Rows the S and W paths pass on (l_i > kWL or w_i > kWW: power-law heads).  Their products are
+// enumerated flat: k_big_prep stores, at every A position a of a big row, loff[a] = the flat
+// offset of list a's first product within the row, and w_r.  Each thread then walks a
+// CONTIGUOUS run of products (one binary search in loff, then linear), so long B rows are
+// spread over many threads and the loads of a thread are sequential.
+//   symbolic  one CTA per row: w <= kMMaxW -> products gathered to shared memory, bitonic sort,
+//             unique; else bitmap windows over the column range (sorted for free).
+//   numeric / backward  work items of kItem products (k_big_items: single-CTA scan of the
+//             per-row item counts), many CTAs per long row.  The C row is staged in shared
+//             memory when nnz(C_i) <= kValSm, else a sampled index of it is, and the search
+//             ends in global memory.  Single-item rows accumulate C_i in shared memory;
+//             other rows add into Cv / dA with global atomics after k_big_zero.
+constexpr int kItem = 4096;
+constexpr int kValSm = 4096;
+
+struct BigRows {
+    const int32_t *rows;
+    const int *count;
+    int64_t *loff;   // [nnz(A)]
+    int64_t *w;      // [m]  products of the r-th big row
+    int32_t *items;  // [m + 1] item offsets
+};
+
+// last a in [lo, hi) with loff[a] <= e (the list holding product e; empty lists skipped)
+__device__ __forceinline__ int64_t big_list_of(const int64_t *loff, int64_t lo, int64_t hi, int64_t e)
 {
-    int64_t lo = 0, hi = n;
+    hi -= 1;
     while (lo < hi) {
-        int64_t mid = (lo + hi) >> 1;
-        if (c[mid] < v) lo = mid + 1; else hi = mid;
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (loff[mid] <= e) lo = mid; else hi = mid - 1;
     }
     return lo;
 }
 
-// w_i = sum_k len_B(k) over row i (block reduction)
-__device__ __forceinline__ int64_t row_work(int64_t as, int64_t ae, const int32_t *__restrict__ Ai,
-                                            const int64_t *__restrict__ Bp, int64_t *s_red)
+__global__ __launch_bounds__(kGemmTPB) void k_big_prep(BigRows br, const int64_t *__restrict__ Ap,
+                                                       const int32_t *__restrict__ Ai, const int64_t *__restrict__ Bp)
 {
-    int64_t w = 0;
-    for (int64_t a = as + threadIdx.x; a < ae; a += kGemmTPB) {
-        const int32_t k = Ai[a];
-        w += Bp[k + 1] - Bp[k];
+    __shared__ int64_t s_red[kGemmTPB / 32];
+    const int n = *(volatile const int *)br.count;
+    for (int r = blockIdx.x; r < n; r += gridDim.x) {
+        const int64_t i = br.rows[r];
+        const int64_t as = Ap[i], ae = Ap[i + 1];
+        int64_t run = 0;
+        for (int64_t a0 = as; a0 < ae; a0 += kGemmTPB) {
+            const int64_t a = a0 + threadIdx.x;
+            int64_t len = 0;
+            if (a < ae) {
+                const int32_t k = Ai[a];
+                len = Bp[k + 1] - Bp[k];
+            }
+            int64_t tot;
+            const int64_t ex = block_excl_scan_i64(len, s_red, tot);
+            if (a < ae) br.loff[a] = run + ex;
+            run += tot;
+        }
+        if (threadIdx.x == 0) br.w[r] = run;
     }
-    return block_sum_i64(w, s_red);
+}
+
+constexpr int kItemsTPB = 1024;
+
+// single CTA: items[r] = sum_{r' < r} ceil(w_r' / kItem), items[n] = total
+__global__ __launch_bounds__(kItemsTPB) void k_big_items(BigRows br)
+{
+    __shared__ int64_t s_w[kItemsTPB / 32];
+    const int n = *(volatile const int *)br.count;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t run = 0;
+    for (int r0 = 0; r0 < n; r0 += kItemsTPB) {
+        const int r = r0 + threadIdx.x;
+        const int64_t c = r < n ? (br.w[r] + kItem - 1) / kItem : 0;
+        int64_t x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_w[warp] = x;
+        __syncthreads();
+        int64_t off = 0, tot = 0;
+        for (int q = 0; q < kItemsTPB / 32; ++q) {
+            if (q < warp) off += s_w[q];
+            tot += s_w[q];
+        }
+        if (r < n) br.items[r] = (int32_t)(run + off + x - c);
+        run += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) br.items[n] = (int32_t)run;
+}
+
+// walk products [e_lo, e_hi) of the row: f(e, a, b) with a = A position, b = B position
+template <typename F>
+__device__ __forceinline__ void big_walk(const int64_t *__restrict__ loff, const int32_t *__restrict__ Ai,
+                                         const int64_t *__restrict__ Bp, int64_t as, int64_t ae, int64_t e_lo,
+                                         int64_t e_hi, F &&f)
+{
+    if (e_lo >= e_hi) return;
+    int64_t a = big_list_of(loff, as, ae, e_lo);
+    int64_t lo = loff[a], bs = Bp[Ai[a]];
+    int64_t nx = a + 1 < ae ? loff[a + 1] : INT64_MAX;
+    for (int64_t e = e_lo; e < e_hi; ++e) {
+        while (e >= nx) {
+            ++a;
+            lo = nx;
+            nx = a + 1 < ae ? loff[a + 1] : INT64_MAX;
+            bs = Bp[Ai[a]];
+        }
+        f(e, a, bs + (e - lo));
+    }
 }
 
 // ---------------------------------------------------------------- big rows: symbolic
-template <int PH>
-__global__ __launch_bounds__(kGemmTPB) void k_gemm_big_sym(BigList big, int64_t ncolsB,
+template <int PH, bool HUGE>
+__global__ __launch_bounds__(kGemmTPB) void k_gemm_big_sym(BigRows br, int64_t ncolsB,
                                                            const int64_t *__restrict__ Ap,
                                                            const int32_t *__restrict__ Ai,
                                                            const int64_t *__restrict__ Bp,
@@ -387,79 +740,67 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_sym(BigList big, int64_t 
                                                            int32_t *__restrict__ Ci)
 {
     extern __shared__ __align__(16) unsigned char smem[];
-    int32_t *s_key = reinterpret_cast<int32_t *>(smem);   // kMMaxW keys (M path)
-    uint32_t *bm = reinterpret_cast<uint32_t *>(smem);    // kBitmapWords (L path)
-    __shared__ int s_cnt;
+    int32_t *s_key = reinterpret_cast<int32_t *>(smem);   // kMMaxW keys (sort path)
+    uint32_t *bm = reinterpret_cast<uint32_t *>(smem);    // kBitmapWords (bitmap path)
     __shared__ int64_t s_red[kGemmTPB / 32];
-    const int nrows = *(volatile int *)big.count;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int it = blockIdx.x; it < nrows; it += gridDim.x) {
-        const int64_t i = big.rows[it];
+    const int nrows = *(volatile const int *)br.count;
+    for (int r = blockIdx.x; r < nrows; r += gridDim.x) {
+        const int64_t i = br.rows[r];
         const int64_t as = Ap[i], ae = Ap[i + 1];
-        const int64_t w = row_work(as, ae, Ai, Bp, s_red);
-        if (w <= kMMaxW) {
-            if (threadIdx.x == 0) s_cnt = 0;
-            __syncthreads();
-            for (int64_t a = as + warp; a < ae; a += kGemmTPB / 32) {
-                const int32_t k = Ai[a];
-                const int64_t bs = Bp[k];
-                const int bl = (int)(Bp[k + 1] - bs);
-                int base = 0;
-                if (lane == 0 && bl > 0) base = atomicAdd(&s_cnt, bl);
-                base = __shfl_sync(0xffffffffu, base, 0);
-                for (int j = lane; j < bl; j += 32) s_key[base + j] = Bi[bs + j];
-            }
-            __syncthreads();
-            const int wn = s_cnt;
+        const int64_t w = br.w[r];
+        if (HUGE != (w > kMMaxW)) continue;  // the other kernel takes this row
+        if (!HUGE) {
+            const int64_t per = (w + kGemmTPB - 1) / kGemmTPB;
+            const int64_t e_lo = threadIdx.x * per, e_hi = e_lo + per < w ? e_lo + per : w;
+            big_walk(br.loff, Ai, Bp, as, ae, e_lo, e_hi, [&](int64_t e, int64_t, int64_t b) { s_key[e] = Bi[b]; });
+            const int wn = (int)w;
             const int P = pow2ceil_i(wn > 0 ? wn : 1);
             for (int e = wn + threadIdx.x; e < P; e += kGemmTPB) s_key[e] = INT32_MAX;
             __syncthreads();
             bitonic_keys(s_key, P);
-            const int per = (P + kGemmTPB - 1) / kGemmTPB;
-            const int e0 = threadIdx.x * per;
+            const int pe = (P + kGemmTPB - 1) / kGemmTPB;
+            const int e0 = threadIdx.x * pe;
             int64_t mine = 0;
-            for (int e = e0; e < e0 + per && e < wn; ++e) mine += (e == 0 || s_key[e] != s_key[e - 1]);
+            for (int e = e0; e < e0 + pe && e < wn; ++e) mine += (e == 0 || s_key[e] != s_key[e - 1]);
             if (PH == PH_COUNT) {
                 const int64_t tot = block_sum_i64(mine, s_red);
                 if (threadIdx.x == 0) Cp[i + 1] = tot;
             } else {
                 int64_t tot;
-                int64_t r = Cp[i] + block_excl_scan_i64(mine, s_red, tot);
-                for (int e = e0; e < e0 + per && e < wn; ++e)
-                    if (e == 0 || s_key[e] != s_key[e - 1]) Ci[r++] = s_key[e];
+                int64_t o = Cp[i] + block_excl_scan_i64(mine, s_red, tot);
+                for (int e = e0; e < e0 + pe && e < wn; ++e)
+                    if (e == 0 || s_key[e] != s_key[e - 1]) Ci[o++] = s_key[e];
             }
             __syncthreads();
             continue;
         }
         // bitmap windows over [0, ncolsB)
         const int64_t W = (int64_t)kBitmapWords * 32;
+        const int64_t per = (w + kGemmTPB - 1) / kGemmTPB;
+        const int64_t e_lo = threadIdx.x * per, e_hi = e_lo + per < w ? e_lo + per : w;
         int64_t done = 0;
         for (int64_t w0 = 0; w0 < ncolsB; w0 += W) {
             for (int e = threadIdx.x; e < kBitmapWords; e += kGemmTPB) bm[e] = 0u;
             __syncthreads();
-            for (int64_t a = as + warp; a < ae; a += kGemmTPB / 32) {
-                const int32_t k = Ai[a];
-                const int64_t bs = Bp[k], be = Bp[k + 1];
-                for (int64_t b = bs + lane; b < be; b += 32) {
-                    const int64_t j = Bi[b];
-                    if (j >= w0 && j < w0 + W) atomicOr(&bm[(j - w0) >> 5], 1u << (j & 31));
-                }
-            }
+            big_walk(br.loff, Ai, Bp, as, ae, e_lo, e_hi, [&](int64_t, int64_t, int64_t b) {
+                const int64_t j = Bi[b];
+                if (j >= w0 && j < w0 + W) atomicOr(&bm[(j - w0) >> 5], 1u << (j & 31));
+            });
             __syncthreads();
-            constexpr int per = kBitmapWords / kGemmTPB;
-            const int e0 = threadIdx.x * per;
+            constexpr int pw = kBitmapWords / kGemmTPB;
+            const int q0 = threadIdx.x * pw;
             int64_t mine = 0;
-            for (int e = e0; e < e0 + per; ++e) mine += __popc(bm[e]);
+            for (int q = q0; q < q0 + pw; ++q) mine += __popc(bm[q]);
             int64_t tot;
             const int64_t off = block_excl_scan_i64(mine, s_red, tot);
             if (PH == PH_FILL) {
-                int64_t r = Cp[i] + done + off;
-                for (int e = e0; e < e0 + per; ++e) {
-                    uint32_t bits = bm[e];
+                int64_t o = Cp[i] + done + off;
+                for (int q = q0; q < q0 + pw; ++q) {
+                    uint32_t bits = bm[q];
                     while (bits) {
                         const int bpos = __ffs(bits) - 1;
                         bits &= bits - 1;
-                        Ci[r++] = (int32_t)(w0 + (int64_t)e * 32 + bpos);
+                        Ci[o++] = (int32_t)(w0 + (int64_t)q * 32 + bpos);
                     }
                 }
             }
@@ -472,9 +813,27 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_sym(BigList big, int64_t 
 }
 
 // ---------------------------------------------------------------- big rows: numeric + backward
-// C row in shared memory when it fits (nnz(C_i) <= kMMaxW), else searched in global memory.
+// zero the outputs that multi-item / unstaged rows accumulate into with atomics
 template <typename T, int PH>
-__global__ __launch_bounds__(kGemmTPB) void k_gemm_big_val(BigList big, const int64_t *__restrict__ Ap,
+__global__ __launch_bounds__(kGemmTPB) void k_big_zero(BigRows br, const int64_t *__restrict__ Ap,
+                                                       const int64_t *__restrict__ Cp, T *__restrict__ Cv,
+                                                       T *__restrict__ dA)
+{
+    const int n = *(volatile const int *)br.count;
+    for (int r = blockIdx.x; r < n; r += gridDim.x) {
+        const int64_t i = br.rows[r];
+        if (PH == PH_NUM) {
+            const int64_t cs = Cp[i], ce = Cp[i + 1];
+            if (br.w[r] <= kItem && ce - cs <= kValSm) continue;
+            for (int64_t e = cs + threadIdx.x; e < ce; e += kGemmTPB) Cv[e] = (T)0;
+        } else if (dA) {
+            for (int64_t e = Ap[i] + threadIdx.x; e < Ap[i + 1]; e += kGemmTPB) dA[e] = (T)0;
+        }
+    }
+}
+
+template <typename T, int PH>
+__global__ __launch_bounds__(kGemmTPB) void k_gemm_big_val(BigRows br, const int64_t *__restrict__ Ap,
                                                            const int32_t *__restrict__ Ai, const T *__restrict__ Av,
                                                            const int64_t *__restrict__ Bp,
                                                            const int32_t *__restrict__ Bi, const T *__restrict__ Bv,
@@ -483,51 +842,72 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_val(BigList big, const in
                                                            const T *__restrict__ dC, T *__restrict__ dA,
                                                            T *__restrict__ dB)
 {
-    extern __shared__ __align__(16) unsigned char smem[];
-    double *s_val = reinterpret_cast<double *>(smem);                             // acc (NUM) or dC (BWD)
-    int32_t *s_col = reinterpret_cast<int32_t *>(smem + sizeof(double) * kMMaxW);
-    const int nrows = *(volatile int *)big.count;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int it = blockIdx.x; it < nrows; it += gridDim.x) {
-        const int64_t i = big.rows[it];
-        const int64_t as = Ap[i], ae = Ap[i + 1];
+    __shared__ int32_t s_col[kValSm];
+    __shared__ double s_acc[kValSm];
+    const int n = *(volatile const int *)br.count;
+    const int total = n > 0 ? br.items[n] : 0;
+    for (int it = blockIdx.x; it < total; it += gridDim.x) {
+        // the row r holding item it: last r with items[r] <= it
+        int lo = 0, hi = n - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (br.items[mid] <= it) lo = mid; else hi = mid - 1;
+        }
+        const int r = lo;
+        const int64_t i = br.rows[r];
+        const int64_t as = Ap[i], ae = Ap[i + 1], w = br.w[r];
+        const int64_t e0 = (int64_t)(it - br.items[r]) * kItem;
+        const int64_t e1 = e0 + kItem < w ? e0 + kItem : w;
         const int64_t cs = Cp[i], nc = Cp[i + 1] - cs;
-        const bool in_smem = nc <= kMMaxW;
-        if (in_smem) {
-            for (int64_t e = threadIdx.x; e < nc; e += kGemmTPB) {
-                s_col[e] = Ci[cs + e];
-                s_val[e] = PH == PH_NUM ? 0.0 : (double)dC[cs + e];
-            }
-        } else if (PH == PH_NUM) {
-            for (int64_t e = threadIdx.x; e < nc; e += kGemmTPB) Cv[cs + e] = (T)0;
+        const bool insm = nc <= kValSm;
+        const bool local = PH == PH_NUM && insm && w <= kItem;  // accumulate the row in shared memory
+        const int64_t stride = insm ? 1 : (nc + kValSm - 1) / kValSm;
+        const int nq = (int)((nc + stride - 1) / stride);
+        for (int q = threadIdx.x; q < nq; q += kGemmTPB) {
+            s_col[q] = Ci[cs + (int64_t)q * stride];
+            if (local) s_acc[q] = 0.0;
+            if (PH == PH_BWD && insm) s_acc[q] = (double)dC[cs + q];
         }
         __syncthreads();
-        const int32_t *ccol = in_smem ? s_col : Ci + cs;
-        for (int64_t a = as + warp; a < ae; a += kGemmTPB / 32) {
-            const int32_t k = Ai[a];
-            const double av = (double)Av[a];
-            const int64_t bs = Bp[k], be = Bp[k + 1];
-            double t = 0.0;
-            for (int64_t b = bs + lane; b < be; b += 32) {
-                const int64_t pos = lbound(ccol, nc, Bi[b]);
-                const double bv = (double)Bv[b];
-                if (PH == PH_NUM) {
-                    if (in_smem) atomicAdd(&s_val[pos], av * bv);
-                    else red_add(&Cv[cs + pos], (T)(av * bv));
-                } else {
-                    const double g = in_smem ? s_val[pos] : (double)dC[cs + pos];
-                    t = fma(g, bv, t);
-                    if (dB) red_add(&dB[b], (T)(av * g));
+        const int64_t per = (e1 - e0 + kGemmTPB - 1) / kGemmTPB;
+        const int64_t p_lo = e0 + threadIdx.x * per, p_hi = p_lo + per < e1 ? p_lo + per : e1;
+        int64_t cur_a = -1;
+        double av = 0.0, dacc = 0.0;
+        big_walk(br.loff, Ai, Bp, as, ae, p_lo, p_hi, [&](int64_t, int64_t a, int64_t b) {
+            if (a != cur_a) {
+                if (PH == PH_BWD && cur_a >= 0 && dA) red_add(&dA[cur_a], (T)dacc);
+                cur_a = a;
+                av = (double)Av[a];
+                dacc = 0.0;
+            }
+            const int32_t j = Bi[b];
+            const double bv = (double)Bv[b];
+            int64_t pos;
+            if (insm) {
+                pos = lbound(s_col, nc, j);
+            } else {
+                int qlo = 0, qhi = nq - 1;  // last q with s_col[q] <= j
+                while (qlo < qhi) {
+                    const int mid = (qlo + qhi + 1) >> 1;
+                    if (s_col[mid] <= j) qlo = mid; else qhi = mid - 1;
                 }
+                const int64_t base = (int64_t)qlo * stride;
+                const int64_t len = base + stride < nc ? stride : nc - base;
+                pos = base + lbound(Ci + cs + base, len, j);
             }
-            if (PH == PH_BWD) {
-                for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-                if (lane == 0 && dA) dA[a] = (T)t;
+            if (PH == PH_NUM) {
+                if (local) atomicAdd(&s_acc[pos], av * bv);
+                else red_add(&Cv[cs + pos], (T)(av * bv));
+            } else {
+                const double g = insm ? s_acc[pos] : (double)dC[cs + pos];
+                dacc = fma(g, bv, dacc);
+                if (dB) red_add(&dB[b], (T)(av * g));
             }
-        }
+        });
+        if (PH == PH_BWD && cur_a >= 0 && dA) red_add(&dA[cur_a], (T)dacc);
         __syncthreads();
-        if (PH == PH_NUM && in_smem)
-            for (int64_t e = threadIdx.x; e < nc; e += kGemmTPB) Cv[cs + e] = (T)s_val[e];
+        if (local)
+            for (int64_t e = threadIdx.x; e < nc; e += kGemmTPB) Cv[cs + e] = (T)s_acc[e];
         __syncthreads();
     }
 }
@@ -536,19 +916,26 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_val(BigList big, const in
 static unsigned big_grid() { return (unsigned)(kNumSMs * 2); }
 
 static size_t big_sym_smem() { return sizeof(uint32_t) * kBitmapWords; }
-static size_t big_val_smem() { return (sizeof(double) + sizeof(int32_t)) * kMMaxW; }
+static size_t big_sort_smem() { return sizeof(int32_t) * kMMaxW; }
+static unsigned sort_grid() { return (unsigned)(kNumSMs * 4); }
+static unsigned val_grid() { return (unsigned)(kNumSMs * 4); }
+static size_t w_smem() { return sizeof(WSmem) * kWWarps; }
+static unsigned w_grid() { return (unsigned)(kNumSMs * 7); }
 
 static int set_smem_attrs()
 {
     static bool done = false;
     if (done) return CSRK_OK;
-    const int bs = (int)big_sym_smem(), bv = (int)big_val_smem();
-    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_sym<PH_COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bs));
-    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_sym<PH_FILL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bs));
-    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_val<double, PH_NUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, bv));
-    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_val<double, PH_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, bv));
-    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_val<float, PH_NUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, bv));
-    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_val<float, PH_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, bv));
+    const int bs = (int)big_sym_smem();
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_sym<PH_COUNT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bs));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_sym<PH_FILL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bs));
+    const int ww = (int)w_smem();
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, ww));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_FILL>, cudaFuncAttributeMaxDynamicSharedMemorySize, ww));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_NUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, ww));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, ww));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<float, PH_NUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, ww));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<float, PH_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, ww));
     done = true;
     return CSRK_OK;
 }
@@ -569,30 +956,48 @@ static size_t s_smem(int PH, int use)
 static int stage_fill() { static int v = knob("GEMM_STAGE_FILL", 1); return v; }
 static int stage_vals() { static int v = knob("GEMM_STAGE_VALS", 0); return v; }
 
-static void carve_big(const csrk_pattern &A, BigList &b, Bump &ws)
+// both queue counters live in one 8-byte word so one memset clears them
+static void carve_lists(const csrk_pattern &A, BigList &wl, BigList &big, BigRows &br, Bump &ws)
 {
-    b.rows = ws.take<int32_t>(A.nrows > 0 ? A.nrows : 1);
-    b.count = ws.take<int>(1);
+    const int64_t m = A.nrows > 0 ? A.nrows : 1;
+    wl.rows = ws.take<int32_t>(m);
+    big.rows = ws.take<int32_t>(m);
+    int *cnt = ws.take<int>(2);
+    wl.count = cnt;
+    big.count = cnt ? cnt + 1 : nullptr;
+    br.rows = big.rows;
+    br.count = big.count;
+    br.loff = ws.take<int64_t>(A.nnz > 0 ? A.nnz : 1);
+    br.w = ws.take<int64_t>(m);
+    br.items = ws.take<int32_t>(m + 1);
 }
 
 int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, int32_t *Ci, int64_t *nnzC_host,
                     Bump &ws, cudaStream_t s)
 {
-    BigList b{};
-    carve_big(A, b, ws);
+    BigList wl{}, b{};
+    BigRows br{};
+    carve_lists(A, wl, b, br, ws);
     if (ws.sizing()) return scan_counts_i64(nullptr, A.nrows, ws, s);
     const int64_t m = A.nrows;
     CSRK_TRY(set_smem_attrs());
     const unsigned gS = (unsigned)cdiv(m, kSTPB);
+    const int32_t *Bi = B.indices;
+    const double *dn = nullptr;
+    double *dw = nullptr;
     if (!Ci) {
         CSRK_CUDA(cudaMemsetAsync(Cp, 0, sizeof(int64_t), s));
         if (m > 0) {
-            CSRK_CUDA(cudaMemsetAsync(b.count, 0, sizeof(int), s));
-            CSRK_LAUNCH((k_gemm_S<double, PH_COUNT>), gS, kSTPB, 0, s, m, A.indptr, A.indices,
-                        (const double *)nullptr, B.indptr, B.indices, (const double *)nullptr, Cp, (int32_t *)nullptr,
-                        (double *)nullptr, (const double *)nullptr, (double *)nullptr, (double *)nullptr, b, 0);
-            CSRK_LAUNCH(k_gemm_big_sym<PH_COUNT>, big_grid(), kGemmTPB, big_sym_smem(), s, b, B.ncols, A.indptr,
-                        A.indices, B.indptr, B.indices, Cp, (int32_t *)nullptr);
+            CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 2 * sizeof(int), s));
+            CSRK_LAUNCH((k_gemm_S<double, PH_COUNT>), gS, kSTPB, 0, s, m, A.indptr, A.indices, dn, B.indptr, Bi, dn,
+                        Cp, (int32_t *)nullptr, dw, dn, dw, dw, wl, b, 0);
+            CSRK_LAUNCH((k_gemm_W<double, PH_COUNT>), w_grid(), kWTPB, w_smem(), s, wl, b, A.indptr, A.indices, dn,
+                        B.indptr, Bi, dn, Cp, (int32_t *)nullptr, dw, dn, dw, dw);
+            CSRK_LAUNCH(k_big_prep, big_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, B.indptr);
+            CSRK_LAUNCH((k_gemm_big_sym<PH_COUNT, false>), sort_grid(), kGemmTPB, big_sort_smem(), s, br, B.ncols,
+                        A.indptr, A.indices, B.indptr, Bi, Cp, (int32_t *)nullptr);
+            CSRK_LAUNCH((k_gemm_big_sym<PH_COUNT, true>), big_grid(), kGemmTPB, big_sym_smem(), s, br, B.ncols,
+                        A.indptr, A.indices, B.indptr, Bi, Cp, (int32_t *)nullptr);
             CSRK_TRY(scan_counts_i64(Cp, m, ws, s));
         }
         CSRK_CUDA(cudaMemcpyAsync(nnzC_host, Cp + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -600,12 +1005,16 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, i
         return CSRK_OK;
     }
     if (m == 0) return CSRK_OK;
-    CSRK_CUDA(cudaMemsetAsync(b.count, 0, sizeof(int), s));
+    CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 2 * sizeof(int), s));
     CSRK_LAUNCH((k_gemm_S<double, PH_FILL>), gS, kSTPB, s_smem<double>(PH_FILL, stage_fill()), s, m, A.indptr,
-                A.indices, (const double *)nullptr, B.indptr, B.indices, (const double *)nullptr, Cp, Ci,
-                (double *)nullptr, (const double *)nullptr, (double *)nullptr, (double *)nullptr, b, stage_fill());
-    CSRK_LAUNCH(k_gemm_big_sym<PH_FILL>, big_grid(), kGemmTPB, big_sym_smem(), s, b, B.ncols, A.indptr, A.indices,
-                B.indptr, B.indices, Cp, Ci);
+                A.indices, dn, B.indptr, Bi, dn, Cp, Ci, dw, dn, dw, dw, wl, b, stage_fill());
+    CSRK_LAUNCH((k_gemm_W<double, PH_FILL>), w_grid(), kWTPB, w_smem(), s, wl, b, A.indptr, A.indices, dn, B.indptr,
+                Bi, dn, Cp, Ci, dw, dn, dw, dw);
+    CSRK_LAUNCH(k_big_prep, big_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, B.indptr);
+    CSRK_LAUNCH((k_gemm_big_sym<PH_FILL, false>), sort_grid(), kGemmTPB, big_sort_smem(), s, br, B.ncols, A.indptr,
+                A.indices, B.indptr, Bi, Cp, Ci);
+    CSRK_LAUNCH((k_gemm_big_sym<PH_FILL, true>), big_grid(), kGemmTPB, big_sym_smem(), s, br, B.ncols, A.indptr,
+                A.indices, B.indptr, Bi, Cp, Ci);
     return CSRK_OK;
 }
 
@@ -613,27 +1022,39 @@ template <typename T>
 static int spgemm_values_t(int PH, const csrk_pattern &A, const T *Av, const csrk_pattern &B, const T *Bv,
                            const csrk_pattern &C, T *Cv, const T *dC, T *dA, T *dB, Bump &ws, cudaStream_t s)
 {
-    BigList b{};
-    carve_big(A, b, ws);
+    BigList wl{}, b{};
+    BigRows br{};
+    carve_lists(A, wl, b, br, ws);
     if (ws.sizing()) return CSRK_OK;
     CSRK_TRY(set_smem_attrs());
     if (PH == PH_BWD && dB) CSRK_CUDA(cudaMemsetAsync(dB, 0, sizeof(T) * (size_t)B.nnz, s));
     const int64_t m = A.nrows;
     if (m == 0) return CSRK_OK;
-    CSRK_CUDA(cudaMemsetAsync(b.count, 0, sizeof(int), s));
+    CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 2 * sizeof(int), s));
     const unsigned gS = (unsigned)cdiv(m, kSTPB);
     int64_t *Cp = const_cast<int64_t *>(C.indptr);
+    T *tn = nullptr;
+    const T *ctn = nullptr;
     if (PH == PH_NUM) {
         CSRK_LAUNCH((k_gemm_S<T, PH_NUM>), gS, kSTPB, s_smem<T>(PH_NUM, stage_vals()), s, m, A.indptr, A.indices,
-                    Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, Cv, (const T *)nullptr, (T *)nullptr,
-                    (T *)nullptr, b, stage_vals());
-        CSRK_LAUNCH((k_gemm_big_val<T, PH_NUM>), big_grid(), kGemmTPB, big_val_smem(), s, b, A.indptr, A.indices, Av,
-                    B.indptr, B.indices, Bv, C.indptr, C.indices, Cv, (const T *)nullptr, (T *)nullptr, (T *)nullptr);
+                    Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, Cv, ctn, tn, tn, wl, b, stage_vals());
+        CSRK_LAUNCH((k_gemm_W<T, PH_NUM>), w_grid(), kWTPB, w_smem(), s, wl, b, A.indptr, A.indices, Av, B.indptr,
+                    B.indices, Bv, Cp, const_cast<int32_t *>(C.indices), Cv, ctn, tn, tn);
+        CSRK_LAUNCH(k_big_prep, big_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, B.indptr);
+        CSRK_LAUNCH(k_big_items, 1, kItemsTPB, 0, s, br);
+        CSRK_LAUNCH((k_big_zero<T, PH_NUM>), big_grid(), kGemmTPB, 0, s, br, A.indptr, C.indptr, Cv, tn);
+        CSRK_LAUNCH((k_gemm_big_val<T, PH_NUM>), val_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, Av, B.indptr,
+                    B.indices, Bv, C.indptr, C.indices, Cv, ctn, tn, tn);
     } else {
         CSRK_LAUNCH((k_gemm_S<T, PH_BWD>), gS, kSTPB, s_smem<T>(PH_BWD, stage_vals()), s, m, A.indptr, A.indices,
-                    Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, (T *)nullptr, dC, dA, dB, b, stage_vals());
-        CSRK_LAUNCH((k_gemm_big_val<T, PH_BWD>), big_grid(), kGemmTPB, big_val_smem(), s, b, A.indptr, A.indices, Av,
-                    B.indptr, B.indices, Bv, C.indptr, C.indices, (T *)nullptr, dC, dA, dB);
+                    Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, tn, dC, dA, dB, wl, b, stage_vals());
+        CSRK_LAUNCH((k_gemm_W<T, PH_BWD>), w_grid(), kWTPB, w_smem(), s, wl, b, A.indptr, A.indices, Av, B.indptr,
+                    B.indices, Bv, Cp, const_cast<int32_t *>(C.indices), tn, dC, dA, dB);
+        CSRK_LAUNCH(k_big_prep, big_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, B.indptr);
+        CSRK_LAUNCH(k_big_items, 1, kItemsTPB, 0, s, br);
+        CSRK_LAUNCH((k_big_zero<T, PH_BWD>), big_grid(), kGemmTPB, 0, s, br, A.indptr, C.indptr, tn, dA);
+        CSRK_LAUNCH((k_gemm_big_val<T, PH_BWD>), val_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, Av, B.indptr,
+                    B.indices, Bv, C.indptr, C.indices, tn, dC, dA, dB);
     }
     return CSRK_OK;
 }
