@@ -282,6 +282,85 @@ def run_trsv_workload(args, torch, ck):
     return 0
 
 
+def run_gcn_workload(args, torch, ck):
+    """GCN layer (PAPER 4.4 Fig. 12) at N = 1: one training step of one layer on a
+    synthetic power-law graph of 2^20 nodes with 5 edges per node on average (the size of the
+    paper's largest SuiteSparse graphs), fp32, C = F = 16 (the paper's hidden width):
+    forward XTheta = X Theta + fused propagation, backward dZ (transposed propagation with a cached
+    plan), dTheta = X^T dZ, dX = dZ Theta^T, dbias.  L2 flushed before every step.
+    Algorithmic bytes per op: every operand read once, every result written once."""
+    dev = torch.device("cuda", 0)
+    s, C, F = 4, 16, 16
+    G = synth.powerlaw_graph(1 << 20, 5.0, 4401, dtype=np.float32)
+    n, nnz = G.nrows, G.nnz
+    Gd = ck.CSR.from_host(G)
+    X = torch.from_numpy(synth.dense((n, C), 1, np.float32)).to(dev)
+    W = torch.from_numpy(synth.dense((C, F), 2, np.float32)).to(dev)
+    b = torch.from_numpy(synth.dense(F, 3, np.float32)).to(dev)
+    dY = torch.from_numpy(synth.dense((n, F), 4, np.float32)).to(dev)
+    plan = ck.csr_transpose(Gd, with_values=False)
+    Z, Y, dZ, dX = (torch.empty((n, F), device=dev), torch.empty((n, F), device=dev),
+                    torch.empty((n, F), device=dev), torch.empty((n, C), device=dev))
+    dW, db = torch.empty((C, F), device=dev), torch.empty(F, device=dev)
+    D = torch.empty(n, dtype=torch.float64, device=dev)
+    pat = 8 * (n + 1) + 4 * nnz
+    ops = {
+        "xtheta": (lambda: ck.dense_gemm_nn(X, W, out=Z), (s * n * (C + F), 2 * n * C * F)),
+        "gcn_fwd": (lambda: ck.gcn_fwd(Gd, Z, b, out=Y, D=D), (pat + s * nnz + 2 * s * n * F + 8 * n, 2 * nnz * F)),
+        "gcn_bwd": (lambda: ck.gcn_bwd(Gd, D, dY, plan=plan, dZ=dZ, dbias=db),
+                    (pat + s * nnz + 2 * s * n * F + 8 * n, 2 * nnz * F + n * F)),
+        "dtheta": (lambda: ck.dense_gemm_tn(X, dZ, out=dW), (s * n * (C + F), 2 * n * C * F)),
+        "dx": (lambda: ck.dense_gemm_nn(dZ, W, transW=True, out=dX), (s * n * (C + F), 2 * n * C * F)),
+    }
+    return _time_ops(args, torch, ck, ops, "GCN layer fwd+bwd algorithmic GB/s", "f32",
+                     "GCN layer (Fig. 12): power-law graph 1,048,576 nodes, 5,242,880 edges (max degree "
+                     f"{int(np.diff(G.indptr).max())}), fp32, C = F = 16, fwd + bwd with a cached transpose plan")
+
+
+def _time_ops(args, torch, ck, ops, metric, dtype, workload):
+    """Time a dict name -> (fn, (bytes, flops)) op by op: CUDA events on the current stream,
+    L2 flushed (512 MiB write) before every op, median over --steps."""
+    dev = torch.device("cuda", 0)
+    l2 = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        for f, _c in ops.values():
+            f()
+    torch.cuda.synchronize()
+    times = {k: [] for k in ops}
+    l0 = ck.launch_count()
+    with Clocks(0) as clk:
+        for _ in range(args.steps):
+            for k, (f, _c) in ops.items():
+                l2.zero_()
+                a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                f()
+                e.record(st)
+                times[k].append((a, e))
+        torch.cuda.synchronize()
+    launches = ck.launch_count() - l0
+    peak = _peak()
+    rep, tot_b, tot_f, tot_ms = {}, 0, 0, 0.0
+    for k, ev in times.items():
+        ms = float(np.median([a.elapsed_time(e) for a, e in ev]))
+        b, fl = ops[k][1]
+        rep[k] = {"ms": round(ms, 4), "GB/s": round(b / ms / 1e6, 1), "GFLOP/s": round(fl / ms / 1e6, 1),
+                  "frac": round(b / ms / 1e6 / peak, 3), "bytes": b}
+        tot_b, tot_f, tot_ms = tot_b + b, tot_f + fl, tot_ms + ms
+    dom = max(rep, key=lambda k: rep[k]["ms"])
+    out = {"metric": metric, "value": round(tot_b / tot_ms / 1e6, 2), "unit": "GB/s", "n_gpus": 1,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot_ms, 4), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+           "config": {"workload": workload, "l2": "flushed (512 MiB write) before every timed op"},
+           "gflops": round(tot_f / tot_ms / 1e6, 2),
+           "roofline": {"bound": "hbm", "kernel": dom, "achieved": rep[dom]["GB/s"], "peak": peak, "unit": "GB/s",
+                        "frac": rep[dom]["frac"], "traffic": None},
+           "ops": rep, "gpu_launches": int(launches / max(args.steps, 1)), "clocks": clk.summary()}
+    print(json.dumps(out))
+    return 0
+
+
 def _peak():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
@@ -491,7 +570,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5", "trsv"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5", "trsv", "gcn"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -505,6 +584,8 @@ def main():
         return run_cfg5(args, torch, ck)
     if args.workload == "trsv":
         return run_trsv_workload(args, torch, ck)
+    if args.workload == "gcn":
+        return run_gcn_workload(args, torch, ck)
     if args.workload in ("cfg3", "cfg4"):
         return run_ops_workload(args, torch, ck, int(args.workload[-1]))
 

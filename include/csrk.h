@@ -81,7 +81,10 @@ typedef enum {
     CSRK_WS_SPADD_SYMBOLIC = 9,/* numeric / bwd need no workspace */
     CSRK_WS_SPAI = 10,       /* A = C = pattern(M A), B = R = pattern(I) U C, k = n */
     CSRK_WS_SPTRSV_FWD = 11, /* A = T */
-    CSRK_WS_SPTRSV_BWD = 12  /* A = T; have_plan = 1 if T^T (pattern + perm) is passed */
+    CSRK_WS_SPTRSV_BWD = 12, /* A = T; have_plan = 1 if T^T (pattern + perm) is passed */
+    CSRK_WS_GCN_FWD = 13,    /* A = graph, k = F */
+    CSRK_WS_GCN_BWD = 14,    /* A = graph, k = F, have_plan */
+    CSRK_WS_DENSE_GEMM_TN = 15 /* A->nrows = n, A->ncols = C, k = F (only the sizes are read) */
 } csrk_ws_op;
 
 /*
@@ -260,6 +263,48 @@ int csrk_sptrsv_fwd(csrk_dtype dtype, csrk_pattern T, const void *T_val, int upp
 int csrk_sptrsv_bwd(csrk_dtype dtype, csrk_pattern T, const void *T_val, const csrk_pattern *TT,
                     const int64_t *TT_perm, int upper, int unit_diag, const void *x, const void *v, void *dT_val,
                     void *db, void *ws, size_t ws_bytes, csrk_stream_t stream);
+
+/*
+ * GCN propagation -- the sparse part of the GCN layer (PAPER 4.4, Eq. gcn_update),
+ * evaluated as the paper's listing (Fig. 12) from XTheta on:
+ *     D_i = (sum of the stored values of row i + 1)^(-1/2)   ("D = (graph.row_sum() + 1.) ** -0.5")
+ *     Y   = D (A (D Z) + D Z) + bias                          ("C = D[:, None] * (graph @ DXTheta
+ *                                                              + DXTheta)", "return C + bias")
+ * A: n x n graph (values = edge weights; the + I of A~ = A + I is implicit, never stored).
+ * Z = X Theta and Y: n x F row-major (ld >= F), 1 <= F <= 128; bias[F] nullable; D[n] (fp64,
+ * required) receives D for the backward.  One fused SpMM (the scalings in its gather and
+ * epilogue).  Y must not alias Z.  Workspace: CSRK_WS_GCN_FWD (k = F).
+ */
+int csrk_gcn_fwd(csrk_dtype dtype, csrk_pattern A, const void *A_val, int64_t F, const void *Z, int64_t ldz,
+                 const void *bias, void *Y, int64_t ldy, double *D, void *ws, size_t ws_bytes, csrk_stream_t stream);
+
+/*
+ * GCN propagation backward (VJP of csrk_gcn_fwd with the graph constant, as in the paper's
+ * training where only Theta and bias are parameters):
+ *     dZ    = D (A^T (D dY) + D dY)     (the transposed propagation; "a matrix transpose is
+ *                                         needed to compute the VJP in the backward pass")
+ *     dbias = sum_i dY_i                (column sums, fp64)
+ * D from csrk_gcn_fwd.  dZ, dbias nullable (both NULL: no-op).  AT / AT_perm: optional cached
+ * transpose plan of A (else built in the workspace).  Workspace: CSRK_WS_GCN_BWD.
+ */
+int csrk_gcn_bwd(csrk_dtype dtype, csrk_pattern A, const void *A_val, const csrk_pattern *AT, const int64_t *AT_perm,
+                 int64_t F, const double *D, const void *dY, int64_t lddy, void *dZ, int64_t lddz, void *dbias,
+                 void *ws, size_t ws_bytes, csrk_stream_t stream);
+
+/*
+ * Small dense products of the GCN layer (Fig. 12 "XTheta = X @ self.weights" and its VJP):
+ *   csrk_dense_gemm_nn:  Z[n x F] = X[n x C] W        (transW = 0, W: C x F row-major)
+ *                        Z[n x F] = X[n x C] W^T      (transW = 1, W: F x C row-major; dX = dZ Theta^T)
+ *                        W is staged in shared memory (C F <= 25600); no workspace.
+ *   csrk_dense_gemm_tn:  dW[C x F] = X^T dZ           (dTheta; fp64 accumulation, workspace
+ *                        CSRK_WS_DENSE_GEMM_TN).
+ * Row-major, ld >= the row width.  Memory-bound tall-skinny products (C, F ~ 16): one pass over
+ * the n rows, no tensor cores.
+ */
+int csrk_dense_gemm_nn(csrk_dtype dtype, int64_t n, int64_t C, int64_t F, const void *X, int64_t ldx, const void *W,
+                       int transW, void *Z, int64_t ldz, csrk_stream_t stream);
+int csrk_dense_gemm_tn(csrk_dtype dtype, int64_t n, int64_t C, int64_t F, const void *X, int64_t ldx, const void *dZ,
+                       int64_t lddz, void *dW, void *ws, size_t ws_bytes, csrk_stream_t stream);
 
 /*
  * Learned-preconditioner PCG training step -- the config-5 composition of SURVEY 8(a) row a14

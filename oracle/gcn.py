@@ -56,9 +56,17 @@ def gcn_prop(A, Z, bias=None, want_grad=None):
         S = S + bt.detach().abs()
     out = {"Y": Y.detach().numpy(), "S": S.numpy(), "D": D.numpy()}
     if want_grad is not None:
-        Y.backward(torch.tensor(np.asarray(want_grad, np.float64)))
+        dY = torch.tensor(np.asarray(want_grad, np.float64))
+        Y.backward(dY)
         out["dZ"] = Zt.grad.numpy()
         out["dbias"] = None if bt is None else bt.grad.numpy()
+        # magnitudes of the adjoint's terms: S_dZ = D (|A|^T |D dY| + |D dY|), S_dbias = sum_i |dY_i|
+        absgT = absg.to_dense().t().to_sparse_csr() if A.nrows <= 4096 else \
+            torch.sparse_coo_tensor(torch.stack([graph.col_indices(), torch.repeat_interleave(
+                torch.arange(A.nrows), graph.crow_indices().diff())]), graph.values().abs(), graph.shape).coalesce()
+        aG = D.abs()[:, None] * dY.abs()
+        out["S_dZ"] = (D.abs()[:, None] * (absgT @ aG + aG)).numpy()
+        out["S_dbias"] = dY.abs().sum(0).numpy()
     return out
 
 

@@ -265,6 +265,60 @@ int csrk_sptrsv_bwd(csrk_dtype dtype, csrk_pattern T, const void *T_val, const c
     });
 }
 
+int csrk_gcn_fwd(csrk_dtype dtype, csrk_pattern A, const void *A_val, int64_t F, const void *Z, int64_t ldz,
+                 const void *bias, void *Y, int64_t ldy, double *D, void *ws, size_t ws_bytes, csrk_stream_t stream)
+{
+    CSRK_TRY(check_dtype(dtype));
+    CSRK_TRY(check_pat(A));
+    if (A.nrows != A.ncols) return CSRK_ERR_DIM_MISMATCH;
+    if (F < 1 || F > 128 || ldz < F || ldy < F) return CSRK_ERR_INVALID_ARG;
+    if (A.nrows > 0 && (!Z || !Y || !D)) return CSRK_ERR_INVALID_ARG;
+    if (A.nnz > 0 && !A_val) return CSRK_ERR_INVALID_ARG;
+    CSRK_TRY(validate_pattern(A, (cudaStream_t)stream));
+    return with_ws(ws, ws_bytes, [&](Bump &bw) {
+        return gcn_fwd(dtype, A, A_val, F, Z, ldz, bias, Y, ldy, D, bw, (cudaStream_t)stream);
+    });
+}
+
+int csrk_gcn_bwd(csrk_dtype dtype, csrk_pattern A, const void *A_val, const csrk_pattern *AT, const int64_t *AT_perm,
+                 int64_t F, const double *D, const void *dY, int64_t lddy, void *dZ, int64_t lddz, void *dbias,
+                 void *ws, size_t ws_bytes, csrk_stream_t stream)
+{
+    CSRK_TRY(check_dtype(dtype));
+    CSRK_TRY(check_pat(A));
+    CSRK_TRY(check_plan(A, AT, AT_perm));
+    if (A.nrows != A.ncols) return CSRK_ERR_DIM_MISMATCH;
+    if (F < 1 || F > 128 || lddy < F || (dZ && lddz < F)) return CSRK_ERR_INVALID_ARG;
+    if (!dZ && !dbias) return CSRK_OK;
+    if (A.nrows > 0 && (!dY || !D)) return CSRK_ERR_INVALID_ARG;
+    if (A.nnz > 0 && !A_val && dZ) return CSRK_ERR_INVALID_ARG;
+    CSRK_TRY(validate_pattern(A, (cudaStream_t)stream));
+    return with_ws(ws, ws_bytes, [&](Bump &bw) {
+        return gcn_bwd(dtype, A, A_val, AT, AT_perm, F, D, dY, lddy, dZ, lddz, dbias, bw, (cudaStream_t)stream);
+    });
+}
+
+int csrk_dense_gemm_nn(csrk_dtype dtype, int64_t n, int64_t C, int64_t F, const void *X, int64_t ldx, const void *W,
+                       int transW, void *Z, int64_t ldz, csrk_stream_t stream)
+{
+    CSRK_TRY(check_dtype(dtype));
+    if (n < 0 || C < 0 || F < 0 || ldx < C || ldz < F) return CSRK_ERR_INVALID_ARG;
+    if (C * F * (int64_t)sizeof(double) > 200 * 1024) return CSRK_ERR_INVALID_ARG;  // W staged in shared memory
+    if (n > 0 && F > 0 && (!Z || (C > 0 && (!X || !W)))) return CSRK_ERR_INVALID_ARG;
+    return dense_gemm_nn(dtype, n, C, F, X, ldx, W, transW ? 1 : 0, Z, ldz, (cudaStream_t)stream);
+}
+
+int csrk_dense_gemm_tn(csrk_dtype dtype, int64_t n, int64_t C, int64_t F, const void *X, int64_t ldx, const void *dZ,
+                       int64_t lddz, void *dW, void *ws, size_t ws_bytes, csrk_stream_t stream)
+{
+    CSRK_TRY(check_dtype(dtype));
+    if (n < 0 || C < 0 || F < 0 || ldx < C || lddz < F) return CSRK_ERR_INVALID_ARG;
+    if (C * F > 0 && (!dW || (n > 0 && (!X || !dZ)))) return CSRK_ERR_INVALID_ARG;
+    return with_ws(ws, ws_bytes, [&](Bump &bw) {
+        return dense_gemm_tn(dtype, n, C, F, X, ldx, dZ, lddz, dW, bw, (cudaStream_t)stream);
+    });
+}
+
 int csrk_pcg_loss_grad(csrk_pattern A, const double *A_val, csrk_pattern L, const double *L_val, const double *b,
                        int n_it, double gamma, double *loss_host, double *resid_host, double *dL_val, void *ws,
                        size_t ws_bytes, csrk_stream_t stream)
@@ -333,6 +387,14 @@ int csrk_workspace_size(csrk_ws_op op, csrk_dtype dtype, const csrk_pattern *A, 
     case CSRK_WS_SPTRSV_FWD: st = sptrsv_fwd(dtype, Ar, d, 0, 0, d, (void *)d, b, 0); break;
     case CSRK_WS_SPTRSV_BWD:
         st = sptrsv_bwd(dtype, Ar, d, plan, pperm, 0, 0, d, d, (void *)d, (void *)d, b, 0);
+        break;
+    case CSRK_WS_GCN_FWD: st = gcn_fwd(dtype, Ar, d, k, d, k, d, (void *)d, k, (double *)d, b, 0); break;
+    case CSRK_WS_GCN_BWD:
+        st = gcn_bwd(dtype, Ar, d, plan, pperm, k, (const double *)d, d, k, (void *)d, k, (void *)d, b, 0);
+        break;
+    case CSRK_WS_DENSE_GEMM_TN:
+        /* A->nrows = n, A->ncols = C, k = F */
+        st = dense_gemm_tn(dtype, Ar.nrows, Ar.ncols, k, d, Ar.ncols, d, k, (void *)d, b, 0);
         break;
     case CSRK_WS_PCG: {
         if (!B || k < 1) return CSRK_ERR_INVALID_ARG;

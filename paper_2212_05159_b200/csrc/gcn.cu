@@ -1,0 +1,343 @@
+// gcn.cu -- the GCN layer of PAPER 4.4, Eq. gcn_update
+// evaluated right to left as the paper's listing does (Fig. 12):
+//
+//   D       = (graph.row_sum() + 1.) ** -0.5             k_gcn_deg
+//   XTheta  = X @ weights                                k_rowgemm        (csrk_dense_gemm_nn)
+//   C       = D[:, None] * (graph @ (D Z) + D Z) + bias  k_gcn_prop       (csrk_gcn_fwd)
+//
+// The propagation is one SpMM with the D scalings fused into its gather (a_p D_j per neighbour)
+// and epilogue (D_i, the identity term D_i Z_i of A~ = A + I, the bias): Z is read once per
+// stored entry and Y written once.  Backward (csrk_gcn_bwd): dZ = D (A^T (D dY) + D dY) -- the
+// same kernel over the rows of A^T (cached plan, or a transpose built in the workspace; values
+// gathered through perm) -- and dbias = column sums of dY.  dTheta = X^T dZ (k_gemm_tn) and
+// dX = dZ Theta^T (k_rowgemm) close the layer.  Rows of width F are handled by G = F / V lanes
+// (V = 4 values per lane, vector loads), 32 / G rows per warp; rows with more than kGcnLong
+// neighbours (power-law hubs) are queued for a warp each.  All reductions in fp64.
+#include "ops.cuh"
+#include "rows.cuh"
+
+namespace csrk {
+
+constexpr int kGcnTPB = 256;
+constexpr int kGcnLong = 64;
+constexpr int kV = 4;
+
+__global__ void k_gcn_deg(int64_t n, const int64_t *__restrict__ indptr, const float *__restrict__ vf,
+                          const double *__restrict__ vd, double *__restrict__ D)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = 1.0;  // the + 1 of A~ = A + I
+    for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) s += vd ? vd[p] : (double)vf[p];
+    D[i] = 1.0 / sqrt(s);
+}
+
+template <typename T>
+struct GcnArgs {
+    int64_t n, F;
+    const int64_t *indptr;
+    const int32_t *indices;
+    const T *vals;
+    const int64_t *perm;  // nullable: value of entry p is vals[perm[p]]
+    const double *D;
+    const T *Z;           // gathered operand (Z fwd, dY bwd)
+    int64_t ldz;
+    const T *bias;        // nullable
+    T *Y;
+    int64_t ldy;
+    RowList L;
+};
+
+template <typename T>
+__device__ __forceinline__ void gcn_load(const T *p, int64_t c, int64_t F, double (&v)[kV])
+{
+#pragma unroll
+    for (int q = 0; q < kV; ++q) v[q] = c + q < F ? (double)p[c + q] : 0.0;
+}
+
+// out row i = D_i (sum_p a_p D_j Z_j + D_i Z_i) + bias, lanes [g*G, g*G + G) of a warp own row i
+template <typename T>
+__device__ __forceinline__ void gcn_finish(const GcnArgs<T> &a, int64_t i, int64_t c, double (&acc)[kV])
+{
+    const double di = a.D[i];
+    double z[kV];
+    gcn_load(a.Z + i * a.ldz, c, a.F, z);
+#pragma unroll
+    for (int q = 0; q < kV; ++q) {
+        if (c + q < a.F) {
+            double y = di * fma(di, z[q], acc[q]);
+            if (a.bias) y += (double)a.bias[c + q];
+            a.Y[i * a.ldy + c + q] = (T)y;
+        }
+    }
+}
+
+template <typename T, int G>
+__global__ __launch_bounds__(kGcnTPB) void k_gcn_prop(GcnArgs<T> a)
+{
+    const int lane = threadIdx.x & 31;
+    const int sub = lane % G;            // lane within the row group
+    const int64_t c = (int64_t)sub * kV; // first column of this lane
+    const int64_t gid = ((int64_t)blockIdx.x * kGcnTPB + threadIdx.x) / G;
+    const int64_t ngroups = (int64_t)gridDim.x * kGcnTPB / G;
+    for (int64_t i = gid; i < a.n; i += ngroups) {
+        const int64_t s = a.indptr[i], e = a.indptr[i + 1];
+        if (e - s > kGcnLong) {
+            if (sub == 0) a.L.rows[atomicAdd(a.L.count, 1)] = (int32_t)i;
+            continue;
+        }
+        double acc[kV] = {0.0, 0.0, 0.0, 0.0};
+        for (int64_t p = s; p < e; ++p) {
+            const int32_t j = a.indices[p];
+            const double w = (double)a.vals[a.perm ? a.perm[p] : p] * a.D[j];
+            double z[kV];
+            gcn_load(a.Z + (int64_t)j * a.ldz, c, a.F, z);
+#pragma unroll
+            for (int q = 0; q < kV; ++q) acc[q] = fma(w, z[q], acc[q]);
+        }
+        gcn_finish(a, i, c, acc);
+    }
+}
+
+// hubs: one warp per row, the 32 / G groups split the neighbours, shuffle-reduced
+template <typename T, int G>
+__global__ __launch_bounds__(kGcnTPB) void k_gcn_prop_long(GcnArgs<T> a)
+{
+    const int lane = threadIdx.x & 31, sub = lane % G, grp = lane / G;
+    constexpr int NG = 32 / G;
+    const int64_t c = (int64_t)sub * kV;
+    const int n = *(volatile int *)a.L.count;
+    for (int it = (blockIdx.x * kGcnTPB + threadIdx.x) / 32; it < n; it += gridDim.x * kGcnTPB / 32) {
+        const int64_t i = a.L.rows[it];
+        double acc[kV] = {0.0, 0.0, 0.0, 0.0};
+        for (int64_t p = a.indptr[i] + grp; p < a.indptr[i + 1]; p += NG) {
+            const int32_t j = a.indices[p];
+            const double w = (double)a.vals[a.perm ? a.perm[p] : p] * a.D[j];
+            double z[kV];
+            gcn_load(a.Z + (int64_t)j * a.ldz, c, a.F, z);
+#pragma unroll
+            for (int q = 0; q < kV; ++q) acc[q] = fma(w, z[q], acc[q]);
+        }
+#pragma unroll
+        for (int o = G; o < 32; o <<= 1)
+#pragma unroll
+            for (int q = 0; q < kV; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+        if (grp == 0) gcn_finish(a, i, c, acc);
+    }
+}
+
+// column sums of dY (n x F) into acc[F] (fp64 atomics; one partial per CTA and column)
+template <typename T>
+__global__ __launch_bounds__(kGcnTPB) void k_colsum(int64_t n, int64_t F, const T *__restrict__ Y, int64_t ld,
+                                                    double *__restrict__ acc)
+{
+    const int64_t rows_per = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per, r1 = r0 + rows_per < n ? r0 + rows_per : n;
+    const int64_t lanes = kGcnTPB - kGcnTPB % F;  // threads (row slot, column)
+    if (threadIdx.x >= lanes) return;
+    const int64_t f = threadIdx.x % F, rs = threadIdx.x / F, rstep = lanes / F;
+    double s = 0.0;
+    for (int64_t r = r0 + rs; r < r1; r += rstep) s += (double)Y[r * ld + f];
+    atomicAdd(&acc[f], s);
+}
+
+template <typename T>
+__global__ void k_to_dtype(int64_t m, const double *__restrict__ a, T *__restrict__ out)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) out[i] = (T)a[i];
+}
+
+// ---------------------------------------------------------------- small dense GEMMs
+// Z[n x F] = X[n x C] W (W: C x F row-major) or X W^T (W: F x C), W staged in shared memory;
+// one thread per (row, 16-column chunk), fp64 accumulation.
+constexpr int kGemmChunk = 16;
+
+template <typename T>
+__global__ __launch_bounds__(kGcnTPB) void k_rowgemm(int64_t n, int64_t C, int64_t F, const T *__restrict__ X,
+                                                     int64_t ldx, const T *__restrict__ W, int transW,
+                                                     T *__restrict__ Z, int64_t ldz)
+{
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    double *sW = reinterpret_cast<double *>(s_raw);  // C x F, [c * F + f]
+    for (int64_t q = threadIdx.x; q < C * F; q += kGcnTPB) {
+        const int64_t cc = q / F, f = q % F;
+        sW[q] = (double)(transW ? W[f * C + cc] : W[cc * F + f]);
+    }
+    __syncthreads();
+    const int64_t nch = (F + kGemmChunk - 1) / kGemmChunk;
+    const int64_t t = (int64_t)blockIdx.x * kGcnTPB + threadIdx.x;
+    const int64_t r = t / nch, ch = t % nch;
+    if (r >= n) return;
+    const int64_t f0 = ch * kGemmChunk;
+    double acc[kGemmChunk];
+#pragma unroll
+    for (int q = 0; q < kGemmChunk; ++q) acc[q] = 0.0;
+    for (int64_t cc = 0; cc < C; ++cc) {
+        const double x = (double)X[r * ldx + cc];
+        const double *w = sW + cc * F + f0;
+#pragma unroll
+        for (int q = 0; q < kGemmChunk; ++q)
+            if (f0 + q < F) acc[q] = fma(x, w[q], acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < kGemmChunk; ++q)
+        if (f0 + q < F) Z[r * ldz + f0 + q] = (T)acc[q];
+}
+
+// dW[C x F] += X^T dZ over this CTA's row slice (fp64 atomics into acc)
+template <typename T>
+__global__ __launch_bounds__(kGcnTPB) void k_gemm_tn(int64_t n, int64_t C, int64_t F, const T *__restrict__ X,
+                                                     int64_t ldx, const T *__restrict__ dZ, int64_t lddz,
+                                                     double *__restrict__ acc)
+{
+    const int64_t rows_per = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per, r1 = r0 + rows_per < n ? r0 + rows_per : n;
+    for (int64_t q = threadIdx.x; q < C * F; q += kGcnTPB) {
+        const int64_t cc = q / F, f = q % F;
+        double s = 0.0;
+        for (int64_t r = r0; r < r1; ++r) s = fma((double)X[r * ldx + cc], (double)dZ[r * lddz + f], s);
+        atomicAdd(&acc[q], s);
+    }
+}
+
+// ---------------------------------------------------------------- host side
+template <typename T, int G>
+static int launch_prop(GcnArgs<T> &a, cudaStream_t s)
+{
+    CSRK_CUDA(cudaMemsetAsync(a.L.count, 0, sizeof(int), s));
+    const int64_t groups = cdiv(a.n, 1);
+    int64_t grid = cdiv(groups * G, kGcnTPB);
+    if (grid > kNumSMs * 16) grid = kNumSMs * 16;
+    CSRK_LAUNCH((k_gcn_prop<T, G>), (unsigned)grid, kGcnTPB, 0, s, a);
+    CSRK_LAUNCH((k_gcn_prop_long<T, G>), (unsigned)(kNumSMs * 2), kGcnTPB, 0, s, a);
+    return CSRK_OK;
+}
+
+template <typename T>
+static int run_prop(GcnArgs<T> &a, cudaStream_t s)
+{
+    if (a.n == 0) return CSRK_OK;
+    const int64_t lanes = cdiv(a.F, kV);
+    if (lanes <= 1) return launch_prop<T, 1>(a, s);
+    if (lanes <= 2) return launch_prop<T, 2>(a, s);
+    if (lanes <= 4) return launch_prop<T, 4>(a, s);
+    if (lanes <= 8) return launch_prop<T, 8>(a, s);
+    if (lanes <= 16) return launch_prop<T, 16>(a, s);
+    return launch_prop<T, 32>(a, s);  // F <= 128 (checked at the ABI)
+}
+
+template <typename T>
+static int gcn_fwd_t(const csrk_pattern &A, const T *Av, int64_t F, const T *Z, int64_t ldz, const T *bias, T *Y,
+                     int64_t ldy, double *D, Bump &ws, cudaStream_t s)
+{
+    GcnArgs<T> a{};
+    carve_rowlist(A.nrows, a.L, ws);
+    if (ws.sizing()) return CSRK_OK;
+    if (A.nrows == 0) return CSRK_OK;
+    const bool f64 = sizeof(T) == 8;
+    CSRK_LAUNCH(k_gcn_deg, (unsigned)cdiv(A.nrows, 256), 256, 0, s, A.nrows, A.indptr,
+                f64 ? nullptr : (const float *)Av, f64 ? (const double *)Av : nullptr, D);
+    a.n = A.nrows; a.F = F; a.indptr = A.indptr; a.indices = A.indices; a.vals = Av; a.D = D;
+    a.Z = Z; a.ldz = ldz; a.bias = bias; a.Y = Y; a.ldy = ldy;
+    return run_prop(a, s);
+}
+
+template <typename T>
+static int gcn_bwd_t(const csrk_pattern &A, const T *Av, const csrk_pattern *AT, const int64_t *perm, int64_t F,
+                     const double *D, const T *dY, int64_t lddy, T *dZ, int64_t lddz, T *dbias, Bump &ws,
+                     cudaStream_t s)
+{
+    const int64_t n = A.nrows;
+    csrk_pattern Tt{};
+    int64_t *tp = nullptr;
+    if (AT) {
+        Tt = *AT;
+    } else {
+        int64_t *ATp = ws.take<int64_t>(n + 1);
+        int32_t *ATi = ws.take<int32_t>(A.nnz > 0 ? A.nnz : 1);
+        tp = ws.take<int64_t>(A.nnz > 0 ? A.nnz : 1);
+        Tt = csrk_pattern{n, n, A.nnz, ATp, ATi};
+    }
+    double *bacc = ws.take<double>(F > 0 ? F : 1);
+    GcnArgs<T> a{};
+    carve_rowlist(n, a.L, ws);
+    if (!AT && dZ) CSRK_TRY(transpose_impl(sizeof(T) == 8 ? CSRK_F64 : CSRK_F32, A, nullptr,
+                                           const_cast<int64_t *>(Tt.indptr), const_cast<int32_t *>(Tt.indices),
+                                           nullptr, tp, ws, s));
+    if (ws.sizing()) return CSRK_OK;
+    if (dbias) {
+        CSRK_CUDA(cudaMemsetAsync(bacc, 0, sizeof(double) * (size_t)F, s));
+        if (n > 0) CSRK_LAUNCH(k_colsum<T>, (unsigned)(kNumSMs * 4), kGcnTPB, 0, s, n, F, dY, lddy, bacc);
+        CSRK_LAUNCH(k_to_dtype<T>, (unsigned)cdiv(F, 256), 256, 0, s, F, bacc, dbias);
+    }
+    if (!dZ || n == 0) return CSRK_OK;
+    a.n = n; a.F = F; a.indptr = Tt.indptr; a.indices = Tt.indices; a.vals = Av; a.perm = AT ? perm : tp;
+    a.D = D; a.Z = dY; a.ldz = lddy; a.bias = nullptr; a.Y = dZ; a.ldy = lddz;
+    return run_prop(a, s);
+}
+
+int gcn_fwd(csrk_dtype dt, const csrk_pattern &A, const void *Av, int64_t F, const void *Z, int64_t ldz,
+            const void *bias, void *Y, int64_t ldy, double *D, Bump &ws, cudaStream_t s)
+{
+    if (dt == CSRK_F64)
+        return gcn_fwd_t<double>(A, (const double *)Av, F, (const double *)Z, ldz, (const double *)bias, (double *)Y,
+                                 ldy, D, ws, s);
+    return gcn_fwd_t<float>(A, (const float *)Av, F, (const float *)Z, ldz, (const float *)bias, (float *)Y, ldy, D,
+                            ws, s);
+}
+
+int gcn_bwd(csrk_dtype dt, const csrk_pattern &A, const void *Av, const csrk_pattern *AT, const int64_t *perm,
+            int64_t F, const double *D, const void *dY, int64_t lddy, void *dZ, int64_t lddz, void *dbias, Bump &ws,
+            cudaStream_t s)
+{
+    if (dt == CSRK_F64)
+        return gcn_bwd_t<double>(A, (const double *)Av, AT, perm, F, D, (const double *)dY, lddy, (double *)dZ, lddz,
+                                 (double *)dbias, ws, s);
+    return gcn_bwd_t<float>(A, (const float *)Av, AT, perm, F, D, (const float *)dY, lddy, (float *)dZ, lddz,
+                            (float *)dbias, ws, s);
+}
+
+template <typename T>
+static int gemm_nn_t(int64_t n, int64_t C, int64_t F, const T *X, int64_t ldx, const T *W, int transW, T *Z,
+                     int64_t ldz, cudaStream_t s)
+{
+    if (n == 0 || F == 0) return CSRK_OK;
+    const size_t smem = sizeof(double) * (size_t)(C * F);
+    if (smem > 48 * 1024) CSRK_CUDA(cudaFuncSetAttribute(k_rowgemm<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         (int)smem));
+    const int64_t threads = n * cdiv(F, kGemmChunk);
+    CSRK_LAUNCH(k_rowgemm<T>, (unsigned)cdiv(threads, kGcnTPB), kGcnTPB, smem, s, n, C, F, X, ldx, W, transW, Z, ldz);
+    return CSRK_OK;
+}
+
+int dense_gemm_nn(csrk_dtype dt, int64_t n, int64_t C, int64_t F, const void *X, int64_t ldx, const void *W,
+                  int transW, void *Z, int64_t ldz, cudaStream_t s)
+{
+    if (dt == CSRK_F64)
+        return gemm_nn_t<double>(n, C, F, (const double *)X, ldx, (const double *)W, transW, (double *)Z, ldz, s);
+    return gemm_nn_t<float>(n, C, F, (const float *)X, ldx, (const float *)W, transW, (float *)Z, ldz, s);
+}
+
+template <typename T>
+static int gemm_tn_t(int64_t n, int64_t C, int64_t F, const T *X, int64_t ldx, const T *dZ, int64_t lddz, T *dW,
+                     Bump &ws, cudaStream_t s)
+{
+    double *acc = ws.take<double>(C * F > 0 ? C * F : 1);
+    if (ws.sizing()) return CSRK_OK;
+    if (C * F == 0) return CSRK_OK;
+    CSRK_CUDA(cudaMemsetAsync(acc, 0, sizeof(double) * (size_t)(C * F), s));
+    if (n > 0) CSRK_LAUNCH(k_gemm_tn<T>, (unsigned)(kNumSMs * 4), kGcnTPB, 0, s, n, C, F, X, ldx, dZ, lddz, acc);
+    CSRK_LAUNCH(k_to_dtype<T>, (unsigned)cdiv(C * F, 256), 256, 0, s, C * F, acc, dW);
+    return CSRK_OK;
+}
+
+int dense_gemm_tn(csrk_dtype dt, int64_t n, int64_t C, int64_t F, const void *X, int64_t ldx, const void *dZ,
+                  int64_t lddz, void *dW, Bump &ws, cudaStream_t s)
+{
+    if (dt == CSRK_F64)
+        return gemm_tn_t<double>(n, C, F, (const double *)X, ldx, (const double *)dZ, lddz, (double *)dW, ws, s);
+    return gemm_tn_t<float>(n, C, F, (const float *)X, ldx, (const float *)dZ, lddz, (float *)dW, ws, s);
+}
+
+}  // namespace csrk

@@ -40,6 +40,16 @@ int sptrsv_fwd(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int uppe
 int sptrsv_bwd(csrk_dtype dt, const csrk_pattern &A, const void *A_val, const csrk_pattern *AT, const int64_t *perm,
                int upper, int unit, const void *x, const void *v, void *dA, void *db, Bump &ws, cudaStream_t s);
 
+int gcn_fwd(csrk_dtype dt, const csrk_pattern &A, const void *Av, int64_t F, const void *Z, int64_t ldz,
+            const void *bias, void *Y, int64_t ldy, double *D, Bump &ws, cudaStream_t s);
+int gcn_bwd(csrk_dtype dt, const csrk_pattern &A, const void *Av, const csrk_pattern *AT, const int64_t *perm,
+            int64_t F, const double *D, const void *dY, int64_t lddy, void *dZ, int64_t lddz, void *dbias, Bump &ws,
+            cudaStream_t s);
+int dense_gemm_nn(csrk_dtype dt, int64_t n, int64_t C, int64_t F, const void *X, int64_t ldx, const void *W,
+                  int transW, void *Z, int64_t ldz, cudaStream_t s);
+int dense_gemm_tn(csrk_dtype dt, int64_t n, int64_t C, int64_t F, const void *X, int64_t ldx, const void *dZ,
+                  int64_t lddz, void *dW, Bump &ws, cudaStream_t s);
+
 int pcg_loss_grad(const csrk_pattern &A, const double *Av, const csrk_pattern &L, const double *Lv, const double *b,
                   int N, double gamma, double *loss_host, double *resid_host, double *dL, Bump &ws, cudaStream_t s);
 

@@ -7,7 +7,8 @@ PyTorch fallback: if libcsrk.so is missing or a call fails, an exception is rais
 Names follow the ABI (and the paper's operations, Table 1):
 spmv_fwd / spmv_bwd (SpMV), spmm_fwd / spmm_bwd (SpDMM), csr_transpose,
 spgemm_symbolic / spgemm_numeric / spgemm_bwd (SpSpMM), spadd_symbolic / spadd_numeric /
-spadd_bwd (Sp + Sp), sptrsv_fwd / sptrsv_bwd (SpTRSV).
+spadd_bwd (Sp + Sp), sptrsv_fwd / sptrsv_bwd (SpTRSV), gcn_fwd / gcn_bwd / dense_gemm_nn /
+dense_gemm_tn (GCN layer, PAPER 4.4).
 """
 from __future__ import annotations
 
@@ -24,14 +25,15 @@ F32, F64 = 0, 1
 OP_N, OP_T = 0, 1
 WS = dict(spmv_fwd=0, spmv_bwd=1, spmm_fwd=2, spmm_bwd=3, csr_transpose=4, spgemm_symbolic=5,
           spgemm_numeric=6, spgemm_bwd=7, pcg=8, spadd_symbolic=9, spai=10, sptrsv_fwd=11,
-          sptrsv_bwd=12)
+          sptrsv_bwd=12, gcn_fwd=13, gcn_bwd=14, dense_gemm_tn=15)
 
 # Every symbol declared in include/csrk.h (checked by tests/test_abi_cpu.py).
 ABI_SYMBOLS = ("csrk_spmv_fwd", "csrk_spmv_bwd", "csrk_spmm_fwd", "csrk_spmm_bwd", "csrk_csr_transpose",
                "csrk_spgemm_symbolic", "csrk_spgemm_numeric", "csrk_spgemm_bwd", "csrk_workspace_size",
                "csrk_status_string", "csrk_launch_count", "csrk_version", "csrk_pcg_loss_grad",
                "csrk_spadd_symbolic", "csrk_spadd_numeric", "csrk_spadd_bwd", "csrk_spai_loss_grad",
-               "csrk_sptrsv_fwd", "csrk_sptrsv_bwd")
+               "csrk_sptrsv_fwd", "csrk_sptrsv_bwd", "csrk_gcn_fwd", "csrk_gcn_bwd", "csrk_dense_gemm_nn",
+               "csrk_dense_gemm_tn")
 
 
 class Pattern(ctypes.Structure):
@@ -75,6 +77,10 @@ def lib() -> ctypes.CDLL:
     L.csrk_spai_loss_grad.argtypes = [Pat, P, Pat, P, Pat, Pat, Pat, ctypes.POINTER(D), P, P, SZ, P]
     L.csrk_sptrsv_fwd.argtypes = [I, Pat, P, I, I, P, P, P, SZ, P]
     L.csrk_sptrsv_bwd.argtypes = [I, Pat, P, PatP, P, I, I, P, P, P, P, P, SZ, P]
+    L.csrk_gcn_fwd.argtypes = [I, Pat, P, I64, P, I64, P, P, I64, P, P, SZ, P]
+    L.csrk_gcn_bwd.argtypes = [I, Pat, P, PatP, P, I64, P, P, I64, P, I64, P, P, SZ, P]
+    L.csrk_dense_gemm_nn.argtypes = [I, I64, I64, I64, P, I64, P, I, P, I64, P]
+    L.csrk_dense_gemm_tn.argtypes = [I, I64, I64, I64, P, I64, P, I64, P, P, SZ, P]
     L.csrk_status_string.restype = ctypes.c_char_p
     L.csrk_status_string.argtypes = [I]
     L.csrk_launch_count.restype = ctypes.c_uint64
@@ -383,6 +389,70 @@ def sptrsv_bwd(T: CSR, x: torch.Tensor, v: torch.Tensor, upper: bool = False, un
                                  _ptr(v), _ptr(dT if need_dT else None), _ptr(db if need_db else None), ws, wsb,
                                  _stream()), "sptrsv_bwd")
     return (dT if need_dT else None), (db if need_db else None)
+
+
+def gcn_fwd(A: CSR, Z: torch.Tensor, bias: torch.Tensor | None = None, out: torch.Tensor | None = None,
+            D: torch.Tensor | None = None):
+    """Y = D (A (D Z) + D Z) + bias, D = (row_sum(A) + 1)^-1/2 (PAPER 4.4 Fig. 12).  Returns (Y, D)."""
+    dt = _dt(Z)
+    n, F = Z.shape
+    Y = out if out is not None else torch.empty((n, F), dtype=Z.dtype, device=Z.device)
+    D = D if D is not None else torch.empty(n, dtype=torch.float64, device=Z.device)
+    ws, wsb = _workspace("gcn_fwd", dt, A, k=F)
+    _check(lib().csrk_gcn_fwd(dt, A.pattern(), _ptr(A.values), F, _ptr(Z), Z.stride(0), _ptr(bias), _ptr(Y),
+                              Y.stride(0), _ptr(D), ws, wsb, _stream()), "gcn_fwd")
+    return Y, D
+
+
+def gcn_bwd(A: CSR, D: torch.Tensor, dY: torch.Tensor, plan: TransposePlan | None = None, need_dZ: bool = True,
+            need_dbias: bool = True, dZ: torch.Tensor | None = None, dbias: torch.Tensor | None = None):
+    """VJP of gcn_fwd (graph constant): dZ = D (A^T (D dY) + D dY), dbias = column sums of dY."""
+    dt = _dt(dY)
+    n, F = dY.shape
+    if need_dZ and dZ is None:
+        dZ = torch.empty_like(dY)
+    if need_dbias and dbias is None:
+        dbias = torch.empty(F, dtype=dY.dtype, device=dY.device)
+    pp = plan.args() if plan else (None, None, None)
+    ws, wsb = _workspace("gcn_bwd", dt, A, k=F, have_plan=plan is not None)
+    _check(lib().csrk_gcn_bwd(dt, A.pattern(), _ptr(A.values), pp[0], pp[1], F, _ptr(D), _ptr(dY), dY.stride(0),
+                              _ptr(dZ if need_dZ else None), dZ.stride(0) if need_dZ else F,
+                              _ptr(dbias if need_dbias else None), ws, wsb, _stream()), "gcn_bwd")
+    return (dZ if need_dZ else None), (dbias if need_dbias else None)
+
+
+def dense_gemm_nn(X: torch.Tensor, W: torch.Tensor, transW: bool = False, out: torch.Tensor | None = None):
+    """Z = X W (W: C x F) or X W^T (W: F x C) -- the XTheta / dX products of the GCN layer."""
+    n, C = X.shape
+    F = W.shape[0] if transW else W.shape[1]
+    Z = out if out is not None else torch.empty((n, F), dtype=X.dtype, device=X.device)
+    _check(lib().csrk_dense_gemm_nn(_dt(X), n, C, F, _ptr(X), X.stride(0), _ptr(W.contiguous()), int(transW), _ptr(Z),
+                                    Z.stride(0), _stream()), "dense_gemm_nn")
+    return Z
+
+
+def dense_gemm_tn(X: torch.Tensor, dZ: torch.Tensor, out: torch.Tensor | None = None):
+    """dW = X^T dZ (C x F) -- dTheta of the GCN layer."""
+    n, C = X.shape
+    F = dZ.shape[1]
+    dW = out if out is not None else torch.empty((C, F), dtype=X.dtype, device=X.device)
+    dims = CSR(n, C, X.new_zeros(1, dtype=torch.int64), X.new_zeros(0, dtype=torch.int32))  # sizes only
+    ws, wsb = _workspace("dense_gemm_tn", _dt(X), dims, k=F)
+    _check(lib().csrk_dense_gemm_tn(_dt(X), n, C, F, _ptr(X), X.stride(0), _ptr(dZ), dZ.stride(0), _ptr(dW), ws, wsb,
+                                    _stream()), "dense_gemm_tn")
+    return dW
+
+
+def gcn_layer_fwd(A: CSR, X: torch.Tensor, Theta: torch.Tensor, bias: torch.Tensor):
+    """The GCN layer of Fig. 12: XTheta = X Theta, then the fused propagation.  Returns (Y, D)."""
+    return gcn_fwd(A, dense_gemm_nn(X, Theta), bias)
+
+
+def gcn_layer_bwd(A: CSR, D: torch.Tensor, X: torch.Tensor, Theta: torch.Tensor, dY: torch.Tensor,
+                  plan: TransposePlan | None = None):
+    """VJP of the layer: (dX, dTheta, dbias) with dZ from gcn_bwd, dTheta = X^T dZ, dX = dZ Theta^T."""
+    dZ, dbias = gcn_bwd(A, D, dY, plan=plan)
+    return dense_gemm_nn(dZ, Theta, transW=True), dense_gemm_tn(X, dZ), dbias
 
 
 def pcg_loss_grad(A: CSR, L: CSR, b: torch.Tensor, n_it: int = 50, gamma: float = 0.6,

@@ -268,3 +268,29 @@ def tri_banded(n: int, per_row: int, band: int, seed: int, upper: bool = False, 
         vals = rng.integers(-3, 4, cols.size).astype(np.float64)
         vals[diag] = rng.choice([-4.0, -2.0, -1.0, 1.0, 2.0, 4.0], diag.sum())
     return CSR(n, n, indptr, cols.astype(np.int32), vals)
+
+
+def powerlaw_graph(n: int, mean: float = 5.0, seed: int = 4401, weighted: bool = False,
+                   dtype=np.float32) -> CSR:
+    """Synthetic graph for the GCN layer (PAPER 4.4 P:951-954: graphs of 1e5 to
+    9e5 nodes, "each node has on average 5 incident edges").  Out-degrees l_i =
+    round((mean/2) u_i^{-1/2}) (u_i = (i+1/2)/n, power law with exponent 3), adjusted by +-1 on the
+    longest / shortest rows to sum exactly to round(mean n), at least 1, seeded row permutation;
+    neighbours l_i distinct uniform draws in [0, n), sorted; edge weights 1 (or U[0.5, 2))."""
+    rng = np.random.default_rng(seed)
+    u = (np.arange(n, dtype=np.float64) + 0.5) / n
+    lengths = np.floor(0.5 * mean * u ** -0.5 + 0.5).astype(np.int64)
+    lengths = np.clip(lengths, 1, min(65536, n))
+    target = int(round(mean * n))
+    d = target - int(lengths.sum())
+    if d > 0:
+        lengths[:d] += 1
+    elif d < 0:
+        idx = np.nonzero(lengths > 1)[0][::-1][:-d]
+        lengths[idx] -= 1
+    lengths = lengths[rng.permutation(n)]
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(lengths, out=indptr[1:])
+    indices = _distinct_sorted_columns(rng, lengths, n)
+    vals = (rng.uniform(0.5, 2.0, indptr[-1]) if weighted else np.ones(indptr[-1])).astype(dtype)
+    return CSR(n, n, indptr, indices, vals)
