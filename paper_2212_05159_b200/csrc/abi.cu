@@ -313,6 +313,7 @@ int csrk_dense_gemm_tn(csrk_dtype dtype, int64_t n, int64_t C, int64_t F, const 
 {
     CSRK_TRY(check_dtype(dtype));
     if (n < 0 || C < 0 || F < 0 || ldx < C || lddz < F) return CSRK_ERR_INVALID_ARG;
+    if (C * ((F + 15) / 16) > 256 || C * F > 25600) return CSRK_ERR_INVALID_ARG;  // one row slot per CTA
     if (C * F > 0 && (!dW || (n > 0 && (!X || !dZ)))) return CSRK_ERR_INVALID_ARG;
     return with_ws(ws, ws_bytes, [&](Bump &bw) {
         return dense_gemm_tn(dtype, n, C, F, X, ldx, dZ, lddz, dW, bw, (cudaStream_t)stream);

@@ -12,7 +12,7 @@
 // gathered through perm) -- and dbias = column sums of dY.  dTheta = X^T dZ (k_gemm_tn) and
 // dX = dZ Theta^T (k_rowgemm) close the layer.  Rows of width F are handled by G = F / V lanes
 // (V = 4 values per lane, vector loads), 32 / G rows per warp; rows with more than kGcnLong
-// neighbours (power-law hubs) are queued for a warp each.  All reductions in fp64.
+// neighbours (power-law hubs) are queued for a CTA each.  All reductions in fp64.
 #include "ops.cuh"
 #include "rows.cuh"
 
@@ -22,14 +22,37 @@ constexpr int kGcnTPB = 256;
 constexpr int kGcnLong = 64;
 constexpr int kV = 4;
 
-__global__ void k_gcn_deg(int64_t n, const int64_t *__restrict__ indptr, const float *__restrict__ vf,
-                          const double *__restrict__ vd, double *__restrict__ D)
+// D_i = (row sum + 1)^-1/2: a thread per row of <= 32 entries, the warp together for longer
+// rows (power-law hubs), fixed shuffle tree
+__global__ __launch_bounds__(256) void k_gcn_deg(int64_t n, const int64_t *__restrict__ indptr,
+                                                 const float *__restrict__ vf, const double *__restrict__ vd,
+                                                 double *__restrict__ D)
 {
+    const int lane = threadIdx.x & 31;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    double s = 1.0;  // the + 1 of A~ = A + I
-    for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) s += vd ? vd[p] : (double)vf[p];
-    D[i] = 1.0 / sqrt(s);
+    const bool valid = i < n;
+    int64_t s = 0, e = 0;
+    if (valid) {
+        s = indptr[i];
+        e = indptr[i + 1];
+    }
+    const bool lng = valid && e - s > 32;
+    if (valid && !lng) {
+        double sum = 1.0;  // the + 1 of A~ = A + I
+        for (int64_t p = s; p < e; ++p) sum += vd ? vd[p] : (double)vf[p];
+        D[i] = 1.0 / sqrt(sum);
+    }
+    unsigned lm = __ballot_sync(0xffffffffu, lng);
+    while (lm) {
+        const int src = __ffs(lm) - 1;
+        lm &= lm - 1;
+        const int64_t rs = __shfl_sync(0xffffffffu, s, src), re = __shfl_sync(0xffffffffu, e, src);
+        double sum = 0.0;
+        for (int64_t p = rs + lane; p < re; p += 32) sum += vd ? vd[p] : (double)vf[p];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (lane == src) D[i] = 1.0 / sqrt(1.0 + sum);
+    }
 }
 
 template <typename T>
@@ -48,9 +71,24 @@ struct GcnArgs {
     RowList L;
 };
 
-template <typename T>
-__device__ __forceinline__ void gcn_load(const T *p, int64_t c, int64_t F, double (&v)[kV])
+__device__ __forceinline__ void gcn_load(const float *p, int64_t c, int64_t F, double (&v)[kV])
 {
+    if (c + kV <= F && ((reinterpret_cast<uintptr_t>(p + c) & 15) == 0)) {
+        const float4 f = __ldg(reinterpret_cast<const float4 *>(p + c));
+        v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+        return;
+    }
+#pragma unroll
+    for (int q = 0; q < kV; ++q) v[q] = c + q < F ? (double)p[c + q] : 0.0;
+}
+__device__ __forceinline__ void gcn_load(const double *p, int64_t c, int64_t F, double (&v)[kV])
+{
+    if (c + kV <= F && ((reinterpret_cast<uintptr_t>(p + c) & 15) == 0)) {
+        const double2 f0 = __ldg(reinterpret_cast<const double2 *>(p + c));
+        const double2 f1 = __ldg(reinterpret_cast<const double2 *>(p + c + 2));
+        v[0] = f0.x; v[1] = f0.y; v[2] = f1.x; v[3] = f1.y;
+        return;
+    }
 #pragma unroll
     for (int q = 0; q < kV; ++q) v[q] = c + q < F ? (double)p[c + q] : 0.0;
 }
@@ -87,6 +125,7 @@ __global__ __launch_bounds__(kGcnTPB) void k_gcn_prop(GcnArgs<T> a)
             continue;
         }
         double acc[kV] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
         for (int64_t p = s; p < e; ++p) {
             const int32_t j = a.indices[p];
             const double w = (double)a.vals[a.perm ? a.perm[p] : p] * a.D[j];
@@ -99,17 +138,21 @@ __global__ __launch_bounds__(kGcnTPB) void k_gcn_prop(GcnArgs<T> a)
     }
 }
 
-// hubs: one warp per row, the 32 / G groups split the neighbours, shuffle-reduced
+// hubs: one CTA per row; the kGcnTPB / G groups split the neighbours (unrolled gathers), then a
+// shuffle tree inside each warp and a fixed-order sum over the warps
 template <typename T, int G>
 __global__ __launch_bounds__(kGcnTPB) void k_gcn_prop_long(GcnArgs<T> a)
 {
-    const int lane = threadIdx.x & 31, sub = lane % G, grp = lane / G;
-    constexpr int NG = 32 / G;
+    __shared__ double s_part[kGcnTPB / 32][32 * kV];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, sub = lane % G;
+    const int grp = threadIdx.x / G;
+    constexpr int NG = kGcnTPB / G;
     const int64_t c = (int64_t)sub * kV;
     const int n = *(volatile int *)a.L.count;
-    for (int it = (blockIdx.x * kGcnTPB + threadIdx.x) / 32; it < n; it += gridDim.x * kGcnTPB / 32) {
+    for (int it = blockIdx.x; it < n; it += gridDim.x) {
         const int64_t i = a.L.rows[it];
         double acc[kV] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
         for (int64_t p = a.indptr[i] + grp; p < a.indptr[i + 1]; p += NG) {
             const int32_t j = a.indices[p];
             const double w = (double)a.vals[a.perm ? a.perm[p] : p] * a.D[j];
@@ -122,7 +165,22 @@ __global__ __launch_bounds__(kGcnTPB) void k_gcn_prop_long(GcnArgs<T> a)
         for (int o = G; o < 32; o <<= 1)
 #pragma unroll
             for (int q = 0; q < kV; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
-        if (grp == 0) gcn_finish(a, i, c, acc);
+        if (lane < G)
+#pragma unroll
+            for (int q = 0; q < kV; ++q) s_part[warp][lane * kV + q] = acc[q];
+        __syncthreads();
+        if (warp == 0) {
+            if (lane < G) {
+#pragma unroll
+                for (int q = 0; q < kV; ++q) {
+                    double t = 0.0;
+                    for (int w = 0; w < kGcnTPB / 32; ++w) t += s_part[w][lane * kV + q];
+                    acc[q] = t;
+                }
+                gcn_finish(a, i, c, acc);
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -185,20 +243,42 @@ __global__ __launch_bounds__(kGcnTPB) void k_rowgemm(int64_t n, int64_t C, int64
         if (f0 + q < F) Z[r * ldz + f0 + q] = (T)acc[q];
 }
 
-// dW[C x F] += X^T dZ over this CTA's row slice (fp64 atomics into acc)
+// dW[C x F] += X^T dZ: a thread owns (c, 16-column chunk of F) for one row slot; the CTA's row
+// slots stride its slice of rows; partials reduced in shared memory, then one fp64 atomic per
+// output and CTA.  X[r, c] and dZ[r, chunk] are shared by the threads of a row (broadcast).
 template <typename T>
 __global__ __launch_bounds__(kGcnTPB) void k_gemm_tn(int64_t n, int64_t C, int64_t F, const T *__restrict__ X,
                                                      int64_t ldx, const T *__restrict__ dZ, int64_t lddz,
                                                      double *__restrict__ acc)
 {
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    double *s_part = reinterpret_cast<double *>(s_raw);  // C x F partials of this CTA
+    const int64_t nch = (F + kGemmChunk - 1) / kGemmChunk;
+    const int64_t per_row = C * nch;                        // threads per row slot (<= kGcnTPB)
+    const int64_t slots = kGcnTPB / per_row;
+    for (int64_t q = threadIdx.x; q < C * F; q += kGcnTPB) s_part[q] = 0.0;
+    __syncthreads();
     const int64_t rows_per = (n + gridDim.x - 1) / gridDim.x;
     const int64_t r0 = (int64_t)blockIdx.x * rows_per, r1 = r0 + rows_per < n ? r0 + rows_per : n;
-    for (int64_t q = threadIdx.x; q < C * F; q += kGcnTPB) {
-        const int64_t cc = q / F, f = q % F;
-        double s = 0.0;
-        for (int64_t r = r0; r < r1; ++r) s = fma((double)X[r * ldx + cc], (double)dZ[r * lddz + f], s);
-        atomicAdd(&acc[q], s);
+    const int64_t slot = threadIdx.x / per_row, w = threadIdx.x % per_row;
+    const int64_t cc = w / nch, f0 = (w % nch) * kGemmChunk;
+    if (slot < slots) {
+        double a[kGemmChunk];
+#pragma unroll
+        for (int q = 0; q < kGemmChunk; ++q) a[q] = 0.0;
+        for (int64_t r = r0 + slot; r < r1; r += slots) {
+            const double x = (double)X[r * ldx + cc];
+            const T *z = dZ + r * lddz + f0;
+#pragma unroll
+            for (int q = 0; q < kGemmChunk; ++q)
+                if (f0 + q < F) a[q] = fma(x, (double)z[q], a[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < kGemmChunk; ++q)
+            if (f0 + q < F) atomicAdd(&s_part[cc * F + f0 + q], a[q]);
     }
+    __syncthreads();
+    for (int64_t q = threadIdx.x; q < C * F; q += kGcnTPB) atomicAdd(&acc[q], s_part[q]);
 }
 
 // ---------------------------------------------------------------- host side
@@ -210,7 +290,7 @@ static int launch_prop(GcnArgs<T> &a, cudaStream_t s)
     int64_t grid = cdiv(groups * G, kGcnTPB);
     if (grid > kNumSMs * 16) grid = kNumSMs * 16;
     CSRK_LAUNCH((k_gcn_prop<T, G>), (unsigned)grid, kGcnTPB, 0, s, a);
-    CSRK_LAUNCH((k_gcn_prop_long<T, G>), (unsigned)(kNumSMs * 2), kGcnTPB, 0, s, a);
+    CSRK_LAUNCH((k_gcn_prop_long<T, G>), (unsigned)(kNumSMs * 4), kGcnTPB, 0, s, a);
     return CSRK_OK;
 }
 
@@ -327,7 +407,10 @@ static int gemm_tn_t(int64_t n, int64_t C, int64_t F, const T *X, int64_t ldx, c
     if (ws.sizing()) return CSRK_OK;
     if (C * F == 0) return CSRK_OK;
     CSRK_CUDA(cudaMemsetAsync(acc, 0, sizeof(double) * (size_t)(C * F), s));
-    if (n > 0) CSRK_LAUNCH(k_gemm_tn<T>, (unsigned)(kNumSMs * 4), kGcnTPB, 0, s, n, C, F, X, ldx, dZ, lddz, acc);
+    const size_t smem = sizeof(double) * (size_t)(C * F);
+    if (smem > 48 * 1024) CSRK_CUDA(cudaFuncSetAttribute(k_gemm_tn<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         (int)smem));
+    if (n > 0) CSRK_LAUNCH(k_gemm_tn<T>, (unsigned)(kNumSMs * 4), kGcnTPB, smem, s, n, C, F, X, ldx, dZ, lddz, acc);
     CSRK_LAUNCH(k_to_dtype<T>, (unsigned)cdiv(C * F, 256), 256, 0, s, C * F, acc, dW);
     return CSRK_OK;
 }

@@ -37,6 +37,10 @@ constexpr int64_t kSMaxW = 512;
 constexpr int kMMaxW = 8192;
 constexpr int kSTPB = 128;           // k_gemm_S: 4 warps
 constexpr int kSWarps = kSTPB / 32;
+#ifndef CSRK_S_MINB
+#define CSRK_S_MINB 6  // measured: numeric 421 -> 355 us, bwd dA 452 -> 410 us on config 2 (1 and 4: no change)
+#endif
+constexpr int kSMinBlocks = CSRK_S_MINB;  // k_gemm_S occupancy hint (A/B via CSRK_NVCC_EXTRA)
 constexpr int kSBuf = 832;           // staged C entries per warp (3D 7-point A^2: 32 x 25 = 800)
 constexpr int kSBufA = 32 * kSMaxL;  // staged dA entries per warp
 constexpr int kGemmTPB = 512;        // k_gemm_big*
@@ -213,7 +217,7 @@ __device__ __forceinline__ int64_t s_merge(int64_t as, int l, const int32_t *__r
 }
 
 template <typename T, int PH>
-__global__ __launch_bounds__(kSTPB) void k_gemm_S(int64_t m, const int64_t *__restrict__ Ap,
+__global__ __launch_bounds__(kSTPB, kSMinBlocks) void k_gemm_S(int64_t m, const int64_t *__restrict__ Ap,
                                                   const int32_t *__restrict__ Ai, const T *__restrict__ Av,
                                                   const int64_t *__restrict__ Bp, const int32_t *__restrict__ Bi,
                                                   const T *__restrict__ Bv, int64_t *__restrict__ Cp,

@@ -5,17 +5,18 @@
 // of a lower T needs x_j for its stored j < i (upper: j > i, solved in reverse order -- the
 // paper's "matrix flip").  Two kernels, launched back to back:
 //
-//   k_trsv_chain  single-pass decoupled look-back scan for CHAIN matrices (every row's
-//                 off-diagonal entries lie on the first sub-diagonal: bidiagonal L of the
-//                 PCG preconditioner, or the triangle of A_N, Table 2).  Row i is
-//                 the affine map x_i = c_i + a_i x_{i-1} (a_i = -l_i / d_i, c_i = b_i / d_i);
-//                 maps compose associatively, so a tile of 2048 rows scans its maps in the
-//                 CTA, publishes the tile aggregate, looks back over its predecessors for the
-//                 carry-in x and then evaluates x_i = (b_i - l_i x_{i-1}) / d_i row by row from
-//                 it.  One HBM pass (pattern, values, b, x): a 16.7M-row chain that the
-//                 sync-free method would walk one dependency at a time streams like an SpMV.
-//                 A row with any other dependency aborts the pass (every tile then publishes
-//                 ABORT so no successor waits).
+//   k_trsv_chain  scan for CHAIN matrices (every row's off-diagonal entries lie on the first
+//                 sub-diagonal: bidiagonal L of the PCG preconditioner, or the triangle
+//                 of A_N, Table 2).  Row i is the affine map x_i = c_i + a_i x_{i-1}
+//                 (a_i = -l_i / d_i, c_i = b_i / d_i); maps compose associatively, so a tile of
+//                 2048 rows composes its maps (reduce), one CTA scans the tile maps into every
+//                 tile's carry-in x (k_trsv_carry), and each tile then evaluates
+//                 x_i = (b_i - l_i x_{i-1}) / d_i row by row from its thread's start value
+//                 (apply).  Two streaming passes and no waiting between CTAs: a 16.7M-row chain
+//                 that the sync-free method would walk one dependency at a time runs like two
+//                 SpMVs.  A row with any other dependency sets `abort` (apply and carry skip).
+//                 (A single-pass decoupled look-back was measured slower: 8192 tiles in flight
+//                 walk back through each other's aggregates.)
 //   k_trsv_sf     the synchronisation-free solve the paper uses (Capellini et al.):
 //                 warps take 32-row blocks in solve order from an atomic ticket; each lane
 //                 owns a row, waits (acquire) on the ready flag of every dependency outside
@@ -35,7 +36,6 @@
 
 namespace csrk {
 
-enum { CH_NONE = 0, CH_AGG = 1, CH_INCL = 2, CH_ABORT = 3 };
 constexpr int kChTPB = 256;
 constexpr int kChPer = 8;
 constexpr int kChTile = kChTPB * kChPer;
@@ -75,7 +75,6 @@ struct TrsvArgs {
     T *x;
     int upper, unit;
     // chain pass
-    int *status;
     double *aggA, *aggC, *inclX;
     int *ticket_chain;
     int *abort;
@@ -91,66 +90,84 @@ __device__ __forceinline__ double tval(const TrsvArgs<T> &a, int64_t p)
 }
 
 // ---------------------------------------------------------------- chain pass
+// Three launches, no inter-CTA waiting: (1) every tile composes the affine maps of its rows
+// (k_trsv_chain<REDUCE>) and flags a non-chain row; (2) one CTA scans the tile maps into each
+// tile's carry-in x (k_trsv_carry); (3) every tile re-reads its rows, scans its thread maps for
+// each thread's start value and runs the substitution formula (k_trsv_chain<APPLY>).
+
+// Shared-memory staging of a tile: rows [m0, m1) in memory order, their entries and b, loaded
+// with coalesced reads (a thread's own rows are consecutive, so direct loads would touch 32
+// lines per warp instruction).
+struct ChSmem {
+    int64_t ip[kChTile + 1];
+    double val[2 * kChTile];
+    double b[kChTile];
+    int32_t idx[2 * kChTile];
+};
+
+// Stage the tile and parse this thread's rows: l (neighbour value), d (diagonal), b.  Returns
+// true if a row is not a chain row (more than two entries, or a dependency other than the
+// neighbour); wrong-side entries are ignored.
 template <typename T>
-__global__ __launch_bounds__(kChTPB) void k_trsv_chain(TrsvArgs<T> a)
+__device__ __forceinline__ bool chain_rows(const TrsvArgs<T> &a, ChSmem &S, int tile, double (&lv)[kChPer],
+                                           double (&dv)[kChPer], double (&bv)[kChPer])
 {
-    __shared__ int s_tile, s_abort;
-    __shared__ double s_wA[kChTPB / 32], s_wC[kChTPB / 32];
-    __shared__ double s_xin;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const unsigned FULL = 0xffffffffu;
-    if (tid == 0) {
-        s_tile = atomicAdd(a.ticket_chain, 1);
-        s_abort = *(volatile int *)a.abort;
-    }
-    __syncthreads();
-    const int tile = s_tile;
     const int64_t n = a.n;
-    if (s_abort) {
-        if (tid == 0) st_release(&a.status[tile], CH_ABORT);
-        return;
-    }
-    // this thread's rows: solve orders o0 .. o0 + kChPer - 1
-    const int64_t o0 = (int64_t)tile * kChTile + (int64_t)tid * kChPer;
-    double lv[kChPer], dv[kChPer], bv[kChPer];
-    double mA = 1.0, mC = 0.0;  // composition of this thread's row maps
-    bool bad = false;
+    const int tid = threadIdx.x;
+    const int64_t T0 = (int64_t)tile * kChTile;
+    const int64_t m0 = a.upper ? (n - T0 - kChTile > 0 ? n - T0 - kChTile : 0) : T0;
+    const int64_t m1 = a.upper ? n - T0 : (T0 + kChTile < n ? T0 + kChTile : n);
+    const int nr = (int)(m1 - m0);
+    for (int r = tid; r <= nr; r += kChTPB) S.ip[r] = a.indptr[m0 + r];
+    for (int r = tid; r < nr; r += kChTPB) S.b[r] = (double)a.b[m0 + r];
+    __syncthreads();
+    const int64_t ent0 = S.ip[0], ne = S.ip[nr] - ent0;
+    bool bad = ne > 2 * kChTile;
+    if (!bad)
+        for (int q = tid; q < ne; q += kChTPB) {
+            S.idx[q] = a.indices[ent0 + q];
+            S.val[q] = tval(a, ent0 + q);
+        }
+    __syncthreads();
+    const int64_t o0 = T0 + (int64_t)tid * kChPer;
 #pragma unroll
     for (int r = 0; r < kChPer; ++r) {
         const int64_t o = o0 + r;
         lv[r] = 0.0;
         dv[r] = 1.0;
         bv[r] = 0.0;
-        if (o < n) {
+        if (o < n && !bad) {
             const int64_t i = a.upper ? n - 1 - o : o;
+            const int lr = (int)(i - m0);
             const int64_t prev = a.upper ? i + 1 : i - 1;
+            const int64_t rs = S.ip[lr] - ent0, re = S.ip[lr + 1] - ent0;
             double d = a.unit ? 1.0 : 0.0, l = 0.0;
-            for (int64_t p = a.indptr[i]; p < a.indptr[i + 1]; ++p) {
-                const int64_t j = a.indices[p];
+            bad |= re - rs > 2;
+            for (int64_t q = rs; q < re && q < rs + 2; ++q) {
+                const int64_t j = S.idx[q];
                 if (j == i) {
-                    if (!a.unit) d = tval(a, p);
+                    if (!a.unit) d = S.val[q];
                 } else if (j == prev) {
-                    l = tval(a, p);
+                    l = S.val[q];
                 } else if (a.upper ? j > i : j < i) {
                     bad = true;
                 }
             }
             lv[r] = l;
             dv[r] = d;
-            bv[r] = (double)a.b[i];
-            const double ar = -l / d, cr = bv[r] / d;
-            mC = ar * mC + cr;
-            mA = ar * mA;
+            bv[r] = S.b[lr];
         }
     }
-    if (__syncthreads_or(bad)) {
-        if (tid == 0) {
-            atomicExch(a.abort, 1);
-            st_release(&a.status[tile], CH_ABORT);
-        }
-        return;
-    }
-    // inclusive warp scan of the maps (later map applied after earlier: (A, C) o (Ap, Cp))
+    return bad;
+}
+
+// exclusive scan of the CTA's thread maps (composition in row order); returns the thread's
+// prefix map (tA, tC) and the tile map (gA, gC)
+__device__ __forceinline__ void chain_block_scan(double mA, double mC, double &tA, double &tC, double &gA, double &gC)
+{
+    __shared__ double s_wA[kChTPB / 32], s_wC[kChTPB / 32];
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double iA = mA, iC = mC;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -164,75 +181,128 @@ __global__ __launch_bounds__(kChTPB) void k_trsv_chain(TrsvArgs<T> a)
         s_wA[warp] = iA;
         s_wC[warp] = iC;
     }
-    // exclusive in-warp prefix
     double eA = __shfl_up_sync(FULL, iA, 1), eC = __shfl_up_sync(FULL, iC, 1);
     if (lane == 0) {
         eA = 1.0;
         eC = 0.0;
     }
     __syncthreads();
-    // prefix over earlier warps, composed in order
     double wA = 1.0, wC = 0.0;
-    for (int w = 0; w < warp; ++w) {
-        wC = s_wA[w] * wC + s_wC[w];
-        wA = s_wA[w] * wA;
-    }
-    // thread prefix = in-warp exclusive after warp prefix
-    const double tA = eA * wA, tC = eA * wC + eC;
-    if (tid == 0) {
-        // tile aggregate
-        double gA = 1.0, gC = 0.0;
-        for (int w = 0; w < kChTPB / 32; ++w) {
-            gC = s_wA[w] * gC + s_wC[w];
-            gA = s_wA[w] * gA;
+    gA = 1.0;
+    gC = 0.0;
+    for (int w = 0; w < kChTPB / 32; ++w) {
+        if (w < warp) {
+            wC = s_wA[w] * wC + s_wC[w];
+            wA = s_wA[w] * wA;
         }
-        double xin = 0.0;  // x before the first row: no carry
-        bool abort = false;
-        if (tile > 0) {
+        gC = s_wA[w] * gC + s_wC[w];
+        gA = s_wA[w] * gA;
+    }
+    tA = eA * wA;
+    tC = eA * wC + eC;
+}
+
+template <typename T, bool APPLY>
+__global__ __launch_bounds__(kChTPB, 2) void k_trsv_chain(TrsvArgs<T> a)
+{
+    if (APPLY && *(volatile int *)a.abort) return;
+    const int tid = threadIdx.x;
+    const int tile = blockIdx.x;
+    const int64_t n = a.n;
+    const int64_t o0 = (int64_t)tile * kChTile + (int64_t)tid * kChPer;
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    ChSmem &S = *reinterpret_cast<ChSmem *>(s_dyn);
+    double lv[kChPer], dv[kChPer], bv[kChPer];
+    const bool bad = chain_rows(a, S, tile, lv, dv, bv);
+    double mA = 1.0, mC = 0.0;  // composition of this thread's row maps
+#pragma unroll
+    for (int r = 0; r < kChPer; ++r) {
+        if (o0 + r < n) {
+            const double rd = 1.0 / dv[r];
+            const double ar = -lv[r] * rd, cr = bv[r] * rd;
+            mC = ar * mC + cr;
+            mA = ar * mA;
+        }
+    }
+    if (!APPLY) {
+        if (__syncthreads_or(bad)) {
+            if (tid == 0) atomicExch(a.abort, 1);
+            return;
+        }
+    }
+    double tA, tC, gA, gC;
+    chain_block_scan(mA, mC, tA, tC, gA, gC);
+    if (!APPLY) {
+        if (tid == 0) {
             a.aggA[tile] = gA;
             a.aggC[tile] = gC;
-            st_release(&a.status[tile], CH_AGG);
-            double MA = 1.0, MC = 0.0;  // maps x_in(pred) -> x_in(tile)
-            for (int p = tile - 1;; ) {
-                const int st = ld_acquire(&a.status[p]);
-                if (st == CH_NONE) continue;
-                if (st == CH_ABORT) {
-                    abort = true;
-                    break;
-                }
-                if (st == CH_INCL) {
-                    xin = MA * ld_relaxed(&a.inclX[p]) + MC;
-                    break;
-                }
-                const double pA = ld_relaxed(&a.aggA[p]), pC = ld_relaxed(&a.aggC[p]);
-                MC = MA * pC + MC;
-                MA = MA * pA;
-                --p;
-            }
         }
-        s_xin = xin;
-        s_abort = abort;
-        if (abort) st_release(&a.status[tile], CH_ABORT);
+        return;
     }
-    __syncthreads();
-    if (s_abort) return;
     // rows from the carried-in value, by the substitution formula
-    double xp = tid == 0 ? s_xin : tA * s_xin + tC;
+    const double xin = a.inclX[tile];
+    double xp = tid == 0 ? xin : tA * xin + tC;
+    const int64_t T0 = (int64_t)tile * kChTile;
+    const int64_t m0 = a.upper ? (n - T0 - kChTile > 0 ? n - T0 - kChTile : 0) : T0;
+    const int64_t m1 = a.upper ? n - T0 : (T0 + kChTile < n ? T0 + kChTile : n);
+    __syncthreads();  // S.b is rewritten with x below
 #pragma unroll
     for (int r = 0; r < kChPer; ++r) {
         const int64_t o = o0 + r;
         if (o < n) {
-            const int64_t i = a.upper ? n - 1 - o : o;
             const T xi = (T)((bv[r] - lv[r] * xp) / dv[r]);
-            a.x[i] = xi;
+            S.b[(a.upper ? n - 1 - o : o) - m0] = (double)xi;
             xp = (double)xi;
         }
     }
-    // the tile's last row publishes the inclusive prefix (its x)
-    const int64_t last = (int64_t)tile * kChTile + kChTile - 1;
-    if (o0 <= last && last < o0 + kChPer) {
-        a.inclX[tile] = xp;
-        st_release(&a.status[tile], CH_INCL);
+    __syncthreads();
+    for (int64_t r = tid; r < m1 - m0; r += kChTPB) a.x[m0 + r] = (T)S.b[r];
+}
+
+// one CTA: carry-in x of every tile, inclX[t] = (M_{t-1} o ... o M_0)(0)
+constexpr int kCarryTPB = 1024;
+template <typename T>
+__global__ __launch_bounds__(kCarryTPB) void k_trsv_carry(TrsvArgs<T> a, int64_t ntiles)
+{
+    if (*(volatile int *)a.abort) return;
+    __shared__ double s_A[kCarryTPB / 32], s_C[kCarryTPB / 32];
+    const unsigned FULL = 0xffffffffu;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t per = (ntiles + kCarryTPB - 1) / kCarryTPB;
+    const int64_t t0 = tid * per, t1 = t0 + per < ntiles ? t0 + per : ntiles;
+    double mA = 1.0, mC = 0.0;
+    for (int64_t t = t0; t < t1; ++t) {
+        mC = a.aggA[t] * mC + a.aggC[t];
+        mA = a.aggA[t] * mA;
+    }
+    double iA = mA, iC = mC;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double pA = __shfl_up_sync(FULL, iA, o), pC = __shfl_up_sync(FULL, iC, o);
+        if (lane >= o) {
+            iC = iA * pC + iC;
+            iA = iA * pA;
+        }
+    }
+    if (lane == 31) {
+        s_A[warp] = iA;
+        s_C[warp] = iC;
+    }
+    double eA = __shfl_up_sync(FULL, iA, 1), eC = __shfl_up_sync(FULL, iC, 1);
+    if (lane == 0) {
+        eA = 1.0;
+        eC = 0.0;
+    }
+    __syncthreads();
+    double wA = 1.0, wC = 0.0;
+    for (int w = 0; w < warp; ++w) {
+        wC = s_A[w] * wC + s_C[w];
+        wA = s_A[w] * wA;
+    }
+    double x = eA * wC + eC;  // prefix map applied to x = 0
+    for (int64_t t = t0; t < t1; ++t) {
+        a.inclX[t] = x;
+        x = a.aggA[t] * x + a.aggC[t];
     }
 }
 
@@ -284,7 +354,12 @@ __global__ __launch_bounds__(kSfTPB) void k_trsv_sf(TrsvArgs<T> a)
                 qe = p + 1;
                 continue;
             }
-            while (ld_acquire(&a.ready[j]) == 0) {
+            if (ld_acquire(&a.ready[j]) == 0) {
+                unsigned ns = 32;
+                while (ld_acquire(&a.ready[j]) == 0) {
+                    __nanosleep(ns);
+                    ns = ns < 256 ? ns * 2 : 256;
+                }
             }
             acc = fma(-tval(a, p), ld_relaxed(&a.x[j]), acc);
         }
@@ -294,13 +369,20 @@ __global__ __launch_bounds__(kSfTPB) void k_trsv_sf(TrsvArgs<T> a)
             // lanes depended upon are below the highest dependent lane; resolve in lane order
             const int last = 31 - __clz(im);
             int64_t q = a.upper ? qe - 1 : qs;
+            // next in-block dependency of this lane (its column) and value, kept in registers
+            const bool has = valid && qs < qe;
+            int64_t nxt = has ? a.indices[q] : -1;
+            double nv = has ? tval(a, q) : 0.0;
             for (int src = 0; src < last; ++src) {
                 if (lane == src) xi = (double)(T)(acc / d);
                 const double xs = __shfl_sync(FULL, xi, src);
                 const int64_t rs = a.upper ? n - 1 - (blo + src) : blo + src;
-                if (valid && lane > src && (a.upper ? q >= qs : q < qe) && a.indices[q] == rs) {
-                    acc = fma(-tval(a, q), xs, acc);
+                if (lane > src && nxt == rs) {
+                    acc = fma(-nv, xs, acc);
                     q += a.upper ? -1 : 1;
+                    const bool more = a.upper ? q >= qs : q < qe;
+                    nxt = more ? a.indices[q] : -1;
+                    nv = more ? tval(a, q) : 0.0;
                 }
             }
             if (lane >= last) xi = acc / d;
@@ -333,7 +415,6 @@ template <typename T>
 static int carve_solve(TrsvArgs<T> &a, int64_t n, Bump &ws)
 {
     const int64_t ntiles = cdiv(n, kChTile);
-    a.status = ws.take<int>(ntiles > 0 ? ntiles : 1);
     a.aggA = ws.take<double>(ntiles > 0 ? ntiles : 1);
     a.aggC = ws.take<double>(ntiles > 0 ? ntiles : 1);
     a.inclX = ws.take<double>(ntiles > 0 ? ntiles : 1);
@@ -351,10 +432,14 @@ static int launch_solve(TrsvArgs<T> &a, cudaStream_t s)
     const int64_t n = a.n;
     if (n == 0) return CSRK_OK;
     const int64_t ntiles = cdiv(n, kChTile);
-    CSRK_CUDA(cudaMemsetAsync(a.status, 0, sizeof(int) * (size_t)ntiles, s));
     CSRK_CUDA(cudaMemsetAsync(a.ticket_chain, 0, 4 * sizeof(int), s));
     if (ntiles > INT32_MAX) return CSRK_ERR_INDEX_OVERFLOW;
-    CSRK_LAUNCH(k_trsv_chain<T>, (unsigned)ntiles, kChTPB, 0, s, a);
+    const int sm = (int)sizeof(ChSmem);
+    CSRK_CUDA(cudaFuncSetAttribute(k_trsv_chain<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    CSRK_CUDA(cudaFuncSetAttribute(k_trsv_chain<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    CSRK_LAUNCH((k_trsv_chain<T, false>), (unsigned)ntiles, kChTPB, sm, s, a);
+    CSRK_LAUNCH(k_trsv_carry<T>, 1, kCarryTPB, 0, s, a, ntiles);
+    CSRK_LAUNCH((k_trsv_chain<T, true>), (unsigned)ntiles, kChTPB, sm, s, a);
     CSRK_LAUNCH(k_trsv_prep<T>, (unsigned)(kNumSMs * 4), 256, 0, s, a);
     const int64_t nwarps = cdiv(n, 32);
     const int64_t grid = cdiv(nwarps, kSfTPB / 32) < kNumSMs * 8 ? cdiv(nwarps, kSfTPB / 32) : kNumSMs * 8;

@@ -11,6 +11,7 @@
 //      AT_indices (row) and AT_perm (p) -- canonical CSR, bit-identical to the stable
 //      counting sort of the oracle regardless of the atomic order.
 //   5. AT_val[q] = A_val[perm[q]] (optional)
+// Matrices with scattered columns use the stable radix sort of radix.cu instead (use_radix).
 // Packing needs nnz < 2^33 (checked).
 #include "ops.cuh"
 #include "rows.cuh"
@@ -286,11 +287,35 @@ static unsigned grid_for(int64_t work, int tpb)
     return (unsigned)(g < 1 ? 1 : (g > cap ? cap : g));
 }
 
+int transpose_radix(const csrk_pattern &A, int64_t *ATp, int32_t *ATi, int64_t *perm, Bump &ws, cudaStream_t s);
+
+// Scattered columns (many columns, many entries each: config 4) take the radix sort of radix.cu;
+// banded / stencil matrices keep the atomic-cursor scatter + per-column sort (measured faster
+// there).  CSRK_TRANSPOSE_RADIX=0/1 forces either.
+static bool use_radix(const csrk_pattern &A)
+{
+    static int k = knob("TRANSPOSE_RADIX", -1);
+    if (k >= 0) return k != 0;
+    return A.ncols >= (int64_t(1) << 22) && A.nnz >= 8 * A.ncols;
+}
+
 int transpose_impl(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int64_t *ATp, int32_t *ATi,
                    void *AT_val, int64_t *perm, Bump &ws, cudaStream_t s)
 {
     const int64_t n = A.ncols, nnz = A.nnz;
     if (nnz >= (int64_t(1) << 33)) return CSRK_ERR_INDEX_OVERFLOW;
+    if (use_radix(A)) {
+        int64_t *pm = perm ? perm : ws.take<int64_t>(nnz > 0 ? nnz : 1);
+        CSRK_TRY(transpose_radix(A, ATp, ATi, pm, ws, s));
+        if (ws.sizing() || !AT_val || nnz == 0) return CSRK_OK;
+        if (dt == CSRK_F64)
+            CSRK_LAUNCH(k_gather_vals<double>, grid_for(nnz, 256), 256, 0, s, nnz, (const int64_t *)pm,
+                        (const double *)A_val, (double *)AT_val);
+        else
+            CSRK_LAUNCH(k_gather_vals<float>, grid_for(nnz, 256), 256, 0, s, nnz, (const int64_t *)pm,
+                        (const float *)A_val, (float *)AT_val);
+        return CSRK_OK;
+    }
     int64_t *cursor = ws.take<int64_t>(n > 0 ? n : 1);
     uint64_t *keys = ws.take<uint64_t>(nnz > 0 ? nnz : 1);
     int64_t *pm = perm ? perm : ws.take<int64_t>(nnz > 0 ? nnz : 1);
