@@ -8,6 +8,10 @@ BASELINE.json config 2: the 2D Poisson 5-point matrix on a 2048 x 2048 grid (4,1
     a8+a9 spgemm_symbolic (C = A A, one host sync)    a10 spgemm_numeric  a11+a12 spgemm_bwd
     a13 (N > 1) row-block partition + halo reduction of the dx / dX / dB partials over NCCL
 
+Per-op times for the ops report and the roofline come from a second pass with events around
+every op (the timed steps carry no per-op events).  Running the SpGEMM half on a second stream
+was measured: no gain (3.45 vs 3.37 ms), the SpMM grids occupy every SM.
+
 Metric (BASELINE.json): algorithmic GB/s of the step (SURVEY.md 8(d) d.4 bytes; one read of
 every operand, one write of every result) -- plus GFLOP/s and the roofline fraction of the
 dominant kernel against the measured HBM copy bandwidth (MEASURED_PEAKS.json).
@@ -603,6 +607,7 @@ def main():
         dist.setup(W)
     l2_flush = torch.empty(512 << 20, dtype=torch.uint8, device=W.dev)  # > 126 MB L2
 
+    stepper = W.step
     for _ in range(args.warmup):
         W.step()
     torch.cuda.synchronize()
@@ -618,13 +623,19 @@ def main():
     launches0 = ck.launch_count()
     st = torch.cuda.current_stream()
     with Clocks(local) as clk:
+        # the timed steps (headline): the whole pass, L2 flushed before each
         for i in range(args.steps):
             flush_l2(torch, l2_flush)
             step_ev[i][0].record(st)
-            W.step(evs[i])
+            stepper()
             step_ev[i][1].record(st)
         torch.cuda.synchronize()
     launches = ck.launch_count() - launches0
+    # per-op times (ops report, roofline): the same pass serialised, each op bracketed by events
+    for i in range(args.steps):
+        flush_l2(torch, l2_flush)
+        W.step(evs[i])
+    torch.cuda.synchronize()
     if world > 1:
         tdist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in step_ev]

@@ -50,7 +50,7 @@ __device__ __forceinline__ void row_elem(const TileArgs<T> &a, int64_t row, int6
 }
 
 template <typename T, int MODE, bool PERM, bool SIDE>
-__global__ __launch_bounds__(kRowsTPB) void k_rows(TileArgs<T> a, RowList L)
+__global__ __launch_bounds__(kRowsTPB, 8) void k_rows(TileArgs<T> a, RowList L)
 {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;

@@ -166,10 +166,13 @@ def _workspace(op: str, dtype: int, A: CSR, B: CSR | None = None, k: int = 0, ha
     if nbytes == 0:
         return None, 0
     dev = A.indptr.device
-    buf = _ws_cache.get(dev)
+    # one cached scratch buffer per (device, stream): ops enqueued on different streams may
+    # run concurrently and must not share scratch
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream)
+    buf = _ws_cache.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
-        _ws_cache[dev] = buf
+        _ws_cache[key] = buf
     return _ptr(buf), buf.numel()
 
 
