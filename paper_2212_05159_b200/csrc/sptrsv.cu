@@ -365,7 +365,25 @@ __global__ __launch_bounds__(kSfTPB) void k_trsv_sf(TrsvArgs<T> a)
         }
         const unsigned im = __ballot_sync(FULL, valid && qs < qe);
         double xi = 0.0;
-        if (im) {
+        // in-block dependencies that form a chain (each lane depends at most on lane - 1, e.g. the
+        // left neighbour of a stencil triangle in natural ordering): the recurrence
+        // x_l = c_l + a_l x_{l-1} is resolved by a warp scan of affine maps instead of 32 steps
+        const int64_t prevrow = a.upper ? i + 1 : i - 1;
+        const bool chainlane = !(valid && qs < qe) || (qe - qs == 1 && lane > 0 && a.indices[qs] == prevrow);
+        if (im && __all_sync(FULL, chainlane)) {
+            const double rd = 1.0 / d;
+            double mA = (valid && qs < qe) ? -tval(a, qs) * rd : 0.0;
+            double mC = acc * rd;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double pA = __shfl_up_sync(FULL, mA, o), pC = __shfl_up_sync(FULL, mC, o);
+                if (lane >= o) {
+                    mC = mA * pC + mC;
+                    mA = mA * pA;
+                }
+            }
+            xi = mC;  // lane 0 has no in-block dependency, so the composed map's offset is x
+        } else if (im) {
             // lanes depended upon are below the highest dependent lane; resolve in lane order
             const int last = 31 - __clz(im);
             int64_t q = a.upper ? qe - 1 : qs;
