@@ -11,7 +11,7 @@
 // same kernel over the rows of A^T (cached plan, or a transpose built in the workspace; values
 // gathered through perm) -- and dbias = column sums of dY.  dTheta = X^T dZ (k_gemm_tn) and
 // dX = dZ Theta^T (k_rowgemm) close the layer.  Rows of width F are handled by G = F / V lanes
-// (V = 4 values per lane, vector loads), 32 / G rows per warp; rows with more than kGcnLong
+// (V = 4 values per lane), 32 / G rows per warp; rows with more than kGcnLong
 // neighbours (power-law hubs) are queued for a CTA each.  All reductions in fp64.
 #include "ops.cuh"
 #include "rows.cuh"
@@ -71,58 +71,11 @@ struct GcnArgs {
     RowList L;
 };
 
-__device__ __forceinline__ void gcn_load(const float *p, int64_t c, int64_t F, double (&v)[kV])
-{
-    if (c + kV <= F && ((reinterpret_cast<uintptr_t>(p + c) & 15) == 0)) {
-        const float4 f = __ldg(reinterpret_cast<const float4 *>(p + c));
-        v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-        return;
-    }
-#pragma unroll
-    for (int q = 0; q < kV; ++q) v[q] = c + q < F ? (double)p[c + q] : 0.0;
-}
-__device__ __forceinline__ void gcn_load(const double *p, int64_t c, int64_t F, double (&v)[kV])
-{
-    if (c + kV <= F && ((reinterpret_cast<uintptr_t>(p + c) & 15) == 0)) {
-        const double2 f0 = __ldg(reinterpret_cast<const double2 *>(p + c));
-        const double2 f1 = __ldg(reinterpret_cast<const double2 *>(p + c + 2));
-        v[0] = f0.x; v[1] = f0.y; v[2] = f1.x; v[3] = f1.y;
-        return;
-    }
-#pragma unroll
-    for (int q = 0; q < kV; ++q) v[q] = c + q < F ? (double)p[c + q] : 0.0;
-}
-
-// acc += sum over entries p = s, s + st, ... < e of a_p D_j Z_j[c .. c + 3]: four neighbours at a
-// time, every index / weight load of a batch issued before the row gathers that depend on them
 template <typename T>
-__device__ __forceinline__ void gcn_accumulate(const GcnArgs<T> &a, int64_t s, int64_t e, int st, int64_t c,
-                                               double (&acc)[kV])
+__device__ __forceinline__ void gcn_load(const T *p, int64_t c, int64_t F, double (&v)[kV])
 {
-    for (int64_t p0 = s; p0 < e; p0 += 4 * (int64_t)st) {
-        int32_t j[4];
-        double w[4];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int64_t p = p0 + (int64_t)b * st;
-            j[b] = p < e ? a.indices[p] : -1;
-            w[b] = p < e ? (double)a.vals[a.perm ? a.perm[p] : p] : 0.0;
-        }
-#pragma unroll
-        for (int b = 0; b < 4; ++b) w[b] *= j[b] >= 0 ? a.D[j[b]] : 0.0;
-        double z[4][kV];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            if (j[b] >= 0) gcn_load(a.Z + (int64_t)j[b] * a.ldz, c, a.F, z[b]);
-            else
-#pragma unroll
-                for (int q = 0; q < kV; ++q) z[b][q] = 0.0;
-        }
-#pragma unroll
-        for (int b = 0; b < 4; ++b)
-#pragma unroll
-            for (int q = 0; q < kV; ++q) acc[q] = fma(w[b], z[b][q], acc[q]);
-    }
+    for (int q = 0; q < kV; ++q) v[q] = c + q < F ? (double)p[c + q] : 0.0;
 }
 
 // out row i = D_i (sum_p a_p D_j Z_j + D_i Z_i) + bias, lanes [g*G, g*G + G) of a warp own row i
@@ -157,7 +110,15 @@ __global__ __launch_bounds__(kGcnTPB) void k_gcn_prop(GcnArgs<T> a)
             continue;
         }
         double acc[kV] = {0.0, 0.0, 0.0, 0.0};
-        gcn_accumulate(a, s, e, 1, c, acc);
+#pragma unroll 4
+        for (int64_t p = s; p < e; ++p) {
+            const int32_t j = a.indices[p];
+            const double w = (double)a.vals[a.perm ? a.perm[p] : p] * a.D[j];
+            double z[kV];
+            gcn_load(a.Z + (int64_t)j * a.ldz, c, a.F, z);
+#pragma unroll
+            for (int q = 0; q < kV; ++q) acc[q] = fma(w, z[q], acc[q]);
+        }
         gcn_finish(a, i, c, acc);
     }
 }
@@ -176,7 +137,15 @@ __global__ __launch_bounds__(kGcnTPB) void k_gcn_prop_long(GcnArgs<T> a)
     for (int it = blockIdx.x; it < n; it += gridDim.x) {
         const int64_t i = a.L.rows[it];
         double acc[kV] = {0.0, 0.0, 0.0, 0.0};
-        gcn_accumulate(a, a.indptr[i] + grp, a.indptr[i + 1], NG, c, acc);
+#pragma unroll 4
+        for (int64_t p = a.indptr[i] + grp; p < a.indptr[i + 1]; p += NG) {
+            const int32_t j = a.indices[p];
+            const double w = (double)a.vals[a.perm ? a.perm[p] : p] * a.D[j];
+            double z[kV];
+            gcn_load(a.Z + (int64_t)j * a.ldz, c, a.F, z);
+#pragma unroll
+            for (int q = 0; q < kV; ++q) acc[q] = fma(w, z[q], acc[q]);
+        }
 #pragma unroll
         for (int o = G; o < 32; o <<= 1)
 #pragma unroll
@@ -231,8 +200,7 @@ __global__ void k_to_dtype(int64_t m, const double *__restrict__ a, T *__restric
 
 // ---------------------------------------------------------------- small dense GEMMs
 // Z[n x F] = X[n x C] W (W: C x F row-major) or X W^T (W: F x C), W staged in shared memory;
-// one thread per output (row, f): a warp's stores are contiguous, X[r, c] is one broadcast load
-// per row of the warp; fp64 accumulation.
+// one thread per (row, 16-column chunk), fp64 accumulation.
 constexpr int kGemmChunk = 16;
 
 template <typename T>
@@ -247,18 +215,24 @@ __global__ __launch_bounds__(kGcnTPB) void k_rowgemm(int64_t n, int64_t C, int64
         sW[q] = (double)(transW ? W[f * C + cc] : W[cc * F + f]);
     }
     __syncthreads();
+    const int64_t nch = (F + kGemmChunk - 1) / kGemmChunk;
     const int64_t t = (int64_t)blockIdx.x * kGcnTPB + threadIdx.x;
-    const int64_t r = t / F, f = t % F;
+    const int64_t r = t / nch, ch = t % nch;
     if (r >= n) return;
-    const T *x = X + r * ldx;
-    double a0 = 0.0, a1 = 0.0;
-    int64_t cc = 0;
-    for (; cc + 1 < C; cc += 2) {
-        a0 = fma((double)x[cc], sW[cc * F + f], a0);
-        a1 = fma((double)x[cc + 1], sW[(cc + 1) * F + f], a1);
+    const int64_t f0 = ch * kGemmChunk;
+    double acc[kGemmChunk];
+#pragma unroll
+    for (int q = 0; q < kGemmChunk; ++q) acc[q] = 0.0;
+    for (int64_t cc = 0; cc < C; ++cc) {
+        const double x = (double)X[r * ldx + cc];
+        const double *w = sW + cc * F + f0;
+#pragma unroll
+        for (int q = 0; q < kGemmChunk; ++q)
+            if (f0 + q < F) acc[q] = fma(x, w[q], acc[q]);
     }
-    if (cc < C) a0 = fma((double)x[cc], sW[cc * F + f], a0);
-    Z[r * ldz + f] = (T)(a0 + a1);
+#pragma unroll
+    for (int q = 0; q < kGemmChunk; ++q)
+        if (f0 + q < F) Z[r * ldz + f0 + q] = (T)acc[q];
 }
 
 // dW[C x F] += X^T dZ: a thread owns (c, 16-column chunk of F) for one row slot; the CTA's row
@@ -284,20 +258,7 @@ __global__ __launch_bounds__(kGcnTPB) void k_gemm_tn(int64_t n, int64_t C, int64
         double a[kGemmChunk];
 #pragma unroll
         for (int q = 0; q < kGemmChunk; ++q) a[q] = 0.0;
-        int64_t r = r0 + slot;
-        for (; r + slots < r1; r += 2 * slots) {  // two rows per step: independent loads in flight
-            const double x0 = (double)X[r * ldx + cc], x1 = (double)X[(r + slots) * ldx + cc];
-            const T *z0 = dZ + r * lddz + f0, *z1 = dZ + (r + slots) * lddz + f0;
-            double v0[kGemmChunk], v1[kGemmChunk];
-#pragma unroll
-            for (int q = 0; q < kGemmChunk; ++q) {
-                v0[q] = f0 + q < F ? (double)z0[q] : 0.0;
-                v1[q] = f0 + q < F ? (double)z1[q] : 0.0;
-            }
-#pragma unroll
-            for (int q = 0; q < kGemmChunk; ++q) a[q] = fma(x1, v1[q], fma(x0, v0[q], a[q]));
-        }
-        for (; r < r1; r += slots) {
+        for (int64_t r = r0 + slot; r < r1; r += slots) {
             const double x = (double)X[r * ldx + cc];
             const T *z = dZ + r * lddz + f0;
 #pragma unroll
@@ -417,7 +378,7 @@ static int gemm_nn_t(int64_t n, int64_t C, int64_t F, const T *X, int64_t ldx, c
     const size_t smem = sizeof(double) * (size_t)(C * F);
     if (smem > 48 * 1024) CSRK_CUDA(cudaFuncSetAttribute(k_rowgemm<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                          (int)smem));
-    const int64_t threads = n * F;
+    const int64_t threads = n * cdiv(F, kGemmChunk);
     CSRK_LAUNCH(k_rowgemm<T>, (unsigned)cdiv(threads, kGcnTPB), kGcnTPB, smem, s, n, C, F, X, ldx, W, transW, Z, ldz);
     return CSRK_OK;
 }
