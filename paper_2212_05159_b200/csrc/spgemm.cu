@@ -332,14 +332,19 @@ __device__ __forceinline__ int64_t lbound(const int32_t *c, int64_t n, int32_t v
 }
 
 // ---------------------------------------------------------------- medium rows: warp per row
-struct WSmem {
-    double val[kWW];     // NUM: row accumulator; BWD: dC row; COUNT: hash table (2 kWW int32)
-    double dA[kWL];      // BWD: dA of the row's A entries
-    double av[kWL];      // NUM / BWD: A values of the row
-    int64_t bs[kWL];     // start in B of list t
-    int32_t key[kWW];    // FILL: product columns (sorted); NUM / BWD: C row columns
-    int32_t off[kWL + 1];// flat offset of list t (off[l] = w)
+template <int WW, int WL, bool VAL>
+struct WSmemT {
+    double val[WW];                 // NUM: row accumulator; BWD: dC row; COUNT: hash table (2 WW int32)
+    double dA[VAL ? WL : 1];        // BWD: dA of the row's A entries
+    double av[VAL ? WL : 1];        // NUM / BWD: A values of the row
+    int64_t bs[WL];                 // start in B of list t
+    int32_t key[WW];                // FILL: product columns (sorted); NUM / BWD: C row columns
+    int32_t off[WL + 1];            // flat offset of list t (off[l] = w)
 };
+using WSmem = WSmemT<kWW, kWL, true>;
+// symbolic-only warp class for 512 < w <= kW2W (config-4 rows the CTA path sorted slowly)
+constexpr int kW2W = 1024;
+using WSmem2 = WSmemT<kW2W, kWL, false>;
 
 // last t in [0, l) with off[t] <= e (the list holding flat product e; empty lists skipped)
 __device__ __forceinline__ int w_list_of(const int32_t *off, int l, int e)
@@ -414,8 +419,8 @@ __device__ __forceinline__ void w_sort_fill(const int32_t *key, int w, int32_t *
     }
 }
 
-template <typename T, int PH>
-__global__ __launch_bounds__(kWTPB) void k_gemm_W(BigList wl, BigList big, const int64_t *__restrict__ Ap,
+template <typename T, int PH, bool W2 = false>
+__global__ __launch_bounds__(kWTPB) void k_gemm_W(BigList wl, BigList big, BigList w2l, const int64_t *__restrict__ Ap,
                                                   const int32_t *__restrict__ Ai, const T *__restrict__ Av,
                                                   const int64_t *__restrict__ Bp, const int32_t *__restrict__ Bi,
                                                   const T *__restrict__ Bv, int64_t *__restrict__ Cp,
@@ -424,7 +429,9 @@ __global__ __launch_bounds__(kWTPB) void k_gemm_W(BigList wl, BigList big, const
 {
     extern __shared__ __align__(16) unsigned char s_dyn[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    WSmem &S = reinterpret_cast<WSmem *>(s_dyn)[warp];
+    constexpr int WW = W2 ? kW2W : kWW;
+    using SM = WSmemT<WW, kWL, !W2>;
+    SM &S = reinterpret_cast<SM *>(s_dyn)[warp];
     const unsigned FULL = 0xffffffffu;
     const int nrows = *(volatile int *)wl.count;
     for (int it = blockIdx.x * kWWarps + warp; it < nrows; it += gridDim.x * kWWarps) {
@@ -449,14 +456,19 @@ __global__ __launch_bounds__(kWTPB) void k_gemm_W(BigList wl, BigList big, const
             }
             const int64_t excl = run + x - len;
             if (t < l) {
-                S.off[t] = excl > kWW ? kWW + 1 : (int32_t)excl;
+                S.off[t] = excl > WW ? WW + 1 : (int32_t)excl;
                 S.bs[t] = bs;
                 if (PH == PH_NUM || PH == PH_BWD) S.av[t] = (double)Av[as + t];
             }
             run += __shfl_sync(FULL, x, 31);
         }
-        if (run > kWW) {  // too many products for the warp: the CTA path takes the row
-            if (lane == 0) big.rows[atomicAdd(big.count, 1)] = (int32_t)i;
+        if (run > WW) {  // too many products for the warp: the symbolic W2 class or the CTA path
+            if (lane == 0) {
+                if (!W2 && (PH == PH_COUNT || PH == PH_FILL) && w2l.rows && run <= kW2W)
+                    w2l.rows[atomicAdd(w2l.count, 1)] = (int32_t)i;
+                else
+                    big.rows[atomicAdd(big.count, 1)] = (int32_t)i;
+            }
             continue;
         }
         const int w = (int)run;
@@ -543,13 +555,17 @@ __global__ __launch_bounds__(kWTPB) void k_gemm_W(BigList wl, BigList big, const
         }
         if (PH == PH_FILL) {
             __syncwarp();
-            const int P = w <= 32 ? 32 : w <= 64 ? 64 : w <= 128 ? 128 : w <= 256 ? 256 : 512;
-            switch (P) {
-            case 32: w_sort_fill<1>(S.key, w, Ci + cs, lane); break;
-            case 64: w_sort_fill<2>(S.key, w, Ci + cs, lane); break;
-            case 128: w_sort_fill<4>(S.key, w, Ci + cs, lane); break;
-            case 256: w_sort_fill<8>(S.key, w, Ci + cs, lane); break;
-            default: w_sort_fill<16>(S.key, w, Ci + cs, lane); break;
+            if (!W2) {
+                const int P = w <= 32 ? 32 : w <= 64 ? 64 : w <= 128 ? 128 : w <= 256 ? 256 : 512;
+                switch (P) {
+                case 32: w_sort_fill<1>(S.key, w, Ci + cs, lane); break;
+                case 64: w_sort_fill<2>(S.key, w, Ci + cs, lane); break;
+                case 128: w_sort_fill<4>(S.key, w, Ci + cs, lane); break;
+                case 256: w_sort_fill<8>(S.key, w, Ci + cs, lane); break;
+                default: w_sort_fill<16>(S.key, w, Ci + cs, lane); break;
+                }
+            } else {
+                w_sort_fill<32>(S.key, w, Ci + cs, lane);  // 512 < w <= kW2W = 1024
             }
         }
         __syncwarp();
@@ -924,6 +940,8 @@ static size_t big_sort_smem() { return sizeof(int32_t) * kMMaxW; }
 static unsigned sort_grid() { return (unsigned)(kNumSMs * 4); }
 static unsigned val_grid() { return (unsigned)(kNumSMs * 4); }
 static size_t w_smem() { return sizeof(WSmem) * kWWarps; }
+static size_t w2_smem() { return sizeof(WSmem2) * kWWarps; }
+static unsigned w2_grid() { return (unsigned)(kNumSMs * 4); }
 static unsigned w_grid() { return (unsigned)(kNumSMs * 7); }
 
 static int set_smem_attrs()
@@ -935,6 +953,9 @@ static int set_smem_attrs()
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_sym<PH_FILL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bs));
     const int ww = (int)w_smem();
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, ww));
+    const int w2s = (int)w2_smem();
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_COUNT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, w2s));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_FILL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, w2s));
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_FILL>, cudaFuncAttributeMaxDynamicSharedMemorySize, ww));
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_NUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, ww));
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, ww));
@@ -961,14 +982,20 @@ static int stage_fill() { static int v = knob("GEMM_STAGE_FILL", 1); return v; }
 static int stage_vals() { static int v = knob("GEMM_STAGE_VALS", 0); return v; }
 
 // both queue counters live in one 8-byte word so one memset clears them
-static void carve_lists(const csrk_pattern &A, BigList &wl, BigList &big, BigRows &br, Bump &ws)
+static void carve_lists(const csrk_pattern &A, BigList &wl, BigList &big, BigRows &br, Bump &ws,
+                        BigList *w2 = nullptr)
 {
     const int64_t m = A.nrows > 0 ? A.nrows : 1;
     wl.rows = ws.take<int32_t>(m);
     big.rows = ws.take<int32_t>(m);
-    int *cnt = ws.take<int>(2);
+    int32_t *w2rows = ws.take<int32_t>(m);
+    int *cnt = ws.take<int>(4);
     wl.count = cnt;
     big.count = cnt ? cnt + 1 : nullptr;
+    if (w2) {
+        w2->rows = w2rows;
+        w2->count = cnt ? cnt + 2 : nullptr;
+    }
     br.rows = big.rows;
     br.count = big.count;
     br.loff = ws.take<int64_t>(A.nnz > 0 ? A.nnz : 1);
@@ -979,9 +1006,9 @@ static void carve_lists(const csrk_pattern &A, BigList &wl, BigList &big, BigRow
 int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, int32_t *Ci, int64_t *nnzC_host,
                     Bump &ws, cudaStream_t s)
 {
-    BigList wl{}, b{};
+    BigList wl{}, b{}, w2{};
     BigRows br{};
-    carve_lists(A, wl, b, br, ws);
+    carve_lists(A, wl, b, br, ws, &w2);
     if (ws.sizing()) return scan_counts_i64(nullptr, A.nrows, ws, s);
     const int64_t m = A.nrows;
     CSRK_TRY(set_smem_attrs());
@@ -992,11 +1019,13 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, i
     if (!Ci) {
         CSRK_CUDA(cudaMemsetAsync(Cp, 0, sizeof(int64_t), s));
         if (m > 0) {
-            CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 2 * sizeof(int), s));
+            CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 4 * sizeof(int), s));
             CSRK_LAUNCH((k_gemm_S<double, PH_COUNT>), gS, kSTPB, 0, s, m, A.indptr, A.indices, dn, B.indptr, Bi, dn,
                         Cp, (int32_t *)nullptr, dw, dn, dw, dw, wl, b, 0);
-            CSRK_LAUNCH((k_gemm_W<double, PH_COUNT>), w_grid(), kWTPB, w_smem(), s, wl, b, A.indptr, A.indices, dn,
-                        B.indptr, Bi, dn, Cp, (int32_t *)nullptr, dw, dn, dw, dw);
+            CSRK_LAUNCH((k_gemm_W<double, PH_COUNT>), w_grid(), kWTPB, w_smem(), s, wl, b, w2, A.indptr, A.indices,
+                        dn, B.indptr, Bi, dn, Cp, (int32_t *)nullptr, dw, dn, dw, dw);
+            CSRK_LAUNCH((k_gemm_W<double, PH_COUNT, true>), w2_grid(), kWTPB, w2_smem(), s, w2, b, BigList{},
+                        A.indptr, A.indices, dn, B.indptr, Bi, dn, Cp, (int32_t *)nullptr, dw, dn, dw, dw);
             CSRK_LAUNCH(k_big_prep, big_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, B.indptr);
             CSRK_LAUNCH((k_gemm_big_sym<PH_COUNT, false>), sort_grid(), kGemmTPB, big_sort_smem(), s, br, B.ncols,
                         A.indptr, A.indices, B.indptr, Bi, Cp, (int32_t *)nullptr);
@@ -1009,11 +1038,13 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, i
         return CSRK_OK;
     }
     if (m == 0) return CSRK_OK;
-    CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 2 * sizeof(int), s));
+    CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 4 * sizeof(int), s));
     CSRK_LAUNCH((k_gemm_S<double, PH_FILL>), gS, kSTPB, s_smem<double>(PH_FILL, stage_fill()), s, m, A.indptr,
                 A.indices, dn, B.indptr, Bi, dn, Cp, Ci, dw, dn, dw, dw, wl, b, stage_fill());
-    CSRK_LAUNCH((k_gemm_W<double, PH_FILL>), w_grid(), kWTPB, w_smem(), s, wl, b, A.indptr, A.indices, dn, B.indptr,
-                Bi, dn, Cp, Ci, dw, dn, dw, dw);
+    CSRK_LAUNCH((k_gemm_W<double, PH_FILL>), w_grid(), kWTPB, w_smem(), s, wl, b, w2, A.indptr, A.indices, dn,
+                B.indptr, Bi, dn, Cp, Ci, dw, dn, dw, dw);
+    CSRK_LAUNCH((k_gemm_W<double, PH_FILL, true>), w2_grid(), kWTPB, w2_smem(), s, w2, b, BigList{}, A.indptr,
+                A.indices, dn, B.indptr, Bi, dn, Cp, Ci, dw, dn, dw, dw);
     CSRK_LAUNCH(k_big_prep, big_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, B.indptr);
     CSRK_LAUNCH((k_gemm_big_sym<PH_FILL, false>), sort_grid(), kGemmTPB, big_sort_smem(), s, br, B.ncols, A.indptr,
                 A.indices, B.indptr, Bi, Cp, Ci);
@@ -1034,7 +1065,7 @@ static int spgemm_values_t(int PH, const csrk_pattern &A, const T *Av, const csr
     if (PH == PH_BWD && dB) CSRK_CUDA(cudaMemsetAsync(dB, 0, sizeof(T) * (size_t)B.nnz, s));
     const int64_t m = A.nrows;
     if (m == 0) return CSRK_OK;
-    CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 2 * sizeof(int), s));
+    CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 4 * sizeof(int), s));
     const unsigned gS = (unsigned)cdiv(m, kSTPB);
     int64_t *Cp = const_cast<int64_t *>(C.indptr);
     T *tn = nullptr;
@@ -1042,7 +1073,8 @@ static int spgemm_values_t(int PH, const csrk_pattern &A, const T *Av, const csr
     if (PH == PH_NUM) {
         CSRK_LAUNCH((k_gemm_S<T, PH_NUM>), gS, kSTPB, s_smem<T>(PH_NUM, stage_vals()), s, m, A.indptr, A.indices,
                     Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, Cv, ctn, tn, tn, wl, b, stage_vals());
-        CSRK_LAUNCH((k_gemm_W<T, PH_NUM>), w_grid(), kWTPB, w_smem(), s, wl, b, A.indptr, A.indices, Av, B.indptr,
+        CSRK_LAUNCH((k_gemm_W<T, PH_NUM>), w_grid(), kWTPB, w_smem(), s, wl, b, BigList{}, A.indptr, A.indices, Av,
+                    B.indptr,
                     B.indices, Bv, Cp, const_cast<int32_t *>(C.indices), Cv, ctn, tn, tn);
         CSRK_LAUNCH(k_big_prep, big_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, B.indptr);
         CSRK_LAUNCH(k_big_items, 1, kItemsTPB, 0, s, br);
@@ -1052,7 +1084,8 @@ static int spgemm_values_t(int PH, const csrk_pattern &A, const T *Av, const csr
     } else {
         CSRK_LAUNCH((k_gemm_S<T, PH_BWD>), gS, kSTPB, s_smem<T>(PH_BWD, stage_vals()), s, m, A.indptr, A.indices,
                     Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, tn, dC, dA, dB, wl, b, stage_vals());
-        CSRK_LAUNCH((k_gemm_W<T, PH_BWD>), w_grid(), kWTPB, w_smem(), s, wl, b, A.indptr, A.indices, Av, B.indptr,
+        CSRK_LAUNCH((k_gemm_W<T, PH_BWD>), w_grid(), kWTPB, w_smem(), s, wl, b, BigList{}, A.indptr, A.indices, Av,
+                    B.indptr,
                     B.indices, Bv, Cp, const_cast<int32_t *>(C.indices), tn, dC, dA, dB);
         CSRK_LAUNCH(k_big_prep, big_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, B.indptr);
         CSRK_LAUNCH(k_big_items, 1, kItemsTPB, 0, s, br);
