@@ -105,7 +105,32 @@ __global__ __launch_bounds__(kRowsTPB, 8) void k_rows(TileArgs<T> a, RowList L)
         }
         return;
     }
-    if (valid && !lng && !huge) {
+    bool done = false;
+    if (MODE == MODE_REDUCE && !hm) {
+        // long average rows (power-law bodies, config 4: 8..32 entries): a 4-lane group per row so
+        // the index / value loads of a warp instruction cover 8 rows instead of 32 (the per-thread
+        // walk is bound by L1 wavefronts there); lane-strided sums + a fixed 2-step shuffle tree
+        const int len = valid && !lng ? (int)(e - s) : 0;
+        const int tot = (int)__reduce_add_sync(FULL, (unsigned)len);
+        if (tot > 32 * 8) {
+            const int g = lane >> 2, sub = lane & 3;
+#pragma unroll 1
+            for (int k = 0; k < 4; ++k) {
+                const int src = 4 * g + k;
+                const int64_t rs = __shfl_sync(FULL, s, src), re = __shfl_sync(FULL, e, src);
+                const bool own = __shfl_sync(FULL, (int)(valid && !lng), src) != 0;
+                double acc = 0.0;
+                if (own)
+#pragma unroll 2
+                    for (int64_t p = rs + sub; p < re; p += 4) row_elem<T, MODE, PERM, SIDE>(a, row - lane + src, p, acc);
+                acc += __shfl_xor_sync(FULL, acc, 1);
+                acc += __shfl_xor_sync(FULL, acc, 2);
+                if (own && sub == 0) a.y[row - lane + src] = (T)acc;
+            }
+            done = true;
+        }
+    }
+    if (valid && !lng && !huge && !done) {
         double acc = 0.0;
 #pragma unroll 4
         for (int64_t p = s; p < e; ++p) row_elem<T, MODE, PERM, SIDE>(a, row, p, acc);
