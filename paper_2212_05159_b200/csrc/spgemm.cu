@@ -32,7 +32,10 @@
 
 namespace csrk {
 
-constexpr int kSMaxL = 8;
+#ifndef CSRK_S_MAXL
+#define CSRK_S_MAXL 8
+#endif
+constexpr int kSMaxL = CSRK_S_MAXL;  // A/B via CSRK_NVCC_EXTRA
 constexpr int64_t kSMaxW = 512;
 constexpr int kMMaxW = 8192;
 constexpr int kSTPB = 128;           // k_gemm_S: 4 warps
@@ -332,19 +335,21 @@ __device__ __forceinline__ int64_t lbound(const int32_t *c, int64_t n, int32_t v
 }
 
 // ---------------------------------------------------------------- medium rows: warp per row
-template <int WW, int WL, bool VAL>
+// per-phase layout (shared memory decides how many warps an SM holds): COUNT keeps a hash table
+// of 2 WW columns, FILL the WW gathered columns, NUM / BWD the C row (columns + fp64 values) and
+// the row's A values / dA
+template <int WW, int WL, int PH>
 struct WSmemT {
-    double val[WW];                 // NUM: row accumulator; BWD: dC row; COUNT: hash table (2 WW int32)
-    double dA[VAL ? WL : 1];        // BWD: dA of the row's A entries
-    double av[VAL ? WL : 1];        // NUM / BWD: A values of the row
-    int64_t bs[WL];                 // start in B of list t
-    int32_t key[WW];                // FILL: product columns (sorted); NUM / BWD: C row columns
-    int32_t off[WL + 1];            // flat offset of list t (off[l] = w)
+    static constexpr bool VAL = PH == PH_NUM || PH == PH_BWD;
+    double val[PH == PH_FILL ? 1 : WW];  // NUM: row accumulator; BWD: dC row; COUNT: hash table (2 WW int32)
+    double dA[VAL ? WL : 1];             // BWD: dA of the row's A entries
+    double av[VAL ? WL : 1];             // NUM / BWD: A values of the row
+    int64_t bs[WL];                      // start in B of list t
+    int32_t key[PH == PH_COUNT ? 1 : WW];// FILL: product columns (sorted); NUM / BWD: C row columns
+    int32_t off[WL + 1];                 // flat offset of list t (off[l] = w)
 };
-using WSmem = WSmemT<kWW, kWL, true>;
 // symbolic-only warp class for 512 < w <= kW2W (config-4 rows the CTA path sorted slowly)
 constexpr int kW2W = 1024;
-using WSmem2 = WSmemT<kW2W, kWL, false>;
 
 // last t in [0, l) with off[t] <= e (the list holding flat product e; empty lists skipped)
 __device__ __forceinline__ int w_list_of(const int32_t *off, int l, int e)
@@ -430,7 +435,7 @@ __global__ __launch_bounds__(kWTPB) void k_gemm_W(BigList wl, BigList big, BigLi
     extern __shared__ __align__(16) unsigned char s_dyn[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int WW = W2 ? kW2W : kWW;
-    using SM = WSmemT<WW, kWL, !W2>;
+    using SM = WSmemT<WW, kWL, PH>;
     SM &S = reinterpret_cast<SM *>(s_dyn)[warp];
     const unsigned FULL = 0xffffffffu;
     const int nrows = *(volatile int *)wl.count;
@@ -939,10 +944,14 @@ static size_t big_sym_smem() { return sizeof(uint32_t) * kBitmapWords; }
 static size_t big_sort_smem() { return sizeof(int32_t) * kMMaxW; }
 static unsigned sort_grid() { return (unsigned)(kNumSMs * 4); }
 static unsigned val_grid() { return (unsigned)(kNumSMs * 4); }
-static size_t w_smem() { return sizeof(WSmem) * kWWarps; }
-static size_t w2_smem() { return sizeof(WSmem2) * kWWarps; }
-static unsigned w2_grid() { return (unsigned)(kNumSMs * 4); }
-static unsigned w_grid() { return (unsigned)(kNumSMs * 7); }
+template <int WW, int PH> static size_t wsm() { return sizeof(WSmemT<WW, kWL, PH>) * kWWarps; }
+// enough CTAs to fill every SM at the occupancy the phase's shared memory allows
+static unsigned wgrid(size_t smem)
+{
+    size_t per = smem > 0 ? (size_t)(227 * 1024) / (smem + 1024) : 16;
+    per = per < 1 ? 1 : per > 16 ? 16 : per;
+    return (unsigned)(kNumSMs * per);
+}
 
 static int set_smem_attrs()
 {
@@ -951,12 +960,15 @@ static int set_smem_attrs()
     const int bs = (int)big_sym_smem();
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_sym<PH_COUNT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bs));
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_sym<PH_FILL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bs));
-    const int ww = (int)w_smem();
-    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, ww));
-    const int w2s = (int)w2_smem();
-    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_COUNT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, w2s));
-    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_FILL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, w2s));
-    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_FILL>, cudaFuncAttributeMaxDynamicSharedMemorySize, ww));
+    const int ww = (int)wsm<kWW, PH_NUM>();
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)wsm<kWW, PH_COUNT>()));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_COUNT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)wsm<kW2W, PH_COUNT>()));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_FILL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)wsm<kW2W, PH_FILL>()));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_FILL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)wsm<kWW, PH_FILL>()));
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_NUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, ww));
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, ww));
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<float, PH_NUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, ww));
@@ -1022,9 +1034,10 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, i
             CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 4 * sizeof(int), s));
             CSRK_LAUNCH((k_gemm_S<double, PH_COUNT>), gS, kSTPB, 0, s, m, A.indptr, A.indices, dn, B.indptr, Bi, dn,
                         Cp, (int32_t *)nullptr, dw, dn, dw, dw, wl, b, 0);
-            CSRK_LAUNCH((k_gemm_W<double, PH_COUNT>), w_grid(), kWTPB, w_smem(), s, wl, b, w2, A.indptr, A.indices,
+            CSRK_LAUNCH((k_gemm_W<double, PH_COUNT>), wgrid((wsm<kWW, PH_COUNT>())), kWTPB, (wsm<kWW, PH_COUNT>()), s, wl, b, w2, A.indptr, A.indices,
                         dn, B.indptr, Bi, dn, Cp, (int32_t *)nullptr, dw, dn, dw, dw);
-            CSRK_LAUNCH((k_gemm_W<double, PH_COUNT, true>), w2_grid(), kWTPB, w2_smem(), s, w2, b, BigList{},
+            CSRK_LAUNCH((k_gemm_W<double, PH_COUNT, true>), wgrid((wsm<kW2W, PH_COUNT>())), kWTPB,
+                        (wsm<kW2W, PH_COUNT>()), s, w2, b, BigList{},
                         A.indptr, A.indices, dn, B.indptr, Bi, dn, Cp, (int32_t *)nullptr, dw, dn, dw, dw);
             CSRK_LAUNCH(k_big_prep, big_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, B.indptr);
             CSRK_LAUNCH((k_gemm_big_sym<PH_COUNT, false>), sort_grid(), kGemmTPB, big_sort_smem(), s, br, B.ncols,
@@ -1041,9 +1054,10 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, i
     CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 4 * sizeof(int), s));
     CSRK_LAUNCH((k_gemm_S<double, PH_FILL>), gS, kSTPB, s_smem<double>(PH_FILL, stage_fill()), s, m, A.indptr,
                 A.indices, dn, B.indptr, Bi, dn, Cp, Ci, dw, dn, dw, dw, wl, b, stage_fill());
-    CSRK_LAUNCH((k_gemm_W<double, PH_FILL>), w_grid(), kWTPB, w_smem(), s, wl, b, w2, A.indptr, A.indices, dn,
+    CSRK_LAUNCH((k_gemm_W<double, PH_FILL>), wgrid((wsm<kWW, PH_FILL>())), kWTPB, (wsm<kWW, PH_FILL>()), s, wl, b, w2, A.indptr, A.indices, dn,
                 B.indptr, Bi, dn, Cp, Ci, dw, dn, dw, dw);
-    CSRK_LAUNCH((k_gemm_W<double, PH_FILL, true>), w2_grid(), kWTPB, w2_smem(), s, w2, b, BigList{}, A.indptr,
+    CSRK_LAUNCH((k_gemm_W<double, PH_FILL, true>), wgrid((wsm<kW2W, PH_FILL>())), kWTPB,
+                (wsm<kW2W, PH_FILL>()), s, w2, b, BigList{}, A.indptr,
                 A.indices, dn, B.indptr, Bi, dn, Cp, Ci, dw, dn, dw, dw);
     CSRK_LAUNCH(k_big_prep, big_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, B.indptr);
     CSRK_LAUNCH((k_gemm_big_sym<PH_FILL, false>), sort_grid(), kGemmTPB, big_sort_smem(), s, br, B.ncols, A.indptr,
@@ -1073,7 +1087,7 @@ static int spgemm_values_t(int PH, const csrk_pattern &A, const T *Av, const csr
     if (PH == PH_NUM) {
         CSRK_LAUNCH((k_gemm_S<T, PH_NUM>), gS, kSTPB, s_smem<T>(PH_NUM, stage_vals()), s, m, A.indptr, A.indices,
                     Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, Cv, ctn, tn, tn, wl, b, stage_vals());
-        CSRK_LAUNCH((k_gemm_W<T, PH_NUM>), w_grid(), kWTPB, w_smem(), s, wl, b, BigList{}, A.indptr, A.indices, Av,
+        CSRK_LAUNCH((k_gemm_W<T, PH_NUM>), wgrid((wsm<kWW, PH_NUM>())), kWTPB, (wsm<kWW, PH_NUM>()), s, wl, b, BigList{}, A.indptr, A.indices, Av,
                     B.indptr,
                     B.indices, Bv, Cp, const_cast<int32_t *>(C.indices), Cv, ctn, tn, tn);
         CSRK_LAUNCH(k_big_prep, big_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, B.indptr);
@@ -1084,7 +1098,7 @@ static int spgemm_values_t(int PH, const csrk_pattern &A, const T *Av, const csr
     } else {
         CSRK_LAUNCH((k_gemm_S<T, PH_BWD>), gS, kSTPB, s_smem<T>(PH_BWD, stage_vals()), s, m, A.indptr, A.indices,
                     Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, tn, dC, dA, dB, wl, b, stage_vals());
-        CSRK_LAUNCH((k_gemm_W<T, PH_BWD>), w_grid(), kWTPB, w_smem(), s, wl, b, BigList{}, A.indptr, A.indices, Av,
+        CSRK_LAUNCH((k_gemm_W<T, PH_BWD>), wgrid((wsm<kWW, PH_BWD>())), kWTPB, (wsm<kWW, PH_BWD>()), s, wl, b, BigList{}, A.indptr, A.indices, Av,
                     B.indptr,
                     B.indices, Bv, Cp, const_cast<int32_t *>(C.indices), tn, dC, dA, dB);
         CSRK_LAUNCH(k_big_prep, big_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, B.indptr);
