@@ -36,7 +36,7 @@
 
 namespace csrk {
 
-constexpr int kChTPB = 256;
+constexpr int kChTPB = 128;
 constexpr int kChPer = 8;
 constexpr int kChTile = kChTPB * kChPer;
 constexpr int kSfTPB = 256;
@@ -203,7 +203,7 @@ __device__ __forceinline__ void chain_block_scan(double mA, double mC, double &t
 }
 
 template <typename T, bool APPLY>
-__global__ __launch_bounds__(kChTPB, 2) void k_trsv_chain(TrsvArgs<T> a)
+__global__ __launch_bounds__(kChTPB, 4) void k_trsv_chain(TrsvArgs<T> a)
 {
     if (APPLY && *(volatile int *)a.abort) return;
     const int tid = threadIdx.x;
