@@ -506,6 +506,22 @@ class Workload:
             rec("halo_reduce", 1)
 
 
+NOMINAL_HBM_GBS = 8000.0  # north_star "~8 TB/s" (SURVEY 8(d) d.1 gates on it)
+
+
+def gate_report(costs, op_ms, peak):
+    """SURVEY 8(d) d.1 gate: (bytes_fwd + bytes_bwd) / (t_fwd + t_bwd) for SpMV and SpMM on config 2,
+    as a fraction of the measured copy peak and of the nominal 8 TB/s (target >= 0.60)."""
+    out = {}
+    for nm in ("spmv", "spmm"):
+        b = costs[f"{nm}_fwd"][0] + costs[f"{nm}_bwd"][0]
+        t = (op_ms[f"{nm}_fwd"] + op_ms[f"{nm}_bwd"]) * 1e-3
+        gbs = b / t / 1e9
+        out[f"{nm}_fwd_bwd"] = {"GB/s": round(gbs, 1), "frac_measured": round(gbs / peak, 3),
+                                "frac_nominal": round(gbs / NOMINAL_HBM_GBS, 3)}
+    return out
+
+
 def flush_l2(torch, buf):
     buf.zero_()
 
@@ -691,7 +707,7 @@ def main():
                "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                             "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
                             "traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes": dom_bytes},
-               "ops": ops_report, "gpu_launches": int(launches),
+               "ops": ops_report, "gate": gate_report(W.costs, op_ms, peak), "gpu_launches": int(launches),
                "clocks": clk.summary()}
     # ---------------- e2e: same metric through the public API with pinned host buffers
     if not args.no_e2e:
