@@ -21,6 +21,10 @@
 
 namespace csrk {
 
+#ifndef CSRK_STREAM_UNROLL
+#define CSRK_STREAM_UNROLL 4
+#endif
+constexpr int kStreamUnroll = CSRK_STREAM_UNROLL;  // A/B via CSRK_NVCC_EXTRA
 constexpr int kShortRow = 32;
 constexpr int kHugeRow = 4096;
 constexpr int kRowsTPB = 256;
@@ -89,7 +93,7 @@ __global__ __launch_bounds__(kRowsTPB, 8) void k_rows(TileArgs<T> a, RowList L)
             const int w = threadIdx.x >> 5;
             for (int64_t p = s; p < e; ++p) s_rw[w][p - e0] = (uint8_t)lane;
             __syncwarp();
-#pragma unroll 4
+#pragma unroll kStreamUnroll
             for (int64_t p = e0 + lane; p < e1; p += 32) row_elem<T, MODE, PERM, SIDE>(a, r0 + s_rw[w][p - e0], p, dummy);
             return;
         }
