@@ -88,3 +88,20 @@ def test_gcn_layer(ck, dt):
     assert_S_close(dX.cpu().numpy(), ref["dX"], 4 * SdZ @ np.abs(W.astype(np.float64)).T, RTOL[dt], "layer dX")
     assert_S_close(dW.cpu().numpy(), ref["dTheta"], 4 * np.abs(X.astype(np.float64)).T @ SdZ, RTOL[dt], "layer dTheta")
     assert_S_close(db.cpu().numpy(), ref["dbias"], P["S_dbias"], RTOL[dt], "layer dbias")
+
+
+def test_gcn_bench_size(ck):
+    """The bench configuration (2^20 nodes, 5 edges per node, hubs up to ~3600, F = 16, fp32):
+    forward and backward propagation against the oracle on every node."""
+    A = synth.powerlaw_graph(1 << 20, 5.0, 4401, dtype=np.float32)
+    n, F = A.nrows, 16
+    Z = synth.dense((n, F), 2, np.float32)
+    b = synth.dense(F, 3, np.float32)
+    dY = synth.dense((n, F), 4, np.float32)
+    Ad = ck.CSR.from_host(A)
+    Y, D = ck.gcn_fwd(Ad, torch.from_numpy(Z).cuda(), torch.from_numpy(b).cuda())
+    dZ, db = ck.gcn_bwd(Ad, D, torch.from_numpy(dY).cuda(), plan=ck.csr_transpose(Ad, with_values=False))
+    ref = ogcn.gcn_prop(A, Z, b, want_grad=dY)
+    assert_S_close(Y.cpu().numpy(), ref["Y"], ref["S"], RTOL[np.float32], "Y")
+    assert_S_close(dZ.cpu().numpy(), ref["dZ"], ref["S_dZ"], RTOL[np.float32], "dZ")
+    assert_S_close(db.cpu().numpy(), ref["dbias"], ref["S_dbias"], RTOL[np.float32], "dbias")
