@@ -528,7 +528,7 @@ __global__ __launch_bounds__(kWTPB) void k_gemm_W(BigList wl, BigList big, BigLi
                     }
                 }
                 if (PH == PH_FILL && ok) S.key[e] = j;
-                if (PH == PH_NUM && ok) {
+                if (PH == PH_NUM && ok) {  // (a match_any merge instead of the atomic: 75 vs 72 ms, config 4)
                     const int64_t pos = lbound(S.key, nc, j);
                     atomicAdd(&S.val[pos], S.av[tv[u]] * bv[u]);
                 }
@@ -549,7 +549,8 @@ __global__ __launch_bounds__(kWTPB) void k_gemm_W(BigList wl, BigList big, BigLi
                         if (lane >= o && ty == tt) v += y;
                     }
                     const int tn = __shfl_down_sync(FULL, tt, 1);
-                    if (ok && (lane == 31 || tn != tt)) atomicAdd(&S.dA[tt], v);
+                    if (ok && (lane == 31 || tn != tt)) S.dA[tt] += v;  // one tail per list per step
+                    __syncwarp();
                 }
             }
         }
