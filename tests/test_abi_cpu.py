@@ -72,3 +72,33 @@ def test_host_side_argument_checks(lib):
     assert lib.csrk_spmv_fwd(1, 0, A, 8, None, None, 8, 8, None, 0, None) == -4
     assert lib.csrk_workspace_size(5, 1, ctypes.byref(A), ctypes.byref(A), 0, 0, ctypes.byref(n)) == 0 and n.value > 0
     assert lib.csrk_launch_count() == 0
+
+
+def test_host_side_argument_checks_f_rows(lib):
+    """Sp+Sp / SpTRSV / GCN entry points reject bad shapes and arguments on the host."""
+    from paper_2212_05159_b200 import csrk
+    P = csrk.Pattern
+    nnz = ctypes.c_int64(0)
+    # Sp + Sp: shapes must match
+    assert lib.csrk_spadd_symbolic(P(3, 4, 0, 8, 0), P(3, 5, 0, 8, 0), 8, None, ctypes.byref(nnz), None, 0,
+                                   None) == -2
+    # SpTRSV: square only, b / x required
+    assert lib.csrk_sptrsv_fwd(1, P(3, 4, 0, 8, 0), None, 0, 0, 8, 8, None, 0, None) == -2
+    assert lib.csrk_sptrsv_fwd(1, P(3, 3, 3, 8, 8), 8, 0, 0, None, 8, None, 0, None) == -1
+    # SpTRSV backward: nothing requested -> no-op
+    assert lib.csrk_sptrsv_bwd(1, P(3, 3, 3, 8, 8), 8, None, None, 0, 0, 8, 8, None, None, None, 0, None) == 0
+    # GCN: width 1..128, ld >= F
+    assert lib.csrk_gcn_fwd(1, P(3, 3, 0, 8, 0), None, 0, 8, 0, None, 8, 0, 8, None, 0, None) == -1
+    assert lib.csrk_gcn_fwd(1, P(3, 3, 0, 8, 0), None, 129, 8, 129, None, 8, 129, 8, None, 0, None) == -1
+    assert lib.csrk_gcn_fwd(1, P(3, 3, 0, 8, 0), None, 16, 8, 8, None, 8, 16, 8, None, 0, None) == -1
+    assert lib.csrk_gcn_fwd(1, P(3, 4, 0, 8, 0), None, 16, 8, 16, None, 8, 16, 8, None, 0, None) == -2
+    # dense products: leading dimensions, shared-memory limits
+    assert lib.csrk_dense_gemm_nn(1, 10, 4, 8, 8, 3, 8, 0, 8, 8, None) == -1
+    assert lib.csrk_dense_gemm_tn(1, 10, 300, 16, 8, 300, 8, 16, 8, None, 0, None) == -1
+    # workspace sizing of the f-row ops is host-only and positive
+    n = ctypes.c_size_t(0)
+    A = P(1000, 1000, 5000, 8, 8)
+    for op, k, plan in ((11, 0, 0), (12, 0, 0), (12, 0, 1), (13, 16, 0), (14, 16, 0), (14, 16, 1)):
+        assert lib.csrk_workspace_size(op, 1, ctypes.byref(A), None, k, plan, ctypes.byref(n)) == 0, op
+        assert n.value > 0, op
+    assert lib.csrk_launch_count() == 0
