@@ -43,7 +43,10 @@ constexpr int kSWarps = kSTPB / 32;
 #ifndef CSRK_S_MINB
 #define CSRK_S_MINB 6  // measured: numeric 421 -> 355 us, bwd dA 452 -> 410 us on config 2 (1 and 4: no change)
 #endif
-constexpr int kSMinBlocks = CSRK_S_MINB;  // k_gemm_S occupancy hint (A/B via CSRK_NVCC_EXTRA)
+constexpr int kSMinBlocks = CSRK_S_MINB;
+#ifndef CSRK_S_BWD_BL
+#define CSRK_S_BWD_BL 0
+#endif  // k_gemm_S occupancy hint (A/B via CSRK_NVCC_EXTRA)
 constexpr int kSBuf = 832;           // staged C entries per warp (3D 7-point A^2: 32 x 25 = 800)
 constexpr int kSBufA = 32 * kSMaxL;  // staged dA entries per warp
 constexpr int kGemmTPB = 512;        // k_gemm_big*
@@ -213,7 +216,7 @@ __device__ __forceinline__ int64_t s_merge(int64_t as, int l, const int32_t *__r
                                            const int32_t *__restrict__ Bi, const T *__restrict__ Bv,
                                            int32_t *outI, T *outV, const T *dCrow, T *dArow, T *__restrict__ dB)
 {
-    if constexpr (PH == PH_NUM)
+    if constexpr (PH == PH_NUM || (PH == PH_BWD && CSRK_S_BWD_BL))
         return s_merge_bl<T, PH, L>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB);
     else
         return s_merge_br<T, PH, L>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB);
