@@ -73,8 +73,11 @@ __global__ __launch_bounds__(kRsTPB) void k_rs_up(int64_t nnz, int64_t ntiles, i
     cnt[1 + (int64_t)tid * ntiles + tile] = s_h[tid];
 }
 
+#ifndef CSRK_RS_MINB
+#define CSRK_RS_MINB 1
+#endif
 template <bool FIRST, bool LAST>
-__global__ __launch_bounds__(kRsTPB) void k_rs_down(int64_t nnz, int64_t ntiles, int shift,
+__global__ __launch_bounds__(kRsTPB, CSRK_RS_MINB) void k_rs_down(int64_t nnz, int64_t ntiles, int shift,
                                                     const int32_t *__restrict__ kin, const uint64_t *__restrict__ vin,
                                                     const int32_t *__restrict__ rows, const int64_t *__restrict__ cnt,
                                                     int32_t *__restrict__ kout, uint64_t *__restrict__ vout,

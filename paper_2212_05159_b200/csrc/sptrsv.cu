@@ -372,7 +372,10 @@ __device__ __forceinline__ bool chain_rows_reg(const TrsvArgs<T> &a, int64_t o0,
 }
 
 template <typename T>
-__global__ __launch_bounds__(kLbTPB) void k_trsv_chain_lb(TrsvArgs<T> a)
+#ifndef CSRK_LB_MINB
+#define CSRK_LB_MINB 4  // measured: chain fwd 0.55 -> 0.48 ms (<= 64 registers, 4 CTAs per SM)
+#endif
+__global__ __launch_bounds__(kLbTPB, CSRK_LB_MINB) void k_trsv_chain_lb(TrsvArgs<T> a)
 {
     __shared__ int s_tile, s_abort;
     __shared__ double s_wA[kLbTPB / 32], s_wC[kLbTPB / 32];
