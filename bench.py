@@ -718,6 +718,10 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = run_cpu_baseline()
         cb.pop("seconds", None)
+        # also single-threaded (the paper's CPU methodology), on a
+        # 1/16 sample of the rows
+        st1 = run_cpu_baseline(threads=1, rows_sample=1 << 18)
+        cb["single_thread"] = {"value": st1["value"], "unit": "GB/s", "cores": 1, "sample": st1["sample"]}
         out["cpu_baseline"] = cb
     if out is not None:
         print(json.dumps(out))

@@ -428,6 +428,17 @@ constexpr int kWCAP = 1536;
 // CTA size per mode (measured, config 2): 256 threads with the band for the forward modes,
 // 128 threads (more, smaller CTAs per SM) for the dot-product modes.
 template <int MODE> constexpr int wide_tpb() { return MODE == SP_FWD || MODE == SP_FWD_PERM ? 256 : 128; }
+#ifndef CSRK_WIDE_MINB_FWD
+#define CSRK_WIDE_MINB_FWD 2
+#endif
+#ifndef CSRK_WIDE_MINB_DOT
+#define CSRK_WIDE_MINB_DOT 4
+#endif
+// occupancy hint (CTAs per SM) per mode; A/B via CSRK_NVCC_EXTRA
+template <int MODE> constexpr int wide_minb()
+{
+    return MODE == SP_FWD || MODE == SP_FWD_PERM ? CSRK_WIDE_MINB_FWD : CSRK_WIDE_MINB_DOT;
+}
 
 struct __align__(16) WideNz {
     double val;
@@ -442,7 +453,7 @@ constexpr int kBandH = 8;
 template <int MODE> constexpr int band_cap() { return wide_tpb<MODE>() / kWG * kWRPG + 2 * kBandH + 1; }
 
 template <typename T, int NV, int MODE, bool BAND>
-__global__ __launch_bounds__(wide_tpb<MODE>(), 512 / wide_tpb<MODE>()) void k_spmm_wide(SpmmArgs<T> a)
+__global__ __launch_bounds__(wide_tpb<MODE>(), wide_minb<MODE>()) void k_spmm_wide(SpmmArgs<T> a)
 {
     constexpr int kWTPB = wide_tpb<MODE>();
     constexpr int kWRT = kWTPB / kWG * kWRPG;
