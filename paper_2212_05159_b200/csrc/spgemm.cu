@@ -86,14 +86,14 @@ __device__ __forceinline__ void ld_pred(double &v, const float *p, bool pred)
 
 // Branchy merge: only the lists whose head matched advance (a divergent branch per list).
 // Measured best for the symbolic phases and the backward pass (fewer registers).
-template <typename T, int PH, int L>
+template <typename T, int PH, int L, typename IX = int64_t>
 __device__ __forceinline__ int64_t s_merge_br(int64_t as, int l, const int32_t *__restrict__ Ai,
                                               const T *__restrict__ Av, const int64_t *__restrict__ Bp,
                                               const int32_t *__restrict__ Bi, const T *__restrict__ Bv,
                                               int32_t *outI, T *outV, const T *dCrow, T *dArow,
                                               T *__restrict__ dB)
 {
-    int64_t cur[L];
+    IX cur[L];
     int rem[L];
     int32_t head[L];
     double av[L], dacc[L];
@@ -105,8 +105,8 @@ __device__ __forceinline__ int64_t s_merge_br(int64_t as, int l, const int32_t *
         av[t] = dacc[t] = 0.0;
         if (t < l) {
             const int32_t k = Ai[as + t];
-            cur[t] = Bp[k];
-            rem[t] = (int)(Bp[k + 1] - cur[t]);
+            cur[t] = (IX)Bp[k];
+            rem[t] = (int)(Bp[k + 1] - Bp[k]);
             if (PH == PH_NUM || PH == PH_BWD) av[t] = (double)Av[as + t];
             if (rem[t] > 0) head[t] = Bi[cur[t]];
         }
@@ -145,7 +145,7 @@ __device__ __forceinline__ int64_t s_merge_br(int64_t as, int l, const int32_t *
 
 // Branch-free merge: every list is updated with selects and predicated loads each step, the
 // head's value cached in a register.  Measured best for the numeric phase.
-template <typename T, int PH, int L>
+template <typename T, int PH, int L, typename IX = int64_t>
 __device__ __forceinline__ int64_t s_merge_bl(int64_t as, int l, const int32_t *__restrict__ Ai,
                                               const T *__restrict__ Av, const int64_t *__restrict__ Bp,
                                               const int32_t *__restrict__ Bi, const T *__restrict__ Bv,
@@ -153,7 +153,7 @@ __device__ __forceinline__ int64_t s_merge_bl(int64_t as, int l, const int32_t *
                                               T *__restrict__ dB)
 {
     constexpr bool VAL = PH == PH_NUM || PH == PH_BWD;
-    int64_t cur[L];   // position in B of list t's head
+    IX cur[L];        // position in B of list t's head
     int rem[L];       // entries left in list t including the head
     int32_t head[L];  // column at the head (INT32_MAX when exhausted)
     double hv[L];     // value at the head (VAL)
@@ -166,8 +166,8 @@ __device__ __forceinline__ int64_t s_merge_bl(int64_t as, int l, const int32_t *
         hv[t] = av[t] = dacc[t] = 0.0;
         if (t < l) {
             const int32_t k = Ai[as + t];
-            cur[t] = Bp[k];
-            rem[t] = (int)(Bp[k + 1] - cur[t]);
+            cur[t] = (IX)Bp[k];
+            rem[t] = (int)(Bp[k + 1] - Bp[k]);
             if (VAL) av[t] = (double)Av[as + t];
             if (rem[t] > 0) {
                 head[t] = Bi[cur[t]];
@@ -210,19 +210,19 @@ __device__ __forceinline__ int64_t s_merge_bl(int64_t as, int l, const int32_t *
     return c;
 }
 
-template <typename T, int PH, int L>
+template <typename T, int PH, int L, typename IX>
 __device__ __forceinline__ int64_t s_merge(int64_t as, int l, const int32_t *__restrict__ Ai,
                                            const T *__restrict__ Av, const int64_t *__restrict__ Bp,
                                            const int32_t *__restrict__ Bi, const T *__restrict__ Bv,
                                            int32_t *outI, T *outV, const T *dCrow, T *dArow, T *__restrict__ dB)
 {
     if constexpr (PH == PH_NUM || (PH == PH_BWD && CSRK_S_BWD_BL))
-        return s_merge_bl<T, PH, L>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB);
+        return s_merge_bl<T, PH, L, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB);
     else
-        return s_merge_br<T, PH, L>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB);
+        return s_merge_br<T, PH, L, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB);
 }
 
-template <typename T, int PH>
+template <typename T, int PH, typename IX = int64_t>
 __global__ __launch_bounds__(kSTPB, kSMinBlocks) void k_gemm_S(int64_t m, const int64_t *__restrict__ Ap,
                                                   const int32_t *__restrict__ Ai, const T *__restrict__ Av,
                                                   const int64_t *__restrict__ Bp, const int32_t *__restrict__ Bi,
@@ -300,14 +300,14 @@ __global__ __launch_bounds__(kSTPB, kSMinBlocks) void k_gemm_S(int64_t m, const 
         T *dArow = (PH == PH_BWD && dA) ? (stage ? s_dA_w + (as - a_lo) : dA + as) : nullptr;
         int64_t cnt = 0;
         switch (Lw) {
-        case 1: cnt = s_merge<T, PH, 1>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
-        case 2: cnt = s_merge<T, PH, 2>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
-        case 3: cnt = s_merge<T, PH, 3>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
-        case 4: cnt = s_merge<T, PH, 4>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
-        case 5: cnt = s_merge<T, PH, 5>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
-        case 6: cnt = s_merge<T, PH, 6>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
-        case 7: cnt = s_merge<T, PH, 7>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
-        case 8: cnt = s_merge<T, PH, 8>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
+        case 1: cnt = s_merge<T, PH, 1, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
+        case 2: cnt = s_merge<T, PH, 2, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
+        case 3: cnt = s_merge<T, PH, 3, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
+        case 4: cnt = s_merge<T, PH, 4, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
+        case 5: cnt = s_merge<T, PH, 5, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
+        case 6: cnt = s_merge<T, PH, 6, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
+        case 7: cnt = s_merge<T, PH, 7, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
+        case 8: cnt = s_merge<T, PH, 8, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
         default: break;  // l == 0: empty row
         }
         if (PH == PH_COUNT) Cp[i + 1] = cnt;
@@ -1019,6 +1019,15 @@ static void carve_lists(const csrk_pattern &A, BigList &wl, BigList &big, BigRow
     br.items = ws.take<int32_t>(m + 1);
 }
 
+// k_gemm_S with 32-bit B positions when B has fewer than 2^31 entries (cheaper merge steps)
+template <typename T, int PH, typename... Args>
+static int launch_S(bool small, unsigned grid, size_t smem, cudaStream_t s, Args... args)
+{
+    if (small) CSRK_LAUNCH((k_gemm_S<T, PH, int32_t>), grid, kSTPB, smem, s, args...);
+    else CSRK_LAUNCH((k_gemm_S<T, PH, int64_t>), grid, kSTPB, smem, s, args...);
+    return CSRK_OK;
+}
+
 int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, int32_t *Ci, int64_t *nnzC_host,
                     Bump &ws, cudaStream_t s)
 {
@@ -1036,8 +1045,8 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, i
         CSRK_CUDA(cudaMemsetAsync(Cp, 0, sizeof(int64_t), s));
         if (m > 0) {
             CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 4 * sizeof(int), s));
-            CSRK_LAUNCH((k_gemm_S<double, PH_COUNT>), gS, kSTPB, 0, s, m, A.indptr, A.indices, dn, B.indptr, Bi, dn,
-                        Cp, (int32_t *)nullptr, dw, dn, dw, dw, wl, b, 0);
+            CSRK_TRY((launch_S<double, PH_COUNT>)(B.nnz < INT32_MAX, gS, 0, s, m, A.indptr, A.indices, dn, B.indptr, Bi, dn,
+                        Cp, (int32_t *)nullptr, dw, dn, dw, dw, wl, b, 0));
             CSRK_LAUNCH((k_gemm_W<double, PH_COUNT>), wgrid((wsm<kWW, PH_COUNT>())), kWTPB, (wsm<kWW, PH_COUNT>()), s, wl, b, w2, A.indptr, A.indices,
                         dn, B.indptr, Bi, dn, Cp, (int32_t *)nullptr, dw, dn, dw, dw);
             CSRK_LAUNCH((k_gemm_W<double, PH_COUNT, true>), wgrid((wsm<kW2W, PH_COUNT>())), kWTPB,
@@ -1056,8 +1065,8 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, i
     }
     if (m == 0) return CSRK_OK;
     CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 4 * sizeof(int), s));
-    CSRK_LAUNCH((k_gemm_S<double, PH_FILL>), gS, kSTPB, s_smem<double>(PH_FILL, stage_fill()), s, m, A.indptr,
-                A.indices, dn, B.indptr, Bi, dn, Cp, Ci, dw, dn, dw, dw, wl, b, stage_fill());
+    CSRK_TRY((launch_S<double, PH_FILL>)(B.nnz < INT32_MAX, gS, s_smem<double>(PH_FILL, stage_fill()), s, m, A.indptr,
+                A.indices, dn, B.indptr, Bi, dn, Cp, Ci, dw, dn, dw, dw, wl, b, stage_fill()));
     CSRK_LAUNCH((k_gemm_W<double, PH_FILL>), wgrid((wsm<kWW, PH_FILL>())), kWTPB, (wsm<kWW, PH_FILL>()), s, wl, b, w2, A.indptr, A.indices, dn,
                 B.indptr, Bi, dn, Cp, Ci, dw, dn, dw, dw);
     CSRK_LAUNCH((k_gemm_W<double, PH_FILL, true>), wgrid((wsm<kW2W, PH_FILL>())), kWTPB,
@@ -1089,8 +1098,8 @@ static int spgemm_values_t(int PH, const csrk_pattern &A, const T *Av, const csr
     T *tn = nullptr;
     const T *ctn = nullptr;
     if (PH == PH_NUM) {
-        CSRK_LAUNCH((k_gemm_S<T, PH_NUM>), gS, kSTPB, s_smem<T>(PH_NUM, stage_vals()), s, m, A.indptr, A.indices,
-                    Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, Cv, ctn, tn, tn, wl, b, stage_vals());
+        CSRK_TRY((launch_S<T, PH_NUM>)(B.nnz < INT32_MAX, gS, s_smem<T>(PH_NUM, stage_vals()), s, m, A.indptr, A.indices,
+                    Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, Cv, ctn, tn, tn, wl, b, stage_vals()));
         CSRK_LAUNCH((k_gemm_W<T, PH_NUM>), wgrid((wsm<kWW, PH_NUM>())), kWTPB, (wsm<kWW, PH_NUM>()), s, wl, b, BigList{}, A.indptr, A.indices, Av,
                     B.indptr,
                     B.indices, Bv, Cp, const_cast<int32_t *>(C.indices), Cv, ctn, tn, tn);
@@ -1100,8 +1109,8 @@ static int spgemm_values_t(int PH, const csrk_pattern &A, const T *Av, const csr
         CSRK_LAUNCH((k_gemm_big_val<T, PH_NUM>), val_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, Av, B.indptr,
                     B.indices, Bv, C.indptr, C.indices, Cv, ctn, tn, tn);
     } else {
-        CSRK_LAUNCH((k_gemm_S<T, PH_BWD>), gS, kSTPB, s_smem<T>(PH_BWD, stage_vals()), s, m, A.indptr, A.indices,
-                    Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, tn, dC, dA, dB, wl, b, stage_vals());
+        CSRK_TRY((launch_S<T, PH_BWD>)(B.nnz < INT32_MAX, gS, s_smem<T>(PH_BWD, stage_vals()), s, m, A.indptr, A.indices,
+                    Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, tn, dC, dA, dB, wl, b, stage_vals()));
         CSRK_LAUNCH((k_gemm_W<T, PH_BWD>), wgrid((wsm<kWW, PH_BWD>())), kWTPB, (wsm<kWW, PH_BWD>()), s, wl, b, BigList{}, A.indptr, A.indices, Av,
                     B.indptr,
                     B.indices, Bv, Cp, const_cast<int32_t *>(C.indices), tn, dC, dA, dB);
