@@ -93,22 +93,20 @@ __device__ __forceinline__ int64_t s_merge_br(int64_t as, int l, const int32_t *
                                               int32_t *outI, T *outV, const T *dCrow, T *dArow,
                                               T *__restrict__ dB)
 {
-    IX cur[L];
-    int rem[L];
+    IX cur[L], end[L];
     int32_t head[L];
     double av[L], dacc[L];
 #pragma unroll
     for (int t = 0; t < L; ++t) {
-        rem[t] = 0;
         head[t] = INT32_MAX;
-        cur[t] = 0;
+        cur[t] = end[t] = 0;
         av[t] = dacc[t] = 0.0;
         if (t < l) {
             const int32_t k = Ai[as + t];
             cur[t] = (IX)Bp[k];
-            rem[t] = (int)(Bp[k + 1] - Bp[k]);
+            end[t] = (IX)Bp[k + 1];
             if (PH == PH_NUM || PH == PH_BWD) av[t] = (double)Av[as + t];
-            if (rem[t] > 0) head[t] = Bi[cur[t]];
+            if (cur[t] < end[t]) head[t] = Bi[cur[t]];
         }
     }
     int64_t c = 0;
@@ -128,7 +126,7 @@ __device__ __forceinline__ int64_t s_merge_br(int64_t as, int l, const int32_t *
                     if (dB) red_add(&dB[cur[t]], (T)(av[t] * g));
                 }
                 ++cur[t];
-                head[t] = --rem[t] > 0 ? Bi[cur[t]] : INT32_MAX;
+                head[t] = cur[t] < end[t] ? Bi[cur[t]] : INT32_MAX;
             }
         }
         if (PH == PH_FILL) outI[c] = v;
