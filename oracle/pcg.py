@@ -10,6 +10,10 @@ CUDA path's hand adjoint independently.  Dense, so only for small n (n <= ~4096)
       q = A p; alpha = rho / (p.q); x += alpha p; r -= alpha q; record ||r||
       z = M r; rho' = r.z; p = z + (rho'/rho) p; rho = rho'
     loss = sum_{i=1}^{N_it} w_i ||r^(i)|| / ||b||,  w_i = gamma^(N_it - i) / sum_j gamma^(N_it - j)
+
+precond="solve" is the SpTRSV extension of SURVEY 8(f) row f3: M = (L L^T)^{-1} applied exactly by
+two triangular solves, z = L^{-T} (L^{-1} r) (an incomplete-Cholesky-type preconditioner whose
+factor L is learned with the same loss); the algorithm is otherwise unchanged.
 """
 from __future__ import annotations
 
@@ -24,7 +28,7 @@ def loss_weights(n_it: int, gamma: float) -> np.ndarray:
 
 
 def pcg_loss_grad(A_dense: np.ndarray, L_pattern_dense: np.ndarray, L_vals_dense: np.ndarray, b: np.ndarray,
-                  n_it: int, gamma: float, reassociate: bool = False):
+                  n_it: int, gamma: float, reassociate: bool = False, precond: str = "mult"):
     """Returns (loss, residual norms [n_it], dL dense masked to L's pattern).
     reassociate=True applies M as (L L^T) v instead of L (L^T v): the same mathematics in a
     different rounding order, used by the tests to measure how strongly n_it chained CG steps
@@ -34,7 +38,13 @@ def pcg_loss_grad(A_dense: np.ndarray, L_pattern_dense: np.ndarray, L_vals_dense
     Lfull = torch.tensor(L_vals_dense, dtype=torch.float64, requires_grad=True)
     L = Lfull * mask                                   # gradient lives on mask(L)
     bt = torch.tensor(b, dtype=torch.float64)
-    if reassociate:
+    if precond == "solve":
+        tri = torch.linalg.solve_triangular
+        if reassociate:
+            M = lambda v: torch.linalg.solve(L @ L.T, v)
+        else:
+            M = lambda v: tri(L.T, tri(L, v[:, None], upper=False), upper=True)[:, 0]
+    elif reassociate:
         M = lambda v: (L @ L.T) @ v
     else:
         M = lambda v: L @ (L.T @ v)

@@ -118,3 +118,63 @@ def test_pcg_config5_directional_derivative(ck):
     fd = (lp - lm) / (2 * h)
     dd = float((dL * V).sum())
     assert abs(fd - dd) <= 1e-6 * max(abs(dd), 1e-12), (fd, dd)
+
+
+# ---------------------------------------------------------------- precond="solve"
+from oracle import pcg  # noqa: E402
+def test_pcg_solve_identity_is_cg(orc):
+    """L = I: M = (L L^T)^{-1} = I, the same CG as the multiplicative form with L = I."""
+    A = synth.poisson2d(6)
+    L = synth.bidiag_lower(A.nrows, "identity")
+    b = np.full(A.nrows, 1.0 / np.sqrt(A.nrows))
+    args = (to_dense(A), pattern_dense(L), to_dense(L), b, 5, 0.6)
+    l1, r1, _ = pcg.pcg_loss_grad(*args)
+    l2, r2, _ = pcg.pcg_loss_grad(*args, precond="solve")
+    assert abs(l1 - l2) <= 1e-14 * abs(l1)
+    np.testing.assert_allclose(r2, r1, rtol=1e-13)
+
+
+def test_pcg_solve_exact_cholesky_converges_in_one_step(orc):
+    """L = chol(A) (dense lower pattern): M = A^{-1}, so the first PCG step solves A x = b and the
+    residual after it vanishes (to rounding) -- exact preconditioning."""
+    A = synth.poisson2d(5)
+    Ad = to_dense(A)
+    Lc = np.linalg.cholesky(Ad)
+    P = np.tril(np.ones_like(Ad)).astype(bool)
+    b = synth.dense(A.nrows, 3)
+    _, res, _ = pcg.pcg_loss_grad(Ad, P, Lc, b, 3, 0.6, precond="solve")
+    assert res[0] <= 1e-12 * np.linalg.norm(b)
+
+
+def test_pcg_solve_diagonal_matches_mult(orc):
+    """L = D diagonal: (L L^T)^{-1} = D^{-2} = (D^{-1})(D^{-1})^T, so precond="solve" with D and the
+    multiplicative form with D^{-1} run the same PCG."""
+    A = synth.poisson2d(6)
+    n = A.nrows
+    d = np.random.default_rng(4).uniform(0.5, 2.0, n)
+    P = np.eye(n, dtype=bool)
+    b = synth.dense(n, 5)
+    l1, r1, _ = pcg.pcg_loss_grad(to_dense(A), P, np.diag(d), b, 6, 0.6, precond="solve")
+    l2, r2, _ = pcg.pcg_loss_grad(to_dense(A), P, np.diag(1.0 / d), b, 6, 0.6)
+    assert abs(l1 - l2) <= 1e-12 * abs(l1)
+    np.testing.assert_allclose(r1, r2, rtol=1e-11)
+
+
+def test_pcg_solve_finite_differences(orc):
+    """Central differences of the solve-preconditioned loss in the stored entries of a seeded
+    bidiagonal L (nonlinear: h = 1e-6, rel 1e-6)."""
+    A = synth.poisson2d(5)
+    L = synth.bidiag_lower(A.nrows, "seeded")
+    b = np.full(A.nrows, 1.0 / np.sqrt(A.nrows))
+    Ad, P, Lv = to_dense(A), pattern_dense(L), to_dense(L)
+    _, _, g = pcg.pcg_loss_grad(Ad, P, Lv, b, 4, 0.6, precond="solve")
+    rows = np.repeat(np.arange(L.nrows), np.diff(L.indptr))
+    h = 1e-6
+    for q in range(0, L.nnz, 5):
+        i, j = rows[q], L.indices[q]
+        Lp, Lm = Lv.copy(), Lv.copy()
+        Lp[i, j] += h
+        Lm[i, j] -= h
+        fd = (pcg.pcg_loss_grad(Ad, P, Lp, b, 4, 0.6, precond="solve")[0]
+              - pcg.pcg_loss_grad(Ad, P, Lm, b, 4, 0.6, precond="solve")[0]) / (2 * h)
+        assert abs(fd - g[i, j]) <= 1e-6 * max(1.0, abs(fd)), (i, j)
