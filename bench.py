@@ -97,8 +97,9 @@ def run_cfg5(args, torch, ck):
     bt = torch.from_numpy(b).cuda()
     dL = torch.empty_like(Ld.values)
     N = 50
+    pc = args.precond
     for _ in range(args.warmup):
-        ck.pcg_loss_grad(Ad, Ld, bt, N, 0.6, dL=dL)
+        ck.pcg_loss_grad(Ad, Ld, bt, N, 0.6, dL=dL, precond=pc)
     torch.cuda.synchronize()
     st = torch.cuda.current_stream()
     l0 = ck.launch_count()
@@ -107,7 +108,7 @@ def run_cfg5(args, torch, ck):
         for _ in range(args.steps):
             a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(st)
-            loss, res, _ = ck.pcg_loss_grad(Ad, Ld, bt, N, 0.6, dL=dL)
+            loss, res, _ = ck.pcg_loss_grad(Ad, Ld, bt, N, 0.6, dL=dL, precond=pc)
             e.record(st)
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(e))
@@ -119,7 +120,9 @@ def run_cfg5(args, torch, ck):
            "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": "config5: 2D Poisson 4096^2 (16,777,216 rows, 83,869,696 nnz), lower-bidiagonal "
-                                  "L (33,554,431 nnz), 50 PCG iterations fwd + reverse, gamma 0.6, 1 GPU"},
+                                  "L (33,554,431 nnz), 50 PCG iterations fwd + reverse, gamma 0.6, 1 GPU",
+                      "preconditioner": "M = L L^T (P:836-839)" if pc == "mult" else
+                      "M = (L L^T)^-1 by two SpTRSV (SURVEY 8(f) f3); bytes counted as for M = L L^T"},
            "step_bytes": byts, "gflops": round(flops / (ms * 1e-3) / 1e9, 2), "loss": loss,
            "roofline": {"bound": "hbm", "kernel": "whole step", "achieved": round(byts / (ms * 1e-3) / 1e9, 1),
                         "peak": peak, "unit": "GB/s", "frac": round(byts / (ms * 1e-3) / 1e9 / peak, 4)},
@@ -592,6 +595,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5", "trsv", "gcn"])
+    ap.add_argument("--precond", default="mult", choices=["mult", "solve"], help="cfg5: M = L L^T or (L L^T)^-1")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

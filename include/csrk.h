@@ -77,7 +77,7 @@ typedef enum {
     CSRK_WS_SPGEMM_SYMBOLIC = 5,
     CSRK_WS_SPGEMM_NUMERIC = 6,
     CSRK_WS_SPGEMM_BWD = 7,
-    CSRK_WS_PCG = 8,         /* B = L, k = n_it */
+    CSRK_WS_PCG = 8,         /* B = L, k = n_it, have_plan = precond */
     CSRK_WS_SPADD_SYMBOLIC = 9,/* numeric / bwd need no workspace */
     CSRK_WS_SPAI = 10,       /* A = C = pattern(M A), B = R = pattern(I) U C, k = n */
     CSRK_WS_SPTRSV_FWD = 11, /* A = T */
@@ -317,11 +317,15 @@ int csrk_dense_gemm_tn(csrk_dtype dtype, int64_t n, int64_t C, int64_t F, const 
  * adjoints), run with the same kernels as the forward.  fp64 only.  All vectors are device
  * arrays of length n = A.nrows; loss_host (required) and resid_host (nullable, n_it entries,
  * ||r^(i)||) are host pointers: the call synchronises `stream` once at the end.
- * Workspace: csrk_workspace_size(CSRK_WS_PCG, CSRK_F64, &A, &L, n_it, 0, &bytes) -- the saved
- * p, q, r vectors of every iteration, (3 n_it + 12) n doubles.
+ * precond = 0: M = L L^T as in the paper (two SpMVs per application).  precond = 1 (SURVEY 8(f)
+ * row f3): M = (L L^T)^{-1} applied exactly by two triangular solves, u = L^{-1} r, z = L^{-T} u
+ * (csrk_sptrsv_*; L must be lower triangular with its diagonal, CSRK_VALIDATE=1 checks), the
+ * reverse pass through the SpTRSV VJPs.
+ * Workspace: csrk_workspace_size(CSRK_WS_PCG, CSRK_F64, &A, &L, n_it, precond, &bytes) -- the
+ * saved p, q, r vectors of every iteration, (3 n_it + 12) n doubles (+ L^T for precond = 1).
  */
 int csrk_pcg_loss_grad(csrk_pattern A, const double *A_val, csrk_pattern L, const double *L_val,
-                       const double *b, int n_it, double gamma, double *loss_host, double *resid_host,
+                       const double *b, int n_it, double gamma, int precond, double *loss_host, double *resid_host,
                        double *dL_val, void *ws, size_t ws_bytes, csrk_stream_t stream);
 
 /*

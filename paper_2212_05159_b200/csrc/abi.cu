@@ -321,19 +321,21 @@ int csrk_dense_gemm_tn(csrk_dtype dtype, int64_t n, int64_t C, int64_t F, const 
 }
 
 int csrk_pcg_loss_grad(csrk_pattern A, const double *A_val, csrk_pattern L, const double *L_val, const double *b,
-                       int n_it, double gamma, double *loss_host, double *resid_host, double *dL_val, void *ws,
-                       size_t ws_bytes, csrk_stream_t stream)
+                       int n_it, double gamma, int precond, double *loss_host, double *resid_host, double *dL_val,
+                       void *ws, size_t ws_bytes, csrk_stream_t stream)
 {
     CSRK_TRY(check_pat(A));
     CSRK_TRY(check_pat(L));
     if (A.nrows != A.ncols || L.nrows != A.nrows || L.ncols != A.nrows) return CSRK_ERR_DIM_MISMATCH;
-    if (n_it < 1 || !(gamma > 0.0) || !loss_host || !b || !dL_val || (A.nnz > 0 && !A_val) ||
+    if (n_it < 1 || !(gamma > 0.0) || (precond != 0 && precond != 1) || !loss_host || !b || !dL_val ||
+        (A.nnz > 0 && !A_val) ||
         (L.nnz > 0 && !L_val))
         return CSRK_ERR_INVALID_ARG;
     CSRK_TRY(validate_pattern(A, (cudaStream_t)stream));
     CSRK_TRY(validate_pattern(L, (cudaStream_t)stream));
+    if (precond) CSRK_TRY(validate_triangular(L, 0, 0, (cudaStream_t)stream));
     return with_ws(ws, ws_bytes, [&](Bump &bw) {
-        return pcg_loss_grad(A, A_val, L, L_val, b, n_it, gamma, loss_host, resid_host, dL_val, bw,
+        return pcg_loss_grad(A, A_val, L, L_val, b, n_it, gamma, precond, loss_host, resid_host, dL_val, bw,
                              (cudaStream_t)stream);
     });
 }
@@ -400,7 +402,7 @@ int csrk_workspace_size(csrk_ws_op op, csrk_dtype dtype, const csrk_pattern *A, 
     case CSRK_WS_PCG: {
         if (!B || k < 1) return CSRK_ERR_INVALID_ARG;
         double dummy = 0.0;
-        st = pcg_loss_grad(Ar, (const double *)d, *B, (const double *)d, (const double *)d, (int)k, 0.6, &dummy,
+        st = pcg_loss_grad(Ar, (const double *)d, *B, (const double *)d, (const double *)d, (int)k, 0.6, have_plan, &dummy,
                            nullptr, (double *)d, b, 0);
         break;
     }

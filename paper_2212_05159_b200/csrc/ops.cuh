@@ -50,7 +50,11 @@ int dense_gemm_nn(csrk_dtype dt, int64_t n, int64_t C, int64_t F, const void *X,
 int dense_gemm_tn(csrk_dtype dt, int64_t n, int64_t C, int64_t F, const void *X, int64_t ldx, const void *dZ,
                   int64_t lddz, void *dW, Bump &ws, cudaStream_t s);
 
+// dA[p] = -(w_i x_j) at the stored (i, j) of A (fp64; the masked outer product of the SpTRSV VJP)
+int trsv_outer(const csrk_pattern &A, const double *w, const double *x, double *dA, cudaStream_t s);
+
 int pcg_loss_grad(const csrk_pattern &A, const double *Av, const csrk_pattern &L, const double *Lv, const double *b,
-                  int N, double gamma, double *loss_host, double *resid_host, double *dL, Bump &ws, cudaStream_t s);
+                  int N, double gamma, int precond, double *loss_host, double *resid_host, double *dL, Bump &ws,
+                  cudaStream_t s);
 
 }  // namespace csrk

@@ -11,6 +11,9 @@
 // Reverse: the adjoint of each step above, in reverse order (see pcg_loss_grad below); L's
 // gradient comes from the SpMV VJPs of z = L u (op N) and u = L^T r (op T), A's products use
 // A^T = the op-T SpMV.  Vectors saved: p_{i-1}, q_i, r_i; u_i, z_i are recomputed.
+// precond = 1: M = (L L^T)^{-1} applied exactly, u = L^{-1} r, z = L^{-T} u, by
+// the SpTRSV kernels; their VJPs (a solve, a transposed solve and two masked outer products)
+// replace the SpMV VJPs.
 // All reductions are fixed-grid, fixed-order (deterministic).
 #include <cmath>
 #include <vector>
@@ -136,6 +139,8 @@ struct PcgWs {
     double *u, *z, *rbar, *pbar, *zbar, *ubar, *qbar, *tmp; // n each
     double *dAt;                                            // nnz(L)
     double *part;
+    csrk_pattern LT;                                        // precond = solve: L^T pattern + perm
+    int64_t *LTperm;
     Scal S;
     void *sub;
     size_t sub_bytes;
@@ -148,7 +153,29 @@ static size_t spmv_ws_bytes(const csrk_pattern &M)
     return b.used + 256;
 }
 
-static void carve_pcg(const csrk_pattern &A, const csrk_pattern &L, int N, PcgWs &w, Bump &ws)
+static size_t solve_ws_bytes(const csrk_pattern &L)
+{
+    size_t m = 0;
+    {
+        Bump b(nullptr, 0);
+        sptrsv_fwd(CSRK_F64, L, nullptr, 0, 0, nullptr, nullptr, b, 0);
+        m = b.used > m ? b.used : m;
+    }
+    {
+        Bump b(nullptr, 0);
+        csrk_pattern T{L.ncols, L.nrows, L.nnz, L.indptr, L.indices};
+        sptrsv_bwd(CSRK_F64, L, nullptr, &T, L.indptr, 0, 0, nullptr, nullptr, nullptr, nullptr, b, 0);
+        m = b.used > m ? b.used : m;
+    }
+    {
+        Bump b(nullptr, 0);
+        transpose_impl(CSRK_F64, L, nullptr, nullptr, nullptr, nullptr, nullptr, b, 0);
+        m = b.used > m ? b.used : m;
+    }
+    return m + 256;
+}
+
+static void carve_pcg(const csrk_pattern &A, const csrk_pattern &L, int N, int precond, PcgWs &w, Bump &ws)
 {
     const int64_t n = A.nrows;
     w.pb = ws.take<double>((size_t)N * n);
@@ -170,6 +197,15 @@ static void carve_pcg(const csrk_pattern &A, const csrk_pattern &L, int N, PcgWs
     w.S.alphabar = w.S.bb + 3;
     w.S.sbar = w.S.bb + 4;
     w.sub_bytes = spmv_ws_bytes(A) > spmv_ws_bytes(L) ? spmv_ws_bytes(A) : spmv_ws_bytes(L);
+    w.LTperm = nullptr;
+    w.LT = csrk_pattern{L.ncols, L.nrows, L.nnz, nullptr, nullptr};
+    if (precond) {
+        w.LT.indptr = ws.take<int64_t>(L.ncols + 1);
+        w.LT.indices = ws.take<int32_t>(L.nnz > 0 ? L.nnz : 1);
+        w.LTperm = ws.take<int64_t>(L.nnz > 0 ? L.nnz : 1);
+        const size_t sb = solve_ws_bytes(L);
+        w.sub_bytes = sb > w.sub_bytes ? sb : w.sub_bytes;
+    }
     w.sub = ws.take<char>(w.sub_bytes);
 }
 
@@ -188,10 +224,11 @@ static int dot_to(int64_t n, const double *x, const double *y, double *dst, doub
 }
 
 int pcg_loss_grad(const csrk_pattern &A, const double *Av, const csrk_pattern &L, const double *Lv, const double *b,
-                  int N, double gamma, double *loss_host, double *resid_host, double *dL, Bump &ws, cudaStream_t s)
+                  int N, double gamma, int precond, double *loss_host, double *resid_host, double *dL, Bump &ws,
+                  cudaStream_t s)
 {
     PcgWs w{};
-    carve_pcg(A, L, N, w, ws);
+    carve_pcg(A, L, N, precond, w, ws);
     if (ws.sizing()) return CSRK_OK;
     const int64_t n = A.nrows;
     auto sub = [&]() { return Bump(w.sub, w.sub_bytes); };
@@ -203,6 +240,59 @@ int pcg_loss_grad(const csrk_pattern &A, const double *Av, const csrk_pattern &L
         Bump bw = sub();
         return spmv_fwd(CSRK_F64, CSRK_OP_N, L, Lv, nullptr, nullptr, in, out, bw, s);
     };
+    if (precond) {  // L^T (pattern + perm) once per call, for the transposed solves
+        Bump bw = sub();
+        CSRK_TRY(transpose_impl(CSRK_F64, L, nullptr, const_cast<int64_t *>(w.LT.indptr),
+                                const_cast<int32_t *>(w.LT.indices), nullptr, w.LTperm, bw, s));
+    }
+    // z = M r with the intermediate in w.u:  M = L L^T: u = L^T r, z = L u;
+    // precond = solve: M = (L L^T)^{-1}: u = L^{-1} r, z = L^{-T} u
+    auto applyM = [&](const double *r, double *z) -> int {
+        if (!precond) {
+            CSRK_TRY(Lt(r, w.u));
+            return Ln(w.u, z);
+        }
+        {
+            Bump bw = sub();
+            CSRK_TRY(sptrsv_fwd(CSRK_F64, L, Lv, 0, 0, r, w.u, bw, s));
+        }
+        Bump bw = sub();
+        return sptrsv_bwd(CSRK_F64, L, Lv, &w.LT, w.LTperm, 0, 0, w.u, w.u, nullptr, z, bw, s);
+    };
+    // adjoint of z = M r given w.zbar (w.u, z of the same r): dL += ..., rbar += M^T zbar (if asked)
+    auto adjM = [&](const double *r, const double *z, bool want_rbar) -> int {
+        if (!precond) {
+            // z = L u:  Lbar += zbar u^T (.) mask(L);  ubar = L^T zbar
+            {
+                Bump bw = sub();
+                CSRK_TRY(spmv_bwd(CSRK_F64, CSRK_OP_N, L, Lv, nullptr, nullptr, w.u, w.zbar, w.dAt, w.ubar, bw, s));
+            }
+            LIN3(L.nnz, dL, ONE, dL, ONE, w.dAt, ONE, nullptr, nullptr, nullptr);
+            // u = L^T r:  Lbar += r ubar^T (.) mask(L);  rbar += L ubar
+            {
+                Bump bw = sub();
+                CSRK_TRY(spmv_bwd(CSRK_F64, CSRK_OP_T, L, Lv, nullptr, nullptr, r, w.ubar, w.dAt,
+                                  want_rbar ? w.tmp : nullptr, bw, s));
+            }
+            LIN3(L.nnz, dL, ONE, dL, ONE, w.dAt, ONE, nullptr, nullptr, nullptr);
+        } else {
+            // z = L^{-T} u:  ubar = L^{-1} zbar;  Lbar += -z ubar^T (.) mask(L)
+            {
+                Bump bw = sub();
+                CSRK_TRY(sptrsv_fwd(CSRK_F64, L, Lv, 0, 0, w.zbar, w.ubar, bw, s));
+            }
+            CSRK_TRY(trsv_outer(L, z, w.ubar, w.dAt, s));
+            LIN3(L.nnz, dL, ONE, dL, ONE, w.dAt, ONE, nullptr, nullptr, nullptr);
+            // u = L^{-1} r:  rbar += L^{-T} ubar;  Lbar += -(L^{-T} ubar) u^T (.) mask(L)
+            {
+                Bump bw = sub();
+                CSRK_TRY(sptrsv_bwd(CSRK_F64, L, Lv, &w.LT, w.LTperm, 0, 0, w.u, w.ubar, w.dAt, w.tmp, bw, s));
+            }
+            LIN3(L.nnz, dL, ONE, dL, ONE, w.dAt, ONE, nullptr, nullptr, nullptr);
+        }
+        if (want_rbar) LIN3(n, w.rbar, ONE, w.rbar, ONE, w.tmp, ONE, nullptr, nullptr, nullptr);
+        return CSRK_OK;
+    };
     const Scal &S = w.S;
     double *part = w.part;
     auto P = [&](int i) { return w.pb + (size_t)i * n; };       // p_i, i = 0..N-1
@@ -212,8 +302,7 @@ int pcg_loss_grad(const csrk_pattern &A, const double *Av, const csrk_pattern &L
     // ---------------- forward
     CSRK_TRY(dot_to(n, b, b, S.bb, 1.0, part, s));
     LIN3(n, R(0), ONE, b, ONE, nullptr, ONE, nullptr, nullptr, nullptr);
-    CSRK_TRY(Lt(b, w.u));
-    CSRK_TRY(Ln(w.u, P(0)));                                   // p0 = z0
+    CSRK_TRY(applyM(b, P(0)));                                 // p0 = z0
     CSRK_TRY(dot_to(n, b, P(0), &S.rho[0], 1.0, part, s));
     for (int i = 1; i <= N; ++i) {
         {
@@ -225,8 +314,7 @@ int pcg_loss_grad(const csrk_pattern &A, const double *Av, const csrk_pattern &L
         LIN3(n, R(i), ONE, R(i - 1), (Cf{-1.0, &S.rho[i - 1], &S.s[i]}), Q(i), ONE, nullptr, nullptr, part);
         CSRK_LAUNCH(k_finish, 1, kVecTPB, 0, s, (const double *)part, kVecGrid, &S.nr2[i], 1.0);
         if (i == N) break;                                     // rho_N, p_N do not reach the loss
-        CSRK_TRY(Lt(R(i), w.u));
-        CSRK_TRY(Ln(w.u, w.z));
+        CSRK_TRY(applyM(R(i), w.z));
         CSRK_TRY(dot_to(n, R(i), w.z, &S.rho[i], 1.0, part, s));
         // p_i = z_i + (rho_i / rho_{i-1}) p_{i-1}
         LIN3(n, P(i), ONE, w.z, (Cf{1.0, &S.rho[i], &S.rho[i - 1]}), P(i - 1), ONE, nullptr, nullptr, nullptr);
@@ -242,25 +330,12 @@ int pcg_loss_grad(const csrk_pattern &A, const double *Av, const csrk_pattern &L
             // p_i = z_i + beta_i p_{i-1}:  betabar = pbar . p_{i-1}
             CSRK_TRY(dot_to(n, w.pbar, P(i - 1), S.betabar, 1.0, part, s));
             CSRK_LAUNCH(k_bwd_beta, 1, 1, 0, s, S, i);
-            CSRK_TRY(Lt(R(i), w.u));
-            CSRK_TRY(Ln(w.u, w.z));
+            CSRK_TRY(applyM(R(i), w.z));                       // recompute u_i, z_i
             // zbar = pbar + rhobar_i r_i ;  rbar += cn_i r_i + rhobar_i z_i
             LIN3(n, w.zbar, ONE, w.pbar, (Cf{1.0, &S.rhobar[i], nullptr}), R(i), ONE, nullptr, nullptr, nullptr);
             LIN3(n, w.rbar, ONE, w.rbar, (Cf{1.0, &S.cn[i], nullptr}), R(i), (Cf{1.0, &S.rhobar[i], nullptr}), w.z,
                  nullptr, nullptr);
-            // z_i = L u_i:  Lbar += zbar u_i^T (.) mask(L);  ubar = L^T zbar
-            {
-                Bump bw = sub();
-                CSRK_TRY(spmv_bwd(CSRK_F64, CSRK_OP_N, L, Lv, nullptr, nullptr, w.u, w.zbar, w.dAt, w.ubar, bw, s));
-            }
-            LIN3(L.nnz, dL, ONE, dL, ONE, w.dAt, ONE, nullptr, nullptr, nullptr);
-            // u_i = L^T r_i:  Lbar += r_i ubar^T (.) mask(L);  rbar += L ubar
-            {
-                Bump bw = sub();
-                CSRK_TRY(spmv_bwd(CSRK_F64, CSRK_OP_T, L, Lv, nullptr, nullptr, R(i), w.ubar, w.dAt, w.tmp, bw, s));
-            }
-            LIN3(L.nnz, dL, ONE, dL, ONE, w.dAt, ONE, nullptr, nullptr, nullptr);
-            LIN3(n, w.rbar, ONE, w.rbar, ONE, w.tmp, ONE, nullptr, nullptr, nullptr);
+            CSRK_TRY(adjM(R(i), w.z, true));
         } else {
             LIN3(n, w.rbar, ONE, w.rbar, (Cf{1.0, &S.cn[i], nullptr}), R(i), ONE, nullptr, nullptr, nullptr);
         }
@@ -279,17 +354,8 @@ int pcg_loss_grad(const csrk_pattern &A, const double *Av, const csrk_pattern &L
     }
     // p0 = z0, rho0 = r0.z0 (r0 = b):  zbar = pbar + rhobar_0 b
     LIN3(n, w.zbar, ONE, w.pbar, (Cf{1.0, &S.rhobar[0], nullptr}), b, ONE, nullptr, nullptr, nullptr);
-    CSRK_TRY(Lt(b, w.u));
-    {
-        Bump bw = sub();
-        CSRK_TRY(spmv_bwd(CSRK_F64, CSRK_OP_N, L, Lv, nullptr, nullptr, w.u, w.zbar, w.dAt, w.ubar, bw, s));
-    }
-    LIN3(L.nnz, dL, ONE, dL, ONE, w.dAt, ONE, nullptr, nullptr, nullptr);
-    {
-        Bump bw = sub();
-        CSRK_TRY(spmv_bwd(CSRK_F64, CSRK_OP_T, L, Lv, nullptr, nullptr, b, w.ubar, w.dAt, nullptr, bw, s));
-    }
-    LIN3(L.nnz, dL, ONE, dL, ONE, w.dAt, ONE, nullptr, nullptr, nullptr);
+    CSRK_TRY(applyM(b, w.z));                                  // recompute u_0, z_0
+    CSRK_TRY(adjM(b, w.z, false));
 
     CSRK_CUDA(cudaMemcpyAsync(loss_host, S.loss, sizeof(double), cudaMemcpyDeviceToHost, s));
     if (resid_host) {

@@ -735,6 +735,14 @@ static int sptrsv_bwd_t(const csrk_pattern &A, const T *Av, const csrk_pattern *
     return CSRK_OK;
 }
 
+int trsv_outer(const csrk_pattern &A, const double *w, const double *x, double *dA, cudaStream_t s)
+{
+    if (A.nrows > 0)
+        CSRK_LAUNCH(k_trsv_dT<double>, (unsigned)cdiv(A.nrows, 256), 256, 0, s, A.nrows, A.indptr, A.indices, w, x, 0,
+                    dA);
+    return CSRK_OK;
+}
+
 int sptrsv_fwd(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int upper, int unit, const void *b, void *x,
                Bump &ws, cudaStream_t s)
 {

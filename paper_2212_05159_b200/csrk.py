@@ -70,7 +70,7 @@ def lib() -> ctypes.CDLL:
     L.csrk_spgemm_bwd.argtypes = [I, Pat, P, Pat, P, Pat, P, P, P, P, SZ, P]
     L.csrk_workspace_size.argtypes = [I, I, PatP, PatP, I64, I, ctypes.POINTER(SZ)]
     D = ctypes.c_double
-    L.csrk_pcg_loss_grad.argtypes = [Pat, P, Pat, P, P, I, D, ctypes.POINTER(D), ctypes.POINTER(D), P, P, SZ, P]
+    L.csrk_pcg_loss_grad.argtypes = [Pat, P, Pat, P, P, I, D, I, ctypes.POINTER(D), ctypes.POINTER(D), P, P, SZ, P]
     L.csrk_spadd_symbolic.argtypes = [Pat, Pat, P, P, ctypes.POINTER(I64), P, SZ, P]
     L.csrk_spadd_numeric.argtypes = [I, D, Pat, P, D, Pat, P, Pat, P, P, SZ, P]
     L.csrk_spadd_bwd.argtypes = [I, D, Pat, D, Pat, Pat, P, P, P, P, SZ, P]
@@ -459,20 +459,22 @@ def gcn_layer_bwd(A: CSR, D: torch.Tensor, X: torch.Tensor, Theta: torch.Tensor,
 
 
 def pcg_loss_grad(A: CSR, L: CSR, b: torch.Tensor, n_it: int = 50, gamma: float = 0.6,
-                  dL: torch.Tensor | None = None):
+                  dL: torch.Tensor | None = None, precond: str = "mult"):
     """Config-5 composition (PAPER 4.3): n_it PCG iterations with M = L L^T, the
     weighted residual loss and its gradient w.r.t. L.values.  fp64.
+    precond="solve": M = (L L^T)^{-1} applied by two triangular solves.
     Returns (loss, residual norms ||r^(1..n_it)||, dL on L's pattern)."""
+    pc = {"mult": 0, "solve": 1}[precond]
     if dL is None:
         dL = torch.empty_like(L.values)
     pa, pl = A.pattern(), L.pattern()
     nbytes = ctypes.c_size_t(0)
-    _check(lib().csrk_workspace_size(WS["pcg"], F64, ctypes.byref(pa), ctypes.byref(pl), n_it, 0,
+    _check(lib().csrk_workspace_size(WS["pcg"], F64, ctypes.byref(pa), ctypes.byref(pl), n_it, pc,
                                      ctypes.byref(nbytes)), "workspace_size(pcg)")
     ws = torch.empty(max(int(nbytes.value), 1), dtype=torch.uint8, device=b.device)
     loss = ctypes.c_double(0.0)
     resid = (ctypes.c_double * n_it)()
-    _check(lib().csrk_pcg_loss_grad(pa, _ptr(A.values), pl, _ptr(L.values), _ptr(b), int(n_it), float(gamma),
+    _check(lib().csrk_pcg_loss_grad(pa, _ptr(A.values), pl, _ptr(L.values), _ptr(b), int(n_it), float(gamma), pc,
                                     ctypes.byref(loss), resid, _ptr(dL), _ptr(ws), ws.numel(), _stream()),
            "pcg_loss_grad")
     return float(loss.value), list(resid), dL

@@ -69,10 +69,11 @@ def ck():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("precond", ["mult", "solve"])
 @pytest.mark.parametrize("N,init,n_it,rtol", [(8, "identity", 4, 1e-11), (8, "seeded", 4, 1e-11),
                                               (16, "seeded", 50, 1e-8), (32, "identity", 50, 1e-8),
                                               (40, "seeded", 50, 1e-8)])
-def test_pcg_gpu_vs_oracle(ck, N, init, n_it, rtol):
+def test_pcg_gpu_vs_oracle(ck, N, init, n_it, rtol, precond):
     """Tolerance: max(rtol, 20 x the oracle's own sensitivity), the latter measured by
     re-running the oracle with b perturbed by ~5 ulps (random relative 1e-15) -- n_it chained
     CG steps amplify rounding-level differences (SURVEY c.4: end-to-end 1e-12 is unpinned),
@@ -80,11 +81,11 @@ def test_pcg_gpu_vs_oracle(ck, N, init, n_it, rtol):
     from oracle import pcg
     A, L, b = problem(N, init)
     args = (to_dense(A), pattern_dense(L), to_dense(L), b, n_it, 0.6)
-    loss_ref, res_ref, g_ref = pcg.pcg_loss_grad(*args)
+    loss_ref, res_ref, g_ref = pcg.pcg_loss_grad(*args, precond=precond)
     bp = b * (1.0 + 1e-15 * np.random.default_rng(1).standard_normal(b.shape))
-    loss_alt, res_alt, g_alt = pcg.pcg_loss_grad(args[0], args[1], args[2], bp, n_it, 0.6)
+    loss_alt, res_alt, g_alt = pcg.pcg_loss_grad(args[0], args[1], args[2], bp, n_it, 0.6, precond=precond)
     Ad, Ld = ck.CSR.from_host(A), ck.CSR.from_host(L)
-    loss, res, dL = ck.pcg_loss_grad(Ad, Ld, torch.from_numpy(b).cuda(), n_it, 0.6)
+    loss, res, dL = ck.pcg_loss_grad(Ad, Ld, torch.from_numpy(b).cuda(), n_it, 0.6, precond=precond)
     rows = np.repeat(np.arange(L.nrows), np.diff(L.indptr))
     g, ga = g_ref[rows, L.indices], g_alt[rows, L.indices]
     gscale = np.max(np.abs(g))
@@ -99,22 +100,24 @@ def test_pcg_gpu_vs_oracle(ck, N, init, n_it, rtol):
 
 @pytest.mark.gpu
 @pytest.mark.slow
-def test_pcg_config5_directional_derivative(ck):
+@pytest.mark.parametrize("precond", ["mult", "solve"])
+def test_pcg_config5_directional_derivative(ck, precond):
     """BASELINE config 5 at full size (2D Poisson 4096^2, 50 iterations): the gradient agrees
-    with a central difference of the GPU loss along a random direction of L.values."""
+    with a central difference of the GPU loss along a random direction of L.values (also with
+    M = (L L^T)^{-1} by triangular solves)."""
     A, L, b = problem(4096, "seeded")
     assert A.nnz == 83869696 and L.nnz == 33554431
     Ad, Ld = ck.CSR.from_host(A), ck.CSR.from_host(L)
     bt = torch.from_numpy(b).cuda()
-    loss, res, dL = ck.pcg_loss_grad(Ad, Ld, bt, 50, 0.6)
+    loss, res, dL = ck.pcg_loss_grad(Ad, Ld, bt, 50, 0.6, precond=precond)
     assert np.isfinite(loss) and all(np.isfinite(res))
     V = torch.from_numpy(synth.dense(L.nnz, 77)).cuda()
     h = 1e-6
     base = Ld.values.clone()
     Ld.values.copy_(base + h * V)
-    lp, _, _ = ck.pcg_loss_grad(Ad, Ld, bt, 50, 0.6)
+    lp, _, _ = ck.pcg_loss_grad(Ad, Ld, bt, 50, 0.6, precond=precond)
     Ld.values.copy_(base - h * V)
-    lm, _, _ = ck.pcg_loss_grad(Ad, Ld, bt, 50, 0.6)
+    lm, _, _ = ck.pcg_loss_grad(Ad, Ld, bt, 50, 0.6, precond=precond)
     fd = (lp - lm) / (2 * h)
     dd = float((dL * V).sum())
     assert abs(fd - dd) <= 1e-6 * max(abs(dd), 1e-12), (fd, dd)
