@@ -324,6 +324,48 @@ def run_gcn_workload(args, torch, ck):
                      f"{int(np.diff(G.indptr).max())}), fp32, C = F = 16, fwd + bwd with a cached transpose plan")
 
 
+def run_f12_workload(args, torch, ck):
+    """Sp + Sp (PAPER 3.1.4) and the SPAI loss + gradient (f2, PAPER 4.6) at N = 1:
+    C = 2A - 3L on config 2's 2D Poisson 2048^2 and its lower-bidiagonal L (union pattern), forward
+    and VJP; ||I - M A||_F^2 and d/dM.values for A = 2D Poisson 1024^2 with pattern(M) = pattern(A)
+    (M = mask(A) all ones).  Algorithmic bytes of the SPAI call = those of its constituent
+    ops (M A numeric, I - C, sum of squares, the Sp+Sp VJP, the left SpGEMM VJP)."""
+    dev = torch.device("cuda", 0)
+    s8 = 8
+    pat = lambda m, nnz: 8 * (m + 1) + 4 * nnz
+    A = synth.poisson2d(GRID)
+    L = synth.bidiag_lower(A.nrows, "seeded")
+    Ad, Ld = ck.CSR.from_host(A), ck.CSR.from_host(L)
+    C = ck.spadd_symbolic(Ad, Ld)
+    Cv = torch.empty(C.nnz, dtype=torch.float64, device=dev)
+    dC = torch.from_numpy(synth.dense(C.nnz, 12)).to(dev)
+    dA, dL = torch.empty_like(Ad.values), torch.empty_like(Ld.values)
+    m, na, nl, nc = A.nrows, A.nnz, L.nnz, C.nnz
+    A2 = synth.poisson2d(1024)
+    A2d = ck.CSR.from_host(A2)
+    M = ck.CSR(A2d.nrows, A2d.ncols, A2d.indptr, A2d.indices, torch.ones_like(A2d.values))
+    plan = ck.spai_plan(M, A2d)
+    dM = torch.empty_like(M.values)
+    n2, nz2, nC2, nR2 = A2.nrows, A2.nnz, plan.C.nnz, plan.R.nnz
+    prod2 = int(np.diff(A2.indptr)[A2.indices].sum())
+    spai_bytes = ((pat(n2, nz2) + s8 * nz2) * 2 + 8 * (n2 + 1) + s8 * nC2          # C = M A
+                  + pat(n2, nC2) + s8 * nC2 + pat(n2, nR2) + s8 * nR2               # R = I - C
+                  + s8 * nR2                                                        # sum R^2
+                  + pat(n2, nR2) + s8 * nR2 + s8 * nC2                              # dC from dR
+                  + (pat(n2, nz2) + s8 * nz2) * 2 + pat(n2, nC2) + s8 * nC2 + s8 * nz2)  # dM
+    ops = {
+        "spadd_symbolic": (lambda: ck.spadd_symbolic(Ad, Ld), (pat(m, na) + pat(m, nl) + pat(m, nc), 0)),
+        "spadd_numeric": (lambda: ck.spadd_numeric(2.0, Ad, -3.0, Ld, C, out=Cv),
+                          (pat(m, na) + pat(m, nl) + pat(m, nc) + s8 * (na + nl + nc), 2 * nc)),
+        "spadd_bwd": (lambda: ck.spadd_bwd(2.0, Ad, -3.0, Ld, C, dC, dA=dA, dB=dL),
+                      (pat(m, na) + pat(m, nl) + pat(m, nc) + s8 * (nc + na + nl), na + nl)),
+        "spai_loss_grad": (lambda: ck.spai_loss_grad(plan, M, A2d, dM=dM), (spai_bytes, 6 * prod2)),
+    }
+    return _time_ops(args, torch, ck, ops, "Sp+Sp and SPAI fwd+bwd algorithmic GB/s", "f64",
+                     "Sp+Sp: 2 A - 3 L, A = 2D Poisson 2048^2, L lower bidiagonal (fwd + VJP); SPAI: ||I - M A||_F^2 "
+                     "+ gradient, A = 2D Poisson 1024^2, pattern(M) = pattern(A)")
+
+
 def _time_ops(args, torch, ck, ops, metric, dtype, workload):
     """Time a dict name -> (fn, (bytes, flops)) op by op: CUDA events on the current stream,
     L2 flushed (512 MiB write) before every op, median over --steps."""
@@ -594,7 +636,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5", "trsv", "gcn"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5", "trsv", "gcn", "f12"])
     ap.add_argument("--precond", default="mult", choices=["mult", "solve"], help="cfg5: M = L L^T or (L L^T)^-1")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -611,6 +653,8 @@ def main():
         return run_trsv_workload(args, torch, ck)
     if args.workload == "gcn":
         return run_gcn_workload(args, torch, ck)
+    if args.workload == "f12":
+        return run_f12_workload(args, torch, ck)
     if args.workload in ("cfg3", "cfg4"):
         return run_ops_workload(args, torch, ck, int(args.workload[-1]))
 
