@@ -317,17 +317,21 @@ __global__ __launch_bounds__(kCarryTPB) void k_trsv_carry(TrsvArgs<T> a, int64_t
 // every awaited tile is resident or finished.
 enum { CH_NONE = 0, CH_AGG = 1, CH_INCL = 2, CH_ABORT = 3 };
 constexpr int kLbTPB = 256;
-constexpr int kLbTile = kLbTPB * kChPer;
+#ifndef CSRK_LB_PER
+#define CSRK_LB_PER 8
+#endif
+constexpr int kLbPer = CSRK_LB_PER;  // rows per thread (A/B via CSRK_NVCC_EXTRA)
+constexpr int kLbTile = kLbTPB * kLbPer;
 
 template <typename T>
-__device__ __forceinline__ bool chain_rows_reg(const TrsvArgs<T> &a, int64_t o0, double (&lv)[kChPer],
-                                               double (&dv)[kChPer], double (&bv)[kChPer])
+__device__ __forceinline__ bool chain_rows_reg(const TrsvArgs<T> &a, int64_t o0, double (&lv)[kLbPer],
+                                               double (&dv)[kLbPer], double (&bv)[kLbPer])
 {
     const int64_t n = a.n;
     bool bad = false;
-    int64_t rs[kChPer], re[kChPer];
+    int64_t rs[kLbPer], re[kLbPer];
 #pragma unroll
-    for (int r = 0; r < kChPer; ++r) {
+    for (int r = 0; r < kLbPer; ++r) {
         const int64_t o = o0 + r;
         const int64_t i = a.upper ? n - 1 - o : o;
         rs[r] = re[r] = 0;
@@ -339,7 +343,7 @@ __device__ __forceinline__ bool chain_rows_reg(const TrsvArgs<T> &a, int64_t o0,
         }
     }
 #pragma unroll
-    for (int r = 0; r < kChPer; ++r) {
+    for (int r = 0; r < kLbPer; ++r) {
         const int64_t o = o0 + r;
         const int64_t len = re[r] - rs[r];
         bad |= len > 2;
@@ -393,8 +397,8 @@ __global__ __launch_bounds__(kLbTPB, CSRK_LB_MINB) void k_trsv_chain_lb(TrsvArgs
         if (tid == 0) st_release(&a.status[tile], CH_ABORT);
         return;
     }
-    const int64_t o0 = (int64_t)tile * kLbTile + (int64_t)tid * kChPer;
-    double lv[kChPer], dv[kChPer], bv[kChPer];
+    const int64_t o0 = (int64_t)tile * kLbTile + (int64_t)tid * kLbPer;
+    double lv[kLbPer], dv[kLbPer], bv[kLbPer];
     const bool bad = chain_rows_reg(a, o0, lv, dv, bv);
     if (__syncthreads_or(bad)) {
         if (tid == 0) {
@@ -405,7 +409,7 @@ __global__ __launch_bounds__(kLbTPB, CSRK_LB_MINB) void k_trsv_chain_lb(TrsvArgs
     }
     double mA = 1.0, mC = 0.0;
 #pragma unroll
-    for (int r = 0; r < kChPer; ++r) {
+    for (int r = 0; r < kLbPer; ++r) {
         if (o0 + r < n) {
             const double rd = 1.0 / dv[r];
             const double ar = -lv[r] * rd, cr = bv[r] * rd;
@@ -506,7 +510,7 @@ __global__ __launch_bounds__(kLbTPB, CSRK_LB_MINB) void k_trsv_chain_lb(TrsvArgs
     if (s_abort) return;
     double xp = tid == 0 ? s_xin : tA * s_xin + tC;
 #pragma unroll
-    for (int r = 0; r < kChPer; ++r) {
+    for (int r = 0; r < kLbPer; ++r) {
         const int64_t o = o0 + r;
         if (o < n) {
             const T xi = (T)((bv[r] - lv[r] * xp) / dv[r]);
