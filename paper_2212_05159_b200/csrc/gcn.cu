@@ -259,7 +259,7 @@ __global__ __launch_bounds__(kGcnTPB) void k_rowgemm(int64_t n, int64_t C, int64
 template <typename T>
 __global__ __launch_bounds__(kGcnTPB) void k_gemm_tn(int64_t n, int64_t C, int64_t F, const T *__restrict__ X,
                                                      int64_t ldx, const T *__restrict__ dZ, int64_t lddz,
-                                                     double *__restrict__ acc, int vec)
+                                                     double *__restrict__ acc)
 {
     extern __shared__ __align__(16) unsigned char s_raw[];
     double *s_part = reinterpret_cast<double *>(s_raw);  // C x F partials of this CTA
@@ -276,27 +276,12 @@ __global__ __launch_bounds__(kGcnTPB) void k_gemm_tn(int64_t n, int64_t C, int64
         double a[kGemmChunk];
 #pragma unroll
         for (int q = 0; q < kGemmChunk; ++q) a[q] = 0.0;
-        if (vec) {  // fp32, F % 16 == 0, 16-byte aligned dZ rows: four float4 loads per row
-            for (int64_t r = r0 + slot; r < r1; r += slots) {
-                const double x = (double)X[r * ldx + cc];
-                const float4 *z = reinterpret_cast<const float4 *>(dZ + r * lddz + f0);
+        for (int64_t r = r0 + slot; r < r1; r += slots) {
+            const double x = (double)X[r * ldx + cc];
+            const T *z = dZ + r * lddz + f0;
 #pragma unroll
-                for (int q4 = 0; q4 < kGemmChunk / 4; ++q4) {
-                    const float4 v = z[q4];
-                    a[4 * q4] = fma(x, (double)v.x, a[4 * q4]);
-                    a[4 * q4 + 1] = fma(x, (double)v.y, a[4 * q4 + 1]);
-                    a[4 * q4 + 2] = fma(x, (double)v.z, a[4 * q4 + 2]);
-                    a[4 * q4 + 3] = fma(x, (double)v.w, a[4 * q4 + 3]);
-                }
-            }
-        } else {
-            for (int64_t r = r0 + slot; r < r1; r += slots) {
-                const double x = (double)X[r * ldx + cc];
-                const T *z = dZ + r * lddz + f0;
-#pragma unroll
-                for (int q = 0; q < kGemmChunk; ++q)
-                    if (f0 + q < F) a[q] = fma(x, (double)z[q], a[q]);
-            }
+            for (int q = 0; q < kGemmChunk; ++q)
+                if (f0 + q < F) a[q] = fma(x, (double)z[q], a[q]);
         }
 #pragma unroll
         for (int q = 0; q < kGemmChunk; ++q)
@@ -438,9 +423,8 @@ static int gemm_tn_t(int64_t n, int64_t C, int64_t F, const T *X, int64_t ldx, c
     const size_t smem = sizeof(double) * (size_t)(C * F);
     if (smem > 48 * 1024) CSRK_CUDA(cudaFuncSetAttribute(k_gemm_tn<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                          (int)smem));
-    const int vec = 0;  // the float4 path measured slower here (0.21 vs 0.18 ms, GCN bench)
-    if (n > 0)
-        CSRK_LAUNCH(k_gemm_tn<T>, (unsigned)(kNumSMs * 4), kGcnTPB, smem, s, n, C, F, X, ldx, dZ, lddz, acc, vec);
+    // (float4 loads of dZ measured slower here: 0.21 vs 0.18 ms on the GCN bench)
+    if (n > 0) CSRK_LAUNCH(k_gemm_tn<T>, (unsigned)(kNumSMs * 4), kGcnTPB, smem, s, n, C, F, X, ldx, dZ, lddz, acc);
     CSRK_LAUNCH(k_to_dtype<T>, (unsigned)cdiv(C * F, 256), 256, 0, s, C * F, acc, dW);
     return CSRK_OK;
 }
