@@ -270,8 +270,10 @@ def run_trsv_workload(args, torch, ck):
     for k, ev in times.items():
         ms = float(np.median([a.elapsed_time(e) for a, e in ev]))
         b, fl = ops[k][1]
+        all_ms = [a.elapsed_time(e) for a, e in ev]
         rep[k] = {"ms": round(ms, 4), "GB/s": round(b / ms / 1e6, 1), "GFLOP/s": round(fl / ms / 1e6, 1),
-                  "frac": round(b / ms / 1e6 / peak, 3), "bytes": b}
+                  "frac": round(b / ms / 1e6 / peak, 3), "bytes": b, "ms_min": round(float(np.min(all_ms)), 4),
+                  "ms_p90": round(float(np.percentile(all_ms, 90)), 4)}
         tot_b, tot_f, tot_ms = tot_b + b, tot_f + fl, tot_ms + ms
     dom = max(rep, key=lambda k: rep[k]["ms"])
     out = {"metric": "SpTRSV fwd+bwd algorithmic GB/s", "value": round(tot_b / tot_ms / 1e6, 2), "unit": "GB/s",
@@ -394,8 +396,10 @@ def _time_ops(args, torch, ck, ops, metric, dtype, workload):
     for k, ev in times.items():
         ms = float(np.median([a.elapsed_time(e) for a, e in ev]))
         b, fl = ops[k][1]
+        all_ms = [a.elapsed_time(e) for a, e in ev]
         rep[k] = {"ms": round(ms, 4), "GB/s": round(b / ms / 1e6, 1), "GFLOP/s": round(fl / ms / 1e6, 1),
-                  "frac": round(b / ms / 1e6 / peak, 3), "bytes": b}
+                  "frac": round(b / ms / 1e6 / peak, 3), "bytes": b, "ms_min": round(float(np.min(all_ms)), 4),
+                  "ms_p90": round(float(np.percentile(all_ms, 90)), 4)}
         tot_b, tot_f, tot_ms = tot_b + b, tot_f + fl, tot_ms + ms
     dom = max(rep, key=lambda k: rep[k]["ms"])
     out = {"metric": metric, "value": round(tot_b / tot_ms / 1e6, 2), "unit": "GB/s", "n_gpus": 1,
@@ -751,6 +755,8 @@ def main():
                           "rows_per_gpu": W.m, "nnz_per_gpu": W.nnz, "nnzC_per_gpu": W.nnzC, "k": K,
                           "l2": "flushed (512 MiB write) between timed steps",
                           "parallelism": f"rowblock{world}"},
+               "step_ms_stats": {"median": round(float(np.median(step_ms)), 4), "min": round(float(np.min(step_ms)), 4),
+                                 "p90": round(float(np.percentile(step_ms, 90)), 4)},
                "gflops": round(step_flops * world / (ms_per_step * 1e-3) / 1e9, 2),
                "step_bytes_per_gpu": step_bytes,
                "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
