@@ -95,8 +95,11 @@ __device__ __forceinline__ void gcn_finish(const GcnArgs<T> &a, int64_t i, int64
     }
 }
 
+#ifndef CSRK_GCN_MINB
+#define CSRK_GCN_MINB 1
+#endif
 template <typename T, int G>
-__global__ __launch_bounds__(kGcnTPB) void k_gcn_prop(GcnArgs<T> a)
+__global__ __launch_bounds__(kGcnTPB, CSRK_GCN_MINB) void k_gcn_prop(GcnArgs<T> a)
 {
     const int lane = threadIdx.x & 31;
     const int sub = lane % G;            // lane within the row group

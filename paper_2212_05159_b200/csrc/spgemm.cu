@@ -425,8 +425,11 @@ __device__ __forceinline__ void w_sort_fill(const int32_t *key, int w, int32_t *
     }
 }
 
+#ifndef CSRK_W_MINB
+#define CSRK_W_MINB 1
+#endif
 template <typename T, int PH, bool W2 = false>
-__global__ __launch_bounds__(kWTPB) void k_gemm_W(BigList wl, BigList big, BigList w2l, const int64_t *__restrict__ Ap,
+__global__ __launch_bounds__(kWTPB, CSRK_W_MINB) void k_gemm_W(BigList wl, BigList big, BigList w2l, const int64_t *__restrict__ Ap,
                                                   const int32_t *__restrict__ Ai, const T *__restrict__ Av,
                                                   const int64_t *__restrict__ Bp, const int32_t *__restrict__ Bi,
                                                   const T *__restrict__ Bv, int64_t *__restrict__ Cp,

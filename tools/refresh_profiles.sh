@@ -8,7 +8,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e \
   > gpurun_out/ncu_bench.log 2>&1
 timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1
-for w in cfg3 cfg4 cfg5 trsv gcn; do
+for w in cfg3 cfg4 cfg5 trsv gcn f12; do
   timeout 900 python bench.py --workload $w --steps 5 > gpurun_out/bench_$w.log 2>&1
 done
 tail -c 400 gpurun_out/bench_default.log
