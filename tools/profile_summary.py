@@ -23,10 +23,14 @@ OP_OF = [  # (substring of the kernel name, op) -- order of the step in bench.py
     ("k_rows<double, 1, 0, 1>", "spmv_bwd"), ("k_rows_long<double, 1, 0, 1>", "spmv_bwd"),
     ("k_spmm<double, 8, 4, 0>", "spmm_fwd"), ("k_spmm<double, 8, 4, 3>", "spmm_bwd"),
     ("k_spmm_wide<double, 2, 0", "spmm_fwd"), ("k_spmm_wide<double, 2, 3", "spmm_bwd"),
-    ("k_gemm_S<double, 0>", "spgemm_symbolic"), ("k_gemm_big_sym<0>", "spgemm_symbolic"),
-    ("k_gemm_S<double, 1>", "spgemm_symbolic"), ("k_gemm_big_sym<1>", "spgemm_symbolic"),
-    ("k_gemm_S<double, 2>", "spgemm_numeric"), ("k_gemm_big_val<double, 2>", "spgemm_numeric"),
-    ("k_gemm_S<double, 3>", "spgemm_bwd"), ("k_gemm_big_val<double, 3>", "spgemm_bwd"),
+    ("k_gemm_S<double, 0,", "spgemm_symbolic"), ("k_gemm_W<double, 0,", "spgemm_symbolic"),
+    ("k_gemm_big_sym<0,", "spgemm_symbolic"),
+    ("k_gemm_S<double, 1,", "spgemm_symbolic"), ("k_gemm_W<double, 1,", "spgemm_symbolic"),
+    ("k_gemm_big_sym<1,", "spgemm_symbolic"),
+    ("k_gemm_S<double, 2,", "spgemm_numeric"), ("k_gemm_W<double, 2,", "spgemm_numeric"),
+    ("k_gemm_big_val<double, 2>", "spgemm_numeric"),
+    ("k_gemm_S<double, 3,", "spgemm_bwd"), ("k_gemm_W<double, 3,", "spgemm_bwd"),
+    ("k_gemm_big_val<double, 3>", "spgemm_bwd"),
 ]
 
 
@@ -51,15 +55,14 @@ def main(src, dst):
     starts = [i for i, ((_, n), _) in enumerate(launches) if "k_col_count" in n]
     step = launches[starts[-1]:] if starts else launches
     ops = collections.OrderedDict()
-    scans_to = "csr_transpose"
+    cur = "csr_transpose"  # helper kernels (scans, big-row prep, zero fills) go to the op they sit in
     for (lid, name), m in step:
         op = next((o for s, o in OP_OF if s in name), None)
-        if op is None and "k_scan" in name:
-            op = scans_to
         if op is None:
-            continue
-        if op == "spgemm_symbolic":
-            scans_to = "spgemm_symbolic"
+            if not name.startswith(("csrk::", "void csrk::")):
+                continue
+            op = cur
+        cur = op
         d = ops.setdefault(op, {"kernels": [], "time_us": 0.0, "dram_bytes": 0.0})
         t = m.get("gpu__time_duration.sum", 0.0) / 1e3
         b = m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
