@@ -25,12 +25,30 @@ extern std::atomic<uint64_t> g_launches;
         if ((expr) != cudaSuccess) return CSRK_ERR_CUDA;        \
     } while (0)
 
+// Programmatic dependent launch (PDL): every kernel is launched with programmatic stream
+// serialization, so its CTAs may be scheduled while the previous kernel on the stream drains,
+// and every kernel begins with pdl_wait() (griddepcontrol.wait), which blocks until that
+// previous grid has completed and its writes are visible.  The launch latency of kernel N+1
+// overlaps the tail of kernel N; the data dependence is unchanged.  CSRK_PDL=0 disables it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+bool pdl_enabled();
+
 // Launch a kernel, count it, and surface launch-configuration errors.
-#define CSRK_LAUNCH(kernel, grid, block, smem, stream, ...)                      \
+#define CSRK_LAUNCH(kernel, grid_, block_, smem_, stream_, ...)                    \
     do {                                                                         \
-        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);              \
+        cudaLaunchConfig_t _cfg = {};                                            \
+        _cfg.gridDim = dim3(grid_);                                               \
+        _cfg.blockDim = dim3(block_);                                            \
+        _cfg.dynamicSmemBytes = (size_t)(smem_);                                \
+        _cfg.stream = (stream_);                                                  \
+        cudaLaunchAttribute _attr[1];                                            \
+        _attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;        \
+        _attr[0].val.programmaticStreamSerializationAllowed = 1;                 \
+        _cfg.attrs = _attr;                                                      \
+        _cfg.numAttrs = ::csrk::pdl_enabled() ? 1 : 0;                           \
+        const cudaError_t _e = cudaLaunchKernelEx(&_cfg, kernel, __VA_ARGS__);   \
         ::csrk::g_launches.fetch_add(1, std::memory_order_relaxed);              \
-        if (cudaPeekAtLastError() != cudaSuccess) {                              \
+        if (_e != cudaSuccess) {                                                 \
             (void)cudaGetLastError();                                            \
             return CSRK_ERR_CUDA;                                                \
         }                                                                        \

@@ -28,6 +28,7 @@ __global__ __launch_bounds__(256) void k_gcn_deg(int64_t n, const int64_t *__res
                                                  const float *__restrict__ vf, const double *__restrict__ vd,
                                                  double *__restrict__ D)
 {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool valid = i < n;
@@ -101,6 +102,7 @@ __device__ __forceinline__ void gcn_finish(const GcnArgs<T> &a, int64_t i, int64
 template <typename T, int G>
 __global__ __launch_bounds__(kGcnTPB, CSRK_GCN_MINB) void k_gcn_prop(GcnArgs<T> a)
 {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const int sub = lane % G;            // lane within the row group
     const int64_t c = (int64_t)sub * kV; // first column of this lane
@@ -131,6 +133,7 @@ __global__ __launch_bounds__(kGcnTPB, CSRK_GCN_MINB) void k_gcn_prop(GcnArgs<T> 
 template <typename T, int G>
 __global__ __launch_bounds__(kGcnTPB) void k_gcn_prop_long(GcnArgs<T> a)
 {
+    pdl_wait();
     __shared__ double s_part[kGcnTPB / 32][32 * kV];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, sub = lane % G;
     const int grp = threadIdx.x / G;
@@ -177,6 +180,7 @@ template <typename T>
 __global__ __launch_bounds__(kGcnTPB) void k_colsum(int64_t n, int64_t F, const T *__restrict__ Y, int64_t ld,
                                                     double *__restrict__ acc)
 {
+    pdl_wait();
     const int64_t rows_per = (n + gridDim.x - 1) / gridDim.x;
     const int64_t r0 = (int64_t)blockIdx.x * rows_per, r1 = r0 + rows_per < n ? r0 + rows_per : n;
     const int64_t lanes = kGcnTPB - kGcnTPB % F;  // threads (row slot, column)
@@ -197,6 +201,7 @@ __global__ __launch_bounds__(kGcnTPB) void k_colsum(int64_t n, int64_t F, const 
 template <typename T>
 __global__ void k_to_dtype(int64_t m, const double *__restrict__ a, T *__restrict__ out)
 {
+    pdl_wait();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < m) out[i] = (T)a[i];
 }
@@ -211,6 +216,7 @@ __global__ __launch_bounds__(kGcnTPB) void k_rowgemm(int64_t n, int64_t C, int64
                                                      int64_t ldx, const T *__restrict__ W, int transW,
                                                      T *__restrict__ Z, int64_t ldz, int vec)
 {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char s_raw[];
     double *sW = reinterpret_cast<double *>(s_raw);  // C x F, [c * F + f]
     for (int64_t q = threadIdx.x; q < C * F; q += kGcnTPB) {
@@ -264,6 +270,7 @@ __global__ __launch_bounds__(kGcnTPB) void k_gemm_tn(int64_t n, int64_t C, int64
                                                      int64_t ldx, const T *__restrict__ dZ, int64_t lddz,
                                                      double *__restrict__ acc)
 {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char s_raw[];
     double *s_part = reinterpret_cast<double *>(s_raw);  // C x F partials of this CTA
     const int64_t nch = (F + kGemmChunk - 1) / kGemmChunk;

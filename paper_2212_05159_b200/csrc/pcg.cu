@@ -56,6 +56,7 @@ __global__ __launch_bounds__(kVecTPB) void k_lin3(int64_t n, double *out, Cf a, 
                                                   const double *y, Cf c, const double *z, const double *w,
                                                   double *part)
 {
+    pdl_wait();
     const double ca = cfv(a), cb = cfv(b), cc = cfv(c);
     double acc = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)kVecTPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * kVecTPB) {
@@ -74,6 +75,7 @@ __global__ __launch_bounds__(kVecTPB) void k_lin3(int64_t n, double *out, Cf a, 
 
 __global__ __launch_bounds__(kVecTPB) void k_dot(int64_t n, const double *x, const double *y, double *part)
 {
+    pdl_wait();
     double acc = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)kVecTPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * kVecTPB)
         acc = fma(x[i], y[i], acc);
@@ -84,6 +86,7 @@ __global__ __launch_bounds__(kVecTPB) void k_dot(int64_t n, const double *x, con
 // dst = sign * sum part[0..nb)  (fixed order)
 __global__ __launch_bounds__(kVecTPB) void k_finish(const double *part, int nb, double *dst, double sign)
 {
+    pdl_wait();
     double acc = 0.0;
     for (int i = threadIdx.x; i < nb; i += kVecTPB) acc += part[i];
     const double t = block_sum(acc);
@@ -103,6 +106,7 @@ struct Scal {         // device scalar layout
 
 __global__ void k_loss(Scal S, int N, double gamma)
 {
+    pdl_wait();
     double wsum = 0.0;
     for (int j = 1; j <= N; ++j) wsum += pow(gamma, (double)(N - j));
     const double nb = sqrt(*S.bb);
@@ -121,6 +125,7 @@ __global__ void k_loss(Scal S, int N, double gamma)
 // beta_i = rho_i / rho_{i-1}:  rhobar_i += betabar / rho_{i-1};  rhobar_{i-1} -= betabar rho_i / rho_{i-1}^2
 __global__ void k_bwd_beta(Scal S, int i)
 {
+    pdl_wait();
     const double bb = *S.betabar, rm = S.rho[i - 1];
     S.rhobar[i] += bb / rm;
     S.rhobar[i - 1] -= bb * S.rho[i] / (rm * rm);
@@ -129,6 +134,7 @@ __global__ void k_bwd_beta(Scal S, int i)
 // alpha_i = rho_{i-1} / s_i:  rhobar_{i-1} += alphabar / s_i;  sbar = -alphabar rho_{i-1} / s_i^2
 __global__ void k_bwd_alpha(Scal S, int i)
 {
+    pdl_wait();
     const double ab = *S.alphabar, si = S.s[i];
     S.rhobar[i - 1] += ab / si;
     *S.sbar = -ab * S.rho[i - 1] / (si * si);

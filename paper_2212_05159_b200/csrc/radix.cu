@@ -26,6 +26,7 @@ constexpr int kRsBins = 256;
 __global__ __launch_bounds__(256) void k_rs_rows(int64_t m, const int64_t *__restrict__ indptr,
                                                  int32_t *__restrict__ rows)
 {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t s = 0, e = 0;
@@ -55,6 +56,7 @@ __device__ __forceinline__ int64_t rs_item(int64_t tile, int warp, int r, int la
 __global__ __launch_bounds__(kRsTPB) void k_rs_up(int64_t nnz, int64_t ntiles, int shift,
                                                   const int32_t *__restrict__ keys, int64_t *__restrict__ cnt)
 {
+    pdl_wait();
     __shared__ int s_h[kRsBins];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t tile = blockIdx.x;
@@ -83,6 +85,7 @@ __global__ __launch_bounds__(kRsTPB, CSRK_RS_MINB) void k_rs_down(int64_t nnz, i
                                                     int32_t *__restrict__ kout, uint64_t *__restrict__ vout,
                                                     int32_t *__restrict__ ATi, int64_t *__restrict__ perm)
 {
+    pdl_wait();
     __shared__ int s_w[kRsWarps][kRsBins];  // per-warp digit counts, then per-warp prefixes
     __shared__ int64_t s_base[kRsBins];
     __shared__ int s_tot[kRsBins], s_start[kRsBins];
@@ -184,6 +187,7 @@ __global__ __launch_bounds__(kRsTPB, CSRK_RS_MINB) void k_rs_down(int64_t nnz, i
 // AT_indptr from the sorted columns: ATp[c] = first position with column >= c
 __global__ void k_rs_indptr(int64_t nnz, int64_t n, const int32_t *__restrict__ keys, int64_t *__restrict__ ATp)
 {
+    pdl_wait();
     const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (q > nnz) return;
     const int64_t c = q < nnz ? keys[q] : n;

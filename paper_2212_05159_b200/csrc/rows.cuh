@@ -56,6 +56,7 @@ __device__ __forceinline__ void row_elem(const TileArgs<T> &a, int64_t row, int6
 template <typename T, int MODE, bool PERM, bool SIDE>
 __global__ __launch_bounds__(kRowsTPB, 8) void k_rows(TileArgs<T> a, RowList L)
 {
+    pdl_wait();
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const int64_t row = (int64_t)blockIdx.x * kRowsTPB + threadIdx.x;
@@ -165,6 +166,7 @@ constexpr int kLongTPB = 256;
 template <typename T, int MODE, bool PERM, bool SIDE>
 __global__ __launch_bounds__(kLongTPB) void k_rows_long(TileArgs<T> a, RowList L)
 {
+    pdl_wait();
     __shared__ double s_red[kLongTPB / 32];
     const int n = *(volatile int *)L.count;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;

@@ -62,6 +62,7 @@ __device__ __forceinline__ int add_merge(const AddArgs<T> &g, const int32_t *ai,
 template <typename T, int PH>
 __global__ __launch_bounds__(kATile) void k_spadd(AddArgs<T> g)
 {
+    pdl_wait();
     __shared__ int64_t s_ap[kATile + 1], s_bp[kATile + 1], s_cp[kATile + 1];
     __shared__ int32_t s_ai[kACapAB], s_bi[kACapAB];
     constexpr bool VAL = PH == AD_NUM || PH == AD_BWD;

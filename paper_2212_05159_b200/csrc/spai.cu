@@ -30,12 +30,14 @@ __device__ __forceinline__ double sq_block_sum(double v)
 
 __global__ __launch_bounds__(kSqTPB) void k_ones(int64_t n, double *x)
 {
+    pdl_wait();
     for (int64_t i = blockIdx.x * (int64_t)kSqTPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * kSqTPB) x[i] = 1.0;
 }
 
 // part[blk] = sum r_i^2 over the block's grid-stride share;  d_i = 2 r_i
 __global__ __launch_bounds__(kSqTPB) void k_sumsq_scale(int64_t n, const double *r, double *d, double *part)
 {
+    pdl_wait();
     double acc = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)kSqTPB + threadIdx.x; i < n; i += (int64_t)gridDim.x * kSqTPB) {
         const double v = r[i];
@@ -48,6 +50,7 @@ __global__ __launch_bounds__(kSqTPB) void k_sumsq_scale(int64_t n, const double 
 
 __global__ __launch_bounds__(kSqTPB) void k_sum_final(const double *part, int nb, double *dst)
 {
+    pdl_wait();
     double acc = 0.0;
     for (int i = threadIdx.x; i < nb; i += kSqTPB) acc += part[i];
     const double t = sq_block_sum(acc);

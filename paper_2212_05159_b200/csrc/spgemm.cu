@@ -229,6 +229,7 @@ __global__ __launch_bounds__(kSTPB, kSMinBlocks) void k_gemm_S(int64_t m, const 
                                                   const T *__restrict__ dC, T *__restrict__ dA, T *__restrict__ dB,
                                                   BigList wl, BigList big, int use_stage)
 {
+    pdl_wait();
     // per-warp staging buffers in dynamic shared memory (none when use_stage == 0, which
     // leaves the whole carve-out to L1 for the merge's list reads)
     constexpr int BUFB = (PH == PH_FILL) ? (int)sizeof(int32_t) * kSBuf : (int)sizeof(T) * kSBuf;
@@ -436,6 +437,7 @@ __global__ __launch_bounds__(kWTPB, CSRK_W_MINB) void k_gemm_W(BigList wl, BigLi
                                                   int32_t *__restrict__ Ci, T *__restrict__ Cv,
                                                   const T *__restrict__ dC, T *__restrict__ dA, T *__restrict__ dB)
 {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char s_dyn[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int WW = W2 ? kW2W : kWW;
@@ -685,6 +687,7 @@ __device__ __forceinline__ int64_t big_list_of(const int64_t *loff, int64_t lo, 
 __global__ __launch_bounds__(kGemmTPB) void k_big_prep(BigRows br, const int64_t *__restrict__ Ap,
                                                        const int32_t *__restrict__ Ai, const int64_t *__restrict__ Bp)
 {
+    pdl_wait();
     __shared__ int64_t s_red[kGemmTPB / 32];
     const int n = *(volatile const int *)br.count;
     for (int r = blockIdx.x; r < n; r += gridDim.x) {
@@ -712,6 +715,7 @@ constexpr int kItemsTPB = 1024;
 // single CTA: items[r] = sum_{r' < r} ceil(w_r' / kItem), items[n] = total
 __global__ __launch_bounds__(kItemsTPB) void k_big_items(BigRows br)
 {
+    pdl_wait();
     __shared__ int64_t s_w[kItemsTPB / 32];
     const int n = *(volatile const int *)br.count;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -769,6 +773,7 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_sym(BigRows br, int64_t n
                                                            const int32_t *__restrict__ Bi, int64_t *__restrict__ Cp,
                                                            int32_t *__restrict__ Ci)
 {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char smem[];
     int32_t *s_key = reinterpret_cast<int32_t *>(smem);   // kMMaxW keys (sort path)
     uint32_t *bm = reinterpret_cast<uint32_t *>(smem);    // kBitmapWords (bitmap path)
@@ -849,6 +854,7 @@ __global__ __launch_bounds__(kGemmTPB) void k_big_zero(BigRows br, const int64_t
                                                        const int64_t *__restrict__ Cp, T *__restrict__ Cv,
                                                        T *__restrict__ dA)
 {
+    pdl_wait();
     const int n = *(volatile const int *)br.count;
     for (int r = blockIdx.x; r < n; r += gridDim.x) {
         const int64_t i = br.rows[r];
@@ -872,6 +878,7 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_val(BigRows br, const int
                                                            const T *__restrict__ dC, T *__restrict__ dA,
                                                            T *__restrict__ dB)
 {
+    pdl_wait();
     __shared__ int32_t s_col[kValSm];
     __shared__ double s_acc[kValSm];
     const int n = *(volatile const int *)br.count;

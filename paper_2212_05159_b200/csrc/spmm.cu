@@ -230,6 +230,7 @@ __device__ __forceinline__ void spmm_rows(const SpmmArgs<T> &a, const int64_t *s
 template <typename T, int G, int W, int MODE>
 __global__ __launch_bounds__(kSpmmTPB, MODE == SP_FUSED_T ? 4 : 5) void k_spmm(SpmmArgs<T> a)
 {
+    pdl_wait();
     constexpr int NG = kSpmmTPB / G;           // groups per CTA
     constexpr int RT = NG * kSpmmRPG;          // rows per tile
     constexpr bool PERM = MODE == SP_FWD_PERM || MODE == SP_FUSED_T;
@@ -278,6 +279,7 @@ static int launch_spmm(const SpmmArgs<T> &a, cudaStream_t s)
 template <typename T, int G, int W, bool PERM>
 __global__ __launch_bounds__(256) void k_spmm_lean(SpmmArgs<T> a)
 {
+    pdl_wait();
     const int lane = threadIdx.x % G;
     const int64_t ngroups = (int64_t)gridDim.x * (256 / G);
     const int npass = (int)((a.k + kPass - 1) / kPass);
@@ -316,6 +318,7 @@ constexpr int kBulkBytes = 40 * 1024;
 template <typename T>
 __global__ __launch_bounds__(kBulkTPB) void k_spmm_bulk(SpmmArgs<T> a, int cap, int64_t ntiles)
 {
+    pdl_wait();
     constexpr int W = 4;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ int64_t s_ptr[2][kBulkRT + 1];
@@ -455,6 +458,7 @@ template <int MODE> constexpr int band_cap() { return wide_tpb<MODE>() / kWG * k
 template <typename T, int NV, int MODE, bool BAND>
 __global__ __launch_bounds__(wide_tpb<MODE>(), wide_minb<MODE>()) void k_spmm_wide(SpmmArgs<T> a)
 {
+    pdl_wait();
     constexpr int kWTPB = wide_tpb<MODE>();
     constexpr int kWRT = kWTPB / kWG * kWRPG;
     constexpr int kBandCap = band_cap<MODE>();

@@ -206,6 +206,7 @@ __device__ __forceinline__ void chain_block_scan(double mA, double mC, double &t
 template <typename T, bool APPLY>
 __global__ __launch_bounds__(kChTPB, 4) void k_trsv_chain(TrsvArgs<T> a)
 {
+    pdl_wait();
     if (APPLY && *(volatile int *)a.abort) return;
     const int tid = threadIdx.x;
     const int tile = blockIdx.x;
@@ -265,6 +266,7 @@ constexpr int kCarryTPB = 1024;
 template <typename T>
 __global__ __launch_bounds__(kCarryTPB) void k_trsv_carry(TrsvArgs<T> a, int64_t ntiles)
 {
+    pdl_wait();
     if (*(volatile int *)a.abort) return;
     __shared__ double s_A[kCarryTPB / 32], s_C[kCarryTPB / 32];
     const unsigned FULL = 0xffffffffu;
@@ -381,6 +383,7 @@ template <typename T>
 #endif
 __global__ __launch_bounds__(kLbTPB, CSRK_LB_MINB) void k_trsv_chain_lb(TrsvArgs<T> a)
 {
+    pdl_wait();
     __shared__ int s_tile, s_abort;
     __shared__ double s_wA[kLbTPB / 32], s_wC[kLbTPB / 32];
     __shared__ double s_xin;
@@ -524,6 +527,7 @@ __global__ __launch_bounds__(kLbTPB, CSRK_LB_MINB) void k_trsv_chain_lb(TrsvArgs
 template <typename T>
 __global__ void k_trsv_prep(TrsvArgs<T> a)
 {
+    pdl_wait();
     if (*(volatile int *)a.abort == 0) return;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x)
         a.ready[i] = 0;
@@ -533,6 +537,7 @@ __global__ void k_trsv_prep(TrsvArgs<T> a)
 template <typename T>
 __global__ __launch_bounds__(kSfTPB) void k_trsv_sf(TrsvArgs<T> a)
 {
+    pdl_wait();
     if (*(volatile int *)a.abort == 0) return;  // the chain pass solved it
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
@@ -633,6 +638,7 @@ template <typename T>
 __global__ void k_trsv_dT(int64_t n, const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
                           const T *__restrict__ w, const T *__restrict__ x, int unit, T *__restrict__ dT)
 {
+    pdl_wait();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double wi = (double)w[i];

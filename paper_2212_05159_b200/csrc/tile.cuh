@@ -82,6 +82,7 @@ __device__ __forceinline__ int64_t tile_merge_rows(int64_t d, int64_t nr, int64_
 template <typename T, int MODE, bool PERM, bool SIDE>
 __global__ __launch_bounds__(kTileTPB) void k_csr_tile(TileArgs<T> a)
 {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr bool NEED_ROW = SIDE || MODE != MODE_REDUCE;
     constexpr bool NEED_U = SIDE || MODE == MODE_SCATTER;

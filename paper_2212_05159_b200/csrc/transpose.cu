@@ -31,6 +31,7 @@ __device__ __forceinline__ int64_t key_pos(uint64_t k) { return (int64_t)(k >> 3
 // Column histogram (plain atomics: warp aggregation with __match_any_sync measured 2x slower).
 __global__ void k_col_count(int64_t nnz, const int32_t *__restrict__ indices, unsigned long long *__restrict__ cnt)
 {
+    pdl_wait();
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x)
         atomicAdd(&cnt[indices[p]], 1ULL);
 }
@@ -100,6 +101,7 @@ __global__ __launch_bounds__(32 * kShortWarps) void k_sort_short(int64_t n, cons
                                                                  int32_t *__restrict__ ATi,
                                                                  int64_t *__restrict__ perm, SortLists L)
 {
+    pdl_wait();
     __shared__ uint64_t s_key[kShortWarps][kShortBuf];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int64_t j0 = ((int64_t)blockIdx.x * kShortWarps + w) * 32; j0 < n;
@@ -175,6 +177,7 @@ __global__ __launch_bounds__(32 * kWarpsPerSortCTA) void k_sort_warp(const int64
                                                                      int32_t *__restrict__ ATi,
                                                                      int64_t *__restrict__ perm, SortLists L)
 {
+    pdl_wait();
     __shared__ uint64_t s_key[kWarpsPerSortCTA][kWarpMax];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int cnt = *(volatile int *)&L.count[0];
@@ -198,6 +201,7 @@ __global__ __launch_bounds__(kSortTPB) void k_sort_block(const int64_t *__restri
                                                          const uint64_t *__restrict__ keys, int32_t *__restrict__ ATi,
                                                          int64_t *__restrict__ perm, SortLists L)
 {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t *s_key = reinterpret_cast<uint64_t *>(smem);
     const int cnt = *(volatile int *)&L.count[1];
@@ -223,6 +227,7 @@ __global__ __launch_bounds__(kSortTPB) void k_sort_huge(const int64_t *__restric
                                                         uint64_t *__restrict__ buf, int32_t *__restrict__ ATi,
                                                         int64_t *__restrict__ perm, SortLists L)
 {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t *s_key = reinterpret_cast<uint64_t *>(smem);
     const int cnt = *(volatile int *)&L.count[2];
@@ -276,6 +281,7 @@ template <typename T>
 __global__ void k_gather_vals(int64_t nnz, const int64_t *__restrict__ perm, const T *__restrict__ A_val,
                               T *__restrict__ AT_val)
 {
+    pdl_wait();
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz; q += (int64_t)gridDim.x * blockDim.x)
         AT_val[q] = A_val[perm[q]];
 }

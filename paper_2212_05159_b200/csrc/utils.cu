@@ -9,6 +9,12 @@ namespace csrk {
 
 std::atomic<uint64_t> g_launches{0};
 
+bool pdl_enabled()
+{
+    static const bool on = knob("PDL", 1) != 0;
+    return on;
+}
+
 int knob(const char *name, int def)
 {
     char key[96];
@@ -54,6 +60,7 @@ __device__ __forceinline__ int64_t block_incl_scan(int64_t v, int64_t *s_warp, i
 __global__ __launch_bounds__(kScanTPB) void k_scan_tile_sums(const int64_t *__restrict__ x, int64_t n,
                                                              int64_t *__restrict__ sums)
 {
+    pdl_wait();
     __shared__ int64_t s_warp[kScanTPB / 32];
     const int64_t base = (int64_t)blockIdx.x * kScanTile;
     int64_t v = 0;
@@ -70,6 +77,7 @@ __global__ __launch_bounds__(kScanTPB) void k_scan_tile_sums(const int64_t *__re
 __global__ __launch_bounds__(kScanTPB) void k_scan_tiles(int64_t *__restrict__ x, int64_t n,
                                                          const int64_t *__restrict__ offsets)
 {
+    pdl_wait();
     __shared__ int64_t s[kScanTile + kScanTile / 16];
     __shared__ int64_t s_warp[kScanTPB / 32];
     const int64_t base = (int64_t)blockIdx.x * kScanTile;
@@ -134,6 +142,7 @@ __device__ int g_bad_pattern;
 __global__ void k_validate(int64_t m, int64_t n, int64_t nnz, const int64_t *__restrict__ indptr,
                            const int32_t *__restrict__ indices)
 {
+    pdl_wait();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
         int64_t s = indptr[i], e = indptr[i + 1];
         bool bad = (i == 0 && s != 0) || (i == m - 1 && e != nnz) || e < s;
@@ -160,6 +169,7 @@ static bool validate_on()
 __global__ void k_validate_tri(int64_t m, const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
                                int upper, int unit)
 {
+    pdl_wait();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
         bool diag = false, bad = false;
         for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) {
