@@ -158,6 +158,11 @@ int csrk_csr_transpose(csrk_dtype dtype, csrk_pattern A, const void *A_val,
  *   (2) C_indices != NULL (caller allocated nnz(C) int32): fills the sorted indices
  *       (C_indptr must hold the result of call 1).  Does not synchronise.
  * A is m x n, B is n x p.
+ * Call (1) also leaves the columns of every short row in `ws`; call (2) copies them instead of
+ * merging again when it is the first fill after the latest count with the same A, B and `ws`
+ * (tracked on the host).  Between the two calls that workspace must not be handed to any other
+ * csrk call; otherwise pass a different workspace to (2) (it then merges again), or set
+ * CSRK_GEMM_FILL_CACHE=0.
  */
 int csrk_spgemm_symbolic(csrk_pattern A, csrk_pattern B, int64_t *C_indptr, int32_t *C_indices,
                          int64_t *nnzC_host, void *ws, size_t ws_bytes, csrk_stream_t stream);

@@ -28,6 +28,9 @@
 //
 // The backward pass computes dA_ik = sum_j dC_ij B_kj per A entry (deterministic) and
 // scatters dB_kj += A_ik dC_ij with global atomic adds (reading A9).
+#include <mutex>
+#include <vector>
+
 #include "ops.cuh"
 
 namespace csrk {
@@ -49,6 +52,7 @@ constexpr int kSMinBlocks = CSRK_S_MINB;
 #endif  // k_gemm_S occupancy hint (A/B via CSRK_NVCC_EXTRA)
 constexpr int kSBuf = 832;           // staged C entries per warp (3D 7-point A^2: 32 x 25 = 800)
 constexpr int kSBufA = 32 * kSMaxL;  // staged dA entries per warp
+constexpr int kSCache = 32;          // symbolic: C columns of a short row kept from COUNT for FILL
 constexpr int kGemmTPB = 512;        // k_gemm_big*
 constexpr int kBitmapWords = 24576;  // 96 KB -> windows of 786,432 columns
 constexpr int kWL = 64;              // k_gemm_W: max entries of the A row
@@ -91,7 +95,7 @@ __device__ __forceinline__ int64_t s_merge_br(int64_t as, int l, const int32_t *
                                               const T *__restrict__ Av, const int64_t *__restrict__ Bp,
                                               const int32_t *__restrict__ Bi, const T *__restrict__ Bv,
                                               int32_t *outI, T *outV, const T *dCrow, T *dArow,
-                                              T *__restrict__ dB)
+                                              T *__restrict__ dB, int64_t cstride = 0)
 {
     IX cur[L], end[L];
     int32_t head[L];
@@ -130,6 +134,7 @@ __device__ __forceinline__ int64_t s_merge_br(int64_t as, int l, const int32_t *
             }
         }
         if (PH == PH_FILL) outI[c] = v;
+        if (PH == PH_COUNT && outI && c < kSCache) outI[c * cstride] = v;  // FILL's copy (k_gemm_S `cache`)
         if (PH == PH_NUM) outV[c] = (T)acc;
         ++c;
     }
@@ -212,12 +217,13 @@ template <typename T, int PH, int L, typename IX>
 __device__ __forceinline__ int64_t s_merge(int64_t as, int l, const int32_t *__restrict__ Ai,
                                            const T *__restrict__ Av, const int64_t *__restrict__ Bp,
                                            const int32_t *__restrict__ Bi, const T *__restrict__ Bv,
-                                           int32_t *outI, T *outV, const T *dCrow, T *dArow, T *__restrict__ dB)
+                                           int32_t *outI, T *outV, const T *dCrow, T *dArow, T *__restrict__ dB,
+                                           int64_t cstride)
 {
     if constexpr (PH == PH_NUM || (PH == PH_BWD && CSRK_S_BWD_BL))
         return s_merge_bl<T, PH, L, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB);
     else
-        return s_merge_br<T, PH, L, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB);
+        return s_merge_br<T, PH, L, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB, cstride);
 }
 
 template <typename T, int PH, typename IX = int64_t>
@@ -227,7 +233,8 @@ __global__ __launch_bounds__(kSTPB, kSMinBlocks) void k_gemm_S(int64_t m, const 
                                                   const T *__restrict__ Bv, int64_t *__restrict__ Cp,
                                                   int32_t *__restrict__ Ci, T *__restrict__ Cv,
                                                   const T *__restrict__ dC, T *__restrict__ dA, T *__restrict__ dB,
-                                                  BigList wl, BigList big, int use_stage)
+                                                  BigList wl, BigList big, int use_stage,
+                                                  int32_t *__restrict__ cache)
 {
     pdl_wait();
     // per-warp staging buffers in dynamic shared memory (none when use_stage == 0, which
@@ -293,20 +300,36 @@ __global__ __launch_bounds__(kSTPB, kSMinBlocks) void k_gemm_S(int64_t m, const 
     }
     if (isS) {
         const int64_t cs = PH == PH_COUNT ? 0 : Cp[i];
-        int32_t *outI = PH == PH_FILL ? (stage ? si + (cs - c_lo) : Ci + cs) : nullptr;
+        int32_t *outI = PH == PH_FILL ? (stage ? si + (cs - c_lo) : Ci + cs)
+                                      : (PH == PH_COUNT && cache ? cache + i : nullptr);
         T *outV = PH == PH_NUM ? (stage ? sv + (cs - c_lo) : Cv + cs) : nullptr;
         const T *dCrow = PH == PH_BWD ? (stage ? sv + (cs - c_lo) : dC + cs) : nullptr;
         T *dArow = (PH == PH_BWD && dA) ? (stage ? s_dA_w + (as - a_lo) : dA + as) : nullptr;
         int64_t cnt = 0;
+        // FILL of a row whose columns COUNT kept (<= kSCache of them): a copy, no second merge
+        const int nfill = PH == PH_FILL && cache ? (int)(Cp[i + 1] - cs) : kSCache + 1;
+        if (PH == PH_FILL && nfill <= kSCache) {
+            // slot c of every row is contiguous (cache[c m + i]): the warp's loads coalesce; a batch
+            // of 8 loads is issued before its stores (independent DRAM round trips in flight)
+            for (int c0 = 0; c0 < nfill; c0 += 8) {
+                int32_t q[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    q[u] = c0 + u < nfill ? __ldcs(cache + (int64_t)(c0 + u) * m + i) : 0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (c0 + u < nfill) outI[c0 + u] = q[u];
+            }
+        } else
         switch (Lw) {
-        case 1: cnt = s_merge<T, PH, 1, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
-        case 2: cnt = s_merge<T, PH, 2, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
-        case 3: cnt = s_merge<T, PH, 3, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
-        case 4: cnt = s_merge<T, PH, 4, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
-        case 5: cnt = s_merge<T, PH, 5, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
-        case 6: cnt = s_merge<T, PH, 6, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
-        case 7: cnt = s_merge<T, PH, 7, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
-        case 8: cnt = s_merge<T, PH, 8, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB); break;
+        case 1: cnt = s_merge<T, PH, 1, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB, m); break;
+        case 2: cnt = s_merge<T, PH, 2, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB, m); break;
+        case 3: cnt = s_merge<T, PH, 3, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB, m); break;
+        case 4: cnt = s_merge<T, PH, 4, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB, m); break;
+        case 5: cnt = s_merge<T, PH, 5, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB, m); break;
+        case 6: cnt = s_merge<T, PH, 6, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB, m); break;
+        case 7: cnt = s_merge<T, PH, 7, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB, m); break;
+        case 8: cnt = s_merge<T, PH, 8, IX>(as, l, Ai, Av, Bp, Bi, Bv, outI, outV, dCrow, dArow, dB, m); break;
         default: break;  // l == 0: empty row
         }
         if (PH == PH_COUNT) Cp[i + 1] = cnt;
@@ -1036,13 +1059,33 @@ static int launch_S(bool small, unsigned grid, size_t smem, cudaStream_t s, Args
     return CSRK_OK;
 }
 
+// The COUNT call keeps each short row's columns (<= kSCache) in the workspace; the FILL call
+// copies them instead of merging again when it receives the same workspace for the same A, B
+// right after that COUNT (checked here on the host; anything else merges again).
+struct CountStamp {
+    const void *ws;
+    const int64_t *Ap, *Bp;
+    const int32_t *Ai, *Bi;
+    int64_t m, nnzA, nnzB;
+    bool operator==(const CountStamp &o) const
+    {
+        return ws == o.ws && Ap == o.Ap && Bp == o.Bp && Ai == o.Ai && Bi == o.Bi && m == o.m && nnzA == o.nnzA &&
+               nnzB == o.nnzB;
+    }
+};
+static std::mutex g_stamp_mu;
+static std::vector<CountStamp> g_stamps;  // one per workspace in use (a handful)
+static int use_fill_cache() { static int v = knob("GEMM_FILL_CACHE", 1); return v; }
+
 int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, int32_t *Ci, int64_t *nnzC_host,
                     Bump &ws, cudaStream_t s)
 {
     BigList wl{}, b{}, w2{};
     BigRows br{};
     carve_lists(A, wl, b, br, ws, &w2);
+    int32_t *cache = use_fill_cache() ? ws.take<int32_t>((size_t)(A.nrows > 0 ? A.nrows : 1) * kSCache) : nullptr;
     if (ws.sizing()) return scan_counts_i64(nullptr, A.nrows, ws, s);
+    const CountStamp stamp{ws.base, A.indptr, B.indptr, A.indices, B.indices, A.nrows, A.nnz, B.nnz};
     const int64_t m = A.nrows;
     CSRK_TRY(set_smem_attrs());
     const unsigned gS = (unsigned)cdiv(m, kSTPB);
@@ -1053,8 +1096,13 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, i
         CSRK_CUDA(cudaMemsetAsync(Cp, 0, sizeof(int64_t), s));
         if (m > 0) {
             CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 4 * sizeof(int), s));
+            {
+                std::lock_guard<std::mutex> g(g_stamp_mu);
+                for (size_t q = 0; q < g_stamps.size(); ++q)
+                    if (g_stamps[q].ws == ws.base) g_stamps.erase(g_stamps.begin() + (long)q--);
+            }
             CSRK_TRY((launch_S<double, PH_COUNT>)(B.nnz < INT32_MAX, gS, 0, s, m, A.indptr, A.indices, dn, B.indptr, Bi, dn,
-                        Cp, (int32_t *)nullptr, dw, dn, dw, dw, wl, b, 0));
+                        Cp, (int32_t *)nullptr, dw, dn, dw, dw, wl, b, 0, cache));
             CSRK_LAUNCH((k_gemm_W<double, PH_COUNT>), wgrid((wsm<kWW, PH_COUNT>())), kWTPB, (wsm<kWW, PH_COUNT>()), s, wl, b, w2, A.indptr, A.indices,
                         dn, B.indptr, Bi, dn, Cp, (int32_t *)nullptr, dw, dn, dw, dw);
             CSRK_LAUNCH((k_gemm_W<double, PH_COUNT, true>), wgrid((wsm<kW2W, PH_COUNT>())), kWTPB,
@@ -1066,15 +1114,30 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, i
             CSRK_LAUNCH((k_gemm_big_sym<PH_COUNT, true>), big_grid(), kGemmTPB, big_sym_smem(), s, br, B.ncols,
                         A.indptr, A.indices, B.indptr, Bi, Cp, (int32_t *)nullptr);
             CSRK_TRY(scan_counts_i64(Cp, m, ws, s));
+            if (cache) {
+                std::lock_guard<std::mutex> g(g_stamp_mu);
+                g_stamps.push_back(stamp);
+            }
         }
         CSRK_CUDA(cudaMemcpyAsync(nnzC_host, Cp + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         CSRK_CUDA(cudaStreamSynchronize(s));
         return CSRK_OK;
     }
     if (m == 0) return CSRK_OK;
+    bool cached = false;
+    if (cache) {
+        std::lock_guard<std::mutex> g(g_stamp_mu);
+        for (size_t q = 0; q < g_stamps.size(); ++q)
+            if (g_stamps[q] == stamp) {
+                cached = true;
+                g_stamps.erase(g_stamps.begin() + (long)q);  // one FILL per COUNT
+                break;
+            }
+    }
     CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 4 * sizeof(int), s));
     CSRK_TRY((launch_S<double, PH_FILL>)(B.nnz < INT32_MAX, gS, s_smem<double>(PH_FILL, stage_fill()), s, m, A.indptr,
-                A.indices, dn, B.indptr, Bi, dn, Cp, Ci, dw, dn, dw, dw, wl, b, stage_fill()));
+                A.indices, dn, B.indptr, Bi, dn, Cp, Ci, dw, dn, dw, dw, wl, b, stage_fill(),
+                cached ? cache : (int32_t *)nullptr));
     CSRK_LAUNCH((k_gemm_W<double, PH_FILL>), wgrid((wsm<kWW, PH_FILL>())), kWTPB, (wsm<kWW, PH_FILL>()), s, wl, b, w2, A.indptr, A.indices, dn,
                 B.indptr, Bi, dn, Cp, Ci, dw, dn, dw, dw);
     CSRK_LAUNCH((k_gemm_W<double, PH_FILL, true>), wgrid((wsm<kW2W, PH_FILL>())), kWTPB,
@@ -1107,7 +1170,8 @@ static int spgemm_values_t(int PH, const csrk_pattern &A, const T *Av, const csr
     const T *ctn = nullptr;
     if (PH == PH_NUM) {
         CSRK_TRY((launch_S<T, PH_NUM>)(B.nnz < INT32_MAX, gS, s_smem<T>(PH_NUM, stage_vals()), s, m, A.indptr, A.indices,
-                    Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, Cv, ctn, tn, tn, wl, b, stage_vals()));
+                    Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, Cv, ctn, tn, tn, wl, b, stage_vals(),
+                    (int32_t *)nullptr));
         CSRK_LAUNCH((k_gemm_W<T, PH_NUM>), wgrid((wsm<kWW, PH_NUM>())), kWTPB, (wsm<kWW, PH_NUM>()), s, wl, b, BigList{}, A.indptr, A.indices, Av,
                     B.indptr,
                     B.indices, Bv, Cp, const_cast<int32_t *>(C.indices), Cv, ctn, tn, tn);
@@ -1118,7 +1182,8 @@ static int spgemm_values_t(int PH, const csrk_pattern &A, const T *Av, const csr
                     B.indices, Bv, C.indptr, C.indices, Cv, ctn, tn, tn);
     } else {
         CSRK_TRY((launch_S<T, PH_BWD>)(B.nnz < INT32_MAX, gS, s_smem<T>(PH_BWD, stage_vals()), s, m, A.indptr, A.indices,
-                    Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, tn, dC, dA, dB, wl, b, stage_vals()));
+                    Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, tn, dC, dA, dB, wl, b, stage_vals(),
+                    (int32_t *)nullptr));
         CSRK_LAUNCH((k_gemm_W<T, PH_BWD>), wgrid((wsm<kWW, PH_BWD>())), kWTPB, (wsm<kWW, PH_BWD>()), s, wl, b, BigList{}, A.indptr, A.indices, Av,
                     B.indptr,
                     B.indices, Bv, Cp, const_cast<int32_t *>(C.indices), tn, dC, dA, dB);

@@ -266,3 +266,32 @@ def test_launch_counter_advances(ck):
     ck.spmv_fwd(A, torch.ones(64, dtype=torch.float64, device="cuda"))
     torch.cuda.synchronize()
     assert ck.launch_count() > before
+
+
+def test_spgemm_symbolic_interleaved_calls(ck, orc):
+    """The fill call reuses the columns its count call left in the workspace only when it is
+    the fill of the LAST count on that workspace (csrk.h): count(A1), count(A2), fill(A1),
+    fill(A2), fill(A2) on one workspace must all equal the oracle (A1's fill and the second
+    fill of A2 merge again; the first fill of A2 copies)."""
+    import ctypes
+    from paper_2212_05159_b200.csrk import _check, _ptr, _stream, _workspace, lib
+    A1, A2 = synth.poisson2d(40), synth.random_csr(1600, 1600, 0.002, 5)
+    d1, d2 = dev(ck, A1), dev(ck, A2)
+    ws, wsb = _workspace("spgemm_symbolic", 0, d1, d1)
+    ws2, wsb2 = _workspace("spgemm_symbolic", 0, d2, d2)
+    assert ws.value == ws2.value and wsb >= wsb2
+    out = {}
+    for name, D in (("A1", d1), ("A2", d2)):
+        Cp = torch.empty(D.nrows + 1, dtype=torch.int64, device="cuda")
+        nnz = ctypes.c_int64(0)
+        _check(lib().csrk_spgemm_symbolic(D.pattern(), D.pattern(), _ptr(Cp), None, ctypes.byref(nnz), ws, wsb,
+                                          _stream()), "count")
+        out[name] = (Cp, int(nnz.value))
+    for name, D, H in (("A1", d1, A1), ("A2", d2, A2), ("A2", d2, A2)):
+        Cp, nnz = out[name]
+        Ci = torch.full((nnz,), -1, dtype=torch.int32, device="cuda")
+        _check(lib().csrk_spgemm_symbolic(D.pattern(), D.pattern(), _ptr(Cp), _ptr(Ci), None, ws, wsb, _stream()),
+               "fill")
+        rp, ri = orc.spgemm_symbolic(H, H)
+        np.testing.assert_array_equal(Cp.cpu().numpy(), rp)
+        np.testing.assert_array_equal(Ci.cpu().numpy(), ri)
