@@ -11,4 +11,9 @@ timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1
 for w in cfg3 cfg4 cfg5 trsv gcn f12; do
   timeout 900 python bench.py --workload $w --steps 5 > gpurun_out/bench_$w.log 2>&1
 done
+timeout 900 python bench.py --workload cfg5 --precond solve --steps 5 > gpurun_out/bench_cfg5_solve.log 2>&1
+# one --set full capture of the main kernels: the workload set-up (plan, symbolic) + the first warm-up step
+timeout 1200 ncu -f --set full --import-source on --clock-control none \
+  -k 'regex:k_spmm_wide|k_gemm_S|k_sort_short|k_col_count|k_rows' -c 22 \
+  -o gpurun_out/full_step python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full.log 2>&1
 tail -c 400 gpurun_out/bench_default.log
