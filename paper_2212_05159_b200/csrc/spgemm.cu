@@ -469,6 +469,7 @@ __global__ __launch_bounds__(kWTPB, CSRK_W_MINB) void k_gemm_W(BigList wl, BigLi
     const unsigned FULL = 0xffffffffu;
     const int nrows = *(volatile int *)wl.count;
     for (int it = blockIdx.x * kWWarps + warp; it < nrows; it += gridDim.x * kWWarps) {
+        __syncwarp();  // the previous row's shared-memory reads complete before this row's writes
         const int64_t i = wl.rows[it];
         const int64_t as = Ap[i];
         const int l = (int)(Ap[i + 1] - as);
