@@ -102,3 +102,23 @@ def test_host_side_argument_checks_f_rows(lib):
         assert lib.csrk_workspace_size(op, 1, ctypes.byref(A), None, k, plan, ctypes.byref(n)) == 0, op
         assert n.value > 0, op
     assert lib.csrk_launch_count() == 0
+
+
+def build_abi_demo(lib, out="/tmp/csrk_abi_demo"):
+    """Compile tests/abi_demo.c as plain C99 against include/csrk.h and link libcsrk.so + cudart."""
+    import subprocess
+    libdir = os.path.join(ROOT, "paper_2212_05159_b200")
+    cuda = "/usr/local/cuda"
+    cmd = ["gcc", "-std=c99", "-Wall", "-Werror", "-O1", os.path.join(ROOT, "tests", "abi_demo.c"),
+           "-I", os.path.join(ROOT, "include"), "-I", os.path.join(cuda, "include"),
+           "-L", libdir, "-lcsrk", "-L", os.path.join(cuda, "lib64"), "-lcudart",
+           f"-Wl,-rpath,{libdir}", f"-Wl,-rpath,{os.path.join(cuda, 'lib64')}", "-o", out]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return out
+
+
+def test_header_is_plain_c_and_links(lib):
+    """include/csrk.h is a C header: a C99 program (tests/abi_demo.c) compiles with -Wall -Werror
+    and links against libcsrk.so (run on the GPU by tests/test_gpu_validate.py)."""
+    assert os.path.exists(build_abi_demo(lib))

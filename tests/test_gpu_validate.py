@@ -56,3 +56,18 @@ def test_validate_mode():
     r = subprocess.run([sys.executable, "-c", SCRIPT, ROOT], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "validate OK" in r.stdout
+
+
+def test_abi_demo_plain_c_program():
+    """tests/abi_demo.c -- a C99 program that uses only include/csrk.h and the CUDA runtime (no
+    Python on the compute path) -- runs SpMV and the two-call SpGEMM on the GPU and checks the
+    closed forms of PAPER Eq. mat_1d_fd (A 1 = e_0 + e_{N-1}; A^2 = tridiag^2 stencil)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from test_abi_cpu import build_abi_demo
+    from paper_2212_05159_b200 import build, csrk
+    build.build()
+    exe = build_abi_demo(csrk.lib(), out=os.path.join("/tmp", f"csrk_abi_demo_{os.getpid()}"))
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "abi_demo OK" in r.stdout, (r.stdout, r.stderr)
