@@ -576,6 +576,24 @@ def flush_l2(torch, buf):
     buf.zero_()
 
 
+def host_cpu_info():
+    """CPU model, logical CPUs available to this process and SMT state."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    smt = None
+    try:
+        smt = open("/sys/devices/system/cpu/smt/active").read().strip() == "1"
+    except OSError:
+        pass
+    return {"model": model, "affinity_cpus": len(os.sched_getaffinity(0)), "smt_active": smt}
+
+
 def run_cpu_baseline(threads=None, rows_sample=1 << 22):
     """The oracle, as it stands, on a bounded sample of the same workload: the 2D Poisson
     5-point stencil on a (rows_sample/2048) x 2048 grid, the same step (all ops), fp64."""
@@ -626,7 +644,8 @@ def run_reference(args):
            "ms_per_step": float(np.median(secs)) * 1e3, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": "config2-sample: 2D Poisson 32x2048 grid, whole hot-path step (oracle)"},
-           "cpu_baseline": {"value": v, "unit": "GB/s", "cores": r["cores"], "kind": "oracle", "sample": r["sample"]},
+           "cpu_baseline": {"value": v, "unit": "GB/s", "cores": r["cores"], "kind": "oracle", "sample": r["sample"],
+                            "host": host_cpu_info()},
            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
     return 0
@@ -705,6 +724,13 @@ def main():
         flush_l2(torch, l2_flush)
         W.step(evs[i])
     torch.cuda.synchronize()
+    # warm-L2 per-op times (SURVEY 8(d) d.5 "also report warm numbers"): no flush between passes
+    evs_warm = [{nm: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for nm in names}
+                for _ in range(max(2, min(args.steps, 5)))]
+    for e in evs_warm:
+        W.step(e)
+    torch.cuda.synchronize()
+    op_ms_warm = {nm: float(np.median([e[nm][0].elapsed_time(e[nm][1]) for e in evs_warm])) for nm in names}
     if world > 1:
         tdist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in step_ev]
@@ -762,7 +788,8 @@ def main():
                "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                             "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
                             "traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes": dom_bytes},
-               "ops": ops_report, "gate": gate_report(W.costs, op_ms, peak), "gpu_launches": int(launches),
+               "ops": ops_report, "ops_warm_ms": {nm: round(v, 4) for nm, v in op_ms_warm.items()},
+               "gate": gate_report(W.costs, op_ms, peak), "gpu_launches": int(launches),
                "clocks": clk.summary()}
     # ---------------- e2e: same metric through the public API with pinned host buffers
     if not args.no_e2e:
@@ -776,6 +803,7 @@ def main():
         # 1/16 sample of the rows
         st1 = run_cpu_baseline(threads=1, rows_sample=1 << 18)
         cb["single_thread"] = {"value": st1["value"], "unit": "GB/s", "cores": 1, "sample": st1["sample"]}
+        cb["host"] = host_cpu_info()
         out["cpu_baseline"] = cb
     if out is not None:
         print(json.dumps(out))
