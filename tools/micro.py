@@ -62,6 +62,8 @@ def main():
         res["spmv_fwd"] = timeit(lambda: ck.spmv_fwd(Ad, x, out=y), args.reps, flush)
         res["spmv_bwd_plan"] = timeit(lambda: ck.spmv_bwd(Ad, x, dy, plan=plan, dA=dA, dx=dx), args.reps, flush)
         res["spmv_bwd_atomic"] = timeit(lambda: ck.spmv_bwd(Ad, x, dy, dA=dA, dx=dx), args.reps, flush)
+        res["spmv_bwd_dA_only"] = timeit(lambda: ck.spmv_bwd(Ad, x, dy, dA=dA, need_dx=False), args.reps, flush)
+        res["spmv_bwd_dx_only"] = timeit(lambda: ck.spmv_bwd(Ad, x, dy, dx=dx, need_dA=False), args.reps, flush)
         res["spmv_fwd_T_atomic"] = timeit(lambda: ck.spmv_fwd(Ad, x, op=ck.OP_T, out=y), args.reps, flush)
     if "spmm" in ops:
         X = torch.rand((n, k), dtype=torch.float64, device=dev)
