@@ -251,17 +251,21 @@ __global__ __launch_bounds__(kSTPB, kSMinBlocks) void k_gemm_S(int64_t m, const 
     int l = 0;
     int64_t w = 0;
     int64_t ll = 0;
+    // rows whose columns COUNT kept (flag byte after the cache slots): FILL needs no
+    // classification (no A-row / B-row-length reads), the row is short by construction
+    uint8_t *cflag = cache ? reinterpret_cast<uint8_t *>(cache + m * kSCache) : nullptr;
+    const bool pre = PH == PH_FILL && cflag && valid && cflag[i];
     if (valid) {
         as = Ap[i];
         ll = Ap[i + 1] - as;
         l = ll > kSMaxL ? kSMaxL + 1 : (int)ll;
-        if (l <= kSMaxL)
+        if (l <= kSMaxL && !pre)
             for (int t = 0; t < l; ++t) {
                 const int32_t k = Ai[as + t];
                 w += Bp[k + 1] - Bp[k];
             }
     }
-    const bool isS = valid && l <= kSMaxL && w <= kSMaxW;
+    const bool isS = valid && (pre || (l <= kSMaxL && w <= kSMaxW));
     // queue the other rows (warp-aggregated): l_i <= kWL to the warp path, longer to the CTA path
     const bool toW = valid && !isS && ll <= kWL;
     const unsigned wmask = __ballot_sync(0xffffffffu, toW);
@@ -333,6 +337,9 @@ __global__ __launch_bounds__(kSTPB, kSMinBlocks) void k_gemm_S(int64_t m, const 
         default: break;  // l == 0: empty row
         }
         if (PH == PH_COUNT) Cp[i + 1] = cnt;
+        if (PH == PH_COUNT && cflag) cflag[i] = cnt <= kSCache ? 1 : 0;
+    } else if (PH == PH_COUNT && cflag && valid) {
+        cflag[i] = 0;
     }
     if (stage) {
         __syncwarp();
@@ -1084,7 +1091,9 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, i
     BigList wl{}, b{}, w2{};
     BigRows br{};
     carve_lists(A, wl, b, br, ws, &w2);
-    int32_t *cache = use_fill_cache() ? ws.take<int32_t>((size_t)(A.nrows > 0 ? A.nrows : 1) * kSCache) : nullptr;
+    // kSCache column slots per row, then one flag byte per row
+    const size_t mr = (size_t)(A.nrows > 0 ? A.nrows : 1);
+    int32_t *cache = use_fill_cache() ? ws.take<int32_t>(mr * kSCache + (mr + 3) / 4) : nullptr;
     if (ws.sizing()) return scan_counts_i64(nullptr, A.nrows, ws, s);
     const CountStamp stamp{ws.base, A.indptr, B.indptr, A.indices, B.indices, A.nrows, A.nnz, B.nnz};
     const int64_t m = A.nrows;
