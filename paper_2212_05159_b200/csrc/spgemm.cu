@@ -1035,6 +1035,15 @@ static size_t s_smem(int PH, int use)
 // 677 vs 802 us on config 2).
 static int stage_fill() { static int v = knob("GEMM_STAGE_FILL", 1); return v; }
 static int stage_vals() { static int v = knob("GEMM_STAGE_VALS", 0); return v; }
+// numeric phase: stage C's values in shared memory when rows of C are long on average (3D
+// stencils: 25 per row, measured 832 -> 796 us on config 3; 2D: 13 per row, staging is slower)
+static int stage_num(const csrk_pattern &A, const csrk_pattern &C)
+{
+    static int v = knob("GEMM_STAGE_NUM", -1);
+    if (v >= 0) return v;
+    if (stage_vals()) return 1;
+    return C.nnz > 20 * (A.nrows > 0 ? A.nrows : 1) ? 1 : 0;
+}
 
 // both queue counters live in one 8-byte word so one memset clears them
 static void carve_lists(const csrk_pattern &A, BigList &wl, BigList &big, BigRows &br, Bump &ws,
@@ -1179,8 +1188,9 @@ static int spgemm_values_t(int PH, const csrk_pattern &A, const T *Av, const csr
     T *tn = nullptr;
     const T *ctn = nullptr;
     if (PH == PH_NUM) {
-        CSRK_TRY((launch_S<T, PH_NUM>)(B.nnz < INT32_MAX, gS, s_smem<T>(PH_NUM, stage_vals()), s, m, A.indptr, A.indices,
-                    Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, Cv, ctn, tn, tn, wl, b, stage_vals(),
+        const int sn = stage_num(A, C);
+        CSRK_TRY((launch_S<T, PH_NUM>)(B.nnz < INT32_MAX, gS, s_smem<T>(PH_NUM, sn), s, m, A.indptr, A.indices,
+                    Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, Cv, ctn, tn, tn, wl, b, sn,
                     (int32_t *)nullptr));
         CSRK_LAUNCH((k_gemm_W<T, PH_NUM>), wgrid((wsm<kWW, PH_NUM>())), kWTPB, (wsm<kWW, PH_NUM>()), s, wl, b, BigList{}, A.indptr, A.indices, Av,
                     B.indptr,
