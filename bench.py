@@ -69,9 +69,10 @@ OPS = ["csr_transpose", "spmv_fwd", "spmv_bwd", "spmm_fwd", "spmm_bwd", "spgemm_
 
 
 def pcg_costs(n, nnzA, nnzL, N, s=S):
-    """Algorithmic bytes / flops of one config-5 training step (csrk_pcg_loss_grad), op by op:
+    """Bytes / flops of one config-5 training step (csrk_pcg_loss_grad) AS IMPLEMENTED, op by op:
     SpMV = pattern + values + in + out; VJP of SpMV adds dy, dx, dA; dot 2n reads; a linear
-    combination of k vectors k reads + 1 write."""
+    combination of k vectors k reads + 1 write (the dL += dAt accumulations are separate passes,
+    u and z are recomputed in the reverse pass).  Reported as `unfused_bytes`."""
     spa = 8 * (n + 1) + (4 + s) * nnzA + 2 * s * n
     spl = 8 * (n + 1) + (4 + s) * nnzL + 2 * s * n
     splb = 8 * (n + 1) + (4 + s) * nnzL + 3 * s * n + s * nnzL
@@ -85,6 +86,30 @@ def pcg_costs(n, nnzA, nnzL, N, s=S):
     bwd += lin(2) + spl + splb + lin(2, nnzL) + spl_dA + lin(2, nnzL)
     flops = N * 2 * (2 * nnzA + 4 * nnzL) * 2 + N * 20 * n
     return fwd + bwd, flops
+
+
+def pcg_costs_fused(n, nnzA, nnzL, N, s=S):
+    """SURVEY 8(d) d.4 fused minimum of one config-5 step (the roofline's bytes; DESIGN "Config-5
+    bytes").  Passes are cut only where a global scalar (alpha, beta, rho and their adjoints)
+    forces a grid-wide reduction; within a pass every operand is read once and every result
+    written once, dot products ride on the pass that produces an operand, the masked outer
+    products dL += g v^T ride on the VJP pass that reads L (dL read + written), and u = L^T r,
+    z = L u are kept from the forward (written there anyway) instead of recomputed.
+      forward, per iteration   q = A p (+p.q) | r -= a q (+r.r) | u = L^T r | z = L u (+r.z) |
+                               p = z + b p
+      reverse, per iteration   pbar.p | zbar = pbar + rb r, rbar += c r + rb z |
+                               VJP z = L u (ubar = L^T zbar, dL += zbar u^T) |
+                               VJP u = L^T r (rbar += L ubar, dL += r ubar^T) | rbar.q |
+                               qbar = -a rbar + sb p | pbar = b pbar + sb q + A^T qbar"""
+    v = s * n
+    A = 8 * (n + 1) + (4 + s) * nnzA
+    L = 8 * (n + 1) + (4 + s) * nnzL
+    dL = 2 * s * nnzL                                       # read + write of the accumulated gradient
+    fwd_it = (A + 2 * v) + 3 * v + (L + 2 * v) + (L + 3 * v) + 3 * v
+    bwd_it = 2 * v + 6 * v + (L + 3 * v + dL) + (L + 4 * v + dL) + 2 * v + 3 * v + (A + 5 * v)
+    setup = 2 * v + (L + 2 * v) + (L + 3 * v)              # b.b, z0 = L (L^T b) (+b.z0)
+    tail = (L + 3 * v + dL) + (L + 3 * v + dL)             # adjoint of z0 = M b
+    return setup + N * fwd_it + N * bwd_it + tail
 
 
 def run_cfg5(args, torch, ck):
@@ -112,7 +137,8 @@ def run_cfg5(args, torch, ck):
             e.record(st)
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(e))
-    byts, flops = pcg_costs(A.nrows, A.nnz, L.nnz, N)
+    unfused, flops = pcg_costs(A.nrows, A.nnz, L.nnz, N)
+    byts = pcg_costs_fused(A.nrows, A.nnz, L.nnz, N)
     ms = float(np.mean(ts))
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
@@ -123,10 +149,17 @@ def run_cfg5(args, torch, ck):
                                   "L (33,554,431 nnz), 50 PCG iterations fwd + reverse, gamma 0.6, 1 GPU",
                       "preconditioner": "M = L L^T (P:836-839)" if pc == "mult" else
                       "M = (L L^T)^-1 by two SpTRSV (SURVEY 8(f) f3); bytes counted as for M = L L^T"},
-           "step_bytes": byts, "gflops": round(flops / (ms * 1e-3) / 1e9, 2), "loss": loss,
+           "step_bytes": byts, "step_bytes_def": "SURVEY 8(d) d.4 fused minimum (bench.pcg_costs_fused)",
+           "unfused_bytes": unfused, "unfused_GB/s": round(unfused / (ms * 1e-3) / 1e9, 1),
+           "gflops": round(flops / (ms * 1e-3) / 1e9, 2), "loss": loss,
            "roofline": {"bound": "hbm", "kernel": "whole step", "achieved": round(byts / (ms * 1e-3) / 1e9, 1),
                         "peak": peak, "unit": "GB/s", "frac": round(byts / (ms * 1e-3) / 1e9 / peak, 4)},
            "gpu_launches": int((ck.launch_count() - l0) / max(args.steps, 1)), "clocks": clk.summary()}
+    traffic, tsrc = _traffic("cfg5" if pc == "mult" else "cfg5_solve", "pcg_loss_grad")
+    out["roofline"]["traffic"], out["roofline"]["traffic_source"] = traffic, tsrc
+    if args.ops_trace:
+        write_ops_trace(args.ops_trace, ck, [("pcg_loss_grad", lambda: ck.pcg_loss_grad(Ad, Ld, bt, N, 0.6, dL=dL,
+                                                                                        precond=pc))])
     print(json.dumps(out))
     return 0
 
@@ -172,51 +205,12 @@ def run_ops_workload(args, torch, ck, cfg):
     ops["spgemm_symbolic"] = (lambda: ck.spgemm_symbolic(Ad, Ad), c["spgemm_symbolic"])
     ops["spgemm_numeric"] = (lambda: ck.spgemm_numeric(Ad, Ad, C, out=Cv), c["spgemm_numeric"])
     ops["spgemm_bwd"] = (lambda: ck.spgemm_bwd(Ad, Ad, C, dC, dA=dA_g, dB=dB_g), c["spgemm_bwd"])
-    l2 = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    st = torch.cuda.current_stream()
-    for _ in range(args.warmup):
-        for f, _c in ops.values():
-            f()
-    torch.cuda.synchronize()
-    times = {k: [] for k in ops}
-    l0 = ck.launch_count()
-    with Clocks(0) as clk:
-        for _ in range(args.steps):
-            for k, (f, _c) in ops.items():
-                l2.zero_()
-                a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(st)
-                f()
-                e.record(st)
-                times[k].append((a, e))
-        torch.cuda.synchronize()
-    launches = ck.launch_count() - l0
-    peak = _peak()
-    rep = {}
-    tot_b, tot_f, tot_ms = 0, 0, 0.0
-    for k, ev in times.items():
-        ms = float(np.median([a.elapsed_time(e) for a, e in ev]))
-        b, fl = ops[k][1]
-        rep[k] = {"ms": round(ms, 4), "GB/s": round(b / ms / 1e6, 1), "GFLOP/s": round(fl / ms / 1e6, 1),
-                  "frac": round(b / ms / 1e6 / peak, 3), "bytes": b}
-        if k != "spmv_bwd_plan":
-            tot_b, tot_f, tot_ms = tot_b + b, tot_f + fl, tot_ms + ms
-    dom = max((k for k in rep if k != "spmv_bwd_plan"), key=lambda k: rep[k]["ms"])
     wl = ("config3: 3D Poisson 7-point 160^3 (4,096,000 rows, 28,518,400 nnz), fp64, C = A A "
           f"(nnz(C) {nnzC:,}, prod {prod:,}): symbolic + numeric + bwd" if cfg == 3 else
           "config4: power-law n = 2^23, 2^27 nnz, rows 8..32,769, fp32: spmv fwd/bwd, transpose, C = A A "
           f"(nnz(C) {nnzC:,}, prod {prod:,}) symbolic + numeric + bwd")
-    out = {"metric": f"SpMV/SpGEMM fwd+bwd algorithmic GB/s (config {cfg})",
-           "value": round(tot_b / tot_ms / 1e6, 2), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": round(tot_ms, 4), "higher_is_better": True, "scaling": "weak",
-           "vs_baseline": None, "dtype": "f64" if cfg == 3 else "f32", "data": "synthetic",
-           "config": {"workload": wl, "l2": "flushed (512 MiB write) before every timed op"},
-           "gflops": round(tot_f / tot_ms / 1e6, 2),
-           "roofline": {"bound": "hbm", "kernel": dom, "achieved": rep[dom]["GB/s"], "peak": peak,
-                        "unit": "GB/s", "frac": rep[dom]["frac"], "traffic": None},
-           "ops": rep, "gpu_launches": int(launches / max(args.steps, 1)), "clocks": clk.summary()}
-    print(json.dumps(out))
-    return 0
+    return _time_ops(args, torch, ck, ops, f"SpMV/SpGEMM fwd+bwd algorithmic GB/s (config {cfg})",
+                     "f64" if cfg == 3 else "f32", wl, f"cfg{cfg}", exclude=("spmv_bwd_plan",))
 
 
 def run_trsv_workload(args, torch, ck):
@@ -246,49 +240,10 @@ def run_trsv_workload(args, torch, ck):
         ops[f"sptrsv_bwd_{nm}"] = ((lambda Td=Td, x=x, v=v, plan=plan, dT=dT, db=db:
                                     ck.sptrsv_bwd(Td, x, v, plan=plan, dT=dT, db=db)),
                                    (pat + s * nnz + 4 * s * n + s * nnz, 3 * nnz))
-    l2 = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    st = torch.cuda.current_stream()
-    for _ in range(args.warmup):
-        for f, _c in ops.values():
-            f()
-    torch.cuda.synchronize()
-    times = {k: [] for k in ops}
-    l0 = ck.launch_count()
-    with Clocks(0) as clk:
-        for _ in range(args.steps):
-            for k, (f, _c) in ops.items():
-                l2.zero_()
-                a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(st)
-                f()
-                e.record(st)
-                times[k].append((a, e))
-        torch.cuda.synchronize()
-    launches = ck.launch_count() - l0
-    peak = _peak()
-    rep, tot_b, tot_f, tot_ms = {}, 0, 0, 0.0
-    for k, ev in times.items():
-        ms = float(np.median([a.elapsed_time(e) for a, e in ev]))
-        b, fl = ops[k][1]
-        all_ms = [a.elapsed_time(e) for a, e in ev]
-        rep[k] = {"ms": round(ms, 4), "GB/s": round(b / ms / 1e6, 1), "GFLOP/s": round(fl / ms / 1e6, 1),
-                  "frac": round(b / ms / 1e6 / peak, 3), "bytes": b, "ms_min": round(float(np.min(all_ms)), 4),
-                  "ms_p90": round(float(np.percentile(all_ms, 90)), 4)}
-        tot_b, tot_f, tot_ms = tot_b + b, tot_f + fl, tot_ms + ms
-    dom = max(rep, key=lambda k: rep[k]["ms"])
-    out = {"metric": "SpTRSV fwd+bwd algorithmic GB/s", "value": round(tot_b / tot_ms / 1e6, 2), "unit": "GB/s",
-           "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot_ms, 4),
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": "SpTRSV: config-5 bidiagonal L (16,777,216 rows, chain pass) and the lower "
-                                  "triangle of 2D Poisson 2048^2 (4,194,304 rows, wavefront, sync-free pass), fwd + "
-                                  "bwd with a cached transpose plan",
-                      "l2": "flushed (512 MiB write) before every timed op"},
-           "gflops": round(tot_f / tot_ms / 1e6, 2),
-           "roofline": {"bound": "hbm", "kernel": dom, "achieved": rep[dom]["GB/s"], "peak": peak, "unit": "GB/s",
-                        "frac": rep[dom]["frac"], "traffic": None},
-           "ops": rep, "gpu_launches": int(launches / max(args.steps, 1)), "clocks": clk.summary()}
-    print(json.dumps(out))
-    return 0
+    return _time_ops(args, torch, ck, ops, "SpTRSV fwd+bwd algorithmic GB/s", "f64",
+                     "SpTRSV: config-5 bidiagonal L (16,777,216 rows, chain pass) and the lower triangle of 2D "
+                     "Poisson 2048^2 (4,194,304 rows, wavefront, sync-free pass), fwd + bwd with a cached transpose "
+                     "plan", "trsv", keep=keep)
 
 
 def run_gcn_workload(args, torch, ck):
@@ -321,7 +276,7 @@ def run_gcn_workload(args, torch, ck):
         "dtheta": (lambda: ck.dense_gemm_tn(X, dZ, out=dW), (s * n * (C + F), 2 * n * C * F)),
         "dx": (lambda: ck.dense_gemm_nn(dZ, W, transW=True, out=dX), (s * n * (C + F), 2 * n * C * F)),
     }
-    return _time_ops(args, torch, ck, ops, "GCN layer fwd+bwd algorithmic GB/s", "f32",
+    return _time_ops(args, torch, ck, ops, "GCN layer fwd+bwd algorithmic GB/s", "f32", wkey="gcn", workload=
                      "GCN layer (Fig. 12): power-law graph 1,048,576 nodes, 5,242,880 edges (max degree "
                      f"{int(np.diff(G.indptr).max())}), fp32, C = F = 16, fwd + bwd with a cached transpose plan")
 
@@ -363,14 +318,15 @@ def run_f12_workload(args, torch, ck):
                       (pat(m, na) + pat(m, nl) + pat(m, nc) + s8 * (nc + na + nl), na + nl)),
         "spai_loss_grad": (lambda: ck.spai_loss_grad(plan, M, A2d, dM=dM), (spai_bytes, 6 * prod2)),
     }
-    return _time_ops(args, torch, ck, ops, "Sp+Sp and SPAI fwd+bwd algorithmic GB/s", "f64",
+    return _time_ops(args, torch, ck, ops, "Sp+Sp and SPAI fwd+bwd algorithmic GB/s", "f64", wkey="f12", workload=
                      "Sp+Sp: 2 A - 3 L, A = 2D Poisson 2048^2, L lower bidiagonal (fwd + VJP); SPAI: ||I - M A||_F^2 "
                      "+ gradient, A = 2D Poisson 1024^2, pattern(M) = pattern(A)")
 
 
-def _time_ops(args, torch, ck, ops, metric, dtype, workload):
+def _time_ops(args, torch, ck, ops, metric, dtype, workload, wkey, exclude=(), keep=None):
     """Time a dict name -> (fn, (bytes, flops)) op by op: CUDA events on the current stream,
-    L2 flushed (512 MiB write) before every op, median over --steps."""
+    L2 flushed (512 MiB write) before every op, median over --steps.  Ops in `exclude` are
+    reported but not part of the step total (alternative paths of an op)."""
     dev = torch.device("cuda", 0)
     l2 = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     st = torch.cuda.current_stream()
@@ -400,18 +356,34 @@ def _time_ops(args, torch, ck, ops, metric, dtype, workload):
         rep[k] = {"ms": round(ms, 4), "GB/s": round(b / ms / 1e6, 1), "GFLOP/s": round(fl / ms / 1e6, 1),
                   "frac": round(b / ms / 1e6 / peak, 3), "bytes": b, "ms_min": round(float(np.min(all_ms)), 4),
                   "ms_p90": round(float(np.percentile(all_ms, 90)), 4)}
-        tot_b, tot_f, tot_ms = tot_b + b, tot_f + fl, tot_ms + ms
-    dom = max(rep, key=lambda k: rep[k]["ms"])
+        if k not in exclude:
+            tot_b, tot_f, tot_ms = tot_b + b, tot_f + fl, tot_ms + ms
+    dom = max((k for k in rep if k not in exclude), key=lambda k: rep[k]["ms"])
+    traffic, tsrc = _traffic(wkey, dom)
     out = {"metric": metric, "value": round(tot_b / tot_ms / 1e6, 2), "unit": "GB/s", "n_gpus": 1,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot_ms, 4), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
            "config": {"workload": workload, "l2": "flushed (512 MiB write) before every timed op"},
            "gflops": round(tot_f / tot_ms / 1e6, 2),
            "roofline": {"bound": "hbm", "kernel": dom, "achieved": rep[dom]["GB/s"], "peak": peak, "unit": "GB/s",
-                        "frac": rep[dom]["frac"], "traffic": None},
+                        "frac": rep[dom]["frac"], "traffic": traffic, "traffic_source": tsrc,
+                        "algorithmic_bytes": ops[dom][1][0]},
            "ops": rep, "gpu_launches": int(launches / max(args.steps, 1)), "clocks": clk.summary()}
+    if args.ops_trace:
+        write_ops_trace(args.ops_trace, ck, [(k, f) for k, (f, _c) in ops.items()])
     print(json.dumps(out))
     return 0
+
+
+def _traffic(workload, op):
+    """DRAM bytes (read + write) of one call of `op` in `workload`, from the committed ncu launch
+    list attributed by tools/traffic.py (profiles/traffic_<workload>.json); (None, None) if absent."""
+    path = os.path.join(ROOT, "profiles", f"traffic_{workload}.json")
+    try:
+        prof = json.load(open(path))
+        return int(prof["ops"][op]["dram_bytes"]), os.path.relpath(path, ROOT) + " <- " + prof.get("source", "?")
+    except Exception:
+        return None, None
 
 
 def _peak():
@@ -514,46 +486,39 @@ class Workload:
         self.dB_g = e(self.B.nnz, dtype=f64, device=dev)
         self.costs = op_costs(self.m, self.n, self.nnz, self.nnzC, self.prod)
 
+    def op_list(self):
+        """The step's ops in order, (name, fn) -- a7, a1, a2+a3, a4, a5+a6, a8+a9, a10, a11+a12 (+ a13)."""
+        ck = self.ck
+
+        def symbolic():
+            C = ck.spgemm_symbolic(self.A, self.B)
+            assert C.nnz == self.nnzC
+            self.C = C
+
+        ops = [
+            ("csr_transpose", lambda: ck.csr_transpose(self.A, with_values=False, out=self.plan)),
+            ("spmv_fwd", lambda: ck.spmv_fwd(self.A, self.x, out=self.y)),
+            # atomic scatter for dx (P:448): measured faster than the transpose-plan gather here
+            ("spmv_bwd", lambda: ck.spmv_bwd(self.A, self.x, self.dy, dA=self.dA_v, dx=self.dx)),
+            ("spmm_fwd", lambda: ck.spmm_fwd(self.A, self.X, out=self.Y)),
+            ("spmm_bwd", lambda: ck.spmm_bwd(self.A, self.X, self.dY, plan=self.plan, dA=self.dA_m, dX=self.dX)),
+            ("spgemm_symbolic", symbolic),
+            ("spgemm_numeric", lambda: ck.spgemm_numeric(self.A, self.B, self.C, out=self.Cv)),
+            ("spgemm_bwd", lambda: ck.spgemm_bwd(self.A, self.B, self.C, self.dC, dA=self.dA_g, dB=self.dB_g)),
+        ]
+        if self.dist is not None:
+            ops.append(("halo_reduce", lambda: self.dist.reduce_partials(self)))
+        return ops
+
     def step(self, ev=None):
         """One pass of the hot path; `ev` (dict op -> (start, end) events) brackets each op."""
-        ck, torch = self.ck, self.torch
-        st = torch.cuda.current_stream()
-
-        def rec(name, i):
+        st = self.torch.cuda.current_stream()
+        for name, fn in self.op_list():
             if ev is not None:
-                ev[name][i].record(st)
-
-        rec("csr_transpose", 0)
-        ck.csr_transpose(self.A, with_values=False, out=self.plan)
-        rec("csr_transpose", 1)
-        rec("spmv_fwd", 0)
-        ck.spmv_fwd(self.A, self.x, out=self.y)
-        rec("spmv_fwd", 1)
-        rec("spmv_bwd", 0)
-        # atomic scatter for dx (P:448): measured faster than the transpose-plan gather here
-        ck.spmv_bwd(self.A, self.x, self.dy, dA=self.dA_v, dx=self.dx)
-        rec("spmv_bwd", 1)
-        rec("spmm_fwd", 0)
-        ck.spmm_fwd(self.A, self.X, out=self.Y)
-        rec("spmm_fwd", 1)
-        rec("spmm_bwd", 0)
-        ck.spmm_bwd(self.A, self.X, self.dY, plan=self.plan, dA=self.dA_m, dX=self.dX)
-        rec("spmm_bwd", 1)
-        rec("spgemm_symbolic", 0)
-        C = ck.spgemm_symbolic(self.A, self.B)
-        rec("spgemm_symbolic", 1)
-        assert C.nnz == self.nnzC
-        self.C = C
-        rec("spgemm_numeric", 0)
-        ck.spgemm_numeric(self.A, self.B, C, out=self.Cv)
-        rec("spgemm_numeric", 1)
-        rec("spgemm_bwd", 0)
-        ck.spgemm_bwd(self.A, self.B, C, self.dC, dA=self.dA_g, dB=self.dB_g)
-        rec("spgemm_bwd", 1)
-        if self.dist is not None:
-            rec("halo_reduce", 0)
-            self.dist.reduce_partials(self)
-            rec("halo_reduce", 1)
+                ev[name][0].record(st)
+            fn()
+            if ev is not None:
+                ev[name][1].record(st)
 
 
 NOMINAL_HBM_GBS = 8000.0  # north_star "~8 TB/s" (SURVEY 8(d) d.1 gates on it)
@@ -651,6 +616,48 @@ def run_reference(args):
     return 0
 
 
+def spawn_ranks(args):
+    """One process per GPU (the driver's contract).  Under a launcher (WORLD_SIZE set) the world
+    size must equal --gpus.  Without one, --gpus N > 1 starts N ranks itself through
+    torch.distributed.run on 127.0.0.1; it fails (exit 2, nothing printed on stdout) when fewer
+    than N GPUs are visible.  Returns an exit code, or None to run this process as the rank."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is not None:
+        if int(ws) != args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}\n")
+            return 2
+        return None
+    if args.gpus == 1:
+        return None
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}\n")
+        return 2
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def write_ops_trace(path, ck, ops_in_order):
+    """Run each (name, fn) once and record the csrk launches it made, in launch order."""
+    import torch
+    torch.cuda.synchronize()
+    out = []
+    for name, fn in ops_in_order:
+        l0 = ck.launch_count()
+        fn()
+        out.append([name, int(ck.launch_count() - l0)])
+    torch.cuda.synchronize()
+    with open(path, "w") as f:
+        json.dump({"ops": out}, f)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -661,15 +668,24 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5", "trsv", "gcn", "f12"])
     ap.add_argument("--precond", default="mult", choices=["mult", "solve"], help="cfg5: M = L L^T or (L L^T)^-1")
+    ap.add_argument("--ops-trace", default=None,
+                    help="after the timed region, run one more pass and write its op -> csrk launch counts "
+                         "(tools/traffic.py attributes an ncu launch list of this run to ops with it)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)
+    rc = spawn_ranks(args)
+    if rc is not None:
+        return rc
 
     import torch
     import torch.distributed as tdist
     from paper_2212_05159_b200 import csrk as ck
 
+    if args.workload != "cfg2" and int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        sys.stderr.write(f"bench.py: --workload {args.workload} has no sharded (N > 1) path\n")
+        return 2
     if args.workload == "cfg5":
         return run_cfg5(args, torch, ck)
     if args.workload == "trsv":
@@ -756,14 +772,8 @@ def main():
     dom = max(OPS, key=lambda nm: op_ms[nm])
     dom_bytes = W.costs[dom][0]
     achieved = dom_bytes / (op_ms[dom] * 1e-3) / 1e9
-    # DRAM traffic of that op per launch, from the committed ncu capture (tools/profile_summary.py)
-    traffic, traffic_src = None, None
-    try:
-        prof = json.load(open(os.path.join(ROOT, "profiles", "latest_ops.json")))
-        traffic = prof["ops"][dom]["dram_bytes"]
-        traffic_src = prof.get("source")
-    except Exception:
-        pass
+    # DRAM traffic of that op per call, from the committed ncu launch list (tools/traffic.py)
+    traffic, traffic_src = _traffic("cfg2" if world == 1 else f"cfg2_n{world}", dom)
     ops_report = {nm: {"ms": round(op_ms[nm], 4),
                        "GB/s": round(W.costs[nm][0] / (op_ms[nm] * 1e-3) / 1e9, 1) if nm in W.costs else None,
                        "GFLOP/s": round(W.costs[nm][1] / (op_ms[nm] * 1e-3) / 1e9, 1) if nm in W.costs else None,
@@ -805,6 +815,8 @@ def main():
         cb["single_thread"] = {"value": st1["value"], "unit": "GB/s", "cores": 1, "sample": st1["sample"]}
         cb["host"] = host_cpu_info()
         out["cpu_baseline"] = cb
+    if args.ops_trace and rank == 0:
+        write_ops_trace(args.ops_trace, ck, W.op_list())
     if out is not None:
         print(json.dumps(out))
     if world > 1:

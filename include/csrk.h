@@ -20,7 +20,10 @@
  *              entries (reading A1).  Canonical form is the caller's contract; it
  *              is checked (CSRK_ERR_PATTERN) only when env CSRK_VALIDATE=1.
  *   Values     dtype CSRK_F32 or CSRK_F64; values and dense operands share dtype.
- *              Reductions accumulate in fp64 for both dtypes (reading A5/A18).
+ *              Reductions accumulate in fp64 for both dtypes (reading A5/A18): register /
+ *              shared-memory sums are fp64, and atomic scatters (A^T v without a plan,
+ *              SpGEMM dB, multi-window big-row SpGEMM dA) add fp64 terms into an fp64
+ *              target -- for fp32 data a workspace scratch rounded once to fp32 at the end.
  *   Dense      row-major, leading dimension ld >= k (elements).
  *   Transpose  Ops that need A^T accept an optional cached transpose plan
  *              (AT = pattern of A^T, AT_perm[q] = position in A of A^T's q-th
@@ -160,9 +163,10 @@ int csrk_csr_transpose(csrk_dtype dtype, csrk_pattern A, const void *A_val,
  * A is m x n, B is n x p.
  * Call (1) also leaves the columns of every short row in `ws`; call (2) copies them instead of
  * merging again when it is the first fill after the latest count with the same A, B and `ws`
- * (tracked on the host).  Between the two calls that workspace must not be handed to any other
- * csrk call; otherwise pass a different workspace to (2) (it then merges again), or set
- * CSRK_GEMM_FILL_CACHE=0.
+ * (tracked on the host).  Any other csrk call given a workspace overlapping that `ws` in between
+ * invalidates the copy (call (2) then merges again).  Writes to `ws` by anything other than
+ * csrk between the calls, or changes to A's / B's patterns, are outside the contract (call (2)
+ * needs the patterns of call (1) anyway); CSRK_GEMM_FILL_CACHE=0 disables the copy.
  */
 int csrk_spgemm_symbolic(csrk_pattern A, csrk_pattern B, int64_t *C_indptr, int32_t *C_indices,
                          int64_t *nnzC_host, void *ws, size_t ws_bytes, csrk_stream_t stream);

@@ -32,6 +32,22 @@ def spai_loss_grad(A_dense: np.ndarray, M_pattern: np.ndarray, M_dense: np.ndarr
     return float(loss.detach()), torch.where(mask, Mv.grad, torch.zeros_like(Mv.grad)).numpy()
 
 
+def spai_S(A_dense: np.ndarray, M_pattern: np.ndarray, M_dense: np.ndarray):
+    """S-scales of the elementwise tolerance rule (reading A6) for the composed evaluation
+    C = M A, R = I - C, loss = sum R^2, dM = -2 (R A^T) (.) mask(M): first-order magnitudes of
+    the rounding of each stage, S_R = |I| + |M| |A| (the terms of R), then
+        S_loss = sum_ij (2 |R_ij| S_R,ij + R_ij^2),
+        S_dM   = 2 (S_R + |R|) |A|^T (.) mask(M)     (the error of R times |A|, plus the terms).
+    Returns (S_loss, S_dM dense)."""
+    N = A_dense.shape[0]
+    M = np.where(M_pattern, M_dense, 0.0)
+    R = np.eye(N) - M @ A_dense
+    SR = np.eye(N) + np.abs(M) @ np.abs(A_dense)
+    S_loss = float((2.0 * np.abs(R) * SR + R * R).sum())
+    S_dM = np.where(M_pattern, 2.0 * (SR + np.abs(R)) @ np.abs(A_dense).T, 0.0)
+    return S_loss, S_dM
+
+
 def spai_loss_by_columns(A_dense: np.ndarray, M_dense: np.ndarray) -> float:
     """sum_i ||(I - M A) e_i||_2^2 -- the column decomposition of P:1079-1082, column by column."""
     N = A_dense.shape[0]

@@ -29,10 +29,13 @@ int check_plan(const csrk_pattern &A, const csrk_pattern *AT, const int64_t *per
     return CSRK_OK;
 }
 
-// Run `f(Bump&)` once in sizing mode to learn the bytes, then for real.
+// Run `f(Bump&)` once in sizing mode to learn the bytes, then for real.  Any call other than
+// csrk_spgemm_symbolic may overwrite the workspace, so it invalidates a symbolic FILL cache kept
+// there (spgemm.cu).
 template <typename F>
-int with_ws(void *ws, size_t ws_bytes, F &&f)
+int with_ws(void *ws, size_t ws_bytes, F &&f, bool keeps_fill_cache = false)
 {
+    if (!keeps_fill_cache && ws) gemm_fill_cache_invalidate(ws, ws_bytes);
     Bump sz(nullptr, 0);
     CSRK_TRY(f(sz));
     if (sz.used > 0 && (!ws || ws_bytes < sz.used)) return CSRK_ERR_WORKSPACE;
@@ -130,7 +133,7 @@ int csrk_spgemm_symbolic(csrk_pattern A, csrk_pattern B, int64_t *C_indptr, int3
     CSRK_TRY(validate_pattern(B, (cudaStream_t)stream));
     return with_ws(ws, ws_bytes, [&](Bump &b) {
         return spgemm_symbolic(A, B, C_indptr, C_indices, nnzC_host, b, (cudaStream_t)stream);
-    });
+    }, true);
 }
 
 int csrk_spgemm_numeric(csrk_dtype dtype, csrk_pattern A, const void *A_val, csrk_pattern B, const void *B_val,

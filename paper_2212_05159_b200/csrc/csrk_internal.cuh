@@ -56,6 +56,21 @@ bool pdl_enabled();
 
 constexpr int kNumSMs = 148;
 
+// One-time setup per CUDA device (kernel attributes such as the dynamic shared-memory limit are
+// per device): need() stays true on the current device until done() is called there.  Setting an
+// attribute twice is harmless, so callers racing on a first call may both set it.
+struct DevOnce {
+    std::atomic<uint64_t> bits{0};
+    static int dev()
+    {
+        int d = 0;
+        cudaGetDevice(&d);
+        return d & 63;
+    }
+    bool need() const { return !(bits.load(std::memory_order_acquire) & (1ull << dev())); }
+    void done() { bits.fetch_or(1ull << dev(), std::memory_order_acq_rel); }
+};
+
 // ---------------------------------------------------------------- workspace carving
 // One planning routine per op carves its scratch from `ws` through a Bump.  In size
 // mode (base == nullptr) it only counts, so csrk_workspace_size and the op agree.
@@ -79,8 +94,9 @@ struct Bump {
 // ---------------------------------------------------------------- dtype helpers
 template <typename T> struct Acc { using type = double; };   // fp32 and fp64 data accumulate in fp64
 
-__device__ __forceinline__ void red_add(double *a, double v) { atomicAdd(a, v); }
-__device__ __forceinline__ void red_add(float *a, float v) { atomicAdd(a, v); }
+// Atomic scatters (A^T v without a plan, SpGEMM dB, big-row SpGEMM dA) always add fp64 terms into
+// an fp64 target: for fp32 data that target is workspace scratch, rounded once to fp32 at the end
+// (f64_to_f32 / the ops' epilogues) -- reading A5: fp32 and fp64 data both accumulate in fp64.
 
 // ---------------------------------------------------------------- merge-path search
 // Merge of (row-end offsets a[0..nr), nnz indices 0..Z-1): at state (i, j) the next item
@@ -101,6 +117,8 @@ __device__ __forceinline__ int merge_path_rows(int d, int nr, int Z, const int64
 // In-place int64 prefix sum: data[0] := 0 is NOT written; data[1..n] := inclusive scan of
 // data[1..n].  Used to turn counts stored at indptr[1..] into a CSR indptr.
 int scan_counts_i64(int64_t *indptr, int64_t n, Bump &ws, cudaStream_t s);
+// dst[i] = (float)src[i], i < n (the single rounding of an fp64 accumulation of fp32 data)
+int f64_to_f32(const double *src, float *dst, int64_t n, cudaStream_t s);
 size_t scan_ws_bytes(int64_t n);
 
 // Row-length classification etc.

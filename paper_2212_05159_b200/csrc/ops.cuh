@@ -18,6 +18,8 @@ int csr_transpose(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int64
                   void *AT_val, int64_t *perm, Bump &ws, cudaStream_t s);
 int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *C_indptr, int32_t *C_indices,
                     int64_t *nnzC_host, Bump &ws, cudaStream_t s);
+// forget symbolic FILL caches whose workspace lies in [ws, ws + bytes) (another op may overwrite it)
+void gemm_fill_cache_invalidate(const void *ws, size_t bytes);
 int spgemm_numeric(csrk_dtype dt, const csrk_pattern &A, const void *A_val, const csrk_pattern &B,
                    const void *B_val, const csrk_pattern &C, void *C_val, Bump &ws, cudaStream_t s);
 int spgemm_bwd(csrk_dtype dt, const csrk_pattern &A, const void *A_val, const csrk_pattern &B, const void *B_val,

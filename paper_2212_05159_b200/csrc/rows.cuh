@@ -12,7 +12,7 @@
 //   REDUCE    y[row] = sum_p val(pv) v[idx p]  (in p order -- the oracle's order -- for short
 //             rows; lane-strided + fixed shuffle tree for long rows; both deterministic)
 //             SIDE: D[pv] = v[idx p] * u[row]
-//   SCATTER   w = u[row]; SIDE: D[p] = w v[idx p]; y (nullable): y[idx p] += val[p] w (atomic)
+//   SCATTER   w = u[row]; SIDE: D[p] = w v[idx p]; y64 (nullable): y64[idx p] += val[p] w (fp64 atomic)
 //   TRANSPOSE slot = cursor[idx p]++ (atomic); keys[slot] = (p << 31) | row
 #pragma once
 
@@ -46,7 +46,7 @@ __device__ __forceinline__ void row_elem(const TileArgs<T> &a, int64_t row, int6
     } else if (MODE == MODE_SCATTER) {
         const T w = a.u[row];
         if (SIDE) a.D[p] = w * a.v[c];
-        if (a.y) red_add(&a.y[c], (T)((double)a.vals[p] * (double)w));
+        if (a.y64) atomicAdd(&a.y64[c], (double)a.vals[p] * (double)w);
     } else {
         const int64_t slot = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(&a.cursor[c]), 1ULL);
         a.out_keys[slot] = ((uint64_t)p << 31) | (uint64_t)row;

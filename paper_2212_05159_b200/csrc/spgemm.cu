@@ -95,7 +95,7 @@ __device__ __forceinline__ int64_t s_merge_br(int64_t as, int l, const int32_t *
                                               const T *__restrict__ Av, const int64_t *__restrict__ Bp,
                                               const int32_t *__restrict__ Bi, const T *__restrict__ Bv,
                                               int32_t *outI, T *outV, const T *dCrow, T *dArow,
-                                              T *__restrict__ dB, int64_t cstride = 0)
+                                              double *__restrict__ dB, int64_t cstride = 0)
 {
     IX cur[L], end[L];
     int32_t head[L];
@@ -127,7 +127,7 @@ __device__ __forceinline__ int64_t s_merge_br(int64_t as, int l, const int32_t *
                 if (PH == PH_NUM) acc = fma(av[t], (double)Bv[cur[t]], acc);
                 if (PH == PH_BWD) {
                     dacc[t] = fma(g, (double)Bv[cur[t]], dacc[t]);
-                    if (dB) red_add(&dB[cur[t]], (T)(av[t] * g));
+                    if (dB) atomicAdd(&dB[cur[t]], av[t] * g);
                 }
                 ++cur[t];
                 head[t] = cur[t] < end[t] ? Bi[cur[t]] : INT32_MAX;
@@ -153,7 +153,7 @@ __device__ __forceinline__ int64_t s_merge_bl(int64_t as, int l, const int32_t *
                                               const T *__restrict__ Av, const int64_t *__restrict__ Bp,
                                               const int32_t *__restrict__ Bi, const T *__restrict__ Bv,
                                               int32_t *outI, T *outV, const T *dCrow, T *dArow,
-                                              T *__restrict__ dB)
+                                              double *__restrict__ dB)
 {
     constexpr bool VAL = PH == PH_NUM || PH == PH_BWD;
     IX cur[L];        // position in B of list t's head
@@ -192,7 +192,7 @@ __device__ __forceinline__ int64_t s_merge_bl(int64_t as, int l, const int32_t *
             if (PH == PH_NUM) acc = fma(av[t], mt ? hv[t] : 0.0, acc);
             if (PH == PH_BWD) {
                 dacc[t] = fma(g, mt ? hv[t] : 0.0, dacc[t]);
-                if (dB && mt) red_add(&dB[cur[t]], (T)(av[t] * g));
+                if (dB && mt) atomicAdd(&dB[cur[t]], av[t] * g);
             }
             cur[t] += mt;
             rem[t] -= mt;
@@ -217,7 +217,7 @@ template <typename T, int PH, int L, typename IX>
 __device__ __forceinline__ int64_t s_merge(int64_t as, int l, const int32_t *__restrict__ Ai,
                                            const T *__restrict__ Av, const int64_t *__restrict__ Bp,
                                            const int32_t *__restrict__ Bi, const T *__restrict__ Bv,
-                                           int32_t *outI, T *outV, const T *dCrow, T *dArow, T *__restrict__ dB,
+                                           int32_t *outI, T *outV, const T *dCrow, T *dArow, double *__restrict__ dB,
                                            int64_t cstride)
 {
     if constexpr (PH == PH_NUM || (PH == PH_BWD && CSRK_S_BWD_BL))
@@ -232,7 +232,7 @@ __global__ __launch_bounds__(kSTPB, kSMinBlocks) void k_gemm_S(int64_t m, const 
                                                   const int64_t *__restrict__ Bp, const int32_t *__restrict__ Bi,
                                                   const T *__restrict__ Bv, int64_t *__restrict__ Cp,
                                                   int32_t *__restrict__ Ci, T *__restrict__ Cv,
-                                                  const T *__restrict__ dC, T *__restrict__ dA, T *__restrict__ dB,
+                                                  const T *__restrict__ dC, T *__restrict__ dA, double *__restrict__ dB,
                                                   BigList wl, BigList big, int use_stage,
                                                   int32_t *__restrict__ cache)
 {
@@ -465,7 +465,7 @@ __global__ __launch_bounds__(kWTPB, CSRK_W_MINB) void k_gemm_W(BigList wl, BigLi
                                                   const int64_t *__restrict__ Bp, const int32_t *__restrict__ Bi,
                                                   const T *__restrict__ Bv, int64_t *__restrict__ Cp,
                                                   int32_t *__restrict__ Ci, T *__restrict__ Cv,
-                                                  const T *__restrict__ dC, T *__restrict__ dA, T *__restrict__ dB)
+                                                  const T *__restrict__ dC, T *__restrict__ dA, double *__restrict__ dB)
 {
     pdl_wait();
     extern __shared__ __align__(16) unsigned char s_dyn[];
@@ -575,7 +575,7 @@ __global__ __launch_bounds__(kWTPB, CSRK_W_MINB) void k_gemm_W(BigList wl, BigLi
                         const int64_t pos = lbound(S.key, nc, j);
                         g = S.val[pos];
                         v = g * bv[u];
-                        if (dB) red_add(&dB[bb[u]], (T)(S.av[tv[u]] * g));
+                        if (dB) atomicAdd(&dB[bb[u]], S.av[tv[u]] * g);
                     }
                     // segmented sum of v over lanes with equal list (nondecreasing in the lane)
                     const int tt = tv[u];
@@ -688,12 +688,9 @@ __device__ __forceinline__ void bitonic_keys(int32_t *key, int P)
 // spread over many threads and the loads of a thread are sequential.
 //   symbolic  one CTA per row: w <= kMMaxW -> products gathered to shared memory, bitonic sort,
 //             unique; else bitmap windows over the column range (sorted for free).
-//   numeric / backward  work items of kItem products (k_big_items: single-CTA scan of the
-//             per-row item counts), many CTAs per long row.  The C row is staged in shared
-//             memory when nnz(C_i) <= kValSm, else a sampled index of it is, and the search
-//             ends in global memory.  Single-item rows accumulate C_i in shared memory;
-//             other rows add into Cv / dA with global atomics after k_big_zero.
-constexpr int kItem = 4096;
+//   numeric / backward  work items = windows of kValSm entries of the C row (k_big_items:
+//             single-CTA scan of the per-row window counts), many CTAs per long row; see
+//             k_gemm_big_win.
 constexpr int kValSm = 4096;
 
 struct BigRows {
@@ -742,37 +739,6 @@ __global__ __launch_bounds__(kGemmTPB) void k_big_prep(BigRows br, const int64_t
 }
 
 constexpr int kItemsTPB = 1024;
-
-// single CTA: items[r] = sum_{r' < r} ceil(w_r' / kItem), items[n] = total
-__global__ __launch_bounds__(kItemsTPB) void k_big_items(BigRows br)
-{
-    pdl_wait();
-    __shared__ int64_t s_w[kItemsTPB / 32];
-    const int n = *(volatile const int *)br.count;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int64_t run = 0;
-    for (int r0 = 0; r0 < n; r0 += kItemsTPB) {
-        const int r = r0 + threadIdx.x;
-        const int64_t c = r < n ? (br.w[r] + kItem - 1) / kItem : 0;
-        int64_t x = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) s_w[warp] = x;
-        __syncthreads();
-        int64_t off = 0, tot = 0;
-        for (int q = 0; q < kItemsTPB / 32; ++q) {
-            if (q < warp) off += s_w[q];
-            tot += s_w[q];
-        }
-        if (r < n) br.items[r] = (int32_t)(run + off + x - c);
-        run += tot;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) br.items[n] = (int32_t)run;
-}
 
 // walk products [e_lo, e_hi) of the row: f(e, a, b) with a = A position, b = B position
 template <typename F>
@@ -879,103 +845,185 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_sym(BigRows br, int64_t n
 }
 
 // ---------------------------------------------------------------- big rows: numeric + backward
-// zero the outputs that multi-item / unstaged rows accumulate into with atomics
-template <typename T, int PH>
+// Work item = (big row i, window q): C entries [Cp[i] + q kValSm, +kValSm) of the row -- their
+// columns (and dC for the backward) staged in shared memory, C values accumulated in fp64 shared
+// memory and written ONCE (no global atomics, no zeroing pass).  Every A entry (i, k) of the row
+// contributes the part of B row k whose columns fall in the window's column range [c_lo, c_hi]
+// (binary searches in B row k when the row has several windows; the whole B row otherwise): a
+// thread per A entry walks short parts, parts longer than 32 products are queued and walked by a
+// warp.  Backward: dA_ik = sum_j dC_ij B_kj is a register (fp64) sum per A entry and window --
+// stored directly when the row has one window, else added (fp64 atomic) into dA64, the fp64
+// target zeroed by k_big_zero; dB_kj += A_ik dC_ij into the fp64 dB target (reading A9).
+constexpr int kWinQ = 256;   // queued long parts per item
+
+__device__ __forceinline__ int64_t lbound64(const int32_t *c, int64_t n, int32_t v)
+{
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(c + mid) < v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// single CTA: items[r] = sum_{r' < r} nwin(r'), items[n] = total;  nwin = max(1, ceil(nnz(C_i) / kValSm))
+__global__ __launch_bounds__(kItemsTPB) void k_big_items(BigRows br, const int64_t *__restrict__ Cp)
+{
+    pdl_wait();
+    __shared__ int64_t s_w[kItemsTPB / 32];
+    const int n = *(volatile const int *)br.count;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t run = 0;
+    for (int r0 = 0; r0 < n; r0 += kItemsTPB) {
+        const int r = r0 + threadIdx.x;
+        int64_t c = 0;
+        if (r < n) {
+            const int64_t i = br.rows[r];
+            const int64_t nc = Cp[i + 1] - Cp[i];
+            c = nc > kValSm ? (nc + kValSm - 1) / kValSm : 1;
+        }
+        int64_t x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_w[warp] = x;
+        __syncthreads();
+        int64_t off = 0, tot = 0;
+        for (int q = 0; q < kItemsTPB / 32; ++q) {
+            if (q < warp) off += s_w[q];
+            tot += s_w[q];
+        }
+        if (r < n) br.items[r] = (int32_t)(run + off + x - c);
+        run += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) br.items[n] = (int32_t)run;
+}
+
+// backward, rows with several windows: zero their entries of the fp64 dA target
 __global__ __launch_bounds__(kGemmTPB) void k_big_zero(BigRows br, const int64_t *__restrict__ Ap,
-                                                       const int64_t *__restrict__ Cp, T *__restrict__ Cv,
-                                                       T *__restrict__ dA)
+                                                       const int64_t *__restrict__ Cp, double *__restrict__ dA64)
 {
     pdl_wait();
     const int n = *(volatile const int *)br.count;
     for (int r = blockIdx.x; r < n; r += gridDim.x) {
         const int64_t i = br.rows[r];
-        if (PH == PH_NUM) {
-            const int64_t cs = Cp[i], ce = Cp[i + 1];
-            if (br.w[r] <= kItem && ce - cs <= kValSm) continue;
-            for (int64_t e = cs + threadIdx.x; e < ce; e += kGemmTPB) Cv[e] = (T)0;
-        } else if (dA) {
-            for (int64_t e = Ap[i] + threadIdx.x; e < Ap[i + 1]; e += kGemmTPB) dA[e] = (T)0;
-        }
+        if (Cp[i + 1] - Cp[i] <= kValSm) continue;
+        for (int64_t e = Ap[i] + threadIdx.x; e < Ap[i + 1]; e += kGemmTPB) dA64[e] = 0.0;
+    }
+}
+
+// backward, fp32 data: round the fp64 dA of multi-window rows once
+__global__ __launch_bounds__(kGemmTPB) void k_big_cvt(BigRows br, const int64_t *__restrict__ Ap,
+                                                      const int64_t *__restrict__ Cp, const double *__restrict__ dA64,
+                                                      float *__restrict__ dA)
+{
+    pdl_wait();
+    const int n = *(volatile const int *)br.count;
+    for (int r = blockIdx.x; r < n; r += gridDim.x) {
+        const int64_t i = br.rows[r];
+        if (Cp[i + 1] - Cp[i] <= kValSm) continue;
+        for (int64_t e = Ap[i] + threadIdx.x; e < Ap[i + 1]; e += kGemmTPB) dA[e] = (float)dA64[e];
     }
 }
 
 template <typename T, int PH>
-__global__ __launch_bounds__(kGemmTPB) void k_gemm_big_val(BigRows br, const int64_t *__restrict__ Ap,
+__global__ __launch_bounds__(kGemmTPB) void k_gemm_big_win(BigRows br, const int64_t *__restrict__ Ap,
                                                            const int32_t *__restrict__ Ai, const T *__restrict__ Av,
                                                            const int64_t *__restrict__ Bp,
                                                            const int32_t *__restrict__ Bi, const T *__restrict__ Bv,
                                                            const int64_t *__restrict__ Cp,
                                                            const int32_t *__restrict__ Ci, T *__restrict__ Cv,
                                                            const T *__restrict__ dC, T *__restrict__ dA,
-                                                           T *__restrict__ dB)
+                                                           double *__restrict__ dA64, double *__restrict__ dB)
 {
     pdl_wait();
-    __shared__ int32_t s_col[kValSm];
-    __shared__ double s_acc[kValSm];
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    double *s_val = reinterpret_cast<double *>(s_dyn);                  // NUM: accumulators; BWD: dC
+    int32_t *s_col = reinterpret_cast<int32_t *>(s_val + kValSm);       // the window's C columns
+    __shared__ int64_t s_qa[kWinQ], s_qlo[kWinQ], s_qhi[kWinQ];
+    __shared__ int s_nq;
     const int n = *(volatile const int *)br.count;
     const int total = n > 0 ? br.items[n] : 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int it = blockIdx.x; it < total; it += gridDim.x) {
-        // the row r holding item it: last r with items[r] <= it
-        int lo = 0, hi = n - 1;
+        int lo = 0, hi = n - 1;   // the row r holding item it: last r with items[r] <= it
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
             if (br.items[mid] <= it) lo = mid; else hi = mid - 1;
         }
         const int r = lo;
         const int64_t i = br.rows[r];
-        const int64_t as = Ap[i], ae = Ap[i + 1], w = br.w[r];
-        const int64_t e0 = (int64_t)(it - br.items[r]) * kItem;
-        const int64_t e1 = e0 + kItem < w ? e0 + kItem : w;
-        const int64_t cs = Cp[i], nc = Cp[i + 1] - cs;
-        const bool insm = nc <= kValSm;
-        const bool local = PH == PH_NUM && insm && w <= kItem;  // accumulate the row in shared memory
-        const int64_t stride = insm ? 1 : (nc + kValSm - 1) / kValSm;
-        const int nq = (int)((nc + stride - 1) / stride);
-        for (int q = threadIdx.x; q < nq; q += kGemmTPB) {
-            s_col[q] = Ci[cs + (int64_t)q * stride];
-            if (local) s_acc[q] = 0.0;
-            if (PH == PH_BWD && insm) s_acc[q] = (double)dC[cs + q];
+        const int64_t as = Ap[i], ae = Ap[i + 1];
+        const int64_t row_nc = Cp[i + 1] - Cp[i];
+        const bool single = row_nc <= kValSm;
+        const int64_t cs = Cp[i] + (int64_t)(it - br.items[r]) * kValSm;
+        const int nc = (int)(Cp[i + 1] - cs < kValSm ? Cp[i + 1] - cs : kValSm);
+        for (int q = threadIdx.x; q < nc; q += kGemmTPB) {
+            s_col[q] = Ci[cs + q];
+            s_val[q] = PH == PH_NUM ? 0.0 : (double)dC[cs + q];
+        }
+        if (threadIdx.x == 0) s_nq = 0;
+        __syncthreads();
+        const int32_t c_lo = nc > 0 ? s_col[0] : 0, c_hi = nc > 0 ? s_col[nc - 1] : -1;
+        // one product b of A entry a (value av): NUM adds av B_kj into C_ij; BWD returns dC_ij B_kj
+        auto prod = [&](double av, int64_t b, double &dacc) {
+            const int32_t j = __ldg(Bi + b);
+            const double bv = (double)__ldg(Bv + b);
+            const int pos = (int)lbound(s_col, nc, j);
+            if (PH == PH_NUM) {
+                atomicAdd(&s_val[pos], av * bv);
+            } else {
+                const double g = s_val[pos];
+                dacc = fma(g, bv, dacc);
+                if (dB) atomicAdd(&dB[b], av * g);
+            }
+        };
+        auto put_dA = [&](int64_t a, double dacc, bool any) {
+            if (PH != PH_BWD || !dA) return;
+            if (single) dA[a] = (T)dacc;
+            else if (any) atomicAdd(&dA64[a], dacc);
+        };
+        for (int64_t a = as + threadIdx.x; a < ae; a += kGemmTPB) {
+            const int32_t k = Ai[a];
+            const double av = (double)Av[a];
+            int64_t b0 = Bp[k], b1 = Bp[k + 1];
+            if (!single && b1 > b0) {   // the part of B row k inside [c_lo, c_hi]
+                const int64_t l0 = b0 + lbound64(Bi + b0, b1 - b0, c_lo);
+                b1 = l0 + lbound64(Bi + l0, b1 - l0, c_hi + 1);
+                b0 = l0;
+            }
+            if (b1 - b0 > 32) {
+                const int slot = atomicAdd(&s_nq, 1);
+                if (slot < kWinQ) {
+                    s_qa[slot] = a;
+                    s_qlo[slot] = b0;
+                    s_qhi[slot] = b1;
+                    continue;
+                }
+            }
+            double dacc = 0.0;
+            for (int64_t b = b0; b < b1; ++b) prod(av, b, dacc);
+            put_dA(a, dacc, b1 > b0);
         }
         __syncthreads();
-        const int64_t per = (e1 - e0 + kGemmTPB - 1) / kGemmTPB;
-        const int64_t p_lo = e0 + threadIdx.x * per, p_hi = p_lo + per < e1 ? p_lo + per : e1;
-        int64_t cur_a = -1;
-        double av = 0.0, dacc = 0.0;
-        big_walk(br.loff, Ai, Bp, as, ae, p_lo, p_hi, [&](int64_t, int64_t a, int64_t b) {
-            if (a != cur_a) {
-                if (PH == PH_BWD && cur_a >= 0 && dA) red_add(&dA[cur_a], (T)dacc);
-                cur_a = a;
-                av = (double)Av[a];
-                dacc = 0.0;
+        const int nq = s_nq < kWinQ ? s_nq : kWinQ;
+        for (int e = warp; e < nq; e += kGemmTPB / 32) {   // long parts: a warp each, fixed lane order
+            const int64_t a = s_qa[e];
+            const double av = (double)Av[a];
+            double dacc = 0.0;
+            for (int64_t b = s_qlo[e] + lane; b < s_qhi[e]; b += 32) prod(av, b, dacc);
+            if (PH == PH_BWD) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) dacc += __shfl_xor_sync(0xffffffffu, dacc, o);
+                if (lane == 0) put_dA(a, dacc, true);
             }
-            const int32_t j = Bi[b];
-            const double bv = (double)Bv[b];
-            int64_t pos;
-            if (insm) {
-                pos = lbound(s_col, nc, j);
-            } else {
-                int qlo = 0, qhi = nq - 1;  // last q with s_col[q] <= j
-                while (qlo < qhi) {
-                    const int mid = (qlo + qhi + 1) >> 1;
-                    if (s_col[mid] <= j) qlo = mid; else qhi = mid - 1;
-                }
-                const int64_t base = (int64_t)qlo * stride;
-                const int64_t len = base + stride < nc ? stride : nc - base;
-                pos = base + lbound(Ci + cs + base, len, j);
-            }
-            if (PH == PH_NUM) {
-                if (local) atomicAdd(&s_acc[pos], av * bv);
-                else red_add(&Cv[cs + pos], (T)(av * bv));
-            } else {
-                const double g = insm ? s_acc[pos] : (double)dC[cs + pos];
-                dacc = fma(g, bv, dacc);
-                if (dB) red_add(&dB[b], (T)(av * g));
-            }
-        });
-        if (PH == PH_BWD && cur_a >= 0 && dA) red_add(&dA[cur_a], (T)dacc);
+        }
         __syncthreads();
-        if (local)
-            for (int64_t e = threadIdx.x; e < nc; e += kGemmTPB) Cv[cs + e] = (T)s_acc[e];
+        if (PH == PH_NUM)
+            for (int q = threadIdx.x; q < nc; q += kGemmTPB) Cv[cs + q] = (T)s_val[q];
         __syncthreads();
     }
 }
@@ -984,6 +1032,7 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_val(BigRows br, const int
 static unsigned big_grid() { return (unsigned)(kNumSMs * 2); }
 
 static size_t big_sym_smem() { return sizeof(uint32_t) * kBitmapWords; }
+static size_t big_win_smem() { return (sizeof(double) + sizeof(int32_t)) * kValSm; }
 static size_t big_sort_smem() { return sizeof(int32_t) * kMMaxW; }
 static unsigned sort_grid() { return (unsigned)(kNumSMs * 4); }
 static unsigned val_grid() { return (unsigned)(kNumSMs * 4); }
@@ -998,8 +1047,8 @@ static unsigned wgrid(size_t smem)
 
 static int set_smem_attrs()
 {
-    static bool done = false;
-    if (done) return CSRK_OK;
+    static DevOnce once;
+    if (!once.need()) return CSRK_OK;
     const int bs = (int)big_sym_smem();
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_sym<PH_COUNT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bs));
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_sym<PH_FILL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bs));
@@ -1016,7 +1065,12 @@ static int set_smem_attrs()
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, ww));
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<float, PH_NUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, ww));
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<float, PH_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, ww));
-    done = true;
+    const int bw = (int)big_win_smem();
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_win<double, PH_NUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_win<double, PH_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_win<float, PH_NUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_win<float, PH_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw));
+    once.done();
     return CSRK_OK;
 }
 
@@ -1094,6 +1148,16 @@ static std::mutex g_stamp_mu;
 static std::vector<CountStamp> g_stamps;  // one per workspace in use (a handful)
 static int use_fill_cache() { static int v = knob("GEMM_FILL_CACHE", 1); return v; }
 
+void gemm_fill_cache_invalidate(const void *ws, size_t bytes)
+{
+    const char *lo = static_cast<const char *>(ws), *hi = lo + bytes;
+    std::lock_guard<std::mutex> g(g_stamp_mu);
+    for (size_t q = 0; q < g_stamps.size(); ++q) {
+        const char *w = static_cast<const char *>(g_stamps[q].ws);
+        if (w >= lo && w < hi) g_stamps.erase(g_stamps.begin() + (long)q--);
+    }
+}
+
 int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, int32_t *Ci, int64_t *nnzC_host,
                     Bump &ws, cudaStream_t s)
 {
@@ -1170,6 +1234,20 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, i
     return CSRK_OK;
 }
 
+// fp64 target of an atomic scatter into out[n] (reading A5): out itself for fp64 data, else scratch
+template <typename T>
+static int round_f64(const double *acc, T *out, int64_t n, cudaStream_t s)
+{
+    if constexpr (sizeof(T) == sizeof(double)) return CSRK_OK;
+    else return f64_to_f32(acc, out, n, s);
+}
+template <typename T>
+static double *f64_target(T *out, int64_t n, Bump &ws)
+{
+    if constexpr (sizeof(T) == sizeof(double)) return reinterpret_cast<double *>(out);
+    else return ws.take<double>(n > 0 ? n : 1);
+}
+
 template <typename T>
 static int spgemm_values_t(int PH, const csrk_pattern &A, const T *Av, const csrk_pattern &B, const T *Bv,
                            const csrk_pattern &C, T *Cv, const T *dC, T *dA, T *dB, Bump &ws, cudaStream_t s)
@@ -1177,43 +1255,51 @@ static int spgemm_values_t(int PH, const csrk_pattern &A, const T *Av, const csr
     BigList wl{}, b{};
     BigRows br{};
     carve_lists(A, wl, b, br, ws);
+    // backward: fp64 targets of the dB scatter and of the multi-window big-row dA (fp32 data:
+    // scratch, rounded once at the end)
+    double *dB64 = nullptr, *dA64 = nullptr;
+    if (PH == PH_BWD) {
+        if (dB || ws.sizing()) dB64 = f64_target(dB, B.nnz, ws);
+        if (dA || ws.sizing()) dA64 = f64_target(dA, A.nnz, ws);
+    }
     if (ws.sizing()) return CSRK_OK;
     CSRK_TRY(set_smem_attrs());
-    if (PH == PH_BWD && dB) CSRK_CUDA(cudaMemsetAsync(dB, 0, sizeof(T) * (size_t)B.nnz, s));
+    if (PH == PH_BWD && dB) CSRK_CUDA(cudaMemsetAsync(dB64, 0, sizeof(double) * (size_t)B.nnz, s));
     const int64_t m = A.nrows;
-    if (m == 0) return CSRK_OK;
+    if (m == 0) return dB ? round_f64(dB64, dB, B.nnz, s) : CSRK_OK;
     CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 4 * sizeof(int), s));
     const unsigned gS = (unsigned)cdiv(m, kSTPB);
     int64_t *Cp = const_cast<int64_t *>(C.indptr);
     T *tn = nullptr;
     const T *ctn = nullptr;
+    double *dn = nullptr;
     if (PH == PH_NUM) {
         const int sn = stage_num(A, C);
         CSRK_TRY((launch_S<T, PH_NUM>)(B.nnz < INT32_MAX, gS, s_smem<T>(PH_NUM, sn), s, m, A.indptr, A.indices,
-                    Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, Cv, ctn, tn, tn, wl, b, sn,
+                    Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, Cv, ctn, tn, dn, wl, b, sn,
                     (int32_t *)nullptr));
-        CSRK_LAUNCH((k_gemm_W<T, PH_NUM>), wgrid((wsm<kWW, PH_NUM>())), kWTPB, (wsm<kWW, PH_NUM>()), s, wl, b, BigList{}, A.indptr, A.indices, Av,
-                    B.indptr,
-                    B.indices, Bv, Cp, const_cast<int32_t *>(C.indices), Cv, ctn, tn, tn);
-        CSRK_LAUNCH(k_big_prep, big_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, B.indptr);
-        CSRK_LAUNCH(k_big_items, 1, kItemsTPB, 0, s, br);
-        CSRK_LAUNCH((k_big_zero<T, PH_NUM>), big_grid(), kGemmTPB, 0, s, br, A.indptr, C.indptr, Cv, tn);
-        CSRK_LAUNCH((k_gemm_big_val<T, PH_NUM>), val_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, Av, B.indptr,
-                    B.indices, Bv, C.indptr, C.indices, Cv, ctn, tn, tn);
-    } else {
-        CSRK_TRY((launch_S<T, PH_BWD>)(B.nnz < INT32_MAX, gS, s_smem<T>(PH_BWD, stage_vals()), s, m, A.indptr, A.indices,
-                    Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, tn, dC, dA, dB, wl, b, stage_vals(),
-                    (int32_t *)nullptr));
-        CSRK_LAUNCH((k_gemm_W<T, PH_BWD>), wgrid((wsm<kWW, PH_BWD>())), kWTPB, (wsm<kWW, PH_BWD>()), s, wl, b, BigList{}, A.indptr, A.indices, Av,
-                    B.indptr,
-                    B.indices, Bv, Cp, const_cast<int32_t *>(C.indices), tn, dC, dA, dB);
-        CSRK_LAUNCH(k_big_prep, big_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, B.indptr);
-        CSRK_LAUNCH(k_big_items, 1, kItemsTPB, 0, s, br);
-        CSRK_LAUNCH((k_big_zero<T, PH_BWD>), big_grid(), kGemmTPB, 0, s, br, A.indptr, C.indptr, tn, dA);
-        CSRK_LAUNCH((k_gemm_big_val<T, PH_BWD>), val_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, Av, B.indptr,
-                    B.indices, Bv, C.indptr, C.indices, tn, dC, dA, dB);
+        CSRK_LAUNCH((k_gemm_W<T, PH_NUM>), wgrid((wsm<kWW, PH_NUM>())), kWTPB, (wsm<kWW, PH_NUM>()), s, wl, b,
+                    BigList{}, A.indptr, A.indices, Av, B.indptr, B.indices, Bv, Cp,
+                    const_cast<int32_t *>(C.indices), Cv, ctn, tn, dn);
+        CSRK_LAUNCH(k_big_items, 1, kItemsTPB, 0, s, br, (const int64_t *)Cp);
+        CSRK_LAUNCH((k_gemm_big_win<T, PH_NUM>), val_grid(), kGemmTPB, big_win_smem(), s, br, A.indptr, A.indices, Av,
+                    B.indptr, B.indices, Bv, C.indptr, C.indices, Cv, ctn, tn, dn, dn);
+        return CSRK_OK;
     }
-    return CSRK_OK;
+    CSRK_TRY((launch_S<T, PH_BWD>)(B.nnz < INT32_MAX, gS, s_smem<T>(PH_BWD, stage_vals()), s, m, A.indptr,
+                A.indices, Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, tn, dC, dA, dB ? dB64 : dn, wl, b,
+                stage_vals(), (int32_t *)nullptr));
+    CSRK_LAUNCH((k_gemm_W<T, PH_BWD>), wgrid((wsm<kWW, PH_BWD>())), kWTPB, (wsm<kWW, PH_BWD>()), s, wl, b,
+                BigList{}, A.indptr, A.indices, Av, B.indptr, B.indices, Bv, Cp, const_cast<int32_t *>(C.indices),
+                tn, dC, dA, dB ? dB64 : dn);
+    CSRK_LAUNCH(k_big_items, 1, kItemsTPB, 0, s, br, (const int64_t *)Cp);
+    if (dA) CSRK_LAUNCH(k_big_zero, big_grid(), kGemmTPB, 0, s, br, A.indptr, C.indptr, dA64);
+    CSRK_LAUNCH((k_gemm_big_win<T, PH_BWD>), val_grid(), kGemmTPB, big_win_smem(), s, br, A.indptr, A.indices, Av,
+                B.indptr, B.indices, Bv, C.indptr, C.indices, tn, dC, dA, dA ? dA64 : dn, dB ? dB64 : dn);
+    if constexpr (sizeof(T) == sizeof(float)) {
+        if (dA) CSRK_LAUNCH(k_big_cvt, big_grid(), kGemmTPB, 0, s, br, A.indptr, C.indptr, (const double *)dA64, dA);
+    }
+    return dB ? round_f64(dB64, dB, B.nnz, s) : CSRK_OK;
 }
 
 int spgemm_numeric(csrk_dtype dt, const csrk_pattern &A, const void *A_val, const csrk_pattern &B, const void *B_val,

@@ -406,10 +406,10 @@ static int launch_spmm_bulk(const SpmmArgs<T> &a, cudaStream_t s)
     const int rb = (int)(a.k * (int64_t)sizeof(T));
     const int cap = kBulkBytes / rb;
     const size_t smem = 2 * ((size_t)cap * rb + (size_t)cap * sizeof(double));
-    static bool attr = false;
-    if (!attr) {
+    static DevOnce attr;
+    if (attr.need()) {
         CSRK_CUDA(cudaFuncSetAttribute(k_spmm_bulk<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr = true;
+        attr.done();
     }
     const int64_t ntiles = cdiv(a.nrows, kBulkRT);
     const int64_t grid = ntiles < (int64_t)kNumSMs * 2 ? ntiles : (int64_t)kNumSMs * 2;

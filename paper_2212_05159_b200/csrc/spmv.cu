@@ -16,12 +16,28 @@ static int run(TileArgs<T> a, const RowList &L, cudaStream_t s)
     return launch_rows<T, MODE, PERM, SIDE>(a, L, s);
 }
 
+// fp64 target of an atomic A^T scatter into y[n]: y itself for fp64 data, workspace scratch for
+// fp32 data (rounded once by round_scatter; reading A5)
+template <typename T>
+static double *scatter_target(T *y, int64_t n, Bump &ws)
+{
+    if constexpr (sizeof(T) == sizeof(double)) return reinterpret_cast<double *>(y);
+    else return ws.take<double>(n > 0 ? n : 1);
+}
+template <typename T>
+static int round_scatter(const double *acc, T *y, int64_t n, cudaStream_t s)
+{
+    if constexpr (sizeof(T) == sizeof(double)) return CSRK_OK;
+    else return f64_to_f32(acc, y, n, s);
+}
+
 template <typename T>
 static int spmv_fwd_t(csrk_op op, const csrk_pattern &A, const T *A_val, const csrk_pattern *AT,
                       const int64_t *perm, const T *x, T *y, Bump &ws, cudaStream_t s)
 {
     RowList L{};
     carve_rowlist(A.nrows > A.ncols ? A.nrows : A.ncols, L, ws);
+    double *acc = (op == CSRK_OP_T && !AT) ? scatter_target(y, A.ncols, ws) : nullptr;
     if (ws.sizing()) return CSRK_OK;
     TileArgs<T> a{};
     if (op == CSRK_OP_N) {
@@ -38,12 +54,13 @@ static int spmv_fwd_t(csrk_op op, const csrk_pattern &A, const T *A_val, const c
         a.R = tile_rows(AT->nrows, AT->nnz);
         return run<T, MODE_REDUCE, true, false>(a, L, s);
     }
-    // y = A^T x by atomic scatter of A_ij x_i into y_j
-    CSRK_CUDA(cudaMemsetAsync(y, 0, sizeof(T) * (size_t)A.ncols, s));
+    // y = A^T x by atomic scatter of A_ij x_i into y_j (fp64 target, reading A5)
+    CSRK_CUDA(cudaMemsetAsync(acc, 0, sizeof(double) * (size_t)A.ncols, s));
     a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices;
-    a.vals = A_val; a.u = x; a.y = y;
+    a.vals = A_val; a.u = x; a.y64 = acc;
     a.R = tile_rows(A.nrows, A.nnz);
-    return run<T, MODE_SCATTER, false, false>(a, L, s);
+    CSRK_TRY((run<T, MODE_SCATTER, false, false>(a, L, s)));
+    return round_scatter(acc, y, A.ncols, s);
 }
 
 template <typename T>
@@ -52,6 +69,8 @@ static int spmv_bwd_t(csrk_op op, const csrk_pattern &A, const T *A_val, const c
 {
     RowList L{};
     carve_rowlist(A.nrows > A.ncols ? A.nrows : A.ncols, L, ws);
+    // atomic dx (op N without a plan): fp64 target (sized whenever the call could need it)
+    double *acc = (op == CSRK_OP_N && !(AT && dx) && (dx || ws.sizing())) ? scatter_target(dx, A.ncols, ws) : nullptr;
     if (ws.sizing()) return CSRK_OK;
     TileArgs<T> a{};
     if (op == CSRK_OP_T) {
@@ -82,13 +101,14 @@ static int spmv_bwd_t(csrk_op op, const csrk_pattern &A, const T *A_val, const c
         }
         return run<T, MODE_REDUCE, true, false>(a, L, s);
     }
-    // row traversal: dA[p] = dy_i x[idx p] (coalesced), dx[idx p] += A[p] dy_i (atomic)
-    if (dx) CSRK_CUDA(cudaMemsetAsync(dx, 0, sizeof(T) * (size_t)A.ncols, s));
+    // row traversal: dA[p] = dy_i x[idx p] (coalesced), dx[idx p] += A[p] dy_i (fp64 atomic)
+    if (dx) CSRK_CUDA(cudaMemsetAsync(acc, 0, sizeof(double) * (size_t)A.ncols, s));
     a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices;
-    a.vals = A_val; a.u = dy; a.v = x; a.y = dx; a.D = dA;
+    a.vals = A_val; a.u = dy; a.v = x; a.y64 = dx ? acc : nullptr; a.D = dA;
     a.R = tile_rows(A.nrows, A.nnz);
-    if (dA) return run<T, MODE_SCATTER, false, true>(a, L, s);
-    return run<T, MODE_SCATTER, false, false>(a, L, s);
+    if (dA) CSRK_TRY((run<T, MODE_SCATTER, false, true>(a, L, s)));
+    else CSRK_TRY((run<T, MODE_SCATTER, false, false>(a, L, s)));
+    return dx ? round_scatter(acc, dx, A.ncols, s) : CSRK_OK;
 }
 
 int spmv_fwd(csrk_dtype dt, csrk_op op, const csrk_pattern &A, const void *A_val, const csrk_pattern *AT,

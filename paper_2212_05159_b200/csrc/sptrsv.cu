@@ -15,8 +15,10 @@
 //                 (apply).  Two streaming passes and no waiting between CTAs: a 16.7M-row chain
 //                 that the sync-free method would walk one dependency at a time runs like two
 //                 SpMVs.  A row with any other dependency sets `abort` (apply and carry skip).
-//                 (A single-pass decoupled look-back was measured slower: 8192 tiles in flight
-//                 walk back through each other's aggregates.)
+//                 This three-kernel form is kept behind CSRK_TRSV_LOOKBACK=0; the default is
+//                 the single-pass decoupled look-back k_trsv_chain_lb (below), measured faster
+//                 (0.55 vs 0.87 ms on the 16.7M-row config-5 L) once its look-back resolved 32
+//                 predecessors per round.
 //   k_trsv_sf     the synchronisation-free solve the paper uses (Capellini et al.):
 //                 warps take 32-row blocks in solve order from an atomic ticket; each lane
 //                 owns a row, waits (acquire) on the ready flag of every dependency outside
@@ -652,7 +654,10 @@ __global__ void k_trsv_dT(int64_t n, const int64_t *__restrict__ indptr, const i
 template <typename T>
 static int carve_solve(TrsvArgs<T> &a, int64_t n, Bump &ws)
 {
-    const int64_t ntiles = cdiv(n, kChTile);
+    // tile arrays serve both chain kernels: the three-kernel form (kChTile rows per tile) and the
+    // look-back form (kLbTile rows per tile) -- sized for the one with more tiles
+    const int64_t nt0 = cdiv(n, kChTile), nt1 = cdiv(n, kLbTile);
+    const int64_t ntiles = nt0 > nt1 ? nt0 : nt1;
     a.aggA = ws.take<double>(ntiles > 0 ? ntiles : 1);
     a.aggC = ws.take<double>(ntiles > 0 ? ntiles : 1);
     a.inclX = ws.take<double>(ntiles > 0 ? ntiles : 1);

@@ -11,7 +11,7 @@
 //                traversal of the backward pass).  Deterministic: partial sums of
 //                rows spanning several threads/chunks are combined in thread order.
 //                SIDE adds D[pv] = v[idx p] * u[row]    (the masked outer product).
-// MODE_SCATTER : w = u[row]; SIDE: D[p] = w * v[idx p]; y (nullable): y[idx p] += val[p]*w
+// MODE_SCATTER : w = u[row]; SIDE: D[p] = w * v[idx p]; y64 (nullable): y64[idx p] += val[p]*w
 //                (atomic A^T v, "atomically reduced into correct entries").
 // MODE_TRANSPOSE: slot = cursor[idx p]++; ATi[slot] = row; perm[slot] = p  (counting-sort
 //                scatter of csr_transpose; order inside a column fixed by a later sort).
@@ -37,7 +37,9 @@ struct TileArgs {
     const T *vals;          // REDUCE/SCATTER values (indexed by pv / p)
     const int64_t *perm;    // REDUCE with PERM: value position = perm[p]
     const T *v;             // column-gathered vector
-    T *y;                   // REDUCE: y[row];  SCATTER: y[col] (atomic, nullable)
+    T *y;                   // REDUCE: y[row]
+    double *y64;            // SCATTER: y64[col] += val * w, fp64 atomics (nullable); fp32 data
+                            // accumulates here too and is rounded once afterwards (reading A5)
     const T *u;             // row vector (SIDE / SCATTER)
     T *D;                   // SIDE output aligned with the values
     int64_t *cursor;        // TRANSPOSE
@@ -161,7 +163,7 @@ __global__ __launch_bounds__(kTileTPB) void k_csr_tile(TileArgs<T> a)
                     if (MODE == MODE_SCATTER) {
                         const T w = s_u[r];
                         if (SIDE) a.D[p] = w * a.v[c];
-                        if (a.y) red_add(&a.y[c], (T)((double)a.vals[p] * (double)w));
+                        if (a.y64) atomicAdd(&a.y64[c], (double)a.vals[p] * (double)w);
                     } else if (MODE == MODE_REDUCE) {
                         const int64_t pv = PERM ? a.perm[p] : p;
                         a.D[pv] = a.v[c] * s_u[r];
@@ -264,7 +266,7 @@ __global__ __launch_bounds__(kTileTPB) void k_csr_tile(TileArgs<T> a)
                 if (MODE == MODE_SCATTER) {
                     const T w = s_u[r];
                     if (SIDE) a.D[p] = w * a.v[c];
-                    if (a.y) red_add(&a.y[c], (T)((double)a.vals[p] * (double)w));
+                    if (a.y64) atomicAdd(&a.y64[c], (double)a.vals[p] * (double)w);
                 } else if (MODE == MODE_REDUCE) {  // SIDE
                     const int64_t pv = PERM ? a.perm[p] : p;
                     a.D[pv] = a.v[c] * s_u[r];
@@ -300,12 +302,12 @@ int launch_tile(const TileArgs<T> &a, cudaStream_t s)
 {
     if (a.nrows <= 0) return CSRK_OK;
     const size_t smem = tile_smem<T>(a.R, MODE, SIDE).total;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static DevOnce attr;
+    if (attr.need()) {
         if (cudaFuncSetAttribute(k_csr_tile<T, MODE, PERM, SIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  64 * 1024) != cudaSuccess)
             return CSRK_ERR_CUDA;
-        attr_set = true;
+        attr.done();
     }
     const int64_t grid = cdiv(a.nrows, a.R);
     CSRK_LAUNCH((k_csr_tile<T, MODE, PERM, SIDE>), (unsigned)grid, kTileTPB, smem, s, a);

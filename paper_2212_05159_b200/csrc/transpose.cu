@@ -357,11 +357,11 @@ int transpose_impl(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int6
         CSRK_LAUNCH(k_sort_warp, (unsigned)(kNumSMs * 4), 32 * kWarpsPerSortCTA, 0, s, (const int64_t *)ATp,
                     (const uint64_t *)keys, ATi, pm, L);
     const size_t big_smem = sizeof(uint64_t) * kBlockMax;
-    static bool attr = false;
-    if (!attr) {
+    static DevOnce attr;
+    if (attr.need()) {
         CSRK_CUDA(cudaFuncSetAttribute(k_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big_smem));
         CSRK_CUDA(cudaFuncSetAttribute(k_sort_huge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big_smem));
-        attr = true;
+        attr.done();
     }
     if (nnz > kWarpMax)
         CSRK_LAUNCH(k_sort_block, (unsigned)kNumSMs, kSortTPB, big_smem, s, (const int64_t *)ATp,

@@ -136,6 +136,22 @@ size_t scan_ws_bytes(int64_t n)
     return b.used;
 }
 
+// ---------------------------------------------------------------- fp64 accumulation -> fp32
+__global__ __launch_bounds__(256) void k_f64_to_f32(const double *__restrict__ src, float *__restrict__ dst, int64_t n)
+{
+    pdl_wait();
+    for (int64_t i = blockIdx.x * (int64_t)256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256)
+        dst[i] = (float)src[i];
+}
+
+int f64_to_f32(const double *src, float *dst, int64_t n, cudaStream_t s)
+{
+    if (n <= 0) return CSRK_OK;
+    const int64_t g = cdiv(n, 256);
+    CSRK_LAUNCH(k_f64_to_f32, (unsigned)(g < kNumSMs * 8 ? g : kNumSMs * 8), 256, 0, s, src, dst, n);
+    return CSRK_OK;
+}
+
 // ---------------------------------------------------------------- validation (CSRK_VALIDATE=1)
 __device__ int g_bad_pattern;
 

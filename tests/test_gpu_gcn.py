@@ -81,12 +81,14 @@ def test_gcn_layer(ck, dt):
     Y, D = ck.gcn_layer_fwd(Ad, t(X), t(W), t(b))
     dX, dW, db = ck.gcn_layer_bwd(Ad, D, t(X), t(W), t(dY))
     ref = ogcn.gcn_layer(A, X, W, b, want_grad=dY)
-    # composite tolerance: the layer's terms are products of the propagation's and the GEMM's
+    # composite S (reading R-GCN): the propagation's magnitude over |X||W| bounds every stage's
+    # terms (the GEMM, the rounding of Z = X W to dtype, the propagation); rtol >> u covers the sum
+    # of the stages' first-order errors
     P = ogcn.gcn_prop(A, np.abs(X.astype(np.float64)) @ np.abs(W.astype(np.float64)), np.abs(b), want_grad=np.abs(dY))
-    assert_S_close(Y.cpu().numpy(), ref["Y"], 4 * P["S"], RTOL[dt], "layer Y")
+    assert_S_close(Y.cpu().numpy(), ref["Y"], P["S"], RTOL[dt], "layer Y")
     SdZ = P["S_dZ"]
-    assert_S_close(dX.cpu().numpy(), ref["dX"], 4 * SdZ @ np.abs(W.astype(np.float64)).T, RTOL[dt], "layer dX")
-    assert_S_close(dW.cpu().numpy(), ref["dTheta"], 4 * np.abs(X.astype(np.float64)).T @ SdZ, RTOL[dt], "layer dTheta")
+    assert_S_close(dX.cpu().numpy(), ref["dX"], SdZ @ np.abs(W.astype(np.float64)).T, RTOL[dt], "layer dX")
+    assert_S_close(dW.cpu().numpy(), ref["dTheta"], np.abs(X.astype(np.float64)).T @ SdZ, RTOL[dt], "layer dTheta")
     assert_S_close(db.cpu().numpy(), ref["dbias"], P["S_dbias"], RTOL[dt], "layer dbias")
 
 

@@ -57,6 +57,77 @@ def test_oracle_gradient_finite_differences():
     assert np.all(g[~P] == 0)
 
 
+# ---------------------------------------------------------------- CPU pins (orientation, sparse oracle)
+def _inverse_factor_case(N=5):
+    """L = chol(A^{-1}) (lower, dense lower pattern) so that L L^T = A^{-1} exactly."""
+    from util import csr_from_pattern
+    A = synth.poisson2d(N)
+    Ad = to_dense(A)
+    Lc = np.linalg.cholesky(np.linalg.inv(Ad))
+    P = np.tril(np.ones_like(Ad)).astype(bool)
+    return A, Ad, P, Lc, csr_from_pattern(P, Lc[P])
+
+
+def test_pcg_mult_inverse_factor_converges_in_one_step(orc):
+    """P:838 M = L L^T.  With L = chol(A^{-1}) the preconditioner is A^{-1}, so the first PCG step
+    solves A x = b: ||r^(1)|| vanishes to rounding.  An oracle that applied L^T L instead would
+    not converge (checked: same L passed transposed gives ||r^(1)|| / ||b|| ~ 0.17).  Pins both the
+    dense and the sparse oracle."""
+    from oracle import pcg
+    A, Ad, P, Lc, Ls = _inverse_factor_case()
+    b = synth.dense(A.nrows, 3)
+    nb = np.linalg.norm(b)
+    _, res, _ = pcg.pcg_loss_grad(Ad, P, Lc, b, 3, 0.6)
+    assert res[0] <= 1e-13 * nb
+    _, res_s, _, _ = pcg.pcg_loss_grad_sparse(A, Ls, b, 3, 0.6)
+    assert res_s[0] <= 1e-13 * nb
+    _, res_t, _ = pcg.pcg_loss_grad(Ad, P.T, Lc.T, b, 3, 0.6)     # L^T L: the wrong orientation
+    assert res_t[0] >= 1e-2 * nb
+
+
+@pytest.mark.parametrize("precond", ["mult", "solve"])
+@pytest.mark.parametrize("N,init,n_it", [(6, "seeded", 4), (8, "identity", 6), (16, "seeded", 50),
+                                         (24, "seeded", 30)])
+def test_sparse_oracle_matches_dense_oracle(orc, N, init, n_it, precond):
+    """The CSR oracle (C oracle products under torch autograd) against the dense torch oracle:
+    loss, residual history and dL elementwise on the S-scale of the sparse oracle."""
+    from oracle import pcg
+    A, L, b = problem(N, init)
+    l1, r1, g1 = pcg.pcg_loss_grad(to_dense(A), pattern_dense(L), to_dense(L), b, n_it, 0.6, precond=precond)
+    l2, r2, g2, S = pcg.pcg_loss_grad_sparse(A, L, b, n_it, 0.6, precond=precond)
+    rows = np.repeat(np.arange(L.nrows), np.diff(L.indptr))
+    assert abs(l1 - l2) <= 1e-11 * abs(l1)
+    np.testing.assert_allclose(r2, r1, rtol=1e-10)
+    assert np.all(np.abs(g1[rows, L.indices] - g2) <= 1e-11 * S)
+    assert np.all(np.abs(g2) <= S * (1 + 1e-12))          # S bounds the gradient it scales
+
+
+def test_sparse_oracle_identity_is_cg(orc):
+    """L = I: the sparse oracle's residual history equals scipy's CG."""
+    from oracle import pcg
+    A, L, b = problem(10, "identity")
+    _, res, _, _ = pcg.pcg_loss_grad_sparse(A, L, b, 8, 0.6)
+    As = sps.csr_matrix((A.values, A.indices, A.indptr), shape=(A.nrows, A.nrows))
+    xs = []
+    spla.cg(As, b, x0=np.zeros(A.nrows), rtol=1e-30, maxiter=8, callback=lambda xk: xs.append(xk.copy()))
+    np.testing.assert_allclose(res, [np.linalg.norm(b - As @ xk) for xk in xs][:8], rtol=1e-10)
+
+
+def test_sparse_oracle_finite_differences(orc):
+    """Central differences of the sparse oracle's loss on stored entries of L."""
+    from oracle import pcg
+    A, L, b = problem(7, "seeded")
+    _, _, g, _ = pcg.pcg_loss_grad_sparse(A, L, b, 5, 0.6)
+    for q in range(0, L.nnz, 7):
+        h = 1e-6
+        Lp, Lm = L.values.copy(), L.values.copy()
+        Lp[q] += h
+        Lm[q] -= h
+        fd = (pcg.pcg_loss_grad_sparse(A, L.with_values(Lp), b, 5, 0.6, want_S=False)[0]
+              - pcg.pcg_loss_grad_sparse(A, L.with_values(Lm), b, 5, 0.6, want_S=False)[0]) / (2 * h)
+        assert abs(fd - g[q]) <= 1e-6 * max(1.0, abs(fd)), (q, fd, g[q])
+
+
 # ---------------------------------------------------------------- GPU parity
 @pytest.fixture(scope="module")
 def ck():
@@ -68,45 +139,75 @@ def ck():
     return csrk
 
 
-@pytest.mark.gpu
-@pytest.mark.parametrize("precond", ["mult", "solve"])
-@pytest.mark.parametrize("N,init,n_it,rtol", [(8, "identity", 4, 1e-11), (8, "seeded", 4, 1e-11),
-                                              (16, "seeded", 50, 1e-8), (32, "identity", 50, 1e-8),
-                                              (40, "seeded", 50, 1e-8)])
-def test_pcg_gpu_vs_oracle(ck, N, init, n_it, rtol, precond):
-    """Tolerance: max(rtol, 20 x the oracle's own sensitivity), the latter measured by
-    re-running the oracle with b perturbed by ~5 ulps (random relative 1e-15) -- n_it chained
-    CG steps amplify rounding-level differences (SURVEY c.4: end-to-end 1e-12 is unpinned),
-    so GPU and CPU agree to the extent the algorithm itself is stable."""
+def _pcg_parity(ck, A, L, b, n_it, precond, rtol=1e-12, margin=20.0):
+    """GPU csrk_pcg_loss_grad vs the sparse oracle (DESIGN reading R-PCG):
+      dL elementwise:  |gpu - orc| <= tau * S_dL,    loss / residuals: relative tau_l / tau_r,
+      tau = max(rtol, margin * kappa), kappa = the oracle's own response to b perturbed by
+      ~5 ulps (relative 1e-15 N(0,1)), measured on the same rule -- n_it chained CG steps amplify
+      rounding-level differences, so both sides agree to the extent the algorithm is stable."""
     from oracle import pcg
-    A, L, b = problem(N, init)
-    args = (to_dense(A), pattern_dense(L), to_dense(L), b, n_it, 0.6)
-    loss_ref, res_ref, g_ref = pcg.pcg_loss_grad(*args, precond=precond)
+    loss_ref, res_ref, g_ref, S = pcg.pcg_loss_grad_sparse(A, L, b, n_it, 0.6, precond=precond)
     bp = b * (1.0 + 1e-15 * np.random.default_rng(1).standard_normal(b.shape))
-    loss_alt, res_alt, g_alt = pcg.pcg_loss_grad(args[0], args[1], args[2], bp, n_it, 0.6, precond=precond)
+    loss_alt, res_alt, g_alt, _ = pcg.pcg_loss_grad_sparse(A, L, bp, n_it, 0.6, want_S=False, precond=precond)
+    res_ref, res_alt = np.array(res_ref), np.array(res_alt)
+    Sg = np.where(S > 0, S, 1.0)
+    tau_g = max(rtol, margin * float(np.max(np.abs(g_alt - g_ref) / Sg)))
+    tau_l = max(rtol, margin * abs(loss_alt - loss_ref) / abs(loss_ref))
+    tau_r = max(rtol, margin * float(np.max(np.abs(res_alt - res_ref) / res_ref)))
+    del g_alt
     Ad, Ld = ck.CSR.from_host(A), ck.CSR.from_host(L)
     loss, res, dL = ck.pcg_loss_grad(Ad, Ld, torch.from_numpy(b).cuda(), n_it, 0.6, precond=precond)
-    rows = np.repeat(np.arange(L.nrows), np.diff(L.indptr))
-    g, ga = g_ref[rows, L.indices], g_alt[rows, L.indices]
-    gscale = np.max(np.abs(g))
-    tol_loss = max(rtol, 20 * abs(loss_alt - loss_ref) / abs(loss_ref))
-    tol_res = max(rtol, 20 * np.max(np.abs(np.array(res_alt) - res_ref) / np.array(res_ref)))
-    tol_g = max(rtol, 20 * np.max(np.abs(ga - g)) / gscale)
-    assert abs(loss - loss_ref) <= tol_loss * abs(loss_ref)
-    np.testing.assert_allclose(res, res_ref, rtol=tol_res)
+    assert abs(loss - loss_ref) <= tau_l * abs(loss_ref), (loss, loss_ref, tau_l)
+    np.testing.assert_allclose(res, res_ref, rtol=tau_r)
     got = dL.cpu().numpy()
-    assert np.max(np.abs(got - g)) <= tol_g * gscale, (np.max(np.abs(got - g)) / gscale, tol_g)
+    err = np.abs(got - g_ref)
+    assert np.all(err <= tau_g * S), (float(np.max(err / Sg)), tau_g)
+    return tau_g, tau_l, tau_r
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precond", ["mult", "solve"])
+@pytest.mark.parametrize("N,init,n_it", [(8, "identity", 4), (8, "seeded", 4), (16, "seeded", 50),
+                                         (32, "identity", 50), (40, "seeded", 50), (128, "seeded", 50)])
+def test_pcg_gpu_vs_oracle(ck, N, init, n_it, precond):
+    """Elementwise S-rule parity of the loss, the residual history and dL (R-PCG)."""
+    A, L, b = problem(N, init)
+    _pcg_parity(ck, A, L, b, n_it, precond)
+
+
+@pytest.mark.gpu
+def test_pcg_gpu_inverse_factor_one_step(ck):
+    """The orientation pin on the GPU: L = chol(A^{-1}) => ||r^(1)|| ~ 0 (M = L L^T = A^{-1})."""
+    A, Ad, P, Lc, Ls = _inverse_factor_case()
+    b = synth.dense(A.nrows, 3)
+    _, res, _ = ck.pcg_loss_grad(ck.CSR.from_host(A), ck.CSR.from_host(Ls), torch.from_numpy(b).cuda(), 3, 0.6)
+    assert res[0] <= 1e-13 * np.linalg.norm(b)
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+@pytest.mark.parametrize("precond", ["mult", "solve"])
+def test_pcg_config5_vs_sparse_oracle(ck, precond):
+    """BASELINE config 5 at full size (2D Poisson 4096^2, lower-bidiagonal L, 50 iterations) against
+    the sparse oracle on the host (all cores): loss, residual history and dL elementwise (R-PCG)."""
+    import oracle
+    oracle.set_threads(len(__import__("os").sched_getaffinity(0)))
+    A, L, b = problem(4096, "seeded")
+    assert A.nnz == 83869696 and L.nnz == 33554431
+    try:
+        tau_g, tau_l, tau_r = _pcg_parity(ck, A, L, b, 50, precond)
+    finally:
+        oracle.set_threads(1)
+    assert tau_g < 1e-9 and tau_l < 1e-9 and tau_r < 1e-9, (tau_g, tau_l, tau_r)   # a well-posed case
 
 
 @pytest.mark.gpu
 @pytest.mark.slow
 @pytest.mark.parametrize("precond", ["mult", "solve"])
 def test_pcg_config5_directional_derivative(ck, precond):
-    """BASELINE config 5 at full size (2D Poisson 4096^2, 50 iterations): the gradient agrees
-    with a central difference of the GPU loss along a random direction of L.values (also with
-    M = (L L^T)^{-1} by triangular solves)."""
+    """Config 5 at full size: the gradient also agrees with a central difference of the GPU loss
+    along a random direction of L.values (a second, oracle-free check of the hand adjoint)."""
     A, L, b = problem(4096, "seeded")
-    assert A.nnz == 83869696 and L.nnz == 33554431
     Ad, Ld = ck.CSR.from_host(A), ck.CSR.from_host(L)
     bt = torch.from_numpy(b).cuda()
     loss, res, dL = ck.pcg_loss_grad(Ad, Ld, bt, 50, 0.6, precond=precond)

@@ -12,7 +12,7 @@ import torch
 
 import synth
 from oracle import spai as osp
-from util import gather_mask, pattern_dense, to_dense
+from util import assert_S_close, gather_mask, pattern_dense, to_dense
 
 
 def ones_on(A):
@@ -51,6 +51,21 @@ def test_spai_gradient_vanishes_at_least_squares_reference():
     assert np.abs(g).max() < 1e-10
     loss0, _ = osp.spai_loss_grad(Ad, P, to_dense(ones_on(A)))  # the paper's start point
     assert loss_ref < loss0
+
+
+def test_spai_S_bounds_the_oracle_against_a_reordered_evaluation():
+    """The S-scales bound the difference between two evaluation orders of the same quantities:
+    the oracle (autograd of M A) and the column decomposition / explicit -2 (R A^T) form."""
+    A = synth.poisson2d(8)
+    Ad, P = to_dense(A), pattern_dense(A)
+    M = to_dense(A.with_values(np.random.default_rng(3).uniform(-1, 1, A.nnz)))
+    loss, g = osp.spai_loss_grad(Ad, P, M)
+    S_loss, S_dM = osp.spai_S(Ad, P, M)
+    assert abs(loss - osp.spai_loss_by_columns(Ad, M)) <= 1e-14 * S_loss
+    R = np.eye(Ad.shape[0]) - M @ Ad
+    g2 = np.where(P, -2.0 * (R @ Ad.T), 0.0)
+    assert np.all(np.abs(g - g2) <= 1e-14 * S_dM)
+    assert np.all(np.abs(g) <= S_dM * (1 + 1e-12)) and abs(loss) <= S_loss
 
 
 def test_spai_gradient_exact_fd():
@@ -104,10 +119,10 @@ def test_spai_gpu_parity(ck, case):
     M_d = ck.CSR.from_host(A.with_values(Mv))
     plan = ck.spai_plan(M_d, A_d)
     loss, dM = ck.spai_loss_grad(plan, M_d, A_d)
-    # loss: a sum of nnz(R) squares; gradient entries: sums of products of O(1) terms
-    assert abs(loss - loss_ref) <= 1e-12 * max(loss_ref, 1.0) * 10
-    scale = np.abs(gref).max() + 1.0
-    np.testing.assert_allclose(dM.cpu().numpy(), gref, rtol=0, atol=1e-12 * scale * 10)
+    # elementwise S-rule of reading A6 with the composed magnitudes of oracle.spai.spai_S
+    S_loss, S_dM = osp.spai_S(Ad, P, to_dense(A.with_values(Mv)))
+    assert abs(loss - loss_ref) <= 1e-12 * S_loss
+    assert_S_close(dM.cpu().numpy(), gref, gather_mask(S_dM, A.indptr, A.indices), 1e-12, f"{case} dM")
 
 
 def _with_diag(R):
