@@ -114,52 +114,99 @@ def pcg_costs_fused(n, nnzA, nnzL, N, s=S):
 
 def run_cfg5(args, torch, ck):
     """BASELINE config 5: one training step = 50 PCG iterations on the 2D
-    Poisson 4096^2 matrix with M = L L^T (lower-bidiagonal L), loss and d loss / d L.values."""
+    Poisson 4096^2 matrix with M = L L^T (lower-bidiagonal L), loss and d loss / d L.values.
+    N > 1: the same problem row-sharded over N GPUs (strong scaling; dist.PcgShard + the NCCL
+    csrk_comm: halo send/recv of the ghost grid lines, allreduced dot products), the whole step
+    one CUDA graph per rank."""
     A = synth.poisson2d(4096)
     L = synth.bidiag_lower(A.nrows, "seeded")
     b = np.full(A.nrows, 1.0 / np.sqrt(A.nrows))
-    Ad, Ld = ck.CSR.from_host(A), ck.CSR.from_host(L)
-    bt = torch.from_numpy(b).cuda()
-    dL = torch.empty_like(Ld.values)
     N = 50
     pc = args.precond
+    world, rank, local = init_dist(torch) if int(os.environ.get("WORLD_SIZE", "1")) > 1 else (1, 0, 0)
+    comm = None
+    if world > 1:
+        if pc != "mult":
+            raise SystemExit("bench.py: --precond solve has no sharded path (the triangular solves are sequential)")
+        from paper_2212_05159_b200 import dist as D
+        sh = D.PcgShard(A, L, b, rank, world)
+        if os.environ.get("CSRK_BENCH_ONE_GPU") == "1":
+            sc = D.StagedComm(sh.halo)
+            comm = sc.csrk_comm()
+            sc.set_extended_length(sh.hi - sh.lo)
+        else:
+            comm = ck.comm_nccl(rank, world, sh.halo)
+        Ad, Ld = ck.CSR.from_host(sh.A), ck.CSR.from_host(sh.L)
+        bt = torch.from_numpy(sh.b).cuda()
+
+        def call():
+            return ck.pcg_loss_grad_dist(comm, sh.own_off, Ad, Ld, bt, N, 0.6, dL=dL, ws=ws_buf)
+    else:
+        Ad, Ld = ck.CSR.from_host(A), ck.CSR.from_host(L)
+        bt = torch.from_numpy(b).cuda()
+
+        def call():
+            return ck.pcg_loss_grad(Ad, Ld, bt, N, 0.6, dL=dL, precond=pc)
+    dL = torch.empty_like(Ld.values)
+    ws_buf = None
+    if world > 1:
+        import ctypes
+        pa, pl = Ad.pattern(), Ld.pattern()
+        nb = ctypes.c_size_t(0)
+        ck.lib().csrk_workspace_size(ck.WS["pcg_dist"], ck.F64, ctypes.byref(pa), ctypes.byref(pl), N, 0,
+                                     ctypes.byref(nb))
+        ws_buf = torch.empty(max(int(nb.value), 1), dtype=torch.uint8, device=bt.device)
     for _ in range(args.warmup):
-        ck.pcg_loss_grad(Ad, Ld, bt, N, 0.6, dL=dL, precond=pc)
+        call()
     torch.cuda.synchronize()
     st = torch.cuda.current_stream()
     l0 = ck.launch_count()
     ts = []
-    with Clocks(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+    with Clocks(local) as clk:
         for _ in range(args.steps):
+            if world > 1:
+                import torch.distributed as tdist
+                tdist.barrier()
             a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(st)
-            loss, res, _ = ck.pcg_loss_grad(Ad, Ld, bt, N, 0.6, dL=dL, precond=pc)
+            loss, res, _ = call()
             e.record(st)
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(e))
     unfused, flops = pcg_costs(A.nrows, A.nnz, L.nnz, N)
     byts = pcg_costs_fused(A.nrows, A.nnz, L.nnz, N)
     ms = float(np.mean(ts))
+    if world > 1:
+        import torch.distributed as tdist
+        ms = float(allreduce_max(torch, torch.tensor([ms], dtype=torch.float64, device=bt.device)).item())
+        tdist.barrier()
+        if os.environ.get("CSRK_BENCH_ONE_GPU") != "1":
+            ck.comm_destroy(comm)
+        tdist.destroy_process_group()
+        if rank != 0:
+            return 0
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
     out = {"metric": "PCG training-step algorithmic GB/s (config 5)", "value": round(byts / (ms * 1e-3) / 1e9, 2),
-           "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": "config5: 2D Poisson 4096^2 (16,777,216 rows, 83,869,696 nnz), lower-bidiagonal "
-                                  "L (33,554,431 nnz), 50 PCG iterations fwd + reverse, gamma 0.6, 1 GPU",
+                                  f"L (33,554,431 nnz), 50 PCG iterations fwd + reverse, gamma 0.6, {world} GPU(s)",
+                      "parallelism": f"rowblock{world}" if world > 1 else "single",
+                      "cuda_graph": os.environ.get("CSRK_PCG_GRAPH", "1") != "0",
                       "preconditioner": "M = L L^T (P:836-839)" if pc == "mult" else
                       "M = (L L^T)^-1 by two SpTRSV (SURVEY 8(f) f3); bytes counted as for M = L L^T"},
            "step_bytes": byts, "step_bytes_def": "SURVEY 8(d) d.4 fused minimum (bench.pcg_costs_fused)",
            "unfused_bytes": unfused, "unfused_GB/s": round(unfused / (ms * 1e-3) / 1e9, 1),
            "gflops": round(flops / (ms * 1e-3) / 1e9, 2), "loss": loss,
            "roofline": {"bound": "hbm", "kernel": "whole step", "achieved": round(byts / (ms * 1e-3) / 1e9, 1),
-                        "peak": peak, "unit": "GB/s", "frac": round(byts / (ms * 1e-3) / 1e9 / peak, 4)},
+                        "peak": peak * world, "unit": "GB/s",
+                        "frac": round(byts / (ms * 1e-3) / 1e9 / (peak * world), 4)},
            "gpu_launches": int((ck.launch_count() - l0) / max(args.steps, 1)), "clocks": clk.summary()}
-    traffic, tsrc = _traffic("cfg5" if pc == "mult" else "cfg5_solve", "pcg_loss_grad")
+    traffic, tsrc = _traffic("cfg5" if pc == "mult" else "cfg5_solve", "pcg_loss_grad") if world == 1 else (None, None)
     out["roofline"]["traffic"], out["roofline"]["traffic_source"] = traffic, tsrc
-    if args.ops_trace:
-        write_ops_trace(args.ops_trace, ck, [("pcg_loss_grad", lambda: ck.pcg_loss_grad(Ad, Ld, bt, N, 0.6, dL=dL,
-                                                                                        precond=pc))])
+    if args.ops_trace and world == 1:
+        write_ops_trace(args.ops_trace, ck, [("pcg_loss_grad", call)])
     print(json.dumps(out))
     return 0
 
@@ -211,6 +258,116 @@ def run_ops_workload(args, torch, ck, cfg):
           f"(nnz(C) {nnzC:,}, prod {prod:,}) symbolic + numeric + bwd")
     return _time_ops(args, torch, ck, ops, f"SpMV/SpGEMM fwd+bwd algorithmic GB/s (config {cfg})",
                      "f64" if cfg == 3 else "f32", wl, f"cfg{cfg}", exclude=("spmv_bwd_plan",))
+
+
+def run_ops_sharded(args, torch, ck, cfg, world, rank, local):
+    """BASELINE configs 3 and 4 row-sharded over N GPUs (strong scaling: the global matrix is
+    split).  Rank r owns a contiguous row block balanced by SpGEMM work w_i (columns
+    compacted to its interval), x over its column interval, and B_r = the rows of A its block
+    references.  Forward ops are rank-local; the dx partial (spmv_bwd) and the dB partial
+    (spgemm_bwd) are combined onto their owners by dist.Combiner -- the halo send/recv for the 3D
+    stencil, one NCCL reduce_scatter for the power-law matrix (every block references ~86 % of
+    the columns).  Each op: barrier, CUDA events on the launching stream, L2 flushed; the op time
+    is the max over ranks; bytes are the global algorithmic bytes of the 1-GPU line."""
+    import torch.distributed as tdist
+    from paper_2212_05159_b200 import dist as D
+    dev = torch.device("cuda", local)
+    if cfg == 3:
+        A = synth.poisson3d(160)
+        s, dt_np, dt = 8, np.float64, torch.float64
+    else:
+        A = synth.powerlaw()
+        s, dt_np, dt = 4, np.float32, torch.float32
+    m, n, nnz = A.nrows, A.ncols, A.nnz
+    lens = np.diff(A.indptr)
+    prod = int(lens[A.indices].sum())
+    work = np.zeros(m, np.int64)
+    np.add.at(work, np.repeat(np.arange(m), lens), lens[A.indices])
+    splits = D.balanced_row_splits(A.indptr, world, work=work)
+    blk = D.make_block(A, rank, world, splits)
+    dg = D.DistGemm(A, blk, device=dev)
+    r0, r1 = int(splits[rank]), int(splits[rank + 1])
+    x = synth.dense(n, synth.seed_of(cfg, 3), dt_np)[blk.col_lo:blk.col_hi]
+    dy = synth.dense(m, synth.seed_of(cfg, 4), dt_np)[r0:r1]
+    del A
+    Ad, Bd = ck.CSR.from_host(blk.A), ck.CSR.from_host(dg.B)
+    dm = D.DistCSR(blk, device=dev)
+    x, dy = torch.from_numpy(np.ascontiguousarray(x)).to(dev), torch.from_numpy(np.ascontiguousarray(dy)).to(dev)
+    plan = ck.csr_transpose(Ad, with_values=False)
+    C = ck.spgemm_symbolic(Ad, Bd)
+    q = torch.arange(C.nnz, device=dev, dtype=torch.int64) + 7919 * rank
+    dC = (((q * 2654435761 + 12345) % 1000003).to(torch.float64) / 500001.5 - 1.0).to(dt)
+    del q
+    Cv = torch.empty(C.nnz, dtype=dt, device=dev)
+    y = torch.empty(Ad.nrows, dtype=dt, device=dev)
+    dA_v = torch.empty(Ad.nnz, dtype=dt, device=dev)
+    dA_g, dB_g = torch.empty(Ad.nnz, dtype=dt, device=dev), torch.empty(Bd.nnz, dtype=dt, device=dev)
+    nnzC = allreduce_sum(torch, torch.tensor([C.nnz], dtype=torch.int64, device=dev))
+    c = op_costs(m, n, nnz, int(nnzC.item()), prod, k=1, s=s)
+
+    def spmv_bwd():
+        _, dx_part = ck.spmv_bwd(Ad, x, dy, dA=dA_v)
+        return dm.vec(dx_part)
+
+    def spgemm_bwd():
+        ck.spgemm_bwd(Ad, Bd, C, dC, dA=dA_g, dB=dB_g)
+        return dg.combine_dB(dB_g)
+
+    ops = {}
+    if cfg == 4:
+        ops["spmv_fwd"] = (lambda: ck.spmv_fwd(Ad, x, out=y), c["spmv_fwd"])
+        ops["spmv_bwd"] = (spmv_bwd, c["spmv_bwd"])
+        ops["csr_transpose"] = (lambda: ck.csr_transpose(Ad, with_values=False, out=plan), c["csr_transpose"])
+    ops["spgemm_symbolic"] = (lambda: ck.spgemm_symbolic(Ad, Bd), c["spgemm_symbolic"])
+    ops["spgemm_numeric"] = (lambda: ck.spgemm_numeric(Ad, Bd, C, out=Cv), c["spgemm_numeric"])
+    ops["spgemm_bwd"] = (spgemm_bwd, c["spgemm_bwd"])
+    l2 = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        for f, _c in ops.values():
+            f()
+    torch.cuda.synchronize()
+    times = {k: [] for k in ops}
+    l0 = ck.launch_count()
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            for k, (f, _c) in ops.items():
+                l2.zero_()
+                tdist.barrier()
+                a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                f()
+                e.record(st)
+                times[k].append((a, e))
+        torch.cuda.synchronize()
+    launches = ck.launch_count() - l0
+    med = torch.tensor([float(np.median([a.elapsed_time(e) for a, e in times[k]])) for k in ops],
+                       dtype=torch.float64, device=dev)
+    allreduce_max(torch, med)
+    peak = _peak()
+    rep, tot_b, tot_f, tot_ms = {}, 0, 0, 0.0
+    for (k, (_f, (b, fl))), ms in zip(ops.items(), med.tolist()):
+        rep[k] = {"ms": round(ms, 4), "GB/s": round(b / ms / 1e6, 1), "GFLOP/s": round(fl / ms / 1e6, 1),
+                  "frac_of_N_peaks": round(b / ms / 1e6 / (peak * world), 3), "bytes": b}
+        tot_b, tot_f, tot_ms = tot_b + b, tot_f + fl, tot_ms + ms
+    dom = max(rep, key=lambda k: rep[k]["ms"])
+    if rank == 0:
+        wl = (f"config3: 3D Poisson 7-point 160^3, fp64, C = A A, row-sharded over {world} GPUs" if cfg == 3 else
+              f"config4: power-law n = 2^23, 2^27 nnz, fp32, spmv + C = A A, row-sharded over {world} GPUs")
+        out = {"metric": f"SpMV/SpGEMM fwd+bwd algorithmic GB/s (config {cfg})",
+               "value": round(tot_b / tot_ms / 1e6, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": round(tot_ms, 4), "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": "f64" if cfg == 3 else "f32", "data": "synthetic",
+               "config": {"workload": wl, "l2": "flushed (512 MiB write) before every timed op",
+                          "parallelism": f"rowblock{world}", "combine": {"dx": dm.vec.mode, "dB": dg.ent.mode},
+                          "row_splits": [int(v) for v in splits]},
+               "gflops": round(tot_f / tot_ms / 1e6, 2),
+               "roofline": {"bound": "hbm", "kernel": dom, "achieved": rep[dom]["GB/s"], "peak": peak * world,
+                            "peak_def": f"{world} x measured HBM copy GB/s", "unit": "GB/s",
+                            "frac": rep[dom]["frac_of_N_peaks"], "traffic": None},
+               "ops": rep, "gpu_launches": int(launches / max(args.steps, 1)), "clocks": clk.summary()}
+        print(json.dumps(out))
+    return 0
 
 
 def run_trsv_workload(args, torch, ck):
@@ -451,11 +608,12 @@ class Workload:
         dev = torch.device("cuda", torch.cuda.current_device())
         self.dev = dev
         # rank's row block of the (GRID*world) x GRID grid: rows [r*m, (r+1)*m)
+        from paper_2212_05159_b200 import dist as D
         if world == 1:
             A = synth.poisson2d(GRID)
             self.col_lo = 0
         else:
-            A, self.col_lo = dist.poisson2d_row_block(GRID * world, GRID, rank, world)
+            A, self.col_lo = D.poisson2d_row_block(GRID * world, GRID, rank, world)
         self.A_host = A
         self.m, self.n, self.nnz = A.nrows, A.ncols, A.nnz
         ck_ = ck
@@ -466,7 +624,7 @@ class Workload:
         self.X = torch.from_numpy(synth.dense((self.n, K), synth.seed_of(cfg, 3) + 100 * rank + 1)).to(dev)
         self.dY = torch.from_numpy(synth.dense((self.m, K), synth.seed_of(cfg, 4) + 100 * rank + 1)).to(dev)
         # C = A B with B = the rows of A over this rank's column interval (B = A at N = 1)
-        self.B = self.A if world == 1 else ck_.CSR.from_host(dist.halo_rows_block(GRID * world, GRID, rank, world))
+        self.B = self.A if world == 1 else ck_.CSR.from_host(D.halo_rows_block(GRID * world, GRID, rank, world))
         # outputs / plans (allocated once, reused)
         self.plan = ck_.csr_transpose(self.A, with_values=False)
         self.C = ck_.spgemm_symbolic(self.A, self.B)
@@ -644,6 +802,46 @@ def spawn_ranks(args):
     return subprocess.call(cmd)
 
 
+def init_dist(torch):
+    """torch.distributed for N > 1: NCCL, one GPU per rank (LOCAL_RANK).  CSRK_BENCH_ONE_GPU=1 runs
+    every rank on cuda:0 over gloo instead -- a functional check of the sharded paths on a 1-GPU box
+    (its numbers are not bench values).  Returns (world, rank, local device index)."""
+    import torch.distributed as tdist
+    world, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
+    one = os.environ.get("CSRK_BENCH_ONE_GPU") == "1"
+    local = 0 if one else int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        if one:
+            tdist.init_process_group("gloo")
+        else:
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def allreduce_max(torch, t):
+    """Max over ranks of a device tensor (staged through the host on gloo)."""
+    import torch.distributed as tdist
+    if tdist.get_backend() == "gloo":
+        h = t.cpu()
+        tdist.all_reduce(h, op=tdist.ReduceOp.MAX)
+        t.copy_(h)
+    else:
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    return t
+
+
+def allreduce_sum(torch, t):
+    import torch.distributed as tdist
+    if tdist.get_backend() == "gloo":
+        h = t.cpu()
+        tdist.all_reduce(h)
+        t.copy_(h)
+    else:
+        tdist.all_reduce(t)
+    return t
+
+
 def write_ops_trace(path, ck, ops_in_order):
     """Run each (name, fn) once and record the csrk launches it made, in launch order."""
     import torch
@@ -683,7 +881,13 @@ def main():
     import torch.distributed as tdist
     from paper_2212_05159_b200 import csrk as ck
 
-    if args.workload != "cfg2" and int(os.environ.get("WORLD_SIZE", "1")) > 1:
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 and args.workload in ("cfg3", "cfg4"):
+        world, rank, local = init_dist(torch)
+        try:
+            return run_ops_sharded(args, torch, ck, int(args.workload[-1]), world, rank, local)
+        finally:
+            tdist.destroy_process_group()
+    if args.workload not in ("cfg2", "cfg3", "cfg4", "cfg5") and int(os.environ.get("WORLD_SIZE", "1")) > 1:
         sys.stderr.write(f"bench.py: --workload {args.workload} has no sharded (N > 1) path\n")
         return 2
     if args.workload == "cfg5":
@@ -697,13 +901,9 @@ def main():
     if args.workload in ("cfg3", "cfg4"):
         return run_ops_workload(args, torch, ck, int(args.workload[-1]))
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    world, rank, local = init_dist(torch)
     dist = None
     if world > 1:
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
         from paper_2212_05159_b200 import dist as dist_mod
         dist = dist_mod.HaloBench(world, rank)
     W = Workload(torch, ck, rank, world, dist)
@@ -753,9 +953,7 @@ def main():
     tot_ms = float(sum(step_ms))
     op_ms = {nm: float(np.mean([e[nm][0].elapsed_time(e[nm][1]) for e in evs])) for nm in names}
     if world > 1:
-        t = torch.tensor([tot_ms], dtype=torch.float64, device=W.dev)
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        tot_ms = float(t.item())
+        tot_ms = float(allreduce_max(torch, torch.tensor([tot_ms], dtype=torch.float64, device=W.dev)).item())
     ms_per_step = tot_ms / args.steps
     step_bytes = sum(b for b, _ in W.costs.values())
     step_flops = sum(f for _, f in W.costs.values())
@@ -890,9 +1088,7 @@ def run_e2e(torch, ck, W, args, world):
     ms = ev0.elapsed_time(ev1) / steps
     if world > 1:
         import torch.distributed as tdist
-        t = torch.tensor([ms], dtype=torch.float64, device=W.dev)
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = float(allreduce_max(torch, torch.tensor([ms], dtype=torch.float64, device=W.dev)).item())
     step_bytes = sum(b for b, _ in W.costs.values())
     return {"value": round(step_bytes * world / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
             "ms_per_step": round(ms, 3), "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),

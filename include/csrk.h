@@ -87,7 +87,8 @@ typedef enum {
     CSRK_WS_SPTRSV_BWD = 12, /* A = T; have_plan = 1 if T^T (pattern + perm) is passed */
     CSRK_WS_GCN_FWD = 13,    /* A = graph, k = F */
     CSRK_WS_GCN_BWD = 14,    /* A = graph, k = F, have_plan */
-    CSRK_WS_DENSE_GEMM_TN = 15 /* A->nrows = n, A->ncols = C, k = F (only the sizes are read) */
+    CSRK_WS_DENSE_GEMM_TN = 15,/* A->nrows = n, A->ncols = C, k = F (only the sizes are read) */
+    CSRK_WS_PCG_DIST = 16    /* A, B = L: the rank's m x n_ext blocks, k = n_it */
 } csrk_ws_op;
 
 /*
@@ -336,6 +337,67 @@ int csrk_dense_gemm_tn(csrk_dtype dtype, int64_t n, int64_t C, int64_t F, const 
 int csrk_pcg_loss_grad(csrk_pattern A, const double *A_val, csrk_pattern L, const double *L_val,
                        const double *b, int n_it, double gamma, int precond, double *loss_host, double *resid_host,
                        double *dL_val, void *ws, size_t ws_bytes, csrk_stream_t stream);
+
+/*
+ * Row-sharded multi-GPU execution (north_star "rows of A are partitioned across the
+ * GPUs ... partial gradients combined by NCCL").  One process per GPU.  A rank owns m consecutive
+ * rows; its vectors are EXTENDED: n_ext entries holding the owned rows at [own_off, own_off + m)
+ * and ghost copies of the neighbours' entries its rows reference around them.  Local matrices
+ * are the rank's rows with columns in extended coordinates (m x n_ext).
+ *
+ * csrk_comm: the three exchanges a sharded step needs, stream-ordered on `stream`:
+ *   allreduce_sum(ctx, buf, count, stream)  in-place sum over ranks of `count` doubles (device)
+ *   halo(ctx, vec, mode, stream)            on an extended vector: mode 0 = GATHER (every ghost
+ *                                           entry receives its owner's value), mode 1 = REDUCE
+ *                                           (every ghost entry is added into its owner's entry;
+ *                                           ghosts are then undefined)
+ *   capturable                              nonzero if both may be captured in a CUDA graph
+ * csrk_comm_nccl_create builds one over NCCL (libnccl.so.2, loaded at run time) from a halo
+ * description; any other implementation (e.g. a host-staged one for tests) may fill the struct.
+ */
+typedef struct {
+    void *ctx;
+    int (*allreduce_sum)(void *ctx, double *buf, int64_t count, csrk_stream_t stream);
+    int (*halo)(void *ctx, double *vec, int mode, csrk_stream_t stream);
+    int capturable;
+} csrk_comm;
+
+/* Halo description of one rank (host arrays of npeers entries, extended coordinates): peer q
+ * holds my owned entries [own_off[q], +own_len[q]) as its ghosts, and my ghost entries
+ * [ghost_off[q], +ghost_len[q]) are owned by peer q.  Ranges are in matching order on both sides
+ * (my own range for q is, element for element, q's ghost range for me). */
+typedef struct {
+    int npeers;
+    const int *peer;
+    const int64_t *own_off, *own_len;
+    const int64_t *ghost_off, *ghost_len;
+} csrk_halo;
+
+/* NCCL unique id (128 bytes) for csrk_comm_nccl_create; call on one rank and broadcast it. */
+int csrk_comm_nccl_unique_id(void *id128);
+/* Collective over the `world` ranks: creates the NCCL communicator and a csrk_comm whose halo
+ * follows `halo` (copied).  Allocates its own device scratch (the max received ghost total) --
+ * the only csrk object that owns device memory; csrk_comm_nccl_destroy frees it. */
+int csrk_comm_nccl_create(const void *id128, int rank, int world, const csrk_halo *halo, csrk_comm *out);
+int csrk_comm_nccl_destroy(csrk_comm *comm);
+
+/*
+ * Config-5 training step, row-sharded (the multi-GPU form of csrk_pcg_loss_grad, M = L L^T):
+ * A and L are this rank's m rows (m x n_ext, columns in extended coordinates), b its owned m
+ * entries, dL_val[nnz(L)] the gradient on its rows.  Every SpMV with A or L reads a halo-gathered
+ * extended input (op N) or produces an extended partial that is halo-reduced (op T); the dot
+ * products are local sums followed by comm->allreduce_sum (p.q and r.z per iteration and their
+ * adjoints; the ||r^(i)||^2 once at the end).  loss_host / resid_host are the global values on
+ * every rank.  comm == NULL (with n_ext == m, own_off == 0) is the single-GPU call.  precond must
+ * be 0.  If comm is NULL or capturable, the whole forward + reverse pass is captured once in a
+ * CUDA graph (per argument set) and replayed (CSRK_PCG_GRAPH=0 disables).
+ * Workspace: csrk_workspace_size(CSRK_WS_PCG_DIST, CSRK_F64, &A, &L, n_it, 0, &bytes) with
+ * A.ncols = L.ncols = n_ext.
+ */
+int csrk_pcg_loss_grad_dist(const csrk_comm *comm, int64_t own_off, csrk_pattern A, const double *A_val,
+                            csrk_pattern L, const double *L_val, const double *b, int n_it, double gamma,
+                            double *loss_host, double *resid_host, double *dL_val, void *ws, size_t ws_bytes,
+                            csrk_stream_t stream);
 
 /*
  * Scratch bytes needed by operation `op` for operands A (and B for SpGEMM, or the

@@ -338,7 +338,29 @@ int csrk_pcg_loss_grad(csrk_pattern A, const double *A_val, csrk_pattern L, cons
     CSRK_TRY(validate_pattern(L, (cudaStream_t)stream));
     if (precond) CSRK_TRY(validate_triangular(L, 0, 0, (cudaStream_t)stream));
     return with_ws(ws, ws_bytes, [&](Bump &bw) {
-        return pcg_loss_grad(A, A_val, L, L_val, b, n_it, gamma, precond, loss_host, resid_host, dL_val, bw,
+        return pcg_loss_grad(nullptr, 0, A, A_val, L, L_val, b, n_it, gamma, precond, loss_host, resid_host, dL_val,
+                             bw, (cudaStream_t)stream);
+    });
+}
+
+int csrk_pcg_loss_grad_dist(const csrk_comm *comm, int64_t own_off, csrk_pattern A, const double *A_val,
+                            csrk_pattern L, const double *L_val, const double *b, int n_it, double gamma,
+                            double *loss_host, double *resid_host, double *dL_val, void *ws, size_t ws_bytes,
+                            csrk_stream_t stream)
+{
+    CSRK_TRY(check_pat(A));
+    CSRK_TRY(check_pat(L));
+    if (L.nrows != A.nrows || L.ncols != A.ncols || own_off < 0 || own_off + A.nrows > A.ncols)
+        return CSRK_ERR_DIM_MISMATCH;
+    if (!comm && (own_off != 0 || A.ncols != A.nrows)) return CSRK_ERR_DIM_MISMATCH;
+    if (comm && (!comm->allreduce_sum || !comm->halo)) return CSRK_ERR_INVALID_ARG;
+    if (n_it < 1 || !(gamma > 0.0) || !loss_host || (A.nrows > 0 && !b) || !dL_val || (A.nnz > 0 && !A_val) ||
+        (L.nnz > 0 && !L_val))
+        return CSRK_ERR_INVALID_ARG;
+    CSRK_TRY(validate_pattern(A, (cudaStream_t)stream));
+    CSRK_TRY(validate_pattern(L, (cudaStream_t)stream));
+    return with_ws(ws, ws_bytes, [&](Bump &bw) {
+        return pcg_loss_grad(comm, own_off, A, A_val, L, L_val, b, n_it, gamma, 0, loss_host, resid_host, dL_val, bw,
                              (cudaStream_t)stream);
     });
 }
@@ -405,8 +427,15 @@ int csrk_workspace_size(csrk_ws_op op, csrk_dtype dtype, const csrk_pattern *A, 
     case CSRK_WS_PCG: {
         if (!B || k < 1) return CSRK_ERR_INVALID_ARG;
         double dummy = 0.0;
-        st = pcg_loss_grad(Ar, (const double *)d, *B, (const double *)d, (const double *)d, (int)k, 0.6, have_plan, &dummy,
-                           nullptr, (double *)d, b, 0);
+        st = pcg_loss_grad(nullptr, 0, Ar, (const double *)d, *B, (const double *)d, (const double *)d, (int)k, 0.6,
+                           have_plan, &dummy, nullptr, (double *)d, b, 0);
+        break;
+    }
+    case CSRK_WS_PCG_DIST: {
+        if (!B || k < 1) return CSRK_ERR_INVALID_ARG;
+        double dummy = 0.0;
+        st = pcg_loss_grad(nullptr, 0, Ar, (const double *)d, *B, (const double *)d, (const double *)d, (int)k, 0.6, 0,
+                           &dummy, nullptr, (double *)d, b, 0);
         break;
     }
     default: return CSRK_ERR_INVALID_ARG;

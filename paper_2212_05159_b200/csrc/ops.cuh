@@ -55,8 +55,9 @@ int dense_gemm_tn(csrk_dtype dt, int64_t n, int64_t C, int64_t F, const void *X,
 // dA[p] = -(w_i x_j) at the stored (i, j) of A (fp64; the masked outer product of the SpTRSV VJP)
 int trsv_outer(const csrk_pattern &A, const double *w, const double *x, double *dA, cudaStream_t s);
 
-int pcg_loss_grad(const csrk_pattern &A, const double *Av, const csrk_pattern &L, const double *Lv, const double *b,
-                  int N, double gamma, int precond, double *loss_host, double *resid_host, double *dL, Bump &ws,
-                  cudaStream_t s);
+// comm == nullptr, off == 0: one GPU; else the rank's rows of a row-sharded step (extended vectors)
+int pcg_loss_grad(const csrk_comm *comm, int64_t off, const csrk_pattern &A, const double *Av, const csrk_pattern &L,
+                  const double *Lv, const double *b, int N, double gamma, int precond, double *loss_host,
+                  double *resid_host, double *dL, Bump &ws, cudaStream_t s);
 
 }  // namespace csrk

@@ -16,6 +16,7 @@
 // replace the SpMV VJPs.
 // All reductions are fixed-grid, fixed-order (deterministic).
 #include <cmath>
+#include <mutex>
 #include <vector>
 
 #include "ops.cuh"
@@ -154,9 +155,16 @@ struct PcgWs {
 
 static size_t spmv_ws_bytes(const csrk_pattern &M)
 {
-    Bump b(nullptr, 0);
-    spmv_fwd(CSRK_F64, CSRK_OP_N, M, nullptr, nullptr, nullptr, nullptr, nullptr, b, 0);
-    return b.used + 256;
+    size_t m = 0;
+    const void *d = M.indptr;
+    for (int op = 0; op < 2; ++op) {
+        Bump f(nullptr, 0), g(nullptr, 0);
+        spmv_fwd(CSRK_F64, (csrk_op)op, M, d, nullptr, nullptr, d, (void *)d, f, 0);
+        spmv_bwd(CSRK_F64, (csrk_op)op, M, d, nullptr, nullptr, d, d, (void *)d, (void *)d, g, 0);
+        m = f.used > m ? f.used : m;
+        m = g.used > m ? g.used : m;
+    }
+    return m + 256;
 }
 
 static size_t solve_ws_bytes(const csrk_pattern &L)
@@ -181,14 +189,17 @@ static size_t solve_ws_bytes(const csrk_pattern &L)
     return m + 256;
 }
 
+// Vectors of length n_ext (extended layout of a row-sharded rank; n_ext = n on one GPU): the
+// owned part is [off, off + m).  Saved per iteration: p_{i-1} (extended: the halo-gathered input of
+// A p), r_i and q_i (owned).
 static void carve_pcg(const csrk_pattern &A, const csrk_pattern &L, int N, int precond, PcgWs &w, Bump &ws)
 {
-    const int64_t n = A.nrows;
-    w.pb = ws.take<double>((size_t)N * n);
-    w.rb = ws.take<double>((size_t)(N + 1) * n);
-    w.qb = ws.take<double>((size_t)N * n);
+    const int64_t m = A.nrows, ne = A.ncols > m ? A.ncols : m;
+    w.pb = ws.take<double>((size_t)N * ne);
+    w.rb = ws.take<double>((size_t)(N + 1) * m);
+    w.qb = ws.take<double>((size_t)N * m);
     double **tv[] = {&w.u, &w.z, &w.rbar, &w.pbar, &w.zbar, &w.ubar, &w.qbar, &w.tmp};
-    for (auto p : tv) *p = ws.take<double>(n);
+    for (auto p : tv) *p = ws.take<double>(ne);
     w.dAt = ws.take<double>(L.nnz > 0 ? L.nnz : 1);
     w.part = ws.take<double>(kVecGrid);
     double *sc = ws.take<double>(5 * (size_t)(N + 1) + 8);
@@ -229,34 +240,38 @@ static int dot_to(int64_t n, const double *x, const double *y, double *dst, doub
     return CSRK_OK;
 }
 
-int pcg_loss_grad(const csrk_pattern &A, const double *Av, const csrk_pattern &L, const double *Lv, const double *b,
-                  int N, double gamma, int precond, double *loss_host, double *resid_host, double *dL, Bump &ws,
-                  cudaStream_t s)
+// The whole step enqueued on `s` (no synchronisation; capturable when the comm is).
+static int pcg_enqueue(const csrk_comm *comm, int64_t off, const csrk_pattern &A, const double *Av,
+                       const csrk_pattern &L, const double *Lv, const double *b, int N, double gamma, int precond,
+                       double *dL, PcgWs &w, cudaStream_t s)
 {
-    PcgWs w{};
-    carve_pcg(A, L, N, precond, w, ws);
-    if (ws.sizing()) return CSRK_OK;
-    const int64_t n = A.nrows;
+    const int64_t m = A.nrows;                 // owned rows
+    auto own = [&](double *v) { return v + off; };
     auto sub = [&]() { return Bump(w.sub, w.sub_bytes); };
-    auto Lt = [&](const double *in, double *out) {   // out = L^T in
-        Bump bw = sub();
-        return spmv_fwd(CSRK_F64, CSRK_OP_T, L, Lv, nullptr, nullptr, in, out, bw, s);
+    // exchanges (no-ops on one GPU)
+    auto gather = [&](double *v) -> int { return comm ? comm->halo(comm->ctx, v, 0, (csrk_stream_t)s) : CSRK_OK; };
+    auto reduce = [&](double *v) -> int { return comm ? comm->halo(comm->ctx, v, 1, (csrk_stream_t)s) : CSRK_OK; };
+    auto allred = [&](double *v, int64_t c) -> int {
+        return comm ? comm->allreduce_sum(comm->ctx, v, c, (csrk_stream_t)s) : CSRK_OK;
     };
-    auto Ln = [&](const double *in, double *out) {   // out = L in
-        Bump bw = sub();
-        return spmv_fwd(CSRK_F64, CSRK_OP_N, L, Lv, nullptr, nullptr, in, out, bw, s);
-    };
-    if (precond) {  // L^T (pattern + perm) once per call, for the transposed solves
+    if (precond) {  // L^T (pattern + perm) once per call, for the transposed solves (one GPU only)
         Bump bw = sub();
         CSRK_TRY(transpose_impl(CSRK_F64, L, nullptr, const_cast<int64_t *>(w.LT.indptr),
                                 const_cast<int32_t *>(w.LT.indices), nullptr, w.LTperm, bw, s));
     }
-    // z = M r with the intermediate in w.u:  M = L L^T: u = L^T r, z = L u;
-    // precond = solve: M = (L L^T)^{-1}: u = L^{-1} r, z = L^{-T} u
+    // z = M r (owned r, owned z) with the intermediate u (extended) in w.u:
+    //   M = L L^T: u = L^T r (op T: an extended partial, halo-reduced, then halo-gathered
+    //   for the op-N product), z = L u;   precond = solve: u = L^{-1} r, z = L^{-T} u
     auto applyM = [&](const double *r, double *z) -> int {
         if (!precond) {
-            CSRK_TRY(Lt(r, w.u));
-            return Ln(w.u, z);
+            {
+                Bump bw = sub();
+                CSRK_TRY(spmv_fwd(CSRK_F64, CSRK_OP_T, L, Lv, nullptr, nullptr, r, w.u, bw, s));
+            }
+            CSRK_TRY(reduce(w.u));
+            CSRK_TRY(gather(w.u));
+            Bump bw = sub();
+            return spmv_fwd(CSRK_F64, CSRK_OP_N, L, Lv, nullptr, nullptr, w.u, z, bw, s);
         }
         {
             Bump bw = sub();
@@ -267,18 +282,21 @@ int pcg_loss_grad(const csrk_pattern &A, const double *Av, const csrk_pattern &L
     };
     // adjoint of z = M r given w.zbar (w.u, z of the same r): dL += ..., rbar += M^T zbar (if asked)
     auto adjM = [&](const double *r, const double *z, bool want_rbar) -> int {
+        double *rb_add = own(w.tmp);           // owned-length contribution to rbar
         if (!precond) {
-            // z = L u:  Lbar += zbar u^T (.) mask(L);  ubar = L^T zbar
+            // z = L gather(u):  Lbar += zbar u^T (.) mask(L);  ubar = reduce(L^T zbar)
             {
                 Bump bw = sub();
                 CSRK_TRY(spmv_bwd(CSRK_F64, CSRK_OP_N, L, Lv, nullptr, nullptr, w.u, w.zbar, w.dAt, w.ubar, bw, s));
             }
             LIN3(L.nnz, dL, ONE, dL, ONE, w.dAt, ONE, nullptr, nullptr, nullptr);
-            // u = L^T r:  Lbar += r ubar^T (.) mask(L);  rbar += L ubar
+            CSRK_TRY(reduce(w.ubar));
+            CSRK_TRY(gather(w.ubar));
+            // u = reduce(L^T r):  Lbar += r ubar^T (.) mask(L);  rbar += L gather(ubar)
             {
                 Bump bw = sub();
                 CSRK_TRY(spmv_bwd(CSRK_F64, CSRK_OP_T, L, Lv, nullptr, nullptr, r, w.ubar, w.dAt,
-                                  want_rbar ? w.tmp : nullptr, bw, s));
+                                  want_rbar ? rb_add : nullptr, bw, s));
             }
             LIN3(L.nnz, dL, ONE, dL, ONE, w.dAt, ONE, nullptr, nullptr, nullptr);
         } else {
@@ -292,77 +310,180 @@ int pcg_loss_grad(const csrk_pattern &A, const double *Av, const csrk_pattern &L
             // u = L^{-1} r:  rbar += L^{-T} ubar;  Lbar += -(L^{-T} ubar) u^T (.) mask(L)
             {
                 Bump bw = sub();
-                CSRK_TRY(sptrsv_bwd(CSRK_F64, L, Lv, &w.LT, w.LTperm, 0, 0, w.u, w.ubar, w.dAt, w.tmp, bw, s));
+                CSRK_TRY(sptrsv_bwd(CSRK_F64, L, Lv, &w.LT, w.LTperm, 0, 0, w.u, w.ubar, w.dAt, rb_add, bw, s));
             }
             LIN3(L.nnz, dL, ONE, dL, ONE, w.dAt, ONE, nullptr, nullptr, nullptr);
         }
-        if (want_rbar) LIN3(n, w.rbar, ONE, w.rbar, ONE, w.tmp, ONE, nullptr, nullptr, nullptr);
+        if (want_rbar) LIN3(m, w.rbar, ONE, w.rbar, ONE, rb_add, ONE, nullptr, nullptr, nullptr);
         return CSRK_OK;
     };
     const Scal &S = w.S;
     double *part = w.part;
-    auto P = [&](int i) { return w.pb + (size_t)i * n; };       // p_i, i = 0..N-1
-    auto R = [&](int i) { return w.rb + (size_t)i * n; };       // r_i, i = 0..N
-    auto Q = [&](int i) { return w.qb + (size_t)(i - 1) * n; }; // q_i, i = 1..N
+    const int64_t ne = A.ncols > m ? A.ncols : m;
+    auto Pe = [&](int i) { return w.pb + (size_t)i * ne; };     // p_i extended, i = 0..N-1
+    auto P = [&](int i) { return Pe(i) + off; };                // its owned part
+    auto R = [&](int i) { return w.rb + (size_t)i * m; };       // r_i, i = 0..N (owned)
+    auto Q = [&](int i) { return w.qb + (size_t)(i - 1) * m; }; // q_i, i = 1..N (owned)
+    // dot over the owned rows, then summed over ranks
+    auto gdot = [&](const double *x, const double *y, double *dst, double sign) -> int {
+        CSRK_TRY(dot_to(m, x, y, dst, sign, part, s));
+        return allred(dst, 1);
+    };
 
     // ---------------- forward
-    CSRK_TRY(dot_to(n, b, b, S.bb, 1.0, part, s));
-    LIN3(n, R(0), ONE, b, ONE, nullptr, ONE, nullptr, nullptr, nullptr);
+    CSRK_TRY(gdot(b, b, S.bb, 1.0));
+    LIN3(m, R(0), ONE, b, ONE, nullptr, ONE, nullptr, nullptr, nullptr);
     CSRK_TRY(applyM(b, P(0)));                                 // p0 = z0
-    CSRK_TRY(dot_to(n, b, P(0), &S.rho[0], 1.0, part, s));
+    CSRK_TRY(gdot(b, P(0), &S.rho[0], 1.0));
     for (int i = 1; i <= N; ++i) {
+        CSRK_TRY(gather(Pe(i - 1)));
         {
             Bump bw = sub();
-            CSRK_TRY(spmv_fwd(CSRK_F64, CSRK_OP_N, A, Av, nullptr, nullptr, P(i - 1), Q(i), bw, s));
+            CSRK_TRY(spmv_fwd(CSRK_F64, CSRK_OP_N, A, Av, nullptr, nullptr, Pe(i - 1), Q(i), bw, s));
         }
-        CSRK_TRY(dot_to(n, P(i - 1), Q(i), &S.s[i], 1.0, part, s));
-        // r_i = r_{i-1} - (rho_{i-1}/s_i) q_i ; nr2_i = r_i.r_i
-        LIN3(n, R(i), ONE, R(i - 1), (Cf{-1.0, &S.rho[i - 1], &S.s[i]}), Q(i), ONE, nullptr, nullptr, part);
+        CSRK_TRY(gdot(P(i - 1), Q(i), &S.s[i], 1.0));
+        // r_i = r_{i-1} - (rho_{i-1}/s_i) q_i ; nr2_i = r_i.r_i (summed over ranks once, at the end)
+        LIN3(m, R(i), ONE, R(i - 1), (Cf{-1.0, &S.rho[i - 1], &S.s[i]}), Q(i), ONE, nullptr, nullptr, part);
         CSRK_LAUNCH(k_finish, 1, kVecTPB, 0, s, (const double *)part, kVecGrid, &S.nr2[i], 1.0);
         if (i == N) break;                                     // rho_N, p_N do not reach the loss
-        CSRK_TRY(applyM(R(i), w.z));
-        CSRK_TRY(dot_to(n, R(i), w.z, &S.rho[i], 1.0, part, s));
+        CSRK_TRY(applyM(R(i), own(w.z)));
+        CSRK_TRY(gdot(R(i), own(w.z), &S.rho[i], 1.0));
         // p_i = z_i + (rho_i / rho_{i-1}) p_{i-1}
-        LIN3(n, P(i), ONE, w.z, (Cf{1.0, &S.rho[i], &S.rho[i - 1]}), P(i - 1), ONE, nullptr, nullptr, nullptr);
+        LIN3(m, P(i), ONE, own(w.z), (Cf{1.0, &S.rho[i], &S.rho[i - 1]}), P(i - 1), ONE, nullptr, nullptr, nullptr);
     }
+    CSRK_TRY(allred(S.nr2 + 1, N));
     CSRK_LAUNCH(k_loss, 1, 1, 0, s, S, N, gamma);
 
     // ---------------- reverse
     CSRK_CUDA(cudaMemsetAsync(dL, 0, sizeof(double) * (size_t)L.nnz, s));
-    CSRK_CUDA(cudaMemsetAsync(w.rbar, 0, sizeof(double) * (size_t)n, s));
-    CSRK_CUDA(cudaMemsetAsync(w.pbar, 0, sizeof(double) * (size_t)n, s));
+    CSRK_CUDA(cudaMemsetAsync(w.rbar, 0, sizeof(double) * (size_t)m, s));
+    CSRK_CUDA(cudaMemsetAsync(w.pbar, 0, sizeof(double) * (size_t)m, s));
     for (int i = N; i >= 1; --i) {
         if (i < N) {
             // p_i = z_i + beta_i p_{i-1}:  betabar = pbar . p_{i-1}
-            CSRK_TRY(dot_to(n, w.pbar, P(i - 1), S.betabar, 1.0, part, s));
+            CSRK_TRY(gdot(w.pbar, P(i - 1), S.betabar, 1.0));
             CSRK_LAUNCH(k_bwd_beta, 1, 1, 0, s, S, i);
-            CSRK_TRY(applyM(R(i), w.z));                       // recompute u_i, z_i
+            CSRK_TRY(applyM(R(i), own(w.z)));                  // recompute u_i, z_i
             // zbar = pbar + rhobar_i r_i ;  rbar += cn_i r_i + rhobar_i z_i
-            LIN3(n, w.zbar, ONE, w.pbar, (Cf{1.0, &S.rhobar[i], nullptr}), R(i), ONE, nullptr, nullptr, nullptr);
-            LIN3(n, w.rbar, ONE, w.rbar, (Cf{1.0, &S.cn[i], nullptr}), R(i), (Cf{1.0, &S.rhobar[i], nullptr}), w.z,
-                 nullptr, nullptr);
-            CSRK_TRY(adjM(R(i), w.z, true));
+            LIN3(m, w.zbar, ONE, w.pbar, (Cf{1.0, &S.rhobar[i], nullptr}), R(i), ONE, nullptr, nullptr, nullptr);
+            LIN3(m, w.rbar, ONE, w.rbar, (Cf{1.0, &S.cn[i], nullptr}), R(i), (Cf{1.0, &S.rhobar[i], nullptr}),
+                 own(w.z), nullptr, nullptr);
+            CSRK_TRY(adjM(R(i), own(w.z), true));
         } else {
-            LIN3(n, w.rbar, ONE, w.rbar, (Cf{1.0, &S.cn[i], nullptr}), R(i), ONE, nullptr, nullptr, nullptr);
+            LIN3(m, w.rbar, ONE, w.rbar, (Cf{1.0, &S.cn[i], nullptr}), R(i), ONE, nullptr, nullptr, nullptr);
         }
         // r_i = r_{i-1} - alpha_i q_i:  alphabar = -rbar . q_i ;  qbar = -alpha_i rbar + sbar p_{i-1}
-        CSRK_TRY(dot_to(n, w.rbar, Q(i), S.alphabar, -1.0, part, s));
+        CSRK_TRY(gdot(w.rbar, Q(i), S.alphabar, -1.0));
         CSRK_LAUNCH(k_bwd_alpha, 1, 1, 0, s, S, i);
-        LIN3(n, w.qbar, (Cf{-1.0, &S.rho[i - 1], &S.s[i]}), w.rbar, (Cf{1.0, S.sbar, nullptr}), P(i - 1), ONE,
+        LIN3(m, w.qbar, (Cf{-1.0, &S.rho[i - 1], &S.s[i]}), w.rbar, (Cf{1.0, S.sbar, nullptr}), P(i - 1), ONE,
              nullptr, nullptr, nullptr);
-        // pbar_{i-1} = beta_i pbar_i + sbar q_i + A^T qbar
+        // q_i = A gather(p_{i-1}):  pbar_{i-1} = beta_i pbar_i + sbar q_i + reduce(A^T qbar)
         {
             Bump bw = sub();
             CSRK_TRY(spmv_fwd(CSRK_F64, CSRK_OP_T, A, Av, nullptr, nullptr, w.qbar, w.tmp, bw, s));
         }
+        CSRK_TRY(reduce(w.tmp));
         const Cf beta = i < N ? Cf{1.0, &S.rho[i], &S.rho[i - 1]} : Cf{0.0, nullptr, nullptr};
-        LIN3(n, w.pbar, beta, w.pbar, (Cf{1.0, S.sbar, nullptr}), Q(i), ONE, w.tmp, nullptr, nullptr);
+        LIN3(m, w.pbar, beta, w.pbar, (Cf{1.0, S.sbar, nullptr}), Q(i), ONE, own(w.tmp), nullptr, nullptr);
     }
     // p0 = z0, rho0 = r0.z0 (r0 = b):  zbar = pbar + rhobar_0 b
-    LIN3(n, w.zbar, ONE, w.pbar, (Cf{1.0, &S.rhobar[0], nullptr}), b, ONE, nullptr, nullptr, nullptr);
-    CSRK_TRY(applyM(b, w.z));                                  // recompute u_0, z_0
-    CSRK_TRY(adjM(b, w.z, false));
+    LIN3(m, w.zbar, ONE, w.pbar, (Cf{1.0, &S.rhobar[0], nullptr}), b, ONE, nullptr, nullptr, nullptr);
+    CSRK_TRY(applyM(b, own(w.z)));                             // recompute u_0, z_0
+    CSRK_TRY(adjM(b, own(w.z), false));
+    return CSRK_OK;
+}
 
+// One CUDA graph per argument set (stream capture of pcg_enqueue), replayed on later calls.
+struct PcgGraphKey {
+    const void *ptr[10];
+    int64_t sz[6];
+    int N;
+    double gamma;
+    bool operator==(const PcgGraphKey &o) const
+    {
+        for (int i = 0; i < 10; ++i)
+            if (ptr[i] != o.ptr[i]) return false;
+        for (int i = 0; i < 6; ++i)
+            if (sz[i] != o.sz[i]) return false;
+        return N == o.N && gamma == o.gamma;
+    }
+};
+struct PcgGraph {
+    PcgGraphKey key;
+    int dev;
+    cudaGraphExec_t exec;
+    uint64_t kernels;   // csrk kernels captured (counted once per replay by csrk_launch_count)
+};
+static std::mutex g_graph_mu;
+static std::vector<PcgGraph> g_graphs;
+
+static cudaStream_t capture_stream(int dev)
+{
+    static std::mutex mu;
+    static cudaStream_t streams[64] = {};
+    std::lock_guard<std::mutex> g(mu);
+    if (!streams[dev & 63] && cudaStreamCreateWithFlags(&streams[dev & 63], cudaStreamNonBlocking) != cudaSuccess)
+        return nullptr;
+    return streams[dev & 63];
+}
+
+int pcg_loss_grad(const csrk_comm *comm, int64_t off, const csrk_pattern &A, const double *Av, const csrk_pattern &L,
+                  const double *Lv, const double *b, int N, double gamma, int precond, double *loss_host,
+                  double *resid_host, double *dL, Bump &ws, cudaStream_t s)
+{
+    PcgWs w{};
+    carve_pcg(A, L, N, precond, w, ws);
+    if (ws.sizing()) return CSRK_OK;
+    const bool graph = knob("PCG_GRAPH", 1) && (!comm || comm->capturable);
+    if (!graph) {
+        CSRK_TRY(pcg_enqueue(comm, off, A, Av, L, Lv, b, N, gamma, precond, dL, w, s));
+    } else {
+        PcgGraphKey key{{A.indptr, A.indices, Av, L.indptr, L.indices, Lv, b, dL, ws.base, comm ? comm->ctx : nullptr},
+                        {A.nrows, A.ncols, A.nnz, L.nnz, off, (int64_t)ws.cap + precond},
+                        N, gamma};
+        const int dev = DevOnce::dev();
+        cudaGraphExec_t exec = nullptr;
+        {
+            std::lock_guard<std::mutex> g(g_graph_mu);
+            for (auto &e : g_graphs)
+                if (e.dev == dev && e.key == key) exec = e.exec;
+        }
+        uint64_t nk = 0;
+        {
+            std::lock_guard<std::mutex> g(g_graph_mu);
+            for (auto &e : g_graphs)
+                if (e.dev == dev && e.key == key) nk = e.kernels;
+        }
+        if (exec) {
+            g_launches.fetch_add(nk, std::memory_order_relaxed);   // the graph's kernels run again
+        } else {
+            // capture on a private non-blocking stream (the caller's may be the legacy default
+            // stream, which cannot be captured); the graph is then launched on the caller's stream
+            cudaStream_t cs = capture_stream(dev);
+            if (!cs) return CSRK_ERR_CUDA;
+            cudaGraph_t gr = nullptr;
+            const uint64_t before = g_launches.load(std::memory_order_relaxed);
+            CSRK_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+            const int st = pcg_enqueue(comm, off, A, Av, L, Lv, b, N, gamma, precond, dL, w, cs);
+            const cudaError_t ce = cudaStreamEndCapture(cs, &gr);
+            if (st != CSRK_OK || ce != cudaSuccess) {
+                if (gr) cudaGraphDestroy(gr);
+                (void)cudaGetLastError();
+                return st != CSRK_OK ? st : CSRK_ERR_CUDA;
+            }
+            const cudaError_t ie = cudaGraphInstantiate(&exec, gr, 0);
+            cudaGraphDestroy(gr);
+            if (ie != cudaSuccess) return CSRK_ERR_CUDA;
+            std::lock_guard<std::mutex> g(g_graph_mu);
+            if (g_graphs.size() >= 8) {     // a handful of argument sets in flight: drop the oldest
+                cudaGraphExecDestroy(g_graphs.front().exec);
+                g_graphs.erase(g_graphs.begin());
+            }
+            g_graphs.push_back(PcgGraph{key, dev, exec, g_launches.load(std::memory_order_relaxed) - before});
+        }
+        CSRK_CUDA(cudaGraphLaunch(exec, s));
+    }
+    const Scal &S = w.S;
     CSRK_CUDA(cudaMemcpyAsync(loss_host, S.loss, sizeof(double), cudaMemcpyDeviceToHost, s));
     if (resid_host) {
         std::vector<double> nr2(N + 1);

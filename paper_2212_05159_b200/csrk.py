@@ -25,7 +25,7 @@ F32, F64 = 0, 1
 OP_N, OP_T = 0, 1
 WS = dict(spmv_fwd=0, spmv_bwd=1, spmm_fwd=2, spmm_bwd=3, csr_transpose=4, spgemm_symbolic=5,
           spgemm_numeric=6, spgemm_bwd=7, pcg=8, spadd_symbolic=9, spai=10, sptrsv_fwd=11,
-          sptrsv_bwd=12, gcn_fwd=13, gcn_bwd=14, dense_gemm_tn=15)
+          sptrsv_bwd=12, gcn_fwd=13, gcn_bwd=14, dense_gemm_tn=15, pcg_dist=16)
 
 # Every symbol declared in include/csrk.h (checked by tests/test_abi_cpu.py).
 ABI_SYMBOLS = ("csrk_spmv_fwd", "csrk_spmv_bwd", "csrk_spmm_fwd", "csrk_spmm_bwd", "csrk_csr_transpose",
@@ -33,12 +33,29 @@ ABI_SYMBOLS = ("csrk_spmv_fwd", "csrk_spmv_bwd", "csrk_spmm_fwd", "csrk_spmm_bwd
                "csrk_status_string", "csrk_launch_count", "csrk_version", "csrk_pcg_loss_grad",
                "csrk_spadd_symbolic", "csrk_spadd_numeric", "csrk_spadd_bwd", "csrk_spai_loss_grad",
                "csrk_sptrsv_fwd", "csrk_sptrsv_bwd", "csrk_gcn_fwd", "csrk_gcn_bwd", "csrk_dense_gemm_nn",
-               "csrk_dense_gemm_tn")
+               "csrk_dense_gemm_tn", "csrk_pcg_loss_grad_dist", "csrk_comm_nccl_unique_id", "csrk_comm_nccl_create",
+               "csrk_comm_nccl_destroy")
 
 
 class Pattern(ctypes.Structure):
     _fields_ = [("nrows", ctypes.c_int64), ("ncols", ctypes.c_int64), ("nnz", ctypes.c_int64),
                 ("indptr", ctypes.c_void_p), ("indices", ctypes.c_void_p)]
+
+
+AllreduceFn = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p)
+HaloFn = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p)
+
+
+class Comm(ctypes.Structure):
+    """csrk_comm (include/csrk.h): the exchanges of a row-sharded step."""
+    _fields_ = [("ctx", ctypes.c_void_p), ("allreduce_sum", AllreduceFn), ("halo", HaloFn),
+                ("capturable", ctypes.c_int)]
+
+
+class Halo(ctypes.Structure):
+    _fields_ = [("npeers", ctypes.c_int), ("peer", ctypes.POINTER(ctypes.c_int)),
+                ("own_off", ctypes.POINTER(ctypes.c_int64)), ("own_len", ctypes.POINTER(ctypes.c_int64)),
+                ("ghost_off", ctypes.POINTER(ctypes.c_int64)), ("ghost_len", ctypes.POINTER(ctypes.c_int64))]
 
 
 class CsrkError(RuntimeError):
@@ -81,6 +98,11 @@ def lib() -> ctypes.CDLL:
     L.csrk_gcn_bwd.argtypes = [I, Pat, P, PatP, P, I64, P, P, I64, P, I64, P, P, SZ, P]
     L.csrk_dense_gemm_nn.argtypes = [I, I64, I64, I64, P, I64, P, I, P, I64, P]
     L.csrk_dense_gemm_tn.argtypes = [I, I64, I64, I64, P, I64, P, I64, P, P, SZ, P]
+    L.csrk_pcg_loss_grad_dist.argtypes = [ctypes.POINTER(Comm), I64, Pat, P, Pat, P, P, I, D, ctypes.POINTER(D),
+                                          ctypes.POINTER(D), P, P, SZ, P]
+    L.csrk_comm_nccl_unique_id.argtypes = [P]
+    L.csrk_comm_nccl_create.argtypes = [P, I, I, ctypes.POINTER(Halo), ctypes.POINTER(Comm)]
+    L.csrk_comm_nccl_destroy.argtypes = [ctypes.POINTER(Comm)]
     L.csrk_status_string.restype = ctypes.c_char_p
     L.csrk_status_string.argtypes = [I]
     L.csrk_launch_count.restype = ctypes.c_uint64
@@ -477,4 +499,58 @@ def pcg_loss_grad(A: CSR, L: CSR, b: torch.Tensor, n_it: int = 50, gamma: float 
     _check(lib().csrk_pcg_loss_grad(pa, _ptr(A.values), pl, _ptr(L.values), _ptr(b), int(n_it), float(gamma), pc,
                                     ctypes.byref(loss), resid, _ptr(dL), _ptr(ws), ws.numel(), _stream()),
            "pcg_loss_grad")
+    return float(loss.value), list(resid), dL
+
+
+# ---------------------------------------------------------------- row-sharded multi-GPU
+def halo_struct(spec):
+    """ctypes csrk_halo from a dict of equal-length lists: peer, own_off, own_len, ghost_off, ghost_len."""
+    n = len(spec["peer"])
+    arr = lambda t, v: (t * max(n, 1))(*v)
+    h = Halo(n, arr(ctypes.c_int, spec["peer"]), arr(ctypes.c_int64, spec["own_off"]),
+             arr(ctypes.c_int64, spec["own_len"]), arr(ctypes.c_int64, spec["ghost_off"]),
+             arr(ctypes.c_int64, spec["ghost_len"]))
+    return h
+
+
+def comm_nccl(rank: int, world: int, halo_spec, group=None) -> Comm:
+    """csrk_comm over NCCL (comm.cu): rank 0 draws the NCCL unique id, torch.distributed broadcasts
+    it, every rank creates its communicator (collective).  Destroy with comm_destroy."""
+    import torch.distributed as tdist
+    buf = (ctypes.c_char * 128)()
+    if rank == 0:
+        _check(lib().csrk_comm_nccl_unique_id(buf), "comm_nccl_unique_id")
+    obj = [bytes(buf)]
+    tdist.broadcast_object_list(obj, src=0, group=group)
+    ctypes.memmove(buf, obj[0], 128)
+    c = Comm()
+    h = halo_struct(halo_spec)
+    _check(lib().csrk_comm_nccl_create(buf, rank, world, ctypes.byref(h), ctypes.byref(c)), "comm_nccl_create")
+    return c
+
+
+def comm_destroy(c: Comm):
+    _check(lib().csrk_comm_nccl_destroy(ctypes.byref(c)), "comm_nccl_destroy")
+
+
+def pcg_loss_grad_dist(comm: Comm | None, own_off: int, A: CSR, L: CSR, b: torch.Tensor, n_it: int = 50,
+                       gamma: float = 0.6, dL: torch.Tensor | None = None, ws: torch.Tensor | None = None):
+    """One rank's share of the row-sharded config-5 step (csrk_pcg_loss_grad_dist): A, L = the
+    rank's rows (columns in extended coordinates), b its owned entries.  Returns (loss, residual
+    norms, dL on L's rows) -- loss and residuals are global.  `ws` may be passed to reuse a
+    workspace across calls (the CUDA-graph cache is keyed by it)."""
+    if dL is None:
+        dL = torch.empty_like(L.values)
+    pa, pl = A.pattern(), L.pattern()
+    nbytes = ctypes.c_size_t(0)
+    _check(lib().csrk_workspace_size(WS["pcg_dist"], F64, ctypes.byref(pa), ctypes.byref(pl), n_it, 0,
+                                     ctypes.byref(nbytes)), "workspace_size(pcg_dist)")
+    if ws is None or ws.numel() < int(nbytes.value):
+        ws = torch.empty(max(int(nbytes.value), 1), dtype=torch.uint8, device=b.device)
+    loss = ctypes.c_double(0.0)
+    resid = (ctypes.c_double * n_it)()
+    _check(lib().csrk_pcg_loss_grad_dist(ctypes.byref(comm) if comm is not None else None, int(own_off), pa,
+                                         _ptr(A.values), pl, _ptr(L.values), _ptr(b), int(n_it), float(gamma),
+                                         ctypes.byref(loss), resid, _ptr(dL), _ptr(ws), ws.numel(), _stream()),
+           "pcg_loss_grad_dist")
     return float(loss.value), list(resid), dL
