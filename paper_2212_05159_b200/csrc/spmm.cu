@@ -621,6 +621,335 @@ __global__ __launch_bounds__(wide_tpb<MODE>(), wide_minb<MODE>()) void k_spmm_wi
     }
 }
 
+// ---------------------------------------------------------------- persistent pipelined wide path
+// k_spmm_wide stages each tile's metadata (indptr slice, then indices / values / perm slices)
+// with dependent loads at the start of the CTA: ncu attributed ~25 % of the backward's stall
+// samples to that chain.  Here persistent CTAs walk tiles t = blockIdx.x + k gridDim.x and the
+// metadata arrives by TMA bulk copies issued AHEAD: the indptr slice two tiles ahead, the
+// index / perm / value slices and the near-diagonal band one tile ahead (their range comes from
+// the indptr slice), each completing on an mbarrier.  Slices are copied as the 16-byte-aligned
+// superset of their range; a tile whose superset would run past the end of an array or that
+// holds more than kPCAP nonzeros reads its metadata from global memory instead ("direct").
+// Values of the transposed traversal are gathered through perm in the compute batch (with the
+// dense-row gathers), not in the staging chain.  The compute is k_spmm_wide's.
+constexpr int kPTPB = 128;
+constexpr int kPRPG = 4;
+constexpr int kPRT = kPTPB / kWG * kPRPG;   // 128 rows per tile
+constexpr int kPCAP = 1024;                 // staged nonzeros per tile
+
+template <typename T, int NV, int MODE, bool BAND>
+struct PipeLayout {
+    static constexpr bool PERM = MODE == SP_FWD_PERM || MODE == SP_FUSED_T;
+    static constexpr bool VAL = MODE == SP_FWD;      // contiguous values staged
+    static constexpr int RB = NV * 128;
+    static constexpr int kBand = kPRT + 2 * kBandH + 1;
+    static constexpr size_t ptr = 0;                                            // int64 [3][kPRT + 4]
+    static constexpr size_t idx = ptr + 3 * (kPRT + 4) * 8;                     // int32 [2][kPCAP + 8]
+    static constexpr size_t perm = idx + 2 * (kPCAP + 8) * 4;                   // int64 [2][kPCAP + 4]
+    static constexpr size_t val = perm + (PERM ? 2 * (kPCAP + 4) * 8 : 0);      // T [2][kPCAP + 32/sizeof T]
+    static constexpr size_t band = (val + (VAL ? 2 * (kPCAP + 32 / sizeof(T)) * sizeof(T) : 0) + 127) & ~size_t(127);
+    static constexpr size_t wrow = band + (BAND ? 2 * (size_t)kBand * RB : 0);   // staged W rows [2][kPRT]
+    static constexpr size_t total_nw = wrow;
+    static constexpr size_t total_w = wrow + 2 * (size_t)kPRT * RB;
+};
+
+template <int MODE, int G> constexpr int pipe_minb()
+{
+    return G == 8 ? 5 : (MODE == SP_FWD || MODE == SP_FWD_PERM ? 3 : 4);
+}
+
+template <typename T, int NV, int MODE, bool BAND, int G, bool WST, bool L1G = false>
+__global__ __launch_bounds__(kPTPB, pipe_minb<MODE, G>()) void k_spmm_pipe(SpmmArgs<T> a, int64_t ntiles)
+{
+    pdl_wait();
+    using PL = PipeLayout<T, NV, MODE, BAND>;
+    constexpr bool PERM = PL::PERM;
+    constexpr bool ACC = MODE != SP_SDDMM;
+    constexpr bool DOT = MODE == SP_SDDMM || MODE == SP_FUSED_T;
+    constexpr int E = V32<T>::E;
+    constexpr int NVL = NV * kWG / G;   // 32-byte vectors per lane (a row is NV * 4 vectors)
+    constexpr int NE = NVL * E;
+    constexpr int RPG = kPRT * G / kPTPB;   // rows per group per tile
+    constexpr int RB = PL::RB;
+    constexpr int kBand = PL::kBand;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bp[3], bm[2];
+    __shared__ int s_off_ptr[3], s_off_idx[2], s_off_perm[2], s_off_val[2], s_direct[2];
+    __shared__ int64_t s_b0[2], s_b1[2];
+    int64_t *ptr_buf = reinterpret_cast<int64_t *>(smem + PL::ptr);
+    int32_t *idx_buf = reinterpret_cast<int32_t *>(smem + PL::idx);
+    int64_t *perm_buf = reinterpret_cast<int64_t *>(smem + PL::perm);
+    T *val_buf = reinterpret_cast<T *>(smem + PL::val);
+    unsigned char *band_buf = smem + PL::band;
+    unsigned char *w_buf = smem + PL::wrow;     // WST: the tile's W rows (dot modes), by TMA
+
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int i = 0; i < 3; ++i) mbar_init(&bp[i], 1);
+        for (int i = 0; i < 2; ++i) mbar_init(&bm[i], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const int64_t nptr = a.nrows + 1;
+    const int64_t nnz_all = a.indptr[a.nrows] - a.indptr[0];   // indptr[0] = 0 (canonical)
+    auto tile_of = [&](int64_t k) { return (int64_t)blockIdx.x + k * (int64_t)gridDim.x; };
+    auto rows_of = [&](int64_t t, int64_t &r0, int &nr) {
+        r0 = t * kPRT;
+        nr = (int)(a.nrows - r0 < kPRT ? a.nrows - r0 : kPRT);
+    };
+    // thread 0: indptr slice of tile t into ptr stage ps (aligned superset, or a plain copy)
+    auto issue_ptr = [&](int64_t t, int ps) {
+        int64_t r0;
+        int nr;
+        rows_of(t, r0, nr);
+        const int64_t lo = r0 & ~int64_t(1), hi = (r0 + nr + 1 + 1) & ~int64_t(1);
+        int64_t *dst = ptr_buf + ps * (kPRT + 4);
+        s_off_ptr[ps] = (int)(r0 - lo);
+        if (hi <= nptr) {
+            mbar_arrive_expect_tx(&bp[ps], (uint32_t)((hi - lo) * 8));
+            bulk_g2s(dst, a.indptr + lo, (uint32_t)((hi - lo) * 8), &bp[ps]);
+        } else {   // the array's last entries: plain loads (this thread), then arrive
+            for (int64_t i = lo; i < r0 + nr + 1; ++i) dst[i - lo] = a.indptr[i];
+            asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bp[ps])) : "memory");
+        }
+    };
+    // thread 0: index / perm / value slices and the band of tile t (its ptr stage ps ready) into
+    // metadata stage ms
+    auto issue_meta = [&](int64_t t, int ps, int ms) {
+        int64_t r0;
+        int nr;
+        rows_of(t, r0, nr);
+        const int64_t *P = ptr_buf + ps * (kPRT + 4) + s_off_ptr[ps];
+        const int64_t e0 = P[0], e1 = P[nr];
+        const int64_t ilo = e0 & ~int64_t(3), ihi = (e1 + 3) & ~int64_t(3);
+        const int64_t plo = e0 & ~int64_t(1), phi = (e1 + 1) & ~int64_t(1);
+        constexpr int VE = 16 / (int)sizeof(T);
+        const int64_t vlo = e0 & ~int64_t(VE - 1), vhi = (e1 + VE - 1) & ~int64_t(VE - 1);
+        bool direct = e1 - e0 > kPCAP || ihi > nnz_all || (PERM && phi > nnz_all) || (PL::VAL && vhi > nnz_all);
+        uint32_t bytes = 0;
+        int64_t b0 = 0, b1 = 0;
+        if (BAND) {
+            const double sc = (double)a.xrows / (double)a.nrows;
+            b0 = (int64_t)((double)r0 * sc) - kBandH;
+            b0 = b0 < 0 ? 0 : b0;
+            b1 = (int64_t)((double)(r0 + nr) * sc) + kBandH + 1;
+            b1 = b1 > a.xrows ? a.xrows : b1;
+            b1 = b1 > b0 + kBand ? b0 + kBand : b1;
+            b1 = b1 < b0 ? b0 : b1;
+            bytes += (uint32_t)((b1 - b0) * RB);
+        }
+        s_b0[ms] = b0;
+        s_b1[ms] = b1;
+        if (WST) bytes += (uint32_t)(nr * RB);
+        if (!direct && e1 > e0) {
+            bytes += (uint32_t)((ihi - ilo) * 4);
+            if (PERM) bytes += (uint32_t)((phi - plo) * 8);
+            if (PL::VAL) bytes += (uint32_t)((vhi - vlo) * sizeof(T));
+        }
+        s_direct[ms] = direct;
+        s_off_idx[ms] = (int)(e0 - ilo);
+        s_off_perm[ms] = (int)(e0 - plo);
+        s_off_val[ms] = (int)(e0 - vlo);
+        if (bytes == 0) {
+            asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bm[ms])) : "memory");
+            return;
+        }
+        mbar_arrive_expect_tx(&bm[ms], bytes);
+        if (BAND && b1 > b0) bulk_g2s(band_buf + (size_t)ms * kBand * RB, a.X + b0 * a.ldx, (uint32_t)((b1 - b0) * RB), &bm[ms]);
+        if (WST && nr > 0) bulk_g2s(w_buf + (size_t)ms * kPRT * RB, a.W + r0 * a.ldw, (uint32_t)(nr * RB), &bm[ms]);
+        if (!direct && e1 > e0) {
+            bulk_g2s(idx_buf + ms * (kPCAP + 8), a.indices + ilo, (uint32_t)((ihi - ilo) * 4), &bm[ms]);
+            if (PERM) bulk_g2s(perm_buf + ms * (kPCAP + 4), a.perm + plo, (uint32_t)((phi - plo) * 8), &bm[ms]);
+            if (PL::VAL)
+                bulk_g2s(val_buf + ms * (kPCAP + 32 / sizeof(T)), a.vals + vlo, (uint32_t)((vhi - vlo) * sizeof(T)),
+                         &bm[ms]);
+        }
+    };
+    // prologue: indptr of the first two tiles, then the metadata of the first
+    if (tid == 0) {
+        if (tile_of(0) < ntiles) issue_ptr(tile_of(0), 0);
+        if (tile_of(1) < ntiles) issue_ptr(tile_of(1), 1);
+        if (tile_of(0) < ntiles) {
+            mbar_wait(&bp[0], 0);
+            issue_meta(tile_of(0), 0, 0);
+        }
+    }
+    const int g = tid / G, l = tid % G;
+    const int lo_e = l * E;
+    const int h = g & 1;
+    for (int64_t k = 0; tile_of(k) < ntiles; ++k) {
+        const int ps = (int)(k % 3), ms = (int)(k & 1);
+        if (tid == 0) {
+            if (tile_of(k + 2) < ntiles) issue_ptr(tile_of(k + 2), (int)((k + 2) % 3));
+            if (tile_of(k + 1) < ntiles) {
+                mbar_wait(&bp[(k + 1) % 3], (uint32_t)(((k + 1) / 3) & 1));
+                issue_meta(tile_of(k + 1), (int)((k + 1) % 3), (int)((k + 1) & 1));
+            }
+        }
+        mbar_wait(&bp[ps], (uint32_t)((k / 3) & 1));
+        mbar_wait(&bm[ms], (uint32_t)((k >> 1) & 1));
+        const int64_t t = tile_of(k);
+        int64_t r0;
+        int nr;
+        rows_of(t, r0, nr);
+        const int64_t *s_ptr = ptr_buf + ps * (kPRT + 4) + s_off_ptr[ps];
+        const int32_t *s_idx = idx_buf + ms * (kPCAP + 8) + s_off_idx[ms];
+        const int64_t *s_perm = perm_buf + ms * (kPCAP + 4) + s_off_perm[ms];
+        const T *s_val = val_buf + ms * (kPCAP + 32 / sizeof(T)) + s_off_val[ms];
+        const unsigned char *s_band = band_buf + (size_t)ms * kBand * RB;
+        const bool staged = !s_direct[ms];
+        const int64_t b0 = s_b0[ms], b1 = s_b1[ms];
+        const int64_t base = s_ptr[0];
+        auto where = [&](int64_t c) -> int64_t {
+            if (BAND && c >= b0 && c < b1) return -1 - (c - b0) * RB;
+            return c * a.ldx;
+        };
+        auto meta = [&](int64_t e) -> WideNz {
+            WideNz z;
+            const int64_t c = staged ? (int64_t)(uint32_t)s_idx[e] : (int64_t)(uint32_t)a.indices[base + e];
+            z.off = where(c);
+            if (!ACC) z.val = 0.0;
+            else if (PERM) z.val = (double)a.vals[staged ? s_perm[e] : a.perm[base + e]];
+            else z.val = (double)(staged ? s_val[e] : a.vals[base + e]);
+            return z;
+        };
+        const int rb = g * RPG < nr ? g * RPG : nr;
+        const int re = rb + RPG < nr ? rb + RPG : nr;
+        const int64_t sb = s_ptr[rb] - base, se = s_ptr[re] - base;
+        const int nbw = (int)__reduce_max_sync(0xffffffffu, (unsigned)((se - sb + G - 1) / G));
+        double acc[NE], xr[NE];
+        int cur = rb;
+        int64_t cend = rb < re ? s_ptr[rb + 1] - base : 0;
+        auto begin = [&]() {
+            if (ACC) {
+#pragma unroll
+                for (int i = 0; i < NE; ++i) acc[i] = 0.0;
+            }
+            if (DOT) {
+                if (WST) {
+                    const T *w = reinterpret_cast<const T *>(w_buf + ((size_t)ms * kPRT + cur) * RB) + lo_e;
+#pragma unroll
+                    for (int v = 0; v < NVL; ++v) lds32(w + v * G * E, xr + v * E, h);
+                } else {
+                    const T *w = a.W + (r0 + cur) * a.ldw + lo_e;
+#pragma unroll
+                    for (int v = 0; v < NVL; ++v) ldv32(w + v * G * E, xr + v * E);
+                }
+            }
+        };
+        auto finish = [&]() {
+            if (ACC) {
+                T *y = a.Y + (r0 + cur) * a.ldy + lo_e;
+#pragma unroll
+                for (int v = 0; v < NVL; ++v) stv32(y + v * G * E, acc + v * E);
+            }
+        };
+        if (rb < re) begin();
+        for (int tb = 0; tb < nbw; ++tb) {
+            const int64_t e0 = sb + (int64_t)G * tb;
+            WideNz z[G];
+            double gv[G][NE];
+#pragma unroll
+            for (int b = 0; b < G; ++b) {
+                if (e0 + b < se) {
+                    z[b] = meta(e0 + b);
+                    if (!BAND || z[b].off >= 0) {
+                        const T *xp = a.X + z[b].off + lo_e;
+#pragma unroll
+                        for (int v = 0; v < NVL; ++v) {
+                            if (L1G) ldv32_l1(xp + v * G * E, gv[b] + v * E);
+                            else ldv32(xp + v * G * E, gv[b] + v * E);
+                        }
+                    } else {
+                        const T *xp = reinterpret_cast<const T *>(s_band + (-1 - z[b].off)) + lo_e;
+#pragma unroll
+                        for (int v = 0; v < NVL; ++v) lds32(xp + v * G * E, gv[b] + v * E, h);
+                    }
+                } else {
+                    z[b].val = 0.0;
+#pragma unroll
+                    for (int i = 0; i < NE; ++i) gv[b][i] = 0.0;
+                }
+            }
+            double d[G];
+#pragma unroll
+            for (int b = 0; b < G; ++b) {
+                if (e0 + b < se) {
+                    while (e0 + b >= cend) {
+                        finish();
+                        ++cur;
+                        cend = s_ptr[cur + 1] - base;
+                        begin();
+                    }
+                }
+                if (ACC) {
+#pragma unroll
+                    for (int i = 0; i < NE; ++i) acc[i] = fma(z[b].val, gv[b][i], acc[i]);
+                }
+                if (DOT) {
+                    double sdot = 0.0;
+#pragma unroll
+                    for (int i = 0; i < NE; ++i) sdot = fma(gv[b][i], xr[i], sdot);
+                    d[b] = sdot;
+                }
+            }
+            if (DOT) {
+                const double dd = transpose_reduce<G>(d, l);
+                const int64_t e = e0 + l;
+                if (e < se)
+                    a.D[MODE == SP_FUSED_T ? (staged ? s_perm[e] : a.perm[base + e]) : base + e] = (T)dd;
+            }
+        }
+        if (rb < re) {
+            finish();
+            while (++cur < re) {
+                if (ACC) {
+#pragma unroll
+                    for (int i = 0; i < NE; ++i) acc[i] = 0.0;
+                }
+                finish();
+            }
+        }
+        __syncthreads();   // the stages of tile k are free for tiles k + 2 (metadata) / k + 3 (indptr)
+    }
+}
+
+template <typename T, int NV, int MODE>
+static int launch_pipe(const SpmmArgs<T> &a, bool band, cudaStream_t s)
+{
+    const int64_t ntiles = cdiv(a.nrows, kPRT);
+    auto go = [&](auto kern, size_t smem) -> int {
+        int per = 0;
+        CSRK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CSRK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kPTPB, smem));
+        per = per < 1 ? 1 : per;
+        const int64_t grid = ntiles < (int64_t)kNumSMs * per ? ntiles : (int64_t)kNumSMs * per;
+        CSRK_LAUNCH(kern, (unsigned)grid, kPTPB, smem, s, a, ntiles);
+        return CSRK_OK;
+    };
+    // lanes per row: 8 (one 32-byte vector each, batches of 8 gathers) for 256-byte rows when asked;
+    // WST: the W rows of a dot mode by TMA with the tile's metadata (needs contiguous W rows)
+    const int g8 = NV == 2 ? knob(MODE == SP_FUSED_T || MODE == SP_SDDMM ? "SPMM_G8_DOT" : "SPMM_G8_FWD", 0) : 0;
+    const bool wst = (MODE == SP_FUSED_T || MODE == SP_SDDMM) && knob("SPMM_PIPE_W", 0) && a.ldw == a.k &&
+                     !(reinterpret_cast<uintptr_t>(a.W) & 15);
+    using PLn = PipeLayout<T, NV, MODE, false>;
+    using PLb = PipeLayout<T, NV, MODE, true>;
+    if constexpr (NV == 2) {
+        if (g8) {
+            if (band) return go(k_spmm_pipe<T, NV, MODE, true, 8, false>, PLb::total_nw);
+            return go(k_spmm_pipe<T, NV, MODE, false, 8, false>, PLn::total_nw);
+        }
+    }
+    if (wst) {
+        if (band) return go(k_spmm_pipe<T, NV, MODE, true, 4, true>, PLb::total_w);
+        return go(k_spmm_pipe<T, NV, MODE, false, 4, true>, PLn::total_w);
+    }
+    if (band) return go(k_spmm_pipe<T, NV, MODE, true, 4, false>, PLb::total_nw);
+    if (knob(MODE == SP_FUSED_T || MODE == SP_SDDMM ? "SPMM_L1_DOT" : "SPMM_L1_FWD", 0))
+        return go(k_spmm_pipe<T, NV, MODE, false, 4, false, true>, PLn::total_nw);
+    return go(k_spmm_pipe<T, NV, MODE, false, 4, false>, PLn::total_nw);
+}
+
 template <typename T, int MODE>
 static bool launch_wide(const SpmmArgs<T> &a, cudaStream_t s, int &st)
 {
@@ -638,6 +967,20 @@ static bool launch_wide(const SpmmArgs<T> &a, cudaStream_t s, int &st)
     const unsigned grid = (unsigned)cdiv(a.nrows, kWTPB / kWG * kWRPG);
     // band staging needs contiguous dense rows (one bulk copy)
     const bool band = knob("SPMM_BAND", 1) && (MODE == SP_FWD || MODE == SP_FWD_PERM) && a.ldx == a.k && a.xrows > 0;
+    // persistent pipelined path (bulk copies of 16-byte aligned slices: every operand 16-byte
+    // aligned, indptr / indices / perm / values as allocated by the caller)
+    if (knob("SPMM_PIPE", 1) && a.nrows >= (int64_t)kNumSMs * kPRT) {
+        // (the band costs the pipelined kernel occupancy: fwd 1.16 vs 0.47 ms, bwd 2.08 vs 0.84 ms on config 2)
+        const int pband = knob("SPMM_PIPE_BAND", 0) && a.ldx == a.k && a.xrows > 0;
+        const bool al16 = !(reinterpret_cast<uintptr_t>(a.indptr) & 15) && !(reinterpret_cast<uintptr_t>(a.indices) & 15) &&
+                          (!a.perm || !(reinterpret_cast<uintptr_t>(a.perm) & 15)) &&
+                          (!a.vals || !(reinterpret_cast<uintptr_t>(a.vals) & 15));
+        if (al16) {
+            if (nv == 1) st = launch_pipe<T, 1, MODE>(a, pband, s);
+            else st = launch_pipe<T, sizeof(T) == 8 ? 2 : 1, MODE>(a, pband, s);
+            return true;
+        }
+    }
     auto go = [&](auto kern, bool bnd) -> int {
         const size_t smem = bnd ? (size_t)band_cap<MODE>() * rb : 0;
         if (bnd) CSRK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -26,6 +26,23 @@ __device__ __forceinline__ void ldv32(const float *p, double *r)
     for (int i = 0; i < 8; ++i) r[i] = (double)f[i];
 }
 
+// The same 32 bytes as two 16-byte loads (LDG.128): these allocate in L1, so rows gathered again by
+// nearby rows of the same CTA hit L1 (the 256-bit form does not).
+__device__ __forceinline__ void ldv32_l1(const double *p, double *r)
+{
+    asm("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(r[0]), "=d"(r[1]) : "l"(p));
+    asm("ld.global.nc.v2.f64 {%0,%1}, [%2+16];" : "=d"(r[2]), "=d"(r[3]) : "l"(p));
+}
+
+__device__ __forceinline__ void ldv32_l1(const float *p, double *r)
+{
+    float f[8];
+    asm("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(f[0]), "=f"(f[1]), "=f"(f[2]), "=f"(f[3]) : "l"(p));
+    asm("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4+16];" : "=f"(f[4]), "=f"(f[5]), "=f"(f[6]), "=f"(f[7]) : "l"(p));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r[i] = (double)f[i];
+}
+
 __device__ __forceinline__ void stv32(double *p, const double *r)
 {
     asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(r[0]), "d"(r[1]), "d"(r[2]), "d"(r[3])
@@ -73,6 +90,33 @@ __device__ __forceinline__ double transpose_reduce4(const double (&d)[4], int l)
     double k = odd ? k1 : k0;
     k += __shfl_xor_sync(0xffffffffu, s, 1);
     return k;
+}
+
+// G consecutive lanes (G = 4 or 8) each hold partial sums d[0..G) of G dot products; after log2 G
+// butterfly steps lane l (of the group) holds the full sum of product l (G - 1 shuffles for G dots;
+// fixed summation order, deterministic).
+template <int G>
+__device__ __forceinline__ double transpose_reduce(const double (&d)[G], int l)
+{
+    if constexpr (G == 4) {
+        return transpose_reduce4(d, l);
+    } else {
+        static_assert(G == 8, "G = 4 or 8");
+        double k[4], k2[2];
+        const bool b4 = l & 4, b2 = l & 2, b1 = l & 1;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const double keep = b4 ? d[4 + i] : d[i], send = b4 ? d[i] : d[4 + i];
+            k[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const double keep = b2 ? k[2 + i] : k[i], send = b2 ? k[i] : k[2 + i];
+            k2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+        }
+        const double keep = b1 ? k2[1] : k2[0], send = b1 ? k2[0] : k2[1];
+        return keep + __shfl_xor_sync(0xffffffffu, send, 1);
+    }
 }
 
 }  // namespace csrk

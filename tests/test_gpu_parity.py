@@ -190,6 +190,35 @@ def test_spmm_fwd_bwd(ck, orc, case, dt, k):
     close(dX, dX_ref.value, dX_ref.S, dt, "dX only", exact)
 
 
+@pytest.mark.parametrize("case", ["poisson2d_150", "powerlaw_32k", "rand_rect_40k"])
+@pytest.mark.parametrize("dt,k", [(np.float64, 32), (np.float32, 32), (np.float64, 16)])
+@pytest.mark.parametrize("values", ["real", "int"])
+def test_spmm_pipelined_path(ck, orc, case, dt, k, values):
+    """Matrices of >= 148 x 128 rows take the persistent TMA-pipelined wide kernel (k_spmm_pipe):
+    every mode (fwd, fused dA + dX, dA only, dX only) against the oracle, ragged last tile."""
+    A = {"poisson2d_150": lambda: synth.poisson2d(150, dtype=dt),
+         "powerlaw_32k": lambda: synth.powerlaw(1 << 15, seed=43, dtype=dt, values=values),
+         "rand_rect_40k": lambda: synth.random_csr(40001, 30011, 0.0002, 12, dt, values, empty_rows=True)}[case]()
+    if values == "int" and case.startswith("poisson"):
+        A = A.with_values(synth.int_values(np.random.default_rng(9), A.nnz, dt))
+    exact = values == "int"
+    m, n = A.nrows, A.ncols
+    X = synth.dense((n, k), 3, dt, values)
+    dY = synth.dense((m, k), 4, dt, values)
+    Ad = dev(ck, A)
+    r = orc.spmm_fwd(A, X)
+    close(ck.spmm_fwd(Ad, t(X)), r.value, r.S, dt, "Y", exact)
+    dA_ref, dX_ref = orc.spmm_bwd(A, X, dY)
+    plan = ck.csr_transpose(Ad)
+    dA, dX = ck.spmm_bwd(Ad, t(X), t(dY), plan=plan)
+    close(dA, dA_ref.value, dA_ref.S, dt, "dA", exact)
+    close(dX, dX_ref.value, dX_ref.S, dt, "dX", exact)
+    dA, _ = ck.spmm_bwd(Ad, t(X), t(dY), need_dX=False)
+    close(dA, dA_ref.value, dA_ref.S, dt, "dA only (SDDMM)", exact)
+    _, dX = ck.spmm_bwd(Ad, t(X), t(dY), plan=plan, need_dA=False)
+    close(dX, dX_ref.value, dX_ref.S, dt, "dX only", exact)
+
+
 def test_spmm_strided_operands(ck, orc):
     """Leading dimensions > k (row-major with padding, reading A10)."""
     A = synth.poisson2d(20)
