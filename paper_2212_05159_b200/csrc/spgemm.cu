@@ -39,7 +39,11 @@ namespace csrk {
 #define CSRK_S_MAXL 8
 #endif
 constexpr int kSMaxL = CSRK_S_MAXL;  // A/B via CSRK_NVCC_EXTRA
-constexpr int64_t kSMaxW = 512;
+#ifndef CSRK_S_MAXW
+#define CSRK_S_MAXW 64  // stencil rows (w <= 49) merge per thread; heavier short rows (power-law, random B rows:
+                        // the per-thread merge becomes a chain of dependent gathers) go to the warp path
+#endif
+constexpr int64_t kSMaxW = CSRK_S_MAXW;
 constexpr int kMMaxW = 8192;
 constexpr int kSTPB = 128;           // k_gemm_S: 4 warps
 constexpr int kSWarps = kSTPB / 32;
@@ -54,7 +58,7 @@ constexpr int kSBuf = 832;           // staged C entries per warp (3D 7-point A^
 constexpr int kSBufA = 32 * kSMaxL;  // staged dA entries per warp
 constexpr int kSCache = 32;          // symbolic: C columns of a short row kept from COUNT for FILL
 constexpr int kGemmTPB = 512;        // k_gemm_big*
-constexpr int kBitmapWords = 24576;  // 96 KB -> windows of 786,432 columns
+constexpr int kBitmapWords = 51200;  // 200 KB -> windows of 1,638,400 columns (config 4: 6 windows)
 constexpr int kWL = 64;              // k_gemm_W: max entries of the A row
 constexpr int kWW = 512;             // k_gemm_W: max products w_i
 constexpr int kWTPB = 128;           // k_gemm_W: 4 warps
@@ -379,6 +383,8 @@ struct WSmemT {
     int64_t bs[WL];                      // start in B of list t
     int32_t key[PH == PH_COUNT ? 1 : WW];// FILL: product columns (sorted); NUM / BWD: C row columns
     int32_t off[WL + 1];                 // flat offset of list t (off[l] = w)
+    int32_t tmp[PH == PH_FILL ? WW : 1]; // FILL: the bucket-sorted columns
+    int32_t cnt[PH == PH_FILL ? WW / 2 : 1];  // FILL: bucket counts / offsets
 };
 // symbolic-only warp class for 512 < w <= kW2W (config-4 rows the CTA path sorted slowly)
 constexpr int kW2W = 1024;
@@ -456,8 +462,88 @@ __device__ __forceinline__ void w_sort_fill(const int32_t *key, int w, int32_t *
     }
 }
 
+// FILL of a warp-path row by a bucket sort (no compare network): the w columns are counted into
+// WW/2 buckets of equal width over [min, max] (shared-memory atomics), the counts scanned, the
+// columns scattered to their buckets, each lane insertion-sorts its WW/64 consecutive buckets, and
+// the distinct columns are written in order.  Linear in w for spread columns (config 4: uniform
+// columns, ~2 per bucket); returns false without writing when a bucket holds more than kBucketMax
+// columns (clustered or repeated columns) -- the caller then runs the bitonic network.
+constexpr int kBucketMax = 16;
+template <int WW>
+__device__ __forceinline__ bool w_bucket_fill(const int32_t *key, int32_t *tmp, int32_t *cnt, int w, int32_t *out,
+                                              int lane)
+{
+    constexpr int NB = WW / 2, PER = NB / 32;
+    const unsigned FULL = 0xffffffffu;
+    __syncwarp();   // the gathered columns of every lane are in key[]
+    int32_t mn = INT32_MAX, mx = 0;
+    for (int e = lane; e < w; e += 32) {
+        const int32_t k = key[e];
+        mn = k < mn ? k : mn;
+        mx = k > mx ? k : mx;
+    }
+    mn = (int32_t)__reduce_min_sync(FULL, (unsigned)mn);
+    mx = (int32_t)__reduce_max_sync(FULL, (unsigned)mx);
+    const uint64_t span = (uint64_t)(mx - mn) + 1;
+    auto bucket = [&](int32_t k) { return (int)(((uint64_t)(k - mn) * NB) / span); };
+    for (int b = lane; b < NB; b += 32) cnt[b] = 0;
+    __syncwarp();
+    for (int e = lane; e < w; e += 32) atomicAdd(&cnt[bucket(key[e])], 1);
+    __syncwarp();
+    int loc[PER], sum = 0, mxc = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        loc[q] = cnt[lane * PER + q];
+        sum += loc[q];
+        mxc = loc[q] > mxc ? loc[q] : mxc;
+    }
+    if (__reduce_max_sync(FULL, (unsigned)mxc) > (unsigned)kBucketMax) return false;
+    int x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
+    }
+    const int s0 = x - sum, s1 = x;   // this lane's region of tmp
+    int run = s0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        cnt[lane * PER + q] = run;
+        run += loc[q];
+    }
+    __syncwarp();
+    for (int e = lane; e < w; e += 32) {
+        const int32_t k = key[e];
+        tmp[atomicAdd(&cnt[bucket(k)], 1)] = k;
+    }
+    __syncwarp();
+    for (int i = s0 + 1; i < s1; ++i) {   // buckets are ordered: an element only moves inside its bucket
+        const int32_t v = tmp[i];
+        int j = i - 1;
+        while (j >= s0 && tmp[j] > v) {
+            tmp[j + 1] = tmp[j];
+            --j;
+        }
+        tmp[j + 1] = v;
+    }
+    __syncwarp();
+    int base = 0;
+    for (int e0 = 0; e0 < w; e0 += 32) {
+        const int e = e0 + lane;
+        const int32_t v = e < w ? tmp[e] : 0;
+        const bool f = e < w && (e == 0 || v != tmp[e - 1]);
+        const unsigned m = __ballot_sync(FULL, f);
+        if (f) out[base + __popc(m & ((1u << lane) - 1))] = v;
+        base += __popc(m);
+    }
+    return true;
+}
+
 #ifndef CSRK_W_MINB
 #define CSRK_W_MINB 1
+#endif
+#ifndef CSRK_W_BUCKET
+#define CSRK_W_BUCKET 1
 #endif
 template <typename T, int PH, bool W2 = false>
 __global__ __launch_bounds__(kWTPB, CSRK_W_MINB) void k_gemm_W(BigList wl, BigList big, BigList w2l, const int64_t *__restrict__ Ap,
@@ -475,6 +561,7 @@ __global__ __launch_bounds__(kWTPB, CSRK_W_MINB) void k_gemm_W(BigList wl, BigLi
     SM &S = reinterpret_cast<SM *>(s_dyn)[warp];
     const unsigned FULL = 0xffffffffu;
     const int nrows = *(volatile int *)wl.count;
+    constexpr bool knob_bucket = CSRK_W_BUCKET != 0;
     for (int it = blockIdx.x * kWWarps + warp; it < nrows; it += gridDim.x * kWWarps) {
         __syncwarp();  // the previous row's shared-memory reads complete before this row's writes
         const int64_t i = wl.rows[it];
@@ -596,7 +683,9 @@ __global__ __launch_bounds__(kWTPB, CSRK_W_MINB) void k_gemm_W(BigList wl, BigLi
             for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
             if (lane == 0) Cp[i + 1] = cnt;
         }
-        if (PH == PH_FILL) {
+        if (PH == PH_FILL && w > 64 && knob_bucket && w_bucket_fill<WW>(S.key, S.tmp, S.cnt, w, Ci + cs, lane)) {
+            // sorted by buckets
+        } else if (PH == PH_FILL) {
             __syncwarp();
             if (!W2) {
                 const int P = w <= 32 ? 32 : w <= 64 ? 64 : w <= 128 ? 128 : w <= 256 ? 256 : 512;
@@ -680,6 +769,85 @@ __device__ __forceinline__ void bitonic_keys(int32_t *key, int P)
 }
 
 
+// CTA-wide FILL of a big row (the CTA analogue of w_bucket_fill): the w gathered columns in key[]
+// are counted into NB = kMMaxW / 2 buckets of equal width over [min, max], scanned, scattered into
+// tmp, every thread insertion-sorts its NB / kGemmTPB consecutive buckets, and writes the distinct
+// columns of its region at their place (a block scan of the per-thread unique counts).  Returns
+// false without writing when a bucket holds more than kBucketMax columns.
+__device__ __forceinline__ int64_t block_max_i64(int64_t v, int64_t *s_red)
+{
+    for (int o = 16; o > 0; o >>= 1) {
+        const int64_t y = __shfl_xor_sync(0xffffffffu, v, o);
+        v = y > v ? y : v;
+    }
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) s_red[w] = v;
+    __syncthreads();
+    int64_t t = s_red[0];
+    for (int i = 1; i < kGemmTPB / 32; ++i) t = s_red[i] > t ? s_red[i] : t;
+    __syncthreads();
+    return t;
+}
+
+__device__ bool cta_bucket_fill(const int32_t *key, int32_t *tmp, int32_t *cnt, int w, int32_t *out, int64_t *s_red)
+{
+    constexpr int NB = kMMaxW / 2, PER = NB / kGemmTPB;
+    int32_t mn = INT32_MAX, mx = 0;
+    for (int e = threadIdx.x; e < w; e += kGemmTPB) {
+        const int32_t k = key[e];
+        mn = k < mn ? k : mn;
+        mx = k > mx ? k : mx;
+    }
+    mn = (int32_t)-block_max_i64(-(int64_t)mn, s_red);
+    mx = (int32_t)block_max_i64(mx, s_red);
+    const uint64_t span = (uint64_t)(mx - mn) + 1;
+    auto bucket = [&](int32_t k) { return (int)(((uint64_t)(k - mn) * NB) / span); };
+    for (int b = threadIdx.x; b < NB; b += kGemmTPB) cnt[b] = 0;
+    __syncthreads();
+    for (int e = threadIdx.x; e < w; e += kGemmTPB) atomicAdd(&cnt[bucket(key[e])], 1);
+    __syncthreads();
+    int loc[PER], sum = 0, mxc = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        loc[q] = cnt[threadIdx.x * PER + q];
+        sum += loc[q];
+        mxc = loc[q] > mxc ? loc[q] : mxc;
+    }
+    if (block_max_i64(mxc, s_red) > kBucketMax) return false;
+    int64_t tot;
+    const int s0 = (int)block_excl_scan_i64(sum, s_red, tot), s1 = s0 + sum;
+    int run = s0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        cnt[threadIdx.x * PER + q] = run;
+        run += loc[q];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < w; e += kGemmTPB) {
+        const int32_t k = key[e];
+        tmp[atomicAdd(&cnt[bucket(k)], 1)] = k;
+    }
+    __syncthreads();
+    for (int i = s0 + 1; i < s1; ++i) {
+        const int32_t v = tmp[i];
+        int j = i - 1;
+        while (j >= s0 && tmp[j] > v) {
+            tmp[j + 1] = tmp[j];
+            --j;
+        }
+        tmp[j + 1] = v;
+    }
+    __syncthreads();
+    int64_t mine = 0;
+    for (int e = s0; e < s1; ++e) mine += (e == 0 || tmp[e] != tmp[e - 1]);
+    int64_t o = block_excl_scan_i64(mine, s_red, tot);
+    for (int e = s0; e < s1; ++e)
+        if (e == 0 || tmp[e] != tmp[e - 1]) out[o++] = tmp[e];
+    __syncthreads();
+    return true;
+}
+
 // ---------------------------------------------------------------- big rows
 // Rows the S and W paths pass on (l_i > kWL or w_i > kWW: power-law heads).  Their products are
 // enumerated flat: k_big_prep stores, at every A position a of a big row, loff[a] = the flat
@@ -762,6 +930,10 @@ __device__ __forceinline__ void big_walk(const int64_t *__restrict__ loff, const
 }
 
 // ---------------------------------------------------------------- big rows: symbolic
+#ifndef CSRK_BIG_HASH
+#define CSRK_BIG_HASH 1   // big-row symbolic: hash-set COUNT + bucket-sort FILL (0: bitonic sort for both)
+#endif
+constexpr bool kBigHash = CSRK_BIG_HASH != 0;
 template <int PH, bool HUGE>
 __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_sym(BigRows br, int64_t ncolsB,
                                                            const int64_t *__restrict__ Ap,
@@ -784,8 +956,34 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_sym(BigRows br, int64_t n
         if (!HUGE) {
             const int64_t per = (w + kGemmTPB - 1) / kGemmTPB;
             const int64_t e_lo = threadIdx.x * per, e_hi = e_lo + per < w ? e_lo + per : w;
+            if (PH == PH_COUNT && kBigHash) {
+                // distinct columns by a shared-memory hash set (no sort needed to count)
+                int32_t *tab = s_key;
+                const int H = pow2ceil_i((int)(2 * w > 64 ? 2 * w : 64));
+                for (int e = threadIdx.x; e < H; e += kGemmTPB) tab[e] = -1;
+                __syncthreads();
+                int64_t mine = 0;
+                big_walk(br.loff, Ai, Bp, as, ae, e_lo, e_hi, [&](int64_t, int64_t, int64_t b) {
+                    const int32_t j = __ldg(Bi + b);
+                    uint32_t h = w_hash(j) & (uint32_t)(H - 1);
+                    while (true) {
+                        const int32_t old = atomicCAS(&tab[h], -1, j);
+                        if (old == -1) { ++mine; break; }
+                        if (old == j) break;
+                        h = (h + 1) & (uint32_t)(H - 1);
+                    }
+                });
+                const int64_t tot = block_sum_i64(mine, s_red);
+                if (threadIdx.x == 0) Cp[i + 1] = tot;
+                __syncthreads();
+                continue;
+            }
             big_walk(br.loff, Ai, Bp, as, ae, e_lo, e_hi, [&](int64_t e, int64_t, int64_t b) { s_key[e] = Bi[b]; });
             const int wn = (int)w;
+            if (PH == PH_FILL && kBigHash) {
+                __syncthreads();
+                if (cta_bucket_fill(s_key, s_key + kMMaxW, s_key + 2 * kMMaxW, wn, Ci + Cp[i], s_red)) continue;
+            }
             const int P = pow2ceil_i(wn > 0 ? wn : 1);
             for (int e = wn + threadIdx.x; e < P; e += kGemmTPB) s_key[e] = INT32_MAX;
             __syncthreads();
@@ -902,7 +1100,12 @@ __global__ __launch_bounds__(kItemsTPB) void k_big_items(BigRows br, const int64
     if (threadIdx.x == 0) br.items[n] = (int32_t)run;
 }
 
-// backward, rows with several windows: zero their entries of the fp64 dA target
+// backward: a big row sums its dA in shared memory when it has one window and at most kDACap A
+// entries; otherwise into the fp64 dA target (zeroed first)
+constexpr int kDACap = 2048;
+__device__ __forceinline__ bool big_dA_global(int64_t nc, int64_t l) { return nc > kValSm || l > kDACap; }
+
+// backward, rows summing dA in the fp64 target: zero their entries first
 __global__ __launch_bounds__(kGemmTPB) void k_big_zero(BigRows br, const int64_t *__restrict__ Ap,
                                                        const int64_t *__restrict__ Cp, double *__restrict__ dA64)
 {
@@ -910,7 +1113,7 @@ __global__ __launch_bounds__(kGemmTPB) void k_big_zero(BigRows br, const int64_t
     const int n = *(volatile const int *)br.count;
     for (int r = blockIdx.x; r < n; r += gridDim.x) {
         const int64_t i = br.rows[r];
-        if (Cp[i + 1] - Cp[i] <= kValSm) continue;
+        if (!big_dA_global(Cp[i + 1] - Cp[i], Ap[i + 1] - Ap[i])) continue;
         for (int64_t e = Ap[i] + threadIdx.x; e < Ap[i + 1]; e += kGemmTPB) dA64[e] = 0.0;
     }
 }
@@ -924,7 +1127,7 @@ __global__ __launch_bounds__(kGemmTPB) void k_big_cvt(BigRows br, const int64_t 
     const int n = *(volatile const int *)br.count;
     for (int r = blockIdx.x; r < n; r += gridDim.x) {
         const int64_t i = br.rows[r];
-        if (Cp[i + 1] - Cp[i] <= kValSm) continue;
+        if (!big_dA_global(Cp[i + 1] - Cp[i], Ap[i + 1] - Ap[i])) continue;
         for (int64_t e = Ap[i] + threadIdx.x; e < Ap[i + 1]; e += kGemmTPB) dA[e] = (float)dA64[e];
     }
 }
@@ -942,7 +1145,8 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_win(BigRows br, const int
     pdl_wait();
     extern __shared__ __align__(16) unsigned char s_dyn[];
     double *s_val = reinterpret_cast<double *>(s_dyn);                  // NUM: accumulators; BWD: dC
-    int32_t *s_col = reinterpret_cast<int32_t *>(s_val + kValSm);       // the window's C columns
+    double *s_dA = s_val + kValSm;                                      // BWD: dA of a one-window row
+    int32_t *s_col = reinterpret_cast<int32_t *>(s_dA + kDACap);        // the window's C columns
     __shared__ int64_t s_qa[kWinQ], s_qlo[kWinQ], s_qhi[kWinQ];
     __shared__ int s_nq;
     const int n = *(volatile const int *)br.count;
@@ -966,7 +1170,51 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_win(BigRows br, const int
             s_val[q] = PH == PH_NUM ? 0.0 : (double)dC[cs + q];
         }
         if (threadIdx.x == 0) s_nq = 0;
+        const int64_t l = ae - as;
+        const bool dA_sm = PH == PH_BWD && dA && !big_dA_global(row_nc, l);
+        if (dA_sm)
+            for (int64_t t = threadIdx.x; t < l; t += kGemmTPB) s_dA[t] = 0.0;
         __syncthreads();
+        if (single) {
+            // one window: the row's w products split into equal contiguous runs (big_walk over the
+            // flat offsets of k_big_prep), whatever the B row lengths
+            const int64_t w = br.w[r];
+            const int64_t per = (w + kGemmTPB - 1) / kGemmTPB;
+            const int64_t p_lo = threadIdx.x * per, p_hi = p_lo + per < w ? p_lo + per : w;
+            int64_t cur_a = -1;
+            double av = 0.0, dacc = 0.0;
+            auto flush = [&]() {
+                if (PH != PH_BWD || !dA || cur_a < 0) return;
+                if (dA_sm) atomicAdd(&s_dA[cur_a - as], dacc);
+                else atomicAdd(&dA64[cur_a], dacc);
+            };
+            big_walk(br.loff, Ai, Bp, as, ae, p_lo, p_hi, [&](int64_t, int64_t a, int64_t b) {
+                if (a != cur_a) {
+                    flush();
+                    cur_a = a;
+                    av = (double)Av[a];
+                    dacc = 0.0;
+                }
+                const int32_t j = __ldg(Bi + b);
+                const double bv = (double)__ldg(Bv + b);
+                const int pos = (int)lbound(s_col, nc, j);
+                if (PH == PH_NUM) {
+                    atomicAdd(&s_val[pos], av * bv);
+                } else {
+                    const double g = s_val[pos];
+                    dacc = fma(g, bv, dacc);
+                    if (dB) atomicAdd(&dB[b], av * g);
+                }
+            });
+            flush();
+            __syncthreads();
+            if (PH == PH_NUM)
+                for (int q = threadIdx.x; q < nc; q += kGemmTPB) Cv[cs + q] = (T)s_val[q];
+            if (dA_sm)
+                for (int64_t t = threadIdx.x; t < l; t += kGemmTPB) dA[as + t] = (T)s_dA[t];
+            __syncthreads();
+            continue;
+        }
         const int32_t c_lo = nc > 0 ? s_col[0] : 0, c_hi = nc > 0 ? s_col[nc - 1] : -1;
         // one product b of A entry a (value av): NUM adds av B_kj into C_ij; BWD returns dC_ij B_kj
         auto prod = [&](double av, int64_t b, double &dacc) {
@@ -983,8 +1231,7 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_win(BigRows br, const int
         };
         auto put_dA = [&](int64_t a, double dacc, bool any) {
             if (PH != PH_BWD || !dA) return;
-            if (single) dA[a] = (T)dacc;
-            else if (any) atomicAdd(&dA64[a], dacc);
+            if (any) atomicAdd(&dA64[a], dacc);
         };
         for (int64_t a = as + threadIdx.x; a < ae; a += kGemmTPB) {
             const int32_t k = Ai[a];
@@ -1032,8 +1279,8 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_win(BigRows br, const int
 static unsigned big_grid() { return (unsigned)(kNumSMs * 2); }
 
 static size_t big_sym_smem() { return sizeof(uint32_t) * kBitmapWords; }
-static size_t big_win_smem() { return (sizeof(double) + sizeof(int32_t)) * kValSm; }
-static size_t big_sort_smem() { return sizeof(int32_t) * kMMaxW; }
+static size_t big_win_smem() { return (sizeof(double) + sizeof(int32_t)) * kValSm + sizeof(double) * kDACap; }
+static size_t big_sort_smem() { return sizeof(int32_t) * (2 * kMMaxW + kMMaxW / 2); }
 static unsigned sort_grid() { return (unsigned)(kNumSMs * 4); }
 static unsigned val_grid() { return (unsigned)(kNumSMs * 4); }
 template <int WW, int PH> static size_t wsm() { return sizeof(WSmemT<WW, kWL, PH>) * kWWarps; }
@@ -1052,6 +1299,10 @@ static int set_smem_attrs()
     const int bs = (int)big_sym_smem();
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_sym<PH_COUNT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bs));
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_sym<PH_FILL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bs));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_sym<PH_COUNT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)big_sort_smem()));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_sym<PH_FILL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)big_sort_smem()));
     const int ww = (int)wsm<kWW, PH_NUM>();
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)wsm<kWW, PH_COUNT>()));
@@ -1281,6 +1532,7 @@ static int spgemm_values_t(int PH, const csrk_pattern &A, const T *Av, const csr
         CSRK_LAUNCH((k_gemm_W<T, PH_NUM>), wgrid((wsm<kWW, PH_NUM>())), kWTPB, (wsm<kWW, PH_NUM>()), s, wl, b,
                     BigList{}, A.indptr, A.indices, Av, B.indptr, B.indices, Bv, Cp,
                     const_cast<int32_t *>(C.indices), Cv, ctn, tn, dn);
+        CSRK_LAUNCH(k_big_prep, big_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, B.indptr);
         CSRK_LAUNCH(k_big_items, 1, kItemsTPB, 0, s, br, (const int64_t *)Cp);
         CSRK_LAUNCH((k_gemm_big_win<T, PH_NUM>), val_grid(), kGemmTPB, big_win_smem(), s, br, A.indptr, A.indices, Av,
                     B.indptr, B.indices, Bv, C.indptr, C.indices, Cv, ctn, tn, dn, dn);
@@ -1292,6 +1544,7 @@ static int spgemm_values_t(int PH, const csrk_pattern &A, const T *Av, const csr
     CSRK_LAUNCH((k_gemm_W<T, PH_BWD>), wgrid((wsm<kWW, PH_BWD>())), kWTPB, (wsm<kWW, PH_BWD>()), s, wl, b,
                 BigList{}, A.indptr, A.indices, Av, B.indptr, B.indices, Bv, Cp, const_cast<int32_t *>(C.indices),
                 tn, dC, dA, dB ? dB64 : dn);
+    CSRK_LAUNCH(k_big_prep, big_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, B.indptr);
     CSRK_LAUNCH(k_big_items, 1, kItemsTPB, 0, s, br, (const int64_t *)Cp);
     if (dA) CSRK_LAUNCH(k_big_zero, big_grid(), kGemmTPB, 0, s, br, A.indptr, C.indptr, dA64);
     CSRK_LAUNCH((k_gemm_big_win<T, PH_BWD>), val_grid(), kGemmTPB, big_win_smem(), s, br, A.indptr, A.indices, Av,
