@@ -252,12 +252,14 @@ def run_ops_workload(args, torch, ck, cfg):
     ops["spgemm_symbolic"] = (lambda: ck.spgemm_symbolic(Ad, Ad), c["spgemm_symbolic"])
     ops["spgemm_numeric"] = (lambda: ck.spgemm_numeric(Ad, Ad, C, out=Cv), c["spgemm_numeric"])
     ops["spgemm_bwd"] = (lambda: ck.spgemm_bwd(Ad, Ad, C, dC, dA=dA_g, dB=dB_g), c["spgemm_bwd"])
+    # deterministic dB (column gather through the transpose plan): reported, not in the total
+    ops["spgemm_bwd_plan"] = (lambda: ck.spgemm_bwd(Ad, Ad, C, dC, dA=dA_g, dB=dB_g, plan=plan), c["spgemm_bwd"])
     wl = ("config3: 3D Poisson 7-point 160^3 (4,096,000 rows, 28,518,400 nnz), fp64, C = A A "
           f"(nnz(C) {nnzC:,}, prod {prod:,}): symbolic + numeric + bwd" if cfg == 3 else
           "config4: power-law n = 2^23, 2^27 nnz, rows 8..32,769, fp32: spmv fwd/bwd, transpose, C = A A "
           f"(nnz(C) {nnzC:,}, prod {prod:,}) symbolic + numeric + bwd")
     return _time_ops(args, torch, ck, ops, f"SpMV/SpGEMM fwd+bwd algorithmic GB/s (config {cfg})",
-                     "f64" if cfg == 3 else "f32", wl, f"cfg{cfg}", exclude=("spmv_bwd_plan",))
+                     "f64" if cfg == 3 else "f32", wl, f"cfg{cfg}", exclude=("spmv_bwd_plan", "spgemm_bwd_plan"))
 
 
 def run_ops_sharded(args, torch, ck, cfg, world, rank, local):

@@ -192,6 +192,20 @@ int csrk_spgemm_bwd(csrk_dtype dtype, csrk_pattern A, const void *A_val,
                     void *dA_val, void *dB_val, void *ws, size_t ws_bytes, csrk_stream_t stream);
 
 /*
+ * csrk_spgemm_bwd with A's transpose plan (AT pattern + AT_perm from csrk_csr_transpose; both
+ * NULL = csrk_spgemm_bwd).  With a plan, dB is computed as the paper's "modified version of the
+ * SpGEMM algorithm that operates on columns of A": each stored (k, j) of B gathers
+ * sum_{i in row k of A^T} A_ik dC_ij in ascending i (fp64, rounded once) -- no atomics, so dB is
+ * bit-identical from run to run (reading A7/A9).  C must be the structural product pattern of
+ * csrk_spgemm_symbolic(A, B) (entries of C_i missing for some j of B_k count as dC_ij = 0).
+ * dA as in csrk_spgemm_bwd.  Workspace: CSRK_WS_SPGEMM_BWD with have_plan = 1 (no dB scratch).
+ */
+int csrk_spgemm_bwd_plan(csrk_dtype dtype, csrk_pattern A, const void *A_val,
+                         const csrk_pattern *AT, const int64_t *AT_perm,
+                         csrk_pattern B, const void *B_val, csrk_pattern C, const void *dC_val,
+                         void *dA_val, void *dB_val, void *ws, size_t ws_bytes, csrk_stream_t stream);
+
+/*
  * Sp + Sp symbolic phase (PAPER 3.1.4):
  *   pattern(C) = pattern(A) U pattern(B) ("mask(C) = mask(A) U mask(B) ... a union over the
  *   rows"), columns ascending, structural (an entry whose values would sum to 0 is

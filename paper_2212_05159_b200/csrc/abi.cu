@@ -154,7 +154,17 @@ int csrk_spgemm_bwd(csrk_dtype dtype, csrk_pattern A, const void *A_val, csrk_pa
                     csrk_pattern C, const void *dC_val, void *dA_val, void *dB_val, void *ws, size_t ws_bytes,
                     csrk_stream_t stream)
 {
+    return csrk_spgemm_bwd_plan(dtype, A, A_val, nullptr, nullptr, B, B_val, C, dC_val, dA_val, dB_val, ws, ws_bytes,
+                                stream);
+}
+
+int csrk_spgemm_bwd_plan(csrk_dtype dtype, csrk_pattern A, const void *A_val, const csrk_pattern *AT,
+                         const int64_t *AT_perm, csrk_pattern B, const void *B_val, csrk_pattern C,
+                         const void *dC_val, void *dA_val, void *dB_val, void *ws, size_t ws_bytes,
+                         csrk_stream_t stream)
+{
     CSRK_TRY(check_dtype(dtype));
+    CSRK_TRY(check_plan(A, AT, AT_perm));
     CSRK_TRY(check_pat(A));
     CSRK_TRY(check_pat(B));
     CSRK_TRY(check_pat(C));
@@ -163,7 +173,8 @@ int csrk_spgemm_bwd(csrk_dtype dtype, csrk_pattern A, const void *A_val, csrk_pa
     if ((C.nnz > 0 && !dC_val) || (A.nnz > 0 && !A_val && dB_val) || (B.nnz > 0 && !B_val && dA_val))
         return CSRK_ERR_INVALID_ARG;
     return with_ws(ws, ws_bytes, [&](Bump &b) {
-        return spgemm_bwd(dtype, A, A_val, B, B_val, C, dC_val, dA_val, dB_val, b, (cudaStream_t)stream);
+        return spgemm_bwd(dtype, A, A_val, AT, AT_perm, B, B_val, C, dC_val, dA_val, dB_val, b,
+                          (cudaStream_t)stream);
     });
 }
 
@@ -397,7 +408,7 @@ int csrk_workspace_size(csrk_ws_op op, csrk_dtype dtype, const csrk_pattern *A, 
         break;
     case CSRK_WS_SPGEMM_BWD:
         if (!B) return CSRK_ERR_INVALID_ARG;
-        st = spgemm_bwd(dtype, Ar, d, *B, d, Ar, d, (void *)d, (void *)d, b, 0);
+        st = spgemm_bwd(dtype, Ar, d, plan, pperm, *B, d, Ar, d, (void *)d, (void *)d, b, 0);
         break;
     case CSRK_WS_SPADD_SYMBOLIC:
         if (!B) return CSRK_ERR_INVALID_ARG;

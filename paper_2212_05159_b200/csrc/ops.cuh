@@ -22,8 +22,10 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *C_ind
 void gemm_fill_cache_invalidate(const void *ws, size_t bytes);
 int spgemm_numeric(csrk_dtype dt, const csrk_pattern &A, const void *A_val, const csrk_pattern &B,
                    const void *B_val, const csrk_pattern &C, void *C_val, Bump &ws, cudaStream_t s);
-int spgemm_bwd(csrk_dtype dt, const csrk_pattern &A, const void *A_val, const csrk_pattern &B, const void *B_val,
-               const csrk_pattern &C, const void *dC, void *dA, void *dB, Bump &ws, cudaStream_t s);
+// AT/perm (A's transpose plan, nullable): dB by the deterministic gather over A's columns
+int spgemm_bwd(csrk_dtype dt, const csrk_pattern &A, const void *A_val, const csrk_pattern *AT, const int64_t *perm,
+               const csrk_pattern &B, const void *B_val, const csrk_pattern &C, const void *dC, void *dA, void *dB,
+               Bump &ws, cudaStream_t s);
 
 int spadd_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *C_indptr, int32_t *C_indices,
                    int64_t *nnzC_host, Bump &ws, cudaStream_t s);

@@ -72,7 +72,7 @@ int spai_loss_grad(const csrk_pattern &A, const double *Av, const csrk_pattern &
         CSRK_TRY(spgemm_numeric(CSRK_F64, M, Mv, A, Av, C, Cv, ws, s));
         CSRK_TRY(spadd_numeric(CSRK_F64, 1.0, -1.0, I, Iv, C, Cv, R, Rv, ws, s));
         CSRK_TRY(spadd_bwd(CSRK_F64, 1.0, -1.0, I, C, R, dR, nullptr, dC, ws, s));
-        return spgemm_bwd(CSRK_F64, M, Mv, A, Av, C, dC, dM, nullptr, ws, s);
+        return spgemm_bwd(CSRK_F64, M, Mv, nullptr, nullptr, A, Av, C, dC, dM, nullptr, ws, s);
     }
     if (n > 0) CSRK_LAUNCH(k_ones, (unsigned)(cdiv(n, kSqTPB) < kSqGrid ? cdiv(n, kSqTPB) : kSqGrid), kSqTPB, 0, s, n, Iv);
     CSRK_TRY(spgemm_numeric(CSRK_F64, M, Mv, A, Av, C, Cv, ws, s));
@@ -80,7 +80,7 @@ int spai_loss_grad(const csrk_pattern &A, const double *Av, const csrk_pattern &
     CSRK_LAUNCH(k_sumsq_scale, kSqGrid, kSqTPB, 0, s, R.nnz, Rv, dR, part);
     CSRK_LAUNCH(k_sum_final, 1, kSqTPB, 0, s, part, kSqGrid, part + kSqGrid);
     CSRK_TRY(spadd_bwd(CSRK_F64, 1.0, -1.0, I, C, R, dR, nullptr, dC, ws, s));
-    if (M.nnz > 0) CSRK_TRY(spgemm_bwd(CSRK_F64, M, Mv, A, Av, C, dC, dM, nullptr, ws, s));
+    if (M.nnz > 0) CSRK_TRY(spgemm_bwd(CSRK_F64, M, Mv, nullptr, nullptr, A, Av, C, dC, dM, nullptr, ws, s));
     CSRK_CUDA(cudaMemcpyAsync(loss_host, part + kSqGrid, sizeof(double), cudaMemcpyDeviceToHost, s));
     CSRK_CUDA(cudaStreamSynchronize(s));
     return CSRK_OK;

@@ -1565,14 +1565,193 @@ int spgemm_numeric(csrk_dtype dt, const csrk_pattern &A, const void *A_val, cons
                                   nullptr, nullptr, nullptr, ws, s);
 }
 
-int spgemm_bwd(csrk_dtype dt, const csrk_pattern &A, const void *A_val, const csrk_pattern &B, const void *B_val,
-               const csrk_pattern &C, const void *dC, void *dA, void *dB, Bump &ws, cudaStream_t s)
+// ---------------------------------------------------------------- deterministic dB (transpose plan)
+// dB_kj = sum_{i : (i,k) in A} A_ik dC_ij, evaluated per stored (k, j) of B as a gather over
+// column k of A -- row k of the caller's A^T plan (pattern + perm) -- i.e. the paper's "modified
+// version of the SpGEMM algorithm that operates on columns of A".  For each i of A^T
+// row k, in ascending order, the columns of B row k are located in C row i (C is the structural
+// product, so C_i contains every column of B_k) and acc_j = fma(A_ik, dC_ij, acc_j) in fp64.
+// Fixed order, no atomics: bit-identical from run to run, whatever the schedule.
+//   k_gemm_dB_rows    one THREAD per row k of B with len(B_k) <= kDbR: the row's columns and
+//                     accumulators in registers; per i one forward (galloping) walk over C_i,
+//                     since B_k's columns come in ascending order.  Longer rows are queued.
+//   k_gemm_dB_long    one WARP per queued row, lanes over B_k's entries, binary search per i.
+constexpr int kDbTPB = 256;
+constexpr int kDbR = 16;
+
+// queued long rows: slot -> row and its first chunk; ctr = (slots << 32) | chunks
+struct DbLong {
+    int32_t *rows;
+    int64_t *chunk0;
+    unsigned long long *ctr;
+};
+
+// first position p in [c, c1) with Ci[p] >= v, searching forward from c (galloping)
+__device__ __forceinline__ int64_t gallop_lb(const int32_t *__restrict__ Ci, int64_t c, int64_t c1, int32_t v)
+{
+    if (c >= c1 || __ldg(Ci + c) >= v) return c;
+    int64_t lo = c, step = 1;   // Ci[lo] < v
+    while (lo + step < c1 && __ldg(Ci + lo + step) < v) {
+        lo += step;
+        step <<= 1;
+    }
+    int64_t hi = lo + step < c1 ? lo + step : c1;   // Ci[hi] >= v or hi == c1
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(Ci + mid) < v) lo = mid; else hi = mid;
+    }
+    return hi;
+}
+
+template <typename T>
+__global__ __launch_bounds__(kDbTPB) void k_gemm_dB_rows(int64_t mB, const int64_t *__restrict__ Bp,
+                                                         const int32_t *__restrict__ Bi,
+                                                         const int64_t *__restrict__ ATp,
+                                                         const int32_t *__restrict__ ATi,
+                                                         const int64_t *__restrict__ perm, const T *__restrict__ Av,
+                                                         const int64_t *__restrict__ Cp,
+                                                         const int32_t *__restrict__ Ci, const T *__restrict__ dC,
+                                                         T *__restrict__ dB, DbLong lng)
+{
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * kDbTPB;
+    for (int64_t k0 = (int64_t)blockIdx.x * kDbTPB + threadIdx.x - lane; k0 < mB; k0 += stride) {
+        const int64_t k = k0 + lane;
+        const bool valid = k < mB;
+        const int64_t b0 = valid ? __ldg(Bp + k) : 0, b1 = valid ? __ldg(Bp + k + 1) : 0;
+        const int lb = (int)(b1 - b0 < kDbR + 1 ? b1 - b0 : kDbR + 1);
+        const bool lng_row = valid && lb > kDbR;
+        if (lng_row) {
+            // one atomic hands out the list slot (high word) and the row's first 32-entry chunk
+            // (low word), so chunk offsets ascend with the slot
+            const unsigned long long nch = (unsigned long long)((b1 - b0 + 31) >> 5);
+            const unsigned long long old = atomicAdd(lng.ctr, (1ull << 32) | nch);
+            const int slot = (int)(old >> 32);
+            lng.rows[slot] = (int32_t)k;
+            lng.chunk0[slot] = (int64_t)(old & 0xffffffffull);
+        }
+        if (!valid || lng_row || lb == 0) continue;
+        int32_t bj[kDbR];
+        double acc[kDbR];
+#pragma unroll
+        for (int p = 0; p < kDbR; ++p) {
+            bj[p] = p < lb ? __ldg(Bi + b0 + p) : 0;
+            acc[p] = 0.0;
+        }
+        const int64_t q1 = __ldg(ATp + k + 1);
+        for (int64_t q = __ldg(ATp + k); q < q1; ++q) {
+            const int32_t i = __ldg(ATi + q);
+            const double a = (double)__ldg(Av + __ldg(perm + q));
+            int64_t c = __ldg(Cp + i);
+            const int64_t c1 = __ldg(Cp + i + 1);
+#pragma unroll
+            for (int p = 0; p < kDbR; ++p) {
+                if (p < lb) {
+                    c = gallop_lb(Ci, c, c1, bj[p]);
+                    if (c < c1 && __ldg(Ci + c) == bj[p]) acc[p] = fma(a, (double)__ldg(dC + c), acc[p]);
+                }
+            }
+        }
+#pragma unroll
+        for (int p = 0; p < kDbR; ++p)
+            if (p < lb) dB[b0 + p] = (T)acc[p];
+    }
+}
+
+template <typename T>
+__global__ __launch_bounds__(kDbTPB) void k_gemm_dB_long(const int64_t *__restrict__ Bp,
+                                                         const int32_t *__restrict__ Bi,
+                                                         const int64_t *__restrict__ ATp,
+                                                         const int32_t *__restrict__ ATi,
+                                                         const int64_t *__restrict__ perm, const T *__restrict__ Av,
+                                                         const int64_t *__restrict__ Cp,
+                                                         const int32_t *__restrict__ Ci, const T *__restrict__ dC,
+                                                         T *__restrict__ dB, DbLong lng)
+{
+    pdl_wait();
+    const unsigned long long ctr = *(volatile const unsigned long long *)lng.ctr;
+    const int n = (int)(ctr >> 32);
+    const int64_t nchunks = (int64_t)(ctr & 0xffffffffull);
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (kDbTPB / 32);
+    // one warp per 32-entry chunk of a long row (many warps per row), lanes over its entries
+    for (int64_t ch = (int64_t)blockIdx.x * (kDbTPB / 32) + (threadIdx.x >> 5); ch < nchunks; ch += warps) {
+        int lo = 0, hi = n - 1;   // the slot holding chunk ch: last slot with chunk0 <= ch
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (lng.chunk0[mid] <= ch) lo = mid; else hi = mid - 1;
+        }
+        const int64_t k = lng.rows[lo];
+        const int64_t pb = __ldg(Bp + k) + (ch - lng.chunk0[lo]) * 32 + lane;
+        if (pb >= __ldg(Bp + k + 1)) continue;
+        const int32_t j = __ldg(Bi + pb);
+        double acc = 0.0;
+        const int64_t q1 = __ldg(ATp + k + 1);
+        for (int64_t q = __ldg(ATp + k); q < q1; ++q) {
+            const int32_t i = __ldg(ATi + q);
+            const double a = (double)__ldg(Av + __ldg(perm + q));
+            const int64_t c0 = __ldg(Cp + i), c1 = __ldg(Cp + i + 1);
+            int64_t l = c0, h = c1;
+            while (l < h) {
+                const int64_t mid = (l + h) >> 1;
+                if (__ldg(Ci + mid) < j) l = mid + 1; else h = mid;
+            }
+            if (l < c1 && __ldg(Ci + l) == j) acc = fma(a, (double)__ldg(dC + l), acc);
+        }
+        dB[pb] = (T)acc;
+    }
+}
+
+template <typename T>
+static int launch_dB_gather(const csrk_pattern &B, const csrk_pattern &AT, const int64_t *perm, const T *Av,
+                            const csrk_pattern &C, const T *dC, T *dB, Bump &ws, cudaStream_t s)
+{
+    DbLong lng{};
+    lng.ctr = ws.take<unsigned long long>(1);
+    lng.rows = ws.take<int32_t>(B.nrows > 0 ? B.nrows : 1);
+    lng.chunk0 = ws.take<int64_t>(B.nrows > 0 ? B.nrows : 1);
+    if (ws.sizing() || B.nnz == 0) return CSRK_OK;
+    if (B.nnz / 32 + B.nrows >= (int64_t)UINT32_MAX) return CSRK_ERR_INDEX_OVERFLOW;
+    CSRK_CUDA(cudaMemsetAsync(lng.ctr, 0, sizeof(unsigned long long), s));
+    const int64_t warps = cdiv(B.nrows, 32);
+    const int64_t cap = (int64_t)kNumSMs * 8 * (kDbTPB / 32);
+    const int64_t grid = cdiv(warps < cap ? warps : cap, kDbTPB / 32);
+    CSRK_LAUNCH(k_gemm_dB_rows<T>, (unsigned)grid, kDbTPB, 0, s, B.nrows, B.indptr, B.indices, AT.indptr, AT.indices,
+                perm, Av, C.indptr, C.indices, dC, dB, lng);
+    CSRK_LAUNCH(k_gemm_dB_long<T>, (unsigned)(kNumSMs * 8), kDbTPB, 0, s, B.indptr, B.indices, AT.indptr,
+                AT.indices, perm, Av, C.indptr, C.indices, dC, dB, lng);
+    return CSRK_OK;
+}
+
+template <typename T>
+static int spgemm_bwd_t(const csrk_pattern &A, const T *Av, const csrk_pattern *AT, const int64_t *perm,
+                        const csrk_pattern &B, const T *Bv, const csrk_pattern &C, const T *dC, T *dA, T *dB,
+                        Bump &ws, cudaStream_t s)
+{
+    if (!AT) return spgemm_values_t<T>(PH_BWD, A, Av, B, Bv, C, nullptr, dC, dA, dB, ws, s);
+    // dA by the row traversal (no dB), then the dB gather; they run in order on one stream and
+    // share the scratch
+    Bump w2 = ws;
+    if (dA || ws.sizing()) CSRK_TRY(spgemm_values_t<T>(PH_BWD, A, Av, B, Bv, C, nullptr, dC, dA, nullptr, w2, s));
+    if (ws.sizing()) {
+        CSRK_TRY(launch_dB_gather<T>(B, *AT, perm, Av, C, dC, dB, ws, s));
+        ws.used = w2.used > ws.used ? w2.used : ws.used;
+        return CSRK_OK;
+    }
+    if (!dB) return CSRK_OK;
+    return launch_dB_gather<T>(B, *AT, perm, Av, C, dC, dB, ws, s);
+}
+
+int spgemm_bwd(csrk_dtype dt, const csrk_pattern &A, const void *A_val, const csrk_pattern *AT, const int64_t *perm,
+               const csrk_pattern &B, const void *B_val, const csrk_pattern &C, const void *dC, void *dA, void *dB,
+               Bump &ws, cudaStream_t s)
 {
     if (dt == CSRK_F64)
-        return spgemm_values_t<double>(PH_BWD, A, (const double *)A_val, B, (const double *)B_val, C, nullptr,
-                                       (const double *)dC, (double *)dA, (double *)dB, ws, s);
-    return spgemm_values_t<float>(PH_BWD, A, (const float *)A_val, B, (const float *)B_val, C, nullptr,
-                                  (const float *)dC, (float *)dA, (float *)dB, ws, s);
+        return spgemm_bwd_t<double>(A, (const double *)A_val, AT, perm, B, (const double *)B_val, C,
+                                    (const double *)dC, (double *)dA, (double *)dB, ws, s);
+    return spgemm_bwd_t<float>(A, (const float *)A_val, AT, perm, B, (const float *)B_val, C, (const float *)dC,
+                               (float *)dA, (float *)dB, ws, s);
 }
 
 }  // namespace csrk

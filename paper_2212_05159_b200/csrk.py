@@ -29,7 +29,8 @@ WS = dict(spmv_fwd=0, spmv_bwd=1, spmm_fwd=2, spmm_bwd=3, csr_transpose=4, spgem
 
 # Every symbol declared in include/csrk.h (checked by tests/test_abi_cpu.py).
 ABI_SYMBOLS = ("csrk_spmv_fwd", "csrk_spmv_bwd", "csrk_spmm_fwd", "csrk_spmm_bwd", "csrk_csr_transpose",
-               "csrk_spgemm_symbolic", "csrk_spgemm_numeric", "csrk_spgemm_bwd", "csrk_workspace_size",
+               "csrk_spgemm_symbolic", "csrk_spgemm_numeric", "csrk_spgemm_bwd", "csrk_spgemm_bwd_plan",
+               "csrk_workspace_size",
                "csrk_status_string", "csrk_launch_count", "csrk_version", "csrk_pcg_loss_grad",
                "csrk_spadd_symbolic", "csrk_spadd_numeric", "csrk_spadd_bwd", "csrk_spai_loss_grad",
                "csrk_sptrsv_fwd", "csrk_sptrsv_bwd", "csrk_gcn_fwd", "csrk_gcn_bwd", "csrk_dense_gemm_nn",
@@ -85,6 +86,7 @@ def lib() -> ctypes.CDLL:
     L.csrk_spgemm_symbolic.argtypes = [Pat, Pat, P, P, ctypes.POINTER(I64), P, SZ, P]
     L.csrk_spgemm_numeric.argtypes = [I, Pat, P, Pat, P, Pat, P, P, SZ, P]
     L.csrk_spgemm_bwd.argtypes = [I, Pat, P, Pat, P, Pat, P, P, P, P, SZ, P]
+    L.csrk_spgemm_bwd_plan.argtypes = [I, Pat, P, PatP, P, Pat, P, Pat, P, P, P, P, SZ, P]
     L.csrk_workspace_size.argtypes = [I, I, PatP, PatP, I64, I, ctypes.POINTER(SZ)]
     D = ctypes.c_double
     L.csrk_pcg_loss_grad.argtypes = [Pat, P, Pat, P, P, I, D, I, ctypes.POINTER(D), ctypes.POINTER(D), P, P, SZ, P]
@@ -298,17 +300,24 @@ def spgemm_numeric(A: CSR, B: CSR, C: CSR, out: torch.Tensor | None = None) -> t
 
 
 def spgemm_bwd(A: CSR, B: CSR, C: CSR, dC: torch.Tensor, need_dA: bool = True, need_dB: bool = True,
-               dA: torch.Tensor | None = None, dB: torch.Tensor | None = None):
-    """VJP of SpGEMM (Table 1): dA = (dC B^T) (.) mask(A), dB = (A^T dC) (.) mask(B)."""
+               dA: torch.Tensor | None = None, dB: torch.Tensor | None = None, plan: TransposePlan | None = None):
+    """VJP of SpGEMM (Table 1): dA = (dC B^T) (.) mask(A), dB = (A^T dC) (.) mask(B).
+    plan = A's transpose plan: dB by the deterministic column gather instead of atomics."""
     dt = _dt(A.values)
     if need_dA and dA is None:
         dA = torch.empty_like(A.values)
     if need_dB and dB is None:
         dB = torch.empty_like(B.values)
-    ws, wsb = _workspace("spgemm_bwd", dt, A, B)
-    _check(lib().csrk_spgemm_bwd(dt, A.pattern(), _ptr(A.values), B.pattern(), _ptr(B.values), C.pattern(),
-                                 _ptr(dC), _ptr(dA if need_dA else None), _ptr(dB if need_dB else None), ws, wsb,
-                                 _stream()), "spgemm_bwd")
+    ws, wsb = _workspace("spgemm_bwd", dt, A, B, have_plan=plan is not None)
+    if plan is None:
+        _check(lib().csrk_spgemm_bwd(dt, A.pattern(), _ptr(A.values), B.pattern(), _ptr(B.values), C.pattern(),
+                                     _ptr(dC), _ptr(dA if need_dA else None), _ptr(dB if need_dB else None), ws,
+                                     wsb, _stream()), "spgemm_bwd")
+    else:
+        pp = plan.args()
+        _check(lib().csrk_spgemm_bwd_plan(dt, A.pattern(), _ptr(A.values), pp[0], pp[1], B.pattern(),
+                                          _ptr(B.values), C.pattern(), _ptr(dC), _ptr(dA if need_dA else None),
+                                          _ptr(dB if need_dB else None), ws, wsb, _stream()), "spgemm_bwd_plan")
     return (dA if need_dA else None), (dB if need_dB else None)
 
 

@@ -277,6 +277,30 @@ def test_spgemm(ck, orc, case, dt, values):
     close(dA2, dA_ref.value, dA_ref.S, dt, "dA only", exact)
     _, dB2 = ck.spgemm_bwd(Ad, Bd, C, t(dC), need_dA=False)
     close(dB2, dB_ref.value, dB_ref.S, dt, "dB only", exact)
+    # deterministic dB: gather over A's columns through A's transpose plan
+    plan = ck.csr_transpose(Ad, with_values=False)
+    dA3, dB3 = ck.spgemm_bwd(Ad, Bd, C, t(dC), plan=plan)
+    close(dA3, dA_ref.value, dA_ref.S, dt, "dA (plan)", exact)
+    close(dB3, dB_ref.value, dB_ref.S, dt, "dB (plan)", exact)
+    _, dB4 = ck.spgemm_bwd(Ad, Bd, C, t(dC), need_dA=False, plan=plan)
+    close(dB4, dB_ref.value, dB_ref.S, dt, "dB only (plan)", exact)
+
+
+@pytest.mark.parametrize("case", ["powerlaw_16k", "skew_big", "poisson3d_17"])
+@pytest.mark.parametrize("dt", DTS)
+def test_spgemm_dB_plan_bitwise_reproducible(ck, orc, case, dt):
+    """The plan dB has no atomics: ten runs give the same bits (reading A7/A9), and they agree
+    with the oracle; the atomic path is only required to agree within the S rule."""
+    A, B = gemm_operands(case, dt, "real")
+    Ad, Bd = dev(ck, A), dev(ck, B)
+    C = ck.spgemm_symbolic(Ad, Bd)
+    dC = synth.dense(C.nnz, 17, dt)
+    plan = ck.csr_transpose(Ad, with_values=False)
+    runs = [ck.spgemm_bwd(Ad, Bd, C, t(dC), need_dA=False, plan=plan)[1].cpu().numpy() for _ in range(10)]
+    for r in runs[1:]:
+        np.testing.assert_array_equal(r, runs[0])
+    _, dB_ref = orc.spgemm_bwd(A, B, C.indptr.cpu().numpy(), C.indices.cpu().numpy(), dC)
+    close(runs[0], dB_ref.value, dB_ref.S, dt, "dB (plan)")
 
 
 def test_spgemm_fig3(ck, orc):

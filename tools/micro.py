@@ -88,6 +88,9 @@ def main():
         res["gemm_bwd"] = timeit(lambda: ck.spgemm_bwd(Ad, Ad, C, dC, dA=dA, dB=dB), args.reps, flush)
         res["gemm_bwd_dA_only"] = timeit(lambda: ck.spgemm_bwd(Ad, Ad, C, dC, dA=dA, need_dB=False), args.reps, flush)
         res["gemm_bwd_dB_only"] = timeit(lambda: ck.spgemm_bwd(Ad, Ad, C, dC, need_dA=False, dB=dB), args.reps, flush)
+        res["gemm_bwd_plan"] = timeit(lambda: ck.spgemm_bwd(Ad, Ad, C, dC, dA=dA, dB=dB, plan=plan), args.reps, flush)
+        res["gemm_bwd_dB_plan"] = timeit(lambda: ck.spgemm_bwd(Ad, Ad, C, dC, need_dA=False, dB=dB, plan=plan),
+                                         args.reps, flush)
     print(json.dumps({kk: round(v, 1) for kk, v in res.items()}))
 
 
