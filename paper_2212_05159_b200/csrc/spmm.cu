@@ -653,9 +653,15 @@ struct PipeLayout {
     static constexpr size_t total_w = wrow + 2 * (size_t)kPRT * RB;
 };
 
+#ifndef CSRK_PIPE_MINB_FWD
+#define CSRK_PIPE_MINB_FWD 4   // measured: config-2 forward 473 -> 445 us (5: spills)
+#endif
+#ifndef CSRK_PIPE_MINB_DOT
+#define CSRK_PIPE_MINB_DOT 4   // 5: 827 -> 1460 us (spills)
+#endif
 template <int MODE, int G> constexpr int pipe_minb()
 {
-    return G == 8 ? 5 : (MODE == SP_FWD || MODE == SP_FWD_PERM ? 3 : 4);
+    return G == 8 ? 5 : (MODE == SP_FWD || MODE == SP_FWD_PERM ? CSRK_PIPE_MINB_FWD : CSRK_PIPE_MINB_DOT);
 }
 
 template <typename T, int NV, int MODE, bool BAND, int G, bool WST, bool L1G = false>
