@@ -116,7 +116,8 @@ __device__ __forceinline__ int merge_path_rows(int d, int nr, int Z, const int64
 // ---------------------------------------------------------------- host utilities (utils.cu)
 // In-place int64 prefix sum: data[0] := 0 is NOT written; data[1..n] := inclusive scan of
 // data[1..n].  Used to turn counts stored at indptr[1..] into a CSR indptr.
-int scan_counts_i64(int64_t *indptr, int64_t n, Bump &ws, cudaStream_t s);
+// run_if (nullable, device): the kernels do nothing unless *run_if != 0.
+int scan_counts_i64(int64_t *indptr, int64_t n, Bump &ws, cudaStream_t s, const int *run_if = nullptr);
 // dst[i] = (float)src[i], i < n (the single rounding of an fp64 accumulation of fp32 data)
 int f64_to_f32(const double *src, float *dst, int64_t n, cudaStream_t s);
 size_t scan_ws_bytes(int64_t n);

@@ -54,12 +54,11 @@ __device__ __forceinline__ void row_elem(const TileArgs<T> &a, int64_t row, int6
 }
 
 template <typename T, int MODE, bool PERM, bool SIDE>
-__global__ __launch_bounds__(kRowsTPB, 8) void k_rows(TileArgs<T> a, RowList L)
+__device__ __forceinline__ void rows_block(const TileArgs<T> &a, const RowList &L, int64_t vb)
 {
-    pdl_wait();
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-    const int64_t row = (int64_t)blockIdx.x * kRowsTPB + threadIdx.x;
+    const int64_t row = vb * kRowsTPB + threadIdx.x;
     const bool valid = row < a.nrows;
     int64_t s = 0, e = 0;
     if (valid) {
@@ -160,6 +159,27 @@ __global__ __launch_bounds__(kRowsTPB, 8) void k_rows(TileArgs<T> a, RowList L)
     }
 }
 
+// One CTA per block of kRowsTPB rows; the transpose scatter (MODE_TRANSPOSE, which runs gated
+// behind the symmetric-pattern transpose) grid-strides over the blocks with a resident-sized grid
+// instead, so that skipping it costs a few CTAs, not one per 256 rows.
+template <int MODE> constexpr bool rows_persistent() { return MODE == MODE_TRANSPOSE; }
+
+template <typename T, int MODE, bool PERM, bool SIDE>
+__global__ __launch_bounds__(kRowsTPB, 8) void k_rows(TileArgs<T> a, RowList L)
+{
+    pdl_wait();
+    if (a.run_if && *(volatile const int *)a.run_if == 0) return;
+    if constexpr (rows_persistent<MODE>()) {
+        const int64_t nvb = cdiv(a.nrows, kRowsTPB);
+        for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+            rows_block<T, MODE, PERM, SIDE>(a, L, vb);
+            __syncwarp();   // the warp's s_rw map is reused by the next block
+        }
+    } else {
+        rows_block<T, MODE, PERM, SIDE>(a, L, blockIdx.x);
+    }
+}
+
 constexpr int kLongTPB = 256;
 
 // One CTA per row longer than kHugeRow (power-law heads).
@@ -167,6 +187,7 @@ template <typename T, int MODE, bool PERM, bool SIDE>
 __global__ __launch_bounds__(kLongTPB) void k_rows_long(TileArgs<T> a, RowList L)
 {
     pdl_wait();
+    if (a.run_if && *(volatile const int *)a.run_if == 0) return;
     __shared__ double s_red[kLongTPB / 32];
     const int n = *(volatile int *)L.count;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -204,7 +225,9 @@ int launch_rows(const TileArgs<T> &a, const RowList &L, cudaStream_t s)
 {
     if (a.nrows <= 0) return CSRK_OK;
     CSRK_CUDA(cudaMemsetAsync(L.count, 0, sizeof(int), s));
-    CSRK_LAUNCH((k_rows<T, MODE, PERM, SIDE>), (unsigned)cdiv(a.nrows, kRowsTPB), kRowsTPB, 0, s, a, L);
+    const int64_t nvb = cdiv(a.nrows, kRowsTPB);
+    const int64_t cap = rows_persistent<MODE>() ? (int64_t)kNumSMs * 8 : nvb;
+    CSRK_LAUNCH((k_rows<T, MODE, PERM, SIDE>), (unsigned)(nvb < cap ? nvb : cap), kRowsTPB, 0, s, a, L);
     CSRK_LAUNCH((k_rows_long<T, MODE, PERM, SIDE>), (unsigned)(kNumSMs * 2), kLongTPB, 0, s, a, L);
     return CSRK_OK;
 }

@@ -13,6 +13,15 @@
 //   5. AT_val[q] = A_val[perm[q]] (optional)
 // Matrices with scattered columns use the stable radix sort of radix.cu instead (use_radix).
 // Packing needs nnz < 2^33 (checked).
+//
+// Structurally symmetric patterns (every stored (i, j) has a stored (j, i): Poisson stencils, the
+// paper's PDE operators, undirected graphs) are tried first (k_tr_sym): then A^T has A's pattern,
+// row j of A^T lists the same columns as row j of A, and the A^T slot of A's entry p = (i, j) is
+// the position q of i inside row j -- one binary search per entry, no counting, no sort:
+// AT_indptr = A_indptr, AT_indices = A_indices, AT_perm[q] = p.  A failed search marks the
+// pattern unsymmetric (device flag), and the general kernels above, which are launched behind it
+// and read the flag, then run; on success they return at once.  Exact either way.
+
 #include "ops.cuh"
 #include "rows.cuh"
 #include "tile.cuh"
@@ -29,9 +38,11 @@ __device__ __forceinline__ int32_t key_row(uint64_t k) { return (int32_t)(k & 0x
 __device__ __forceinline__ int64_t key_pos(uint64_t k) { return (int64_t)(k >> 31); }
 
 // Column histogram (plain atomics: warp aggregation with __match_any_sync measured 2x slower).
-__global__ void k_col_count(int64_t nnz, const int32_t *__restrict__ indices, unsigned long long *__restrict__ cnt)
+__global__ void k_col_count(int64_t nnz, const int32_t *__restrict__ indices, unsigned long long *__restrict__ cnt,
+                            const int *run_if)
 {
     pdl_wait();
+    if (run_if && *(volatile const int *)run_if == 0) return;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x)
         atomicAdd(&cnt[indices[p]], 1ULL);
 }
@@ -99,9 +110,11 @@ constexpr int kShortBuf = 512;   // keys staged per warp
 __global__ __launch_bounds__(32 * kShortWarps) void k_sort_short(int64_t n, const int64_t *__restrict__ ATp,
                                                                  const uint64_t *__restrict__ keys,
                                                                  int32_t *__restrict__ ATi,
-                                                                 int64_t *__restrict__ perm, SortLists L)
+                                                                 int64_t *__restrict__ perm, SortLists L,
+                                                                 const int *run_if)
 {
     pdl_wait();
+    if (run_if && *(volatile const int *)run_if == 0) return;
     __shared__ uint64_t s_key[kShortWarps][kShortBuf];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int64_t j0 = ((int64_t)blockIdx.x * kShortWarps + w) * 32; j0 < n;
@@ -286,6 +299,120 @@ __global__ void k_gather_vals(int64_t nnz, const int64_t *__restrict__ perm, con
         AT_val[q] = A_val[perm[q]];
 }
 
+// ---------------------------------------------------------------- structurally symmetric patterns
+constexpr int kSymTPB = 256;
+constexpr int kSymShort = 32;
+#ifndef CSRK_SYM_U
+#define CSRK_SYM_U 4
+#endif
+constexpr int kSymU = CSRK_SYM_U;   // k_tr_sym: entries searched in lock step (A/B via CSRK_NVCC_EXTRA)
+
+// position of v in the sorted c[lo, hi), or -1
+__device__ __forceinline__ int64_t sym_find(const int32_t *__restrict__ c, int64_t lo, int64_t hi, int32_t v)
+{
+    int64_t l = lo, h = hi;
+    while (l < h) {
+        const int64_t mid = (l + h) >> 1;
+        if (__ldg(c + mid) < v) l = mid + 1; else h = mid;
+    }
+    return (l < hi && __ldg(c + l) == v) ? l : -1;
+}
+
+// One thread per row of A (rows longer than kSymShort: the warp, lanes over the entries).  For
+// every entry p = (i, j): q = position of i in row j (binary search; kSymU entries of a row at a
+// time, their searches in flight together); AT_perm[q] = p, AT_indices[p] = j.  `bad` is set
+// when some (j, i) is missing; warps stop early once it is.
+__global__ __launch_bounds__(kSymTPB) void k_tr_sym(int64_t m, const int64_t *__restrict__ Ap,
+                                                    const int32_t *__restrict__ Ai, int64_t *__restrict__ ATp,
+                                                    int32_t *__restrict__ ATi, int64_t *__restrict__ perm, int *bad)
+{
+    pdl_wait();
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * kSymTPB + threadIdx.x;
+    if (__any_sync(FULL, *(volatile int *)bad != 0)) return;
+    const bool valid = i < m;
+    int64_t s = 0, e = 0;
+    if (valid) {
+        s = Ap[i];
+        e = Ap[i + 1];
+        ATp[i] = s;
+        if (i == m - 1) ATp[m] = e;
+    }
+    bool miss = false;
+    const bool lng = e - s > kSymShort;
+    if (!lng)
+        for (int64_t p0 = s; p0 < e; p0 += kSymU) {
+            int64_t lo[kSymU], end[kSymU];
+            int32_t len[kSymU];
+#pragma unroll
+            for (int u = 0; u < kSymU; ++u) {
+                lo[u] = end[u] = 0;
+                len[u] = 0;
+                if (p0 + u < e) {
+                    const int32_t j = Ai[p0 + u];
+                    ATi[p0 + u] = j;
+                    lo[u] = __ldg(Ap + j);
+                    end[u] = __ldg(Ap + j + 1);
+                    len[u] = (int32_t)(end[u] - lo[u]);
+                }
+            }
+            bool any = true;
+            while (any) {   // lower bound of i in row j: len = entries left to the right of lo
+                any = false;
+#pragma unroll
+                for (int u = 0; u < kSymU; ++u) {
+                    if (len[u] > 0) {
+                        const int32_t half = len[u] >> 1;
+                        if (__ldg(Ai + lo[u] + half) < (int32_t)i) {
+                            lo[u] += half + 1;
+                            len[u] -= half + 1;
+                        } else {
+                            len[u] = half;
+                        }
+                        any = true;
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kSymU; ++u) {
+                if (p0 + u >= e) continue;
+                const bool hit = lo[u] < end[u] && __ldg(Ai + lo[u]) == (int32_t)i;
+                if (!hit) miss = true; else perm[lo[u]] = p0 + u;
+            }
+        }
+    unsigned lm = __ballot_sync(FULL, lng);
+    while (lm) {
+        const int src = __ffs(lm) - 1;
+        lm &= lm - 1;
+        const int64_t rs = __shfl_sync(FULL, s, src), re = __shfl_sync(FULL, e, src);
+        const int32_t r = (int32_t)(i - lane + src);
+        for (int64_t p = rs + lane; p < re; p += 32) {
+            const int32_t j = Ai[p];
+            ATi[p] = j;
+            const int64_t q = sym_find(Ai, Ap[j], Ap[j + 1], r);
+            if (q < 0) miss = true; else perm[q] = p;
+        }
+    }
+    if (__any_sync(FULL, miss) && lane == 0) atomicExch(bad, 1);
+}
+
+// x[0..n) = 0 / dst[0..n) = src[0..n), unless *run_if == 0
+__global__ void k_zero_i64_if(int64_t *__restrict__ x, int64_t n, const int *run_if)
+{
+    pdl_wait();
+    if (*(volatile const int *)run_if == 0) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = 0;
+}
+__global__ void k_copy_i64_if(int64_t *__restrict__ dst, const int64_t *__restrict__ src, int64_t n, const int *run_if)
+{
+    pdl_wait();
+    if (*(volatile const int *)run_if == 0) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
 static unsigned grid_for(int64_t work, int tpb)
 {
     int64_t g = cdiv(work, tpb);
@@ -333,26 +460,40 @@ int transpose_impl(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int6
     uint64_t *buf = ws.take<uint64_t>(nnz > kBlockMax ? nnz : 1);
     RowList RL{};
     carve_rowlist(A.nrows, RL, ws);
+    int *sym_bad = ws.take<int>(1);
     if (ws.sizing()) return scan_counts_i64(nullptr, n, ws, s);  // carve the scan scratch
 
-    CSRK_CUDA(cudaMemsetAsync(ATp, 0, sizeof(int64_t) * (size_t)(n + 1), s));
+    // symmetric pattern first (square, not the SPMV_TILE A/B path); the general kernels below
+    // run only if it failed (run_if = sym_bad)
+    const bool try_sym = A.nrows == A.ncols && nnz > 0 && knob("TRANSPOSE_SYM", 1) && !knob("SPMV_TILE", 0);
+    const int *run_if = try_sym ? sym_bad : nullptr;
+    if (try_sym) {
+        CSRK_CUDA(cudaMemsetAsync(sym_bad, 0, sizeof(int), s));
+        CSRK_LAUNCH(k_tr_sym, (unsigned)cdiv(A.nrows, kSymTPB), kSymTPB, 0, s, A.nrows, A.indptr, A.indices, ATp,
+                    ATi, pm, sym_bad);
+        CSRK_LAUNCH(k_zero_i64_if, grid_for(n + 1, 256), 256, 0, s, ATp, n + 1, run_if);
+    } else {
+        CSRK_CUDA(cudaMemsetAsync(ATp, 0, sizeof(int64_t) * (size_t)(n + 1), s));
+    }
     if (nnz > 0)
         CSRK_LAUNCH(k_col_count, grid_for(nnz, 256), 256, 0, s, nnz, A.indices,
-                    reinterpret_cast<unsigned long long *>(ATp + 1));
-    CSRK_TRY(scan_counts_i64(ATp, n, ws, s));
+                    reinterpret_cast<unsigned long long *>(ATp + 1), run_if);
+    CSRK_TRY(scan_counts_i64(ATp, n, ws, s, run_if));
     if (nnz == 0) return CSRK_OK;
-    CSRK_CUDA(cudaMemcpyAsync(cursor, ATp, sizeof(int64_t) * (size_t)n, cudaMemcpyDeviceToDevice, s));
+    if (try_sym) CSRK_LAUNCH(k_copy_i64_if, grid_for(n, 256), 256, 0, s, cursor, (const int64_t *)ATp, n, run_if);
+    else CSRK_CUDA(cudaMemcpyAsync(cursor, ATp, sizeof(int64_t) * (size_t)n, cudaMemcpyDeviceToDevice, s));
     CSRK_CUDA(cudaMemsetAsync(L.count, 0, sizeof(int) * 4, s));
     {
         TileArgs<double> a{};
         a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices;
         a.cursor = cursor; a.out_keys = keys;
         a.R = tile_rows(A.nrows, nnz);
+        a.run_if = run_if;
         if (knob("SPMV_TILE", 0)) CSRK_TRY((launch_tile<double, MODE_TRANSPOSE, false, false>(a, s)));
         else CSRK_TRY((launch_rows<double, MODE_TRANSPOSE, false, false>(a, RL, s)));
     }
     CSRK_LAUNCH(k_sort_short, grid_for(cdiv(n, 32) * 32, 32 * kShortWarps), 32 * kShortWarps, 0, s, n,
-                (const int64_t *)ATp, (const uint64_t *)keys, ATi, pm, L);
+                (const int64_t *)ATp, (const uint64_t *)keys, ATi, pm, L, run_if);
     if (nnz > kRegMax)
         CSRK_LAUNCH(k_sort_warp, (unsigned)(kNumSMs * 4), 32 * kWarpsPerSortCTA, 0, s, (const int64_t *)ATp,
                     (const uint64_t *)keys, ATi, pm, L);

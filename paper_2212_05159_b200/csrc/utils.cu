@@ -58,9 +58,10 @@ __device__ __forceinline__ int64_t block_incl_scan(int64_t v, int64_t *s_warp, i
 }
 
 __global__ __launch_bounds__(kScanTPB) void k_scan_tile_sums(const int64_t *__restrict__ x, int64_t n,
-                                                             int64_t *__restrict__ sums)
+                                                             int64_t *__restrict__ sums, const int *run_if)
 {
     pdl_wait();
+    if (run_if && *(volatile const int *)run_if == 0) return;
     __shared__ int64_t s_warp[kScanTPB / 32];
     const int64_t base = (int64_t)blockIdx.x * kScanTile;
     int64_t v = 0;
@@ -75,9 +76,10 @@ __global__ __launch_bounds__(kScanTPB) void k_scan_tile_sums(const int64_t *__re
 }
 
 __global__ __launch_bounds__(kScanTPB) void k_scan_tiles(int64_t *__restrict__ x, int64_t n,
-                                                         const int64_t *__restrict__ offsets)
+                                                         const int64_t *__restrict__ offsets, const int *run_if)
 {
     pdl_wait();
+    if (run_if && *(volatile const int *)run_if == 0) return;
     __shared__ int64_t s[kScanTile + kScanTile / 16];
     __shared__ int64_t s_warp[kScanTPB / 32];
     const int64_t base = (int64_t)blockIdx.x * kScanTile;
@@ -107,26 +109,26 @@ __global__ __launch_bounds__(kScanTPB) void k_scan_tiles(int64_t *__restrict__ x
     }
 }
 
-static int incl_scan_i64(int64_t *x, int64_t n, Bump &ws, cudaStream_t s)
+static int incl_scan_i64(int64_t *x, int64_t n, Bump &ws, cudaStream_t s, const int *run_if)
 {
     if (n <= 0) return CSRK_OK;
     int64_t nb = cdiv(n, kScanTile);
     if (nb == 1) {
         if (ws.sizing()) return CSRK_OK;
-        CSRK_LAUNCH(k_scan_tiles, 1, kScanTPB, 0, s, x, n, (const int64_t *)nullptr);
+        CSRK_LAUNCH(k_scan_tiles, 1, kScanTPB, 0, s, x, n, (const int64_t *)nullptr, run_if);
         return CSRK_OK;
     }
     int64_t *sums = ws.take<int64_t>(nb);
-    if (!ws.sizing()) CSRK_LAUNCH(k_scan_tile_sums, (unsigned)nb, kScanTPB, 0, s, x, n, sums);
-    CSRK_TRY(incl_scan_i64(sums, nb, ws, s));
-    if (!ws.sizing()) CSRK_LAUNCH(k_scan_tiles, (unsigned)nb, kScanTPB, 0, s, x, n, (const int64_t *)sums);
+    if (!ws.sizing()) CSRK_LAUNCH(k_scan_tile_sums, (unsigned)nb, kScanTPB, 0, s, x, n, sums, run_if);
+    CSRK_TRY(incl_scan_i64(sums, nb, ws, s, run_if));
+    if (!ws.sizing()) CSRK_LAUNCH(k_scan_tiles, (unsigned)nb, kScanTPB, 0, s, x, n, (const int64_t *)sums, run_if);
     return CSRK_OK;
 }
 
-int scan_counts_i64(int64_t *indptr, int64_t n, Bump &ws, cudaStream_t s)
+int scan_counts_i64(int64_t *indptr, int64_t n, Bump &ws, cudaStream_t s, const int *run_if)
 {
     if (ws.overflow) return CSRK_ERR_WORKSPACE;
-    return incl_scan_i64(indptr ? indptr + 1 : nullptr, n, ws, s);
+    return incl_scan_i64(indptr ? indptr + 1 : nullptr, n, ws, s, run_if);
 }
 
 size_t scan_ws_bytes(int64_t n)

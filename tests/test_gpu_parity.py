@@ -160,6 +160,47 @@ def test_csr_transpose(ck, orc, case):
     np.testing.assert_array_equal(back.AT.values.cpu().numpy(), A.values)
 
 
+def _symmetrized(A, drop=None, seed=3):
+    """pattern(A) U pattern(A^T) with seeded values (structurally symmetric, unsymmetric values);
+    drop = index of one stored entry to remove (then the pattern is no longer symmetric)."""
+    import scipy.sparse as sp
+    M = sp.csr_matrix((np.ones(A.nnz), A.indices, A.indptr), shape=(A.nrows, A.ncols))
+    S = (M + M.T).tocsr()
+    S.sort_indices()
+    indptr, indices = S.indptr.astype(np.int64), S.indices.astype(np.int32)
+    if drop is not None:
+        row = int(np.searchsorted(indptr, drop, side="right") - 1)
+        indices = np.delete(indices, drop)
+        indptr = indptr.copy()
+        indptr[row + 1:] -= 1
+    vals = synth.real_values(np.random.default_rng(seed), len(indices))
+    return synth.CSR(A.nrows, A.ncols, indptr, indices, vals)
+
+
+@pytest.mark.parametrize("case", ["sym_powerlaw", "sym_skew", "sym_drop_first", "sym_drop_mid", "sym_drop_last",
+                                  "poisson3d_17"])
+def test_csr_transpose_symmetric_path(ck, orc, case):
+    """Structurally symmetric patterns take the one-search-per-entry path (k_tr_sym: long rows by
+    the warp); patterns one entry short of symmetric must be detected and fall back, bit-exact."""
+    base = synth.powerlaw(1 << 12, seed=5)
+    if case == "sym_powerlaw":
+        A = _symmetrized(base)
+    elif case == "sym_skew":
+        A = _symmetrized(skew(3000, 2500, 4))
+    elif case == "poisson3d_17":
+        A = make(case, np.float64)
+    else:
+        S = _symmetrized(base)
+        A = _symmetrized(base, drop={"sym_drop_first": 0, "sym_drop_mid": S.nnz // 2,
+                                     "sym_drop_last": S.nnz - 1}[case])
+    ATp, ATi, ATv, perm = orc.csr_transpose(A)
+    plan = ck.csr_transpose(dev(ck, A))
+    np.testing.assert_array_equal(plan.AT.indptr.cpu().numpy(), ATp)
+    np.testing.assert_array_equal(plan.AT.indices.cpu().numpy(), ATi)
+    np.testing.assert_array_equal(plan.perm.cpu().numpy(), perm)
+    np.testing.assert_array_equal(plan.AT.values.cpu().numpy(), ATv)
+
+
 # ---------------------------------------------------------------- SpMM
 @pytest.mark.parametrize("case", ["config1_poisson16", "poisson2d_70", "rand_rect_empty_rows", "skew_mid",
                                   "tiny_3x3", "nnz0", "powerlaw_16k"])
