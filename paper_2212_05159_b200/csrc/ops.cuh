@@ -7,8 +7,10 @@ namespace csrk {
 
 int spmv_fwd(csrk_dtype dt, csrk_op op, const csrk_pattern &A, const void *A_val, const csrk_pattern *AT,
              const int64_t *perm, const void *x, void *y, Bump &ws, cudaStream_t s);
+// accumulate_dA (internal, not in the ABI): dA += the masked gradient instead of dA = (PCG's dL)
 int spmv_bwd(csrk_dtype dt, csrk_op op, const csrk_pattern &A, const void *A_val, const csrk_pattern *AT,
-             const int64_t *perm, const void *x, const void *dy, void *dA, void *dx, Bump &ws, cudaStream_t s);
+             const int64_t *perm, const void *x, const void *dy, void *dA, void *dx, Bump &ws, cudaStream_t s,
+             int accumulate_dA = 0);
 int spmm_fwd(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int64_t k, const void *X, int64_t ldx,
              void *Y, int64_t ldy, Bump &ws, cudaStream_t s);
 int spmm_bwd(csrk_dtype dt, const csrk_pattern &A, const void *A_val, const csrk_pattern *AT, const int64_t *perm,

@@ -285,20 +285,19 @@ static int pcg_enqueue(const csrk_comm *comm, int64_t off, const csrk_pattern &A
         double *rb_add = own(w.tmp);           // owned-length contribution to rbar
         if (!precond) {
             // z = L gather(u):  Lbar += zbar u^T (.) mask(L);  ubar = reduce(L^T zbar)
+            // (the masked gradients are added into dL by the SpMV VJP kernels themselves)
             {
                 Bump bw = sub();
-                CSRK_TRY(spmv_bwd(CSRK_F64, CSRK_OP_N, L, Lv, nullptr, nullptr, w.u, w.zbar, w.dAt, w.ubar, bw, s));
+                CSRK_TRY(spmv_bwd(CSRK_F64, CSRK_OP_N, L, Lv, nullptr, nullptr, w.u, w.zbar, dL, w.ubar, bw, s, 1));
             }
-            LIN3(L.nnz, dL, ONE, dL, ONE, w.dAt, ONE, nullptr, nullptr, nullptr);
             CSRK_TRY(reduce(w.ubar));
             CSRK_TRY(gather(w.ubar));
             // u = reduce(L^T r):  Lbar += r ubar^T (.) mask(L);  rbar += L gather(ubar)
             {
                 Bump bw = sub();
-                CSRK_TRY(spmv_bwd(CSRK_F64, CSRK_OP_T, L, Lv, nullptr, nullptr, r, w.ubar, w.dAt,
-                                  want_rbar ? rb_add : nullptr, bw, s));
+                CSRK_TRY(spmv_bwd(CSRK_F64, CSRK_OP_T, L, Lv, nullptr, nullptr, r, w.ubar, dL,
+                                  want_rbar ? rb_add : nullptr, bw, s, 1));
             }
-            LIN3(L.nnz, dL, ONE, dL, ONE, w.dAt, ONE, nullptr, nullptr, nullptr);
         } else {
             // z = L^{-T} u:  ubar = L^{-1} zbar;  Lbar += -z ubar^T (.) mask(L)
             {

@@ -34,6 +34,13 @@ struct RowList {
     int *count;
 };
 
+// D += product, the product rounded first (no contraction): the same bits as forming the product
+// into a scratch array and adding it afterwards
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+
 template <typename T, int MODE, bool PERM, bool SIDE>
 __device__ __forceinline__ void row_elem(const TileArgs<T> &a, int64_t row, int64_t p, double &acc)
 {
@@ -42,10 +49,10 @@ __device__ __forceinline__ void row_elem(const TileArgs<T> &a, int64_t row, int6
         const int64_t pv = PERM ? a.perm[p] : p;
         const T vc = a.v[c];
         acc = fma((double)a.vals[pv], (double)vc, acc);
-        if (SIDE) a.D[pv] = vc * a.u[row];
+        if (SIDE) a.D[pv] = a.accD ? add_rn(a.D[pv], mul_rn(vc, a.u[row])) : (T)(vc * a.u[row]);
     } else if (MODE == MODE_SCATTER) {
         const T w = a.u[row];
-        if (SIDE) a.D[p] = w * a.v[c];
+        if (SIDE) a.D[p] = a.accD ? add_rn(a.D[p], mul_rn(w, a.v[c])) : (T)(w * a.v[c]);
         if (a.y64) atomicAdd(&a.y64[c], (double)a.vals[p] * (double)w);
     } else {
         const int64_t slot = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(&a.cursor[c]), 1ULL);

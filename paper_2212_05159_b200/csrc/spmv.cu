@@ -12,7 +12,7 @@ namespace csrk {
 template <typename T, int MODE, bool PERM, bool SIDE>
 static int run(TileArgs<T> a, const RowList &L, cudaStream_t s)
 {
-    if (knob("SPMV_TILE", 0)) return launch_tile<T, MODE, PERM, SIDE>(a, s);
+    if (knob("SPMV_TILE", 0) && !a.accD) return launch_tile<T, MODE, PERM, SIDE>(a, s);
     return launch_rows<T, MODE, PERM, SIDE>(a, L, s);
 }
 
@@ -65,7 +65,8 @@ static int spmv_fwd_t(csrk_op op, const csrk_pattern &A, const T *A_val, const c
 
 template <typename T>
 static int spmv_bwd_t(csrk_op op, const csrk_pattern &A, const T *A_val, const csrk_pattern *AT,
-                      const int64_t *perm, const T *x, const T *dy, T *dA, T *dx, Bump &ws, cudaStream_t s)
+                      const int64_t *perm, const T *x, const T *dy, T *dA, T *dx, Bump &ws, cudaStream_t s,
+                      int accD)
 {
     RowList L{};
     carve_rowlist(A.nrows > A.ncols ? A.nrows : A.ncols, L, ws);
@@ -73,6 +74,7 @@ static int spmv_bwd_t(csrk_op op, const csrk_pattern &A, const T *A_val, const c
     double *acc = (op == CSRK_OP_N && !(AT && dx) && (dx || ws.sizing())) ? scatter_target(dx, A.ncols, ws) : nullptr;
     if (ws.sizing()) return CSRK_OK;
     TileArgs<T> a{};
+    a.accD = accD;
     if (op == CSRK_OP_T) {
         // y = A^T x:  dx = A dy (row inner products),  dA[p] = x_i dy_{idx p}
         a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices;
@@ -120,13 +122,14 @@ int spmv_fwd(csrk_dtype dt, csrk_op op, const csrk_pattern &A, const void *A_val
 }
 
 int spmv_bwd(csrk_dtype dt, csrk_op op, const csrk_pattern &A, const void *A_val, const csrk_pattern *AT,
-             const int64_t *perm, const void *x, const void *dy, void *dA, void *dx, Bump &ws, cudaStream_t s)
+             const int64_t *perm, const void *x, const void *dy, void *dA, void *dx, Bump &ws, cudaStream_t s,
+             int accumulate_dA)
 {
     if (dt == CSRK_F64)
         return spmv_bwd_t<double>(op, A, (const double *)A_val, AT, perm, (const double *)x, (const double *)dy,
-                                  (double *)dA, (double *)dx, ws, s);
+                                  (double *)dA, (double *)dx, ws, s, accumulate_dA);
     return spmv_bwd_t<float>(op, A, (const float *)A_val, AT, perm, (const float *)x, (const float *)dy,
-                             (float *)dA, (float *)dx, ws, s);
+                             (float *)dA, (float *)dx, ws, s, accumulate_dA);
 }
 
 }  // namespace csrk
