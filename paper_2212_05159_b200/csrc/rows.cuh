@@ -4,8 +4,8 @@
 // thread; the thread's index/value loads are contiguous, and across a warp the L1 serves the
 // neighbouring rows' lines, so short-row matrices (stencils) stream at near copy bandwidth
 // without staging or block synchronisation.  Rows of kShortRow < l <= kHugeRow are then taken
-// by the whole warp one at a time (coalesced over the row); longer rows are appended
-// (warp-aggregated) to a list that k_rows_long processes with one CTA per row.  Per-element
+// by the whole warp one at a time (coalesced over the row); longer rows by the whole CTA once
+// its block is done (no second kernel launch).  Per-element
 // modes (scatter, transpose) stream the warp's element range instead, unless it holds a
 // huge row.
 // Modes (same semantics as tile.cuh):
@@ -61,7 +61,7 @@ __device__ __forceinline__ void row_elem(const TileArgs<T> &a, int64_t row, int6
 }
 
 template <typename T, int MODE, bool PERM, bool SIDE>
-__device__ __forceinline__ void rows_block(const TileArgs<T> &a, const RowList &L, int64_t vb)
+__device__ __forceinline__ void rows_block(const TileArgs<T> &a, int64_t vb, int *s_nh, int32_t *s_h)
 {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
@@ -74,11 +74,11 @@ __device__ __forceinline__ void rows_block(const TileArgs<T> &a, const RowList &
     }
     const bool huge = valid && e - s > kHugeRow;
     const unsigned hm = __ballot_sync(FULL, huge);
-    if (hm) {  // rows longer than kHugeRow: one CTA each in k_rows_long
+    if (hm) {  // rows longer than kHugeRow: taken by the whole CTA afterwards (rows_huge)
         int base = 0;
-        if (lane == 0) base = atomicAdd(L.count, __popc(hm));
+        if (lane == 0) base = atomicAdd(s_nh, __popc(hm));
         base = __shfl_sync(FULL, base, 0);
-        if (huge) L.rows[base + __popc(hm & ((1u << lane) - 1))] = (int32_t)row;
+        if (huge) s_h[base + __popc(hm & ((1u << lane) - 1))] = (int32_t)row;
     }
     const bool lng = valid && e - s > kShortRow && !huge;
     if (MODE != MODE_REDUCE && !hm) {
@@ -166,57 +166,61 @@ __device__ __forceinline__ void rows_block(const TileArgs<T> &a, const RowList &
     }
 }
 
-// One CTA per block of kRowsTPB rows; the transpose scatter (MODE_TRANSPOSE, which runs gated
-// behind the symmetric-pattern transpose) grid-strides over the blocks with a resident-sized grid
-// instead, so that skipping it costs a few CTAs, not one per 256 rows.
-template <int MODE> constexpr bool rows_persistent() { return MODE == MODE_TRANSPOSE; }
-
+// One row longer than kHugeRow, by the whole CTA (lane-strided; REDUCE: fixed warp and block
+// trees -- deterministic)
 template <typename T, int MODE, bool PERM, bool SIDE>
-__global__ __launch_bounds__(kRowsTPB, 8) void k_rows(TileArgs<T> a, RowList L)
+__device__ __forceinline__ void rows_huge(const TileArgs<T> &a, int64_t row, double *s_red)
 {
-    pdl_wait();
-    if (a.run_if && *(volatile const int *)a.run_if == 0) return;
-    if constexpr (rows_persistent<MODE>()) {
-        const int64_t nvb = cdiv(a.nrows, kRowsTPB);
-        for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
-            rows_block<T, MODE, PERM, SIDE>(a, L, vb);
-            __syncwarp();   // the warp's s_rw map is reused by the next block
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t s = a.indptr[row], e = a.indptr[row + 1];
+    double acc = 0.0;
+#pragma unroll 4
+    for (int64_t p = s + threadIdx.x; p < e; p += kRowsTPB) row_elem<T, MODE, PERM, SIDE>(a, row, p, acc);
+    if (MODE == MODE_REDUCE) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) s_red[w] = acc;
+        __syncthreads();
+        if (w == 0) {
+            acc = lane < kRowsTPB / 32 ? s_red[lane] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) a.y[row] = (T)acc;
         }
-    } else {
-        rows_block<T, MODE, PERM, SIDE>(a, L, blockIdx.x);
+        __syncthreads();
     }
 }
 
-constexpr int kLongTPB = 256;
+// One CTA per block of kRowsTPB rows, which then takes the block's rows longer than kHugeRow
+// together (no second kernel); the transpose scatter (MODE_TRANSPOSE, which runs gated behind the
+// symmetric-pattern transpose) grid-strides over the blocks with a resident-sized grid instead,
+// so that skipping it costs a few CTAs, not one per 256 rows.
+template <int MODE> constexpr bool rows_persistent() { return MODE == MODE_TRANSPOSE; }
 
-// One CTA per row longer than kHugeRow (power-law heads).
 template <typename T, int MODE, bool PERM, bool SIDE>
-__global__ __launch_bounds__(kLongTPB) void k_rows_long(TileArgs<T> a, RowList L)
+__global__ __launch_bounds__(kRowsTPB, 8) void k_rows(TileArgs<T> a)
 {
     pdl_wait();
     if (a.run_if && *(volatile const int *)a.run_if == 0) return;
-    __shared__ double s_red[kLongTPB / 32];
-    const int n = *(volatile int *)L.count;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int it = blockIdx.x; it < n; it += gridDim.x) {
-        const int64_t row = L.rows[it];
-        const int64_t s = a.indptr[row], e = a.indptr[row + 1];
-        double acc = 0.0;
-#pragma unroll 4
-        for (int64_t p = s + threadIdx.x; p < e; p += kLongTPB) row_elem<T, MODE, PERM, SIDE>(a, row, p, acc);
-        if (MODE == MODE_REDUCE) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0) s_red[w] = acc;
-            __syncthreads();
-            if (w == 0) {
-                acc = lane < kLongTPB / 32 ? s_red[lane] : 0.0;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                if (lane == 0) a.y[row] = (T)acc;
-            }
-            __syncthreads();
+    __shared__ int s_nh;
+    __shared__ int32_t s_h[kRowsTPB];
+    __shared__ double s_red[kRowsTPB / 32];
+    auto block = [&](int64_t vb) {
+        if (threadIdx.x == 0) s_nh = 0;
+        __syncthreads();
+        rows_block<T, MODE, PERM, SIDE>(a, vb, &s_nh, s_h);
+        __syncthreads();
+        const int nh = s_nh;
+        for (int h = 0; h < nh; ++h) rows_huge<T, MODE, PERM, SIDE>(a, s_h[h], s_red);
+    };
+    if constexpr (rows_persistent<MODE>()) {
+        const int64_t nvb = cdiv(a.nrows, kRowsTPB);
+        for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+            block(vb);
+            __syncthreads();   // s_nh, s_h and the warps' s_rw maps are reused by the next block
         }
+    } else {
+        block(blockIdx.x);
     }
 }
 
@@ -228,14 +232,12 @@ inline void carve_rowlist(int64_t nrows, RowList &L, Bump &ws)
 }
 
 template <typename T, int MODE, bool PERM, bool SIDE>
-int launch_rows(const TileArgs<T> &a, const RowList &L, cudaStream_t s)
+int launch_rows(const TileArgs<T> &a, const RowList &, cudaStream_t s)
 {
     if (a.nrows <= 0) return CSRK_OK;
-    CSRK_CUDA(cudaMemsetAsync(L.count, 0, sizeof(int), s));
     const int64_t nvb = cdiv(a.nrows, kRowsTPB);
     const int64_t cap = rows_persistent<MODE>() ? (int64_t)kNumSMs * 8 : nvb;
-    CSRK_LAUNCH((k_rows<T, MODE, PERM, SIDE>), (unsigned)(nvb < cap ? nvb : cap), kRowsTPB, 0, s, a, L);
-    CSRK_LAUNCH((k_rows_long<T, MODE, PERM, SIDE>), (unsigned)(kNumSMs * 2), kLongTPB, 0, s, a, L);
+    CSRK_LAUNCH((k_rows<T, MODE, PERM, SIDE>), (unsigned)(nvb < cap ? nvb : cap), kRowsTPB, 0, s, a);
     return CSRK_OK;
 }
 

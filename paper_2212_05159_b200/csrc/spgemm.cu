@@ -1389,6 +1389,7 @@ struct CountStamp {
     const int64_t *Ap, *Bp;
     const int32_t *Ai, *Bi;
     int64_t m, nnzA, nnzB;
+    int ncls[3];   // rows COUNT queued to the W / big / W2 paths (not part of the identity)
     bool operator==(const CountStamp &o) const
     {
         return ws == o.ws && Ap == o.Ap && Bp == o.Bp && Ai == o.Ai && Bi == o.Bi && m == o.m && nnzA == o.nnzA &&
@@ -1419,7 +1420,7 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, i
     const size_t mr = (size_t)(A.nrows > 0 ? A.nrows : 1);
     int32_t *cache = use_fill_cache() ? ws.take<int32_t>(mr * kSCache + (mr + 3) / 4) : nullptr;
     if (ws.sizing()) return scan_counts_i64(nullptr, A.nrows, ws, s);
-    const CountStamp stamp{ws.base, A.indptr, B.indptr, A.indices, B.indices, A.nrows, A.nnz, B.nnz};
+    CountStamp stamp{ws.base, A.indptr, B.indptr, A.indices, B.indices, A.nrows, A.nnz, B.nnz, {1, 1, 1}};
     const int64_t m = A.nrows;
     CSRK_TRY(set_smem_attrs());
     const unsigned gS = (unsigned)cdiv(m, kSTPB);
@@ -1448,40 +1449,55 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, i
             CSRK_LAUNCH((k_gemm_big_sym<PH_COUNT, true>), big_grid(), kGemmTPB, big_sym_smem(), s, br, B.ncols,
                         A.indptr, A.indices, B.indptr, Bi, Cp, (int32_t *)nullptr);
             CSRK_TRY(scan_counts_i64(Cp, m, ws, s));
-            if (cache) {
-                std::lock_guard<std::mutex> g(g_stamp_mu);
-                g_stamps.push_back(stamp);
-            }
         }
         CSRK_CUDA(cudaMemcpyAsync(nnzC_host, Cp + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        int cls[4] = {1, 1, 1, 1};
+        if (m > 0) CSRK_CUDA(cudaMemcpyAsync(cls, wl.count, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
         CSRK_CUDA(cudaStreamSynchronize(s));
+        if (m > 0) {
+            // the class sizes travel with the stamp: FILL on the same arguments skips the launches
+            // of the empty classes (the row classes depend on A's and B's patterns only)
+            stamp.ncls[0] = cls[0];
+            stamp.ncls[1] = cls[1];
+            stamp.ncls[2] = cls[2];
+            std::lock_guard<std::mutex> g(g_stamp_mu);
+            g_stamps.push_back(stamp);
+        }
         return CSRK_OK;
     }
     if (m == 0) return CSRK_OK;
-    bool cached = false;
-    if (cache) {
+    bool found = false;
+    {
         std::lock_guard<std::mutex> g(g_stamp_mu);
         for (size_t q = 0; q < g_stamps.size(); ++q)
             if (g_stamps[q] == stamp) {
-                cached = true;
+                found = true;
+                for (int c = 0; c < 3; ++c) stamp.ncls[c] = g_stamps[q].ncls[c];
                 g_stamps.erase(g_stamps.begin() + (long)q);  // one FILL per COUNT
                 break;
             }
     }
+    const bool cached = found && cache;
+    // without the COUNT of these arguments every class is launched (ncls stays {1, 1, 1})
     CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 4 * sizeof(int), s));
     CSRK_TRY((launch_S<double, PH_FILL>)(B.nnz < INT32_MAX, gS, s_smem<double>(PH_FILL, stage_fill()), s, m, A.indptr,
                 A.indices, dn, B.indptr, Bi, dn, Cp, Ci, dw, dn, dw, dw, wl, b, stage_fill(),
                 cached ? cache : (int32_t *)nullptr));
-    CSRK_LAUNCH((k_gemm_W<double, PH_FILL>), wgrid((wsm<kWW, PH_FILL>())), kWTPB, (wsm<kWW, PH_FILL>()), s, wl, b, w2, A.indptr, A.indices, dn,
-                B.indptr, Bi, dn, Cp, Ci, dw, dn, dw, dw);
-    CSRK_LAUNCH((k_gemm_W<double, PH_FILL, true>), wgrid((wsm<kW2W, PH_FILL>())), kWTPB,
-                (wsm<kW2W, PH_FILL>()), s, w2, b, BigList{}, A.indptr,
-                A.indices, dn, B.indptr, Bi, dn, Cp, Ci, dw, dn, dw, dw);
-    CSRK_LAUNCH(k_big_prep, big_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, B.indptr);
-    CSRK_LAUNCH((k_gemm_big_sym<PH_FILL, false>), sort_grid(), kGemmTPB, big_sort_smem(), s, br, B.ncols, A.indptr,
-                A.indices, B.indptr, Bi, Cp, Ci);
-    CSRK_LAUNCH((k_gemm_big_sym<PH_FILL, true>), big_grid(), kGemmTPB, big_sym_smem(), s, br, B.ncols, A.indptr,
-                A.indices, B.indptr, Bi, Cp, Ci);
+    // the W kernel also forwards rows to the W2 list: it runs when either class is non-empty
+    if (stamp.ncls[0] || stamp.ncls[2])
+        CSRK_LAUNCH((k_gemm_W<double, PH_FILL>), wgrid((wsm<kWW, PH_FILL>())), kWTPB, (wsm<kWW, PH_FILL>()), s, wl, b,
+                    w2, A.indptr, A.indices, dn, B.indptr, Bi, dn, Cp, Ci, dw, dn, dw, dw);
+    if (stamp.ncls[2])
+        CSRK_LAUNCH((k_gemm_W<double, PH_FILL, true>), wgrid((wsm<kW2W, PH_FILL>())), kWTPB,
+                    (wsm<kW2W, PH_FILL>()), s, w2, b, BigList{}, A.indptr,
+                    A.indices, dn, B.indptr, Bi, dn, Cp, Ci, dw, dn, dw, dw);
+    if (stamp.ncls[1]) {
+        CSRK_LAUNCH(k_big_prep, big_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, B.indptr);
+        CSRK_LAUNCH((k_gemm_big_sym<PH_FILL, false>), sort_grid(), kGemmTPB, big_sort_smem(), s, br, B.ncols,
+                    A.indptr, A.indices, B.indptr, Bi, Cp, Ci);
+        CSRK_LAUNCH((k_gemm_big_sym<PH_FILL, true>), big_grid(), kGemmTPB, big_sym_smem(), s, br, B.ncols,
+                    A.indptr, A.indices, B.indptr, Bi, Cp, Ci);
+    }
     return CSRK_OK;
 }
 

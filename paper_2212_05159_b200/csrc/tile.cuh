@@ -45,7 +45,7 @@ struct TileArgs {
     int64_t *cursor;        // TRANSPOSE
     uint64_t *out_keys;     // TRANSPOSE: packed (p << 31) | row per claimed slot
     int R;                  // rows per tile
-    const int *run_if;      // non-null: k_rows / k_rows_long do nothing unless *run_if != 0
+    const int *run_if;      // non-null: k_rows does nothing unless *run_if != 0
     int accD;               // k_rows SIDE: D += instead of D = (internal: the PCG's dL accumulation)
 };
 
