@@ -320,8 +320,9 @@ int csrk_gcn_bwd(csrk_dtype dtype, csrk_pattern A, const void *A_val, const csrk
  *   csrk_dense_gemm_nn:  Z[n x F] = X[n x C] W        (transW = 0, W: C x F row-major)
  *                        Z[n x F] = X[n x C] W^T      (transW = 1, W: F x C row-major; dX = dZ Theta^T)
  *                        W is staged in shared memory (C F <= 25600); no workspace.
- *   csrk_dense_gemm_tn:  dW[C x F] = X^T dZ           (dTheta; fp64 accumulation, workspace
- *                        CSRK_WS_DENSE_GEMM_TN; C * ceil(F / 16) <= 256).
+ *   csrk_dense_gemm_tn:  dW[C x F] = X^T dZ           (dTheta; fp64 accumulation in a fixed order --
+ *                        per-CTA partials summed in block order, no atomics, so the same bits on
+ *                        every run; workspace CSRK_WS_DENSE_GEMM_TN; C * ceil(F / 16) <= 256).
  * Row-major, ld >= the row width.  Memory-bound tall-skinny products (C, F ~ 16): one pass over
  * the n rows, no tensor cores.
  */

@@ -79,6 +79,20 @@ __device__ __forceinline__ void gcn_load(const T *p, int64_t c, int64_t F, doubl
     for (int q = 0; q < kV; ++q) v[q] = c + q < F ? (double)p[c + q] : 0.0;
 }
 
+// the lane's kV values of a row as one 16-byte (fp32) / two 16-byte (fp64) loads: F % 4 == 0 and
+// 16-byte aligned rows (checked on the host)
+__device__ __forceinline__ void gcn_load_vec(const float *p, int64_t c, double (&v)[kV])
+{
+    const float4 f = __ldg(reinterpret_cast<const float4 *>(p + c));
+    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+}
+__device__ __forceinline__ void gcn_load_vec(const double *p, int64_t c, double (&v)[kV])
+{
+    const double2 a = __ldg(reinterpret_cast<const double2 *>(p + c));
+    const double2 b = __ldg(reinterpret_cast<const double2 *>(p + c) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+
 // out row i = D_i (sum_p a_p D_j Z_j + D_i Z_i) + bias, lanes [g*G, g*G + G) of a warp own row i
 template <typename T>
 __device__ __forceinline__ void gcn_finish(const GcnArgs<T> &a, int64_t i, int64_t c, double (&acc)[kV])
@@ -97,9 +111,9 @@ __device__ __forceinline__ void gcn_finish(const GcnArgs<T> &a, int64_t i, int64
 }
 
 #ifndef CSRK_GCN_MINB
-#define CSRK_GCN_MINB 1
+#define CSRK_GCN_MINB 4   // measured (1 / 4 / 6 / 8): fwd 356 / 324 / 344 / 445 us on the f4 workload
 #endif
-template <typename T, int G>
+template <typename T, int G, bool VEC>
 __global__ __launch_bounds__(kGcnTPB, CSRK_GCN_MINB) void k_gcn_prop(GcnArgs<T> a)
 {
     pdl_wait();
@@ -120,7 +134,8 @@ __global__ __launch_bounds__(kGcnTPB, CSRK_GCN_MINB) void k_gcn_prop(GcnArgs<T> 
             const int32_t j = a.indices[p];
             const double w = (double)a.vals[a.perm ? a.perm[p] : p] * a.D[j];
             double z[kV];
-            gcn_load(a.Z + (int64_t)j * a.ldz, c, a.F, z);
+            if (VEC) gcn_load_vec(a.Z + (int64_t)j * a.ldz, c, z);
+            else gcn_load(a.Z + (int64_t)j * a.ldz, c, a.F, z);
 #pragma unroll
             for (int q = 0; q < kV; ++q) acc[q] = fma(w, z[q], acc[q]);
         }
@@ -265,27 +280,32 @@ __global__ __launch_bounds__(kGcnTPB) void k_rowgemm(int64_t n, int64_t C, int64
 // dW[C x F] += X^T dZ: a thread owns (c, 16-column chunk of F) for one row slot; the CTA's row
 // slots stride its slice of rows; partials reduced in shared memory, then one fp64 atomic per
 // output and CTA.  X[r, c] and dZ[r, chunk] are shared by the threads of a row (broadcast).
+// dW = X^T dZ (C x F) for tall X (n x C), dZ (n x F): each CTA sums a contiguous block of rows;
+// its 256 threads are `slots` row slots x (C x ceil(F/16)) column blocks, each thread owning 16
+// fp64 accumulators.  The slots' partials are added in slot order in shared memory and the
+// CTA's C x F partial is written to part[blockIdx]; k_tn_sum adds the CTAs' partials in block
+// order.  No atomics: the result is the same bits on every run.
 template <typename T>
 __global__ __launch_bounds__(kGcnTPB) void k_gemm_tn(int64_t n, int64_t C, int64_t F, const T *__restrict__ X,
                                                      int64_t ldx, const T *__restrict__ dZ, int64_t lddz,
-                                                     double *__restrict__ acc)
+                                                     double *__restrict__ part)
 {
     pdl_wait();
     extern __shared__ __align__(16) unsigned char s_raw[];
-    double *s_part = reinterpret_cast<double *>(s_raw);  // C x F partials of this CTA
+    double *s_part = reinterpret_cast<double *>(s_raw);  // [slots][C x F]
     const int64_t nch = (F + kGemmChunk - 1) / kGemmChunk;
     const int64_t per_row = C * nch;                        // threads per row slot (<= kGcnTPB)
     const int64_t slots = kGcnTPB / per_row;
-    for (int64_t q = threadIdx.x; q < C * F; q += kGcnTPB) s_part[q] = 0.0;
-    __syncthreads();
     const int64_t rows_per = (n + gridDim.x - 1) / gridDim.x;
     const int64_t r0 = (int64_t)blockIdx.x * rows_per, r1 = r0 + rows_per < n ? r0 + rows_per : n;
     const int64_t slot = threadIdx.x / per_row, w = threadIdx.x % per_row;
     const int64_t cc = w / nch, f0 = (w % nch) * kGemmChunk;
+    const int64_t CF = C * F;
     if (slot < slots) {
         double a[kGemmChunk];
 #pragma unroll
         for (int q = 0; q < kGemmChunk; ++q) a[q] = 0.0;
+#pragma unroll 2
         for (int64_t r = r0 + slot; r < r1; r += slots) {
             const double x = (double)X[r * ldx + cc];
             const T *z = dZ + r * lddz + f0;
@@ -295,10 +315,32 @@ __global__ __launch_bounds__(kGcnTPB) void k_gemm_tn(int64_t n, int64_t C, int64
         }
 #pragma unroll
         for (int q = 0; q < kGemmChunk; ++q)
-            if (f0 + q < F) atomicAdd(&s_part[cc * F + f0 + q], a[q]);
+            if (f0 + q < F) s_part[slot * CF + cc * F + f0 + q] = a[q];
     }
     __syncthreads();
-    for (int64_t q = threadIdx.x; q < C * F; q += kGcnTPB) atomicAdd(&acc[q], s_part[q]);
+    for (int64_t q = threadIdx.x; q < CF; q += kGcnTPB) {
+        double t = 0.0;
+        for (int64_t sl = 0; sl < slots; ++sl) t += s_part[sl * CF + q];
+        part[(int64_t)blockIdx.x * CF + q] = t;
+    }
+}
+
+// dW[q] = sum_b part[b][q] in a fixed order: a warp per output, lane-strided partial sums then a
+// fixed shuffle tree (a single thread's chain over all CTAs' partials would be ~600 dependent loads)
+template <typename T>
+__global__ __launch_bounds__(kGcnTPB) void k_tn_sum(int64_t CF, int nb, const double *__restrict__ part,
+                                                    T *__restrict__ dW)
+{
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (kGcnTPB / 32);
+    for (int64_t q = (int64_t)blockIdx.x * (kGcnTPB / 32) + (threadIdx.x >> 5); q < CF; q += warps) {
+        double t = 0.0;
+        for (int b = lane; b < nb; b += 32) t += part[(int64_t)b * CF + q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) dW[q] = (T)t;
+    }
 }
 
 // ---------------------------------------------------------------- host side
@@ -309,7 +351,10 @@ static int launch_prop(GcnArgs<T> &a, cudaStream_t s)
     const int64_t groups = cdiv(a.n, 1);
     int64_t grid = cdiv(groups * G, kGcnTPB);
     if (grid > kNumSMs * 16) grid = kNumSMs * 16;
-    CSRK_LAUNCH((k_gcn_prop<T, G>), (unsigned)grid, kGcnTPB, 0, s, a);
+    const bool vec = a.F % kV == 0 && (a.ldz * (int64_t)sizeof(T)) % 16 == 0 &&
+                     !(reinterpret_cast<uintptr_t>(a.Z) & 15) && knob("GCN_VEC", 1);
+    if (vec) CSRK_LAUNCH((k_gcn_prop<T, G, true>), (unsigned)grid, kGcnTPB, 0, s, a);
+    else CSRK_LAUNCH((k_gcn_prop<T, G, false>), (unsigned)grid, kGcnTPB, 0, s, a);
     CSRK_LAUNCH((k_gcn_prop_long<T, G>), (unsigned)(kNumSMs * 4), kGcnTPB, 0, s, a);
     return CSRK_OK;
 }
@@ -426,16 +471,18 @@ template <typename T>
 static int gemm_tn_t(int64_t n, int64_t C, int64_t F, const T *X, int64_t ldx, const T *dZ, int64_t lddz, T *dW,
                      Bump &ws, cudaStream_t s)
 {
-    double *acc = ws.take<double>(C * F > 0 ? C * F : 1);
+    constexpr int nb = kNumSMs * 4;
+    double *part = ws.take<double>((size_t)nb * (C * F > 0 ? C * F : 1));
     if (ws.sizing()) return CSRK_OK;
     if (C * F == 0) return CSRK_OK;
-    CSRK_CUDA(cudaMemsetAsync(acc, 0, sizeof(double) * (size_t)(C * F), s));
-    const size_t smem = sizeof(double) * (size_t)(C * F);
+    if (n == 0) return cudaMemsetAsync(dW, 0, sizeof(T) * (size_t)(C * F), s) == cudaSuccess ? CSRK_OK : CSRK_ERR_CUDA;
+    const int64_t per_row = C * ((F + kGemmChunk - 1) / kGemmChunk);
+    const size_t smem = sizeof(double) * (size_t)(kGcnTPB / per_row) * (size_t)(C * F);
     if (smem > 48 * 1024) CSRK_CUDA(cudaFuncSetAttribute(k_gemm_tn<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                          (int)smem));
-    // (float4 loads of dZ measured slower here: 0.21 vs 0.18 ms on the GCN bench)
-    if (n > 0) CSRK_LAUNCH(k_gemm_tn<T>, (unsigned)(kNumSMs * 4), kGcnTPB, smem, s, n, C, F, X, ldx, dZ, lddz, acc);
-    CSRK_LAUNCH(k_to_dtype<T>, (unsigned)cdiv(C * F, 256), 256, 0, s, C * F, acc, dW);
+    CSRK_LAUNCH(k_gemm_tn<T>, (unsigned)nb, kGcnTPB, smem, s, n, C, F, X, ldx, dZ, lddz, part);
+    CSRK_LAUNCH(k_tn_sum<T>, (unsigned)cdiv(C * F, kGcnTPB / 32), kGcnTPB, 0, s, C * F, nb, (const double *)part,
+                dW);
     return CSRK_OK;
 }
 
