@@ -14,6 +14,8 @@ done
 timeout 900 python bench.py --workload cfg5 --precond solve --steps 5 > gpurun_out/bench_cfg5_solve.log 2>&1
 # one --set full capture of the main kernels: the workload set-up (plan, symbolic) + the first warm-up step
 timeout 1200 ncu -f --set full --import-source on --clock-control none \
-  -k 'regex:k_spmm_wide|k_gemm_S|k_sort_short|k_col_count|k_rows' -c 22 \
+  -k 'regex:k_spmm_pipe|k_gemm_S|k_tr_sym|k_rows' -c 16 \
   -o gpurun_out/full_step python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full.log 2>&1
 tail -c 400 gpurun_out/bench_default.log
+# per-op attribution of the default step (profiles/traffic_cfg2.json source)
+bash tools/traffic_run.sh cfg2 > gpurun_out/traffic_run.log 2>&1
