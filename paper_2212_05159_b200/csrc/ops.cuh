@@ -5,12 +5,23 @@
 
 namespace csrk {
 
+// A dot product fused into an SpMV (internal): *out = sum_i y_i w_i over the product's rows, from
+// per-CTA partials in part[cdiv(nrows, 256)], summed in a fixed order.
+struct FusedDot {
+    const void *w;
+    double *part;
+    double *out;
+};
+// accumulate_y (internal, fp64, not in the ABI): y += op(A) x instead of y = (PCG adjoint sums);
+// dot (internal, fp64 op N): the fused dot product of y with dot->w
 int spmv_fwd(csrk_dtype dt, csrk_op op, const csrk_pattern &A, const void *A_val, const csrk_pattern *AT,
-             const int64_t *perm, const void *x, void *y, Bump &ws, cudaStream_t s);
-// accumulate_dA (internal, not in the ABI): dA += the masked gradient instead of dA = (PCG's dL)
+             const int64_t *perm, const void *x, void *y, Bump &ws, cudaStream_t s, int accumulate_y = 0,
+             const FusedDot *dot = nullptr);
+// accumulate_dA / accumulate_dx (internal, not in the ABI): dA += the masked gradient, dx += op(A)^T dy
+// (fp64 only) instead of overwriting (the PCG's dL and rbar)
 int spmv_bwd(csrk_dtype dt, csrk_op op, const csrk_pattern &A, const void *A_val, const csrk_pattern *AT,
              const int64_t *perm, const void *x, const void *dy, void *dA, void *dx, Bump &ws, cudaStream_t s,
-             int accumulate_dA = 0);
+             int accumulate_dA = 0, int accumulate_dx = 0);
 int spmm_fwd(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int64_t k, const void *X, int64_t ldx,
              void *Y, int64_t ldy, Bump &ws, cudaStream_t s);
 int spmm_bwd(csrk_dtype dt, const csrk_pattern &A, const void *A_val, const csrk_pattern *AT, const int64_t *perm,

@@ -146,6 +146,7 @@ struct PcgWs {
     double *u, *z, *rbar, *pbar, *zbar, *ubar, *qbar, *tmp; // n each
     double *dAt;                                            // nnz(L)
     double *part;
+    double *dpart;                                          // fused-dot CTA partials (cdiv(m, 256))
     csrk_pattern LT;                                        // precond = solve: L^T pattern + perm
     int64_t *LTperm;
     Scal S;
@@ -202,6 +203,7 @@ static void carve_pcg(const csrk_pattern &A, const csrk_pattern &L, int N, int p
     for (auto p : tv) *p = ws.take<double>(ne);
     w.dAt = ws.take<double>(L.nnz > 0 ? L.nnz : 1);
     w.part = ws.take<double>(kVecGrid);
+    w.dpart = ws.take<double>((size_t)cdiv(m > 0 ? m : 1, 256));
     double *sc = ws.take<double>(5 * (size_t)(N + 1) + 8);
     w.S.rho = sc;
     w.S.s = sc + (N + 1);
@@ -262,7 +264,8 @@ static int pcg_enqueue(const csrk_comm *comm, int64_t off, const csrk_pattern &A
     // z = M r (owned r, owned z) with the intermediate u (extended) in w.u:
     //   M = L L^T: u = L^T r (op T: an extended partial, halo-reduced, then halo-gathered
     //   for the op-N product), z = L u;   precond = solve: u = L^{-1} r, z = L^{-T} u
-    auto applyM = [&](const double *r, double *z) -> int {
+    // rz (nullable): also *rz = r.z over the owned rows, fused into the last product (M = L L^T)
+    auto applyM = [&](const double *r, double *z, double *rz = nullptr) -> int {
         if (!precond) {
             {
                 Bump bw = sub();
@@ -271,7 +274,8 @@ static int pcg_enqueue(const csrk_comm *comm, int64_t off, const csrk_pattern &A
             CSRK_TRY(reduce(w.u));
             CSRK_TRY(gather(w.u));
             Bump bw = sub();
-            return spmv_fwd(CSRK_F64, CSRK_OP_N, L, Lv, nullptr, nullptr, w.u, z, bw, s);
+            const FusedDot fd{r, w.dpart, rz};
+            return spmv_fwd(CSRK_F64, CSRK_OP_N, L, Lv, nullptr, nullptr, w.u, z, bw, s, 0, rz ? &fd : nullptr);
         }
         {
             Bump bw = sub();
@@ -293,10 +297,10 @@ static int pcg_enqueue(const csrk_comm *comm, int64_t off, const csrk_pattern &A
             CSRK_TRY(reduce(w.ubar));
             CSRK_TRY(gather(w.ubar));
             // u = reduce(L^T r):  Lbar += r ubar^T (.) mask(L);  rbar += L gather(ubar)
-            {
+            {   // (rbar += L gather(ubar) straight into rbar: accumulate mode)
                 Bump bw = sub();
                 CSRK_TRY(spmv_bwd(CSRK_F64, CSRK_OP_T, L, Lv, nullptr, nullptr, r, w.ubar, dL,
-                                  want_rbar ? rb_add : nullptr, bw, s, 1));
+                                  want_rbar ? w.rbar : nullptr, bw, s, 1, 1));
             }
         } else {
             // z = L^{-T} u:  ubar = L^{-1} zbar;  Lbar += -z ubar^T (.) mask(L)
@@ -313,7 +317,7 @@ static int pcg_enqueue(const csrk_comm *comm, int64_t off, const csrk_pattern &A
             }
             LIN3(L.nnz, dL, ONE, dL, ONE, w.dAt, ONE, nullptr, nullptr, nullptr);
         }
-        if (want_rbar) LIN3(m, w.rbar, ONE, w.rbar, ONE, rb_add, ONE, nullptr, nullptr, nullptr);
+        if (want_rbar && precond) LIN3(m, w.rbar, ONE, w.rbar, ONE, rb_add, ONE, nullptr, nullptr, nullptr);
         return CSRK_OK;
     };
     const Scal &S = w.S;
@@ -336,17 +340,23 @@ static int pcg_enqueue(const csrk_comm *comm, int64_t off, const csrk_pattern &A
     CSRK_TRY(gdot(b, P(0), &S.rho[0], 1.0));
     for (int i = 1; i <= N; ++i) {
         CSRK_TRY(gather(Pe(i - 1)));
-        {
+        {   // q_i = A p_{i-1} with s_i = p_{i-1}.q_i fused into the product
             Bump bw = sub();
-            CSRK_TRY(spmv_fwd(CSRK_F64, CSRK_OP_N, A, Av, nullptr, nullptr, Pe(i - 1), Q(i), bw, s));
+            const FusedDot fd{P(i - 1), w.dpart, &S.s[i]};
+            CSRK_TRY(spmv_fwd(CSRK_F64, CSRK_OP_N, A, Av, nullptr, nullptr, Pe(i - 1), Q(i), bw, s, 0, &fd));
         }
-        CSRK_TRY(gdot(P(i - 1), Q(i), &S.s[i], 1.0));
+        CSRK_TRY(allred(&S.s[i], 1));
         // r_i = r_{i-1} - (rho_{i-1}/s_i) q_i ; nr2_i = r_i.r_i (summed over ranks once, at the end)
         LIN3(m, R(i), ONE, R(i - 1), (Cf{-1.0, &S.rho[i - 1], &S.s[i]}), Q(i), ONE, nullptr, nullptr, part);
         CSRK_LAUNCH(k_finish, 1, kVecTPB, 0, s, (const double *)part, kVecGrid, &S.nr2[i], 1.0);
         if (i == N) break;                                     // rho_N, p_N do not reach the loss
-        CSRK_TRY(applyM(R(i), own(w.z)));
-        CSRK_TRY(gdot(R(i), own(w.z), &S.rho[i], 1.0));
+        if (!precond) {
+            CSRK_TRY(applyM(R(i), own(w.z), &S.rho[i]));        // rho_i = r_i.z_i fused into z = L u
+            CSRK_TRY(allred(&S.rho[i], 1));
+        } else {
+            CSRK_TRY(applyM(R(i), own(w.z)));
+            CSRK_TRY(gdot(R(i), own(w.z), &S.rho[i], 1.0));
+        }
         // p_i = z_i + (rho_i / rho_{i-1}) p_{i-1}
         LIN3(m, P(i), ONE, own(w.z), (Cf{1.0, &S.rho[i], &S.rho[i - 1]}), P(i - 1), ONE, nullptr, nullptr, nullptr);
     }
@@ -377,13 +387,21 @@ static int pcg_enqueue(const csrk_comm *comm, int64_t off, const csrk_pattern &A
         LIN3(m, w.qbar, (Cf{-1.0, &S.rho[i - 1], &S.s[i]}), w.rbar, (Cf{1.0, S.sbar, nullptr}), P(i - 1), ONE,
              nullptr, nullptr, nullptr);
         // q_i = A gather(p_{i-1}):  pbar_{i-1} = beta_i pbar_i + sbar q_i + reduce(A^T qbar)
-        {
-            Bump bw = sub();
-            CSRK_TRY(spmv_fwd(CSRK_F64, CSRK_OP_T, A, Av, nullptr, nullptr, w.qbar, w.tmp, bw, s));
-        }
-        CSRK_TRY(reduce(w.tmp));
         const Cf beta = i < N ? Cf{1.0, &S.rho[i], &S.rho[i - 1]} : Cf{0.0, nullptr, nullptr};
-        LIN3(m, w.pbar, beta, w.pbar, (Cf{1.0, S.sbar, nullptr}), Q(i), ONE, own(w.tmp), nullptr, nullptr);
+        if (!comm) {
+            // one GPU: pbar = beta pbar + sbar q first, then A^T qbar scattered straight into it
+            // (no zeroed scratch, no third pass)
+            LIN3(m, w.pbar, beta, w.pbar, (Cf{1.0, S.sbar, nullptr}), Q(i), ONE, nullptr, nullptr, nullptr);
+            Bump bw = sub();
+            CSRK_TRY(spmv_fwd(CSRK_F64, CSRK_OP_T, A, Av, nullptr, nullptr, w.qbar, w.pbar, bw, s, 1));
+        } else {
+            {
+                Bump bw = sub();
+                CSRK_TRY(spmv_fwd(CSRK_F64, CSRK_OP_T, A, Av, nullptr, nullptr, w.qbar, w.tmp, bw, s));
+            }
+            CSRK_TRY(reduce(w.tmp));
+            LIN3(m, w.pbar, beta, w.pbar, (Cf{1.0, S.sbar, nullptr}), Q(i), ONE, own(w.tmp), nullptr, nullptr);
+        }
     }
     // p0 = z0, rho0 = r0.z0 (r0 = b):  zbar = pbar + rhobar_0 b
     LIN3(m, w.zbar, ONE, w.pbar, (Cf{1.0, &S.rhobar[0], nullptr}), b, ONE, nullptr, nullptr, nullptr);

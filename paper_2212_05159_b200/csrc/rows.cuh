@@ -41,6 +41,16 @@ __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, 
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
 
+// REDUCE output: y[row] = acc, or y[row] += acc (accY, internal: the PCG's adjoint accumulation)
+// dotw (internal): dp += y_row * dotw[row] for the thread that stores the row (fused dot product)
+template <typename T>
+__device__ __forceinline__ void store_y(const TileArgs<T> &a, int64_t row, double acc, double &dp)
+{
+    const T y = a.accY ? add_rn(a.y[row], (T)acc) : (T)acc;
+    a.y[row] = y;
+    if (a.dotw) dp = fma((double)y, (double)a.dotw[row], dp);
+}
+
 template <typename T, int MODE, bool PERM, bool SIDE>
 __device__ __forceinline__ void row_elem(const TileArgs<T> &a, int64_t row, int64_t p, double &acc)
 {
@@ -61,7 +71,7 @@ __device__ __forceinline__ void row_elem(const TileArgs<T> &a, int64_t row, int6
 }
 
 template <typename T, int MODE, bool PERM, bool SIDE>
-__device__ __forceinline__ void rows_block(const TileArgs<T> &a, int64_t vb, int *s_nh, int32_t *s_h)
+__device__ __forceinline__ void rows_block(const TileArgs<T> &a, int64_t vb, int *s_nh, int32_t *s_h, double &dp)
 {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
@@ -136,7 +146,7 @@ __device__ __forceinline__ void rows_block(const TileArgs<T> &a, int64_t vb, int
                     for (int64_t p = rs + sub; p < re; p += 4) row_elem<T, MODE, PERM, SIDE>(a, row - lane + src, p, acc);
                 acc += __shfl_xor_sync(FULL, acc, 1);
                 acc += __shfl_xor_sync(FULL, acc, 2);
-                if (own && sub == 0) a.y[row - lane + src] = (T)acc;
+                if (own && sub == 0) store_y(a, row - lane + src, acc, dp);
             }
             done = true;
         }
@@ -145,7 +155,7 @@ __device__ __forceinline__ void rows_block(const TileArgs<T> &a, int64_t vb, int
         double acc = 0.0;
 #pragma unroll 4
         for (int64_t p = s; p < e; ++p) row_elem<T, MODE, PERM, SIDE>(a, row, p, acc);
-        if (MODE == MODE_REDUCE) a.y[row] = (T)acc;
+        if (MODE == MODE_REDUCE) store_y(a, row, acc, dp);
     }
     // rows of kShortRow < l <= kHugeRow: the warp takes them one by one (coalesced over the row,
     // fixed shuffle tree -- deterministic)
@@ -161,7 +171,7 @@ __device__ __forceinline__ void rows_block(const TileArgs<T> &a, int64_t vb, int
         if (MODE == MODE_REDUCE) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
-            if (lane == 0) a.y[r] = (T)acc;
+            if (lane == 0) store_y(a, r, acc, dp);
         }
     }
 }
@@ -169,7 +179,7 @@ __device__ __forceinline__ void rows_block(const TileArgs<T> &a, int64_t vb, int
 // One row longer than kHugeRow, by the whole CTA (lane-strided; REDUCE: fixed warp and block
 // trees -- deterministic)
 template <typename T, int MODE, bool PERM, bool SIDE>
-__device__ __forceinline__ void rows_huge(const TileArgs<T> &a, int64_t row, double *s_red)
+__device__ __forceinline__ void rows_huge(const TileArgs<T> &a, int64_t row, double *s_red, double &dp)
 {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t s = a.indptr[row], e = a.indptr[row + 1];
@@ -185,7 +195,7 @@ __device__ __forceinline__ void rows_huge(const TileArgs<T> &a, int64_t row, dou
             acc = lane < kRowsTPB / 32 ? s_red[lane] : 0.0;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0) a.y[row] = (T)acc;
+            if (lane == 0) store_y(a, row, acc, dp);
         }
         __syncthreads();
     }
@@ -205,13 +215,14 @@ __global__ __launch_bounds__(kRowsTPB, 8) void k_rows(TileArgs<T> a)
     __shared__ int s_nh;
     __shared__ int32_t s_h[kRowsTPB];
     __shared__ double s_red[kRowsTPB / 32];
+    double dp = 0.0;   // fused dot product (dotw): this thread's rows
     auto block = [&](int64_t vb) {
         if (threadIdx.x == 0) s_nh = 0;
         __syncthreads();
-        rows_block<T, MODE, PERM, SIDE>(a, vb, &s_nh, s_h);
+        rows_block<T, MODE, PERM, SIDE>(a, vb, &s_nh, s_h, dp);
         __syncthreads();
         const int nh = s_nh;
-        for (int h = 0; h < nh; ++h) rows_huge<T, MODE, PERM, SIDE>(a, s_h[h], s_red);
+        for (int h = 0; h < nh; ++h) rows_huge<T, MODE, PERM, SIDE>(a, s_h[h], s_red, dp);
     };
     if constexpr (rows_persistent<MODE>()) {
         const int64_t nvb = cdiv(a.nrows, kRowsTPB);
@@ -221,6 +232,37 @@ __global__ __launch_bounds__(kRowsTPB, 8) void k_rows(TileArgs<T> a)
         }
     } else {
         block(blockIdx.x);
+    }
+    if (MODE == MODE_REDUCE && a.dotw) {   // the CTA's partial, fixed shuffle + warp-order tree
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dp += __shfl_xor_sync(0xffffffffu, dp, o);
+        __syncthreads();
+        if (lane == 0) s_red[w] = dp;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int q = 0; q < kRowsTPB / 32; ++q) t += s_red[q];
+            a.dotpart[blockIdx.x] = t;
+        }
+    }
+}
+
+// *out = sum of the nb CTA partials of a fused dot product, in a fixed order
+static __global__ __launch_bounds__(256) void k_dot_finish(const double *__restrict__ part, int64_t nb, double *out)
+{
+    pdl_wait();
+    __shared__ double s[8];
+    double acc = 0.0;
+    for (int64_t q = threadIdx.x; q < nb; q += 256) acc += part[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int q = 0; q < 8; ++q) t += s[q];
+        *out = t;
     }
 }
 
@@ -237,7 +279,9 @@ int launch_rows(const TileArgs<T> &a, const RowList &, cudaStream_t s)
     if (a.nrows <= 0) return CSRK_OK;
     const int64_t nvb = cdiv(a.nrows, kRowsTPB);
     const int64_t cap = rows_persistent<MODE>() ? (int64_t)kNumSMs * 8 : nvb;
-    CSRK_LAUNCH((k_rows<T, MODE, PERM, SIDE>), (unsigned)(nvb < cap ? nvb : cap), kRowsTPB, 0, s, a);
+    const int64_t grid = nvb < cap ? nvb : cap;
+    CSRK_LAUNCH((k_rows<T, MODE, PERM, SIDE>), (unsigned)grid, kRowsTPB, 0, s, a);
+    if (MODE == MODE_REDUCE && a.dotw) CSRK_LAUNCH(k_dot_finish, 1, 256, 0, s, (const double *)a.dotpart, grid, a.dotout);
     return CSRK_OK;
 }
 

@@ -12,7 +12,7 @@ namespace csrk {
 template <typename T, int MODE, bool PERM, bool SIDE>
 static int run(TileArgs<T> a, const RowList &L, cudaStream_t s)
 {
-    if (knob("SPMV_TILE", 0) && !a.accD) return launch_tile<T, MODE, PERM, SIDE>(a, s);
+    if (knob("SPMV_TILE", 0) && !a.accD && !a.accY && !a.dotw) return launch_tile<T, MODE, PERM, SIDE>(a, s);
     return launch_rows<T, MODE, PERM, SIDE>(a, L, s);
 }
 
@@ -33,17 +33,24 @@ static int round_scatter(const double *acc, T *y, int64_t n, cudaStream_t s)
 
 template <typename T>
 static int spmv_fwd_t(csrk_op op, const csrk_pattern &A, const T *A_val, const csrk_pattern *AT,
-                      const int64_t *perm, const T *x, T *y, Bump &ws, cudaStream_t s)
+                      const int64_t *perm, const T *x, T *y, Bump &ws, cudaStream_t s, int accY, const FusedDot *fd)
 {
+    if (accY && sizeof(T) != sizeof(double)) return CSRK_ERR_INVALID_ARG;   // internal, fp64 only
     RowList L{};
     carve_rowlist(A.nrows > A.ncols ? A.nrows : A.ncols, L, ws);
     double *acc = (op == CSRK_OP_T && !AT) ? scatter_target(y, A.ncols, ws) : nullptr;
     if (ws.sizing()) return CSRK_OK;
     TileArgs<T> a{};
+    a.accY = accY;
     if (op == CSRK_OP_N) {
         // y_i = sum_{p in row i} A[p] x[idx p]
         a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices;
         a.vals = A_val; a.v = x; a.y = y;
+        if (fd) {
+            a.dotw = static_cast<const T *>(fd->w);
+            a.dotpart = fd->part;
+            a.dotout = fd->out;
+        }
         a.R = tile_rows(A.nrows, A.nnz);
         return run<T, MODE_REDUCE, false, false>(a, L, s);
     }
@@ -54,8 +61,8 @@ static int spmv_fwd_t(csrk_op op, const csrk_pattern &A, const T *A_val, const c
         a.R = tile_rows(AT->nrows, AT->nnz);
         return run<T, MODE_REDUCE, true, false>(a, L, s);
     }
-    // y = A^T x by atomic scatter of A_ij x_i into y_j (fp64 target, reading A5)
-    CSRK_CUDA(cudaMemsetAsync(acc, 0, sizeof(double) * (size_t)A.ncols, s));
+    // y = A^T x by atomic scatter of A_ij x_i into y_j (fp64 target, reading A5); accY: into y as is
+    if (!accY) CSRK_CUDA(cudaMemsetAsync(acc, 0, sizeof(double) * (size_t)A.ncols, s));
     a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices;
     a.vals = A_val; a.u = x; a.y64 = acc;
     a.R = tile_rows(A.nrows, A.nnz);
@@ -66,8 +73,9 @@ static int spmv_fwd_t(csrk_op op, const csrk_pattern &A, const T *A_val, const c
 template <typename T>
 static int spmv_bwd_t(csrk_op op, const csrk_pattern &A, const T *A_val, const csrk_pattern *AT,
                       const int64_t *perm, const T *x, const T *dy, T *dA, T *dx, Bump &ws, cudaStream_t s,
-                      int accD)
+                      int accD, int accY)
 {
+    if (accY && sizeof(T) != sizeof(double)) return CSRK_ERR_INVALID_ARG;   // internal, fp64 only
     RowList L{};
     carve_rowlist(A.nrows > A.ncols ? A.nrows : A.ncols, L, ws);
     // atomic dx (op N without a plan): fp64 target (sized whenever the call could need it)
@@ -75,6 +83,7 @@ static int spmv_bwd_t(csrk_op op, const csrk_pattern &A, const T *A_val, const c
     if (ws.sizing()) return CSRK_OK;
     TileArgs<T> a{};
     a.accD = accD;
+    a.accY = accY;
     if (op == CSRK_OP_T) {
         // y = A^T x:  dx = A dy (row inner products),  dA[p] = x_i dy_{idx p}
         a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices;
@@ -104,7 +113,7 @@ static int spmv_bwd_t(csrk_op op, const csrk_pattern &A, const T *A_val, const c
         return run<T, MODE_REDUCE, true, false>(a, L, s);
     }
     // row traversal: dA[p] = dy_i x[idx p] (coalesced), dx[idx p] += A[p] dy_i (fp64 atomic)
-    if (dx) CSRK_CUDA(cudaMemsetAsync(acc, 0, sizeof(double) * (size_t)A.ncols, s));
+    if (dx && !accY) CSRK_CUDA(cudaMemsetAsync(acc, 0, sizeof(double) * (size_t)A.ncols, s));
     a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices;
     a.vals = A_val; a.u = dy; a.v = x; a.y64 = dx ? acc : nullptr; a.D = dA;
     a.R = tile_rows(A.nrows, A.nnz);
@@ -114,22 +123,26 @@ static int spmv_bwd_t(csrk_op op, const csrk_pattern &A, const T *A_val, const c
 }
 
 int spmv_fwd(csrk_dtype dt, csrk_op op, const csrk_pattern &A, const void *A_val, const csrk_pattern *AT,
-             const int64_t *perm, const void *x, void *y, Bump &ws, cudaStream_t s)
+             const int64_t *perm, const void *x, void *y, Bump &ws, cudaStream_t s, int accumulate_y,
+             const FusedDot *dot)
 {
+    if (dot && (op != CSRK_OP_N || dt != CSRK_F64)) return CSRK_ERR_INVALID_ARG;   // internal, fp64 op N
     if (dt == CSRK_F64)
-        return spmv_fwd_t<double>(op, A, (const double *)A_val, AT, perm, (const double *)x, (double *)y, ws, s);
-    return spmv_fwd_t<float>(op, A, (const float *)A_val, AT, perm, (const float *)x, (float *)y, ws, s);
+        return spmv_fwd_t<double>(op, A, (const double *)A_val, AT, perm, (const double *)x, (double *)y, ws, s,
+                                  accumulate_y, dot);
+    return spmv_fwd_t<float>(op, A, (const float *)A_val, AT, perm, (const float *)x, (float *)y, ws, s,
+                             accumulate_y, nullptr);
 }
 
 int spmv_bwd(csrk_dtype dt, csrk_op op, const csrk_pattern &A, const void *A_val, const csrk_pattern *AT,
              const int64_t *perm, const void *x, const void *dy, void *dA, void *dx, Bump &ws, cudaStream_t s,
-             int accumulate_dA)
+             int accumulate_dA, int accumulate_dx)
 {
     if (dt == CSRK_F64)
         return spmv_bwd_t<double>(op, A, (const double *)A_val, AT, perm, (const double *)x, (const double *)dy,
-                                  (double *)dA, (double *)dx, ws, s, accumulate_dA);
+                                  (double *)dA, (double *)dx, ws, s, accumulate_dA, accumulate_dx);
     return spmv_bwd_t<float>(op, A, (const float *)A_val, AT, perm, (const float *)x, (const float *)dy,
-                             (float *)dA, (float *)dx, ws, s, accumulate_dA);
+                             (float *)dA, (float *)dx, ws, s, accumulate_dA, accumulate_dx);
 }
 
 }  // namespace csrk

@@ -47,6 +47,10 @@ struct TileArgs {
     int R;                  // rows per tile
     const int *run_if;      // non-null: k_rows does nothing unless *run_if != 0
     int accD;               // k_rows SIDE: D += instead of D = (internal: the PCG's dL accumulation)
+    int accY;               // k_rows REDUCE y += / SCATTER into y as is (internal: PCG adjoint sums)
+    const T *dotw;          // k_rows REDUCE (internal): also *dotout = sum_row y_row dotw_row
+    double *dotpart;        //   per-CTA partials, cdiv(nrows, 256) of them
+    double *dotout;
 };
 
 // Dynamic shared-memory layout (bytes offsets), identical on host and device.
