@@ -657,7 +657,7 @@ struct PipeLayout {
 #define CSRK_PIPE_MINB_FWD 4   // measured: config-2 forward 473 -> 445 us (5: spills)
 #endif
 #ifndef CSRK_PIPE_MINB_DOT
-#define CSRK_PIPE_MINB_DOT 4   // 5: 827 -> 1460 us (spills)
+#define CSRK_PIPE_MINB_DOT 3   // measured 3 / 4 / 5: 805 / 817 / 1460 us (4: small spills, 5: heavy)
 #endif
 template <int MODE, int G> constexpr int pipe_minb()
 {
