@@ -656,12 +656,15 @@ struct PipeLayout {
 #ifndef CSRK_PIPE_MINB_FWD
 #define CSRK_PIPE_MINB_FWD 4   // measured: config-2 forward 473 -> 445 us (5: spills)
 #endif
+#ifndef CSRK_PIPE_MINB_G8
+#define CSRK_PIPE_MINB_G8 5
+#endif
 #ifndef CSRK_PIPE_MINB_DOT
 #define CSRK_PIPE_MINB_DOT 3   // measured 3 / 4 / 5: 805 / 817 / 1460 us (4: small spills, 5: heavy)
 #endif
 template <int MODE, int G> constexpr int pipe_minb()
 {
-    return G == 8 ? 5 : (MODE == SP_FWD || MODE == SP_FWD_PERM ? CSRK_PIPE_MINB_FWD : CSRK_PIPE_MINB_DOT);
+    return G == 8 ? CSRK_PIPE_MINB_G8 : (MODE == SP_FWD || MODE == SP_FWD_PERM ? CSRK_PIPE_MINB_FWD : CSRK_PIPE_MINB_DOT);
 }
 
 template <typename T, int NV, int MODE, bool BAND, int G, bool WST, bool L1G = false>
