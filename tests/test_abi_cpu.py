@@ -71,6 +71,18 @@ def test_host_side_argument_checks(lib):
     # a too-small workspace is rejected on the host before any launch
     assert lib.csrk_spmv_fwd(1, 0, A, 8, None, None, 8, 8, None, 0, None) == -4
     assert lib.csrk_workspace_size(5, 1, ctypes.byref(A), ctypes.byref(A), 0, 0, ctypes.byref(n)) == 0 and n.value > 0
+    # SpGEMM backward with a transpose plan: the plan must be A^T's shape, plan and perm together;
+    # the plan path needs no dB scratch (its workspace is not larger than the atomic path's)
+    S = P(4, 4, 6, 8, 8)
+    bad_T = P(4, 5, 6, 8, 8)
+    assert lib.csrk_spgemm_bwd_plan(1, S, 8, ctypes.byref(bad_T), 8, S, 8, S, 8, 8, 8, None, 0, None) == -2
+    good_T = P(4, 4, 6, 8, 8)
+    assert lib.csrk_spgemm_bwd_plan(1, S, 8, ctypes.byref(good_T), None, S, 8, S, 8, 8, 8, None, 0, None) == -1
+    assert lib.csrk_spgemm_bwd_plan(1, S, 8, None, None, P(5, 4, 6, 8, 8), 8, S, 8, 8, 8, None, 0, None) == -2
+    n_plain, n_plan = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    assert lib.csrk_workspace_size(7, 0, ctypes.byref(A), ctypes.byref(A), 0, 0, ctypes.byref(n_plain)) == 0
+    assert lib.csrk_workspace_size(7, 0, ctypes.byref(A), ctypes.byref(A), 0, 1, ctypes.byref(n_plan)) == 0
+    assert 0 < n_plan.value <= n_plain.value + (1 << 20)
     assert lib.csrk_launch_count() == 0
 
 
