@@ -31,6 +31,16 @@ static int round_scatter(const double *acc, T *y, int64_t n, cudaStream_t s)
     else return f64_to_f32(acc, y, n, s);
 }
 
+// Plan-path SpMV backward with dA split off into the row traversal: for matrices with scattered
+// columns (the radix-transpose regime, config 4), where writing dA through perm is random.
+// CSRK_SPMV_PLAN_SPLIT=0/1 forces either.
+static bool split_plan(const csrk_pattern &A)
+{
+    static int k = knob("SPMV_PLAN_SPLIT", -1);
+    if (k >= 0) return k != 0;
+    return A.ncols >= (int64_t(1) << 22) && A.nnz >= 8 * A.ncols;
+}
+
 template <typename T>
 static int spmv_fwd_t(csrk_op op, const csrk_pattern &A, const T *A_val, const csrk_pattern *AT,
                       const int64_t *perm, const T *x, T *y, Bump &ws, cudaStream_t s, int accY, const FusedDot *fd)
@@ -102,7 +112,18 @@ static int spmv_bwd_t(csrk_op op, const csrk_pattern &A, const T *A_val, const c
     }
     // op N (y = A x)
     if (AT && dx) {
-        // transposed traversal: dx_j = sum_q A[perm q] dy[AT idx q];  dA[perm q] = dy[AT idx q] x_j
+        // transposed traversal: dx_j = sum_q A[perm q] dy[AT idx q];  dA[perm q] = dy[AT idx q] x_j.
+        // Scattered patterns (use_split_plan): dA through perm would be one random sector write per
+        // entry, so dA takes the coalesced row traversal instead and the transposed pass only
+        // gathers dx (config 4: 10.2 -> ~2 ms).
+        if (dA && split_plan(A)) {
+            TileArgs<T> r = a;
+            r.nrows = A.nrows; r.indptr = A.indptr; r.indices = A.indices;
+            r.vals = A_val; r.u = dy; r.v = x; r.D = dA;
+            r.R = tile_rows(A.nrows, A.nnz);
+            CSRK_TRY((run<T, MODE_SCATTER, false, true>(r, L, s)));
+            dA = nullptr;
+        }
         a.nrows = AT->nrows; a.indptr = AT->indptr; a.indices = AT->indices;
         a.vals = A_val; a.perm = perm; a.v = dy; a.u = x; a.y = dx;
         a.R = tile_rows(AT->nrows, AT->nnz);
