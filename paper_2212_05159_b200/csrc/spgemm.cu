@@ -1719,10 +1719,84 @@ __global__ __launch_bounds__(kDbTPB) void k_gemm_dB_long(const int64_t *__restri
     }
 }
 
+// Scattered patterns (config 4: C rows are random, far beyond L2): the thread-per-row walk reads C
+// rows sector by sector from DRAM, so every stored entry of B is taken as in k_gemm_dB_long, a warp
+// per 32 consecutive entries (binary search per i); the chunk's first row by a binary search over
+// B's row starts, each lane's row by a galloping search from there.
+template <typename T>
+__global__ __launch_bounds__(kDbTPB) void k_gemm_dB_flat(int64_t nnzB, int64_t mB, const int64_t *__restrict__ Bp,
+                                                         const int32_t *__restrict__ Bi,
+                                                         const int64_t *__restrict__ ATp,
+                                                         const int32_t *__restrict__ ATi,
+                                                         const int64_t *__restrict__ perm, const T *__restrict__ Av,
+                                                         const int64_t *__restrict__ Cp,
+                                                         const int32_t *__restrict__ Ci, const T *__restrict__ dC,
+                                                         T *__restrict__ dB)
+{
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * kDbTPB;
+    for (int64_t base = ((int64_t)blockIdx.x * kDbTPB + threadIdx.x) - lane; base < nnzB; base += stride) {
+        int64_t k0 = 0;
+        if (lane == 0) {
+            int64_t lo = 0, hi = mB - 1;   // last row r with Bp[r] <= base
+            while (lo < hi) {
+                const int64_t mid = (lo + hi + 1) >> 1;
+                if (__ldg(Bp + mid) <= base) lo = mid; else hi = mid - 1;
+            }
+            k0 = lo;
+        }
+        k0 = __shfl_sync(0xffffffffu, k0, 0);
+        const int64_t pb = base + lane;
+        if (pb >= nnzB) continue;
+        int64_t lo = k0, step = 1;   // last r >= k0 with Bp[r] <= pb
+        while (lo + step < mB && __ldg(Bp + lo + step) <= pb) {
+            lo += step;
+            step <<= 1;
+        }
+        int64_t hi = lo + step < mB ? lo + step : mB;
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (__ldg(Bp + mid) <= pb) lo = mid; else hi = mid;
+        }
+        const int64_t k = lo;
+        const int32_t j = __ldg(Bi + pb);
+        double acc = 0.0;
+        const int64_t q1 = __ldg(ATp + k + 1);
+        for (int64_t q = __ldg(ATp + k); q < q1; ++q) {
+            const int32_t i = __ldg(ATi + q);
+            const double a = (double)__ldg(Av + __ldg(perm + q));
+            const int64_t c0 = __ldg(Cp + i), c1 = __ldg(Cp + i + 1);
+            int64_t l = c0, h = c1;
+            while (l < h) {
+                const int64_t mid = (l + h) >> 1;
+                if (__ldg(Ci + mid) < j) l = mid + 1; else h = mid;
+            }
+            if (l < c1 && __ldg(Ci + l) == j) acc = fma(a, (double)__ldg(dC + l), acc);
+        }
+        dB[pb] = (T)acc;
+    }
+}
+
+static bool dB_flat(const csrk_pattern &B)
+{
+    static int k = knob("GEMM_DB_FLAT", -1);
+    if (k >= 0) return k != 0;
+    return B.ncols >= (int64_t(1) << 22) && B.nnz >= 8 * B.ncols;
+}
+
 template <typename T>
 static int launch_dB_gather(const csrk_pattern &B, const csrk_pattern &AT, const int64_t *perm, const T *Av,
                             const csrk_pattern &C, const T *dC, T *dB, Bump &ws, cudaStream_t s)
 {
+    if (!ws.sizing() && B.nnz > 0 && dB_flat(B)) {
+        const int64_t warps = cdiv(B.nnz, 32);
+        const int64_t cap = (int64_t)kNumSMs * 8 * (kDbTPB / 32);
+        const int64_t grid = cdiv(warps < cap ? warps : cap, kDbTPB / 32);
+        CSRK_LAUNCH(k_gemm_dB_flat<T>, (unsigned)grid, kDbTPB, 0, s, B.nnz, B.nrows, B.indptr, B.indices, AT.indptr,
+                    AT.indices, perm, Av, C.indptr, C.indices, dC, dB);
+        return CSRK_OK;
+    }
     DbLong lng{};
     lng.ctr = ws.take<unsigned long long>(1);
     lng.rows = ws.take<int32_t>(B.nrows > 0 ? B.nrows : 1);
