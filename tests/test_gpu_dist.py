@@ -196,3 +196,62 @@ def test_gpu_pcg_sharded_matches_single_gpu_and_oracle(tmp_path, world, N, n_it)
     # sharded vs single GPU: same kernels, only the dot summation order differs
     assert abs(float(R[0]["loss"]) - loss1) <= tau_l * abs(loss1)
     assert np.all(np.abs(dLs - dL1) <= tau_g * S)
+
+
+def _nccl_worker(rank, world, port, N, n_it, out_dir):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)   # only to broadcast the NCCL id
+    from paper_2212_05159_b200 import csrk as ck
+    from paper_2212_05159_b200 import dist as D
+    torch.cuda.set_device(0)
+    A, L, b = _pcg_problem(N)
+    sh = D.PcgShard(A, L, b, rank, world)
+    comm = ck.comm_nccl(rank, world, sh.halo)
+    Ad, Ld, bt = ck.CSR.from_host(sh.A), ck.CSR.from_host(sh.L), torch.from_numpy(sh.b).cuda()
+    out = {}
+    for rep in range(2):   # first call captures the CUDA graph (NCCL calls inside), the second replays it
+        loss, res, dL = ck.pcg_loss_grad_dist(comm, sh.own_off, Ad, Ld, bt, n_it, 0.6)
+        out[f"loss{rep}"], out[f"dL{rep}"], out[f"res{rep}"] = loss, dL.cpu().numpy(), np.array(res)
+    ck.comm_destroy(comm)
+    np.savez(os.path.join(out_dir, f"n{rank}.npz"), **out)
+    tdist.destroy_process_group()
+
+
+def test_gpu_pcg_nccl_comm_one_rank(tmp_path):
+    """The real NCCL csrk_comm (comm.cu: communicator creation, ncclAllReduce of the dot products,
+    graph capture of a step containing NCCL calls) at world size 1 -- the only size one GPU admits
+    (NCCL refuses two ranks per device).  No halo peers, so the sharded step must reproduce the
+    single-GPU step up to summation order, and the replayed graph must reproduce the loss bit for
+    bit."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2212_05159_b200 import build
+    build.build()
+    from paper_2212_05159_b200 import csrk as ck
+    N, n_it = 48, 30
+    mp.spawn(_nccl_worker, args=(1, _free_port(), N, n_it, str(tmp_path)), nprocs=1, join=True)
+    R = np.load(tmp_path / "n0.npz")
+    # the forward pass sums at most two terms per atomic target (L^T r, L bidiagonal): the replayed
+    # graph reproduces the loss bit for bit; the reverse pass's A^T qbar (five terms) does not
+    assert float(R["loss0"]) == float(R["loss1"])
+    A, L, b = _pcg_problem(N)
+    loss1, res1, dL1 = ck.pcg_loss_grad(ck.CSR.from_host(A), ck.CSR.from_host(L), torch.from_numpy(b).cuda(), n_it,
+                                        0.6)
+    dL1 = dL1.cpu().numpy()
+    # The two runs differ only in summation order (the op-T products scatter with atomics, in no
+    # fixed order, on either path), which CG amplifies over the iterations: tolerances are the
+    # problem's own sensitivity, measured by the oracle under a 1e-15 relative perturbation of b
+    # (DESIGN R-PCG), as in the multi-rank test above.
+    from oracle import pcg
+    loss_ref, res_ref, g_ref, S = pcg.pcg_loss_grad_sparse(A, L, b, n_it, 0.6)
+    bp = b * (1.0 + 1e-15 * np.random.default_rng(1).standard_normal(b.shape))
+    loss_alt, res_alt, g_alt, _ = pcg.pcg_loss_grad_sparse(A, L, bp, n_it, 0.6, want_S=False)
+    Sg = np.where(S > 0, S, 1.0)
+    tau_g = max(1e-12, 20 * float(np.max(np.abs(g_alt - g_ref) / Sg)))
+    tau_l = max(1e-12, 20 * abs(loss_alt - loss_ref) / abs(loss_ref))
+    tau_r = max(1e-12, 20 * float(np.max(np.abs(np.array(res_alt) - res_ref) / np.array(res_ref))))
+    assert abs(float(R["loss0"]) - loss1) <= tau_l * abs(loss1)
+    np.testing.assert_allclose(R["res0"], np.array(res1), rtol=tau_r)
+    assert np.all(np.abs(R["dL0"] - dL1) <= tau_g * S)
+    assert np.all(np.abs(R["dL1"] - dL1) <= tau_g * S)
