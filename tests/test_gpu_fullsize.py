@@ -177,7 +177,11 @@ def test_config4_powerlaw(ck, orc):
     ATs, _ = sub_rows(AT, rows)
     r = orc.spmv_fwd(ATs, dy)
     close(h(dx_plan)[rows], r.value, r.S, dt, "dx (plan) sampled cols")
-    del dx_plan, plan
+    # with dA too: scattered pattern -> dA by the row traversal, dx by the transposed gather
+    dA_plan, dx_plan2 = ck.spmv_bwd(Ad, xt, dyt, plan=plan)
+    np.testing.assert_array_equal(h(dA_plan), h(dA))          # single products: bit-exact
+    np.testing.assert_array_equal(h(dx_plan2), h(dx_plan))     # same gather, same order
+    del dx_plan, dx_plan2, dA_plan
     torch.cuda.empty_cache()
     # SpGEMM
     C = ck.spgemm_symbolic(Ad, Ad)
@@ -202,3 +206,8 @@ def test_config4_powerlaw(ck, orc):
     C_v = np.zeros(C.nnz, np.float32)
     C_v[cpos] = Cv[cpos_t].cpu().numpy()
     check_spgemm(orc, A, A, AT, C_p, C_i, C_v, dC_host, h(dAg), h(dBg), dt, srows, brows)
+    # deterministic dB (flat per-entry gather on this scattered pattern) on the same samples, twice
+    _, dBp = ck.spgemm_bwd(Ad, Ad, C, dCd, need_dA=False, plan=plan)
+    _, dBp2 = ck.spgemm_bwd(Ad, Ad, C, dCd, need_dA=False, plan=plan)
+    np.testing.assert_array_equal(h(dBp), h(dBp2))
+    check_spgemm(orc, A, A, AT, C_p, C_i, C_v, dC_host, h(dAg), h(dBp), dt, srows, brows)
