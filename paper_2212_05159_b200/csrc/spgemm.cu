@@ -306,6 +306,7 @@ __global__ __launch_bounds__(kSTPB, kSMinBlocks) void k_gemm_S(int64_t m, const 
         for (int64_t e = c_lo + lane; e < c_hi; e += 32) sv[e - c_lo] = dC[e];
         __syncwarp();
     }
+    bool unc = false;
     if (isS) {
         const int64_t cs = PH == PH_COUNT ? 0 : Cp[i];
         int32_t *outI = PH == PH_FILL ? (stage ? si + (cs - c_lo) : Ci + cs)
@@ -342,8 +343,13 @@ __global__ __launch_bounds__(kSTPB, kSMinBlocks) void k_gemm_S(int64_t m, const 
         }
         if (PH == PH_COUNT) Cp[i + 1] = cnt;
         if (PH == PH_COUNT && cflag) cflag[i] = cnt <= kSCache ? 1 : 0;
+        unc = PH == PH_COUNT && cflag && cnt > kSCache;
     } else if (PH == PH_COUNT && cflag && valid) {
         cflag[i] = 0;
+    }
+    if (PH == PH_COUNT && cflag) {   // short rows whose columns the cache could not keep (wl.count[3])
+        const unsigned um = __ballot_sync(0xffffffffu, unc);
+        if (um && lane == 0) atomicAdd(wl.count + 3, __popc(um));
     }
     if (stage) {
         __syncwarp();
@@ -1389,7 +1395,7 @@ struct CountStamp {
     const int64_t *Ap, *Bp;
     const int32_t *Ai, *Bi;
     int64_t m, nnzA, nnzB;
-    int ncls[3];   // rows COUNT queued to the W / big / W2 paths (not part of the identity)
+    int ncls[4];   // rows COUNT queued to the W / big / W2 paths, short rows not cached (not identity)
     bool operator==(const CountStamp &o) const
     {
         return ws == o.ws && Ap == o.Ap && Bp == o.Bp && Ai == o.Ai && Bi == o.Bi && m == o.m && nnzA == o.nnzA &&
@@ -1410,6 +1416,38 @@ void gemm_fill_cache_invalidate(const void *ws, size_t bytes)
     }
 }
 
+// FILL when COUNT kept every row's columns (all rows short, <= kSCache columns each): a warp per
+// 32 rows loads slot c of its rows coalesced (cache[c m + i]), kFcBatch slots in flight per
+// thread, stages the rows in shared memory in C order and writes the warp's C range coalesced.
+constexpr int kFcTPB = 256;
+constexpr int kFcBatch = 16;
+__global__ __launch_bounds__(kFcTPB) void k_fill_copy(int64_t m, const int64_t *__restrict__ Cp,
+                                                      const int32_t *__restrict__ cache, int32_t *__restrict__ Ci)
+{
+    pdl_wait();
+    __shared__ int32_t s_c[kFcTPB / 32][32 * kSCache];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t i0 = (int64_t)blockIdx.x * kFcTPB + w * 32;
+    if (i0 >= m) return;
+    const int64_t i = i0 + lane;
+    const int64_t iend = i0 + 32 < m ? i0 + 32 : m;
+    const int64_t c0 = Cp[i0], c1 = Cp[iend];
+    const int64_t cs = i < m ? Cp[i] : c1;
+    const int n = i < m ? (int)(Cp[i + 1] - cs) : 0;
+    const int nmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)n);
+    int32_t *dst = s_c[w] + (cs - c0);
+    for (int b = 0; b < nmax; b += kFcBatch) {
+        int32_t q[kFcBatch];
+#pragma unroll
+        for (int u = 0; u < kFcBatch; ++u) q[u] = b + u < n ? __ldcs(cache + (int64_t)(b + u) * m + i) : 0;
+#pragma unroll
+        for (int u = 0; u < kFcBatch; ++u)
+            if (b + u < n) dst[b + u] = q[u];
+    }
+    __syncwarp();
+    for (int64_t e = c0 + lane; e < c1; e += 32) Ci[e] = s_c[w][e - c0];
+}
+
 int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, int32_t *Ci, int64_t *nnzC_host,
                     Bump &ws, cudaStream_t s)
 {
@@ -1420,7 +1458,7 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, i
     const size_t mr = (size_t)(A.nrows > 0 ? A.nrows : 1);
     int32_t *cache = use_fill_cache() ? ws.take<int32_t>(mr * kSCache + (mr + 3) / 4) : nullptr;
     if (ws.sizing()) return scan_counts_i64(nullptr, A.nrows, ws, s);
-    CountStamp stamp{ws.base, A.indptr, B.indptr, A.indices, B.indices, A.nrows, A.nnz, B.nnz, {1, 1, 1}};
+    CountStamp stamp{ws.base, A.indptr, B.indptr, A.indices, B.indices, A.nrows, A.nnz, B.nnz, {1, 1, 1, 1}};
     const int64_t m = A.nrows;
     CSRK_TRY(set_smem_attrs());
     const unsigned gS = (unsigned)cdiv(m, kSTPB);
@@ -1457,9 +1495,7 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, i
         if (m > 0) {
             // the class sizes travel with the stamp: FILL on the same arguments skips the launches
             // of the empty classes (the row classes depend on A's and B's patterns only)
-            stamp.ncls[0] = cls[0];
-            stamp.ncls[1] = cls[1];
-            stamp.ncls[2] = cls[2];
+            for (int c = 0; c < 4; ++c) stamp.ncls[c] = cls[c];
             std::lock_guard<std::mutex> g(g_stamp_mu);
             g_stamps.push_back(stamp);
         }
@@ -1472,13 +1508,19 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, i
         for (size_t q = 0; q < g_stamps.size(); ++q)
             if (g_stamps[q] == stamp) {
                 found = true;
-                for (int c = 0; c < 3; ++c) stamp.ncls[c] = g_stamps[q].ncls[c];
+                for (int c = 0; c < 4; ++c) stamp.ncls[c] = g_stamps[q].ncls[c];
                 g_stamps.erase(g_stamps.begin() + (long)q);  // one FILL per COUNT
                 break;
             }
     }
     const bool cached = found && cache;
-    // without the COUNT of these arguments every class is launched (ncls stays {1, 1, 1})
+    // without the COUNT of these arguments every class is launched (ncls stays {1, 1, 1, 1})
+    if (cached && !stamp.ncls[0] && !stamp.ncls[1] && !stamp.ncls[2] && !stamp.ncls[3] && knob("GEMM_FILL_COPY", 1)) {
+        // every row is short and kept in the cache: FILL is a copy (k_fill_copy), nothing else
+        const unsigned g = (unsigned)cdiv(m, kFcTPB);
+        CSRK_LAUNCH(k_fill_copy, g, kFcTPB, 0, s, m, (const int64_t *)Cp, (const int32_t *)cache, Ci);
+        return CSRK_OK;
+    }
     CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 4 * sizeof(int), s));
     CSRK_TRY((launch_S<double, PH_FILL>)(B.nnz < INT32_MAX, gS, s_smem<double>(PH_FILL, stage_fill()), s, m, A.indptr,
                 A.indices, dn, B.indptr, Bi, dn, Cp, Ci, dw, dn, dw, dw, wl, b, stage_fill(),
