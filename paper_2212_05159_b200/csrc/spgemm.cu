@@ -1419,8 +1419,14 @@ void gemm_fill_cache_invalidate(const void *ws, size_t bytes)
 // FILL when COUNT kept every row's columns (all rows short, <= kSCache columns each): a warp per
 // 32 rows loads slot c of its rows coalesced (cache[c m + i]), kFcBatch slots in flight per
 // thread, stages the rows in shared memory in C order and writes the warp's C range coalesced.
-constexpr int kFcTPB = 256;
-constexpr int kFcBatch = 16;
+#ifndef CSRK_FC_TPB
+#define CSRK_FC_TPB 256
+#endif
+#ifndef CSRK_FC_BATCH
+#define CSRK_FC_BATCH 8   // measured (4 / 6 / 8 / 16 / 32): 8 and below ~342 us, 16: 353, 32: 556 (config 2)
+#endif
+constexpr int kFcTPB = CSRK_FC_TPB;       // A/B via CSRK_NVCC_EXTRA
+constexpr int kFcBatch = CSRK_FC_BATCH;
 __global__ __launch_bounds__(kFcTPB) void k_fill_copy(int64_t m, const int64_t *__restrict__ Cp,
                                                       const int32_t *__restrict__ cache, int32_t *__restrict__ Ci)
 {
