@@ -22,6 +22,7 @@
 // pattern unsymmetric (device flag), and the general kernels above, which are launched behind it
 // and read the flag, then run; on success they return at once.  Exact either way.
 
+#include "condgraph.cuh"
 #include "ops.cuh"
 #include "rows.cuh"
 #include "tile.cuh"
@@ -463,40 +464,6 @@ int transpose_impl(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int6
     int *sym_bad = ws.take<int>(1);
     if (ws.sizing()) return scan_counts_i64(nullptr, n, ws, s);  // carve the scan scratch
 
-    // symmetric pattern first (square, not the SPMV_TILE A/B path); the general kernels below
-    // run only if it failed (run_if = sym_bad)
-    const bool try_sym = A.nrows == A.ncols && nnz > 0 && knob("TRANSPOSE_SYM", 1) && !knob("SPMV_TILE", 0);
-    const int *run_if = try_sym ? sym_bad : nullptr;
-    if (try_sym) {
-        CSRK_CUDA(cudaMemsetAsync(sym_bad, 0, sizeof(int), s));
-        CSRK_LAUNCH(k_tr_sym, (unsigned)cdiv(A.nrows, kSymTPB), kSymTPB, 0, s, A.nrows, A.indptr, A.indices, ATp,
-                    ATi, pm, sym_bad);
-        CSRK_LAUNCH(k_zero_i64_if, grid_for(n + 1, 256), 256, 0, s, ATp, n + 1, run_if);
-    } else {
-        CSRK_CUDA(cudaMemsetAsync(ATp, 0, sizeof(int64_t) * (size_t)(n + 1), s));
-    }
-    if (nnz > 0)
-        CSRK_LAUNCH(k_col_count, grid_for(nnz, 256), 256, 0, s, nnz, A.indices,
-                    reinterpret_cast<unsigned long long *>(ATp + 1), run_if);
-    CSRK_TRY(scan_counts_i64(ATp, n, ws, s, run_if));
-    if (nnz == 0) return CSRK_OK;
-    if (try_sym) CSRK_LAUNCH(k_copy_i64_if, grid_for(n, 256), 256, 0, s, cursor, (const int64_t *)ATp, n, run_if);
-    else CSRK_CUDA(cudaMemcpyAsync(cursor, ATp, sizeof(int64_t) * (size_t)n, cudaMemcpyDeviceToDevice, s));
-    CSRK_CUDA(cudaMemsetAsync(L.count, 0, sizeof(int) * 4, s));
-    {
-        TileArgs<double> a{};
-        a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices;
-        a.cursor = cursor; a.out_keys = keys;
-        a.R = tile_rows(A.nrows, nnz);
-        a.run_if = run_if;
-        if (knob("SPMV_TILE", 0)) CSRK_TRY((launch_tile<double, MODE_TRANSPOSE, false, false>(a, s)));
-        else CSRK_TRY((launch_rows<double, MODE_TRANSPOSE, false, false>(a, RL, s)));
-    }
-    CSRK_LAUNCH(k_sort_short, grid_for(cdiv(n, 32) * 32, 32 * kShortWarps), 32 * kShortWarps, 0, s, n,
-                (const int64_t *)ATp, (const uint64_t *)keys, ATi, pm, L, run_if);
-    if (nnz > kRegMax)
-        CSRK_LAUNCH(k_sort_warp, (unsigned)(kNumSMs * 4), 32 * kWarpsPerSortCTA, 0, s, (const int64_t *)ATp,
-                    (const uint64_t *)keys, ATi, pm, L);
     const size_t big_smem = sizeof(uint64_t) * kBlockMax;
     static DevOnce attr;
     if (attr.need()) {
@@ -504,12 +471,67 @@ int transpose_impl(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int6
         CSRK_CUDA(cudaFuncSetAttribute(k_sort_huge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big_smem));
         attr.done();
     }
-    if (nnz > kWarpMax)
-        CSRK_LAUNCH(k_sort_block, (unsigned)kNumSMs, kSortTPB, big_smem, s, (const int64_t *)ATp,
-                    (const uint64_t *)keys, ATi, pm, L);
-    if (nnz > kBlockMax)
-        CSRK_LAUNCH(k_sort_huge, (unsigned)kNumSMs, kSortTPB, big_smem, s, (const int64_t *)ATp, keys, buf, ATi, pm,
-                    L);
+    // The general counting-sort path on stream st.  gate (device flag, nullable): every kernel
+    // returns at once unless *gate != 0 -- how it runs behind the symmetric attempt on a plain stream.
+    auto general = [&](cudaStream_t st, const int *gate, Bump &w) -> int {
+        if (gate) CSRK_LAUNCH(k_zero_i64_if, grid_for(n + 1, 256), 256, 0, st, ATp, n + 1, gate);
+        else CSRK_CUDA(cudaMemsetAsync(ATp, 0, sizeof(int64_t) * (size_t)(n + 1), st));
+        if (nnz > 0)
+            CSRK_LAUNCH(k_col_count, grid_for(nnz, 256), 256, 0, st, nnz, A.indices,
+                        reinterpret_cast<unsigned long long *>(ATp + 1), gate);
+        CSRK_TRY(scan_counts_i64(ATp, n, w, st, gate));
+        if (nnz == 0) return CSRK_OK;
+        if (gate) CSRK_LAUNCH(k_copy_i64_if, grid_for(n, 256), 256, 0, st, cursor, (const int64_t *)ATp, n, gate);
+        else CSRK_CUDA(cudaMemcpyAsync(cursor, ATp, sizeof(int64_t) * (size_t)n, cudaMemcpyDeviceToDevice, st));
+        CSRK_CUDA(cudaMemsetAsync(L.count, 0, sizeof(int) * 4, st));
+        {
+            TileArgs<double> a{};
+            a.nrows = A.nrows; a.indptr = A.indptr; a.indices = A.indices;
+            a.cursor = cursor; a.out_keys = keys;
+            a.R = tile_rows(A.nrows, nnz);
+            a.run_if = gate;
+            if (knob("SPMV_TILE", 0)) CSRK_TRY((launch_tile<double, MODE_TRANSPOSE, false, false>(a, st)));
+            else CSRK_TRY((launch_rows<double, MODE_TRANSPOSE, false, false>(a, RL, st)));
+        }
+        CSRK_LAUNCH(k_sort_short, grid_for(cdiv(n, 32) * 32, 32 * kShortWarps), 32 * kShortWarps, 0, st, n,
+                    (const int64_t *)ATp, (const uint64_t *)keys, ATi, pm, L, gate);
+        if (nnz > kRegMax)
+            CSRK_LAUNCH(k_sort_warp, (unsigned)(kNumSMs * 4), 32 * kWarpsPerSortCTA, 0, st, (const int64_t *)ATp,
+                        (const uint64_t *)keys, ATi, pm, L);
+        if (nnz > kWarpMax)
+            CSRK_LAUNCH(k_sort_block, (unsigned)kNumSMs, kSortTPB, big_smem, st, (const int64_t *)ATp,
+                        (const uint64_t *)keys, ATi, pm, L);
+        if (nnz > kBlockMax)
+            CSRK_LAUNCH(k_sort_huge, (unsigned)kNumSMs, kSortTPB, big_smem, st, (const int64_t *)ATp, keys, buf, ATi,
+                        pm, L);
+        return CSRK_OK;
+    };
+    auto sym = [&](cudaStream_t st) -> int {
+        CSRK_CUDA(cudaMemsetAsync(sym_bad, 0, sizeof(int), st));
+        CSRK_LAUNCH(k_tr_sym, (unsigned)cdiv(A.nrows, kSymTPB), kSymTPB, 0, st, A.nrows, A.indptr, A.indices, ATp,
+                    ATi, pm, sym_bad);
+        return CSRK_OK;
+    };
+    // Symmetric pattern first (square, not the SPMV_TILE A/B path).  Default: one CUDA graph whose
+    // conditional node runs the general path only if k_tr_sym found a missing mirror (no launches
+    // at all otherwise); fallback / CSRK_TRANSPOSE_GRAPH=0: the general kernels gated on the flag.
+    const bool try_sym = A.nrows == A.ncols && nnz > 0 && knob("TRANSPOSE_SYM", 1) && !knob("SPMV_TILE", 0);
+    bool done = false;
+    if (try_sym && knob("TRANSPOSE_GRAPH", 1)) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const CondKey key = cond_key({(uint64_t)A.indptr, (uint64_t)A.indices, (uint64_t)A.nrows, (uint64_t)nnz,
+                                      (uint64_t)ATp, (uint64_t)ATi, (uint64_t)pm, (uint64_t)ws.base, (uint64_t)ws.cap,
+                                      (uint64_t)dev});
+        Bump wb = ws;
+        done = cond_graph_run(1, key, s, sym_bad, sym, [&](cudaStream_t cs) { return general(cs, nullptr, wb); }) ==
+               CSRK_OK;
+    }
+    if (!done) {
+        if (try_sym) CSRK_TRY(sym(s));
+        CSRK_TRY(general(s, try_sym ? sym_bad : nullptr, ws));
+    }
+    if (nnz == 0) return CSRK_OK;
     if (AT_val) {
         if (dt == CSRK_F64)
             CSRK_LAUNCH(k_gather_vals<double>, grid_for(nnz, 256), 256, 0, s, nnz, (const int64_t *)pm,

@@ -3,6 +3,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "condgraph.cuh"
 #include "csrk_internal.cuh"
 
 namespace csrk {
@@ -219,6 +220,24 @@ int validate_pattern(const csrk_pattern &A, cudaStream_t s)
     CSRK_CUDA(cudaMemcpyFromSymbolAsync(&bad, g_bad_pattern, sizeof(int), 0, cudaMemcpyDeviceToHost, s));
     CSRK_CUDA(cudaStreamSynchronize(s));
     return bad ? CSRK_ERR_PATTERN : CSRK_OK;
+}
+
+// ---------------------------------------------------------------- conditional graphs (condgraph.cuh)
+__global__ void k_set_cond(cudaGraphConditionalHandle h, const int *flag)
+{
+    cudaGraphSetConditional(h, *(volatile const int *)flag != 0 ? 1u : 0u);
+}
+
+cudaStream_t cond_capture_stream(int which)
+{
+    static std::mutex mu;
+    static cudaStream_t streams[64][2] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> g(mu);
+    cudaStream_t &st = streams[dev & 63][which & 1];
+    if (!st && cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    return st;
 }
 
 }  // namespace csrk
