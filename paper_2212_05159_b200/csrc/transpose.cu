@@ -517,7 +517,11 @@ int transpose_impl(csrk_dtype dt, const csrk_pattern &A, const void *A_val, int6
     // at all otherwise); fallback / CSRK_TRANSPOSE_GRAPH=0: the general kernels gated on the flag.
     const bool try_sym = A.nrows == A.ncols && nnz > 0 && knob("TRANSPOSE_SYM", 1) && !knob("SPMV_TILE", 0);
     bool done = false;
-    if (try_sym && knob("TRANSPOSE_GRAPH", 1)) {
+    // not while the caller's stream is being captured (e.g. inside the PCG step's graph): a graph
+    // cannot be captured and launched inside another capture -- the flag-gated kernels are captured
+    cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
+    const bool capturing = cudaStreamIsCapturing(s, &cap_st) != cudaSuccess || cap_st != cudaStreamCaptureStatusNone;
+    if (try_sym && knob("TRANSPOSE_GRAPH", 1) && !capturing) {
         int dev = 0;
         cudaGetDevice(&dev);
         const CondKey key = cond_key({(uint64_t)A.indptr, (uint64_t)A.indices, (uint64_t)A.nrows, (uint64_t)nnz,
