@@ -376,6 +376,56 @@ __device__ __forceinline__ int64_t lbound(const int32_t *c, int64_t n, int32_t v
     return lo;
 }
 
+// Position index of a sorted C row (columns key[0..nc), distinct) held in shared memory: the
+// column range [key[0], key[nc-1]] is cut into NB buckets by a monotone map (the identity when
+// the range has at most NB columns, else a 32-bit fixed-point scale), and bst[b] = first position
+// whose column maps to a bucket >= b (bst[NB] = nc).  A column j of the row then lies in
+// [bst[b(j)], bst[b(j)+1]) -- a binary search over ~nc / NB entries instead of log2(nc) steps
+// (config 4's C rows have uniformly spread columns: ~1-2 entries per bucket).  Exact for any
+// column distribution: a clustered row only makes its buckets longer.
+struct PosIdx {
+    int32_t mn;
+    uint32_t scale;   // 0: identity map
+};
+__device__ __forceinline__ int pos_bucket(const PosIdx &x, int32_t j)
+{
+    const uint32_t d = (uint32_t)(j - x.mn);
+    return (int)(x.scale ? __umulhi(d, x.scale) : d);
+}
+template <int NB>
+__device__ __forceinline__ PosIdx pos_index_params(const int32_t *key, int nc)
+{
+    PosIdx x;
+    x.mn = nc > 0 ? key[0] : 0;
+    const uint64_t span = nc > 0 ? (uint64_t)(key[nc - 1] - x.mn) + 1 : 1;
+    x.scale = span <= (uint64_t)NB ? 0u : (uint32_t)(((uint64_t)NB << 32) / span);
+    return x;
+}
+// build bst[0..NB] with threads t = 0..nt-1 (the caller synchronises before and after)
+template <int NB>
+__device__ __forceinline__ void pos_index_build(const int32_t *key, int nc, const PosIdx &x, uint16_t *bst, int t,
+                                                int nt)
+{
+    for (int q = t; q < nc; q += nt) {
+        const int bq = pos_bucket(x, key[q]);
+        const int bp = q > 0 ? pos_bucket(x, key[q - 1]) : -1;
+        for (int b = bp + 1; b <= bq; ++b) bst[b] = (uint16_t)q;
+    }
+    const int blast = nc > 0 ? pos_bucket(x, key[nc - 1]) : -1;
+    for (int b = blast + 1 + t; b <= NB; b += nt) bst[b] = (uint16_t)nc;
+}
+// position of column j (present in the row)
+__device__ __forceinline__ int pos_find(const int32_t *key, const uint16_t *bst, const PosIdx &x, int32_t j)
+{
+    const int b = pos_bucket(x, j);
+    int lo = bst[b], hi = bst[b + 1];
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (key[mid] < j) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
 // ---------------------------------------------------------------- medium rows: warp per row
 // per-phase layout (shared memory decides how many warps an SM holds): COUNT keeps a hash table
 // of 2 WW columns, FILL the WW gathered columns, NUM / BWD the C row (columns + fp64 values) and
@@ -391,6 +441,7 @@ struct WSmemT {
     int32_t off[WL + 1];                 // flat offset of list t (off[l] = w)
     int32_t tmp[PH == PH_FILL ? WW : 1]; // FILL: the bucket-sorted columns
     int32_t cnt[PH == PH_FILL ? WW / 2 : 1];  // FILL: bucket counts / offsets
+    uint16_t bst[VAL ? WW / 2 + 1 : 1];       // NUM / BWD: position index of the C row (PosIdx)
 };
 // symbolic-only warp class for 512 < w <= kW2W (config-4 rows the CTA path sorted slowly)
 constexpr int kW2W = 1024;
@@ -599,7 +650,7 @@ __global__ __launch_bounds__(kWTPB, CSRK_W_MINB) void k_gemm_W(BigList wl, BigLi
         }
         if (run > WW) {  // too many products for the warp: the symbolic W2 class or the CTA path
             if (lane == 0) {
-                if (!W2 && (PH == PH_COUNT || PH == PH_FILL) && w2l.rows && run <= kW2W)
+                if (!W2 && w2l.rows && run <= kW2W)
                     w2l.rows[atomicAdd(w2l.count, 1)] = (int32_t)i;
                 else
                     big.rows[atomicAdd(big.count, 1)] = (int32_t)i;
@@ -625,6 +676,12 @@ __global__ __launch_bounds__(kWTPB, CSRK_W_MINB) void k_gemm_W(BigList wl, BigLi
                 for (int t = lane; t < l; t += 32) S.dA[t] = 0.0;
         }
         __syncwarp();
+        PosIdx px{};
+        if (PH == PH_NUM || PH == PH_BWD) {
+            px = pos_index_params<WW / 2>(S.key, nc);
+            pos_index_build<WW / 2>(S.key, nc, px, S.bst, lane, 32);
+            __syncwarp();
+        }
         int cnt = 0;
         int t = w > 0 ? w_list_of(S.off, l, lane < w ? lane : 0) : 0;
         constexpr int U = 8;  // products gathered per lane before use: U loads in flight
@@ -659,13 +716,13 @@ __global__ __launch_bounds__(kWTPB, CSRK_W_MINB) void k_gemm_W(BigList wl, BigLi
                 }
                 if (PH == PH_FILL && ok) S.key[e] = j;
                 if (PH == PH_NUM && ok) {  // (a match_any merge instead of the atomic: 75 vs 72 ms, config 4)
-                    const int64_t pos = lbound(S.key, nc, j);
+                    const int pos = pos_find(S.key, S.bst, px, j);
                     atomicAdd(&S.val[pos], S.av[tv[u]] * bv[u]);
                 }
                 if (PH == PH_BWD && e00 + u * 32 < w) {
                     double g = 0.0, v = 0.0;
                     if (ok) {
-                        const int64_t pos = lbound(S.key, nc, j);
+                        const int pos = pos_find(S.key, S.bst, px, j);
                         g = S.val[pos];
                         v = g * bv[u];
                         if (dB) atomicAdd(&dB[bb[u]], S.av[tv[u]] * g);
@@ -1153,18 +1210,23 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_win(BigRows br, const int
     double *s_val = reinterpret_cast<double *>(s_dyn);                  // NUM: accumulators; BWD: dC
     double *s_dA = s_val + kValSm;                                      // BWD: dA of a one-window row
     int32_t *s_col = reinterpret_cast<int32_t *>(s_dA + kDACap);        // the window's C columns
+    uint16_t *s_bst = reinterpret_cast<uint16_t *>(s_col + kValSm);     // position index of the window
     __shared__ int64_t s_qa[kWinQ], s_qlo[kWinQ], s_qhi[kWinQ];
-    __shared__ int s_nq;
+    __shared__ int s_nq, s_r;
     const int n = *(volatile const int *)br.count;
     const int total = n > 0 ? br.items[n] : 0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int it = blockIdx.x; it < total; it += gridDim.x) {
-        int lo = 0, hi = n - 1;   // the row r holding item it: last r with items[r] <= it
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (br.items[mid] <= it) lo = mid; else hi = mid - 1;
+        if (threadIdx.x == 0) {
+            int lo = 0, hi = n - 1;   // the row r holding item it: last r with items[r] <= it
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (br.items[mid] <= it) lo = mid; else hi = mid - 1;
+            }
+            s_r = lo;
         }
-        const int r = lo;
+        __syncthreads();
+        const int r = s_r;
         const int64_t i = br.rows[r];
         const int64_t as = Ap[i], ae = Ap[i + 1];
         const int64_t row_nc = Cp[i + 1] - Cp[i];
@@ -1180,6 +1242,9 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_win(BigRows br, const int
         const bool dA_sm = PH == PH_BWD && dA && !big_dA_global(row_nc, l);
         if (dA_sm)
             for (int64_t t = threadIdx.x; t < l; t += kGemmTPB) s_dA[t] = 0.0;
+        __syncthreads();
+        const PosIdx px = pos_index_params<kValSm / 2>(s_col, nc);
+        pos_index_build<kValSm / 2>(s_col, nc, px, s_bst, threadIdx.x, kGemmTPB);
         __syncthreads();
         if (single) {
             // one window: the row's w products split into equal contiguous runs (big_walk over the
@@ -1203,7 +1268,7 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_win(BigRows br, const int
                 }
                 const int32_t j = __ldg(Bi + b);
                 const double bv = (double)__ldg(Bv + b);
-                const int pos = (int)lbound(s_col, nc, j);
+                const int pos = pos_find(s_col, s_bst, px, j);
                 if (PH == PH_NUM) {
                     atomicAdd(&s_val[pos], av * bv);
                 } else {
@@ -1226,7 +1291,7 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_win(BigRows br, const int
         auto prod = [&](double av, int64_t b, double &dacc) {
             const int32_t j = __ldg(Bi + b);
             const double bv = (double)__ldg(Bv + b);
-            const int pos = (int)lbound(s_col, nc, j);
+            const int pos = pos_find(s_col, s_bst, px, j);
             if (PH == PH_NUM) {
                 atomicAdd(&s_val[pos], av * bv);
             } else {
@@ -1285,7 +1350,10 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_win(BigRows br, const int
 static unsigned big_grid() { return (unsigned)(kNumSMs * 2); }
 
 static size_t big_sym_smem() { return sizeof(uint32_t) * kBitmapWords; }
-static size_t big_win_smem() { return (sizeof(double) + sizeof(int32_t)) * kValSm + sizeof(double) * kDACap; }
+static size_t big_win_smem()
+{
+    return (sizeof(double) + sizeof(int32_t)) * kValSm + sizeof(double) * kDACap + sizeof(uint16_t) * (kValSm / 2 + 1);
+}
 static size_t big_sort_smem() { return sizeof(int32_t) * (2 * kMMaxW + kMMaxW / 2); }
 static unsigned sort_grid() { return (unsigned)(kNumSMs * 4); }
 static unsigned val_grid() { return (unsigned)(kNumSMs * 4); }
@@ -1322,6 +1390,11 @@ static int set_smem_attrs()
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, ww));
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<float, PH_NUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, ww));
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<float, PH_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, ww));
+    const int w2n = (int)wsm<kW2W, PH_NUM>(), w2b = (int)wsm<kW2W, PH_BWD>();
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_NUM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, w2n));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<double, PH_BWD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, w2b));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<float, PH_NUM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, w2n));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_W<float, PH_BWD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, w2b));
     const int bw = (int)big_win_smem();
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_win<double, PH_NUM>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw));
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_win<double, PH_BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, bw));
@@ -1567,9 +1640,9 @@ template <typename T>
 static int spgemm_values_t(int PH, const csrk_pattern &A, const T *Av, const csrk_pattern &B, const T *Bv,
                            const csrk_pattern &C, T *Cv, const T *dC, T *dA, T *dB, Bump &ws, cudaStream_t s)
 {
-    BigList wl{}, b{};
+    BigList wl{}, b{}, w2{};
     BigRows br{};
-    carve_lists(A, wl, b, br, ws);
+    carve_lists(A, wl, b, br, ws, &w2);
     // backward: fp64 targets of the dB scatter and of the multi-window big-row dA (fp32 data:
     // scratch, rounded once at the end)
     double *dB64 = nullptr, *dA64 = nullptr;
@@ -1594,7 +1667,10 @@ static int spgemm_values_t(int PH, const csrk_pattern &A, const T *Av, const csr
                     Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, Cv, ctn, tn, dn, wl, b, sn,
                     (int32_t *)nullptr));
         CSRK_LAUNCH((k_gemm_W<T, PH_NUM>), wgrid((wsm<kWW, PH_NUM>())), kWTPB, (wsm<kWW, PH_NUM>()), s, wl, b,
-                    BigList{}, A.indptr, A.indices, Av, B.indptr, B.indices, Bv, Cp,
+                    w2, A.indptr, A.indices, Av, B.indptr, B.indices, Bv, Cp,
+                    const_cast<int32_t *>(C.indices), Cv, ctn, tn, dn);
+        CSRK_LAUNCH((k_gemm_W<T, PH_NUM, true>), wgrid((wsm<kW2W, PH_NUM>())), kWTPB, (wsm<kW2W, PH_NUM>()), s, w2,
+                    b, BigList{}, A.indptr, A.indices, Av, B.indptr, B.indices, Bv, Cp,
                     const_cast<int32_t *>(C.indices), Cv, ctn, tn, dn);
         CSRK_LAUNCH(k_big_prep, big_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, B.indptr);
         CSRK_LAUNCH(k_big_items, 1, kItemsTPB, 0, s, br, (const int64_t *)Cp);
@@ -1606,6 +1682,9 @@ static int spgemm_values_t(int PH, const csrk_pattern &A, const T *Av, const csr
                 A.indices, Av, B.indptr, B.indices, Bv, Cp, (int32_t *)nullptr, tn, dC, dA, dB ? dB64 : dn, wl, b,
                 stage_vals(), (int32_t *)nullptr));
     CSRK_LAUNCH((k_gemm_W<T, PH_BWD>), wgrid((wsm<kWW, PH_BWD>())), kWTPB, (wsm<kWW, PH_BWD>()), s, wl, b,
+                w2, A.indptr, A.indices, Av, B.indptr, B.indices, Bv, Cp, const_cast<int32_t *>(C.indices),
+                tn, dC, dA, dB ? dB64 : dn);
+    CSRK_LAUNCH((k_gemm_W<T, PH_BWD, true>), wgrid((wsm<kW2W, PH_BWD>())), kWTPB, (wsm<kW2W, PH_BWD>()), s, w2, b,
                 BigList{}, A.indptr, A.indices, Av, B.indptr, B.indices, Bv, Cp, const_cast<int32_t *>(C.indices),
                 tn, dC, dA, dB ? dB64 : dn);
     CSRK_LAUNCH(k_big_prep, big_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, B.indptr);
