@@ -519,6 +519,41 @@ __device__ __forceinline__ void w_sort_fill(const int32_t *key, int w, int32_t *
     }
 }
 
+// FILL fallback of a warp-path row with w > 64 whose columns overflow a bucket (clustered or
+// repeated columns): bitonic sort of the P = pow2ceil(w) <= WW keys in shared memory (no register
+// arrays: keeps the kernel's register count, hence its occupancy, at the bucket path's), then the
+// distinct ones written in order
+__device__ __noinline__ void w_smem_sort_fill(int32_t *key, int w, int32_t *out, int lane)
+{
+    const unsigned FULL = 0xffffffffu;
+    int P = 32;
+    while (P < w) P <<= 1;
+    for (int e = w + lane; e < P; e += 32) key[e] = INT32_MAX;
+    __syncwarp();
+    for (int k = 2; k <= P; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = lane; i < P; i += 32) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const bool asc = (i & k) == 0;
+                    const int32_t a = key[i], b = key[ixj];
+                    if ((a > b) == asc) { key[i] = b; key[ixj] = a; }
+                }
+            }
+            __syncwarp();
+        }
+    int base = 0;
+    for (int e0 = 0; e0 < w; e0 += 32) {
+        const int e = e0 + lane;
+        const int32_t v = e < w ? key[e] : 0;
+        const bool f = e < w && (e == 0 || v != key[e - 1]);
+        const unsigned m = __ballot_sync(FULL, f);
+        if (f) out[base + __popc(m & ((1u << lane) - 1))] = v;
+        base += __popc(m);
+    }
+    __syncwarp();
+}
+
 // FILL of a warp-path row by a bucket sort (no compare network): the w columns are counted into
 // WW/2 buckets of equal width over [min, max] (shared-memory atomics), the counts scanned, the
 // columns scattered to their buckets, each lane insertion-sorts its WW/64 consecutive buckets, and
@@ -542,7 +577,13 @@ __device__ __forceinline__ bool w_bucket_fill(const int32_t *key, int32_t *tmp, 
     mn = (int32_t)__reduce_min_sync(FULL, (unsigned)mn);
     mx = (int32_t)__reduce_max_sync(FULL, (unsigned)mx);
     const uint64_t span = (uint64_t)(mx - mn) + 1;
-    auto bucket = [&](int32_t k) { return (int)(((uint64_t)(k - mn) * NB) / span); };
+    // monotone bucket map without a per-key 64-bit division: identity when the span has at most
+    // NB columns, else floor((k - mn) * floor(2^32 NB / span) / 2^32) < NB
+    const uint32_t scale = span <= (uint64_t)NB ? 0u : (uint32_t)(((uint64_t)NB << 32) / span);
+    auto bucket = [&](int32_t k) {
+        const uint32_t d = (uint32_t)(k - mn);
+        return (int)(scale ? __umulhi(d, scale) : d);
+    };
     for (int b = lane; b < NB; b += 32) cnt[b] = 0;
     __syncwarp();
     for (int e = lane; e < w; e += 32) atomicAdd(&cnt[bucket(key[e])], 1);
@@ -750,18 +791,9 @@ __global__ __launch_bounds__(kWTPB, CSRK_W_MINB) void k_gemm_W(BigList wl, BigLi
             // sorted by buckets
         } else if (PH == PH_FILL) {
             __syncwarp();
-            if (!W2) {
-                const int P = w <= 32 ? 32 : w <= 64 ? 64 : w <= 128 ? 128 : w <= 256 ? 256 : 512;
-                switch (P) {
-                case 32: w_sort_fill<1>(S.key, w, Ci + cs, lane); break;
-                case 64: w_sort_fill<2>(S.key, w, Ci + cs, lane); break;
-                case 128: w_sort_fill<4>(S.key, w, Ci + cs, lane); break;
-                case 256: w_sort_fill<8>(S.key, w, Ci + cs, lane); break;
-                default: w_sort_fill<16>(S.key, w, Ci + cs, lane); break;
-                }
-            } else {
-                w_sort_fill<32>(S.key, w, Ci + cs, lane);  // 512 < w <= kW2W = 1024
-            }
+            if (w <= 32) w_sort_fill<1>(S.key, w, Ci + cs, lane);
+            else if (w <= 64) w_sort_fill<2>(S.key, w, Ci + cs, lane);
+            else w_smem_sort_fill(S.key, w, Ci + cs, lane);   // rare: a bucket overflowed
         }
         __syncwarp();
         if (PH == PH_NUM)
@@ -865,7 +897,11 @@ __device__ bool cta_bucket_fill(const int32_t *key, int32_t *tmp, int32_t *cnt, 
     mn = (int32_t)-block_max_i64(-(int64_t)mn, s_red);
     mx = (int32_t)block_max_i64(mx, s_red);
     const uint64_t span = (uint64_t)(mx - mn) + 1;
-    auto bucket = [&](int32_t k) { return (int)(((uint64_t)(k - mn) * NB) / span); };
+    const uint32_t scale = span <= (uint64_t)NB ? 0u : (uint32_t)(((uint64_t)NB << 32) / span);  // as w_bucket_fill
+    auto bucket = [&](int32_t k) {
+        const uint32_t d = (uint32_t)(k - mn);
+        return (int)(scale ? __umulhi(d, scale) : d);
+    };
     for (int b = threadIdx.x; b < NB; b += kGemmTPB) cnt[b] = 0;
     __syncthreads();
     for (int e = threadIdx.x; e < w; e += kGemmTPB) atomicAdd(&cnt[bucket(key[e])], 1);

@@ -279,10 +279,32 @@ def test_spmm_strided_operands(ck, orc):
 
 # ---------------------------------------------------------------- SpGEMM
 GEMM_CASES = ["config1_poisson16", "poisson2d_70", "poisson3d_17", "rand_rect_empty_rows", "powerlaw_16k",
-              "skew_mid", "tiny_3x3", "one_row", "nnz0", "skew_big"]
+              "skew_mid", "tiny_3x3", "one_row", "nnz0", "skew_big", "clustered"]
+
+
+def clustered_operands(dt, values):
+    """Warp-path rows (l in {20, 40, 60, 70}: W, W2 and CTA classes) times B rows whose 12 columns
+    sit in one of three 24-column clusters: ~3 products per C column and ~25 per bucket of the
+    FILL bucket sort -- the buckets overflow, so FILL takes its shared-memory bitonic fallback, and
+    the numeric / backward position index sees long, clustered buckets."""
+    rng = np.random.default_rng(515)
+    n = 3000
+    la = rng.choice([20, 40, 60, 70], size=n)
+    a_cols = [np.sort(rng.choice(n, size=int(l), replace=False)) for l in la]
+    b_cols = [np.sort(rng.choice(24, size=12, replace=False) + 1000 * (k % 3)) for k in range(n)]
+
+    def csr(cols):
+        indptr = np.zeros(n + 1, np.int64)
+        indptr[1:] = np.cumsum([len(c) for c in cols])
+        idx = np.concatenate(cols).astype(np.int32)
+        vals = synth.real_values(rng, idx.size, dt) if values == "real" else synth.int_values(rng, idx.size, dt)
+        return synth.CSR(n, n, indptr, idx, vals)
+    return csr(a_cols), csr(b_cols)
 
 
 def gemm_operands(case, dt, values):
+    if case == "clustered":
+        return clustered_operands(dt, values)
     if case == "skew_big":
         A = skew(9000, 8500, 21, dt, values)
         return A, A
