@@ -28,6 +28,7 @@
 //
 // The backward pass computes dA_ik = sum_j dC_ij B_kj per A entry (deterministic) and
 // scatters dB_kj += A_ik dC_ij with global atomic adds (reading A9).
+#include <cooperative_groups.h>
 #include <mutex>
 #include <vector>
 
@@ -966,6 +967,8 @@ struct BigRows {
     int64_t *loff;   // [nnz(A)]
     int64_t *w;      // [m]  products of the r-th big row
     int32_t *items;  // [m + 1] item offsets
+    int32_t *huge;   // symbolic (nullable): big-row ordinals r with w > kMMaxW, appended by k_big_prep
+    int *nhuge;
 };
 
 // last a in [lo, hi) with loff[a] <= e (the list holding product e; empty lists skipped)
@@ -1001,7 +1004,10 @@ __global__ __launch_bounds__(kGemmTPB) void k_big_prep(BigRows br, const int64_t
             if (a < ae) br.loff[a] = run + ex;
             run += tot;
         }
-        if (threadIdx.x == 0) br.w[r] = run;
+        if (threadIdx.x == 0) {
+            br.w[r] = run;
+            if (br.huge && run > kMMaxW) br.huge[atomicAdd(br.nhuge, 1)] = r;
+        }
     }
 }
 
@@ -1138,6 +1144,88 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_sym(BigRows br, int64_t n
         }
         if (PH == PH_COUNT && threadIdx.x == 0) Cp[i + 1] = done;
         __syncthreads();
+    }
+}
+
+// Huge rows (w > kMMaxW), symbolic: one 8-CTA thread-block CLUSTER per row.  CTA c of the cluster
+// owns the bitmap of columns [s0 + c W, s0 + (c + 1) W) (W = 1.6M columns, 200 KB of shared memory),
+// so a super-window of 8 W = 13.1M columns (all of config 4's 8.4M) is covered in ONE pass over the
+// row's products: the 4096 threads of the cluster split the products into equal contiguous runs and
+// set each column's bit in the owning CTA's bitmap through distributed shared memory (remote
+// atomicOr).  Each CTA then counts its window (block scan of the per-thread popcounts), the window
+// counts are exchanged over DSMEM for the offsets, and FILL writes the set bits in ascending order.
+// (The one-CTA-per-row form walked every product once per 1.6M-column window, and the largest rows
+// -- 500K products -- set the kernel's critical path.)
+constexpr int kHugeCl = 8;
+template <int PH>
+__global__ void __cluster_dims__(kHugeCl, 1, 1) __launch_bounds__(kGemmTPB)
+    k_gemm_huge_sym(BigRows br, int64_t ncolsB, const int64_t *__restrict__ Ap, const int32_t *__restrict__ Ai,
+                    const int64_t *__restrict__ Bp, const int32_t *__restrict__ Bi, int64_t *__restrict__ Cp,
+                    int32_t *__restrict__ Ci)
+{
+    namespace cg = cooperative_groups;
+    pdl_wait();
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint32_t *bm = reinterpret_cast<uint32_t *>(smem);
+    __shared__ int64_t s_red[kGemmTPB / 32];
+    __shared__ int64_t s_cnt;
+    const int rank = (int)cl.block_rank();
+    const int ncl = (int)(gridDim.x / kHugeCl), cid = (int)(blockIdx.x / kHugeCl);
+    const int nh = *(volatile const int *)br.nhuge;
+    constexpr int64_t W = (int64_t)kBitmapWords * 32;
+    constexpr int64_t SW = W * kHugeCl;
+    constexpr int pw = kBitmapWords / kGemmTPB;
+    for (int h = cid; h < nh; h += ncl) {
+        const int r = br.huge[h];
+        const int64_t i = br.rows[r];
+        const int64_t as = Ap[i], ae = Ap[i + 1];
+        const int64_t w = br.w[r];
+        const int64_t per = (w + kHugeCl * kGemmTPB - 1) / (kHugeCl * kGemmTPB);
+        const int64_t e_lo = ((int64_t)rank * kGemmTPB + threadIdx.x) * per;
+        const int64_t e_hi = e_lo + per < w ? e_lo + per : w;
+        int64_t done = 0;
+        for (int64_t s0 = 0; s0 < ncolsB; s0 += SW) {
+            for (int e = threadIdx.x; e < kBitmapWords; e += kGemmTPB) bm[e] = 0u;
+            cl.sync();
+            big_walk(br.loff, Ai, Bp, as, ae, e_lo, e_hi, [&](int64_t, int64_t, int64_t b) {
+                const int64_t d = (int64_t)__ldg(Bi + b) - s0;
+                if (d >= 0 && d < SW) {
+                    const int c = (int)(d / W);
+                    const int64_t q = d - c * W;
+                    atomicOr(cl.map_shared_rank(bm, c) + (q >> 5), 1u << (q & 31));
+                }
+            });
+            cl.sync();
+            const int q0 = threadIdx.x * pw;
+            int64_t mine = 0;
+            for (int q = q0; q < q0 + pw; ++q) mine += __popc(bm[q]);
+            int64_t tot;
+            const int64_t off = block_excl_scan_i64(mine, s_red, tot);
+            if (threadIdx.x == 0) s_cnt = tot;
+            cl.sync();
+            int64_t before = 0, all = 0;
+            for (int c = 0; c < kHugeCl; ++c) {
+                const int64_t v = *cl.map_shared_rank(&s_cnt, c);
+                before += c < rank ? v : 0;
+                all += v;
+            }
+            if (PH == PH_FILL) {
+                int64_t o = Cp[i] + done + before + off;
+                const int64_t c0 = s0 + (int64_t)rank * W;
+                for (int q = q0; q < q0 + pw; ++q) {
+                    uint32_t bits = bm[q];
+                    while (bits) {
+                        const int bpos = __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        Ci[o++] = (int32_t)(c0 + (int64_t)q * 32 + bpos);
+                    }
+                }
+            }
+            done += all;
+            cl.sync();   // remote reads of s_cnt done before it and the bitmaps are reused
+        }
+        if (PH == PH_COUNT && rank == 0 && threadIdx.x == 0) Cp[i + 1] = done;
     }
 }
 
@@ -1409,6 +1497,8 @@ static int set_smem_attrs()
     const int bs = (int)big_sym_smem();
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_sym<PH_COUNT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bs));
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_sym<PH_FILL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bs));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_huge_sym<PH_COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bs));
+    CSRK_CUDA(cudaFuncSetAttribute(k_gemm_huge_sym<PH_FILL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bs));
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_sym<PH_COUNT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)big_sort_smem()));
     CSRK_CUDA(cudaFuncSetAttribute(k_gemm_big_sym<PH_FILL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1466,6 +1556,7 @@ static int stage_num(const csrk_pattern &A, const csrk_pattern &C)
 }
 
 // both queue counters live in one 8-byte word so one memset clears them
+static bool huge_cluster() { static int v = knob("GEMM_HUGE_CLUSTER", 1); return v != 0; }
 static void carve_lists(const csrk_pattern &A, BigList &wl, BigList &big, BigRows &br, Bump &ws,
                         BigList *w2 = nullptr)
 {
@@ -1473,7 +1564,7 @@ static void carve_lists(const csrk_pattern &A, BigList &wl, BigList &big, BigRow
     wl.rows = ws.take<int32_t>(m);
     big.rows = ws.take<int32_t>(m);
     int32_t *w2rows = ws.take<int32_t>(m);
-    int *cnt = ws.take<int>(4);
+    int *cnt = ws.take<int>(5);
     wl.count = cnt;
     big.count = cnt ? cnt + 1 : nullptr;
     if (w2) {
@@ -1485,6 +1576,10 @@ static void carve_lists(const csrk_pattern &A, BigList &wl, BigList &big, BigRow
     br.loff = ws.take<int64_t>(A.nnz > 0 ? A.nnz : 1);
     br.w = ws.take<int64_t>(m);
     br.items = ws.take<int32_t>(m + 1);
+    if (w2 && huge_cluster()) {   // symbolic: the huge-row list reuses the W2 list (consumed before k_big_prep)
+        br.huge = w2rows;
+        br.nhuge = cnt ? cnt + 4 : nullptr;
+    }
 }
 
 // k_gemm_S with 32-bit B positions when B has fewer than 2^31 entries (cheaper merge steps)
@@ -1583,7 +1678,7 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, i
     if (!Ci) {
         CSRK_CUDA(cudaMemsetAsync(Cp, 0, sizeof(int64_t), s));
         if (m > 0) {
-            CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 4 * sizeof(int), s));
+            CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 5 * sizeof(int), s));
             {
                 std::lock_guard<std::mutex> g(g_stamp_mu);
                 for (size_t q = 0; q < g_stamps.size(); ++q)
@@ -1599,8 +1694,12 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, i
             CSRK_LAUNCH(k_big_prep, big_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, B.indptr);
             CSRK_LAUNCH((k_gemm_big_sym<PH_COUNT, false>), sort_grid(), kGemmTPB, big_sort_smem(), s, br, B.ncols,
                         A.indptr, A.indices, B.indptr, Bi, Cp, (int32_t *)nullptr);
-            CSRK_LAUNCH((k_gemm_big_sym<PH_COUNT, true>), big_grid(), kGemmTPB, big_sym_smem(), s, br, B.ncols,
-                        A.indptr, A.indices, B.indptr, Bi, Cp, (int32_t *)nullptr);
+            if (br.huge)
+                CSRK_LAUNCH(k_gemm_huge_sym<PH_COUNT>, (unsigned)(kNumSMs / kHugeCl * kHugeCl), kGemmTPB,
+                            big_sym_smem(), s, br, B.ncols, A.indptr, A.indices, B.indptr, Bi, Cp, (int32_t *)nullptr);
+            else
+                CSRK_LAUNCH((k_gemm_big_sym<PH_COUNT, true>), big_grid(), kGemmTPB, big_sym_smem(), s, br, B.ncols,
+                            A.indptr, A.indices, B.indptr, Bi, Cp, (int32_t *)nullptr);
             CSRK_TRY(scan_counts_i64(Cp, m, ws, s));
         }
         CSRK_CUDA(cudaMemcpyAsync(nnzC_host, Cp + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -1636,7 +1735,7 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, i
         CSRK_LAUNCH(k_fill_copy, g, kFcTPB, 0, s, m, (const int64_t *)Cp, (const int32_t *)cache, Ci);
         return CSRK_OK;
     }
-    CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 4 * sizeof(int), s));
+    CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 5 * sizeof(int), s));
     CSRK_TRY((launch_S<double, PH_FILL>)(B.nnz < INT32_MAX, gS, s_smem<double>(PH_FILL, stage_fill()), s, m, A.indptr,
                 A.indices, dn, B.indptr, Bi, dn, Cp, Ci, dw, dn, dw, dw, wl, b, stage_fill(),
                 cached ? cache : (int32_t *)nullptr));
@@ -1652,7 +1751,11 @@ int spgemm_symbolic(const csrk_pattern &A, const csrk_pattern &B, int64_t *Cp, i
         CSRK_LAUNCH(k_big_prep, big_grid(), kGemmTPB, 0, s, br, A.indptr, A.indices, B.indptr);
         CSRK_LAUNCH((k_gemm_big_sym<PH_FILL, false>), sort_grid(), kGemmTPB, big_sort_smem(), s, br, B.ncols,
                     A.indptr, A.indices, B.indptr, Bi, Cp, Ci);
-        CSRK_LAUNCH((k_gemm_big_sym<PH_FILL, true>), big_grid(), kGemmTPB, big_sym_smem(), s, br, B.ncols,
+        if (br.huge)
+            CSRK_LAUNCH(k_gemm_huge_sym<PH_FILL>, (unsigned)(kNumSMs / kHugeCl * kHugeCl), kGemmTPB, big_sym_smem(),
+                        s, br, B.ncols, A.indptr, A.indices, B.indptr, Bi, Cp, Ci);
+        else
+            CSRK_LAUNCH((k_gemm_big_sym<PH_FILL, true>), big_grid(), kGemmTPB, big_sym_smem(), s, br, B.ncols,
                     A.indptr, A.indices, B.indptr, Bi, Cp, Ci);
     }
     return CSRK_OK;
@@ -1679,6 +1782,7 @@ static int spgemm_values_t(int PH, const csrk_pattern &A, const T *Av, const csr
     BigList wl{}, b{}, w2{};
     BigRows br{};
     carve_lists(A, wl, b, br, ws, &w2);
+    br.huge = nullptr;   // (the huge-row list is the symbolic phase's)
     // backward: fp64 targets of the dB scatter and of the multi-window big-row dA (fp32 data:
     // scratch, rounded once at the end)
     double *dB64 = nullptr, *dA64 = nullptr;
@@ -1691,7 +1795,7 @@ static int spgemm_values_t(int PH, const csrk_pattern &A, const T *Av, const csr
     if (PH == PH_BWD && dB) CSRK_CUDA(cudaMemsetAsync(dB64, 0, sizeof(double) * (size_t)B.nnz, s));
     const int64_t m = A.nrows;
     if (m == 0) return dB ? round_f64(dB64, dB, B.nnz, s) : CSRK_OK;
-    CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 4 * sizeof(int), s));
+    CSRK_CUDA(cudaMemsetAsync(wl.count, 0, 5 * sizeof(int), s));
     const unsigned gS = (unsigned)cdiv(m, kSTPB);
     int64_t *Cp = const_cast<int64_t *>(C.indptr);
     T *tn = nullptr;

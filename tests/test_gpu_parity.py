@@ -279,7 +279,8 @@ def test_spmm_strided_operands(ck, orc):
 
 # ---------------------------------------------------------------- SpGEMM
 GEMM_CASES = ["config1_poisson16", "poisson2d_70", "poisson3d_17", "rand_rect_empty_rows", "powerlaw_16k",
-              "skew_mid", "tiny_3x3", "one_row", "nnz0", "skew_big", "clustered"]
+              "skew_mid", "tiny_3x3", "one_row", "nnz0", "skew_big", "clustered",
+              "wide_huge"]
 
 
 def clustered_operands(dt, values):
@@ -303,6 +304,18 @@ def clustered_operands(dt, values):
 
 
 def gemm_operands(case, dt, values):
+    if case == "wide_huge":
+        # huge rows (w = 10,000 > 8192 products) over 2*10^7 columns: the cluster kernel's eight
+        # 1.6M-column windows and a second super-window (columns beyond 8 x 1,638,400)
+        A = synth.random_csr(24, 3000, 1 / 3, 31, dt, values)
+        rng = np.random.default_rng(32)
+        cols = np.sort(rng.choice(20_000_000, size=(3000, 12), replace=True), axis=1)
+        keep = np.concatenate([np.ones((3000, 1), bool), cols[:, 1:] != cols[:, :-1]], axis=1)
+        indptr = np.zeros(3001, np.int64)
+        indptr[1:] = np.cumsum(keep.sum(1))
+        idx = cols[keep].astype(np.int32)
+        vals = synth.real_values(rng, idx.size, dt) if values == "real" else synth.int_values(rng, idx.size, dt)
+        return A, synth.CSR(3000, 20_000_000, indptr, idx, vals)
     if case == "clustered":
         return clustered_operands(dt, values)
     if case == "skew_big":
