@@ -726,7 +726,10 @@ __global__ __launch_bounds__(kWTPB, CSRK_W_MINB) void k_gemm_W(BigList wl, BigLi
         }
         int cnt = 0;
         int t = w > 0 ? w_list_of(S.off, l, lane < w ? lane : 0) : 0;
-        constexpr int U = 8;  // products gathered per lane before use: U loads in flight
+#ifndef CSRK_W_U
+#define CSRK_W_U 8
+#endif
+        constexpr int U = CSRK_W_U;  // products gathered per lane before use: U loads in flight
         for (int e00 = 0; e00 < w; e00 += 32 * U) {
             int32_t jv[U];
             double bv[U];
@@ -1239,7 +1242,7 @@ __global__ void __cluster_dims__(kHugeCl, 1, 1) __launch_bounds__(kGemmTPB)
 // warp.  Backward: dA_ik = sum_j dC_ij B_kj is a register (fp64) sum per A entry and window --
 // stored directly when the row has one window, else added (fp64 atomic) into dA64, the fp64
 // target zeroed by k_big_zero; dB_kj += A_ik dC_ij into the fp64 dB target (reading A9).
-constexpr int kWinQ = 256;   // queued long parts per item
+constexpr int kWinQ = 128;   // queued long parts per item (static shared memory: 3 CTAs per SM)
 
 __device__ __forceinline__ int64_t lbound64(const int32_t *c, int64_t n, int32_t v)
 {
@@ -1319,8 +1322,17 @@ __global__ __launch_bounds__(kGemmTPB) void k_big_cvt(BigRows br, const int64_t 
     }
 }
 
+#ifndef CSRK_BIG_FLAT
+#define CSRK_BIG_FLAT 1   // one-window rows: equal flat product runs per thread (0: a thread per A entry)
+#endif
+#ifndef CSRK_BIG_WIN_MINB
+#define CSRK_BIG_WIN_MINB 2   // measured (config 4): 2 CTAs x batch 8: numeric 57.1 -> 53.1 ms, backward 67.1 -> 61.7 ms
+#endif
+#ifndef CSRK_BIG_BATCH
+#define CSRK_BIG_BATCH 8
+#endif
 template <typename T, int PH>
-__global__ __launch_bounds__(kGemmTPB) void k_gemm_big_win(BigRows br, const int64_t *__restrict__ Ap,
+__global__ __launch_bounds__(kGemmTPB, CSRK_BIG_WIN_MINB) void k_gemm_big_win(BigRows br, const int64_t *__restrict__ Ap,
                                                            const int32_t *__restrict__ Ai, const T *__restrict__ Av,
                                                            const int64_t *__restrict__ Bp,
                                                            const int32_t *__restrict__ Bi, const T *__restrict__ Bv,
@@ -1337,6 +1349,7 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_win(BigRows br, const int
     uint16_t *s_bst = reinterpret_cast<uint16_t *>(s_col + kValSm);     // position index of the window
     __shared__ int64_t s_qa[kWinQ], s_qlo[kWinQ], s_qhi[kWinQ];
     __shared__ int s_nq, s_r;
+    __shared__ int32_t s_alist[kGemmTPB];   // one-window rows: the A entry holding each thread's first product
     const int n = *(volatile const int *)br.count;
     const int total = n > 0 ? br.items[n] : 0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1370,11 +1383,21 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_win(BigRows br, const int
         const PosIdx px = pos_index_params<kValSm / 2>(s_col, nc);
         pos_index_build<kValSm / 2>(s_col, nc, px, s_bst, threadIdx.x, kGemmTPB);
         __syncthreads();
-        if (single) {
-            // one window: the row's w products split into equal contiguous runs (big_walk over the
-            // flat offsets of k_big_prep), whatever the B row lengths
+        if (single && CSRK_BIG_FLAT) {
+            // one window: the row's w products split into equal contiguous runs of the flat order
+            // of k_big_prep, whatever the B row lengths.  The A entry holding each run's first
+            // product is scattered into s_alist by the lists themselves (list a covers the runs
+            // starting in [loff[a], loff[a+1])): no per-thread binary search over loff in global
+            // memory.  A run is walked in batches of CSRK_BIG_BATCH products, loads first.
             const int64_t w = br.w[r];
             const int64_t per = (w + kGemmTPB - 1) / kGemmTPB;
+            for (int64_t a = as + threadIdx.x; a < ae; a += kGemmTPB) {
+                const int64_t lo = br.loff[a], hi = a + 1 < ae ? br.loff[a + 1] : w;
+                int64_t t0 = (lo + per - 1) / per, t1 = (hi + per - 1) / per;
+                t1 = t1 < kGemmTPB ? t1 : kGemmTPB;
+                for (int64_t t = t0; t < t1; ++t) s_alist[t] = (int32_t)(a - as);
+            }
+            __syncthreads();
             const int64_t p_lo = threadIdx.x * per, p_hi = p_lo + per < w ? p_lo + per : w;
             int64_t cur_a = -1;
             double av = 0.0, dacc = 0.0;
@@ -1383,24 +1406,53 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_win(BigRows br, const int
                 if (dA_sm) atomicAdd(&s_dA[cur_a - as], dacc);
                 else atomicAdd(&dA64[cur_a], dacc);
             };
-            big_walk(br.loff, Ai, Bp, as, ae, p_lo, p_hi, [&](int64_t, int64_t a, int64_t b) {
-                if (a != cur_a) {
-                    flush();
-                    cur_a = a;
-                    av = (double)Av[a];
-                    dacc = 0.0;
+            if (p_lo < p_hi) {
+                int64_t a = as + s_alist[threadIdx.x];
+                int64_t lo = br.loff[a], bs = Bp[Ai[a]];
+                int64_t nx = a + 1 < ae ? br.loff[a + 1] : INT64_MAX;
+                constexpr int UB = CSRK_BIG_BATCH;
+                for (int64_t e0 = p_lo; e0 < p_hi; e0 += UB) {
+                    int32_t jv[UB];
+                    double bv[UB];
+                    int64_t bb[UB], aa[UB];
+#pragma unroll
+                    for (int u = 0; u < UB; ++u) {
+                        const int64_t e = e0 + u;
+                        if (e < p_hi) {
+                            while (e >= nx) {
+                                ++a;
+                                lo = nx;
+                                nx = a + 1 < ae ? br.loff[a + 1] : INT64_MAX;
+                                bs = Bp[Ai[a]];
+                            }
+                            bb[u] = bs + (e - lo);
+                            aa[u] = a;
+                            jv[u] = __ldg(Bi + bb[u]);
+                            bv[u] = (double)__ldg(Bv + bb[u]);
+                        } else {
+                            aa[u] = -1;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < UB; ++u) {
+                        if (aa[u] < 0) break;
+                        if (aa[u] != cur_a) {
+                            flush();
+                            cur_a = aa[u];
+                            av = (double)Av[cur_a];
+                            dacc = 0.0;
+                        }
+                        const int pos = pos_find(s_col, s_bst, px, jv[u]);
+                        if (PH == PH_NUM) {
+                            atomicAdd(&s_val[pos], av * bv[u]);
+                        } else {
+                            const double g = s_val[pos];
+                            dacc = fma(g, bv[u], dacc);
+                            if (dB) atomicAdd(&dB[bb[u]], av * g);
+                        }
+                    }
                 }
-                const int32_t j = __ldg(Bi + b);
-                const double bv = (double)__ldg(Bv + b);
-                const int pos = pos_find(s_col, s_bst, px, j);
-                if (PH == PH_NUM) {
-                    atomicAdd(&s_val[pos], av * bv);
-                } else {
-                    const double g = s_val[pos];
-                    dacc = fma(g, bv, dacc);
-                    if (dB) atomicAdd(&dB[b], av * g);
-                }
-            });
+            }
             flush();
             __syncthreads();
             if (PH == PH_NUM)
@@ -1425,8 +1477,9 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_win(BigRows br, const int
             }
         };
         auto put_dA = [&](int64_t a, double dacc, bool any) {
-            if (PH != PH_BWD || !dA) return;
-            if (any) atomicAdd(&dA64[a], dacc);
+            if (PH != PH_BWD || !dA || !any) return;
+            if (dA_sm) atomicAdd(&s_dA[a - as], dacc);
+            else atomicAdd(&dA64[a], dacc);
         };
         for (int64_t a = as + threadIdx.x; a < ae; a += kGemmTPB) {
             const int32_t k = Ai[a];
@@ -1466,6 +1519,8 @@ __global__ __launch_bounds__(kGemmTPB) void k_gemm_big_win(BigRows br, const int
         __syncthreads();
         if (PH == PH_NUM)
             for (int q = threadIdx.x; q < nc; q += kGemmTPB) Cv[cs + q] = (T)s_val[q];
+        if (dA_sm)
+            for (int64_t t = threadIdx.x; t < l; t += kGemmTPB) dA[as + t] = (T)s_dA[t];
         __syncthreads();
     }
 }
