@@ -37,8 +37,20 @@ def load(path):
     return [(name, m) for (_, name), m in sorted(k.items(), key=lambda kv: kv[0][0])]
 
 
+def is_csrk(name):
+    """A csrk kernel: namespaced (stream launches) or, for CUDA-graph kernel nodes (which ncu names
+    without the namespace), a k_* function that is not a torch / library kernel."""
+    if "csrk::" in name:
+        return True
+    head = name.strip()
+    if head.startswith("void "):
+        head = head[5:]
+    head = head.split("(")[0].split("<")[0].strip()
+    return head.startswith("k_") and "::" not in head
+
+
 def main(csv_path, trace_path, out_path):
-    kern = [(n, m) for n, m in load(csv_path) if "csrk::" in n]
+    kern = [(n, m) for n, m in load(csv_path) if is_csrk(n)]
     trace = json.load(open(trace_path))["ops"]
     total = sum(c for _, c in trace)
     if total > len(kern):
