@@ -2041,6 +2041,190 @@ __global__ __launch_bounds__(kDbTPB) void k_gemm_dB_long(const int64_t *__restri
     }
 }
 
+// Fused deterministic backward through A's transpose plan (short rows of B): the thread of B row k
+// walks, for every i of A^T row k (ascending), C row i against B row k (B_k is a subset of C_i's
+// columns) and reads each dC_ij once for BOTH gradients:
+//   dB_kj += A_ik dC_ij           (fp64 register accumulators, i ascending -- k_gemm_dB_rows' order)
+//   dA_ik  = sum_j dC_ij B_kj     (j ascending -- the row traversal's order: the same bits)
+// C row i is read in chunks of 16 columns loaded together (independent loads) and matched against
+// B_k's columns in registers, instead of a galloping search of dependent loads per column.  dA of
+// the entries of long B rows is left to k_gemm_dA_long.  No atomics: bit-reproducible.
+constexpr int kBwdR = 8;       // B rows of at most 8 entries (stencils: 5 / 7); longer ones are queued
+constexpr int kBwdChunk = 8;   // C-row columns (and dC) loaded together
+constexpr int kBwdQ = 8;       // A^T rows of at most 8 entries: metadata preloaded
+#ifndef CSRK_BWD_PRELOAD
+#define CSRK_BWD_PRELOAD 1
+#endif
+template <typename T>
+__global__ __launch_bounds__(kDbTPB) void k_gemm_bwd_rows(int64_t mB, const int64_t *__restrict__ Bp,
+                                                          const int32_t *__restrict__ Bi, const T *__restrict__ Bv,
+                                                          const int64_t *__restrict__ ATp,
+                                                          const int32_t *__restrict__ ATi,
+                                                          const int64_t *__restrict__ perm, const T *__restrict__ Av,
+                                                          const int64_t *__restrict__ Cp,
+                                                          const int32_t *__restrict__ Ci, const T *__restrict__ dC,
+                                                          T *__restrict__ dA, T *__restrict__ dB, DbLong lng)
+{
+    pdl_wait();
+    // the thread's B row (columns, values) and dB accumulators in shared memory, [entry][thread]:
+    // the merge pointer into them is data-dependent (registers would spill)
+    __shared__ int32_t s_bj[kBwdR][kDbTPB];
+    __shared__ double s_bv[kBwdR][kDbTPB], s_acc[kBwdR][kDbTPB];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int64_t stride = (int64_t)gridDim.x * kDbTPB;
+    for (int64_t k0 = (int64_t)blockIdx.x * kDbTPB + tid - lane; k0 < mB; k0 += stride) {
+        const int64_t k = k0 + lane;
+        const bool valid = k < mB;
+        const int64_t b0 = valid ? __ldg(Bp + k) : 0, b1 = valid ? __ldg(Bp + k + 1) : 0;
+        const int lb = (int)(b1 - b0 < kBwdR + 1 ? b1 - b0 : kBwdR + 1);
+        const bool lng_row = valid && lb > kBwdR;
+        if (lng_row) {
+            const unsigned long long nch = (unsigned long long)((b1 - b0 + 31) >> 5);
+            const unsigned long long old = atomicAdd(lng.ctr, (1ull << 32) | nch);
+            const int slot = (int)(old >> 32);
+            lng.rows[slot] = (int32_t)k;
+            lng.chunk0[slot] = (int64_t)(old & 0xffffffffull);
+        }
+        if (!valid || lng_row) continue;
+        const int64_t q0 = __ldg(ATp + k), q1 = __ldg(ATp + k + 1);
+        for (int p = 0; p < lb; ++p) {
+            s_bj[p][tid] = __ldg(Bi + b0 + p);
+            s_bv[p][tid] = (double)__ldg(Bv + b0 + p);
+            s_acc[p][tid] = 0.0;
+        }
+        // walk C row i against B row k: B_k's columns are a sorted subset of C_i's (two pointers)
+        auto walk = [&](int64_t pa, double a, int64_t c0, int64_t c1) {
+            double dacc = 0.0;
+            int p = 0;
+            int32_t cur = lb > 0 ? s_bj[0][tid] : INT32_MAX;
+            for (int64_t cb = c0; cb < c1 && p < lb; cb += kBwdChunk) {
+                int32_t cc[kBwdChunk];
+                double dv[kBwdChunk];
+#pragma unroll
+                for (int t = 0; t < kBwdChunk; ++t) {
+                    const bool in = cb + t < c1;
+                    cc[t] = in ? __ldg(Ci + cb + t) : INT32_MIN;
+                    dv[t] = in ? (double)__ldg(dC + cb + t) : 0.0;
+                }
+#pragma unroll
+                for (int t = 0; t < kBwdChunk; ++t) {
+                    if (cc[t] == cur) {
+                        const double g = dv[t];
+                        s_acc[p][tid] = fma(a, g, s_acc[p][tid]);
+                        dacc = fma(g, s_bv[p][tid], dacc);
+                        ++p;
+                        cur = p < lb ? s_bj[p][tid] : INT32_MAX;
+                    }
+                }
+            }
+            if (dA) dA[pa] = (T)dacc;
+        };
+        if (CSRK_BWD_PRELOAD && q1 - q0 <= kBwdQ) {
+            // the row's A^T entries, their C-row extents and A values loaded together up front:
+            // three levels of dependent loads per B row instead of three per entry
+            const int lq = (int)(q1 - q0);
+            int32_t iu[kBwdQ];
+            int64_t pau[kBwdQ], cs[kBwdQ];
+            int32_t cn[kBwdQ];
+            double au[kBwdQ];
+#pragma unroll
+            for (int u = 0; u < kBwdQ; ++u) {
+                iu[u] = u < lq ? __ldg(ATi + q0 + u) : 0;
+                pau[u] = u < lq ? __ldg(perm + q0 + u) : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < kBwdQ; ++u) {
+                cs[u] = u < lq ? __ldg(Cp + iu[u]) : 0;
+                cn[u] = u < lq ? (int32_t)(__ldg(Cp + iu[u] + 1) - cs[u]) : 0;
+                au[u] = u < lq ? (double)__ldg(Av + pau[u]) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kBwdQ; ++u)
+                if (u < lq) walk(pau[u], au[u], cs[u], cs[u] + cn[u]);
+        } else
+        for (int64_t q = q0; q < q1; ++q) {
+            const int32_t i = __ldg(ATi + q);
+            const int64_t pa = __ldg(perm + q);
+            const double a = (double)__ldg(Av + pa);
+            const int64_t c1 = __ldg(Cp + i + 1);
+            double dacc = 0.0;
+            int p = 0;
+            int32_t cur = lb > 0 ? s_bj[0][tid] : INT32_MAX;
+            // two-pointer walk: B_k's columns are a sorted subset of C_i's
+            for (int64_t cb = __ldg(Cp + i); cb < c1 && p < lb; cb += kBwdChunk) {
+                int32_t cc[kBwdChunk];
+                double dv[kBwdChunk];
+#pragma unroll
+                for (int t = 0; t < kBwdChunk; ++t) {
+                    const bool in = cb + t < c1;
+                    cc[t] = in ? __ldg(Ci + cb + t) : INT32_MIN;
+                    dv[t] = in ? (double)__ldg(dC + cb + t) : 0.0;
+                }
+#pragma unroll
+                for (int t = 0; t < kBwdChunk; ++t) {
+                    if (cc[t] == cur) {
+                        const double g = dv[t];
+                        s_acc[p][tid] = fma(a, g, s_acc[p][tid]);
+                        dacc = fma(g, s_bv[p][tid], dacc);
+                        ++p;
+                        cur = p < lb ? s_bj[p][tid] : INT32_MAX;
+                    }
+                }
+            }
+            if (dA) dA[pa] = (T)dacc;
+        }
+        if (dB)
+            for (int p = 0; p < lb; ++p) dB[b0 + p] = (T)s_acc[p][tid];
+    }
+}
+
+// dA of the A entries (i, k) whose B row k is long (queued by k_gemm_bwd_rows): one warp per row,
+// lanes over B_k's entries in chunks of 32, binary search of each column in C_i, the chunk's
+// partial sums reduced in a fixed lane order and added in chunk order -- deterministic.
+template <typename T>
+__global__ __launch_bounds__(kDbTPB) void k_gemm_dA_long(const int64_t *__restrict__ Bp,
+                                                         const int32_t *__restrict__ Bi, const T *__restrict__ Bv,
+                                                         const int64_t *__restrict__ ATp,
+                                                         const int32_t *__restrict__ ATi,
+                                                         const int64_t *__restrict__ perm,
+                                                         const int64_t *__restrict__ Cp,
+                                                         const int32_t *__restrict__ Ci, const T *__restrict__ dC,
+                                                         T *__restrict__ dA, DbLong lng)
+{
+    pdl_wait();
+    const unsigned long long ctr = *(volatile const unsigned long long *)lng.ctr;
+    const int n = (int)(ctr >> 32);
+    const int lane = threadIdx.x & 31;
+    const int warps = (int)(gridDim.x * (kDbTPB / 32));
+    for (int r = blockIdx.x * (kDbTPB / 32) + (threadIdx.x >> 5); r < n; r += warps) {
+        const int64_t k = lng.rows[r];
+        const int64_t b0 = __ldg(Bp + k), b1 = __ldg(Bp + k + 1);
+        const int64_t q1 = __ldg(ATp + k + 1);
+        for (int64_t q = __ldg(ATp + k); q < q1; ++q) {
+            const int32_t i = __ldg(ATi + q);
+            const int64_t c0 = __ldg(Cp + i), c1 = __ldg(Cp + i + 1);
+            double tot = 0.0;
+            for (int64_t pb0 = b0; pb0 < b1; pb0 += 32) {
+                const int64_t pb = pb0 + lane;
+                double v = 0.0;
+                if (pb < b1) {
+                    const int32_t j = __ldg(Bi + pb);
+                    int64_t l = c0, h = c1;
+                    while (l < h) {
+                        const int64_t mid = (l + h) >> 1;
+                        if (__ldg(Ci + mid) < j) l = mid + 1; else h = mid;
+                    }
+                    if (l < c1 && __ldg(Ci + l) == j) v = (double)__ldg(dC + l) * (double)__ldg(Bv + pb);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                tot += v;
+            }
+            if (lane == 0) dA[__ldg(perm + q)] = (T)tot;
+        }
+    }
+}
+
 // Scattered patterns (config 4: C rows are random, far beyond L2): the thread-per-row walk reads C
 // rows sector by sector from DRAM, so every stored entry of B is taken as in k_gemm_dB_long, a warp
 // per 32 consecutive entries (binary search per i); the chunk's first row by a binary search over
@@ -2100,6 +2284,7 @@ __global__ __launch_bounds__(kDbTPB) void k_gemm_dB_flat(int64_t nnzB, int64_t m
     }
 }
 
+static bool fused_plan_bwd() { static int v = knob("GEMM_BWD_FUSED", 1); return v != 0; }
 static bool dB_flat(const csrk_pattern &B)
 {
     static int k = knob("GEMM_DB_FLAT", -1);
@@ -2142,6 +2327,40 @@ static int spgemm_bwd_t(const csrk_pattern &A, const T *Av, const csrk_pattern *
                         Bump &ws, cudaStream_t s)
 {
     if (!AT) return spgemm_values_t<T>(PH_BWD, A, Av, B, Bv, C, nullptr, dC, dA, dB, ws, s);
+    size_t fused_used = 0;
+    if (!dB_flat(B) && fused_plan_bwd() && (ws.sizing() || (dA && dB))) {
+        // both gradients in one pass over B's rows (k_gemm_bwd_rows), dB of long B rows by
+        // k_gemm_dB_long and their dA by k_gemm_dA_long.  (Sizing: the larger of this and the
+        // two-pass path below, which a call without dA or dB takes.)
+        Bump wf = ws;
+        DbLong lng{};
+        lng.ctr = wf.take<unsigned long long>(1);
+        lng.rows = wf.take<int32_t>(B.nrows > 0 ? B.nrows : 1);
+        lng.chunk0 = wf.take<int64_t>(B.nrows > 0 ? B.nrows : 1);
+        if (wf.overflow) return CSRK_ERR_WORKSPACE;
+        fused_used = wf.used;
+    }
+    if (!ws.sizing() && fused_used) {
+        DbLong lng{};
+        lng.ctr = ws.take<unsigned long long>(1);
+        lng.rows = ws.take<int32_t>(B.nrows > 0 ? B.nrows : 1);
+        lng.chunk0 = ws.take<int64_t>(B.nrows > 0 ? B.nrows : 1);
+        if (A.nnz == 0) return B.nnz > 0 ? (cudaMemsetAsync(dB, 0, sizeof(T) * (size_t)B.nnz, s) == cudaSuccess
+                                            ? CSRK_OK : CSRK_ERR_CUDA) : CSRK_OK;
+        if (B.nnz / 32 + B.nrows >= (int64_t)UINT32_MAX) return CSRK_ERR_INDEX_OVERFLOW;
+        CSRK_CUDA(cudaMemsetAsync(lng.ctr, 0, sizeof(unsigned long long), s));
+        const int64_t warps = cdiv(B.nrows, 32);
+        const int64_t cap = (int64_t)kNumSMs * 8 * (kDbTPB / 32);
+        const int64_t grid = cdiv(warps < cap ? warps : cap, kDbTPB / 32);
+        if (B.nrows > 0)
+            CSRK_LAUNCH(k_gemm_bwd_rows<T>, (unsigned)grid, kDbTPB, 0, s, B.nrows, B.indptr, B.indices, Bv, AT->indptr,
+                        AT->indices, perm, Av, C.indptr, C.indices, dC, dA, dB, lng);
+        CSRK_LAUNCH(k_gemm_dB_long<T>, (unsigned)(kNumSMs * 8), kDbTPB, 0, s, B.indptr, B.indices, AT->indptr,
+                    AT->indices, perm, Av, C.indptr, C.indices, dC, dB, lng);
+        CSRK_LAUNCH(k_gemm_dA_long<T>, (unsigned)(kNumSMs * 4), kDbTPB, 0, s, B.indptr, B.indices, Bv, AT->indptr,
+                    AT->indices, perm, C.indptr, C.indices, dC, dA, lng);
+        return CSRK_OK;
+    }
     // dA by the row traversal (no dB), then the dB gather; they run in order on one stream and
     // share the scratch
     Bump w2 = ws;
@@ -2149,6 +2368,7 @@ static int spgemm_bwd_t(const csrk_pattern &A, const T *Av, const csrk_pattern *
     if (ws.sizing()) {
         CSRK_TRY(launch_dB_gather<T>(B, *AT, perm, Av, C, dC, dB, ws, s));
         ws.used = w2.used > ws.used ? w2.used : ws.used;
+        ws.used = fused_used > ws.used ? fused_used : ws.used;
         return CSRK_OK;
     }
     if (!dB) return CSRK_OK;
