@@ -2050,13 +2050,19 @@ __global__ __launch_bounds__(kDbTPB) void k_gemm_dB_long(const int64_t *__restri
 // B_k's columns in registers, instead of a galloping search of dependent loads per column.  dA of
 // the entries of long B rows is left to k_gemm_dA_long.  No atomics: bit-reproducible.
 constexpr int kBwdR = 8;       // B rows of at most 8 entries (stencils: 5 / 7); longer ones are queued
-constexpr int kBwdChunk = 8;   // C-row columns (and dC) loaded together
+#ifndef CSRK_BWD_CHUNK
+#define CSRK_BWD_CHUNK 8
+#endif
+constexpr int kBwdChunk = CSRK_BWD_CHUNK;   // C-row columns (and dC) loaded together
 constexpr int kBwdQ = 8;       // A^T rows of at most 8 entries: metadata preloaded
 #ifndef CSRK_BWD_PRELOAD
 #define CSRK_BWD_PRELOAD 1
 #endif
+#ifndef CSRK_BWD_MINB
+#define CSRK_BWD_MINB 1
+#endif
 template <typename T>
-__global__ __launch_bounds__(kDbTPB) void k_gemm_bwd_rows(int64_t mB, const int64_t *__restrict__ Bp,
+__global__ __launch_bounds__(kDbTPB, CSRK_BWD_MINB) void k_gemm_bwd_rows(int64_t mB, const int64_t *__restrict__ Bp,
                                                           const int32_t *__restrict__ Bi, const T *__restrict__ Bv,
                                                           const int64_t *__restrict__ ATp,
                                                           const int32_t *__restrict__ ATi,
