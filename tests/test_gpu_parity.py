@@ -130,6 +130,37 @@ def test_spmv_fwd_bwd(ck, orc, case, dt, values):
     np.testing.assert_array_equal(dA.cpu().numpy(), dA_ref)
 
 
+WIN_CASES = {
+    # square operators of ~10^6 rows (several waves of the scatter kernel): banded, odd order,
+    # scattered power-law columns with a few long rows
+    "poisson2d_1024": lambda dt, v: synth.poisson2d(1024, dtype=dt),
+    "poisson2d_1023": lambda dt, v: synth.poisson2d(1023, dtype=dt),
+    "powerlaw_2p20": lambda dt, v: synth.powerlaw(1 << 20, seed=17, dtype=dt, values=v),
+}
+
+
+@pytest.mark.parametrize("case", list(WIN_CASES))
+@pytest.mark.parametrize("dt", DTS)
+@pytest.mark.parametrize("values", ["real", "int"])
+def test_spmv_bwd_large(ck, orc, case, dt, values):
+    """SpMV backward without a plan (atomic dx scatter) at ~10^6 rows: dA bit-exact, dx within
+    the S rule (exact for integer data), also dx only."""
+    A = WIN_CASES[case](dt, values)
+    if values == "int" and case.startswith("poisson"):
+        rng = np.random.default_rng(9)
+        A = A.with_values(synth.int_values(rng, A.nnz, dt))
+    assert A.nrows == A.ncols and A.nrows >= 148 * 4096
+    x = synth.dense(A.ncols, 13, dt, values)
+    dy = synth.dense(A.nrows, 14, dt, values)
+    dA_ref, dx_ref = orc.spmv_bwd(A, x, dy)
+    Ad = dev(ck, A)
+    dA, dx = ck.spmv_bwd(Ad, t(x), t(dy))
+    np.testing.assert_array_equal(dA.cpu().numpy(), dA_ref)
+    close(dx, dx_ref.value, dx_ref.S, dt, "dx", values == "int")
+    _, dx2 = ck.spmv_bwd(Ad, t(x), t(dy), need_dA=False)
+    close(dx2, dx_ref.value, dx_ref.S, dt, "dx only", values == "int")
+
+
 def test_spmv_deterministic(ck):
     A = synth.powerlaw(1 << 14, seed=3, dtype=np.float64)
     Ad = dev(ck, A)
