@@ -2135,6 +2135,24 @@ __global__ __launch_bounds__(kDbTPB, CSRK_BWD_MINB) void k_gemm_bwd_rows(int64_t
                     }
                 }
             }
+            if (p < lb) {
+                // the walk stalled on B_k's column p, absent from C_i (a caller's C narrower than
+                // the structural product: dC_ij = 0 there, csrk.h); the columns after it are
+                // located by binary search, in ascending order (same summation order)
+                for (int pp = p + 1; pp < lb; ++pp) {
+                    const int32_t j = s_bj[pp][tid];
+                    int64_t lo = c0, hi = c1;
+                    while (lo < hi) {
+                        const int64_t mid = (lo + hi) >> 1;
+                        if (__ldg(Ci + mid) < j) lo = mid + 1; else hi = mid;
+                    }
+                    if (lo < c1 && __ldg(Ci + lo) == j) {
+                        const double g = (double)__ldg(dC + lo);
+                        s_acc[pp][tid] = fma(a, g, s_acc[pp][tid]);
+                        dacc = fma(g, s_bv[pp][tid], dacc);
+                    }
+                }
+            }
             if (dA) dA[pa] = (T)dacc;
         };
         if (CSRK_BWD_PRELOAD && q1 - q0 <= kBwdQ) {
@@ -2159,37 +2177,12 @@ __global__ __launch_bounds__(kDbTPB, CSRK_BWD_MINB) void k_gemm_bwd_rows(int64_t
 #pragma unroll
             for (int u = 0; u < kBwdQ; ++u)
                 if (u < lq) walk(pau[u], au[u], cs[u], cs[u] + cn[u]);
-        } else
-        for (int64_t q = q0; q < q1; ++q) {
-            const int32_t i = __ldg(ATi + q);
-            const int64_t pa = __ldg(perm + q);
-            const double a = (double)__ldg(Av + pa);
-            const int64_t c1 = __ldg(Cp + i + 1);
-            double dacc = 0.0;
-            int p = 0;
-            int32_t cur = lb > 0 ? s_bj[0][tid] : INT32_MAX;
-            // two-pointer walk: B_k's columns are a sorted subset of C_i's
-            for (int64_t cb = __ldg(Cp + i); cb < c1 && p < lb; cb += kBwdChunk) {
-                int32_t cc[kBwdChunk];
-                double dv[kBwdChunk];
-#pragma unroll
-                for (int t = 0; t < kBwdChunk; ++t) {
-                    const bool in = cb + t < c1;
-                    cc[t] = in ? __ldg(Ci + cb + t) : INT32_MIN;
-                    dv[t] = in ? (double)__ldg(dC + cb + t) : 0.0;
-                }
-#pragma unroll
-                for (int t = 0; t < kBwdChunk; ++t) {
-                    if (cc[t] == cur) {
-                        const double g = dv[t];
-                        s_acc[p][tid] = fma(a, g, s_acc[p][tid]);
-                        dacc = fma(g, s_bv[p][tid], dacc);
-                        ++p;
-                        cur = p < lb ? s_bj[p][tid] : INT32_MAX;
-                    }
-                }
+        } else {
+            for (int64_t q = q0; q < q1; ++q) {
+                const int32_t i = __ldg(ATi + q);
+                const int64_t pa = __ldg(perm + q);
+                walk(pa, (double)__ldg(Av + pa), __ldg(Cp + i), __ldg(Cp + i + 1));
             }
-            if (dA) dA[pa] = (T)dacc;
         }
         if (dB)
             for (int p = 0; p < lb; ++p) dB[b0 + p] = (T)s_acc[p][tid];

@@ -394,6 +394,40 @@ def test_spgemm(ck, orc, case, dt, values):
     close(dB4, dB_ref.value, dB_ref.S, dt, "dB only (plan)", exact)
 
 
+@pytest.mark.parametrize("dt", DTS)
+def test_spgemm_bwd_plan_narrow_C(ck, dt):
+    """csrk.h: with A's transpose plan, entries of C_i missing for some j of B_k count as
+    dC_ij = 0.  C = the structural product of a 20x20 Poisson A with every third entry of each row
+    dropped; dA and dB against the dense definition (dC_dense B^T) o mask(A), (A^T dC_dense) o
+    mask(B), exact for integer data."""
+    A = synth.poisson2d(20, dtype=dt)
+    rng = np.random.default_rng(21)
+    A = A.with_values(synth.int_values(rng, A.nnz, dt))
+    Ad = dev(ck, A)
+    C = ck.spgemm_symbolic(Ad, Ad)
+    Cp, Ci = C.indptr.cpu().numpy(), C.indices.cpu().numpy()
+    keep = np.ones(Ci.size, bool)
+    for r in range(A.nrows):
+        keep[Cp[r] + 1:Cp[r + 1]:3] = False
+    Cp2 = np.zeros_like(Cp)
+    Cp2[1:] = np.cumsum([keep[Cp[r]:Cp[r + 1]].sum() for r in range(A.nrows)])
+    Ci2 = Ci[keep]
+    C2 = ck.CSR.from_host(synth.CSR(A.nrows, A.ncols, Cp2, Ci2, np.zeros(Ci2.size, dt)))
+    dC = synth.int_values(rng, Ci2.size, dt)
+    n = A.nrows
+    Dd = np.zeros((n, n))
+    Dd[np.repeat(np.arange(n), np.diff(Cp2)), Ci2] = dC
+    Ad_dense = np.zeros((n, n))
+    rows = np.repeat(np.arange(n), np.diff(A.indptr))
+    Ad_dense[rows, A.indices] = A.values
+    dA_ref = (Dd @ Ad_dense.T)[rows, A.indices]
+    dB_ref = (Ad_dense.T @ Dd)[rows, A.indices]
+    plan = ck.csr_transpose(Ad, with_values=False)
+    dA, dB = ck.spgemm_bwd(Ad, Ad, C2, t(dC), plan=plan)
+    np.testing.assert_array_equal(dA.cpu().numpy(), dA_ref.astype(dt))
+    np.testing.assert_array_equal(dB.cpu().numpy(), dB_ref.astype(dt))
+
+
 @pytest.mark.parametrize("case", ["powerlaw_16k", "skew_big", "poisson3d_17"])
 @pytest.mark.parametrize("dt", DTS)
 def test_spgemm_dB_plan_bitwise_reproducible(ck, orc, case, dt):
