@@ -1000,26 +1000,33 @@ __device__ __forceinline__ int64_t big_list_of(const int64_t *loff, int64_t lo, 
 __global__ __launch_bounds__(kGemmTPB) void k_big_prep(BigRows br, const int64_t *__restrict__ Ap,
                                                        const int32_t *__restrict__ Ai, const int64_t *__restrict__ Bp)
 {
+    // one warp per big row (most have 33..512 A entries: a CTA per row left most threads idle
+    // behind three block barriers per 512 entries); lanes over the row's entries, warp scans
     pdl_wait();
-    __shared__ int64_t s_red[kGemmTPB / 32];
     const int n = *(volatile const int *)br.count;
-    for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int warps = (int)(gridDim.x * (kGemmTPB / 32));
+    for (int r = blockIdx.x * (kGemmTPB / 32) + (threadIdx.x >> 5); r < n; r += warps) {
         const int64_t i = br.rows[r];
         const int64_t as = Ap[i], ae = Ap[i + 1];
         int64_t run = 0;
-        for (int64_t a0 = as; a0 < ae; a0 += kGemmTPB) {
-            const int64_t a = a0 + threadIdx.x;
+        for (int64_t a0 = as; a0 < ae; a0 += 32) {
+            const int64_t a = a0 + lane;
             int64_t len = 0;
             if (a < ae) {
                 const int32_t k = Ai[a];
                 len = Bp[k + 1] - Bp[k];
             }
-            int64_t tot;
-            const int64_t ex = block_excl_scan_i64(len, s_red, tot);
-            if (a < ae) br.loff[a] = run + ex;
-            run += tot;
+            int64_t x = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (a < ae) br.loff[a] = run + x - len;
+            run += __shfl_sync(0xffffffffu, x, 31);
         }
-        if (threadIdx.x == 0) {
+        if (lane == 0) {
             br.w[r] = run;
             if (br.huge && run > kMMaxW) br.huge[atomicAdd(br.nhuge, 1)] = r;
         }
